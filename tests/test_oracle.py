@@ -1,0 +1,456 @@
+"""Pins for the CPU oracle (oracle/moe_oracle.py) — no GPU needed.
+
+Each test pins the oracle to something other than itself: the paper's / SPEC's
+worked examples (tests/golden/*, each citing its source), closed forms,
+invariants, brute force on tiny inputs, and three independent formulations of
+the layer written here in plain torch float64 (dense all-experts-then-mask,
+token dropping at capacity factor E with batched matmul, per-expert loop),
+plus finite differences and torch.autograd for the backward pass.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_kv, read_golden
+from oracle import moe_oracle as O
+from synth import inputs as S
+
+
+def nums(vals, t=float):
+    return [t(v) for v in vals]
+
+
+# ---------------------------------------------------------------- golden pins
+
+def test_softmax_golden():
+    g = golden_kv("softmax_S49.txt")
+    p = O.softmax(np.array([nums(g["input"])]))
+    np.testing.assert_allclose(p[0], nums(g["output"]), atol=1e-8)
+
+
+def test_softmax_shift_invariance_and_rows_sum_to_one():
+    rng = np.random.default_rng(0)
+    L = rng.normal(size=(16, 7))
+    p = O.softmax(L)
+    np.testing.assert_allclose(p.sum(1), 1.0, atol=1e-12)
+    np.testing.assert_allclose(O.softmax(L + 3.5), p, atol=1e-12)
+    assert (p >= 0).all()
+
+
+def test_router_golden():
+    for line in read_golden("router_S267.txt"):
+        logits, k, idx, gate = [s.strip() for s in line.split("|")]
+        L = np.array([nums(logits.split())])
+        i, g = O.topk(L, int(k))
+        assert i[0, 0] == int(idx)
+        assert abs(g[0, 0] - float(gate)) < 1e-8
+
+
+def test_topk_brute_force_with_ties():
+    # brute force: enumerate all k-subsets ordered by (-score, index) lexicographically
+    rng = np.random.default_rng(1)
+    for trial in range(200):
+        E = int(rng.integers(1, 7))
+        k = int(rng.integers(1, E + 1))
+        L = rng.integers(0, 3, size=(1, E)).astype(np.float64)  # many exact ties
+        best = None
+        for combo in itertools.permutations(range(E), k):
+            key = [(-L[0, e], e) for e in combo]
+            if key != sorted(key):
+                continue
+            score = sorted(((-L[0, e], e) for e in combo))
+            rest = sorted((-L[0, e], e) for e in range(E) if e not in combo)
+            if rest and score[-1] > rest[0]:
+                continue  # a better candidate was left out
+            best = list(combo)
+        idx, gates = O.topk(L, k)
+        assert list(idx[0]) == best, (L, k)
+        np.testing.assert_allclose(gates[0], O.softmax(L)[0, best], atol=0)
+
+
+def test_topk_single_expert_gate_is_one():
+    idx, g = O.topk(np.random.default_rng(2).normal(size=(5, 1)), 1)
+    assert (idx == 0).all() and np.allclose(g, 1.0)
+
+
+def test_plan_golden():
+    g = golden_kv("plan_S287.txt")
+    counts, bs = nums(g["counts"], int), int(g["block"][0])
+    idx = np.repeat(np.arange(len(counts)), counts).astype(np.int32)
+    plan = O.make_plan(idx, len(counts), bs)
+    assert list(plan.padded_counts) == nums(g["padded_counts"], int)
+    assert plan.Tp == int(g["total"][0])
+    assign = np.array(nums(g["assign"], int), np.int32)
+    p2 = O.make_plan(assign, 2, 4)
+    assert list(p2.sorted_idx) == nums(g["gather_order"], int)
+
+
+def test_bcsr_golden():
+    g = golden_kv("bcsr_S114.txt")
+    nbr, nbc = nums(g["grid"], int)
+    blocks = [tuple(map(int, b.split(","))) for b in g["blocks"]]
+    t = O.topology_from_blocks(blocks, nbr, nbc, 1)
+    for key in ["row_offsets", "col_indices", "row_indices", "t_col_offsets",
+                "t_block_offsets", "t_row_indices"]:
+        assert list(getattr(t, key)) == nums(g[key], int), key
+
+
+def test_bcsr_empty():
+    t = O.topology_from_blocks([], 3, 2, 4)
+    assert t.nnz == 0 and list(t.row_offsets) == [0, 0, 0, 0] and list(t.t_col_offsets) == [0, 0, 0]
+
+
+def test_moe_topology_golden():
+    g = golden_kv("moe_topology_S317.txt")
+    counts = nums(g["counts"], int)
+    bs, ffn = int(g["block"][0]), int(g["ffn"][0])
+    idx = np.repeat(np.arange(len(counts)), counts).astype(np.int32)
+    plan = O.make_plan(idx, len(counts), bs)
+    blocks = sorted(tuple(map(int, b.split(","))) for b in g["blocks"])
+    assert sorted(O.moe_topology_blocks(plan, bs, ffn)) == blocks
+    for topo in (O.make_topology(plan, bs, ffn), O.make_topology_closed_form(plan, bs, ffn)):
+        for key in ["row_offsets", "col_indices", "row_indices", "t_col_offsets",
+                    "t_block_offsets", "t_row_indices"]:
+            assert list(getattr(topo, key)) == nums(g[key], int), key
+
+
+def test_gelu_golden_and_derivative():
+    for line in read_golden("gelu_S58.txt"):
+        kind, x, want, tol = line.split()
+        kid = {"gelu": O.ACT_GELU, "relu": O.ACT_RELU}[kind]
+        assert abs(O.act(kid, np.array([float(x)]))[0] - float(want)) <= float(tol)
+    xs = np.array([-1.0, 0.5, 2.0, -3.0, 0.1])
+    eps = 1e-6
+    for kid in (O.ACT_IDENTITY, O.ACT_GELU, O.ACT_RELU):
+        fd = (O.act(kid, xs + eps) - O.act(kid, xs - eps)) / (2 * eps)
+        np.testing.assert_allclose(O.act_grad(kid, xs), fd, rtol=1e-6, atol=1e-8)
+
+
+def test_capacity_golden():
+    for line in read_golden("capacity_P115.txt"):
+        T, E, cf, cap = line.split()
+        assert O.expert_capacity(int(T), int(E), float(cf)) == int(cap)
+
+
+# ---------------------------------------------------------------- invariants
+
+def to_dense(vals, topo):
+    bs = topo.bs
+    d = np.zeros((topo.n_block_rows * bs, topo.n_block_cols * bs))
+    for s in range(topo.nnz):
+        r, c = topo.row_indices[s], topo.col_indices[s]
+        d[r * bs:(r + 1) * bs, c * bs:(c + 1) * bs] = vals[s]
+    return d
+
+
+def mask_of(topo):
+    return to_dense(np.ones((topo.nnz, topo.bs, topo.bs)), topo)
+
+
+def random_topology(rng, max_grid=6, bs=None):
+    nbr, nbc = int(rng.integers(1, max_grid + 1)), int(rng.integers(1, max_grid + 1))
+    bs = bs or int(rng.choice([1, 2, 3, 4]))
+    dens = rng.uniform(0, 1)
+    coords = [(r, c) for r in range(nbr) for c in range(nbc) if rng.uniform() < dens]
+    return O.topology_from_blocks(coords, nbr, nbc, bs)
+
+
+def test_transpose_index_equals_explicit_transpose_200_topologies():
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        t = random_topology(rng)
+        vals = rng.normal(size=(t.nnz, t.bs, t.bs))
+        dense_t = to_dense(vals, t).T
+        # rebuild the transposed matrix only through the transpose index
+        bs = t.bs
+        d2 = np.zeros((t.n_block_cols * bs, t.n_block_rows * bs))
+        for c in range(t.n_block_cols):
+            for i in range(t.t_col_offsets[c], t.t_col_offsets[c + 1]):
+                b, r = t.t_block_offsets[i], t.t_row_indices[i]
+                d2[c * bs:(c + 1) * bs, r * bs:(r + 1) * bs] = vals[b].T
+        np.testing.assert_array_equal(d2, dense_t)
+        assert sorted(t.t_block_offsets.tolist()) == list(range(t.nnz))
+        assert t.row_offsets[-1] == t.nnz == t.t_col_offsets[-1]
+
+
+def test_moe_closed_form_equals_generic_random_plans():
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        E = int(rng.integers(1, 7))
+        bs = int(rng.choice([1, 2, 4]))
+        F = int(rng.integers(1, 4))
+        T = int(rng.integers(0, 30))
+        k = int(rng.integers(1, E + 1))
+        idx = np.stack([rng.permutation(E)[:k] for _ in range(T)]) if T else np.zeros((0, k), np.int32)
+        plan = O.make_plan(idx, E, bs)
+        a = O.make_topology(plan, bs, F * bs)
+        b = O.make_topology_closed_form(plan, bs, F * bs)
+        for key in ["row_offsets", "col_indices", "row_indices", "t_col_offsets",
+                    "t_block_offsets", "t_row_indices"]:
+            np.testing.assert_array_equal(getattr(a, key), getattr(b, key), err_msg=key)
+        # plan invariants
+        assert plan.counts.sum() == T * k
+        assert plan.Tp == plan.padded_bins[-1]
+        assert a.nnz == (plan.Tp // bs) * F
+        assert (plan.padded_counts % bs == 0).all()
+        assert ((plan.padded_counts == 0) == (plan.counts == 0)).all()
+        assert plan.Tp <= O.max_padded_rows(T, k, E, bs) or T == 0
+
+
+def test_plan_positions_stable_and_padding_at_tail():
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, 5, size=(40, 1)).astype(np.int32)
+    plan = O.make_plan(idx, 5, 4)
+    start = plan.padded_bins - plan.padded_counts
+    for e in range(5):
+        ids = [i for i in range(40) if idx[i, 0] == e]
+        assert [plan.pos[i] for i in ids] == list(range(start[e], start[e] + len(ids)))
+    x = rng.normal(size=(40, 3))
+    xg = O.padded_gather(x, plan, 1)
+    real = set(plan.pos.tolist())
+    for p in range(plan.Tp):
+        if p not in real:
+            assert (xg[p] == 0).all()          # pad rows exactly zero
+    y = O.padded_scatter(xg, plan, np.ones((40, 1)), 40, 1)
+    np.testing.assert_array_equal(y, x)        # round trip with unit gates
+
+
+def test_scatter_topk2_weighted_sum():
+    # S:308 / P:157: g1*y1 + g2*y2
+    idx = np.array([[0, 1]], np.int32)
+    plan = O.make_plan(idx, 2, 1)
+    yg = np.array([[1.0, 2.0], [10.0, 20.0]])
+    y = O.padded_scatter(yg, plan, np.array([[0.25, 0.75]]), 1, 2)
+    np.testing.assert_allclose(y, [[0.25 * 1 + 0.75 * 10, 0.25 * 2 + 0.75 * 20]])
+
+
+# ---------------------------------------------------------------- products vs densify
+
+@pytest.mark.parametrize("seed", range(60))
+def test_products_match_densify_oracle(seed):
+    rng = np.random.default_rng(100 + seed)
+    t = random_topology(rng, max_grid=5)
+    bs = t.bs
+    M, N = t.n_block_rows * bs, t.n_block_cols * bs
+    K = int(rng.integers(1, 7))
+    vals = rng.normal(size=(t.nnz, bs, bs))
+    S_d = to_dense(vals, t)
+    mask = mask_of(t)
+    a, b = rng.normal(size=(M, K)), rng.normal(size=(K, N))
+    # SDD, with transposed operands
+    np.testing.assert_allclose(to_dense(O.sdd(a, b, t), t), (a @ b) * mask, atol=1e-12)
+    np.testing.assert_allclose(to_dense(O.sdd(a.T.copy(), b, t, trans_a=True), t), (a @ b) * mask, atol=1e-12)
+    np.testing.assert_allclose(to_dense(O.sdd(a, b.T.copy(), t, trans_b=True), t), (a @ b) * mask, atol=1e-12)
+    # DSD, DSD^T-style (dense operand transposed), DS^TD
+    bn = rng.normal(size=(N, K))
+    np.testing.assert_allclose(O.dsd(vals, bn, t), S_d @ bn, atol=1e-12)
+    np.testing.assert_allclose(O.dsd(vals, bn.T.copy(), t, trans_b=True), S_d @ bn, atol=1e-12)
+    bm = rng.normal(size=(M, K))
+    np.testing.assert_allclose(O.dsd(vals, bm, t, trans_s=True), S_d.T @ bm, atol=1e-12)
+    # DDS, DD^TS, DDS^T
+    am = rng.normal(size=(K, M))
+    np.testing.assert_allclose(O.dds(am, vals, t), am @ S_d, atol=1e-12)
+    np.testing.assert_allclose(O.dds(am.T.copy(), vals, t, trans_a=True), am @ S_d, atol=1e-12)
+    an = rng.normal(size=(K, N))
+    np.testing.assert_allclose(O.dds(an, vals, t, trans_s=True), an @ S_d.T, atol=1e-12)
+
+
+def test_sdd_dense_limit_and_work_count():
+    rng = np.random.default_rng(6)
+    bs, nbr, nbc, K = 2, 3, 4, 5
+    t = O.topology_from_blocks([(r, c) for r in range(nbr) for c in range(nbc)], nbr, nbc, bs)
+    a, b = rng.normal(size=(nbr * bs, K)), rng.normal(size=(K, nbc * bs))
+    np.testing.assert_allclose(to_dense(O.sdd(a, b, t), t), a @ b, atol=1e-12)
+
+
+# ---------------------------------------------------------------- independent layer formulations (torch fp64)
+
+def t64(a):
+    return torch.tensor(np.asarray(a), dtype=torch.float64)
+
+
+def torch_act(kind, h):
+    if kind == O.ACT_IDENTITY:
+        return h
+    if kind == O.ACT_RELU:
+        return torch.relu(h)
+    return torch.nn.functional.gelu(h, approximate="tanh")
+
+
+def dense_masked_moe(x, wr, w1, w2, k, f, act_kind):
+    """Formulation (i): every expert computes every token, then mask by routing."""
+    L = x @ wr
+    p = torch.softmax(L, dim=1)
+    idx = torch.topk(L, k, dim=1).indices
+    E = wr.shape[1]
+    y = torch.zeros_like(x)
+    for e in range(E):
+        ye = torch_act(act_kind, x @ w1[:, e * f:(e + 1) * f]) @ w2[e * f:(e + 1) * f]
+        sel = (idx == e).any(dim=1).to(x.dtype)
+        y = y + (sel * p[:, e])[:, None] * ye
+    return y, idx
+
+
+def dropping_moe_cf(x, wr, w1, w2, k, f, act_kind, cf):
+    """Formulation (ii): token-dropping MoE with capacity
+    num_tokens/num_experts*cf, keep-earliest, batched matmul over experts
+    (Fig. 3A). With cf = E nothing is dropped."""
+    T, h = x.shape
+    E = wr.shape[1]
+    C = O.expert_capacity(T, E, cf)
+    L = x @ wr
+    p = torch.softmax(L, dim=1)
+    idx = torch.topk(L, k, dim=1).indices
+    xb = torch.zeros(E, C, h, dtype=x.dtype)
+    slot = {}
+    fill = [0] * E
+    for t in range(T):
+        for j in range(k):
+            e = int(idx[t, j])
+            if fill[e] < C:
+                slot[(t, j)] = (e, fill[e])
+                xb[e, fill[e]] = x[t]
+                fill[e] += 1
+    W1 = torch.stack([w1[:, e * f:(e + 1) * f] for e in range(E)])
+    W2 = torch.stack([w2[e * f:(e + 1) * f] for e in range(E)])
+    yb = torch.bmm(torch_act(act_kind, torch.bmm(xb, W1)), W2)
+    y = torch.zeros_like(x)
+    for (t, j), (e, c) in slot.items():
+        y[t] += p[t, e] * yb[e, c]
+    return y, len(slot)
+
+
+def per_expert_loop(x, wr, w1, w2, k, f, act_kind):
+    """Formulation (iii): loop over experts, each on exactly its own tokens."""
+    L = x @ wr
+    p = torch.softmax(L, dim=1)
+    idx = torch.topk(L, k, dim=1).indices
+    y = torch.zeros_like(x)
+    for e in range(wr.shape[1]):
+        rows, slots = torch.nonzero(idx == e, as_tuple=True)
+        if rows.numel() == 0:
+            continue
+        ye = torch_act(act_kind, x[rows] @ w1[:, e * f:(e + 1) * f]) @ w2[e * f:(e + 1) * f]
+        y.index_add_(0, rows, p[rows, e][:, None] * ye)
+    return y
+
+
+SMALL = [
+    # T, h, f, E, k, bs, act
+    (40, 8, 8, 4, 1, 4, O.ACT_GELU),
+    (33, 6, 6, 3, 2, 2, O.ACT_RELU),
+    (25, 4, 8, 5, 3, 4, O.ACT_IDENTITY),
+    (64, 16, 8, 8, 2, 8, O.ACT_GELU),
+    (7, 4, 4, 1, 1, 4, O.ACT_GELU),
+]
+
+
+def small_inputs(T, h, f, E, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.normal(size=(T, h)), rng.normal(size=(h, E)) / math.sqrt(h),
+            rng.normal(size=(h, E * f)) / math.sqrt(h), rng.normal(size=(E * f, h)) / math.sqrt(f),
+            rng.normal(size=(T, h)))
+
+
+@pytest.mark.parametrize("cfg", SMALL)
+def test_layer_forward_three_formulations(cfg):
+    T, h, f, E, k, bs, a = cfg
+    x, wr, w1, w2, _ = small_inputs(T, h, f, E, 7)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, bs, f, a)
+    y_i, idx_i = dense_masked_moe(t64(x), t64(wr), t64(w1), t64(w2), k, f, a)
+    assert (idx_i.numpy() == cache.expert_idx).all()
+    np.testing.assert_allclose(y, y_i.numpy(), atol=1e-11)
+    y_ii, kept = dropping_moe_cf(t64(x), t64(wr), t64(w1), t64(w2), k, f, a, cf=E)
+    assert kept == T * k                         # cf = E drops nothing
+    np.testing.assert_allclose(y, y_ii.numpy(), atol=1e-11)
+    y_iii = per_expert_loop(t64(x), t64(wr), t64(w1), t64(w2), k, f, a)
+    np.testing.assert_allclose(y, y_iii.numpy(), atol=1e-11)
+
+
+def test_dropping_cf1_drops_one_minus_one_over_E():
+    # 8 tokens all to expert 0 of 4 experts, cf 1 -> capacity 2, drop 6/8
+    T, h, f, E = 8, 4, 4, 4
+    x = np.ones((T, h))
+    wr = np.zeros((h, E)); wr[:, 0] = 1.0
+    w1 = np.random.default_rng(0).normal(size=(h, E * f))
+    w2 = np.random.default_rng(1).normal(size=(E * f, h))
+    _, kept = dropping_moe_cf(t64(x), t64(wr), t64(w1), t64(w2), 1, f, O.ACT_GELU, cf=1.0)
+    assert 1 - kept / T == 1 - 1 / E
+
+
+def test_single_expert_is_dense_mlp():
+    T, h, f = 9, 4, 8
+    x, wr, w1, w2, _ = small_inputs(T, h, f, 1, 8)
+    y, _ = O.dmoe_forward(x, wr, w1, w2, 1, 4, f, O.ACT_IDENTITY)
+    np.testing.assert_allclose(y, (x @ w1) @ w2, atol=1e-12)
+
+
+def test_uniform_routing_equals_bmm():
+    # exact-uniform routing, count multiple of bs -> block-sparse == batched matmul (A5)
+    T, h, f, E, bs = 32, 8, 8, 4, 4
+    x, wr, w1, w2, _ = small_inputs(T, h, f, E, 9)
+    idx = S.uniform_expert_idx(T, E, 1).numpy()
+    plan = O.make_plan(idx, E, bs)
+    topo = O.make_topology(plan, bs, f)
+    xg = O.padded_gather(x, plan, 1)
+    assert plan.Tp == T                          # no padding under exact-uniform routing
+    hs = O.sdd(xg, w1, topo)
+    xb = t64(xg).reshape(E, T // E, h)
+    W1 = torch.stack([t64(w1)[:, e * f:(e + 1) * f] for e in range(E)])
+    hb = torch.bmm(xb, W1).numpy()
+    # block (r, e*F+j) of the SDD = rows r*bs.. of expert e's batched product, cols j*bs..
+    F = f // bs
+    for s in range(topo.nnz):
+        r, c = topo.row_indices[s], topo.col_indices[s]
+        e, j = c // F, c % F
+        rr = r * bs - e * (T // E)
+        np.testing.assert_allclose(hs[s], hb[e, rr:rr + bs, j * bs:(j + 1) * bs], atol=1e-12)
+
+
+@pytest.mark.parametrize("cfg", SMALL)
+def test_layer_backward_vs_autograd(cfg):
+    T, h, f, E, k, bs, a = cfg
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 10)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, bs, f, a)
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    tx, twr, tw1, tw2 = (t64(v).requires_grad_() for v in (x, wr, w1, w2))
+    yt, _ = dense_masked_moe(tx, twr, tw1, tw2, k, f, a)
+    (yt * t64(dy)).sum().backward()
+    np.testing.assert_allclose(g["dx"], tx.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
+
+
+def test_layer_backward_finite_differences():
+    T, h, f, E, k, bs, a = 12, 4, 4, 3, 2, 2, O.ACT_GELU
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 11)
+    _, cache = O.dmoe_forward(x, wr, w1, w2, k, bs, f, a)
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    eps = 1e-6
+
+    def loss(x_, wr_, w1_, w2_):
+        y_, c_ = O.dmoe_forward(x_, wr_, w1_, w2_, k, bs, f, a)
+        assert (c_.expert_idx == cache.expert_idx).all()
+        return float((y_ * dy).sum())
+
+    rng = np.random.default_rng(12)
+    for name, arr, pos in [("dw1", w1, 0), ("dw2", w2, 1), ("dwr", wr, 2), ("dx", x, 3)]:
+        for _ in range(6):
+            i = tuple(int(rng.integers(0, n)) for n in arr.shape)
+            args = [w1, w2, wr, x]
+            plus = [v.copy() for v in args]; plus[pos][i] += eps
+            minus = [v.copy() for v in args]; minus[pos][i] -= eps
+            fd = (loss(plus[3], plus[2], plus[0], plus[1]) - loss(minus[3], minus[2], minus[0], minus[1])) / (2 * eps)
+            assert abs(fd - g[name][i]) < 1e-6 * max(1.0, abs(fd)), (name, i, fd, g[name][i])
+
+
+def test_max_padded_rows_bound_is_tight():
+    # all experts get exactly one assignment -> every group pads to bs
+    T, k, E, bs = 8, 1, 8, 4
+    idx = np.arange(8).reshape(8, 1).astype(np.int32)
+    plan = O.make_plan(idx, E, bs)
+    assert plan.Tp == O.max_padded_rows(T, k, E, bs) == 32
