@@ -1,0 +1,249 @@
+/*
+ * moe.h — C ABI of the B200-native dropless-MoE hot path (MegaBlocks,
+ * arXiv 2211.15841). Only plain C types cross this boundary.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (section / figure),
+ *            S:n = SPEC.md line n (interfaces only). Readings R1..R16 of points
+ *            the paper leaves open are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless stated, allocated and owned by the
+ *    caller (e.g. through torch). The library never allocates, frees or
+ *    synchronises on these calls; all work is enqueued on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Dense matrices are row-major. bf16 tensors are raw IEEE bfloat16
+ *    (uint16) buffers. Indices are int32.
+ *  - Sparse values (S) are [nnz, bs, bs] bf16: nonzero blocks contiguous in
+ *    BCSR (row-major block) order, each block row-major (Fig. 4).
+ *  - Data-dependent sizes (padded rows Tp, nonzero blocks nnz) are never read
+ *    back to the host: moe_topology writes them to topo->sizes on the device and
+ *    every later kernel reads them there. Buffers are sized with the worst-case
+ *    queries below. Contents at or beyond the device-side sizes are unspecified.
+ *  - Arguments are validated on the host before any launch; a bad argument
+ *    returns MOE_EINVAL / MOE_ESHAPE / MOE_EUNSUPPORTED and launches nothing.
+ *    Launch failures return MOE_ECUDA. Asynchronous device faults surface at
+ *    the caller's next synchronisation. moe_last_error() gives a message.
+ *  - Deterministic: identical inputs give bitwise-identical outputs (no
+ *    floating-point atomics; each output element is reduced by one CTA in a
+ *    fixed order).
+ *  - Reentrant across streams and threads; the only global state is the
+ *    thread-local error string.
+ */
+#ifndef MOE_H_
+#define MOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_EINVAL = 1,       /* NULL pointer / bad enum / bad value */
+  MOE_ESHAPE = 2,       /* inconsistent sizes */
+  MOE_EUNSUPPORTED = 3, /* valid for the method but not on this GPU path (e.g. bs != 128) */
+  MOE_ECUDA = 4,        /* CUDA launch/driver error */
+  MOE_ENCCL = 5,        /* reserved (collectives are issued by the caller's process group) */
+  MOE_EWORKSPACE = 6    /* workspace too small */
+} moe_status;
+
+/* Expert activation between SDD and DSD. The paper does not name it
+ * ("iterate between SDD and DSD"); reading R2: gelu with the tanh
+ * approximation is the default, identity and relu are also offered. */
+typedef enum { MOE_ACT_IDENTITY = 0, MOE_ACT_GELU_TANH = 1, MOE_ACT_RELU = 2 } moe_act;
+
+/* Layer hyper-parameters (Fig. 1; Table 1/2 P:124-140).
+ * tokens = T, hidden = h, num_experts = E, top_k = k, ffn_hidden = f (per
+ * expert; inner_dim = E*f), block_size = bs (128). */
+typedef struct {
+  int64_t tokens;
+  int64_t hidden;
+  int64_t num_experts;
+  int64_t top_k;
+  int64_t ffn_hidden;
+  int64_t block_size;
+  int32_t act;      /* moe_act */
+  int32_t reserved; /* must be 0 */
+} moe_config;
+
+/* ---- configuration and size queries (host only, no CUDA calls) ---------- */
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* moe_last_error(void);
+
+/* MOE_OK iff: T >= 1, h >= 1, 1 <= k <= E, f % bs == 0, act valid; and for the
+ * GPU path: bs == 128, h % 128 == 0, E <= 1024. */
+moe_status moe_check_config(const moe_config* cfg);
+
+/* Worst-case padded rows: Tp = sum_e bs*ceil(c_e/bs) <= bs*floor((R + min(E,R)*(bs-1))/bs),
+ * R = T*k (P:297 padding to a multiple of the block size). */
+int64_t moe_max_padded_rows(const moe_config* cfg);
+
+/* Worst-case nonzero blocks: max_padded_rows/bs * f/bs (Fig. 3C). */
+int64_t moe_max_nnz_blocks(const moe_config* cfg);
+
+/* Device scratch (bytes) needed by moe_router, moe_topology, moe_forward,
+ * moe_backward and moe_router_bwd for this config (a single buffer can serve
+ * all of them, but not concurrently). 256-byte aligned pointer required. */
+size_t moe_workspace_bytes(const moe_config* cfg);
+
+/* Number of SMs the library sizes its persistent grids for (queried once). */
+int moe_device_sm_count(void);
+
+/* ---- topology (Fig. 5 make_topology; P:235-242 hybrid
+ *      blocked-CSR-COO; P:287-292 transpose indices; P:299 built together) -- */
+typedef struct {
+  int32_t* counts;          /* [E]  assignments per expert                                  */
+  int32_t* bins;            /* [E]  inclusive cumsum of counts                               */
+  int32_t* padded_bins;     /* [E]  inclusive cumsum of bs*ceil(counts/bs)                   */
+  int32_t* sorted_idx;      /* [R]  flat ids i = t*k + j in expert order, stable in i (R7)   */
+  int32_t* pos;             /* [R]  padded row of flat id i (pad rows at group tail, R8)     */
+  int32_t* sorted_pos;      /* [R]  unpadded expert-order position of flat id i              */
+  int32_t* row_offsets;     /* [max_rows/bs + 1]  BCSR row offsets (block units)      */
+  int32_t* col_indices;     /* [max_nnz]          BCSR column of each block                  */
+  int32_t* row_indices;     /* [max_nnz]          COO row of each block              */
+  int32_t* t_col_offsets;   /* [E*f/bs + 1]       transposed offsets per block-column (R9)   */
+  int32_t* t_block_offsets; /* [max_nnz]          storage index of each block, in (col,row)
+                                                  order: the transpose index          */
+  int32_t* t_row_indices;   /* [max_nnz]          row of each block in transposed order      */
+  int32_t* sizes;           /* [2] = {Tp, nnz}, written on the device                        */
+} moe_topology_t;
+
+/* Router, §2.1: logits = x . wr (fp32 accumulate of bf16 inputs),
+ * then moe_topk. x [T,h] bf16, wr [h,E] bf16; logits [T,E] fp32 (kept for the
+ * backward pass), expert_idx [T,k] int32, gates [T,k] fp32. */
+moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, float* logits,
+                      int32_t* expert_idx, float* gates, void* ws, void* stream);
+
+/* Top-k from fp32 logits ("greedily selecting the top_k scoring
+ * experts"): per token the k largest logits in descending order, exact ties to
+ * the lower expert index (R6); gate = softmax probability of the chosen
+ * expert, no renormalisation (R4). Bit-exact selection contract. */
+moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_idx, float* gates,
+                    void* stream);
+
+/* Topology + permutation plan from expert_idx [T*k].
+ * Writes every array of *topo (caller-allocated, sized by the max queries)
+ * and topo->sizes = {Tp, nnz}. Integer outputs are bit-exact (closed form of
+ * the block-diagonal pattern). ws: moe_workspace_bytes. */
+moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
+                        void* ws, void* stream);
+
+/* Padded gather, Fig. 5 line 15 fused with zero padding:
+ * x_g[pos[t*k+j]] = x[t]; every pad row = 0. x [T,h], x_g [max_rows,h] bf16. */
+moe_status moe_gather(const moe_config* cfg, const void* x, const moe_topology_t* topo, void* x_g,
+                      void* stream);
+
+/* Padded scatter + weighting, Fig. 5 lines 26-27, §2.4:
+ * y[t] = sum_{j ascending} gates[t,j] * y_g[pos[t*k+j]], fp32 accumulate, bf16
+ * out. gates may be NULL (unit gates). */
+moe_status moe_scatter(const moe_config* cfg, const void* y_g, const moe_topology_t* topo,
+                       const float* gates, void* y, void* stream);
+
+/* Backward of moe_scatter: dy_g[pos[t*k+j]] = gates[t,j]*dy[t] (pad rows 0);
+ * dgates[t,j] = <y_g[pos[t*k+j]], dy[t]> (fp32). dgates may be NULL. */
+moe_status moe_scatter_bwd(const moe_config* cfg, const void* dy, const void* y_g,
+                           const moe_topology_t* topo, const float* gates, void* dy_g, float* dgates,
+                           void* stream);
+
+/* Backward of moe_gather: dx[t] = sum_j dx_g[pos[t*k+j]] (bf16 out). */
+moe_status moe_gather_bwd(const moe_config* cfg, const void* dx_g, const moe_topology_t* topo, void* dx,
+                          void* stream);
+
+/* Unpadded expert-order permutation used by expert parallelism:
+ * x_sorted[j] = x[sorted_idx[j] / k], j < T*k. */
+moe_status moe_sort_rows(const moe_config* cfg, const void* x, const moe_topology_t* topo, void* x_sorted,
+                         void* stream);
+/* y[t] = sum_j gates[t,j] * y_sorted[sorted_pos[t*k+j]] (gates may be NULL). */
+moe_status moe_unsort_rows(const moe_config* cfg, const void* y_sorted, const moe_topology_t* topo,
+                           const float* gates, void* y, void* stream);
+/* Backward of moe_unsort_rows: dy_sorted[sorted_pos[i]] = g*dy[t];
+ * dgates[t,j] = <y_sorted[sorted_pos[i]], dy[t]>. */
+moe_status moe_unsort_rows_bwd(const moe_config* cfg, const void* dy, const void* y_sorted,
+                               const moe_topology_t* topo, const float* gates, void* dy_sorted,
+                               float* dgates, void* stream);
+/* Backward of moe_sort_rows: dx[t] = sum_j dx_sorted[sorted_pos[t*k+j]]. */
+moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
+                             void* dx, void* stream);
+
+/* ---- block-sparse products, Triton notation, §5.1 ----
+ * The sparse operand has the MoE topology: logical shape [Tp, E*f] with
+ * 128x128 blocks. bf16 in, fp32 accumulate on the tensor cores, bf16 out.
+ *
+ * moe_sdd: out_s = act(A . B) on the topology's nonzero blocks (SDD),
+ *   A = a [max_rows, h]; B = b [h, E*f] (trans_b = 0, forward: W1) or
+ *   B = b^T with b [E*f, h] (trans_b = 1, SDD^T backward: W2).
+ *   out_pre (optional) receives the pre-activation A.B.
+ *   act_grad_src != NULL selects the backward epilogue
+ *   out_s = (A.B) * act'(act_grad_src) where act_grad_src is the saved
+ *   pre-activation [nnz,bs,bs] (SDD^T fused with the activation derivative).
+ * moe_dsd: trans_s = 0: out [max_rows, h] = S . B_eff (DSD; DSD^T uses
+ *   trans_b = 1 with b = W1 [h, E*f]); B_eff = b [E*f, h] or b^T.
+ *   trans_s = 1: out [E*f, h] = S^T . B_eff (DS^TD), walking the
+ *   transpose index; B_eff = b [max_rows, h] (trans_b = 0) or
+ *   b^T with b [h, max_rows] (trans_b = 1).
+ * moe_dds: trans_s = 0: out [h, E*f] = A_eff . S (DD^TS with trans_a = 1 and
+ *   a = X_g [max_rows, h]; trans_a = 0: a [h, max_rows]) via the
+ *   transpose index. trans_s = 1: out [h, max_rows] = A_eff . S^T with
+ *   A_eff = a [h, E*f] or a^T (a [E*f, h]).
+ */
+moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                   const moe_topology_t* topo, int32_t act, const void* act_grad_src, void* out_s,
+                   void* out_pre, void* stream);
+moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
+                   const moe_topology_t* topo, void* out, void* stream);
+moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
+                   const moe_topology_t* topo, void* out, void* stream);
+
+/* Router backward (softmax chain rule): dp[t,e] = dgates[t,j] where
+ * e = expert_idx[t,j], else 0; dlogits = p * (dp - <p,dp>), p = softmax(logits);
+ * dwr [h,E] fp32 = x^T . dlogits;  dx [T,h] bf16 += dlogits . wr^T (in place). */
+moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, const float* logits,
+                          const int32_t* expert_idx, const float* dgates, float* dwr, void* dx,
+                          void* ws, void* stream);
+
+/* ---- the layer: Fig. 5 forward, §5.1 backward ---- */
+typedef struct {
+  const void* wr; /* [h, E]   bf16 */
+  const void* w1; /* [h, E*f] bf16 */
+  const void* w2; /* [E*f, h] bf16 (R1: P:274 is garbled) */
+} moe_weights;
+
+typedef struct {
+  float* dwr; /* [h, E]   fp32 */
+  void* dw1;  /* [h, E*f] bf16 (fp32 accumulate) */
+  void* dw2;  /* [E*f, h] bf16 (fp32 accumulate) */
+} moe_grads;
+
+/* Tensors the forward pass keeps for the backward pass (caller-allocated). */
+typedef struct {
+  float* logits;      /* [T, E] fp32 */
+  int32_t* expert_idx;/* [T, k] */
+  float* gates;       /* [T, k] fp32 */
+  moe_topology_t topo;
+  void* x_g;          /* [max_rows, h] bf16 */
+  void* h_pre;        /* [max_nnz, bs, bs] bf16 pre-activation (may equal a for identity) */
+  void* a;            /* [max_nnz, bs, bs] bf16 activation */
+  void* y_g;          /* [max_rows, h] bf16 */
+} moe_saved;
+
+/* y [T,h] bf16 = dMoE(x [T,h] bf16): router, topology, padded gather,
+ * SDD(+act), DSD, weighted scatter; stream-ordered, no host synchronisation. */
+moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* x, void* y, moe_saved* saved,
+                       void* ws, void* stream);
+
+/* Gradients of sum(y * dy): dx [T,h] bf16 and *grads, via scatter-bwd, SDD^T
+ * (+act'), DS^TD, DSD^T, DD^TS, gather-bwd, router-bwd. */
+moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_saved* saved, const void* x,
+                        const void* dy, void* dx, moe_grads* grads, void* ws, void* stream);
+
+/* Number of kernel launches the last moe_forward / moe_backward on this
+ * thread enqueued (for the bench's gpu_launches count). */
+int moe_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_H_ */

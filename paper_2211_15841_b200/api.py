@@ -1,0 +1,265 @@
+"""Thin Python binding of the C ABI (include/moe.h), same names as the C entry
+points. Argument marshalling only: torch supplies device memory and the
+current CUDA stream; every step runs in libmoe.so kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import (MoeConfig, MoeGrads, MoeSaved, MoeTopology, MoeWeights, TOPO_FIELDS, check, lib)
+
+ACT_IDENTITY, ACT_GELU, ACT_RELU = 0, 1, 2
+
+
+def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU) -> MoeConfig:
+    return MoeConfig(int(tokens), int(hidden), int(num_experts), int(top_k), int(ffn_hidden), int(block_size),
+                     int(act), 0)
+
+
+def cfg_replace(cfg: MoeConfig, **kw) -> MoeConfig:
+    d = {n: getattr(cfg, n) for n, _ in MoeConfig._fields_}
+    d.update(kw)
+    return MoeConfig(**d)
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def moe_check_config(cfg):
+    return lib.moe_check_config(ctypes.byref(cfg))
+
+
+def moe_max_padded_rows(cfg) -> int:
+    return int(lib.moe_max_padded_rows(ctypes.byref(cfg)))
+
+
+def moe_max_nnz_blocks(cfg) -> int:
+    return int(lib.moe_max_nnz_blocks(ctypes.byref(cfg)))
+
+
+def moe_workspace_bytes(cfg) -> int:
+    return int(lib.moe_workspace_bytes(ctypes.byref(cfg)))
+
+
+def workspace(cfg, device="cuda") -> torch.Tensor:
+    return torch.empty(max(moe_workspace_bytes(cfg), 256), dtype=torch.uint8, device=device)
+
+
+class Topology:
+    """Device buffers of moe_topology_t, sized to the worst case."""
+
+    def __init__(self, cfg, device="cuda"):
+        E, bs = cfg.num_experts, cfg.block_size
+        R = cfg.tokens * cfg.top_k
+        rows, nnz = moe_max_padded_rows(cfg), moe_max_nnz_blocks(cfg)
+        F = cfg.ffn_hidden // bs
+        shapes = {"counts": E, "bins": E, "padded_bins": E, "sorted_idx": R, "pos": R, "sorted_pos": R,
+                  "row_offsets": rows // bs + 1, "col_indices": nnz, "row_indices": nnz,
+                  "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "sizes": 2}
+        self.t = {n: torch.empty(max(int(shapes[n]), 1), dtype=torch.int32, device=device) for n in TOPO_FIELDS}
+        self.struct = MoeTopology(*[self.t[n].data_ptr() for n in TOPO_FIELDS])
+
+    def __getitem__(self, name):
+        return self.t[name]
+
+    def sizes(self):
+        """(Tp, nnz) — reads back from the device (tests / host orchestration only)."""
+        s = self.t["sizes"].cpu()
+        return int(s[0]), int(s[1])
+
+
+def moe_topk(cfg, logits, expert_idx=None, gates=None):
+    T, k = cfg.tokens, cfg.top_k
+    expert_idx = expert_idx if expert_idx is not None else torch.empty(T, k, dtype=torch.int32, device=logits.device)
+    gates = gates if gates is not None else torch.empty(T, k, dtype=torch.float32, device=logits.device)
+    check("moe_topk", lib.moe_topk(ctypes.byref(cfg), _p(logits), _p(expert_idx), _p(gates), _stream()))
+    return expert_idx, gates
+
+
+def moe_router(cfg, x, wr, ws=None):
+    T, E, k = cfg.tokens, cfg.num_experts, cfg.top_k
+    dev = x.device
+    logits = torch.empty(T, E, dtype=torch.float32, device=dev)
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    gates = torch.empty(T, k, dtype=torch.float32, device=dev)
+    ws = ws if ws is not None else workspace(cfg, dev)
+    check("moe_router", lib.moe_router(ctypes.byref(cfg), _p(x), _p(wr), _p(logits), _p(idx), _p(gates), _p(ws),
+                                       _stream()))
+    return logits, idx, gates
+
+
+def moe_topology(cfg, expert_idx, topo: Topology | None = None, ws=None) -> Topology:
+    topo = topo if topo is not None else Topology(cfg, expert_idx.device)
+    ws = ws if ws is not None else workspace(cfg, expert_idx.device)
+    check("moe_topology", lib.moe_topology(ctypes.byref(cfg), _p(expert_idx), ctypes.byref(topo.struct), _p(ws),
+                                           _stream()))
+    return topo
+
+
+def moe_gather(cfg, x, topo: Topology, x_g=None):
+    x_g = x_g if x_g is not None else torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=x.dtype,
+                                                  device=x.device)
+    check("moe_gather", lib.moe_gather(ctypes.byref(cfg), _p(x), ctypes.byref(topo.struct), _p(x_g), _stream()))
+    return x_g
+
+
+def moe_scatter(cfg, y_g, topo: Topology, gates=None, y=None):
+    y = y if y is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=y_g.dtype, device=y_g.device)
+    check("moe_scatter", lib.moe_scatter(ctypes.byref(cfg), _p(y_g), ctypes.byref(topo.struct), _p(gates), _p(y),
+                                         _stream()))
+    return y
+
+
+def moe_scatter_bwd(cfg, dy, y_g, topo: Topology, gates=None, want_dgates=True):
+    dy_g = torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=dy.dtype, device=dy.device)
+    dg = torch.empty(cfg.tokens, cfg.top_k, dtype=torch.float32, device=dy.device) if want_dgates else None
+    check("moe_scatter_bwd", lib.moe_scatter_bwd(ctypes.byref(cfg), _p(dy), _p(y_g), ctypes.byref(topo.struct),
+                                                 _p(gates), _p(dy_g), _p(dg), _stream()))
+    return dy_g, dg
+
+
+def moe_gather_bwd(cfg, dx_g, topo: Topology, dx=None):
+    dx = dx if dx is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=dx_g.dtype, device=dx_g.device)
+    check("moe_gather_bwd", lib.moe_gather_bwd(ctypes.byref(cfg), _p(dx_g), ctypes.byref(topo.struct), _p(dx),
+                                               _stream()))
+    return dx
+
+
+def moe_sort_rows(cfg, x, topo: Topology, out=None):
+    out = out if out is not None else torch.empty(cfg.tokens * cfg.top_k, cfg.hidden, dtype=x.dtype, device=x.device)
+    check("moe_sort_rows", lib.moe_sort_rows(ctypes.byref(cfg), _p(x), ctypes.byref(topo.struct), _p(out),
+                                             _stream()))
+    return out
+
+
+def moe_unsort_rows(cfg, y_sorted, topo: Topology, gates=None, y=None):
+    y = y if y is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=y_sorted.dtype, device=y_sorted.device)
+    check("moe_unsort_rows", lib.moe_unsort_rows(ctypes.byref(cfg), _p(y_sorted), ctypes.byref(topo.struct),
+                                                 _p(gates), _p(y), _stream()))
+    return y
+
+
+def moe_unsort_rows_bwd(cfg, dy, y_sorted, topo: Topology, gates=None, want_dgates=True):
+    dys = torch.empty(cfg.tokens * cfg.top_k, cfg.hidden, dtype=dy.dtype, device=dy.device)
+    dg = torch.empty(cfg.tokens, cfg.top_k, dtype=torch.float32, device=dy.device) if want_dgates else None
+    check("moe_unsort_rows_bwd", lib.moe_unsort_rows_bwd(ctypes.byref(cfg), _p(dy), _p(y_sorted),
+                                                         ctypes.byref(topo.struct), _p(gates), _p(dys), _p(dg),
+                                                         _stream()))
+    return dys, dg
+
+
+def moe_sort_rows_bwd(cfg, dx_sorted, topo: Topology, dx=None):
+    dx = dx if dx is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=dx_sorted.dtype, device=dx_sorted.device)
+    check("moe_sort_rows_bwd", lib.moe_sort_rows_bwd(ctypes.byref(cfg), _p(dx_sorted), ctypes.byref(topo.struct),
+                                                     _p(dx), _stream()))
+    return dx
+
+
+def _nnz_values(cfg, device, dtype=torch.bfloat16):
+    bs = cfg.block_size
+    return torch.empty(moe_max_nnz_blocks(cfg), bs, bs, dtype=dtype, device=device)
+
+
+def moe_sdd(cfg, a, b, trans_b, topo: Topology, act=ACT_IDENTITY, act_grad_src=None, want_pre=False, out=None):
+    out = out if out is not None else _nnz_values(cfg, a.device)
+    pre = _nnz_values(cfg, a.device) if want_pre else None
+    check("moe_sdd", lib.moe_sdd(ctypes.byref(cfg), _p(a), _p(b), int(trans_b), ctypes.byref(topo.struct), int(act),
+                                 _p(act_grad_src), _p(out), _p(pre), _stream()))
+    return (out, pre) if want_pre else out
+
+
+def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
+    rows = moe_max_padded_rows(cfg)
+    n_out = cfg.num_experts * cfg.ffn_hidden if trans_s else rows
+    out = out if out is not None else torch.empty(n_out, cfg.hidden, dtype=torch.bfloat16, device=s.device)
+    check("moe_dsd", lib.moe_dsd(ctypes.byref(cfg), _p(s), int(trans_s), _p(b), int(trans_b),
+                                 ctypes.byref(topo.struct), _p(out), _stream()))
+    return out
+
+
+def moe_dds(cfg, a, trans_a, s, trans_s, topo: Topology, out=None):
+    rows = moe_max_padded_rows(cfg)
+    n_out = rows if trans_s else cfg.num_experts * cfg.ffn_hidden
+    out = out if out is not None else torch.empty(cfg.hidden, n_out, dtype=torch.bfloat16, device=s.device)
+    check("moe_dds", lib.moe_dds(ctypes.byref(cfg), _p(a), int(trans_a), _p(s), int(trans_s),
+                                 ctypes.byref(topo.struct), _p(out), _stream()))
+    return out
+
+
+def moe_router_bwd(cfg, x, wr, logits, expert_idx, dgates, dx, ws=None):
+    dwr = torch.empty(cfg.hidden, cfg.num_experts, dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else workspace(cfg, x.device)
+    check("moe_router_bwd", lib.moe_router_bwd(ctypes.byref(cfg), _p(x), _p(wr), _p(logits), _p(expert_idx),
+                                               _p(dgates), _p(dwr), _p(dx), _p(ws), _stream()))
+    return dwr
+
+
+@dataclass
+class Saved:
+    logits: torch.Tensor
+    expert_idx: torch.Tensor
+    gates: torch.Tensor
+    topo: Topology
+    x_g: torch.Tensor
+    h_pre: torch.Tensor | None
+    a: torch.Tensor
+    y_g: torch.Tensor
+    struct: MoeSaved = None
+
+    @staticmethod
+    def allocate(cfg, device="cuda") -> "Saved":
+        T, E, k, h = cfg.tokens, cfg.num_experts, cfg.top_k, cfg.hidden
+        rows = moe_max_padded_rows(cfg)
+        s = Saved(torch.empty(T, E, dtype=torch.float32, device=device),
+                  torch.empty(T, k, dtype=torch.int32, device=device),
+                  torch.empty(T, k, dtype=torch.float32, device=device),
+                  Topology(cfg, device),
+                  torch.empty(rows, h, dtype=torch.bfloat16, device=device),
+                  None if cfg.act == ACT_IDENTITY else _nnz_values(cfg, device),
+                  _nnz_values(cfg, device),
+                  torch.empty(rows, h, dtype=torch.bfloat16, device=device))
+        s.struct = MoeSaved(s.logits.data_ptr(), s.expert_idx.data_ptr(), s.gates.data_ptr(), s.topo.struct,
+                            s.x_g.data_ptr(), None if s.h_pre is None else s.h_pre.data_ptr(), s.a.data_ptr(),
+                            s.y_g.data_ptr())
+        return s
+
+
+def weights_struct(wr, w1, w2) -> MoeWeights:
+    return MoeWeights(wr.data_ptr(), w1.data_ptr(), w2.data_ptr())
+
+
+def moe_forward(cfg, wr, w1, w2, x, y=None, saved: Saved | None = None, ws=None):
+    y = y if y is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device=x.device)
+    saved = saved if saved is not None else Saved.allocate(cfg, x.device)
+    ws = ws if ws is not None else workspace(cfg, x.device)
+    w = weights_struct(wr, w1, w2)
+    check("moe_forward", lib.moe_forward(ctypes.byref(cfg), ctypes.byref(w), _p(x), _p(y), ctypes.byref(saved.struct),
+                                         _p(ws), _stream()))
+    return y, saved
+
+
+def moe_backward(cfg, wr, w1, w2, saved: Saved, x, dy, dx=None, grads=None, ws=None):
+    dev = x.device
+    dx = dx if dx is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device=dev)
+    if grads is None:
+        grads = (torch.empty(cfg.hidden, cfg.num_experts, dtype=torch.float32, device=dev),
+                 torch.empty(cfg.hidden, cfg.num_experts * cfg.ffn_hidden, dtype=torch.bfloat16, device=dev),
+                 torch.empty(cfg.num_experts * cfg.ffn_hidden, cfg.hidden, dtype=torch.bfloat16, device=dev))
+    ws = ws if ws is not None else workspace(cfg, dev)
+    w = weights_struct(wr, w1, w2)
+    g = MoeGrads(grads[0].data_ptr(), grads[1].data_ptr(), grads[2].data_ptr())
+    check("moe_backward", lib.moe_backward(ctypes.byref(cfg), ctypes.byref(w), ctypes.byref(saved.struct), _p(x),
+                                           _p(dy), _p(dx), ctypes.byref(g), _p(ws), _stream()))
+    return dx, grads
+
+
+def moe_last_launch_count() -> int:
+    return int(lib.moe_last_launch_count())

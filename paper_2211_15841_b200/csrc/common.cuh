@@ -1,0 +1,62 @@
+// common.cuh — shared host helpers for the C ABI: error reporting, argument
+// validation, workspace layout, launch accounting.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/moe.h"
+
+namespace moe {
+
+moe_status set_error(moe_status st, const char* fmt, ...);
+void clear_error();
+void count_launch(int n = 1);
+void reset_launch_count();
+
+#define MOE_CHECK_ARG(cond, ...)                              \
+  do {                                                        \
+    if (!(cond)) return ::moe::set_error(MOE_EINVAL, __VA_ARGS__); \
+  } while (0)
+
+#define MOE_CHECK_LAUNCH(name)                                                         \
+  do {                                                                                 \
+    cudaError_t _e = cudaGetLastError();                                               \
+    if (_e != cudaSuccess)                                                             \
+      return ::moe::set_error(MOE_ECUDA, "%s: %s", name, cudaGetErrorString(_e));      \
+    ::moe::count_launch();                                                             \
+  } while (0)
+
+#define MOE_TRY(expr)                  \
+  do {                                 \
+    moe_status _s = (expr);            \
+    if (_s != MOE_OK) return _s;       \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Host-side config validation for the GPU path.
+moe_status check_config_gpu(const moe_config* cfg);
+moe_status check_topo(const moe_topology_t* t);
+
+// Workspace layout (byte offsets inside the caller's ws buffer).
+struct WsLayout {
+  size_t topo_chunk_counts;  // int32 [n_chunks][E]
+  size_t topo_end;
+  // backward scratch
+  size_t dy_g;      // bf16 [max_rows, h]
+  size_t dh;        // bf16 [max_nnz, bs, bs]
+  size_t dx_g;      // bf16 [max_rows, h]
+  size_t dgates;    // f32 [T, k]
+  size_t dlogits;   // f32 [T, E]
+  size_t dwr_part;  // f32 [n_parts, h, E]
+  size_t total;
+};
+constexpr int kTopoChunk = 1024;  // assignments per topology CTA
+int router_bwd_parts(const moe_config* cfg);
+WsLayout ws_layout(const moe_config* cfg);
+
+}  // namespace moe

@@ -1,0 +1,65 @@
+// layer.cu — the dMoE layer as one stream-ordered sequence of the kernels
+// above. Forward follows Fig. 5; backward follows the operation
+// list of §5.1. No host synchronisation: data-dependent sizes live
+// in saved->topo.sizes on the device.
+#include "common.cuh"
+
+using namespace moe;
+
+extern "C" {
+
+moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* x, void* y, moe_saved* sv,
+                       void* ws, void* stream) {
+  reset_launch_count();
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(w && w->wr && w->w1 && w->w2 && x && y && sv && ws, "moe_forward: NULL pointer");
+  MOE_CHECK_ARG(sv->logits && sv->expert_idx && sv->gates && sv->x_g && sv->a && sv->y_g,
+                "moe_forward: NULL saved tensor");
+  const bool id = cfg->act == MOE_ACT_IDENTITY;
+  MOE_CHECK_ARG(id || sv->h_pre, "moe_forward: saved->h_pre required for a non-identity activation");
+  // (1) indices, weights = router(x)
+  MOE_TRY(moe_router(cfg, x, w->wr, sv->logits, sv->expert_idx, sv->gates, ws, stream));
+  // (2) topology = make_topology(indices)
+  MOE_TRY(moe_topology(cfg, sv->expert_idx, &sv->topo, ws, stream));
+  // (3) x = padded_gather(x, indices)
+  MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
+  // (4) x = sdd(x, w1, topology) [+ act]; x = dsd(x, w2)
+  MOE_TRY(moe_sdd(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->h_pre, stream));
+  MOE_TRY(moe_dsd(cfg, sv->a, 0, w->w2, 0, &sv->topo, sv->y_g, stream));
+  // (5) x = padded_scatter(x, indices) * weights
+  MOE_TRY(moe_scatter(cfg, sv->y_g, &sv->topo, sv->gates, y, stream));
+  return MOE_OK;
+}
+
+moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_saved* sv, const void* x,
+                        const void* dy, void* dx, moe_grads* g, void* ws, void* stream) {
+  reset_launch_count();
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(w && sv && x && dy && dx && g && g->dwr && g->dw1 && g->dw2 && ws, "moe_backward: NULL pointer");
+  const bool id = cfg->act == MOE_ACT_IDENTITY;
+  const WsLayout L = ws_layout(cfg);
+  char* wsb = reinterpret_cast<char*>(ws);
+  void* dy_g = wsb + L.dy_g;
+  void* dh = wsb + L.dh;
+  void* dx_g = wsb + L.dx_g;
+  float* dgates = reinterpret_cast<float*>(wsb + L.dgates);
+  const moe_topology_t* topo = &sv->topo;
+  // b1: dY_g = gates * dy (un-permuted rows), dgates = <Y_g, dy>
+  MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
+  // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
+  MOE_TRY(moe_sdd(cfg, dy_g, w->w2, 1, topo, id ? MOE_ACT_IDENTITY : cfg->act, id ? nullptr : sv->h_pre, dh,
+                  nullptr, stream));
+  // b3: DS^TD: dW2 = A^T . dY_g                              "second layer weight gradient"
+  MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
+  // b4: DSD^T: dX_g = dH . W1^T                              "first layer data gradient"
+  MOE_TRY(moe_dsd(cfg, dh, 0, w->w1, 1, topo, dx_g, stream));
+  // b5: DD^TS: dW1 = X_g^T . dH                              "first layer weight gradient"
+  MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
+  // b6: dx = sum_j dX_g[pos]
+  MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
+  // b7: router backward (dWr, dx += dlogits . Wr^T)
+  MOE_TRY(moe_router_bwd(cfg, x, w->wr, sv->logits, sv->expert_idx, dgates, g->dwr, dx, ws, stream));
+  return MOE_OK;
+}
+
+}  // extern "C"

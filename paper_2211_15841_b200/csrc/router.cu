@@ -1,0 +1,271 @@
+// router.cu — learned router (§2.1): logits = x . Wr, softmax,
+// greedy top-k; and its backward pass (softmax chain rule).
+//
+// v1 SIMT implementation (fp32 FMA on CUDA cores, bf16 operands staged in
+// shared memory). The router is ~4% of the strict layer roofline (SURVEY.md
+// §8(a) a1/b7); DESIGN.md §5 tracks moving it onto tcgen05.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <float.h>
+
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int RT_TOK = 64;   // tokens per CTA
+constexpr int RT_EXP = 64;   // experts per CTA
+constexpr int RT_K = 32;     // contraction chunk
+
+// logits[t, e] = sum_i x[t,i] * wr[i,e]; 256 threads, each 4 tokens x 4 experts.
+__global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16* __restrict__ x,
+                                                             const __nv_bfloat16* __restrict__ wr,
+                                                             float* __restrict__ logits, int T, int h, int E) {
+  __shared__ float sx[RT_K][RT_TOK + 1];
+  __shared__ float sw[RT_K][RT_EXP];
+  const int t0 = blockIdx.x * RT_TOK, e0 = blockIdx.y * RT_EXP;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // experts tx*4.., tokens ty*4..
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < h; k0 += RT_K) {
+    for (int i = threadIdx.x; i < RT_TOK * RT_K; i += 256) {
+      const int tt = i / RT_K, kk = i % RT_K;
+      const int t = t0 + tt;
+      sx[kk][tt] = (t < T && k0 + kk < h) ? __bfloat162float(x[(size_t)t * h + k0 + kk]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < RT_K * RT_EXP; i += 256) {
+      const int kk = i / RT_EXP, ee = i % RT_EXP;
+      const int e = e0 + ee;
+      sw[kk][ee] = (e < E && k0 + kk < h) ? __bfloat162float(wr[(size_t)(k0 + kk) * E + e]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < RT_K; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sx[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sw[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int t = t0 + ty * 4 + i;
+    if (t >= T) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = e0 + tx * 4 + j;
+      if (e < E) logits[(size_t)t * E + e] = acc[i][j];
+    }
+  }
+}
+
+// One warp per token: top-k of the fp32 logits (descending, ties -> lower e)
+// then gates = softmax probabilities of the chosen experts.
+constexpr int kMaxTopK = 32;
+__global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ gates,
+                            int T, int E, int k) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= T) return;
+  const float* row = logits + (size_t)t * E;
+  // softmax denominator with the row max (fixed ascending-e per-lane order, then tree)
+  float m = -FLT_MAX;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, row[e]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float ssum = 0.f;
+  for (int e = lane; e < E; e += 32) ssum += expf(row[e] - m);
+  for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  // k rounds of arg-max excluding already chosen experts
+  unsigned chosen = 0;  // per-lane bitmask of chosen experts e = lane + 32*b (E <= 1024)
+  for (int j = 0; j < k; ++j) {
+    float bv = -FLT_MAX;
+    int be = 0x7fffffff;
+    for (int b = 0, e = lane; e < E; ++b, e += 32) {
+      const bool taken = (chosen >> b) & 1u;
+      const float v = row[e];
+      if (!taken && (v > bv || (v == bv && e < be))) {
+        bv = v;
+        be = e;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, be, o);
+      if (ov > bv || (ov == bv && oe < be)) {
+        bv = ov;
+        be = oe;
+      }
+    }
+    if ((be & 31) == lane) chosen |= 1u << (be >> 5);
+    if (lane == 0) {
+      idx[(size_t)t * k + j] = be;
+      gates[(size_t)t * k + j] = expf(bv - m) / ssum;
+    }
+  }
+}
+
+// dlogits[t,:] = p * (dp - <p, dp>) with p = softmax(logits[t,:]), dp sparse from dgates.
+__global__ void router_dlogits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
+                                      const float* __restrict__ dgates, float* __restrict__ dlogits, int T, int E,
+                                      int k) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= T) return;
+  const float* row = logits + (size_t)t * E;
+  float m = -FLT_MAX;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, row[e]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float ssum = 0.f;
+  for (int e = lane; e < E; e += 32) ssum += expf(row[e] - m);
+  for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+  const float inv = 1.f / ssum;
+  // <p, dp> = sum_j p[idx_j] * dgates_j
+  float pdp = 0.f;
+  for (int j = 0; j < k; ++j) {
+    const int e = idx[(size_t)t * k + j];
+    pdp += expf(row[e] - m) * inv * dgates[(size_t)t * k + j];
+  }
+  for (int e = lane; e < E; e += 32) {
+    float dp = 0.f;
+    for (int j = 0; j < k; ++j)
+      if (idx[(size_t)t * k + j] == e) dp += dgates[(size_t)t * k + j];
+    const float p = expf(row[e] - m) * inv;
+    dlogits[(size_t)t * E + e] = p * (dp - pdp);
+  }
+}
+
+// Partial dWr over a token range: part[q][i][e] = sum_{t in range q} x[t,i] dlogits[t,e].
+// grid (parts, ceil(h/32)), 256 threads: 32 rows i x 64 experts per CTA slice.
+__global__ void __launch_bounds__(256) router_dwr_part_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const float* __restrict__ dlogits,
+                                                               float* __restrict__ part, int T, int h, int E,
+                                                               int tok_per_part) {
+  __shared__ float sx[32][33];
+  __shared__ float sd[32][64];
+  const int q = blockIdx.x, i0 = blockIdx.y * 32;
+  const int tb = q * tok_per_part, te = min(T, tb + tok_per_part);
+  for (int e0 = 0; e0 < E; e0 += 64) {
+    const int ti = threadIdx.x / 8;        // row i within slice (0..31)
+    const int tj = (threadIdx.x % 8) * 8;  // 8 experts
+    float acc[8] = {};
+    for (int t0 = tb; t0 < te; t0 += 32) {
+      for (int u = threadIdx.x; u < 32 * 32; u += 256) {
+        const int tt = u / 32, ii = u % 32;
+        const int t = t0 + tt, i = i0 + ii;
+        sx[tt][ii] = (t < te && i < h) ? __bfloat162float(x[(size_t)t * h + i]) : 0.f;
+      }
+      for (int u = threadIdx.x; u < 32 * 64; u += 256) {
+        const int tt = u / 64, ee = u % 64;
+        const int t = t0 + tt, e = e0 + ee;
+        sd[tt][ee] = (t < te && e < E) ? dlogits[(size_t)t * E + e] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int tt = 0; tt < 32; ++tt) {
+        const float a = sx[tt][ti];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fmaf(a, sd[tt][tj + j], acc[j]);
+      }
+      __syncthreads();
+    }
+    const int i = i0 + ti;
+    if (i < h)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = e0 + tj + j;
+        if (e < E) part[((size_t)q * h + i) * E + e] = acc[j];
+      }
+  }
+}
+
+__global__ void router_dwr_reduce_kernel(const float* __restrict__ part, float* __restrict__ dwr, int parts, int n) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  float s = 0.f;
+  for (int q = 0; q < parts; ++q) s += part[(size_t)q * n + o];
+  dwr[o] = s;
+}
+
+// dx[t, i] += sum_e dlogits[t,e] * wr[i,e]; one warp per token, wr^T slices cached in smem.
+__global__ void __launch_bounds__(256) router_dx_kernel(const float* __restrict__ dlogits,
+                                                         const __nv_bfloat16* __restrict__ wr,
+                                                         __nv_bfloat16* __restrict__ dx, int T, int h, int E) {
+  extern __shared__ float s_dl[];  // [8 warps][E]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t < T)
+    for (int e = lane; e < E; e += 32) s_dl[warp * E + e] = dlogits[(size_t)t * E + e];
+  __syncwarp();
+  if (t >= T) return;
+  for (int i = lane; i < h; i += 32) {
+    const __nv_bfloat16* w = wr + (size_t)i * E;
+    float s = 0.f;
+    for (int e = 0; e < E; ++e) s = fmaf(s_dl[warp * E + e], __bfloat162float(w[e]), s);
+    const size_t o = (size_t)t * h + i;
+    dx[o] = __float2bfloat16_rn(__bfloat162float(dx[o]) + s);
+  }
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_idx, float* gates, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(logits && expert_idx && gates, "moe_topk: NULL pointer");
+  if (cfg->top_k > kMaxTopK) return set_error(MOE_EUNSUPPORTED, "top_k=%lld > %d", (long long)cfg->top_k, kMaxTopK);
+  const int T = (int)cfg->tokens;
+  topk_kernel<<<(int)ceil_div(T, 8), 256, 0, as_stream(stream)>>>(logits, expert_idx, gates, T,
+                                                                   (int)cfg->num_experts, (int)cfg->top_k);
+  MOE_CHECK_LAUNCH("moe_topk");
+  return MOE_OK;
+}
+
+moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, float* logits, int32_t* expert_idx,
+                      float* gates, void* ws, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(x && wr && logits && expert_idx && gates, "moe_router: NULL pointer");
+  (void)ws;
+  const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
+  dim3 grid((unsigned)ceil_div(T, RT_TOK), (unsigned)ceil_div(E, RT_EXP));
+  router_logits_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x),
+                                                            reinterpret_cast<const __nv_bfloat16*>(wr), logits, T, h,
+                                                            E);
+  MOE_CHECK_LAUNCH("router_logits");
+  return moe_topk(cfg, logits, expert_idx, gates, stream);
+}
+
+moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, const float* logits,
+                          const int32_t* expert_idx, const float* dgates, float* dwr, void* dx, void* ws,
+                          void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(x && wr && logits && expert_idx && dgates && dwr && dx && ws, "moe_router_bwd: NULL pointer");
+  const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts, k = (int)cfg->top_k;
+  const WsLayout L = ws_layout(cfg);
+  float* dlogits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + L.dlogits);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + L.dwr_part);
+  cudaStream_t s = as_stream(stream);
+  router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, dlogits, T, E, k);
+  MOE_CHECK_LAUNCH("router_dlogits");
+  const int parts = router_bwd_parts(cfg);
+  const int tpp = (int)ceil_div(T, parts);
+  router_dwr_part_kernel<<<dim3(parts, (unsigned)ceil_div(h, 32)), 256, 0, s>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);
+  MOE_CHECK_LAUNCH("router_dwr_part");
+  router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
+  MOE_CHECK_LAUNCH("router_dwr_reduce");
+  const size_t smem = 8 * E * sizeof(float);
+  if (smem > 48 * 1024) return set_error(MOE_EUNSUPPORTED, "router_bwd: num_experts too large");
+  router_dx_kernel<<<(int)ceil_div(T, 8), 256, smem, s>>>(dlogits, reinterpret_cast<const __nv_bfloat16*>(wr),
+                                                          reinterpret_cast<__nv_bfloat16*>(dx), T, h, E);
+  MOE_CHECK_LAUNCH("router_dx");
+  return MOE_OK;
+}
+
+}  // extern "C"

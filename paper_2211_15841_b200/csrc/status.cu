@@ -1,0 +1,144 @@
+// status.cu — error reporting, config validation and size queries of the C ABI
+// (include/moe.h). Host only; no CUDA calls except the SM-count query.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace moe {
+
+static thread_local char g_err[512] = "";
+static thread_local int g_launches = 0;
+
+moe_status set_error(moe_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+void clear_error() { g_err[0] = 0; }
+void count_launch(int n) { g_launches += n; }
+void reset_launch_count() { g_launches = 0; }
+
+moe_status check_config_gpu(const moe_config* cfg) {
+  moe_status st = moe_check_config(cfg);
+  return st;
+}
+
+moe_status check_topo(const moe_topology_t* t) {
+  if (!t) return set_error(MOE_EINVAL, "topology pointer is NULL");
+  if (!t->counts || !t->bins || !t->padded_bins || !t->sorted_idx || !t->pos || !t->sorted_pos ||
+      !t->row_offsets || !t->col_indices || !t->row_indices || !t->t_col_offsets || !t->t_block_offsets ||
+      !t->t_row_indices || !t->sizes)
+    return set_error(MOE_EINVAL, "topology has a NULL array");
+  return MOE_OK;
+}
+
+int router_bwd_parts(const moe_config* cfg) {
+  // split of the token (K) dimension of dWr = x^T dlogits; fixed per config so
+  // the reduction order is deterministic
+  int64_t parts = ceil_div(cfg->tokens, 256);
+  if (parts > 256) parts = 256;
+  if (parts < 1) parts = 1;
+  return (int)parts;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+WsLayout ws_layout(const moe_config* cfg) {
+  WsLayout L{};
+  const int64_t R = cfg->tokens * cfg->top_k;
+  const int64_t n_chunks = ceil_div(R > 0 ? R : 1, kTopoChunk);
+  const int64_t rows = moe_max_padded_rows(cfg);
+  const int64_t nnz = moe_max_nnz_blocks(cfg);
+  const int64_t bs = cfg->block_size, h = cfg->hidden, E = cfg->num_experts;
+  size_t off = 0;
+  L.topo_chunk_counts = off;
+  off = align256(off + sizeof(int32_t) * n_chunks * E);
+  L.topo_end = off;
+  L.dy_g = off;
+  off = align256(off + 2 * rows * h);
+  L.dh = off;
+  off = align256(off + 2 * nnz * bs * bs);
+  L.dx_g = off;
+  off = align256(off + 2 * rows * h);
+  L.dgates = off;
+  off = align256(off + 4 * R);
+  L.dlogits = off;
+  off = align256(off + 4 * cfg->tokens * E);
+  L.dwr_part = off;
+  off = align256(off + 4 * (size_t)router_bwd_parts(cfg) * h * E);
+  L.total = off;
+  return L;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+const char* moe_last_error(void) { return g_err; }
+
+int moe_last_launch_count(void) { return g_launches; }
+
+moe_status moe_check_config(const moe_config* cfg) {
+  if (!cfg) return set_error(MOE_EINVAL, "config pointer is NULL");
+  if (cfg->tokens < 1) return set_error(MOE_EINVAL, "tokens=%lld must be >= 1", (long long)cfg->tokens);
+  if (cfg->hidden < 1) return set_error(MOE_EINVAL, "hidden=%lld must be >= 1", (long long)cfg->hidden);
+  if (cfg->num_experts < 1)
+    return set_error(MOE_EINVAL, "num_experts=%lld must be >= 1", (long long)cfg->num_experts);
+  if (cfg->top_k < 1 || cfg->top_k > cfg->num_experts)
+    return set_error(MOE_EINVAL, "top_k=%lld must be in [1, num_experts=%lld]", (long long)cfg->top_k,
+                     (long long)cfg->num_experts);
+  if (cfg->block_size < 1) return set_error(MOE_EINVAL, "block_size must be >= 1");
+  if (cfg->ffn_hidden < 1 || cfg->ffn_hidden % cfg->block_size)
+    return set_error(MOE_ESHAPE, "ffn_hidden=%lld must be a positive multiple of block_size=%lld",
+                     (long long)cfg->ffn_hidden, (long long)cfg->block_size);
+  if (cfg->act < MOE_ACT_IDENTITY || cfg->act > MOE_ACT_RELU)
+    return set_error(MOE_EINVAL, "act=%d is not a moe_act", cfg->act);
+  if (cfg->reserved != 0) return set_error(MOE_EINVAL, "reserved field must be 0");
+  if (cfg->block_size != 128)
+    return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
+                     (long long)cfg->block_size);
+  if (cfg->hidden % 128)
+    return set_error(MOE_EUNSUPPORTED, "hidden=%lld must be a multiple of 128 on the GPU path",
+                     (long long)cfg->hidden);
+  if (cfg->num_experts > 1024)
+    return set_error(MOE_EUNSUPPORTED, "num_experts=%lld > 1024", (long long)cfg->num_experts);
+  if (cfg->tokens * cfg->top_k > (int64_t)1 << 30)
+    return set_error(MOE_EUNSUPPORTED, "tokens*top_k too large for int32 indices");
+  return MOE_OK;
+}
+
+int64_t moe_max_padded_rows(const moe_config* cfg) {
+  if (!cfg || cfg->block_size < 1) return 0;
+  const int64_t R = cfg->tokens * cfg->top_k, bs = cfg->block_size;
+  const int64_t nonempty = R < cfg->num_experts ? R : cfg->num_experts;
+  return bs * ((R + nonempty * (bs - 1)) / bs);
+}
+
+int64_t moe_max_nnz_blocks(const moe_config* cfg) {
+  if (!cfg || cfg->block_size < 1) return 0;
+  return moe_max_padded_rows(cfg) / cfg->block_size * (cfg->ffn_hidden / cfg->block_size);
+}
+
+size_t moe_workspace_bytes(const moe_config* cfg) {
+  if (!cfg) return 0;
+  return ws_layout(cfg).total;
+}
+
+int moe_device_sm_count(void) {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) ==
+                                                   cudaSuccess)
+      cached = n;
+    else
+      return 148;
+  }
+  return cached;
+}
+
+}  // extern "C"

@@ -1,0 +1,395 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bars: bit-exact for routing indices, histograms, bins,
+positions and every BCSR / COO / transpose index; bf16 tensors within a
+relative Frobenius error of 1e-2 of the fp64 oracle (BASELINE.json north_star);
+fp32 gates / logits within 1e-4 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as O
+from synth import inputs as S
+
+pytestmark = pytest.mark.gpu
+
+FRO_TOL = 1e-2
+
+
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def api():
+    from paper_2211_15841_b200 import api as A
+    return A
+
+
+def rel_fro(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (den if den > 0 else 1.0)
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def oracle_plan_topo(idx_np, E, f):
+    plan = O.make_plan(idx_np, E, 128)
+    return plan, O.make_topology_closed_form(plan, 128, f)
+
+
+def check_topology_exact(A, topo_gpu, plan, topo, R):
+    Tp, nnz = topo_gpu.sizes()
+    assert Tp == plan.Tp and nnz == topo.nnz
+    g = {k: v.cpu().numpy() for k, v in topo_gpu.t.items()}
+    np.testing.assert_array_equal(g["counts"], plan.counts)
+    np.testing.assert_array_equal(g["bins"], plan.bins)
+    np.testing.assert_array_equal(g["padded_bins"], plan.padded_bins)
+    np.testing.assert_array_equal(g["sorted_idx"][:R], plan.sorted_idx)
+    np.testing.assert_array_equal(g["pos"][:R], plan.pos)
+    inv = np.empty(R, np.int64)
+    inv[plan.sorted_idx] = np.arange(R)
+    np.testing.assert_array_equal(g["sorted_pos"][:R], inv)
+    np.testing.assert_array_equal(g["row_offsets"][:Tp // 128 + 1], topo.row_offsets)
+    np.testing.assert_array_equal(g["col_indices"][:nnz], topo.col_indices)
+    np.testing.assert_array_equal(g["row_indices"][:nnz], topo.row_indices)
+    np.testing.assert_array_equal(g["t_col_offsets"], topo.t_col_offsets)
+    np.testing.assert_array_equal(g["t_block_offsets"][:nnz], topo.t_block_offsets)
+    np.testing.assert_array_equal(g["t_row_indices"][:nnz], topo.t_row_indices)
+
+
+# ------------------------------------------------------------------ routing
+
+@pytest.mark.parametrize("T,E,k,ties", [(1000, 64, 1, False), (777, 64, 2, True), (4096, 4, 1, True),
+                                        (513, 8, 3, False), (100, 1, 1, False), (64, 256, 4, True)])
+def test_topk_bit_exact(T, E, k, ties):
+    d = dev()
+    A = api()
+    logits = S.random_logits(T, E, seed=T + E, ties=ties)
+    cfg = A.make_config(T, 128, E, k, 128)
+    idx, gates = A.moe_topk(cfg, logits.to(d))
+    want_idx, want_g = O.topk(S.to_f64(logits), k)
+    np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
+    np.testing.assert_allclose(gates.cpu().numpy(), want_g, rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("name,T", [("C0", 1000), ("C1", 4096), ("C2", 2048)])
+def test_router_logits_and_routing(name, T):
+    d = dev()
+    A = api()
+    shp = S.CONFIGS[name]
+    inp = S.make_inputs(shp, seed=1, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn)
+    logits, idx, gates = A.moe_router(cfg, inp["x"].to(d), inp["wr"].to(d))
+    L = O.router_logits(S.to_f64(inp["x"]), S.to_f64(inp["wr"]))
+    err = np.abs(logits.cpu().double().numpy() - L).max()
+    assert err < 1e-4 * max(1.0, np.abs(L).max()), err
+    want_idx, want_g = O.topk(L, shp.top_k)
+    got = idx.cpu().numpy()
+    # routing must agree except where the oracle's top-k margin is inside the
+    # fp32 accumulation error (several results correct there: check validity)
+    srt = -np.sort(-L, axis=1)
+    margin = srt[:, shp.top_k - 1] - srt[:, shp.top_k] if shp.experts > shp.top_k else np.full(T, np.inf)
+    near = margin < 4 * err + 1e-7
+    assert (got[~near] == want_idx[~near]).all()
+    for t in np.nonzero(near)[0]:
+        assert L[t, got[t, -1]] >= srt[t, shp.top_k - 1] - 8 * err - 1e-7
+    np.testing.assert_allclose(gates.cpu().numpy()[~near], want_g[~near], rtol=1e-4, atol=1e-6)
+
+
+# ------------------------------------------------------------------ topology
+
+@pytest.mark.parametrize("T,E,k,f,zipf", [(1000, 4, 1, 512, 0.0), (32768, 64, 1, 2048, 0.0), (8192, 64, 2, 4096, 0.0),
+                                          (5000, 64, 1, 3072, 1.5), (3, 64, 1, 256, 0.0), (4099, 16, 4, 128, 0.7),
+                                          (20000, 1024, 2, 128, 0.3), (1, 1, 1, 128, 0.0)])
+def test_topology_bit_exact(T, E, k, f, zipf):
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(T, E, k, seed=T, zipf=zipf)
+    cfg = A.make_config(T, 128, E, k, f)
+    topo = A.moe_topology(cfg, idx.to(d))
+    plan, otopo = oracle_plan_topo(idx.numpy(), E, f)
+    check_topology_exact(A, topo, plan, otopo, T * k)
+
+
+def test_topology_deterministic_repeat():
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(30000, 64, 2, seed=9, zipf=0.5).to(d)
+    cfg = A.make_config(30000, 128, 64, 2, 512)
+    t1 = A.moe_topology(cfg, idx)
+    t2 = A.moe_topology(cfg, idx)
+    for name in t1.t:
+        assert torch.equal(t1[name], t2[name]), name
+
+
+# ------------------------------------------------------------------ permutation
+
+@pytest.mark.parametrize("T,h,E,k", [(1000, 256, 4, 1), (3000, 512, 64, 2), (777, 1024, 8, 3)])
+def test_permutation_kernels(T, h, E, k):
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(T, E, k, seed=T + 1, zipf=0.8)
+    cfg = A.make_config(T, h, E, k, 128)
+    g = torch.Generator().manual_seed(T)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    gates = torch.rand(T, k, generator=g)
+    topo = A.moe_topology(cfg, idx.to(d))
+    plan, _ = oracle_plan_topo(idx.numpy(), E, 128)
+    Tp = plan.Tp
+    # gather: bit-exact copy with zero pad rows
+    xg = A.moe_gather(cfg, x.to(d), topo)
+    want = O.padded_gather(S.to_f64(x), plan, k)
+    np.testing.assert_array_equal(f64(xg[:Tp]), want)
+    # scatter: weighted sum (fp32 accumulate, bf16 out)
+    yg = torch.randn(A.moe_max_padded_rows(cfg), h, generator=g).to(torch.bfloat16)
+    y = A.moe_scatter(cfg, yg.to(d), topo, gates.to(d))
+    want_y = O.padded_scatter(f64(yg[:Tp]), plan, S.to_f64(gates), T, k)
+    assert rel_fro(f64(y), want_y) < 4e-3
+    if k == 1:  # unit gates, top-1 -> exact round trip
+        y1 = A.moe_scatter(cfg, xg, topo, None)
+        assert torch.equal(y1.cpu(), x)
+    # scatter backward: dY_g rows = g*dy, pad rows 0; dgates = <Y_g, dy>
+    dy = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    dyg, dg = A.moe_scatter_bwd(cfg, dy.to(d), yg.to(d), topo, gates.to(d))
+    want_dyg = np.zeros((Tp, h))
+    want_dg = np.zeros((T, k))
+    for t in range(T):
+        for j in range(k):
+            p = plan.pos[t * k + j]
+            want_dyg[p] = float(gates[t, j]) * S.to_f64(dy[t])
+            want_dg[t, j] = f64(yg[p]) @ S.to_f64(dy[t])
+    assert rel_fro(f64(dyg[:Tp]), want_dyg) < 4e-3
+    pad = np.ones(Tp, bool)
+    pad[plan.pos] = False
+    assert (f64(dyg[:Tp])[pad] == 0).all()
+    assert rel_fro(dg.cpu().numpy(), want_dg) < 1e-4
+    # gather backward
+    dxg = torch.randn(A.moe_max_padded_rows(cfg), h, generator=g).to(torch.bfloat16)
+    dx = A.moe_gather_bwd(cfg, dxg.to(d), topo)
+    want_dx = np.zeros((T, h))
+    for i in range(T * k):
+        want_dx[i // k] += f64(dxg[plan.pos[i]])
+    assert rel_fro(f64(dx), want_dx) < 4e-3
+    # unpadded expert-order permutation (expert-parallel dispatch) round trip
+    xs = A.moe_sort_rows(cfg, x.to(d), topo)
+    np.testing.assert_array_equal(f64(xs), S.to_f64(x)[plan.sorted_idx // k])
+    yb = A.moe_unsort_rows(cfg, xs, topo, None)
+    np.testing.assert_allclose(f64(yb), k * S.to_f64(x), rtol=1e-2)
+
+
+# ------------------------------------------------------------------ block-sparse products
+
+def product_case(T, h, f, E, k, zipf, seed):
+    idx = S.random_expert_idx(T, E, k, seed=seed, zipf=zipf)
+    plan, topo = oracle_plan_topo(idx.numpy(), E, f)
+    g = torch.Generator().manual_seed(seed)
+    rows = O.max_padded_rows(T, k, E, 128)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    w1 = (torch.randn(h, E * f, generator=g) / h ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(E * f, h, generator=g) / f ** 0.5).to(torch.bfloat16)
+    dyg = torch.randn(rows, h, generator=g).to(torch.bfloat16)
+    dyg[plan.Tp:] = 0
+    return idx, plan, topo, x, w1, w2, dyg
+
+
+PRODUCT_CASES = [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2), (2500, 768, 384, 8, 1, 0.5, 3)]
+
+
+@pytest.mark.parametrize("case", PRODUCT_CASES)
+def test_six_products(case):
+    d = dev()
+    A = api()
+    T, h, f, E, k, zipf, seed = case
+    idx, plan, topo, x, w1, w2, dyg = product_case(*case)
+    Tp, nnz = plan.Tp, topo.nnz
+    cfg = A.make_config(T, h, E, k, f, act=A.ACT_GELU)
+    tg = A.moe_topology(cfg, idx.to(d))
+    xg = A.moe_gather(cfg, x.to(d), tg)
+    xg64 = O.padded_gather(S.to_f64(x), plan, k)
+    # SDD (+gelu, pre-activation kept)
+    a_s, h_s = A.moe_sdd(cfg, xg, w1.to(d), 0, tg, act=A.ACT_GELU, want_pre=True)
+    H = O.sdd(xg64, S.to_f64(w1), topo)
+    assert rel_fro(f64(h_s[:nnz]), H) < FRO_TOL
+    Aact = O.act(O.ACT_GELU, H)
+    assert rel_fro(f64(a_s[:nnz]), Aact) < FRO_TOL
+    # plain SDD (identity, no pre)
+    s_plain = A.moe_sdd(cfg, xg, w1.to(d), 0, tg)
+    assert rel_fro(f64(s_plain[:nnz]), H) < FRO_TOL
+    # DSD: Y_g = A . W2
+    yg = A.moe_dsd(cfg, a_s, 0, w2.to(d), 0, tg)
+    Y = O.dsd(f64(a_s[:nnz]), S.to_f64(w2), topo)
+    assert rel_fro(f64(yg[:Tp]), Y) < FRO_TOL
+    # SDD^T with act': dH = (dY_g . W2^T) * gelu'(H)
+    dh = A.moe_sdd(cfg, dyg.to(d), w2.to(d), 1, tg, act=A.ACT_GELU, act_grad_src=h_s)
+    dA = O.sdd(S.to_f64(dyg[:Tp]), S.to_f64(w2), topo, trans_b=True)
+    dH = dA * O.act_grad(O.ACT_GELU, f64(h_s[:nnz]))
+    assert rel_fro(f64(dh[:nnz]), dH) < FRO_TOL
+    # DS^TD: dW2 = A^T . dY_g
+    dw2 = A.moe_dsd(cfg, a_s, 1, dyg.to(d), 0, tg)
+    want = O.dsd(f64(a_s[:nnz]), S.to_f64(dyg[:Tp]), topo, trans_s=True)
+    assert rel_fro(f64(dw2), want) < FRO_TOL
+    # DSD^T: dX_g = dH . W1^T
+    dxg = A.moe_dsd(cfg, dh, 0, w1.to(d), 1, tg)
+    want = O.dsd(f64(dh[:nnz]), S.to_f64(w1), topo, trans_b=True)
+    assert rel_fro(f64(dxg[:Tp]), want) < FRO_TOL
+    # DD^TS: dW1 = X_g^T . dH
+    dw1 = A.moe_dds(cfg, xg, 1, dh, 0, tg)
+    want = O.dds(xg64, f64(dh[:nnz]), topo, trans_a=True)
+    assert rel_fro(f64(dw1), want) < FRO_TOL
+    # remaining transpose combinations of the API
+    rows = A.moe_max_padded_rows(cfg)
+    w2t = w2.t().contiguous()
+    yg2 = A.moe_dsd(cfg, a_s, 0, w2t.to(d), 1, tg)                  # DSD with b given transposed
+    assert rel_fro(f64(yg2[:Tp]), Y) < FRO_TOL
+    dygt = torch.zeros(h, rows, dtype=torch.bfloat16)
+    dygt[:, :Tp] = dyg[:Tp].t()
+    dw2b = A.moe_dsd(cfg, a_s, 1, dygt.to(d), 1, tg)                # DS^TD with b^T
+    assert rel_fro(f64(dw2b), O.dsd(f64(a_s[:nnz]), S.to_f64(dyg[:Tp]), topo, trans_s=True)) < FRO_TOL
+    xgt = xg.t().contiguous()
+    dw1b = A.moe_dds(cfg, xgt, 0, dh, 0, tg)                        # DDS with a given as [h, rows]
+    assert rel_fro(f64(dw1b), O.dds(xg64, f64(dh[:nnz]), topo, trans_a=True)) < FRO_TOL
+    w1t = w1.t().contiguous()                                       # [E*f, h]
+    out_r = A.moe_dds(cfg, w1.to(d), 0, dh, 1, tg)                   # DDS^T: W1 . dH^T -> [h, rows]
+    want_r = O.dds(S.to_f64(w1), f64(dh[:nnz]), topo, trans_s=True)
+    assert rel_fro(f64(out_r[:, :Tp]), want_r) < FRO_TOL
+    out_r2 = A.moe_dds(cfg, w1t.to(d), 1, dh, 1, tg)
+    assert rel_fro(f64(out_r2[:, :Tp]), want_r) < FRO_TOL
+    s_t = A.moe_sdd(cfg, xg, w1t.to(d), 1, tg)                       # SDD with b given as [E*f, h]
+    assert rel_fro(f64(s_t[:nnz]), H) < FRO_TOL
+
+
+def test_empty_expert_columns_are_zero():
+    """Experts with no tokens: their dW columns must be exactly zero."""
+    d = dev()
+    A = api()
+    T, h, f, E = 600, 256, 256, 8
+    idx = torch.tensor([[e % 3] for e in range(T)], dtype=torch.int32)   # experts 3..7 empty
+    cfg = A.make_config(T, h, E, 1, f, act=A.ACT_IDENTITY)
+    tg = A.moe_topology(cfg, idx.to(d))
+    rows = A.moe_max_padded_rows(cfg)
+    a_s = torch.randn(A.moe_max_nnz_blocks(cfg), 128, 128, device=d).to(torch.bfloat16)
+    dyg = torch.randn(rows, h, device=d).to(torch.bfloat16)
+    dw2 = A.moe_dsd(cfg, a_s, 1, dyg, 0, tg)
+    assert (dw2[3 * f:].float() == 0).all()
+    xg = torch.randn(rows, h, device=d).to(torch.bfloat16)
+    dw1 = A.moe_dds(cfg, xg, 1, a_s, 0, tg)
+    assert (dw1[:, 3 * f:].float() == 0).all()
+
+
+# ------------------------------------------------------------------ layer
+
+LAYER_CASES = [
+    ("C0", 1024, 1, S.CONFIGS["C0"]),
+    ("C0-ragged-k2", 1000, 2, S.CONFIGS["C0"].replace(top_k=2)),
+    ("C1-reduced", 4096, 1, S.CONFIGS["C1"]),
+    ("C2-reduced-skew", 4096, 1, S.CONFIGS["C2"]),
+    ("C4-reduced", 2048, 2, S.CONFIGS["C4"]),
+    ("C0-relu", 1024, 1, S.CONFIGS["C0"].replace(act=2)),
+    ("C0-identity", 1024, 1, S.CONFIGS["C0"].replace(act=0)),
+]
+
+
+def oracle_layer(inp, shp, T, logits=None):
+    x, wr, w1, w2, dy = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    y, cache = O.dmoe_forward(x, wr, w1, w2, shp.top_k, 128, shp.ffn, shp.act, logits=logits)
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    return y, cache, g
+
+
+@pytest.mark.parametrize("name,T,k,shp", LAYER_CASES)
+def test_layer_forward_backward(name, T, k, shp):
+    d = dev()
+    A = api()
+    inp = S.make_inputs(shp, seed=3, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    yo, cache, go = oracle_layer(inp, shp, T)
+    got_idx = saved.expert_idx.cpu().numpy()
+    flips = (got_idx != cache.expert_idx).any(axis=1)
+    assert flips.mean() < 1e-3, flips.sum()          # only fp32-vs-fp64 near-ties may differ
+    ok = ~flips
+    assert rel_fro(f64(y)[ok], yo[ok]) < FRO_TOL
+    assert rel_fro(f64(dx)[ok], go["dx"][ok]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+    assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
+    if not flips.any():
+        plan, topo = cache.plan, cache.topo
+        check_topology_exact(A, saved.topo, plan, O.make_topology_closed_form(plan, 128, shp.ffn), T * shp.top_k)
+
+
+def test_layer_deterministic():
+    d = dev()
+    A = api()
+    shp = S.CONFIGS["C1"]
+    T = 8192
+    inp = S.make_inputs(shp, seed=4, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    args = [inp[n].to(d) for n in ("wr", "w1", "w2")]
+    outs = []
+    for _ in range(2):
+        y, sv = A.moe_forward(cfg, *args, inp["x"].to(d))
+        dx, gr = A.moe_backward(cfg, *args, sv, inp["x"].to(d), inp["dy"].to(d))
+        outs.append([y, dx, *gr])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_c1_full_size_sampled():
+    """BASELINE config[1] (MoE-XS) at full size, in bench.py's launch
+    configuration: exact topology; sampled output rows / weight-gradient
+    columns computed one by one by the oracle."""
+    d = dev()
+    A = api()
+    shp = S.CONFIGS["C1"]
+    T = shp.tokens
+    inp = S.make_inputs(shp, seed=0)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    L = O.router_logits(x64, wr64)
+    idx_o, gates_o = O.topk(L, 1)
+    idx_g = saved.expert_idx.cpu().numpy()
+    assert (idx_g != idx_o).sum() <= 3
+    # topology: exact against the oracle run on the GPU's routing decisions is
+    # NOT used (no CUDA-derived oracle inputs); instead check the oracle plan of
+    # the oracle routing when routing agrees everywhere.
+    if (idx_g == idx_o).all():
+        plan = O.make_plan(idx_o, shp.experts, 128)
+        check_topology_exact(A, saved.topo, plan, O.make_topology_closed_form(plan, 128, shp.ffn), T)
+    f = shp.ffn
+    rng = np.random.default_rng(0)
+    rows = rng.choice(T, 48, replace=False)
+    yg = f64(y)
+    for t in rows:
+        e = idx_o[t, 0]
+        if idx_g[t, 0] != e:
+            continue
+        hpre = x64[t] @ w164[:, e * f:(e + 1) * f]
+        want = gates_o[t, 0] * (O.act(shp.act, hpre) @ w264[e * f:(e + 1) * f])
+        assert rel_fro(yg[t], want) < FRO_TOL
+    # sampled dW2 rows of expert 5: dW2[e*f + c, :] = sum over its tokens of A[t,c] * g_t dy[t]
+    e = 5
+    toks = np.nonzero(idx_o[:, 0] == e)[0]
+    Hx = x64[toks] @ w164[:, e * f:(e + 1) * f]
+    Ax = O.act(shp.act, Hx)
+    dY = gates_o[toks, 0:1] * dy64[toks]
+    cols = rng.choice(f, 8, replace=False)
+    got = f64(dw2[e * f + cols])
+    want = Ax[:, cols].T @ dY
+    assert rel_fro(got, want) < FRO_TOL
