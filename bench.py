@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""bench.py — dropless-MoE layer fwd+bwd throughput on B200 (BASELINE.json metric).
+
+One "step" = one full pass of the hot path over one batch: router, top-k,
+topology, padded gather, SDD(+gelu), DSD, weighted scatter, then the backward
+pass (scatter-bwd, SDD^T(+gelu'), DS^TD, DSD^T, DD^TS, gather-bwd, router-bwd)
+— SURVEY.md §8(a) rows a1..a7, b1..b7. N=1 workload: BASELINE configs[1]
+(MoE-XS: T=32768, h=512, f=2048, E=64, top_k=1, bf16, gelu). N>1: expert
+parallelism, T=32768 tokens per rank, E=64 experts split over ranks (weak
+scaling), NCCL all-to-all dispatch/combine.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+METRIC = "dropless MoE layer fwd+bwd tokens/s"
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        p["source"] = "measured"
+        return p
+    except Exception:
+        return dict(FALLBACK)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- work model
+def work_model(T, h, f, E, k, Tp):
+    """Algorithmic FLOPs / bytes per unit."""
+    R = T * k
+    prod_flop = 2 * R * h * f                       # useful, per product
+    prod_bytes = 2 * (R * h + R * f + E * h * f)    # minimal bytes, per product
+    return {
+        "useful_flop_step": 6 * prod_flop + 2 * T * h * E + 4 * T * h * E,
+        "executed_flop_step": 6 * 2 * Tp * h * f,
+        "prod_flop": prod_flop,
+        "prod_bytes": prod_bytes,
+        "sddt_bytes": prod_bytes + 2 * R * f,
+        "gather_bytes": 2 * (T * h + R * h) + 4 * R,
+        "scatter_bytes": 2 * (R * h + T * h) + 8 * R,
+        "scatter_bwd_bytes": 2 * (T * h + 2 * R * h) + 4 * R,
+        "gather_bwd_bytes": 2 * (R * h + T * h),
+    }
+
+
+# ----------------------------------------------------------------------------- our arm, 1 GPU
+class Step:
+    """The layer step as the exact C-ABI call sequence of moe_forward +
+    moe_backward (layer.cu), prebuilt ctypes arguments, CUDA events between
+    calls so every kernel's time is measured live on the launching stream."""
+
+    def __init__(self, A, cfg, tensors, stream):
+        from paper_2211_15841_b200._lib import lib
+        self.lib = lib
+        self.A = A
+        self.cfg = cfg
+        t = tensors
+        P = ctypes.c_void_p
+        c = ctypes.byref(cfg)
+        sv = t["saved"]
+        topo = ctypes.byref(sv.topo.struct)
+        s = P(stream.cuda_stream)
+        ws = P(t["ws"].data_ptr())
+        d = lambda x: P(x.data_ptr()) if x is not None else None  # noqa: E731
+        idn = cfg.act == 0
+        L = lib
+        wsl = t["ws_layout"]
+        self.calls = [
+            ("router", L.moe_router, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), d(sv.gates), ws, s)),
+            ("topology", L.moe_topology, (c, d(sv.expert_idx), topo, ws, s)),
+            ("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
+            ("sdd", L.moe_sdd, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
+                                None if idn else d(sv.h_pre), s)),
+            ("dsd", L.moe_dsd, (c, d(sv.a), 0, d(t["w2"]), 0, topo, d(sv.y_g), s)),
+            ("scatter", L.moe_scatter, (c, d(sv.y_g), topo, d(sv.gates), d(t["y"]), s)),
+            ("scatter_bwd", L.moe_scatter_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"], wsl["dgates"],
+                                                s)),
+            ("sddT", L.moe_sdd, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act, None if idn else d(sv.h_pre),
+                                 wsl["dh"], None, s)),
+            ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
+            ("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
+            ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
+            ("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
+            ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), wsl["dgates"],
+                                              d(t["dwr"]), d(t["dx"]), ws, s)),
+        ]
+        self.names = [n for n, _, _ in self.calls]
+
+    def run(self, events=None):
+        for i, (name, fn, args) in enumerate(self.calls):
+            if events is not None:
+                events[i].record()
+            st = fn(*args)
+            if st != 0:
+                raise RuntimeError(f"{name}: {self.lib.moe_last_error().decode()}")
+        if events is not None:
+            events[len(self.calls)].record()
+
+
+def ws_views(A, cfg, ws):
+    """Pointers inside the workspace exactly as moe_backward lays them out
+    (status.cu ws_layout): dY_g, dH, dX_g, dgates."""
+    h, bs = cfg.hidden, cfg.block_size
+    rows = A.moe_max_padded_rows(cfg)
+    nnz = A.moe_max_nnz_blocks(cfg)
+    R = cfg.tokens * cfg.top_k
+    E = cfg.num_experts
+    n_chunks = -(-R // 1024)
+    al = lambda v: (v + 255) & ~255  # noqa: E731
+    off = al(4 * n_chunks * E)
+    dy_g = off
+    off = al(off + 2 * rows * h)
+    dh = off
+    off = al(off + 2 * nnz * bs * bs)
+    dx_g = off
+    off = al(off + 2 * rows * h)
+    dgates = off
+    base = ws.data_ptr()
+    P = ctypes.c_void_p
+    return {"dy_g": P(base + dy_g), "dh": P(base + dh), "dx_g": P(base + dx_g), "dgates": P(base + dgates)}
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def run_ours_single(args, peaks):
+    from paper_2211_15841_b200 import api as A
+    from synth import inputs as S
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    shp = S.CONFIGS[args.config]
+    T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
+    inp = S.make_inputs(shp, seed=0)
+    cfg = A.make_config(T, h, E, k, f, act=shp.act)
+    stream = torch.cuda.current_stream()
+    x = inp["x"].to(dev)
+    dy = inp["dy"].to(dev)
+    wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
+    saved = A.Saved.allocate(cfg, dev)
+    ws = A.workspace(cfg, dev)
+    t = {"x": x, "dy": dy, "wr": wr, "w1": w1, "w2": w2, "saved": saved, "ws": ws,
+         "y": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
+         "dx": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
+         "dwr": torch.empty(h, E, dtype=torch.float32, device=dev),
+         "dw1": torch.empty(h, E * f, dtype=torch.bfloat16, device=dev),
+         "dw2": torch.empty(E * f, h, dtype=torch.bfloat16, device=dev)}
+    t["ws_layout"] = ws_views(A, cfg, ws)
+    step = Step(A, cfg, t, stream)
+    l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        flush_l2(l2)
+        step.run()
+    torch.cuda.synchronize()
+    n = len(step.calls)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n + 1)] for _ in range(args.steps)]
+    launches0 = A.lib.moe_total_launch_count()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush_l2(l2)                      # between timed steps, outside the events
+        step.run(evs[i])
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = A.lib.moe_total_launch_count() - launches0
+    per_call = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(n)] for i in range(args.steps)])
+    step_ms = per_call.sum(axis=1)
+    total_ms = float(step_ms.sum())
+    Tp, nnz = saved.topo.sizes()
+    counts = saved.topo["counts"].cpu().numpy()
+    value = T * args.steps / (total_ms / 1e3)
+
+    # ---- roofline for the dominant kernel (largest share of the step)
+    wm = work_model(T, h, f, E, k, Tp)
+    mean_call = per_call.mean(axis=0)
+    shares = mean_call / mean_call.sum()
+    dom = int(np.argmax(mean_call))
+    dname = step.names[dom]
+    prod_names = {"sdd": "prod_bytes", "dsd": "prod_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
+                  "dsdT": "prod_bytes", "ddTs": "prod_bytes"}
+    byte_names = {"gather": "gather_bytes", "scatter": "scatter_bytes", "scatter_bwd": "scatter_bwd_bytes",
+                  "gather_bwd": "gather_bwd_bytes"}
+    dur_s = mean_call[dom] / 1e3
+    roof = {"kernel": dname, "launch_ms": round(float(mean_call[dom]), 4), "share_of_step": round(float(shares[dom]), 4)}
+    if dname in prod_names:
+        bytes_ = wm[prod_names[dname]]
+        flop = wm["prod_flop"]
+        t_mem, t_flop = bytes_ / (peaks["hbm_gbs"] * 1e9), flop / (peaks["bf16_tflops"] * 1e12)
+        if t_mem >= t_flop:
+            roof.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s")
+        else:
+            roof.update(bound="tensor", achieved=round(flop / dur_s / 1e12, 1), peak=peaks["bf16_tflops"],
+                        unit="TFLOP/s")
+        roof["tflops_useful"] = round(flop / dur_s / 1e12, 1)
+        roof["tflops_frac_of_bf16_peak"] = round(flop / dur_s / 1e12 / peaks["bf16_tflops"], 4)
+    elif dname in byte_names:
+        bytes_ = wm[byte_names[dname]]
+        roof.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s")
+    else:
+        roof.update(bound="hbm", achieved=None, peak=peaks["hbm_gbs"], unit="GB/s")
+    if roof.get("achieved") is not None:
+        roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["peak_source"] = peaks.get("source", "measured") + " (burst)"
+    roof["traffic"] = load_traffic(dname)
+    breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4)}
+                 for nm, m, s_ in zip(step.names, mean_call, shares)}
+    gemm_ms = sum(mean_call[step.names.index(p)] for p in prod_names)
+    gemm = {"ms": round(float(gemm_ms), 4),
+            "useful_tflops": round(6 * wm["prod_flop"] / (gemm_ms / 1e3) / 1e12, 1),
+            "executed_tflops": round(wm["executed_flop_step"] / (gemm_ms / 1e3) / 1e12, 1)}
+    gemm["frac_of_bf16_peak"] = round(gemm["useful_tflops"] / peaks["bf16_tflops"], 4)
+
+    e2e = run_e2e(A, cfg, t, args, dev) if not args.no_e2e else None
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) inputs, "
+        "random-init weights of the MoE-XS shape)",
+        "config": {"workload": shp.name, "tokens": T, "hidden": h, "ffn_hidden": f, "num_experts": E, "top_k": k,
+                   "block_size": 128, "act": "gelu_tanh", "routing": shp.routing, "parallelism": "ep1",
+                   "padded_rows": Tp, "nnz_blocks": nnz,
+                   "expert_load_max_over_mean": round(float(counts.max() / counts.mean()), 3),
+                   "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
+        "roofline": roof,
+        "gemm": gemm,
+        "breakdown_ms": breakdown,
+        "clocks": clk,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(shp)
+    return out
+
+
+def load_traffic(kernel_name):
+    """dram bytes per launch for the dominant kernel from the committed ncu
+    capture summary (profiles/traffic.json), else null."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel_name)
+    except Exception:
+        return None
+
+
+def run_e2e(A, cfg, t, args, dev):
+    """Same metric through the public API (moe_forward + moe_backward) with
+    pinned HOST inputs copied in and results (y, dx) copied out every step."""
+    T, h = cfg.tokens, cfg.hidden
+    hx = t["x"].cpu().pin_memory()
+    hdy = t["dy"].cpu().pin_memory()
+    hy = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+    hdx = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+    xd, dyd = torch.empty_like(t["x"]), torch.empty_like(t["dy"])
+    saved, ws = t["saved"], t["ws"]
+    grads = (t["dwr"], t["dw1"], t["dw2"])
+
+    def one():
+        xd.copy_(hx, non_blocking=True)
+        dyd.copy_(hdy, non_blocking=True)
+        y, _ = A.moe_forward(cfg, t["wr"], t["w1"], t["w2"], xd, y=t["y"], saved=saved, ws=ws)
+        dx, _ = A.moe_backward(cfg, t["wr"], t["w1"], t["w2"], saved, xd, dyd, dx=t["dx"], grads=grads, ws=ws)
+        hy.copy_(y, non_blocking=True)
+        hdx.copy_(dx, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        one()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(args.steps):
+        one()
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en)
+    return {"value": round(T * args.steps / (ms / 1e3), 1), "unit": "tokens/s",
+            "h2d_bytes_per_step": 2 * T * h * 2, "d2h_bytes_per_step": 2 * T * h * 2,
+            "ms_per_step": round(ms / args.steps, 4), "api": "moe_forward+moe_backward (C ABI)"}
+
+
+# ----------------------------------------------------------------------------- oracle timings
+def oracle_step(inp, shp, T_sample):
+    from oracle import moe_oracle as O
+    from synth import inputs as S
+    x, wr, w1, w2, dy = (S.to_f64(inp[n][:T_sample]) if n in ("x", "dy") else S.to_f64(inp[n])
+                         for n in ("x", "wr", "w1", "w2", "dy"))
+    y, cache = O.dmoe_forward(x, wr, w1, w2, shp.top_k, 128, shp.ffn, shp.act)
+    O.dmoe_backward(cache, dy, wr, w1, w2)
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+        if n:
+            return int(n[0])
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_baseline(shp, T_sample=16384):
+    from synth import inputs as S
+    inp = S.make_inputs(shp, seed=0, tokens=T_sample)
+    t0 = time.perf_counter()
+    oracle_step(inp, shp, T_sample)
+    dt = time.perf_counter() - t0
+    return {"value": round(T_sample / dt, 1), "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"first {T_sample} tokens of the {shp.name} workload, one fwd+bwd of oracle/moe_oracle.py "
+                      f"(numpy fp64, OpenBLAS matmul per block) in {dt:.2f} s"}
+
+
+def run_reference(args):
+    from synth import inputs as S
+    shp = S.CONFIGS[args.config]
+    T_sample = args.ref_tokens
+    inp = S.make_inputs(shp, seed=0, tokens=T_sample)
+    for _ in range(args.warmup):
+        oracle_step(inp, shp, T_sample)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(inp, shp, T_sample)
+    dt = time.perf_counter() - t0
+    value = T_sample * args.steps / dt
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": shp.name, "tokens_per_step_sample": T_sample,
+                                           "hidden": shp.hidden, "ffn_hidden": shp.ffn,
+                                           "num_experts": shp.experts, "top_k": shp.top_k},
+            "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": f"{T_sample} tokens of {shp.name} per step (full h, f, E)"},
+            "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-tokens", type=int, default=2048)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    peaks = load_peaks()
+    if world > 1:
+        from paper_2211_15841_b200 import ep
+        out = ep.bench_ep(args, peaks)
+        if rank == 0 and out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    out = run_ours_single(args, peaks)
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -243,6 +243,9 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
  * thread enqueued (for the bench's gpu_launches count). */
 int moe_last_launch_count(void);
 
+/* Kernel launches enqueued by this library since it was loaded (all threads). */
+int64_t moe_total_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

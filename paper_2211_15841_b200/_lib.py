@@ -75,6 +75,7 @@ SIGNATURES = {
     "moe_backward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), ctypes.POINTER(MoeSaved), P, P, P,
                               ctypes.POINTER(MoeGrads), P, P]),
     "moe_last_launch_count": (ctypes.c_int, []),
+    "moe_total_launch_count": (ctypes.c_int64, []),
 }
 
 STATUS_NAMES = {0: "MOE_OK", 1: "MOE_EINVAL", 2: "MOE_ESHAPE", 3: "MOE_EUNSUPPORTED", 4: "MOE_ECUDA",

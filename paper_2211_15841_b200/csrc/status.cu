@@ -2,12 +2,15 @@
 // (include/moe.h). Host only; no CUDA calls except the SM-count query.
 #include <string.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace moe {
 
 static thread_local char g_err[512] = "";
 static thread_local int g_launches = 0;
+static std::atomic<long long> g_total_launches{0};
 
 moe_status set_error(moe_status st, const char* fmt, ...) {
   va_list ap;
@@ -17,7 +20,10 @@ moe_status set_error(moe_status st, const char* fmt, ...) {
   return st;
 }
 void clear_error() { g_err[0] = 0; }
-void count_launch(int n) { g_launches += n; }
+void count_launch(int n) {
+  g_launches += n;
+  g_total_launches += n;
+}
 void reset_launch_count() { g_launches = 0; }
 
 moe_status check_config_gpu(const moe_config* cfg) {
@@ -81,6 +87,8 @@ extern "C" {
 const char* moe_last_error(void) { return g_err; }
 
 int moe_last_launch_count(void) { return g_launches; }
+
+int64_t moe_total_launch_count(void) { return g_total_launches.load(); }
 
 moe_status moe_check_config(const moe_config* cfg) {
   if (!cfg) return set_error(MOE_EINVAL, "config pointer is NULL");

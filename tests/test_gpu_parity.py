@@ -125,8 +125,13 @@ def test_topology_deterministic_repeat():
     cfg = A.make_config(30000, 128, 64, 2, 512)
     t1 = A.moe_topology(cfg, idx)
     t2 = A.moe_topology(cfg, idx)
+    Tp, nnz = t1.sizes()
+    assert (Tp, nnz) == t2.sizes()
+    valid = {"row_offsets": Tp // 128 + 1, "col_indices": nnz, "row_indices": nnz, "t_block_offsets": nnz,
+             "t_row_indices": nnz}   # contents beyond the device-side sizes are unspecified (moe.h)
     for name in t1.t:
-        assert torch.equal(t1[name], t2[name]), name
+        n = valid.get(name, t1[name].numel())
+        assert torch.equal(t1[name][:n], t2[name][:n]), name
 
 
 # ------------------------------------------------------------------ permutation
