@@ -1,4 +1,5 @@
-// bsgemm.cu — block-sparse SDD / DSD / DDS on sm_100a tensor cores.
+// bsgemm.cu — block-sparse SDD / DSD / DDS (and the router's dense GEMMs) on
+// sm_100a tensor cores.
 //
 // The paper's products (§5.1; Triton notation P:177) over the
 // hybrid blocked-CSR-COO topology with transpose indices
@@ -6,25 +7,32 @@
 // them; the modes differ only in how a 128 x BN output tile enumerates its
 // K-steps and where TMA fetches the two operand tiles from:
 //
-//   SDD     out block s=(r,c)          K = dense dim, COO (row_indices, col_indices) lookup
-//   DSD_ROW out [r-block, n-tile]      K walks the BCSR row r (row_offsets, col_indices)
-//   DS_COL  out [c-block, n-tile]      K walks column c through the transpose index
-//   DDS_COL out [m-tile, c-block]      K walks column c through the transpose index
-//   DDS_ROW out [m-tile, r-block]      K walks the BCSR row r
+//   SDD     out blocks (r,c..c+BN/128)   K = dense dim; COO (row_indices, col_indices) lookup
+//   DSD_ROW out [r-block, n-tile]         K walks the BCSR row r (row_offsets, col_indices)
+//   DS_COL  out [c-block, n-tile]         K walks column c through the transpose index
+//   DDS_COL out [m-tile, c..c+BN/128]     K walks column c through the transpose index
+//   DDS_ROW out [m-tile, r-block]         K walks the BCSR row r
+//   DENSE   out [m-tile, n-tile] (+split-K)  router logits, dWr, dx (router term)
 //
 // Transposition never moves values: a transposed sparse or dense operand is
 // fed to tcgen05.mma as an MN-major instead of K-major shared-memory tile
 // (descriptor bit), loaded by TMA from the same row-major storage.
+// BN = 256 tiles pair two adjacent block-columns of the same expert (F even):
+// they share their row set, so one walk of the transpose index serves both.
 //
 // Warp roles (192 threads, 1 CTA/SM): warp 0 = TMA producer, warp 1 = TMEM
-// allocator + single-thread MMA issuer, warps 2-5 = epilogue (TMEM -> regs ->
-// global). Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a
-// double-buffered TMEM accumulator (tfull/tempty) so the epilogue of tile i
-// overlaps the main loop of tile i+1.
+// allocator + single-thread MMA issuer, warps 2-5 = epilogue. Pipelines:
+// STAGES-deep smem ring (full/empty mbarriers), double-buffered TMEM
+// accumulator (tfull/tempty) so the epilogue of tile i overlaps the main loop
+// of tile i+1. The epilogue stages bf16 results in 128B-swizzled shared memory
+// and writes them with TMA bulk stores (coalesced, asynchronous); the SDD^T
+// epilogue prefetches the saved pre-activation H by TMA.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <float.h>
 
+#include "bsgemm.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"
@@ -33,79 +41,78 @@ namespace moe {
 
 using namespace sm100;
 
-enum GemmMode { SDD = 0, DSD_ROW = 1, DS_COL = 2, DDS_COL = 3, DDS_ROW = 4 };
-enum EpiKind { EPI_STORE = 0, EPI_ACT_FWD = 1, EPI_ACT_BWD = 2 };
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NUM_THREADS = 192;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int EPI_BUF = 32 * 128;                 // one warp's 32 rows x 64 bf16 (128 B)
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;        // 4 warps x double buffer
+constexpr int SMEM_LIMIT = 232448;                // 227 KB opt-in
+constexpr int SMEM_FIXED = 1024 + 512;            // alignment slack + barriers
+constexpr int kMaxRouterTopK = 8;
 
-struct GemmParams {
-  const int32_t* sizes;  // {Tp, nnz}
-  const int32_t* row_offsets;
-  const int32_t* col_indices;
-  const int32_t* row_indices;
-  const int32_t* t_col_offsets;
-  const int32_t* t_block_offsets;
-  const int32_t* t_row_indices;
-  int n_block_cols;  // E*F
-  int dense_tiles;   // 128-wide tiles along the dense output dimension
-  int k_dense;       // SDD: contraction length (multiple of 64)
-  __nv_bfloat16* out;
-  __nv_bfloat16* out_pre;
-  const __nv_bfloat16* act_src;
-  long long ld_out;
-  int epi;
-  int act;
+template <int BN, bool EPI_H>
+struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES) / STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI_BYTES + H_BYTES;
+  static_assert(STAGES >= 2, "not enough shared memory for two stages");
+  static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
 
-constexpr int BM = 128;
-constexpr int BN = 128;
-constexpr int BK = 64;
-constexpr int STAGES = 6;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_TX = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 2 * BN;
-constexpr int NUM_THREADS = 192;
-constexpr size_t SMEM_BYTES = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 256;
-
-__device__ __forceinline__ int num_tiles(const GemmParams& p, int mode) {
-  const int Tp = p.sizes[0], nnz = p.sizes[1];
+__device__ __forceinline__ int num_tiles(const GemmParams& p, int mode, int pair) {
+  const int Tp = p.sizes ? p.sizes[0] : 0, nnz = p.sizes ? p.sizes[1] : 0;
   switch (mode) {
-    case SDD: return nnz;
+    case SDD: return nnz / pair;
     case DSD_ROW: return (Tp / BM) * p.dense_tiles;
     case DS_COL: return p.n_block_cols * p.dense_tiles;
-    case DDS_COL: return p.n_block_cols * p.dense_tiles;
-    default: return (Tp / BM) * p.dense_tiles;  // DDS_ROW
+    case DDS_COL: return (p.n_block_cols / pair) * p.dense_tiles;
+    case DDS_ROW: return (Tp / BM) * p.dense_tiles;
+    default: return p.splits * p.m_tiles * p.n_tiles;  // DENSE
   }
 }
 
-// Per-tile decode: number of 64-wide K steps, the sparse walk start, and the
-// output-tile coordinates (major index `u` = block row/col, minor `v` = dense tile).
 struct TileInfo {
   int kiters;
-  int walk_begin;  // first storage index (row walk) or transpose position (col walk)
-  int u, v;        // SDD: (r, c); DSD_ROW/DDS_ROW: (r, dense tile); DS_COL/DDS_COL: (c, dense tile)
-  int s;           // SDD: block storage index
+  int walk_begin;  // first storage index (row walk) or transpose position (column walk)
+  int u, v;        // SDD: (block row, block col); DSD_ROW/DDS_ROW: (r, dense tile);
+                   // DS_COL/DDS_COL: (block col, dense tile); DENSE: (m tile, n tile)
+  int s;           // SDD: first block storage index; DENSE: split
 };
 
-__device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int tile) {
+__device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pair, int tile) {
   TileInfo t;
-  t.s = tile;
+  t.s = 0;
+  t.walk_begin = 0;
   if (mode == SDD) {
-    t.u = __ldg(p.row_indices + tile);
-    t.v = __ldg(p.col_indices + tile);
+    t.s = tile * pair;
+    t.u = __ldg(p.row_indices + t.s);
+    t.v = __ldg(p.col_indices + t.s);
     t.kiters = p.k_dense / BK;
-    t.walk_begin = 0;
   } else if (mode == DSD_ROW || mode == DDS_ROW) {
     t.u = tile / p.dense_tiles;
     t.v = tile % p.dense_tiles;
     const int b = __ldg(p.row_offsets + t.u), e = __ldg(p.row_offsets + t.u + 1);
     t.walk_begin = b;
     t.kiters = 2 * (e - b);
-  } else {
-    t.u = tile / p.dense_tiles;
+  } else if (mode == DS_COL || mode == DDS_COL) {
+    t.u = (tile / p.dense_tiles) * (mode == DDS_COL ? pair : 1);
     t.v = tile % p.dense_tiles;
     const int b = __ldg(p.t_col_offsets + t.u), e = __ldg(p.t_col_offsets + t.u + 1);
     t.walk_begin = b;
     t.kiters = 2 * (e - b);
+  } else {  // DENSE: tile = (split * m_tiles + m) * n_tiles + n
+    t.v = tile % p.n_tiles;
+    const int rest = tile / p.n_tiles;
+    t.u = rest % p.m_tiles;
+    t.s = rest / p.m_tiles;
+    const int k0 = t.s * p.kiters_split;
+    const int left = p.k_iters_total - k0;
+    t.kiters = left < p.kiters_split ? (left > 0 ? left : 0) : p.kiters_split;
   }
   return t;
 }
@@ -129,30 +136,69 @@ __device__ __forceinline__ float act_grad(int kind, float x) {
   return 1.f;
 }
 
-// Output tile origin (element offset) and leading dimension.
-__device__ __forceinline__ long long out_origin(const GemmParams& p, int mode, const TileInfo& t) {
+// TMA coordinates (inner column, outer row) of the 64-column chunk `c` of the
+// output tile, for the epilogue warp whose rows start at `row0` in the tile.
+__device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const TileInfo& t, int c, int row0,
+                                           int BN, int& x, int& y) {
+  const int col = c * 64;
   switch (mode) {
-    case SDD: return (long long)t.s * (BM * BN);
-    case DSD_ROW: return (long long)t.u * BM * p.ld_out + (long long)t.v * BN;
-    case DS_COL: return (long long)t.u * BM * p.ld_out + (long long)t.v * BN;
-    case DDS_COL: return (long long)t.v * BM * p.ld_out + (long long)t.u * BN;
-    default: return (long long)t.v * BM * p.ld_out + (long long)t.u * BN;  // DDS_ROW
+    case SDD: {  // values as [nnz*128, 128]
+      const int blk = t.s + col / 128;
+      x = col % 128;
+      y = blk * BM + row0;
+      break;
+    }
+    case DSD_ROW: x = t.v * BN + col; y = t.u * BM + row0; break;
+    case DS_COL: x = t.v * BN + col; y = t.u * BM + row0; break;
+    case DDS_COL: x = t.u * 128 + col; y = t.v * BM + row0; break;
+    case DDS_ROW: x = t.u * 128 + col; y = t.v * BM + row0; break;
+    default: x = t.v * BN + col; y = t.u * BM + row0; break;  // DENSE
   }
 }
 
-template <int MODE, bool A_MN, bool B_MN>
+__device__ __forceinline__ void unpack8(const uint4& w, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+
+// Write 64 fp32 values of this thread's row as bf16 into a 128B-swizzled
+// [32 rows][128 B] staging buffer (row = lane).
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
+  uint8_t* row = buf + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 w = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) = w;
+  }
+}
+
+template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     bsgemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                  const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
                   const GemmParams p) {
+  using C = Cfg<BN, EPI_H>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int PAIR = (MODE == SDD || MODE == DDS_COL) ? BN / 128 : 1;
+  constexpr int NCHUNK = BN / 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_b + STAGES * B_BYTES);
+  uint8_t* smem_b = smem_a + STAGES * A_BYTES;
+  uint8_t* smem_epi = smem_b + STAGES * C::B_BYTES;
+  uint8_t* smem_h = smem_epi + EPI_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* hbar = tempty + 2;  // [4 warps][2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 8);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -166,36 +212,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_holder);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int ntiles = num_tiles(p, MODE);
+  const int ntiles = num_tiles(p, MODE, PAIR);
 
   if (warp == 0) {
     // ===================== TMA producer (whole warp walks, lane 0 issues) =====================
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const TileInfo t = decode(p, MODE, tile);
+      const TileInfo t = decode(p, MODE, PAIR, tile);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit >> 1, kk = kit & 1;
-        if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
+        if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0) {
           const int q = t.walk_begin + blk + lane;
-          const int lim = t.walk_begin + (t.kiters >> 1);
-          if (q < lim) {
+          if (q < t.walk_begin + (t.kiters >> 1)) {
             if (MODE == DSD_ROW || MODE == DDS_ROW) {
-              idx_a = q;                            // storage index
-              idx_b = __ldg(p.col_indices + q);     // block column
+              idx_a = q;
+              idx_b = __ldg(p.col_indices + q);
             } else {
-              idx_a = __ldg(p.t_block_offsets + q); // storage index
-              idx_b = __ldg(p.t_row_indices + q);   // block row
+              idx_a = __ldg(p.t_block_offsets + q);
+              idx_b = __ldg(p.t_row_indices + q);
             }
           }
         }
@@ -204,55 +250,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           uint8_t* sa = smem_a + stage * A_BYTES;
-          uint8_t* sb = smem_b + stage * B_BYTES;
-          mbar_arrive_expect_tx(&full[stage], STAGE_TX);
+          uint8_t* sb = smem_b + stage * C::B_BYTES;
+          uint64_t* fb = &full[stage];
+          mbar_arrive_expect_tx(fb, C::STAGE);
           if (MODE == SDD) {
             const int k0 = kit * BK;
-            // A: dense [rows, K] K-major tile at (k0, r*128)
-            tma_load_2d(sa, &tmap_a, &full[stage], k0, t.u * BM);
-            if (B_MN) {  // b [K, N] row-major: two 64-wide N chunks
-              tma_load_2d(sb, &tmap_b, &full[stage], t.v * BN, k0);
-              tma_load_2d(sb + 8192, &tmap_b, &full[stage], t.v * BN + 64, k0);
-            } else {     // b [N, K] row-major
-              tma_load_2d(sb, &tmap_b, &full[stage], k0, t.v * BN);
+            tma_load_2d(sa, &tmap_a, fb, k0, t.u * BM);
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * 128 + j * 64, k0);
+            } else {
+              tma_load_2d(sb, &tmap_b, fb, k0, t.v * 128);
             }
           } else if (MODE == DSD_ROW) {
-            // A = S_s (K-major); B rows of block column c
-            tma_load_2d(sa, &tmap_a, &full[stage], kk * BK, sblk * BM);
+            tma_load_2d(sa, &tmap_a, fb, kk * BK, sblk * BM);
             if (B_MN) {
-              tma_load_2d(sb, &tmap_b, &full[stage], t.v * BN, oblk * BM + kk * BK);
-              tma_load_2d(sb + 8192, &tmap_b, &full[stage], t.v * BN + 64, oblk * BM + kk * BK);
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
             } else {
-              tma_load_2d(sb, &tmap_b, &full[stage], oblk * BM + kk * BK, t.v * BN);
+              tma_load_2d(sb, &tmap_b, fb, oblk * BM + kk * BK, t.v * BN);
             }
           } else if (MODE == DS_COL) {
-            // A = S_blk^T (MN-major view of the row-major block); B = dense rows of block row r
-            tma_load_2d(sa, &tmap_a, &full[stage], 0, sblk * BM + kk * BK);
-            tma_load_2d(sa + 8192, &tmap_a, &full[stage], 64, sblk * BM + kk * BK);
+            tma_load_2d(sa, &tmap_a, fb, 0, sblk * BM + kk * BK);
+            tma_load_2d(sa + 8192, &tmap_a, fb, 64, sblk * BM + kk * BK);
             if (B_MN) {
-              tma_load_2d(sb, &tmap_b, &full[stage], t.v * BN, oblk * BM + kk * BK);
-              tma_load_2d(sb + 8192, &tmap_b, &full[stage], t.v * BN + 64, oblk * BM + kk * BK);
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
             } else {
-              tma_load_2d(sb, &tmap_b, &full[stage], oblk * BM + kk * BK, t.v * BN);
+              tma_load_2d(sb, &tmap_b, fb, oblk * BM + kk * BK, t.v * BN);
             }
           } else if (MODE == DDS_COL) {
-            // A = dense [m-tile, r-block]; B = S_blk (MN-major: N = block column contiguous)
             if (A_MN) {
-              tma_load_2d(sa, &tmap_a, &full[stage], t.v * BM, oblk * BM + kk * BK);
-              tma_load_2d(sa + 8192, &tmap_a, &full[stage], t.v * BM + 64, oblk * BM + kk * BK);
+              tma_load_2d(sa, &tmap_a, fb, t.v * BM, oblk * BM + kk * BK);
+              tma_load_2d(sa + 8192, &tmap_a, fb, t.v * BM + 64, oblk * BM + kk * BK);
             } else {
-              tma_load_2d(sa, &tmap_a, &full[stage], oblk * BM + kk * BK, t.v * BM);
+              tma_load_2d(sa, &tmap_a, fb, oblk * BM + kk * BK, t.v * BM);
             }
-            tma_load_2d(sb, &tmap_b, &full[stage], 0, sblk * BM + kk * BK);
-            tma_load_2d(sb + 8192, &tmap_b, &full[stage], 64, sblk * BM + kk * BK);
-          } else {  // DDS_ROW: A = dense [m-tile, c-block]; B = S_s^T (K-major view)
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)  // blocks (r, c + j/2): storage sblk + j/2
+              tma_load_2d(sb + j * 8192, &tmap_b, fb, (j & 1) * 64, (sblk + (j >> 1)) * BM + kk * BK);
+          } else if (MODE == DDS_ROW) {
             if (A_MN) {
-              tma_load_2d(sa, &tmap_a, &full[stage], t.v * BM, oblk * BM + kk * BK);
-              tma_load_2d(sa + 8192, &tmap_a, &full[stage], t.v * BM + 64, oblk * BM + kk * BK);
+              tma_load_2d(sa, &tmap_a, fb, t.v * BM, oblk * BM + kk * BK);
+              tma_load_2d(sa + 8192, &tmap_a, fb, t.v * BM + 64, oblk * BM + kk * BK);
             } else {
-              tma_load_2d(sa, &tmap_a, &full[stage], oblk * BM + kk * BK, t.v * BM);
+              tma_load_2d(sa, &tmap_a, fb, oblk * BM + kk * BK, t.v * BM);
             }
-            tma_load_2d(sb, &tmap_b, &full[stage], kk * BK, sblk * BM);
+            tma_load_2d(sb, &tmap_b, fb, kk * BK, sblk * BM);
+          } else {  // DENSE
+            const int k0 = (t.s * p.kiters_split + kit) * BK;
+            if (A_MN) {
+              tma_load_2d(sa, &tmap_a, fb, t.u * BM, k0);
+              tma_load_2d(sa + 8192, &tmap_a, fb, t.u * BM + 64, k0);
+            } else {
+              tma_load_2d(sa, &tmap_a, fb, k0, t.u * BM);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, k0);
+            } else {
+              tma_load_2d(sb, &tmap_b, fb, k0, t.v * BN);
+            }
           }
         }
         __syncwarp();
@@ -271,7 +331,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const TileInfo t = decode(p, MODE, tile);
+        const TileInfo t = decode(p, MODE, PAIR, tile);
         if (t.kiters == 0) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -280,7 +340,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(smem_a + stage * A_BYTES);
-          const uint32_t b_base = smem_u32(smem_b + stage * B_BYTES);
+          const uint32_t b_base = smem_u32(smem_b + stage * C::B_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t adesc =
@@ -302,97 +362,277 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ===================== epilogue (warps 2..5) =====================
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;   // output row within the tile
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const int wq = warp - 2;  // staging-buffer owner index
+    const int row0 = q * 32;  // first tile row of this warp
+    uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
+    uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
+    uint64_t* hb = hbar + wq * 2;
+    uint32_t hphase[2] = {0, 0};
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const TileInfo t = decode(p, MODE, tile);
-      __nv_bfloat16* out_row = p.out + out_origin(p, MODE, t) + (long long)row * (MODE == SDD ? BN : p.ld_out);
-      if (t.kiters == 0) {  // empty block column (expert without tokens): zero output
-        uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int c = 0; c < BN; c += 8) *reinterpret_cast<uint4*>(out_row + c) = z;
-        continue;
+    const bool bf16_out = p.epi == EPI_STORE || p.epi == EPI_ACT_FWD || p.epi == EPI_ACT_BWD || p.epi == EPI_ADD_ROWS;
+
+    auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
+      if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 stores ago has read it
+      __syncwarp();
+      stage_row(stg + sbuf * EPI_BUF, lane, v);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
+        bulk_commit();
       }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      sbuf ^= 1;
+    };
+    auto load_h = [&](const TileInfo& t, int c, int b) {
+      if (lane == 0) {
+        fence_proxy_async_smem();  // prior generic reads of this buffer before the async write
+        int x, y;
+        out_coords(p, MODE, t, c, row0, BN, x, y);
+        mbar_arrive_expect_tx(&hb[b], EPI_BUF);
+        tma_load_2d(hst + b * EPI_BUF, &tmap_d, &hb[b], x, y);
+      }
+    };
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const TileInfo t = decode(p, MODE, PAIR, tile);
+      const bool has_acc = t.kiters > 0;
+      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, 0, 0);
+      if (has_acc) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+      }
+      const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * BN;
+
+      if (bf16_out) {
 #pragma unroll 1
-      for (int chunk = 0; chunk < BN / 32; ++chunk) {
-        uint32_t r[32];
-        tmem_ld32(taddr + chunk * 32, r);
-        tmem_ld_wait();
-        float v[32];
+        for (int c = 0; c < NCHUNK; ++c) {
+          float v[64];
+          // rows to add (router backward: dx += ...), issued before the TMEM read
+          uint4 add_raw[8];
+          int add_row = -1;
+          if (p.epi == EPI_ADD_ROWS) {
+            const int trow = t.u * BM + row0 + lane;
+            if (trow < p.rows_valid) {
+              add_row = trow;
+              const uint4* src =
+                  reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + t.v * BN + c * 64);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        const int col = chunk * 32;
-        if (p.epi == EPI_ACT_FWD) {
-          if (p.out_pre) {
-            __nv_bfloat16* pre_row = p.out_pre + (long long)t.s * (BM * BN) + (long long)row * BN + col;
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              uint4 w = make_uint4(pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
-                                   pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
-              *reinterpret_cast<uint4*>(pre_row + i) = w;
+              for (int j = 0; j < 8; ++j) add_raw[j] = __ldg(src + j);
             }
           }
+          if (has_acc) {
+            uint32_t r0[32], r1[32];
+            tmem_ld32(taddr + c * 64, r0);
+            tmem_ld32(taddr + c * 64 + 32, r1);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = act_fwd(p.act, v[i]);
-        } else if (p.epi == EPI_ACT_BWD) {
-          const __nv_bfloat16* src = p.act_src + (long long)t.s * (BM * BN) + (long long)row * BN + col;
+            for (int i = 0; i < 32; ++i) {
+              v[i] = __uint_as_float(r0[i]);
+              v[32 + i] = __uint_as_float(r1[i]);
+            }
+          } else {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 w = *reinterpret_cast<const uint4*>(src + i);
-            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&w);
+            for (int i = 0; i < 64; ++i) v[i] = 0.f;
+          }
+          int x, y;
+          out_coords(p, MODE, t, c, row0, BN, x, y);
+          if (p.epi == EPI_ACT_FWD) {
+            if (p.has_pre) store_chunk(&tmap_d, v, x, y);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[i + j] *= act_grad(p.act, __bfloat162float(hv[j]));
+            for (int i = 0; i < 64; ++i) v[i] = act_fwd(p.act, v[i]);
+          } else if (EPI_H && p.epi == EPI_ACT_BWD) {
+            mbar_wait(&hb[c & 1], hphase[c & 1]);
+            hphase[c & 1] ^= 1;
+            const uint8_t* hrow = hst + (c & 1) * EPI_BUF + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float hf[8];
+              unpack8(*reinterpret_cast<const uint4*>(hrow + ((j ^ (lane & 7)) << 4)), hf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[8 * j + e] *= act_grad(p.act, hf[e]);
+            }
+            __syncwarp();
+            if (c + 1 < NCHUNK) load_h(t, c + 1, (c + 1) & 1);
+          } else if (p.epi == EPI_ADD_ROWS && add_row >= 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float af[8];
+              unpack8(add_raw[j], af);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[8 * j + e] += af[e];
+            }
+          }
+          store_chunk(&tmap_c, v, x, y);
+        }
+      } else if (p.epi == EPI_ROUTER) {
+        // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e), softmax gates
+        const int tok = t.u * BM + row0 + lane;
+        const bool valid = tok < p.rows_valid;
+        float bv[kMaxRouterTopK];
+        int be[kMaxRouterTopK];
+#pragma unroll
+        for (int j = 0; j < kMaxRouterTopK; ++j) {
+          bv[j] = -FLT_MAX;
+          be[j] = 0x7fffffff;
+        }
+        float mx = -FLT_MAX;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
+          if (valid) {
+            float4* lrow = reinterpret_cast<float4*>(p.logits + (long long)tok * p.E + c * 32);
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              lrow[i / 4] = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                                        __uint_as_float(r[i + 3]));
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float x = __uint_as_float(r[i]);
+            const int e = c * 32 + i;
+            mx = fmaxf(mx, x);
+            // stable insertion into the descending list (experts arrive in ascending e;
+            // strict '>' keeps the lower e first on ties). Back to front, reading the
+            // not-yet-updated predecessor.
+#pragma unroll
+            for (int j = kMaxRouterTopK - 1; j >= 0; --j) {
+              if (j < p.topk && x > bv[j]) {
+                if (j > 0 && x > bv[j - 1]) {
+                  bv[j] = bv[j - 1];
+                  be[j] = be[j - 1];
+                } else {
+                  bv[j] = x;
+                  be[j] = e;
+                }
+              }
+            }
           }
         }
+        float ssum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 w = make_uint4(pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
-                               pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
-          *reinterpret_cast<uint4*>(out_row + col + i) = w;
+          for (int i = 0; i < 32; ++i) ssum += __expf(__uint_as_float(r[i]) - mx);
+        }
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < kMaxRouterTopK; ++j) {
+            if (j < p.topk) {
+              p.idx[(long long)tok * p.topk + j] = be[j];
+              p.gates[(long long)tok * p.topk + j] = __expf(bv[j] - mx) / ssum;
+            }
+          }
+        }
+      } else {  // EPI_F32: fp32 partial tile (split-K)
+        const int r = t.u * BM + row0 + lane;
+        float* dst = p.out_f32 + (long long)t.s * p.split_stride + (long long)r * p.ld_f32 + t.v * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t rr[32];
+          if (has_acc) {  // warp-uniform: every lane takes part in the collective TMEM load
+            tmem_ld32(taddr + c * 32, rr);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rr[i] = 0u;
+          }
+          if (r < p.rows_valid) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              *reinterpret_cast<float4*>(dst + c * 32 + i) =
+                  make_float4(__uint_as_float(rr[i]), __uint_as_float(rr[i + 1]), __uint_as_float(rr[i + 2]),
+                              __uint_as_float(rr[i + 3]));
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (has_acc) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
     }
+    if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<TMEM_COLS>(tmem_base);
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
 // ------------------------------------------------------------------ host side
 
-template <int MODE, bool A_MN, bool B_MN>
-static moe_status launch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int max_tiles,
-                         cudaStream_t stream, const char* name) {
-  auto kern = bsgemm_kernel<MODE, A_MN, B_MN>;
+template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
+static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
+  using C = Cfg<BN, EPI_H>;
+  auto kern = bsgemm_kernel<MODE, A_MN, B_MN, BN, EPI_H>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", name, cudaGetErrorString(e));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
     attr_set = true;
   }
   int grid = moe_device_sm_count();
-  if (max_tiles < grid) grid = max_tiles;
+  if (L.max_tiles < grid) grid = L.max_tiles;
   if (grid < 1) grid = 1;
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
-  MOE_CHECK_LAUNCH(name);
+  kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, L.p);
+  MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
 }
 
-static GemmParams base_params(const moe_config* cfg, const moe_topology_t* topo) {
+#define MOE_GEMM_CASE(MODE, AMN, BMN, BN, H)                                                     \
+  if (L.mode == MODE && L.a_mn == AMN && L.b_mn == BMN && L.bn == BN && L.epi_h == H)          \
+    return launch_t<MODE, AMN, BMN, BN, H>(L, stream);
+
+moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream) {
+  // forward / backward products of the layer, 256-wide tiles
+  MOE_GEMM_CASE(SDD, false, true, 256, false)     // SDD      X_g . W1
+  MOE_GEMM_CASE(SDD, false, false, 256, true)     // SDD^T    dY_g . W2^T (+act')
+  MOE_GEMM_CASE(SDD, false, false, 256, false)
+  MOE_GEMM_CASE(DSD_ROW, false, true, 256, false)  // DSD      A . W2
+  MOE_GEMM_CASE(DSD_ROW, false, false, 256, false) // DSD^T    dH . W1^T
+  MOE_GEMM_CASE(DS_COL, true, true, 256, false)    // DS^TD    A^T . dY_g
+  MOE_GEMM_CASE(DS_COL, true, false, 256, false)
+  MOE_GEMM_CASE(DDS_COL, true, true, 256, false)   // DD^TS    X_g^T . dH
+  MOE_GEMM_CASE(DDS_COL, false, true, 256, false)
+  // 128-wide tiles (odd block-columns per expert, h % 256 != 0, DDS^T)
+  MOE_GEMM_CASE(SDD, false, true, 128, false)
+  MOE_GEMM_CASE(SDD, false, false, 128, true)
+  MOE_GEMM_CASE(SDD, false, false, 128, false)
+  MOE_GEMM_CASE(DSD_ROW, false, true, 128, false)
+  MOE_GEMM_CASE(DSD_ROW, false, false, 128, false)
+  MOE_GEMM_CASE(DS_COL, true, true, 128, false)
+  MOE_GEMM_CASE(DS_COL, true, false, 128, false)
+  MOE_GEMM_CASE(DDS_COL, true, true, 128, false)
+  MOE_GEMM_CASE(DDS_COL, false, true, 128, false)
+  MOE_GEMM_CASE(DDS_ROW, false, false, 128, false)
+  MOE_GEMM_CASE(DDS_ROW, true, false, 128, false)
+  // router
+  MOE_GEMM_CASE(DENSE, false, true, 64, false)     // logits = x . Wr (+top-k epilogue)
+  MOE_GEMM_CASE(DENSE, false, true, 128, false)
+  MOE_GEMM_CASE(DENSE, false, true, 256, false)
+  MOE_GEMM_CASE(DENSE, true, true, 64, false)      // dWr partials = x^T . dlogits
+  MOE_GEMM_CASE(DENSE, true, true, 128, false)
+  MOE_GEMM_CASE(DENSE, true, true, 256, false)
+  MOE_GEMM_CASE(DENSE, false, false, 256, false)   // dx += dlogits . Wr^T
+  MOE_GEMM_CASE(DENSE, false, false, 128, false)
+  return set_error(MOE_EUNSUPPORTED, "%s: no kernel instance for mode=%d a_mn=%d b_mn=%d bn=%d", L.name, L.mode,
+                   (int)L.a_mn, (int)L.b_mn, L.bn);
+}
+
+GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo) {
   GemmParams p{};
   p.sizes = topo->sizes;
   p.row_offsets = topo->row_offsets;
@@ -402,11 +642,18 @@ static GemmParams base_params(const moe_config* cfg, const moe_topology_t* topo)
   p.t_block_offsets = topo->t_block_offsets;
   p.t_row_indices = topo->t_row_indices;
   p.n_block_cols = (int)(cfg->num_experts * cfg->ffn_hidden / cfg->block_size);
-  p.dense_tiles = (int)(cfg->hidden / BN);
   p.k_dense = (int)cfg->hidden;
   p.epi = EPI_STORE;
   p.act = MOE_ACT_IDENTITY;
   return p;
+}
+
+// 256-wide tiles when every expert has an even number of block-columns and the
+// hidden size is a multiple of 256; 128 otherwise.
+static int pick_bn(const moe_config* cfg, bool pairs_columns) {
+  const int64_t F = cfg->ffn_hidden / cfg->block_size;
+  if (pairs_columns) return (F % 2 == 0) ? 256 : 128;
+  return (cfg->hidden % 256 == 0) ? 256 : 128;
 }
 
 }  // namespace moe
@@ -423,22 +670,28 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   MOE_CHECK_ARG(act >= 0 && act <= 2, "moe_sdd: bad act %d", act);
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  CUtensorMap ta, tb;
-  MOE_TRY(make_tmap_bf16(&ta, a, h, rows, h, 64, 128, "moe_sdd a"));
-  GemmParams p = base_params(cfg, topo);
-  p.out = reinterpret_cast<__nv_bfloat16*>(out_s);
-  p.out_pre = reinterpret_cast<__nv_bfloat16*>(out_pre);
-  p.act_src = reinterpret_cast<const __nv_bfloat16*>(act_grad_src);
-  p.ld_out = BN;
-  p.act = act;
-  p.epi = act_grad_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_pre) ? EPI_ACT_FWD : EPI_STORE);
-  if (!trans_b) {  // b [h, E*f]
-    MOE_TRY(make_tmap_bf16(&tb, b, N, h, N, 64, 64, "moe_sdd b"));
-    return launch<SDD, false, true>(ta, tb, p, (int)nnz, as_stream(stream), "moe_sdd");
-  } else {  // b [E*f, h]
-    MOE_TRY(make_tmap_bf16(&tb, b, h, N, h, 64, 128, "moe_sdd b^T"));
-    return launch<SDD, false, false>(ta, tb, p, (int)nnz, as_stream(stream), "moe_sdd(T)");
-  }
+  GemmLaunch L{};
+  L.name = trans_b ? "moe_sdd(T)" : "moe_sdd";
+  L.mode = SDD;
+  L.bn = pick_bn(cfg, true);
+  L.a_mn = false;
+  L.b_mn = !trans_b;
+  L.p = gemm_params_topo(cfg, topo);
+  L.p.act = act;
+  L.p.epi = act_grad_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_pre) ? EPI_ACT_FWD : EPI_STORE);
+  L.p.has_pre = out_pre != nullptr;
+  L.epi_h = L.p.epi == EPI_ACT_BWD;
+  L.max_tiles = (int)(nnz / (L.bn / 128));
+  MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 128, "moe_sdd a"));
+  if (!trans_b)
+    MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, 64, "moe_sdd b"));
+  else
+    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
+  MOE_TRY(make_tmap_bf16(&L.tc, out_s, 128, nnz * 128, 128, 64, 32, "moe_sdd out"));
+  if (out_pre) MOE_TRY(make_tmap_bf16(&L.td, out_pre, 128, nnz * 128, 128, 64, 32, "moe_sdd pre"));
+  if (act_grad_src) MOE_TRY(make_tmap_bf16(&L.td, act_grad_src, 128, nnz * 128, 128, 64, 32, "moe_sdd act src"));
+  if (!out_pre && !act_grad_src) L.td = L.tc;
+  return gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
@@ -448,32 +701,36 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  GemmParams p = base_params(cfg, topo);
-  p.out = reinterpret_cast<__nv_bfloat16*>(out);
-  p.ld_out = h;
-  CUtensorMap ta, tb;
+  GemmLaunch L{};
+  L.p = gemm_params_topo(cfg, topo);
+  L.bn = pick_bn(cfg, false);
+  L.p.dense_tiles = (int)(h / L.bn);
+  L.b_mn = !trans_b;
   if (!trans_s) {
-    // S [rows, E*f] values as [nnz*128, 128] row-major, K-major A
-    MOE_TRY(make_tmap_bf16(&ta, s, 128, nnz * 128, 128, 64, 128, "moe_dsd s"));
-    const int max_tiles = (int)(rows / BM * p.dense_tiles);
-    if (!trans_b) {  // b [E*f, h]: MN-major B
-      MOE_TRY(make_tmap_bf16(&tb, b, h, N, h, 64, 64, "moe_dsd b"));
-      return launch<DSD_ROW, false, true>(ta, tb, p, max_tiles, as_stream(stream), "moe_dsd");
-    } else {  // b [h, E*f]: K-major B
-      MOE_TRY(make_tmap_bf16(&tb, b, N, h, N, 64, 128, "moe_dsd b^T"));
-      return launch<DSD_ROW, false, false>(ta, tb, p, max_tiles, as_stream(stream), "moe_dsd(T)");
-    }
+    L.name = trans_b ? "moe_dsd(T)" : "moe_dsd";
+    L.mode = DSD_ROW;
+    L.a_mn = false;
+    L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
+    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 128, "moe_dsd s"));
+    if (!trans_b)
+      MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, 64, "moe_dsd b"));
+    else
+      MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, L.bn, "moe_dsd b^T"));
+    MOE_TRY(make_tmap_bf16(&L.tc, out, h, rows, h, 64, 32, "moe_dsd out"));
   } else {
-    MOE_TRY(make_tmap_bf16(&ta, s, 128, nnz * 128, 128, 64, 64, "moe_dsd s^T"));
-    const int max_tiles = p.n_block_cols * p.dense_tiles;
-    if (!trans_b) {  // b [rows, h]
-      MOE_TRY(make_tmap_bf16(&tb, b, h, rows, h, 64, 64, "moe_dsd b"));
-      return launch<DS_COL, true, true>(ta, tb, p, max_tiles, as_stream(stream), "moe_dsd(S^T)");
-    } else {  // b [h, rows]
-      MOE_TRY(make_tmap_bf16(&tb, b, rows, h, rows, 64, 128, "moe_dsd b^T"));
-      return launch<DS_COL, true, false>(ta, tb, p, max_tiles, as_stream(stream), "moe_dsd(S^T,T)");
-    }
+    L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
+    L.mode = DS_COL;
+    L.a_mn = true;
+    L.max_tiles = L.p.n_block_cols * L.p.dense_tiles;
+    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 64, "moe_dsd s^T"));
+    if (!trans_b)
+      MOE_TRY(make_tmap_bf16(&L.tb, b, h, rows, h, 64, 64, "moe_dsd b"));
+    else
+      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, L.bn, "moe_dsd b^T"));
+    MOE_TRY(make_tmap_bf16(&L.tc, out, h, N, h, 64, 32, "moe_dsd out"));
   }
+  L.td = L.tc;
+  return gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
@@ -483,34 +740,39 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
   MOE_CHECK_ARG(a && s && out, "moe_dds: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  GemmParams p = base_params(cfg, topo);
-  p.out = reinterpret_cast<__nv_bfloat16*>(out);
-  CUtensorMap ta, tb;
+  GemmLaunch L{};
+  L.p = gemm_params_topo(cfg, topo);
+  L.p.dense_tiles = (int)(h / BM);
+  L.a_mn = trans_a != 0;
   if (!trans_s) {
-    // out [h, E*f] = A_eff [h, rows] . S ; walk columns via the transpose index
-    p.ld_out = N;
-    MOE_TRY(make_tmap_bf16(&tb, s, 128, nnz * 128, 128, 64, 64, "moe_dds s"));
-    const int max_tiles = p.n_block_cols * p.dense_tiles;
-    if (trans_a) {  // a = [rows, h]: A_eff = a^T, MN-major
-      MOE_TRY(make_tmap_bf16(&ta, a, h, rows, h, 64, 64, "moe_dds a^T"));
-      return launch<DDS_COL, true, true>(ta, tb, p, max_tiles, as_stream(stream), "moe_dds(T)");
-    } else {  // a = [h, rows]: K-major
-      MOE_TRY(make_tmap_bf16(&ta, a, rows, h, rows, 64, 128, "moe_dds a"));
-      return launch<DDS_COL, false, true>(ta, tb, p, max_tiles, as_stream(stream), "moe_dds");
-    }
+    // out [h, E*f] = A_eff [h, rows] . S ; walk column pairs via the transpose index
+    L.name = trans_a ? "moe_dds(T)" : "moe_dds";
+    L.mode = DDS_COL;
+    L.bn = pick_bn(cfg, true);
+    L.b_mn = true;
+    L.max_tiles = L.p.n_block_cols / (L.bn / 128) * L.p.dense_tiles;
+    MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 64, "moe_dds s"));
+    if (trans_a)
+      MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 64, "moe_dds a^T"));
+    else
+      MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, 64, 128, "moe_dds a"));
+    MOE_TRY(make_tmap_bf16(&L.tc, out, N, h, N, 64, 32, "moe_dds out"));
   } else {
     // out [h, rows] = A_eff [h, E*f] . S^T ; walk rows
-    p.ld_out = rows;
-    MOE_TRY(make_tmap_bf16(&tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
-    const int max_tiles = (int)(rows / BM * p.dense_tiles);
-    if (trans_a) {  // a = [E*f, h]
-      MOE_TRY(make_tmap_bf16(&ta, a, h, N, h, 64, 64, "moe_dds a^T"));
-      return launch<DDS_ROW, true, false>(ta, tb, p, max_tiles, as_stream(stream), "moe_dds(T,S^T)");
-    } else {  // a = [h, E*f]
-      MOE_TRY(make_tmap_bf16(&ta, a, N, h, N, 64, 128, "moe_dds a"));
-      return launch<DDS_ROW, false, false>(ta, tb, p, max_tiles, as_stream(stream), "moe_dds(S^T)");
-    }
+    L.name = trans_a ? "moe_dds(T,S^T)" : "moe_dds(S^T)";
+    L.mode = DDS_ROW;
+    L.bn = 128;
+    L.b_mn = false;
+    L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
+    MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
+    if (trans_a)
+      MOE_TRY(make_tmap_bf16(&L.ta, a, h, N, h, 64, 64, "moe_dds a^T"));
+    else
+      MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
+    MOE_TRY(make_tmap_bf16(&L.tc, out, rows, h, rows, 64, 32, "moe_dds out"));
   }
+  L.td = L.tc;
+  return gemm_launch(L, as_stream(stream));
 }
 
 }  // extern "C"

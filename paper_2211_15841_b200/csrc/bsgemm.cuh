@@ -1,0 +1,58 @@
+// bsgemm.cuh — launch interface of the tcgen05 GEMM engine (bsgemm.cu), shared
+// by the block-sparse products and the router's dense GEMMs.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/moe.h"
+
+namespace moe {
+
+enum GemmMode { SDD = 0, DSD_ROW = 1, DS_COL = 2, DDS_COL = 3, DDS_ROW = 4, DENSE = 5 };
+enum EpiKind { EPI_STORE = 0, EPI_ACT_FWD = 1, EPI_ACT_BWD = 2, EPI_ROUTER = 3, EPI_F32 = 4, EPI_ADD_ROWS = 5 };
+
+struct GemmParams {
+  // sparse topology (device)
+  const int32_t* sizes;  // {Tp, nnz}
+  const int32_t* row_offsets;
+  const int32_t* col_indices;
+  const int32_t* row_indices;
+  const int32_t* t_col_offsets;
+  const int32_t* t_block_offsets;
+  const int32_t* t_row_indices;
+  int n_block_cols;  // E*F
+  int dense_tiles;   // output tiles along the dense dimension
+  int k_dense;       // SDD contraction length
+  // DENSE mode: tiles = splits x m_tiles x n_tiles, kiters_split K-steps of 64 per split
+  int m_tiles, n_tiles, splits, kiters_split, k_iters_total;
+  // epilogue
+  int epi, act, has_pre;
+  int rows_valid;  // rows of the output that exist (DENSE: M)
+  // EPI_ROUTER
+  float* logits;
+  int32_t* idx;
+  float* gates;
+  int E, topk;
+  // EPI_F32
+  float* out_f32;
+  long long ld_f32, split_stride;
+  // EPI_ADD_ROWS: out = acc + addend[row]
+  const __nv_bfloat16* addend;
+  long long ld_add;
+};
+
+struct GemmLaunch {
+  const char* name;
+  int mode, bn;
+  bool a_mn, b_mn, epi_h;
+  int max_tiles;
+  CUtensorMap ta, tb, tc, td;
+  GemmParams p;
+};
+
+moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
+GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo);
+
+}  // namespace moe

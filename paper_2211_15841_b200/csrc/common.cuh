@@ -57,6 +57,7 @@ struct WsLayout {
 };
 constexpr int kTopoChunk = 1024;  // assignments per topology CTA
 int router_bwd_parts(const moe_config* cfg);
+bool router_on_tensor_cores(const moe_config* cfg);
 WsLayout ws_layout(const moe_config* cfg);
 
 }  // namespace moe

@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 #include <float.h>
 
+#include "bsgemm.cuh"
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace moe {
 
@@ -110,8 +112,8 @@ __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restric
 
 // dlogits[t,:] = p * (dp - <p, dp>) with p = softmax(logits[t,:]), dp sparse from dgates.
 __global__ void router_dlogits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
-                                      const float* __restrict__ dgates, float* __restrict__ dlogits, int T, int E,
-                                      int k) {
+                                      const float* __restrict__ dgates, float* __restrict__ dlogits,
+                                      __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k) {
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (t >= T) return;
@@ -134,7 +136,10 @@ __global__ void router_dlogits_kernel(const float* __restrict__ logits, const in
     for (int j = 0; j < k; ++j)
       if (idx[(size_t)t * k + j] == e) dp += dgates[(size_t)t * k + j];
     const float p = expf(row[e] - m) * inv;
-    dlogits[(size_t)t * E + e] = p * (dp - pdp);
+    if (dlogits_bf16)
+      dlogits_bf16[(size_t)t * E + e] = __float2bfloat16_rn(p * (dp - pdp));
+    else
+      dlogits[(size_t)t * E + e] = p * (dp - pdp);
   }
 }
 
@@ -233,6 +238,32 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
   MOE_CHECK_ARG(x && wr && logits && expert_idx && gates, "moe_router: NULL pointer");
   (void)ws;
   const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
+  if (router_on_tensor_cores(cfg)) {
+    // logits = x . Wr on tcgen05 (M = tokens, N = E, K = h) with the greedy
+    // top-k + softmax gate epilogue fused (one thread per token row)
+    GemmLaunch L{};
+    L.name = "moe_router";
+    L.mode = DENSE;
+    L.bn = E;
+    L.a_mn = false;
+    L.b_mn = true;
+    L.p.m_tiles = (int)ceil_div(T, 128);
+    L.p.n_tiles = 1;
+    L.p.splits = 1;
+    L.p.k_iters_total = L.p.kiters_split = (int)ceil_div(h, 64);
+    L.p.epi = EPI_ROUTER;
+    L.p.rows_valid = T;
+    L.p.logits = logits;
+    L.p.idx = expert_idx;
+    L.p.gates = gates;
+    L.p.E = E;
+    L.p.topk = (int)cfg->top_k;
+    L.max_tiles = L.p.m_tiles;
+    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 128, "moe_router x"));
+    MOE_TRY(make_tmap_bf16(&L.tb, wr, E, h, E, 64, 64, "moe_router wr"));
+    L.tc = L.td = L.ta;
+    return gemm_launch(L, as_stream(stream));
+  }
   dim3 grid((unsigned)ceil_div(T, RT_TOK), (unsigned)ceil_div(E, RT_EXP));
   router_logits_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x),
                                                             reinterpret_cast<const __nv_bfloat16*>(wr), logits, T, h,
@@ -247,13 +278,63 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
   MOE_TRY(moe_check_config(cfg));
   MOE_CHECK_ARG(x && wr && logits && expert_idx && dgates && dwr && dx && ws, "moe_router_bwd: NULL pointer");
   const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts, k = (int)cfg->top_k;
-  const WsLayout L = ws_layout(cfg);
-  float* dlogits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + L.dlogits);
-  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + L.dwr_part);
+  const WsLayout WL = ws_layout(cfg);
+  float* dlogits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WL.dlogits);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WL.dwr_part);
   cudaStream_t s = as_stream(stream);
-  router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, dlogits, T, E, k);
-  MOE_CHECK_LAUNCH("router_dlogits");
   const int parts = router_bwd_parts(cfg);
+  if (router_on_tensor_cores(cfg)) {
+    __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(dlogits);
+    router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, nullptr, dl16, T, E, k);
+    MOE_CHECK_LAUNCH("router_dlogits");
+    // dWr partials = x^T . dlogits, split over tokens (M = h, N = E, K = T)
+    GemmLaunch L{};
+    L.name = "moe_router_bwd dWr";
+    L.mode = DENSE;
+    L.bn = E;
+    L.a_mn = true;
+    L.b_mn = true;
+    L.p.m_tiles = (int)ceil_div(h, 128);
+    L.p.n_tiles = 1;
+    L.p.splits = parts;
+    L.p.k_iters_total = (int)ceil_div(T, 64);
+    L.p.kiters_split = (int)ceil_div(L.p.k_iters_total, parts);
+    L.p.epi = EPI_F32;
+    L.p.rows_valid = h;
+    L.p.out_f32 = part;
+    L.p.ld_f32 = E;
+    L.p.split_stride = (long long)h * E;
+    L.max_tiles = parts * L.p.m_tiles;
+    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 64, "router_bwd x^T"));
+    MOE_TRY(make_tmap_bf16(&L.tb, dl16, E, T, E, 64, 64, "router_bwd dlogits"));
+    L.tc = L.td = L.ta;
+    MOE_TRY(gemm_launch(L, s));
+    router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
+    MOE_CHECK_LAUNCH("router_dwr_reduce");
+    // dx += dlogits . Wr^T (M = T, N = h, K = E), read-modify-write through the epilogue
+    GemmLaunch D{};
+    D.name = "moe_router_bwd dx";
+    D.mode = DENSE;
+    D.bn = h % 256 == 0 ? 256 : 128;
+    D.a_mn = false;
+    D.b_mn = false;
+    D.p.m_tiles = (int)ceil_div(T, 128);
+    D.p.n_tiles = h / D.bn;
+    D.p.splits = 1;
+    D.p.k_iters_total = D.p.kiters_split = E / 64;
+    D.p.epi = EPI_ADD_ROWS;
+    D.p.rows_valid = T;
+    D.p.addend = reinterpret_cast<const __nv_bfloat16*>(dx);
+    D.p.ld_add = h;
+    D.max_tiles = D.p.m_tiles * D.p.n_tiles;
+    MOE_TRY(make_tmap_bf16(&D.ta, dl16, E, T, E, 64, 128, "router_bwd dlogits"));
+    MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, 64, D.bn, "router_bwd wr"));
+    MOE_TRY(make_tmap_bf16(&D.tc, dx, h, T, h, 64, 32, "router_bwd dx"));
+    D.td = D.tc;
+    return gemm_launch(D, s);
+  }
+  router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, dlogits, nullptr, T, E, k);
+  MOE_CHECK_LAUNCH("router_dlogits");
   const int tpp = (int)ceil_div(T, parts);
   router_dwr_part_kernel<<<dim3(parts, (unsigned)ceil_div(h, 32)), 256, 0, s>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);

@@ -40,11 +40,22 @@ moe_status check_topo(const moe_topology_t* t) {
   return MOE_OK;
 }
 
+bool router_on_tensor_cores(const moe_config* cfg) {
+  return cfg->num_experts % 64 == 0 && cfg->num_experts <= 256 && cfg->top_k <= 8;
+}
+
 int router_bwd_parts(const moe_config* cfg) {
-  // split of the token (K) dimension of dWr = x^T dlogits; fixed per config so
-  // the reduction order is deterministic
-  int64_t parts = ceil_div(cfg->tokens, 256);
-  if (parts > 256) parts = 256;
+  // split of the token (K) dimension of dWr = x^T dlogits; fixed per config
+  // (independent of the device) so the reduction order is deterministic
+  int64_t parts;
+  if (router_on_tensor_cores(cfg)) {
+    const int64_t m_tiles = ceil_div(cfg->hidden, 128), k_iters = ceil_div(cfg->tokens, 64);
+    parts = ceil_div(148, m_tiles);
+    if (parts > k_iters) parts = k_iters;
+  } else {
+    parts = ceil_div(cfg->tokens, 256);
+    if (parts > 256) parts = 256;
+  }
   if (parts < 1) parts = 1;
   return (int)parts;
 }

@@ -1,0 +1,239 @@
+"""Expert parallelism for the dropless-MoE layer ("distributed training
+of MoEs with both data and expert model parallelism"; "8-way expert
+model parallelism for MoE layers and data parallelism for all other layers").
+
+Rank r of P owns the contiguous experts [r*E/P, (r+1)*E/P) and their W1 / W2
+slices; the router weights are replicated (data parallel). One process per
+GPU; the token exchange is torch.distributed all_to_all_single over NCCL
+(NVLink 5 / NVSwitch). Every compute step runs in libmoe.so kernels through
+the binding (`backend`); this module is plumbing: split sizes, the exchange
+and the ordering contract.
+
+Ordering contract: the sender lists its assignments in
+(global expert, flat id) order (moe_sort_rows over the local topology), so the
+chunk for rank q is contiguous. The receiver gets rows ordered
+(source rank, local expert, token); moe_topology's stable grouping by local
+expert then yields (local expert, source rank, token) = ascending global token
+id within each expert, i.e. each rank's expert topology is exactly the
+single-device topology of the global batch restricted to its experts.
+
+The host needs the per-rank counts to size the all-to-all (one small
+all_gather + device->host copy per forward); the single-GPU path has no host
+synchronisation at all.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+# ----------------------------------------------------------------------------- host logic (pure)
+
+def local_expert_range(rank: int, world: int, num_experts: int):
+    if num_experts % world:
+        raise ValueError(f"num_experts={num_experts} not divisible by world size {world}")
+    el = num_experts // world
+    return rank * el, (rank + 1) * el
+
+
+def send_splits(counts_row: np.ndarray, world: int) -> list[int]:
+    """Rows this rank sends to each destination: its assignments to the
+    destination's experts (counts_row = this rank's per-global-expert counts)."""
+    E = counts_row.size
+    el = E // world
+    return [int(counts_row[q * el:(q + 1) * el].sum()) for q in range(world)]
+
+
+def recv_plan(counts_all: np.ndarray, rank: int, world: int):
+    """counts_all [P, E]: assignments of source rank q to global expert e.
+    Returns (recv_splits per source, local expert id of every received row in
+    arrival order (source, local expert, token))."""
+    P, E = counts_all.shape
+    e0, e1 = local_expert_range(rank, world, E)
+    splits = [int(counts_all[q, e0:e1].sum()) for q in range(P)]
+    ids = [np.repeat(np.arange(e1 - e0, dtype=np.int32), counts_all[q, e0:e1]) for q in range(P)]
+    return splits, (np.concatenate(ids) if ids else np.zeros(0, np.int32))
+
+
+# ----------------------------------------------------------------------------- layer
+
+@dataclass
+class EPState:
+    cfg_local: object
+    cfg_e: object
+    logits: torch.Tensor
+    expert_idx: torch.Tensor
+    gates: torch.Tensor
+    topo_local: object
+    topo_e: object
+    sends: list
+    recvs: list
+    x_g: torch.Tensor | None
+    h_pre: torch.Tensor | None
+    a: torch.Tensor | None
+    y_sorted: torch.Tensor
+    n_recv: int
+
+
+class ExpertParallelMoE:
+    """Dropless MoE layer sharded by experts over a process group.
+
+    backend: object exposing the C-ABI binding functions (paper_2211_15841_b200.api
+    on GPUs). Weights: wr [h, E] (replicated), w1_local [h, E_l*f],
+    w2_local [E_l*f, h] of this rank's experts.
+    """
+
+    def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128):
+        self.B = backend
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.h, self.E, self.k, self.f, self.act, self.bs = hidden, num_experts, top_k, ffn_hidden, act, block_size
+        self.e0, self.e1 = local_expert_range(self.rank, self.world, num_experts)
+        self.El = self.e1 - self.e0
+
+    def _cfg(self, tokens, experts, k):
+        return self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def forward(self, x, wr, w1_local, w2_local):
+        B = self.B
+        T = x.shape[0]
+        cfg_l = self._cfg(T, self.E, self.k)
+        # (1) local router + top-k, grouped by GLOBAL expert
+        logits, idx, gates = B.moe_router(cfg_l, x, wr)
+        topo_l = B.moe_topology(cfg_l, idx)
+        x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
+        # (2) count exchange -> split sizes (the one host synchronisation)
+        counts = topo_l["counts"][: self.E].to(torch.int64)
+        gathered = [torch.empty_like(counts) for _ in range(self.world)]
+        dist.all_gather(gathered, counts, group=self.group)
+        counts_all = torch.stack(gathered).cpu().numpy()
+        sends = send_splits(counts_all[self.rank], self.world)
+        recvs, recv_ids = recv_plan(counts_all, self.rank, self.world)
+        n_recv = int(sum(recvs))
+        # (3) dispatch
+        recv_x = x.new_empty(n_recv, self.h)
+        self._a2a(recv_x, x_sorted, recvs, sends)
+        # (4) local experts: topology over E_l experts, padded gather, SDD(+act), DSD, un-pad
+        cfg_e = self._cfg(n_recv, self.El, 1)
+        topo_e = x_g = h_pre = a = None
+        y_recv = x.new_empty(n_recv, self.h)
+        if n_recv > 0:
+            ids = torch.from_numpy(recv_ids).to(x.device)
+            topo_e = B.moe_topology(cfg_e, ids)
+            x_g = B.moe_gather(cfg_e, recv_x, topo_e)
+            if self.act != 0:
+                a, h_pre = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_pre=True)
+            else:
+                a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
+            y_g = B.moe_dsd(cfg_e, a, 0, w2_local, 0, topo_e)
+            B.moe_scatter(cfg_e, y_g, topo_e, None, y=y_recv)
+        # (5) combine: reverse exchange, then gate-weighted sum in token order
+        y_sorted = x.new_empty(T * self.k, self.h)
+        self._a2a(y_sorted, y_recv, sends, recvs)
+        y = B.moe_unsort_rows(cfg_l, y_sorted, topo_l, gates)
+        st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, sends, recvs, x_g, h_pre, a, y_sorted, n_recv)
+        return y, st
+
+    def backward(self, st: EPState, x, dy, wr, w1_local, w2_local):
+        B = self.B
+        cfg_l, cfg_e = st.cfg_local, st.cfg_e
+        # b1 on the token owner: dY rows in expert order, dgates
+        dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
+        dy_recv = dy.new_empty(st.n_recv, self.h)
+        self._a2a(dy_recv, dy_sorted, st.recvs, st.sends)
+        dw1 = torch.zeros(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device)
+        dw2 = torch.zeros(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device)
+        dx_recv = dy.new_empty(st.n_recv, self.h)
+        if st.n_recv > 0:
+            dy_g = B.moe_gather(cfg_e, dy_recv, st.topo_e)
+            if self.act != 0:
+                dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, act_grad_src=st.h_pre)
+            else:
+                dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e)
+            B.moe_dsd(cfg_e, st.a, 1, dy_g, 0, st.topo_e, out=dw2)
+            dx_g = B.moe_dsd(cfg_e, dh, 0, w1_local, 1, st.topo_e)
+            B.moe_dds(cfg_e, st.x_g, 1, dh, 0, st.topo_e, out=dw1)
+            B.moe_gather_bwd(cfg_e, dx_g, st.topo_e, dx=dx_recv)
+        dx_sorted = dy.new_empty(cfg_l.tokens * self.k, self.h)
+        self._a2a(dx_sorted, dx_recv, st.sends, st.recvs)
+        dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
+        dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
+        dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
+        return dx, dwr, dw1, dw2
+
+
+# ----------------------------------------------------------------------------- bench (N > 1)
+
+def bench_ep(args, peaks):
+    """Weak-scaling EP benchmark: T_local tokens per rank of the BASELINE
+    config, experts split over ranks, NCCL all-to-all. Returns rank 0's JSON
+    dict (others None). Timed on the device, max over ranks."""
+    import json  # noqa: F401
+    import os
+    import time
+
+    from . import api as A
+    from synth import inputs as S
+
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    shp = S.CONFIGS[args.config]
+    T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
+    wts = S.make_inputs(shp, seed=0, tokens=1)                 # identical global weights on every rank
+    inp = S.make_inputs(shp, seed=100 + rank)                  # rank-local tokens
+    e0, e1 = local_expert_range(rank, world, E)
+    wr = wts["wr"].to(dev)
+    w1l = wts["w1"][:, e0 * f:e1 * f].contiguous().to(dev)
+    w2l = wts["w2"][e0 * f:e1 * f].contiguous().to(dev)
+    x, dy = inp["x"].to(dev), inp["dy"].to(dev)
+    del wts
+    layer = ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act)
+    l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        y, st = layer.forward(x, wr, w1l, w2l)
+        layer.backward(st, x, dy, wr, w1l, w2l)
+
+    for _ in range(args.warmup):
+        l2.zero_()
+        step()
+    torch.cuda.synchronize()
+    launches0 = A.lib.moe_total_launch_count()
+    total = 0.0
+    for _ in range(args.steps):
+        l2.zero_()
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        step()
+        e.record()
+        torch.cuda.synchronize()
+        total += s.elapsed_time(e)
+    launches = A.lib.moe_total_launch_count() - launches0
+    t = torch.tensor([total], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    out = None
+    if rank == 0:
+        out = {"metric": "dropless MoE layer fwd+bwd tokens/s", "value": round(T * world * args.steps / (ms / 1e3), 1),
+               "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "config": {"workload": shp.name, "tokens_per_rank": T, "hidden": h, "ffn_hidden": f,
+                          "num_experts": E, "top_k": k, "parallelism": f"ep{world}",
+                          "l2": "flushed between timed steps"},
+               "gpu_launches": int(launches), "roofline": None, "e2e": None}
+    dist.barrier()
+    dist.destroy_process_group()
+    return out

@@ -1,0 +1,141 @@
+"""Test-only CPU stand-in for the C-ABI binding, built on the oracle, so the
+expert-parallel orchestration (paper_2211_15841_b200.ep: split sizes, the
+all-to-all exchange, the ordering contract) can run under torch.distributed
+gloo with world_size 2 on a machine without GPUs. Never used by the product."""
+import types
+
+import numpy as np
+import torch
+
+from oracle import moe_oracle as O
+
+
+def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=4, act=1):
+    return types.SimpleNamespace(tokens=tokens, hidden=hidden, num_experts=num_experts, top_k=top_k,
+                                 ffn_hidden=ffn_hidden, block_size=4, act=act)
+
+
+def _np(t):
+    return t.detach().cpu().double().numpy()
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float64))
+
+
+class Topo:
+    def __init__(self, cfg, idx):
+        self.k = idx.shape[1] if idx.ndim == 2 else 1
+        self.plan = O.make_plan(idx.reshape(-1, self.k), cfg.num_experts, cfg.block_size)
+        self.topo = O.make_topology(self.plan, cfg.block_size, cfg.ffn_hidden)
+        R = self.plan.pos.size
+        self.sorted_pos = np.empty(R, np.int64)
+        self.sorted_pos[self.plan.sorted_idx] = np.arange(R)
+
+    def __getitem__(self, name):
+        return torch.from_numpy(getattr(self.plan, name).astype(np.int64))
+
+
+def moe_router(cfg, x, wr):
+    L = O.router_logits(_np(x), _np(wr))
+    idx, g = O.topk(L, cfg.top_k)
+    return _t(L), torch.from_numpy(idx), _t(g)
+
+
+def moe_topology(cfg, idx):
+    i = idx.numpy().reshape(-1, cfg.top_k) if cfg.top_k > 1 or idx.ndim == 2 else idx.numpy().reshape(-1, 1)
+    return Topo(cfg, i)
+
+
+def moe_sort_rows(cfg, x, topo):
+    return _t(_np(x)[topo.plan.sorted_idx // cfg.top_k])
+
+
+def moe_gather(cfg, x, topo):
+    return _t(O.padded_gather(_np(x), topo.plan, cfg.top_k))
+
+
+def moe_sdd(cfg, a, b, trans_b, topo, act=0, act_grad_src=None, want_pre=False, out=None):
+    H = O.sdd(_np(a), _np(b), topo.topo, trans_b=bool(trans_b))
+    if act_grad_src is not None:
+        return _t(H * O.act_grad(act, _np(act_grad_src)))
+    A = O.act(act, H)
+    return (_t(A), _t(H)) if want_pre else _t(A)
+
+
+def moe_dsd(cfg, s, trans_s, b, trans_b, topo, out=None):
+    r = _t(O.dsd(_np(s), _np(b), topo.topo, trans_s=bool(trans_s), trans_b=bool(trans_b)))
+    if out is not None:
+        out.copy_(r)
+        return out
+    return r
+
+
+def moe_dds(cfg, a, trans_a, s, trans_s, topo, out=None):
+    r = _t(O.dds(_np(a), _np(s), topo.topo, trans_a=bool(trans_a), trans_s=bool(trans_s)))
+    if out is not None:
+        out.copy_(r)
+        return out
+    return r
+
+
+def moe_scatter(cfg, y_g, topo, gates=None, y=None):
+    g = np.ones((cfg.tokens, cfg.top_k)) if gates is None else _np(gates)
+    r = _t(O.padded_scatter(_np(y_g), topo.plan, g, cfg.tokens, cfg.top_k))
+    if y is not None:
+        y.copy_(r)
+        return y
+    return r
+
+
+def moe_unsort_rows(cfg, y_sorted, topo, gates=None):
+    ys = _np(y_sorted)
+    k = cfg.top_k
+    g = np.ones((cfg.tokens, k)) if gates is None else _np(gates)
+    y = np.zeros((cfg.tokens, ys.shape[1]))
+    for t in range(cfg.tokens):
+        for j in range(k):
+            y[t] += g[t, j] * ys[topo.sorted_pos[t * k + j]]
+    return _t(y)
+
+
+def moe_unsort_rows_bwd(cfg, dy, y_sorted, topo, gates=None):
+    ys, d = _np(y_sorted), _np(dy)
+    k = cfg.top_k
+    g = np.ones((cfg.tokens, k)) if gates is None else _np(gates)
+    dys = np.zeros_like(ys)
+    dg = np.zeros((cfg.tokens, k))
+    for t in range(cfg.tokens):
+        for j in range(k):
+            u = topo.sorted_pos[t * k + j]
+            dys[u] = g[t, j] * d[t]
+            dg[t, j] = ys[u] @ d[t]
+    return _t(dys), _t(dg)
+
+
+def moe_gather_bwd(cfg, dx_g, topo, dx=None):
+    dg = _np(dx_g)
+    k = cfg.top_k
+    r = np.zeros((cfg.tokens, dg.shape[1]))
+    for i in range(cfg.tokens * k):
+        r[i // k] += dg[topo.plan.pos[i]]
+    if dx is not None:
+        dx.copy_(_t(r))
+        return dx
+    return _t(r)
+
+
+def moe_sort_rows_bwd(cfg, dx_sorted, topo):
+    return moe_unsort_rows(cfg, dx_sorted, topo, None)
+
+
+def moe_router_bwd(cfg, x, wr, logits, expert_idx, dgates, dx):
+    L, idx, dg = _np(logits), expert_idx.numpy(), _np(dgates)
+    p = O.softmax(L)
+    dp = np.zeros_like(p)
+    for t in range(L.shape[0]):
+        for j in range(cfg.top_k):
+            dp[t, idx[t, j]] += dg[t, j]
+    dl = p * (dp - (p * dp).sum(1, keepdims=True))
+    dx += _t(dl @ _np(wr).T)
+    return _t(_np(x).T @ dl)

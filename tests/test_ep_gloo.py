@@ -1,0 +1,108 @@
+"""Expert parallelism host logic under torch.distributed gloo, world_size 2,
+on CPU: the EP layer (paper_2211_15841_b200.ep) with the test-only oracle
+backend must reproduce the single-process oracle over the concatenated global
+batch — outputs, input gradients, expert weight-gradient slices and the
+all-reduced router gradient."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import moe_oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs(T, h, f, E, seed):
+    rng = np.random.default_rng(seed)
+    return (rng.normal(size=(T, h)), rng.normal(size=(h, E)) / np.sqrt(h), rng.normal(size=(h, E * f)) / np.sqrt(h),
+            rng.normal(size=(E * f, h)) / np.sqrt(f), rng.normal(size=(T, h)))
+
+
+def _worker(rank, world, port, cfgd, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import ep_cpu_backend as B
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "ep_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "paper_2211_15841_b200", "ep.py"))
+    ep = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ep)         # the EP module alone (no libmoe.so needed for host logic)
+    T, h, f, E, k, act = cfgd["T"], cfgd["h"], cfgd["f"], cfgd["E"], cfgd["k"], cfgd["act"]
+    x, wr, w1, w2, dy = _inputs(T * world, h, f, E, 0)
+    sl = slice(rank * T, (rank + 1) * T)
+    e0, e1 = ep.local_expert_range(rank, world, E)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    layer = ep.ExpertParallelMoE(B, dist.group.WORLD, h, E, k, f, act=act, block_size=4)
+    xl, dyl = t(x[sl]), t(dy[sl])
+    w1l, w2l = t(w1[:, e0 * f:e1 * f]), t(w2[e0 * f:e1 * f])
+    y, st = layer.forward(xl, t(wr), w1l, w2l)
+    dx, dwr, dw1, dw2 = layer.backward(st, xl, dyl, t(wr), w1l, w2l)
+    q.put((rank, y.numpy(), dx.numpy(), dwr.numpy(), dw1.numpy(), dw2.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfgd", [dict(T=24, h=6, f=8, E=4, k=1, act=1), dict(T=17, h=4, f=4, E=6, k=2, act=2),
+                                  dict(T=9, h=4, f=4, E=2, k=1, act=0)])
+def test_ep_world2_matches_global_oracle(cfgd):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfgd, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=300)
+        res[r[0]] = r[1:]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    T, h, f, E, k, act = cfgd["T"], cfgd["h"], cfgd["f"], cfgd["E"], cfgd["k"], cfgd["act"]
+    x, wr, w1, w2, dy = _inputs(T * world, h, f, E, 0)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, act)
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    El = E // world
+    for r in range(world):
+        yr, dxr, dwrr, dw1r, dw2r = res[r]
+        sl = slice(r * T, (r + 1) * T)
+        np.testing.assert_allclose(yr, y[sl], atol=1e-10)
+        np.testing.assert_allclose(dxr, g["dx"][sl], atol=1e-10)
+        np.testing.assert_allclose(dwrr, g["dwr"], atol=1e-10)
+        np.testing.assert_allclose(dw1r, g["dw1"][:, r * El * f:(r + 1) * El * f], atol=1e-10)
+        np.testing.assert_allclose(dw2r, g["dw2"][r * El * f:(r + 1) * El * f], atol=1e-10)
+
+
+def test_split_helpers():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "ep_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "paper_2211_15841_b200", "ep.py"))
+    ep = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ep)
+    counts = np.array([[3, 0, 2, 1], [1, 4, 0, 0]])
+    assert ep.send_splits(counts[0], 2) == [3, 3]
+    assert ep.send_splits(counts[1], 2) == [5, 0]
+    splits, ids = ep.recv_plan(counts, 1, 2)
+    assert splits == [3, 0]
+    assert ids.tolist() == [0, 0, 1]
+    splits, ids = ep.recv_plan(counts, 0, 2)
+    assert splits == [3, 5] and ids.tolist() == [0, 0, 0, 0, 1, 1, 1, 1]
+    with pytest.raises(ValueError):
+        ep.local_expert_range(0, 3, 4)

@@ -103,6 +103,44 @@ def test_router_logits_and_routing(name, T):
     np.testing.assert_allclose(gates.cpu().numpy()[~near], want_g[~near], rtol=1e-4, atol=1e-6)
 
 
+@pytest.mark.parametrize("E,k", [(64, 1), (64, 2), (128, 3), (256, 8)])
+def test_router_tensor_core_ties_and_topk(E, k):
+    """tcgen05 router epilogue: duplicated Wr columns give bit-identical logits,
+    so exact ties must resolve to the lower expert (R6); selection vs the
+    oracle's top-k on the GPU's own logits values is bit-exact."""
+    d = dev()
+    A = api()
+    T, h = 1000, 256
+    g = torch.Generator().manual_seed(E + k)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16)
+    for a, b in [(3, 7), (10, 11), (20, 5), (40, 41)]:
+        wr[:, b] = wr[:, a]                  # exact duplicate columns -> exact logit ties
+    cfg = A.make_config(T, h, E, k, 128)
+    logits, idx, gates = A.moe_router(cfg, x.to(d), wr.to(d))
+    L = logits.cpu().double().numpy()
+    got = idx.cpu().numpy()
+    assert (L[:, 3] == L[:, 7]).all() and (L[:, 10] == L[:, 11]).all()
+    # validity of the selection on the kernel's own fp32 scores (property
+    # check written here, not an oracle input): descending, ties -> lower e
+    for t in range(T):
+        order = sorted(range(E), key=lambda e: (-L[t, e], e))[:k]
+        assert list(got[t]) == order, t
+    p = np.exp(L - L.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    np.testing.assert_allclose(gates.cpu().numpy(), np.take_along_axis(p, got.astype(np.int64), 1),
+                               rtol=2e-5, atol=1e-7)
+    # against the oracle: logits within fp32 accumulation error, routing equal
+    # wherever the oracle's top-k margin exceeds that error
+    Lo = O.router_logits(S.to_f64(x), S.to_f64(wr))
+    err = np.abs(L - Lo).max()
+    assert err < 1e-4
+    want_idx, _ = O.topk(Lo, k)
+    srt = -np.sort(-Lo, axis=1)
+    near = (srt[:, k - 1] - srt[:, k]) < 4 * err + 1e-7 if E > k else np.zeros(T, bool)
+    assert (got[~near] == want_idx[~near]).all()
+
+
 # ------------------------------------------------------------------ topology
 
 @pytest.mark.parametrize("T,E,k,f,zipf", [(1000, 4, 1, 512, 0.0), (32768, 64, 1, 2048, 0.0), (8192, 64, 2, 4096, 0.0),
