@@ -43,10 +43,12 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_EPI_WARPS = 8;                  // 2 per TMEM lane quarter (column halves)
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int EPI_BUF = 32 * 128;                 // one warp's 32 rows x 64 bf16 (128 B)
-constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;        // 4 warps x double buffer
+constexpr int EPI_COLS = 32;                      // epilogue chunk: 32 rows x 32 columns per warp
+constexpr int EPI_BUF = 32 * EPI_COLS * 2;        // one warp's chunk, bf16, 64B-swizzled rows
+constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF;  // double buffered
 constexpr int SMEM_LIMIT = 232448;                // 227 KB opt-in
 constexpr int SMEM_FIXED = 1024 + 512;            // alignment slack + barriers
 constexpr int kMaxRouterTopK = 8;
@@ -117,20 +119,30 @@ __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pa
   return t;
 }
 
+// tanh on the SFU (MUFU.TANH, max rel. error ~2^-11, below the bf16 output ulp)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// gelu, tanh approximation (reading R2): 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
 __device__ __forceinline__ float act_fwd(int kind, float x) {
   if (kind == MOE_ACT_GELU_TANH) {
-    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-    return 0.5f * x * (1.0f + tanhf(u));
+    const float x2 = x * x;
+    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_fast(u), hx);
   }
   if (kind == MOE_ACT_RELU) return x > 0.f ? x : 0.f;
   return x;
 }
 __device__ __forceinline__ float act_grad(int kind, float x) {
   if (kind == MOE_ACT_GELU_TANH) {
-    const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-    const float t = tanhf(u);
-    const float du = 0.7978845608028654f * (1.0f + 3.0f * 0.044715f * x * x);
-    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+    const float x2 = x * x;
+    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
+    const float t = tanh_fast(u);
+    const float du = fmaf(0.7978845608028654f * 3.0f * 0.044715f, x2, 0.7978845608028654f);
+    return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), 0.5f * (1.0f + t));
   }
   if (kind == MOE_ACT_RELU) return x > 0.f ? 1.f : 0.f;
   return 1.f;
@@ -140,7 +152,7 @@ __device__ __forceinline__ float act_grad(int kind, float x) {
 // output tile, for the epilogue warp whose rows start at `row0` in the tile.
 __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const TileInfo& t, int c, int row0,
                                            int BN, int& x, int& y) {
-  const int col = c * 64;
+  const int col = c * EPI_COLS;
   switch (mode) {
     case SDD: {  // values as [nnz*128, 128]
       const int blk = t.s + col / 128;
@@ -166,15 +178,18 @@ __device__ __forceinline__ void unpack8(const uint4& w, float* f) {
   }
 }
 
-// Write 64 fp32 values of this thread's row as bf16 into a 128B-swizzled
-// [32 rows][128 B] staging buffer (row = lane).
+// 64B swizzle (TMA SWIZZLE_64B): 16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3).
+__device__ __forceinline__ int swz64(int j, int row) { return (j ^ ((row >> 1) & 3)) << 4; }
+
+// Write 32 fp32 values of this thread's row as bf16 into a 64B-swizzled
+// [32 rows][64 B] staging buffer (row = lane): conflict-free 16-byte stores.
 __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
-  uint8_t* row = buf + lane * 128;
+  uint8_t* row = buf + lane * 64;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < 4; ++j) {
     const uint4 w = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
                                pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-    *reinterpret_cast<uint4*>(row + ((j ^ (lane & 7)) << 4)) = w;
+    *reinterpret_cast<uint4*>(row + swz64(j, lane)) = w;
   }
 }
 
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using C = Cfg<BN, EPI_H>;
   constexpr int STAGES = C::STAGES;
   constexpr int PAIR = (MODE == SDD || MODE == DDS_COL) ? BN / 128 : 1;
-  constexpr int NCHUNK = BN / 64;
+  constexpr int NCHUNK = BN / EPI_COLS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -197,8 +212,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* hbar = tempty + 2;  // [4 warps][2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 8);
+  uint64_t* hbar = tempty + 2;  // [NUM_EPI_WARPS][2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * NUM_EPI_WARPS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -210,9 +225,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], NUM_EPI_WARPS);
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&hbar[i], 1);
+    for (int i = 0; i < 2 * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -361,14 +376,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    const int q = warp & 3;   // TMEM lane quarter this warp may access
-    const int wq = warp - 2;  // staging-buffer owner index
-    const int row0 = q * 32;  // first tile row of this warp
+    // ===================== epilogue (warps 2..9) =====================
+    // Warp w reads TMEM lane quarter w % 4 (rows 32q..32q+31 of the tile) and
+    // the 32-column chunks c = half, half + 2, ... (half = (w - 2) / 4).
+    const int q = warp & 3;
+    const int wq = warp - 2;
+    const int half = wq >> 2;
+    const int row0 = q * 32;
     uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
     uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
     uint64_t* hb = hbar + wq * 2;
     uint32_t hphase[2] = {0, 0};
+    int hslot = 0;
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -399,7 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo t = decode(p, MODE, PAIR, tile);
       const bool has_acc = t.kiters > 0;
-      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, 0, 0);
+      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, half, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -408,57 +427,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
       if (bf16_out) {
 #pragma unroll 1
-        for (int c = 0; c < NCHUNK; ++c) {
-          float v[64];
+        for (int c = half; c < NCHUNK; c += 2) {
+          float v[32];
           // rows to add (router backward: dx += ...), issued before the TMEM read
-          uint4 add_raw[8];
-          int add_row = -1;
+          uint4 add_raw[4];
+          bool add_ok = false;
           if (p.epi == EPI_ADD_ROWS) {
             const int trow = t.u * BM + row0 + lane;
             if (trow < p.rows_valid) {
-              add_row = trow;
-              const uint4* src =
-                  reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + t.v * BN + c * 64);
+              add_ok = true;
+              const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + t.v * BN +
+                                                                c * EPI_COLS);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) add_raw[j] = __ldg(src + j);
+              for (int j = 0; j < 4; ++j) add_raw[j] = __ldg(src + j);
             }
           }
           if (has_acc) {
-            uint32_t r0[32], r1[32];
-            tmem_ld32(taddr + c * 64, r0);
-            tmem_ld32(taddr + c * 64 + 32, r1);
+            uint32_t r[32];
+            tmem_ld32(taddr + c * EPI_COLS, r);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              v[i] = __uint_as_float(r0[i]);
-              v[32 + i] = __uint_as_float(r1[i]);
-            }
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = 0.f;
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
           int x, y;
           out_coords(p, MODE, t, c, row0, BN, x, y);
           if (p.epi == EPI_ACT_FWD) {
             if (p.has_pre) store_chunk(&tmap_d, v, x, y);
 #pragma unroll
-            for (int i = 0; i < 64; ++i) v[i] = act_fwd(p.act, v[i]);
+            for (int i = 0; i < 32; ++i) v[i] = act_fwd(p.act, v[i]);
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
-            mbar_wait(&hb[c & 1], hphase[c & 1]);
-            hphase[c & 1] ^= 1;
-            const uint8_t* hrow = hst + (c & 1) * EPI_BUF + lane * 128;
+            mbar_wait(&hb[hslot], hphase[hslot]);
+            hphase[hslot] ^= 1;
+            const uint8_t* hrow = hst + hslot * EPI_BUF + lane * 64;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               float hf[8];
-              unpack8(*reinterpret_cast<const uint4*>(hrow + ((j ^ (lane & 7)) << 4)), hf);
+              unpack8(*reinterpret_cast<const uint4*>(hrow + swz64(j, lane)), hf);
 #pragma unroll
               for (int e = 0; e < 8; ++e) v[8 * j + e] *= act_grad(p.act, hf[e]);
             }
             __syncwarp();
-            if (c + 1 < NCHUNK) load_h(t, c + 1, (c + 1) & 1);
-          } else if (p.epi == EPI_ADD_ROWS && add_row >= 0) {
+            hslot ^= 1;
+            if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);
+          } else if (p.epi == EPI_ADD_ROWS && add_ok) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               float af[8];
               unpack8(add_raw[j], af);
 #pragma unroll
@@ -468,66 +484,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           store_chunk(&tmap_c, v, x, y);
         }
       } else if (p.epi == EPI_ROUTER) {
-        // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e), softmax gates
-        const int tok = t.u * BM + row0 + lane;
-        const bool valid = tok < p.rows_valid;
-        float bv[kMaxRouterTopK];
-        int be[kMaxRouterTopK];
+        // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e),
+        // softmax gates. Column-half 0 warps own whole rows.
+        if (half == 0) {
+          const int tok = t.u * BM + row0 + lane;
+          const bool valid = tok < p.rows_valid;
+          float bv[kMaxRouterTopK];
+          int be[kMaxRouterTopK];
 #pragma unroll
-        for (int j = 0; j < kMaxRouterTopK; ++j) {
-          bv[j] = -FLT_MAX;
-          be[j] = 0x7fffffff;
-        }
-        float mx = -FLT_MAX;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_ld_wait();
-          if (valid) {
-            float4* lrow = reinterpret_cast<float4*>(p.logits + (long long)tok * p.E + c * 32);
-#pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              lrow[i / 4] = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-                                        __uint_as_float(r[i + 3]));
+          for (int j = 0; j < kMaxRouterTopK; ++j) {
+            bv[j] = -FLT_MAX;
+            be[j] = 0x7fffffff;
           }
+          float mx = -FLT_MAX;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
+            tmem_ld_wait();
+            if (valid) {
+              float4* lrow = reinterpret_cast<float4*>(p.logits + (long long)tok * p.E + c * 32);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float x = __uint_as_float(r[i]);
-            const int e = c * 32 + i;
-            mx = fmaxf(mx, x);
-            // stable insertion into the descending list (experts arrive in ascending e;
-            // strict '>' keeps the lower e first on ties). Back to front, reading the
-            // not-yet-updated predecessor.
+              for (int i = 0; i < 32; i += 4)
+                lrow[i / 4] = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            }
 #pragma unroll
-            for (int j = kMaxRouterTopK - 1; j >= 0; --j) {
-              if (j < p.topk && x > bv[j]) {
-                if (j > 0 && x > bv[j - 1]) {
-                  bv[j] = bv[j - 1];
-                  be[j] = be[j - 1];
-                } else {
-                  bv[j] = x;
-                  be[j] = e;
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(r[i]);
+              const int e = c * 32 + i;
+              mx = fmaxf(mx, x);
+              // stable insertion into the descending list (experts arrive in ascending e;
+              // strict '>' keeps the lower e first on ties). Back to front, reading the
+              // not-yet-updated predecessor.
+#pragma unroll
+              for (int j = kMaxRouterTopK - 1; j >= 0; --j) {
+                if (j < p.topk && x > bv[j]) {
+                  if (j > 0 && x > bv[j - 1]) {
+                    bv[j] = bv[j - 1];
+                    be[j] = be[j - 1];
+                  } else {
+                    bv[j] = x;
+                    be[j] = e;
+                  }
                 }
               }
             }
           }
-        }
-        float ssum = 0.f;
+          float ssum = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(taddr + c * 32, r);
-          tmem_ld_wait();
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * 32, r);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) ssum += __expf(__uint_as_float(r[i]) - mx);
-        }
-        if (valid) {
+            for (int i = 0; i < 32; ++i) ssum += __expf(__uint_as_float(r[i]) - mx);
+          }
+          if (valid) {
 #pragma unroll
-          for (int j = 0; j < kMaxRouterTopK; ++j) {
-            if (j < p.topk) {
-              p.idx[(long long)tok * p.topk + j] = be[j];
-              p.gates[(long long)tok * p.topk + j] = __expf(bv[j] - mx) / ssum;
+            for (int j = 0; j < kMaxRouterTopK; ++j) {
+              if (j < p.topk) {
+                p.idx[(long long)tok * p.topk + j] = be[j];
+                p.gates[(long long)tok * p.topk + j] = __expf(bv[j] - mx) / ssum;
+              }
             }
           }
         }
@@ -535,7 +554,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r = t.u * BM + row0 + lane;
         float* dst = p.out_f32 + (long long)t.s * p.split_stride + (long long)r * p.ld_f32 + t.v * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
+        for (int c = half; c < BN / 32; c += 2) {
           uint32_t rr[32];
           if (has_acc) {  // warp-uniform: every lane takes part in the collective TMEM load
             tmem_ld32(taddr + c * 32, rr);
@@ -687,9 +706,9 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
     MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, 64, "moe_sdd b"));
   else
     MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
-  MOE_TRY(make_tmap_bf16(&L.tc, out_s, 128, nnz * 128, 128, 64, 32, "moe_sdd out"));
-  if (out_pre) MOE_TRY(make_tmap_bf16(&L.td, out_pre, 128, nnz * 128, 128, 64, 32, "moe_sdd pre"));
-  if (act_grad_src) MOE_TRY(make_tmap_bf16(&L.td, act_grad_src, 128, nnz * 128, 128, 64, 32, "moe_sdd act src"));
+  MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
+  if (out_pre) MOE_TRY(make_tmap_epi(&L.td, out_pre, 128, nnz * 128, 128, "moe_sdd pre"));
+  if (act_grad_src) MOE_TRY(make_tmap_epi(&L.td, act_grad_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_pre && !act_grad_src) L.td = L.tc;
   return gemm_launch(L, as_stream(stream));
 }
@@ -716,7 +735,7 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
       MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, 64, "moe_dsd b"));
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, L.bn, "moe_dsd b^T"));
-    MOE_TRY(make_tmap_bf16(&L.tc, out, h, rows, h, 64, 32, "moe_dsd out"));
+    MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
   } else {
     L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
     L.mode = DS_COL;
@@ -727,7 +746,7 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
       MOE_TRY(make_tmap_bf16(&L.tb, b, h, rows, h, 64, 64, "moe_dsd b"));
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, L.bn, "moe_dsd b^T"));
-    MOE_TRY(make_tmap_bf16(&L.tc, out, h, N, h, 64, 32, "moe_dsd out"));
+    MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
   }
   L.td = L.tc;
   return gemm_launch(L, as_stream(stream));
@@ -756,7 +775,7 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
       MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 64, "moe_dds a^T"));
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, 64, 128, "moe_dds a"));
-    MOE_TRY(make_tmap_bf16(&L.tc, out, N, h, N, 64, 32, "moe_dds out"));
+    MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
   } else {
     // out [h, rows] = A_eff [h, E*f] . S^T ; walk rows
     L.name = trans_a ? "moe_dds(T,S^T)" : "moe_dds(S^T)";
@@ -769,7 +788,7 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
       MOE_TRY(make_tmap_bf16(&L.ta, a, h, N, h, 64, 64, "moe_dds a^T"));
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
-    MOE_TRY(make_tmap_bf16(&L.tc, out, rows, h, rows, 64, 32, "moe_dds out"));
+    MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));
   }
   L.td = L.tc;
   return gemm_launch(L, as_stream(stream));

@@ -329,7 +329,7 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
     D.max_tiles = D.p.m_tiles * D.p.n_tiles;
     MOE_TRY(make_tmap_bf16(&D.ta, dl16, E, T, E, 64, 128, "router_bwd dlogits"));
     MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, 64, D.bn, "router_bwd wr"));
-    MOE_TRY(make_tmap_bf16(&D.tc, dx, h, T, h, 64, 32, "router_bwd dx"));
+    MOE_TRY(make_tmap_epi(&D.tc, dx, h, T, h, "router_bwd dx"));
     D.td = D.tc;
     return gemm_launch(D, s);
   }

@@ -26,7 +26,7 @@ static EncodeTiledFn get_encode() {
 }
 
 moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
-                          uint32_t box_inner, uint32_t box_outer, const char* what) {
+                          uint32_t box_inner, uint32_t box_outer, const char* what, int swizzle_bytes) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
   if (!base) return set_error(MOE_EINVAL, "%s: NULL pointer", what);
@@ -39,7 +39,9 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return set_error(MOE_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d) dims=[%llu,%llu] box=[%u,%u]", what, (int)r,

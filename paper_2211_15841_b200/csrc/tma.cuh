@@ -5,7 +5,13 @@
 
 namespace moe {
 // 2-D bf16 tensor map, SWIZZLE_128B, element coordinates (inner, outer).
-// row_elems: row pitch in elements. box_inner must be 64 (128 B swizzle span).
+// row_elems: row pitch in elements. box_inner * 2 bytes must equal the
+// swizzle span (64 elements for 128 B, 32 for 64 B).
 moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
-                          uint32_t box_inner, uint32_t box_outer, const char* what);
+                          uint32_t box_inner, uint32_t box_outer, const char* what, int swizzle_bytes = 128);
+// Epilogue store / H-prefetch maps: 32 x 32 boxes, 64 B swizzle.
+inline moe_status make_tmap_epi(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                uint64_t row_elems, const char* what) {
+  return make_tmap_bf16(map, base, inner, outer, row_elems, 32, 32, what, 64);
+}
 }  // namespace moe
