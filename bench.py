@@ -110,7 +110,8 @@ def work_model(T, h, f, E, k, Tp):
         "executed_flop_step": 6 * 2 * Tp * h * f,
         "prod_flop": prod_flop,
         "prod_bytes": prod_bytes,
-        "sddt_bytes": prod_bytes + 2 * R * f,
+        "sddt_bytes": prod_bytes + 2 * R * f,      # + read of the saved pre-activation H
+        "sdd_bytes": prod_bytes + 2 * R * f,       # + write of H (kept for act' in the backward)
         "gather_bytes": 2 * (T * h + R * h) + 4 * R,
         "scatter_bytes": 2 * (R * h + T * h) + 8 * R,
         "scatter_bwd_bytes": 2 * (T * h + 2 * R * h) + 4 * R,
@@ -148,17 +149,30 @@ class Step:
                                 None if idn else d(sv.h_pre), s)),
             ("dsd", L.moe_dsd, (c, d(sv.a), 0, d(t["w2"]), 0, topo, d(sv.y_g), s)),
             ("scatter", L.moe_scatter, (c, d(sv.y_g), topo, d(sv.gates), d(t["y"]), s)),
-            ("scatter_bwd", L.moe_scatter_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"], wsl["dgates"],
-                                                s)),
+        ]
+        fused =cfg.num_experts % 64 == 0 and cfg.num_experts <= 256 and cfg.top_k <= 8
+        if fused:   # moe_backward's tensor-core router path (layer.cu)
+            bwd = [("scatter_bwd", L.moe_scatter_bwd_router, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), d(sv.logits),
+                                                              d(sv.expert_idx), wsl["dy_g"], wsl["dgates"],
+                                                              wsl["dlogits"], s))]
+        else:
+            bwd = [("scatter_bwd", L.moe_scatter_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"],
+                                                       wsl["dgates"], s))]
+        bwd += [
             ("sddT", L.moe_sdd, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act, None if idn else d(sv.h_pre),
                                  wsl["dh"], None, s)),
             ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
             ("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
             ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
-            ("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
-            ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), wsl["dgates"],
-                                              d(t["dwr"]), d(t["dx"]), ws, s)),
         ]
+        if fused:
+            bwd += [("router_dwr", L.moe_router_dwr, (c, d(t["x"]), wsl["dlogits"], d(t["dwr"]), ws, s)),
+                    ("router_dx", L.moe_router_dx, (c, wsl["dlogits"], d(t["wr"]), wsl["dx_g"], topo, d(t["dx"]), s))]
+        else:
+            bwd += [("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
+                    ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
+                                                      wsl["dgates"], d(t["dwr"]), d(t["dx"]), ws, s))]
+        self.calls += bwd
         self.names = [n for n, _, _ in self.calls]
 
     def run(self, events=None):
@@ -173,26 +187,11 @@ class Step:
 
 
 def ws_views(A, cfg, ws):
-    """Pointers inside the workspace exactly as moe_backward lays them out
-    (status.cu ws_layout): dY_g, dH, dX_g, dgates."""
-    h, bs = cfg.hidden, cfg.block_size
-    rows = A.moe_max_padded_rows(cfg)
-    nnz = A.moe_max_nnz_blocks(cfg)
-    R = cfg.tokens * cfg.top_k
-    E = cfg.num_experts
-    n_chunks = -(-R // 1024)
-    al = lambda v: (v + 255) & ~255  # noqa: E731
-    off = al(4 * n_chunks * E)
-    dy_g = off
-    off = al(off + 2 * rows * h)
-    dh = off
-    off = al(off + 2 * nnz * bs * bs)
-    dx_g = off
-    off = al(off + 2 * rows * h)
-    dgates = off
+    """Pointers inside the workspace exactly where moe_backward keeps its
+    scratch tensors (moe_workspace_offset)."""
     base = ws.data_ptr()
-    P = ctypes.c_void_p
-    return {"dy_g": P(base + dy_g), "dh": P(base + dh), "dx_g": P(base + dx_g), "dgates": P(base + dgates)}
+    off = lambda i: ctypes.c_void_p(base + A.lib.moe_workspace_offset(ctypes.byref(cfg), i))  # noqa: E731
+    return {"dy_g": off(0), "dh": off(1), "dx_g": off(2), "dgates": off(3), "dlogits": off(4)}
 
 
 def flush_l2(buf):
@@ -254,7 +253,7 @@ def run_ours_single(args, peaks):
     shares = mean_call / mean_call.sum()
     dom = int(np.argmax(mean_call))
     dname = step.names[dom]
-    prod_names = {"sdd": "prod_bytes", "dsd": "prod_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
+    prod_names = {"sdd": "sdd_bytes", "dsd": "prod_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
                   "dsdT": "prod_bytes", "ddTs": "prod_bytes"}
     byte_names = {"gather": "gather_bytes", "scatter": "scatter_bytes", "scatter_bwd": "scatter_bwd_bytes",
                   "gather_bwd": "gather_bwd_bytes"}

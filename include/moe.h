@@ -74,7 +74,7 @@ typedef struct {
 const char* moe_last_error(void);
 
 /* MOE_OK iff: T >= 1, h >= 1, 1 <= k <= E, f % bs == 0, act valid; and for the
- * GPU path: bs == 128, h % 128 == 0, E <= 1024. */
+ * GPU path: bs == 128, h % 256 == 0 and h <= 2048, E <= 1024. */
 moe_status moe_check_config(const moe_config* cfg);
 
 /* Worst-case padded rows: Tp = sum_e bs*ceil(c_e/bs) <= bs*floor((R + min(E,R)*(bs-1))/bs),
@@ -88,6 +88,12 @@ int64_t moe_max_nnz_blocks(const moe_config* cfg);
  * moe_backward and moe_router_bwd for this config (a single buffer can serve
  * all of them, but not concurrently). 256-byte aligned pointer required. */
 size_t moe_workspace_bytes(const moe_config* cfg);
+
+/* Byte offset inside the workspace of the scratch tensors moe_backward uses:
+ * which = 0 dY_g [max_rows,h] bf16, 1 dH [max_nnz,bs,bs] bf16, 2 dX_g
+ * [max_rows,h] bf16, 3 dgates [T,k] fp32, 4 dlogits [T,E] (bf16 on the
+ * tensor-core router path). Returns (size_t)-1 for an unknown `which`. */
+size_t moe_workspace_offset(const moe_config* cfg, int which);
 
 /* Number of SMs the library sizes its persistent grids for (queried once). */
 int moe_device_sm_count(void);
@@ -203,6 +209,26 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
 moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, const float* logits,
                           const int32_t* expert_idx, const float* dgates, float* dwr, void* dx,
                           void* ws, void* stream);
+
+/* ---- fused backward pieces used by moe_backward when the router runs on the
+ *      tensor cores (E % 64 == 0, E <= 256, top_k <= 8; else MOE_EUNSUPPORTED) --- */
+
+/* b1 + the softmax part of b7 in one pass per token: dy_g and dgates exactly as
+ * moe_scatter_bwd, and dlogits_bf16 [T,E] = p * (dp - <p,dp>) rounded to bf16,
+ * p = softmax(logits[t,:]), dp[e] = sum_{j: expert_idx[t,j] = e} dgates[t,j]. */
+moe_status moe_scatter_bwd_router(const moe_config* cfg, const void* dy, const void* y_g, const moe_topology_t* topo,
+                                  const float* gates, const float* logits, const int32_t* expert_idx, void* dy_g,
+                                  float* dgates, void* dlogits_bf16, void* stream);
+
+/* b7: dwr [h,E] fp32 = x^T . dlogits (tcgen05, token dimension split into a
+ * fixed number of ranges, partials reduced in a fixed order). ws as above. */
+moe_status moe_router_dwr(const moe_config* cfg, const void* x, const void* dlogits_bf16, float* dwr, void* ws,
+                          void* stream);
+
+/* b6 + b7: dx [T,h] bf16 = sum_j dx_g[pos[t*k+j]] + dlogits . wr^T (tcgen05,
+ * the padded-gather backward fused into the GEMM epilogue). */
+moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const void* wr, const void* dx_g,
+                         const moe_topology_t* topo, void* dx, void* stream);
 
 /* ---- the layer: Fig. 5 forward, §5.1 backward ---- */
 typedef struct {

@@ -56,6 +56,7 @@ SIGNATURES = {
     "moe_max_nnz_blocks": (ctypes.c_int64, [CFG]),
     "moe_workspace_bytes": (ctypes.c_size_t, [CFG]),
     "moe_device_sm_count": (ctypes.c_int, []),
+    "moe_workspace_offset": (ctypes.c_size_t, [CFG, ctypes.c_int]),
     "moe_router": (STATUS, [CFG, P, P, P, P, P, P, P]),
     "moe_topk": (STATUS, [CFG, P, P, P, P]),
     "moe_topology": (STATUS, [CFG, P, TOPO, P, P]),
@@ -71,6 +72,9 @@ SIGNATURES = {
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_dds": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),
+    "moe_scatter_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),
+    "moe_router_dwr": (STATUS, [CFG, P, P, P, P, P]),
+    "moe_router_dx": (STATUS, [CFG, P, P, P, TOPO, P, P]),
     "moe_forward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), P, P, ctypes.POINTER(MoeSaved), P, P]),
     "moe_backward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), ctypes.POINTER(MoeSaved), P, P, P,
                               ctypes.POINTER(MoeGrads), P, P]),

@@ -432,14 +432,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // rows to add (router backward: dx += ...), issued before the TMEM read
           uint4 add_raw[4];
           bool add_ok = false;
+          float add_f[32];
           if (p.epi == EPI_ADD_ROWS) {
             const int trow = t.u * BM + row0 + lane;
             if (trow < p.rows_valid) {
               add_ok = true;
-              const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + t.v * BN +
-                                                                c * EPI_COLS);
+              const long long col0 = (long long)t.v * BN + c * EPI_COLS;
+              if (p.addend_map) {  // gathered rows (fused gather backward): sum_j addend[map[trow*k+j]]
 #pragma unroll
-              for (int j = 0; j < 4; ++j) add_raw[j] = __ldg(src + j);
+                for (int i = 0; i < 32; ++i) add_f[i] = 0.f;
+                for (int j = 0; j < p.addend_k; ++j) {
+                  const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
+                  const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
+#pragma unroll
+                  for (int q2 = 0; q2 < 4; ++q2) {
+                    float af[8];
+                    unpack8(__ldg(src + q2), af);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) add_f[8 * q2 + e] += af[e];
+                  }
+                }
+              } else {
+                const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + col0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) add_raw[j] = __ldg(src + j);
+              }
             }
           }
           if (has_acc) {
@@ -473,12 +490,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             hslot ^= 1;
             if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);
           } else if (p.epi == EPI_ADD_ROWS && add_ok) {
+            if (p.addend_map) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float af[8];
-              unpack8(add_raw[j], af);
+              for (int i = 0; i < 32; ++i) v[i] += add_f[i];
+            } else {
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[8 * j + e] += af[e];
+              for (int j = 0; j < 4; ++j) {
+                float af[8];
+                unpack8(add_raw[j], af);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[8 * j + e] += af[e];
+              }
             }
           }
           store_chunk(&tmap_c, v, x, y);

@@ -38,10 +38,21 @@ struct GemmParams {
   // EPI_F32
   float* out_f32;
   long long ld_f32, split_stride;
-  // EPI_ADD_ROWS: out = acc + addend[row]
+  // EPI_ADD_ROWS: out = acc + addend[row], or with addend_map:
+  // out = acc + sum_{j < addend_k} addend[addend_map[row * addend_k + j]]
   const __nv_bfloat16* addend;
   long long ld_add;
+  const int32_t* addend_map;
+  int addend_k;
 };
+
+// Router backward on tcgen05 (router.cu): dWr = x^T . dlogits and
+// dx = dlogits . Wr^T + addend (optionally gathered through addend_map).
+moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat16* dlogits, float* dwr, void* ws,
+                         cudaStream_t s);
+moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, const void* wr, void* dx,
+                        const void* addend, const int32_t* addend_map, int addend_k, long long ld_add,
+                        cudaStream_t s);
 
 struct GemmLaunch {
   const char* name;

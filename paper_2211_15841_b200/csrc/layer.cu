@@ -2,7 +2,9 @@
 // above. Forward follows Fig. 5; backward follows the operation
 // list of §5.1. No host synchronisation: data-dependent sizes live
 // in saved->topo.sizes on the device.
+#include "bsgemm.cuh"
 #include "common.cuh"
+#include "permute.cuh"
 
 using namespace moe;
 
@@ -44,8 +46,16 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   void* dx_g = wsb + L.dx_g;
   float* dgates = reinterpret_cast<float*>(wsb + L.dgates);
   const moe_topology_t* topo = &sv->topo;
+  const bool fused_router = router_on_tensor_cores(cfg);
+  __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(wsb + L.dlogits);
   // b1: dY_g = gates * dy (un-permuted rows), dgates = <Y_g, dy>
-  MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
+  //     [+ b7's dlogits = p * (dp - <p,dp>) in the same pass]
+  if (fused_router) {
+    MOE_TRY(moe_scatter_bwd_router(cfg, dy, sv->y_g, topo, sv->gates, sv->logits, sv->expert_idx, dy_g, dgates,
+                                   dl16, stream));
+  } else {
+    MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
+  }
   // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
   MOE_TRY(moe_sdd(cfg, dy_g, w->w2, 1, topo, id ? MOE_ACT_IDENTITY : cfg->act, id ? nullptr : sv->h_pre, dh,
                   nullptr, stream));
@@ -55,6 +65,11 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   MOE_TRY(moe_dsd(cfg, dh, 0, w->w1, 1, topo, dx_g, stream));
   // b5: DD^TS: dW1 = X_g^T . dH                              "first layer weight gradient"
   MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
+  if (fused_router) {
+    // b7: dWr = x^T . dlogits; b6+b7: dx = sum_j dX_g[pos[t*k+j]] + dlogits . Wr^T
+    MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
+    return moe_router_dx(cfg, dl16, w->wr, dx_g, topo, dx, stream);
+  }
   // b6: dx = sum_j dX_g[pos]
   MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
   // b7: router backward (dWr, dx += dlogits . Wr^T)

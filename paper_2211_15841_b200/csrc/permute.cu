@@ -4,39 +4,23 @@
 // §2.4) and their backward passes, plus the unpadded expert-order
 // permutation used for expert-parallel dispatch.
 //
-// All kernels are HBM-bandwidth bound row copies: one warp per output row,
-// 16-byte vector loads/stores, loads of a row issued before its stores,
-// grid-stride over rows with the device-side row count (no host sync).
+// All kernels are HBM-bandwidth-bound row copies. Design for latency: every
+// warp owns ROWS rows at once (ROWS = 8 / VEC, VEC = 16-byte vectors per lane
+// per row), loads all their indices with one coalesced load + shuffles, issues
+// all row loads, then all stores — 8 x 16 B in flight per lane. Copies are
+// input-driven (one index load per row); the zero pad rows of every expert
+// group are written by a second phase of the same kernel. Grid = SMs x 8 CTAs
+// of 8 warps, grid-stride, reading device-side sizes (no host sync).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <float.h>
 
 #include "common.cuh"
+#include "permute.cuh"
 
 namespace moe {
 
 constexpr int kWarpsPerCta = 8;
-constexpr int kMaxVec = 8;  // h <= 8 * 32 * 8 = 2048 elements per lane pass
-
-struct RowCtx {
-  const int32_t* counts;
-  const int32_t* bins;
-  const int32_t* padded_bins;
-  const int32_t* sorted_idx;
-  const int32_t* col_indices;
-  const int32_t* sizes;
-  int F, bs;
-};
-
-// Flat id (t*k+j) stored in padded row p, or -1 for a pad row.
-__device__ __forceinline__ int padded_row_source(const RowCtx& c, int p) {
-  const int r = p / c.bs;
-  const int e = __ldg(c.col_indices + (size_t)r * c.F) / c.F;
-  const int cnt = __ldg(c.counts + e);
-  const int pc = ((cnt + c.bs - 1) / c.bs) * c.bs;
-  const int rank = p - (__ldg(c.padded_bins + e) - pc);
-  if (rank >= cnt) return -1;
-  return __ldg(c.sorted_idx + __ldg(c.bins + e) - cnt + rank);
-}
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& w, float* f) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
@@ -55,153 +39,260 @@ __device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
   return w;
 }
 
-// x_g[p] = x[src(p)/k] or 0   (output-driven: every row of x_g written once)
-__global__ void gather_kernel(const uint4* __restrict__ x, uint4* __restrict__ xg, RowCtx c, int k, int vec) {
-  const int Tp = c.sizes[0];
+__device__ __forceinline__ int warp_global() { return (blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
+__device__ __forceinline__ int warps_total() { return (gridDim.x * blockDim.x) >> 5; }
+
+// Zero the pad rows of every expert group: rows [start_e + c_e, start_e + pc_e).
+template <int VEC>
+__device__ void zero_pad_rows(uint4* __restrict__ dst, const int32_t* __restrict__ counts,
+                              const int32_t* __restrict__ padded_bins, int E, int bs) {
   const int lane = threadIdx.x & 31;
-  for (int p = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); p < Tp; p += gridDim.x * kWarpsPerCta) {
-    const int i = padded_row_source(c, p);
-    uint4 v[kMaxVec];
-    if (i >= 0) {
-      const uint4* src = x + (size_t)(i / k) * vec;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int w = warp_global(); w < E * bs; w += warps_total()) {
+    const int e = w / bs, j = w - e * bs;
+    const int c = __ldg(counts + e);
+    const int pc = ((c + bs - 1) / bs) * bs;
+    if (j >= pc - c) continue;
+    uint4* row = dst + (size_t)(__ldg(padded_bins + e) - pc + c + j) * VEC * 32;
 #pragma unroll
-      for (int u = 0; u < kMaxVec; ++u)
-        if (lane + 32 * u < vec) v[u] = __ldg(src + lane + 32 * u);
-    } else {
-#pragma unroll
-      for (int u = 0; u < kMaxVec; ++u) v[u] = make_uint4(0, 0, 0, 0);
-    }
-    uint4* dst = xg + (size_t)p * vec;
-#pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
-      if (lane + 32 * u < vec) dst[lane + 32 * u] = v[u];
+    for (int u = 0; u < VEC; ++u) row[lane + 32 * u] = z;
   }
 }
 
-// y[t] = sum_j g[t,j] * rows[map[t*k+j]]  (fp32 accumulate, ascending j)
-__global__ void combine_kernel(const uint4* __restrict__ rows, const int32_t* __restrict__ map,
-                               const float* __restrict__ gates, uint4* __restrict__ y, int T, int k, int vec) {
+// dst[map[i]] = src[i / k] for i < R (rows of h = VEC*256 bf16); optional pad zeroing.
+template <int VEC>
+__global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ map,
+                                                            uint4* __restrict__ dst, int R, int k,
+                                                            const int32_t* __restrict__ counts,
+                                                            const int32_t* __restrict__ padded_bins, int E, int bs) {
+  constexpr int ROWS = 8 / VEC;
+  constexpr int RV = VEC * 32;  // uint4 per row
   const int lane = threadIdx.x & 31;
-  for (int t = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); t < T; t += gridDim.x * kWarpsPerCta) {
-    float acc[kMaxVec][8];
+  for (int base = warp_global() * ROWS; base < R; base += warps_total() * ROWS) {
+    const int my = base + lane;
+    const int midx = (lane < ROWS && my < R) ? __ldg(map + my) : -1;
+    uint4 v[ROWS][VEC];
 #pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
+    for (int r = 0; r < ROWS; ++r) {
+      const int i = base + r;
+      if (i < R) {
+        const uint4* s = src + (size_t)(i / k) * RV;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+        for (int u = 0; u < VEC; ++u) v[r][u] = __ldg(s + lane + 32 * u);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int d = __shfl_sync(0xffffffffu, midx, r);
+      if (base + r < R) {
+        uint4* o = dst + (size_t)d * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) o[lane + 32 * u] = v[r][u];
+      }
+    }
+  }
+  if (counts) zero_pad_rows<VEC>(dst, counts, padded_bins, E, bs);
+}
+
+// y[t] = sum_{j ascending} g[t,j] * rows[map[t*k+j]]   (fp32 accumulate, bf16 out)
+template <int VEC>
+__global__ void __launch_bounds__(256) combine_kernel(const uint4* __restrict__ rows, const int32_t* __restrict__ map,
+                                                       const float* __restrict__ gates, uint4* __restrict__ y, int T,
+                                                       int k) {
+  constexpr int ROWS = 8 / VEC;
+  constexpr int RV = VEC * 32;
+  const int lane = threadIdx.x & 31;
+  for (int base = warp_global() * ROWS; base < T; base += warps_total() * ROWS) {
+    float acc[ROWS][VEC][8];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+      for (int u = 0; u < VEC; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[r][u][q] = 0.f;
     for (int j = 0; j < k; ++j) {
-      const int i = t * k + j;
-      const float g = gates ? __ldg(gates + i) : 1.0f;
-      const uint4* src = rows + (size_t)__ldg(map + i) * vec;
+      const int t_l = base + lane;
+      const bool lv = lane < ROWS && t_l < T;
+      const int midx = lv ? __ldg(map + (size_t)t_l * k + j) : 0;
+      const float g = (lv && gates) ? __ldg(gates + (size_t)t_l * k + j) : 1.0f;
+      uint4 v[ROWS][VEC];
 #pragma unroll
-      for (int u = 0; u < kMaxVec; ++u) {
-        if (lane + 32 * u < vec) {
-          float f[8];
-          bf16x8_to_f32(__ldg(src + lane + 32 * u), f);
+      for (int r = 0; r < ROWS; ++r) {
+        const int m = __shfl_sync(0xffffffffu, midx, r);
+        if (base + r < T) {
+          const uint4* s = rows + (size_t)m * RV;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[u][q] = fmaf(g, f[q], acc[u][q]);
+          for (int u = 0; u < VEC; ++u) v[r][u] = __ldg(s + lane + 32 * u);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        const float gr = __shfl_sync(0xffffffffu, g, r);
+        if (base + r < T) {
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) {
+            float f[8];
+            bf16x8_to_f32(v[r][u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[r][u][q] = fmaf(gr, f[q], acc[r][u][q]);
+          }
         }
       }
     }
-    uint4* dst = y + (size_t)t * vec;
 #pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
-      if (lane + 32 * u < vec) dst[lane + 32 * u] = f32_to_bf16x8(acc[u]);
+    for (int r = 0; r < ROWS; ++r) {
+      if (base + r < T) {
+        uint4* o = y + (size_t)(base + r) * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) o[lane + 32 * u] = f32_to_bf16x8(acc[r][u]);
+      }
+    }
   }
 }
 
-// dy_g[p] = g * dy[t] (0 for pad rows); dgates[i] = <y_g[p], dy[t]>.
-// Output-driven over padded rows when `padded`, else over sorted rows u < R.
-__global__ void scatter_bwd_kernel(const uint4* __restrict__ dy, const uint4* __restrict__ yg, RowCtx c,
-                                   const float* __restrict__ gates, uint4* __restrict__ dyg, float* __restrict__ dgates,
-                                   int k, int vec, int padded, int R) {
+// Per token t (one warp): dy_rows[map[i]] = g_i * dy[t]; dgates[i] = <y_rows[map[i]], dy[t]>,
+// i = t*k + j. Optionally fused router backward (P:98 softmax chain rule):
+// dlogits[t,:] = p * (dp - <p,dp>), p = softmax(logits[t,:]), dp[e] = sum_{j: idx_j = e} dgates_j.
+template <int VEC>
+__global__ void __launch_bounds__(256) scatter_bwd_kernel(
+    const uint4* __restrict__ dy, const uint4* __restrict__ y_rows, const int32_t* __restrict__ map,
+    const float* __restrict__ gates, uint4* __restrict__ dy_rows, float* __restrict__ dgates, int T, int k,
+    const float* __restrict__ logits, const int32_t* __restrict__ expert_idx, int E,
+    __nv_bfloat16* __restrict__ dlogits_bf16, float* __restrict__ dlogits_f32, const int32_t* __restrict__ counts,
+    const int32_t* __restrict__ padded_bins, int bs) {
+  constexpr int RV = VEC * 32;
   const int lane = threadIdx.x & 31;
-  const int nrows = padded ? c.sizes[0] : R;
-  for (int p = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); p < nrows; p += gridDim.x * kWarpsPerCta) {
-    const int i = padded ? padded_row_source(c, p) : __ldg(c.sorted_idx + p);
-    uint4* dst = dyg + (size_t)p * vec;
-    if (i < 0) {
+  const bool want_dg = dgates != nullptr;
+  for (int t = warp_global(); t < T; t += warps_total()) {
+    uint4 d[VEC];
+    const uint4* ds = dy + (size_t)t * RV;
 #pragma unroll
-      for (int u = 0; u < kMaxVec; ++u)
-        if (lane + 32 * u < vec) dst[lane + 32 * u] = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const float g = gates ? __ldg(gates + i) : 1.0f;
-    const uint4* d = dy + (size_t)(i / k) * vec;
-    const uint4* yr = yg + (size_t)p * vec;
-    uint4 dv[kMaxVec], yv[kMaxVec];
+    for (int u = 0; u < VEC; ++u) d[u] = __ldg(ds + lane + 32 * u);
+    float df[VEC][8];
 #pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
-      if (lane + 32 * u < vec) {
-        dv[u] = __ldg(d + lane + 32 * u);
-        if (dgates) yv[u] = __ldg(yr + lane + 32 * u);
+    for (int u = 0; u < VEC; ++u) bf16x8_to_f32(d[u], df[u]);
+    const int midx = lane < k ? __ldg(map + (size_t)t * k + lane) : 0;
+    const float gl = lane < k ? (gates ? __ldg(gates + (size_t)t * k + lane) : 1.0f) : 0.f;
+    float dg_lane = 0.f;  // lane j holds dgates[t, j]
+    for (int j = 0; j < k; ++j) {
+      const int m = __shfl_sync(0xffffffffu, midx, j);
+      const float g = __shfl_sync(0xffffffffu, gl, j);
+      uint4 yv[VEC];
+      if (want_dg) {
+        const uint4* ys = y_rows + (size_t)m * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) yv[u] = __ldg(ys + lane + 32 * u);
       }
-    float dot = 0.f;
+      uint4* o = dy_rows + (size_t)m * RV;
 #pragma unroll
-    for (int u = 0; u < kMaxVec; ++u) {
-      if (lane + 32 * u < vec) {
-        float fd[8];
-        bf16x8_to_f32(dv[u], fd);
-        if (dgates) {
+      for (int u = 0; u < VEC; ++u) {
+        float f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = g * df[u][q];
+        o[lane + 32 * u] = f32_to_bf16x8(f);
+      }
+      if (want_dg) {
+        float dot = 0.f;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) {
           float fy[8];
           bf16x8_to_f32(yv[u], fy);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) dot = fmaf(fy[q], fd[q], dot);
+          for (int q = 0; q < 8; ++q) dot = fmaf(fy[q], df[u][q], dot);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) fd[q] *= g;
-        dst[lane + 32 * u] = f32_to_bf16x8(fd);
+        for (int o2 = 16; o2 > 0; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+        if (lane == j) dg_lane = dot;
       }
     }
-    if (dgates) {
+    if (want_dg && lane < k) dgates[(size_t)t * k + lane] = dg_lane;
+    if (logits && (dlogits_bf16 || dlogits_f32)) {  // E <= 256 (checked on the host)
+      const float* row = logits + (size_t)t * E;
+      float lv[8];
+      float m = -FLT_MAX;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (lane == 0) dgates[i] = dot;
+      for (int q = 0; q < 8; ++q) {
+        const int e = lane + 32 * q;
+        lv[q] = e < E ? row[e] : -FLT_MAX;
+        m = fmaxf(m, lv[q]);
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o2));
+      float ssum = 0.f, pv[8], dpl[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        pv[q] = lane + 32 * q < E ? __expf(lv[q] - m) : 0.f;
+        ssum += pv[q];
+        dpl[q] = 0.f;
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o2);
+      const float inv = 1.f / ssum;
+      const int ej = lane < k ? __ldg(expert_idx + (size_t)t * k + lane) : -1;
+      float pdp = 0.f;
+      for (int j = 0; j < k; ++j) {  // warp-uniform
+        const int ejj = __shfl_sync(0xffffffffu, ej, j);
+        const float dgj = __shfl_sync(0xffffffffu, dg_lane, j);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (lane + 32 * q == ejj) {
+            dpl[q] += dgj;
+            pdp += pv[q] * inv * dgj;
+          }
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) pdp += __shfl_xor_sync(0xffffffffu, pdp, o2);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = lane + 32 * q;
+        if (e < E) {
+          const float dl = pv[q] * inv * (dpl[q] - pdp);
+          if (dlogits_bf16)
+            dlogits_bf16[(size_t)t * E + e] = __float2bfloat16_rn(dl);
+          else
+            dlogits_f32[(size_t)t * E + e] = dl;
+        }
+      }
     }
   }
+  if (counts) zero_pad_rows<VEC>(dy_rows, counts, padded_bins, E, bs);
 }
 
-// dst[u] = src[sorted_idx[u] / k], u < R   (unpadded expert-order permutation)
-__global__ void sort_rows_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ sorted_idx,
-                                 uint4* __restrict__ out, int R, int k, int vec) {
-  const int lane = threadIdx.x & 31;
-  for (int u0 = blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5); u0 < R; u0 += gridDim.x * kWarpsPerCta) {
-    const uint4* src = x + (size_t)(__ldg(sorted_idx + u0) / k) * vec;
-    uint4 v[kMaxVec];
-#pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
-      if (lane + 32 * u < vec) v[u] = __ldg(src + lane + 32 * u);
-    uint4* dst = out + (size_t)u0 * vec;
-#pragma unroll
-    for (int u = 0; u < kMaxVec; ++u)
-      if (lane + 32 * u < vec) dst[lane + 32 * u] = v[u];
-  }
-}
-
-static int row_grid(int64_t rows) {
-  int64_t g = ceil_div(rows > 0 ? rows : 1, kWarpsPerCta);
-  const int64_t cap = (int64_t)moe_device_sm_count() * 16;
-  return (int)(g < cap ? g : cap);
-}
-
-static RowCtx row_ctx(const moe_config* cfg, const moe_topology_t* t) {
-  RowCtx c;
-  c.counts = t->counts;
-  c.bins = t->bins;
-  c.padded_bins = t->padded_bins;
-  c.sorted_idx = t->sorted_idx;
-  c.col_indices = t->col_indices;
-  c.sizes = t->sizes;
-  c.F = (int)(cfg->ffn_hidden / cfg->block_size);
-  c.bs = (int)cfg->block_size;
-  return c;
-}
+static int row_grid() { return moe_device_sm_count() * 8; }
 
 static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, const char* name) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
-  if (cfg->hidden % 8 || cfg->hidden > 8 * 32 * kMaxVec)
-    return set_error(MOE_EUNSUPPORTED, "%s: hidden=%lld must be a multiple of 8 and <= %d", name,
-                     (long long)cfg->hidden, 8 * 32 * kMaxVec);
+  if (cfg->hidden % 256 || cfg->hidden > 2048)
+    return set_error(MOE_EUNSUPPORTED, "%s: hidden=%lld must be a multiple of 256 and <= 2048", name,
+                     (long long)cfg->hidden);
+  return MOE_OK;
+}
+
+#define MOE_VEC_DISPATCH(VEC_EXPR, KERNEL, ...)                                                         \
+  switch (VEC_EXPR) {                                                                                   \
+    case 1: KERNEL<1><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 2: KERNEL<2><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 3: KERNEL<3><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 4: KERNEL<4><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 5: KERNEL<5><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 6: KERNEL<6><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    case 7: KERNEL<7><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
+    default: KERNEL<8><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                    \
+  }
+
+moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* y_rows, const int32_t* map,
+                             const float* gates, void* dy_rows, float* dgates, const float* logits,
+                             const int32_t* expert_idx, __nv_bfloat16* dlogits_bf16, float* dlogits_f32,
+                             const moe_topology_t* pad_topo, cudaStream_t s) {
+  const int vec = (int)(cfg->hidden / 256);
+  const int T = (int)cfg->tokens, k = (int)cfg->top_k, E = (int)cfg->num_experts, bs = (int)cfg->block_size;
+  const int32_t* counts = pad_topo ? pad_topo->counts : nullptr;
+  const int32_t* pbins = pad_topo ? pad_topo->padded_bins : nullptr;
+  MOE_VEC_DISPATCH(vec, scatter_bwd_kernel, reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows),
+                   map, gates, reinterpret_cast<uint4*>(dy_rows), dgates, T, k, logits, expert_idx, E, dlogits_bf16,
+                   dlogits_f32, counts, pbins, bs);
+  MOE_CHECK_LAUNCH("scatter_bwd");
   return MOE_OK;
 }
 
@@ -214,9 +305,11 @@ extern "C" {
 moe_status moe_gather(const moe_config* cfg, const void* x, const moe_topology_t* topo, void* x_g, void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_gather"));
   MOE_CHECK_ARG(x && x_g, "moe_gather: NULL pointer");
-  const int vec = (int)(cfg->hidden / 8);
-  gather_kernel<<<row_grid(moe_max_padded_rows(cfg)), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(x), reinterpret_cast<uint4*>(x_g), row_ctx(cfg, topo), (int)cfg->top_k, vec);
+  cudaStream_t s = as_stream(stream);
+  const int R = (int)(cfg->tokens * cfg->top_k);
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->pos,
+                   reinterpret_cast<uint4*>(x_g), R, (int)cfg->top_k, topo->counts, topo->padded_bins,
+                   (int)cfg->num_experts, (int)cfg->block_size);
   MOE_CHECK_LAUNCH("moe_gather");
   return MOE_OK;
 }
@@ -225,10 +318,9 @@ moe_status moe_scatter(const moe_config* cfg, const void* y_g, const moe_topolog
                        void* y, void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_scatter"));
   MOE_CHECK_ARG(y_g && y, "moe_scatter: NULL pointer");
-  const int T = (int)cfg->tokens;
-  combine_kernel<<<row_grid(T), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(y_g), topo->pos, gates, reinterpret_cast<uint4*>(y), T, (int)cfg->top_k,
-      (int)(cfg->hidden / 8));
+  cudaStream_t s = as_stream(stream);
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(y_g), topo->pos, gates,
+                   reinterpret_cast<uint4*>(y), (int)cfg->tokens, (int)cfg->top_k);
   MOE_CHECK_LAUNCH("moe_scatter");
   return MOE_OK;
 }
@@ -237,21 +329,17 @@ moe_status moe_scatter_bwd(const moe_config* cfg, const void* dy, const void* y_
                            const float* gates, void* dy_g, float* dgates, void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_scatter_bwd"));
   MOE_CHECK_ARG(dy && dy_g && (y_g || !dgates), "moe_scatter_bwd: NULL pointer");
-  scatter_bwd_kernel<<<row_grid(moe_max_padded_rows(cfg)), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_g), row_ctx(cfg, topo), gates,
-      reinterpret_cast<uint4*>(dy_g), dgates, (int)cfg->top_k, (int)(cfg->hidden / 8), 1, 0);
-  MOE_CHECK_LAUNCH("moe_scatter_bwd");
-  return MOE_OK;
+  return scatter_bwd_fused(cfg, dy, y_g, topo->pos, gates, dy_g, dgates, nullptr, nullptr, nullptr, nullptr, topo,
+                           as_stream(stream));
 }
 
 moe_status moe_gather_bwd(const moe_config* cfg, const void* dx_g, const moe_topology_t* topo, void* dx,
                           void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_gather_bwd"));
   MOE_CHECK_ARG(dx_g && dx, "moe_gather_bwd: NULL pointer");
-  const int T = (int)cfg->tokens;
-  combine_kernel<<<row_grid(T), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(dx_g), topo->pos, nullptr, reinterpret_cast<uint4*>(dx), T, (int)cfg->top_k,
-      (int)(cfg->hidden / 8));
+  cudaStream_t s = as_stream(stream);
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(dx_g), topo->pos, nullptr,
+                   reinterpret_cast<uint4*>(dx), (int)cfg->tokens, (int)cfg->top_k);
   MOE_CHECK_LAUNCH("moe_gather_bwd");
   return MOE_OK;
 }
@@ -260,10 +348,10 @@ moe_status moe_sort_rows(const moe_config* cfg, const void* x, const moe_topolog
                          void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_sort_rows"));
   MOE_CHECK_ARG(x && x_sorted, "moe_sort_rows: NULL pointer");
+  cudaStream_t s = as_stream(stream);
   const int R = (int)(cfg->tokens * cfg->top_k);
-  sort_rows_kernel<<<row_grid(R), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(x), topo->sorted_idx, reinterpret_cast<uint4*>(x_sorted), R, (int)cfg->top_k,
-      (int)(cfg->hidden / 8));
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->sorted_pos,
+                   reinterpret_cast<uint4*>(x_sorted), R, (int)cfg->top_k, nullptr, nullptr, 0, 1);
   MOE_CHECK_LAUNCH("moe_sort_rows");
   return MOE_OK;
 }
@@ -272,10 +360,9 @@ moe_status moe_unsort_rows(const moe_config* cfg, const void* y_sorted, const mo
                            const float* gates, void* y, void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_unsort_rows"));
   MOE_CHECK_ARG(y_sorted && y, "moe_unsort_rows: NULL pointer");
-  const int T = (int)cfg->tokens;
-  combine_kernel<<<row_grid(T), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(y_sorted), topo->sorted_pos, gates, reinterpret_cast<uint4*>(y), T,
-      (int)cfg->top_k, (int)(cfg->hidden / 8));
+  cudaStream_t s = as_stream(stream);
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(y_sorted),
+                   topo->sorted_pos, gates, reinterpret_cast<uint4*>(y), (int)cfg->tokens, (int)cfg->top_k);
   MOE_CHECK_LAUNCH("moe_unsort_rows");
   return MOE_OK;
 }
@@ -284,12 +371,8 @@ moe_status moe_unsort_rows_bwd(const moe_config* cfg, const void* dy, const void
                                const float* gates, void* dy_sorted, float* dgates, void* stream) {
   MOE_TRY(check_rows(cfg, topo, "moe_unsort_rows_bwd"));
   MOE_CHECK_ARG(dy && dy_sorted && (y_sorted || !dgates), "moe_unsort_rows_bwd: NULL pointer");
-  const int R = (int)(cfg->tokens * cfg->top_k);
-  scatter_bwd_kernel<<<row_grid(R), 32 * kWarpsPerCta, 0, as_stream(stream)>>>(
-      reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_sorted), row_ctx(cfg, topo), gates,
-      reinterpret_cast<uint4*>(dy_sorted), dgates, (int)cfg->top_k, (int)(cfg->hidden / 8), 0, R);
-  MOE_CHECK_LAUNCH("moe_unsort_rows_bwd");
-  return MOE_OK;
+  return scatter_bwd_fused(cfg, dy, y_sorted, topo->sorted_pos, gates, dy_sorted, dgates, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, as_stream(stream));
 }
 
 moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo, void* dx,

@@ -10,6 +10,7 @@
 
 #include "bsgemm.cuh"
 #include "common.cuh"
+#include "permute.cuh"
 #include "tma.cuh"
 
 namespace moe {
@@ -217,6 +218,74 @@ __global__ void __launch_bounds__(256) router_dx_kernel(const float* __restrict_
 
 }  // namespace moe
 
+namespace moe {
+
+// dWr = x^T . dlogits on tcgen05 (M = h, N = E, K = T split over `parts`
+// token ranges into fp32 partials, then a fixed-order reduction).
+moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat16* dlogits, float* dwr, void* ws,
+                         cudaStream_t s) {
+  const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
+  const int parts = router_bwd_parts(cfg);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + ws_layout(cfg).dwr_part);
+  GemmLaunch L{};
+  L.name = "router dWr";
+  L.mode = DENSE;
+  L.bn = E;
+  L.a_mn = true;
+  L.b_mn = true;
+  L.p.m_tiles = (int)ceil_div(h, 128);
+  L.p.n_tiles = 1;
+  L.p.splits = parts;
+  L.p.k_iters_total = (int)ceil_div(T, 64);
+  L.p.kiters_split = (int)ceil_div(L.p.k_iters_total, parts);
+  L.p.epi = EPI_F32;
+  L.p.rows_valid = h;
+  L.p.out_f32 = part;
+  L.p.ld_f32 = E;
+  L.p.split_stride = (long long)h * E;
+  L.max_tiles = parts * L.p.m_tiles;
+  MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 64, "router dWr x^T"));
+  MOE_TRY(make_tmap_bf16(&L.tb, dlogits, E, T, E, 64, 64, "router dWr dlogits"));
+  L.tc = L.td = L.ta;
+  MOE_TRY(gemm_launch(L, s));
+  router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
+  MOE_CHECK_LAUNCH("router_dwr_reduce");
+  return MOE_OK;
+}
+
+// dx = dlogits . Wr^T + addend on tcgen05 (M = T, N = h, K = E); the addend is
+// the row t of `addend` or, with addend_map, sum_j addend[addend_map[t*k+j]]
+// (the padded-gather backward fused into the epilogue).
+moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, const void* wr, void* dx,
+                        const void* addend, const int32_t* addend_map, int addend_k, long long ld_add,
+                        cudaStream_t s) {
+  const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
+  GemmLaunch D{};
+  D.name = "router dx";
+  D.mode = DENSE;
+  D.bn = h % 256 == 0 ? 256 : 128;
+  D.a_mn = false;
+  D.b_mn = false;
+  D.p.m_tiles = (int)ceil_div(T, 128);
+  D.p.n_tiles = h / D.bn;
+  D.p.splits = 1;
+  D.p.k_iters_total = D.p.kiters_split = E / 64;
+  D.p.epi = EPI_ADD_ROWS;
+  D.p.rows_valid = T;
+  D.p.addend = reinterpret_cast<const __nv_bfloat16*>(addend);
+  D.p.ld_add = ld_add;
+  D.p.addend_map = addend_map;
+  D.p.addend_k = addend_k;
+  D.max_tiles = D.p.m_tiles * D.p.n_tiles;
+  MOE_TRY(make_tmap_bf16(&D.ta, dlogits, E, T, E, 64, 128, "router dx dlogits"));
+  MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, 64, D.bn, "router dx wr"));
+  MOE_TRY(make_tmap_epi(&D.tc, dx, h, T, h, "router dx out"));
+  D.td = D.tc;
+  return gemm_launch(D, s);
+}
+
+}  // namespace moe
+
 using namespace moe;
 
 extern "C" {
@@ -287,51 +356,8 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
     __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(dlogits);
     router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, nullptr, dl16, T, E, k);
     MOE_CHECK_LAUNCH("router_dlogits");
-    // dWr partials = x^T . dlogits, split over tokens (M = h, N = E, K = T)
-    GemmLaunch L{};
-    L.name = "moe_router_bwd dWr";
-    L.mode = DENSE;
-    L.bn = E;
-    L.a_mn = true;
-    L.b_mn = true;
-    L.p.m_tiles = (int)ceil_div(h, 128);
-    L.p.n_tiles = 1;
-    L.p.splits = parts;
-    L.p.k_iters_total = (int)ceil_div(T, 64);
-    L.p.kiters_split = (int)ceil_div(L.p.k_iters_total, parts);
-    L.p.epi = EPI_F32;
-    L.p.rows_valid = h;
-    L.p.out_f32 = part;
-    L.p.ld_f32 = E;
-    L.p.split_stride = (long long)h * E;
-    L.max_tiles = parts * L.p.m_tiles;
-    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 64, "router_bwd x^T"));
-    MOE_TRY(make_tmap_bf16(&L.tb, dl16, E, T, E, 64, 64, "router_bwd dlogits"));
-    L.tc = L.td = L.ta;
-    MOE_TRY(gemm_launch(L, s));
-    router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
-    MOE_CHECK_LAUNCH("router_dwr_reduce");
-    // dx += dlogits . Wr^T (M = T, N = h, K = E), read-modify-write through the epilogue
-    GemmLaunch D{};
-    D.name = "moe_router_bwd dx";
-    D.mode = DENSE;
-    D.bn = h % 256 == 0 ? 256 : 128;
-    D.a_mn = false;
-    D.b_mn = false;
-    D.p.m_tiles = (int)ceil_div(T, 128);
-    D.p.n_tiles = h / D.bn;
-    D.p.splits = 1;
-    D.p.k_iters_total = D.p.kiters_split = E / 64;
-    D.p.epi = EPI_ADD_ROWS;
-    D.p.rows_valid = T;
-    D.p.addend = reinterpret_cast<const __nv_bfloat16*>(dx);
-    D.p.ld_add = h;
-    D.max_tiles = D.p.m_tiles * D.p.n_tiles;
-    MOE_TRY(make_tmap_bf16(&D.ta, dl16, E, T, E, 64, 128, "router_bwd dlogits"));
-    MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, 64, D.bn, "router_bwd wr"));
-    MOE_TRY(make_tmap_epi(&D.tc, dx, h, T, h, "router_bwd dx"));
-    D.td = D.tc;
-    return gemm_launch(D, s);
+    MOE_TRY(router_dwr_tc(cfg, x, dl16, dwr, ws, s));
+    return router_dx_tc(cfg, dl16, wr, dx, dx, nullptr, 1, h, s);  // dx += dlogits . Wr^T (in place)
   }
   router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, dlogits, nullptr, T, E, k);
   MOE_CHECK_LAUNCH("router_dlogits");
@@ -347,6 +373,43 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
                                                           reinterpret_cast<__nv_bfloat16*>(dx), T, h, E);
   MOE_CHECK_LAUNCH("router_dx");
   return MOE_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+moe_status moe_scatter_bwd_router(const moe_config* cfg, const void* dy, const void* y_g, const moe_topology_t* topo,
+                                  const float* gates, const float* logits, const int32_t* expert_idx, void* dy_g,
+                                  float* dgates, void* dlogits_bf16, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(dy && y_g && gates && logits && expert_idx && dy_g && dgates && dlogits_bf16,
+                "moe_scatter_bwd_router: NULL pointer");
+  if (!router_on_tensor_cores(cfg))
+    return set_error(MOE_EUNSUPPORTED, "moe_scatter_bwd_router: needs E %% 64 == 0, E <= 256, top_k <= 8");
+  return scatter_bwd_fused(cfg, dy, y_g, topo->pos, gates, dy_g, dgates, logits, expert_idx,
+                           reinterpret_cast<__nv_bfloat16*>(dlogits_bf16), nullptr, topo, as_stream(stream));
+}
+
+moe_status moe_router_dwr(const moe_config* cfg, const void* x, const void* dlogits_bf16, float* dwr, void* ws,
+                          void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(x && dlogits_bf16 && dwr && ws, "moe_router_dwr: NULL pointer");
+  if (!router_on_tensor_cores(cfg))
+    return set_error(MOE_EUNSUPPORTED, "moe_router_dwr: needs E %% 64 == 0, E <= 256, top_k <= 8");
+  return router_dwr_tc(cfg, x, reinterpret_cast<const __nv_bfloat16*>(dlogits_bf16), dwr, ws, as_stream(stream));
+}
+
+moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const void* wr, const void* dx_g,
+                         const moe_topology_t* topo, void* dx, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(dlogits_bf16 && wr && dx_g && dx, "moe_router_dx: NULL pointer");
+  if (!router_on_tensor_cores(cfg))
+    return set_error(MOE_EUNSUPPORTED, "moe_router_dx: needs E %% 64 == 0, E <= 256, top_k <= 8");
+  return router_dx_tc(cfg, reinterpret_cast<const __nv_bfloat16*>(dlogits_bf16), wr, dx, dx_g, topo->pos,
+                      (int)cfg->top_k, cfg->hidden, as_stream(stream));
 }
 
 }  // extern "C"

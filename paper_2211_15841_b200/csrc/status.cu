@@ -120,8 +120,8 @@ moe_status moe_check_config(const moe_config* cfg) {
   if (cfg->block_size != 128)
     return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
                      (long long)cfg->block_size);
-  if (cfg->hidden % 128)
-    return set_error(MOE_EUNSUPPORTED, "hidden=%lld must be a multiple of 128 on the GPU path",
+  if (cfg->hidden % 256 || cfg->hidden > 2048)
+    return set_error(MOE_EUNSUPPORTED, "hidden=%lld must be a multiple of 256 and <= 2048 on the GPU path",
                      (long long)cfg->hidden);
   if (cfg->num_experts > 1024)
     return set_error(MOE_EUNSUPPORTED, "num_experts=%lld > 1024", (long long)cfg->num_experts);
@@ -145,6 +145,19 @@ int64_t moe_max_nnz_blocks(const moe_config* cfg) {
 size_t moe_workspace_bytes(const moe_config* cfg) {
   if (!cfg) return 0;
   return ws_layout(cfg).total;
+}
+
+size_t moe_workspace_offset(const moe_config* cfg, int which) {
+  if (!cfg) return (size_t)-1;
+  const WsLayout L = ws_layout(cfg);
+  switch (which) {
+    case 0: return L.dy_g;
+    case 1: return L.dh;
+    case 2: return L.dx_g;
+    case 3: return L.dgates;
+    case 4: return L.dlogits;
+    default: return (size_t)-1;
+  }
 }
 
 int moe_device_sm_count(void) {

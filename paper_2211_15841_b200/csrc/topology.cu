@@ -75,10 +75,15 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
   // (1) per-expert exclusive scan over chunks (chunk_counts becomes chunk base rank)
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
-    for (int c = 0; c < n_chunks; ++c) {
-      int32_t v = chunk_counts[(size_t)c * E + e];
-      chunk_counts[(size_t)c * E + e] = run;
-      run += v;
+    for (int c0 = 0; c0 < n_chunks; c0 += 16) {
+      int32_t v[16];  // batch the loads so they are in flight together
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = c0 + u < n_chunks ? chunk_counts[(size_t)(c0 + u) * E + e] : 0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (c0 + u < n_chunks) chunk_counts[(size_t)(c0 + u) * E + e] = run;
+        run += v[u];
+      }
     }
     s_counts[e] = run;
     s_pad[e] = ((run + bs - 1) / bs) * bs;

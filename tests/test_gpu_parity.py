@@ -72,7 +72,7 @@ def test_topk_bit_exact(T, E, k, ties):
     d = dev()
     A = api()
     logits = S.random_logits(T, E, seed=T + E, ties=ties)
-    cfg = A.make_config(T, 128, E, k, 128)
+    cfg = A.make_config(T, 256, E, k, 128)
     idx, gates = A.moe_topk(cfg, logits.to(d))
     want_idx, want_g = O.topk(S.to_f64(logits), k)
     np.testing.assert_array_equal(idx.cpu().numpy(), want_idx)
@@ -150,7 +150,7 @@ def test_topology_bit_exact(T, E, k, f, zipf):
     d = dev()
     A = api()
     idx = S.random_expert_idx(T, E, k, seed=T, zipf=zipf)
-    cfg = A.make_config(T, 128, E, k, f)
+    cfg = A.make_config(T, 256, E, k, f)
     topo = A.moe_topology(cfg, idx.to(d))
     plan, otopo = oracle_plan_topo(idx.numpy(), E, f)
     check_topology_exact(A, topo, plan, otopo, T * k)
@@ -160,7 +160,7 @@ def test_topology_deterministic_repeat():
     d = dev()
     A = api()
     idx = S.random_expert_idx(30000, 64, 2, seed=9, zipf=0.5).to(d)
-    cfg = A.make_config(30000, 128, 64, 2, 512)
+    cfg = A.make_config(30000, 256, 64, 2, 512)
     t1 = A.moe_topology(cfg, idx)
     t2 = A.moe_topology(cfg, idx)
     Tp, nnz = t1.sizes()
