@@ -114,7 +114,9 @@ typedef struct {
   int32_t* t_block_offsets; /* [max_nnz]          storage index of each block, in (col,row)
                                                   order: the transpose index          */
   int32_t* t_row_indices;   /* [max_nnz]          row of each block in transposed order      */
-  int32_t* sizes;           /* [2] = {Tp, nnz}, written on the device                        */
+  int32_t* pair_bins;       /* [E]  inclusive cumsum of ceil(block_rows_e / 2): pairs of
+                                    same-expert block-rows (2-SM tiles of the GEMMs)          */
+  int32_t* sizes;           /* [3] = {Tp, nnz, row pairs}, written on the device             */
 } moe_topology_t;
 
 /* Router, §2.1: logits = x . wr (fp32 accumulate of bf16 inputs),

@@ -22,7 +22,7 @@ class MoeConfig(ctypes.Structure):
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",
-               "col_indices", "row_indices", "t_col_offsets", "t_block_offsets", "t_row_indices", "sizes"]
+               "col_indices", "row_indices", "t_col_offsets", "t_block_offsets", "t_row_indices", "pair_bins", "sizes"]
 
 
 class MoeTopology(ctypes.Structure):

@@ -63,7 +63,7 @@ class Topology:
         F = cfg.ffn_hidden // bs
         shapes = {"counts": E, "bins": E, "padded_bins": E, "sorted_idx": R, "pos": R, "sorted_pos": R,
                   "row_offsets": rows // bs + 1, "col_indices": nnz, "row_indices": nnz,
-                  "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "sizes": 2}
+                  "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "pair_bins": E, "sizes": 3}
         self.t = {n: torch.empty(max(int(shapes[n]), 1), dtype=torch.int32, device=device) for n in TOPO_FIELDS}
         self.struct = MoeTopology(*[self.t[n].data_ptr() for n in TOPO_FIELDS])
 

@@ -31,8 +31,10 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include "bsgemm.cuh"
+#include "gemm_util.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"
@@ -40,18 +42,6 @@
 namespace moe {
 
 using namespace sm100;
-
-constexpr int BM = 128;
-constexpr int BK = 64;
-constexpr int NUM_EPI_WARPS = 8;                  // 2 per TMEM lane quarter (column halves)
-constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int EPI_COLS = 32;                      // epilogue chunk: 32 rows x 32 columns per warp
-constexpr int EPI_BUF = 32 * EPI_COLS * 2;        // one warp's chunk, bf16, 64B-swizzled rows
-constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF;  // double buffered
-constexpr int SMEM_LIMIT = 232448;                // 227 KB opt-in
-constexpr int SMEM_FIXED = 1024 + 512;            // alignment slack + barriers
-constexpr int kMaxRouterTopK = 8;
 
 template <int BN, bool EPI_H>
 struct Cfg {
@@ -119,35 +109,6 @@ __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pa
   return t;
 }
 
-// tanh on the SFU (MUFU.TANH, max rel. error ~2^-11, below the bf16 output ulp)
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// gelu, tanh approximation (reading R2): 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
-__device__ __forceinline__ float act_fwd(int kind, float x) {
-  if (kind == MOE_ACT_GELU_TANH) {
-    const float x2 = x * x;
-    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
-    const float hx = 0.5f * x;
-    return fmaf(hx, tanh_fast(u), hx);
-  }
-  if (kind == MOE_ACT_RELU) return x > 0.f ? x : 0.f;
-  return x;
-}
-__device__ __forceinline__ float act_grad(int kind, float x) {
-  if (kind == MOE_ACT_GELU_TANH) {
-    const float x2 = x * x;
-    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
-    const float t = tanh_fast(u);
-    const float du = fmaf(0.7978845608028654f * 3.0f * 0.044715f, x2, 0.7978845608028654f);
-    return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), 0.5f * (1.0f + t));
-  }
-  if (kind == MOE_ACT_RELU) return x > 0.f ? 1.f : 0.f;
-  return 1.f;
-}
-
 // TMA coordinates (inner column, outer row) of the 64-column chunk `c` of the
 // output tile, for the epilogue warp whose rows start at `row0` in the tile.
 __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const TileInfo& t, int c, int row0,
@@ -165,31 +126,6 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
     case DDS_COL: x = t.u * 128 + col; y = t.v * BM + row0; break;
     case DDS_ROW: x = t.u * 128 + col; y = t.v * BM + row0; break;
     default: x = t.v * BN + col; y = t.u * BM + row0; break;  // DENSE
-  }
-}
-
-__device__ __forceinline__ void unpack8(const uint4& w, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 v = __bfloat1622float2(h[i]);
-    f[2 * i] = v.x;
-    f[2 * i + 1] = v.y;
-  }
-}
-
-// 64B swizzle (TMA SWIZZLE_64B): 16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3).
-__device__ __forceinline__ int swz64(int j, int row) { return (j ^ ((row >> 1) & 3)) << 4; }
-
-// Write 32 fp32 values of this thread's row as bf16 into a 64B-swizzled
-// [32 rows][64 B] staging buffer (row = lane): conflict-free 16-byte stores.
-__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
-  uint8_t* row = buf + lane * 64;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint4 w = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-    *reinterpret_cast<uint4*>(row + swz64(j, lane)) = w;
   }
 }
 
@@ -682,6 +618,10 @@ GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo) {
   p.t_col_offsets = topo->t_col_offsets;
   p.t_block_offsets = topo->t_block_offsets;
   p.t_row_indices = topo->t_row_indices;
+  p.pair_bins = topo->pair_bins;
+  p.padded_bins = topo->padded_bins;
+  p.F = (int)(cfg->ffn_hidden / cfg->block_size);
+  p.E = (int)cfg->num_experts;
   p.n_block_cols = (int)(cfg->num_experts * cfg->ffn_hidden / cfg->block_size);
   p.k_dense = (int)cfg->hidden;
   p.epi = EPI_STORE;
@@ -695,6 +635,18 @@ static int pick_bn(const moe_config* cfg, bool pairs_columns) {
   const int64_t F = cfg->ffn_hidden / cfg->block_size;
   if (pairs_columns) return (F % 2 == 0) ? 256 : 128;
   return (cfg->hidden % 256 == 0) ? 256 : 128;
+}
+
+// 2-SM (cta_group::2) 256 x 256 tiles: needs even F and h % 256 == 0.
+// MOE_GEMM_PAIR=0 in the environment selects the 1-SM kernels (A/B testing).
+static bool use_pair(const moe_config* cfg) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MOE_GEMM_PAIR");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int64_t F = cfg->ffn_hidden / cfg->block_size;
+  return env && F % 2 == 0 && cfg->hidden % 256 == 0;
 }
 
 }  // namespace moe
@@ -711,6 +663,7 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   MOE_CHECK_ARG(act >= 0 && act <= 2, "moe_sdd: bad act %d", act);
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
+  const bool pair = use_pair(cfg);
   GemmLaunch L{};
   L.name = trans_b ? "moe_sdd(T)" : "moe_sdd";
   L.mode = SDD;
@@ -722,17 +675,18 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   L.p.epi = act_grad_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_pre) ? EPI_ACT_FWD : EPI_STORE);
   L.p.has_pre = out_pre != nullptr;
   L.epi_h = L.p.epi == EPI_ACT_BWD;
-  L.max_tiles = (int)(nnz / (L.bn / 128));
+  L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
+  const int bbox = pair ? 128 : L.bn;
   MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 128, "moe_sdd a"));
   if (!trans_b)
     MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, 64, "moe_sdd b"));
   else
-    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
+    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, bbox, "moe_sdd b^T"));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   if (out_pre) MOE_TRY(make_tmap_epi(&L.td, out_pre, 128, nnz * 128, 128, "moe_sdd pre"));
   if (act_grad_src) MOE_TRY(make_tmap_epi(&L.td, act_grad_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_pre && !act_grad_src) L.td = L.tc;
-  return gemm_launch(L, as_stream(stream));
+  return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
@@ -742,36 +696,39 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
+  const bool pair = use_pair(cfg);
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.bn = pick_bn(cfg, false);
   L.p.dense_tiles = (int)(h / L.bn);
   L.b_mn = !trans_b;
+  const int bbox = pair ? 128 : L.bn;
   if (!trans_s) {
     L.name = trans_b ? "moe_dsd(T)" : "moe_dsd";
     L.mode = DSD_ROW;
     L.a_mn = false;
-    L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
+    L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * L.p.dense_tiles)
+                       : (int)(rows / BM * L.p.dense_tiles);
     MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 128, "moe_dsd s"));
     if (!trans_b)
       MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, 64, "moe_dsd b"));
     else
-      MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, L.bn, "moe_dsd b^T"));
+      MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, bbox, "moe_dsd b^T"));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
   } else {
     L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
     L.mode = DS_COL;
     L.a_mn = true;
-    L.max_tiles = L.p.n_block_cols * L.p.dense_tiles;
+    L.max_tiles = (pair ? L.p.n_block_cols / 2 : L.p.n_block_cols) * L.p.dense_tiles;
     MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 64, "moe_dsd s^T"));
     if (!trans_b)
       MOE_TRY(make_tmap_bf16(&L.tb, b, h, rows, h, 64, 64, "moe_dsd b"));
     else
-      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, L.bn, "moe_dsd b^T"));
+      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, bbox, "moe_dsd b^T"));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
   }
   L.td = L.tc;
-  return gemm_launch(L, as_stream(stream));
+  return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
@@ -783,14 +740,15 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
-  L.p.dense_tiles = (int)(h / BM);
   L.a_mn = trans_a != 0;
   if (!trans_s) {
     // out [h, E*f] = A_eff [h, rows] . S ; walk column pairs via the transpose index
+    const bool pair = use_pair(cfg);
     L.name = trans_a ? "moe_dds(T)" : "moe_dds";
     L.mode = DDS_COL;
     L.bn = pick_bn(cfg, true);
     L.b_mn = true;
+    L.p.dense_tiles = (int)(h / (pair ? 2 * BM : BM));
     L.max_tiles = L.p.n_block_cols / (L.bn / 128) * L.p.dense_tiles;
     MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 64, "moe_dds s"));
     if (trans_a)
@@ -798,20 +756,22 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, 64, 128, "moe_dds a"));
     MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
-  } else {
-    // out [h, rows] = A_eff [h, E*f] . S^T ; walk rows
-    L.name = trans_a ? "moe_dds(T,S^T)" : "moe_dds(S^T)";
-    L.mode = DDS_ROW;
-    L.bn = 128;
-    L.b_mn = false;
-    L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
-    MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
-    if (trans_a)
-      MOE_TRY(make_tmap_bf16(&L.ta, a, h, N, h, 64, 64, "moe_dds a^T"));
-    else
-      MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
-    MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));
+    L.td = L.tc;
+    return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
   }
+  // out [h, rows] = A_eff [h, E*f] . S^T ; walk rows
+  L.p.dense_tiles = (int)(h / BM);
+  L.name = trans_a ? "moe_dds(T,S^T)" : "moe_dds(S^T)";
+  L.mode = DDS_ROW;
+  L.bn = 128;
+  L.b_mn = false;
+  L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
+  MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
+  if (trans_a)
+    MOE_TRY(make_tmap_bf16(&L.ta, a, h, N, h, 64, 64, "moe_dds a^T"));
+  else
+    MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
+  MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));
   L.td = L.tc;
   return gemm_launch(L, as_stream(stream));
 }

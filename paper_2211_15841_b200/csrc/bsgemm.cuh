@@ -22,7 +22,10 @@ struct GemmParams {
   const int32_t* t_col_offsets;
   const int32_t* t_block_offsets;
   const int32_t* t_row_indices;
+  const int32_t* pair_bins;    // [E] inclusive cumsum of same-expert block-row pairs
+  const int32_t* padded_bins;  // [E]
   int n_block_cols;  // E*F
+  int F;             // block-columns per expert
   int dense_tiles;   // output tiles along the dense dimension
   int k_dense;       // SDD contraction length
   // DENSE mode: tiles = splits x m_tiles x n_tiles, kiters_split K-steps of 64 per split
@@ -64,6 +67,9 @@ struct GemmLaunch {
 };
 
 moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
+// CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
+// 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
+moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);
 GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo);
 
 }  // namespace moe

@@ -1,0 +1,432 @@
+// bsgemm2.cu — the six block-sparse products on CTA pairs (tcgen05.mma
+// cta_group::2): one 256 x 256 output tile per 2-SM cluster, each SM holding
+// half of A (128 rows) and half of B (128 columns) in shared memory, so per-SM
+// operand traffic per MMA flop is two thirds of the 1-SM 128 x 256 tile's
+// (bsgemm.cu). Same products, same topology walks (§5.1; P:238,
+// P:242):
+//
+//   SDD     rows (r0, r1) of one expert x block-columns (c, c+1)        K = dense dim
+//   DSD_ROW rows (r0, r1) of one expert x 256 dense columns              K walks row r0's blocks
+//   DS_COL  block-columns (c, c+1) of one expert x 256 dense columns     K walks column c (transpose index)
+//   DDS_COL 256 dense rows x block-columns (c, c+1)                      K walks column c (transpose index)
+//
+// Rows r0, r1 = r0+1 of the same expert share their block-column set, and
+// columns c, c+1 of the same expert share their block-row set, so one walk
+// serves both halves. Row pairs come from the topology's pair_bins (an expert
+// with an odd number of block-rows leaves one half-empty pair: the second CTA
+// computes on padding and stores nothing).
+//
+// Roles as in bsgemm.cu; the leader CTA (rank 0) issues all MMAs; both CTAs'
+// TMA loads signal the leader's full barrier; the MMA commit multicasts to
+// both CTAs' empty / tmem-full barriers; both CTAs' epilogues release the
+// leader's tmem-empty barrier.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "bsgemm.cuh"
+#include "common.cuh"
+#include "gemm_util.cuh"
+#include "sm100.cuh"
+#include "tma.cuh"
+
+namespace moe {
+
+constexpr int P_BN = 256;                      // N of the pair MMA
+constexpr int P_BH = 128;                      // B columns held per CTA
+constexpr int P_A_BYTES = A_BYTES;             // 128 x 64
+constexpr int P_B_BYTES = P_BH * BK * 2;       // 128 x 64
+constexpr int P_STAGE = P_A_BYTES + P_B_BYTES;
+
+template <bool EPI_H>
+struct Cfg2 {
+  static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES) / P_STAGE;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = 2 * P_BN;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + EPI_BYTES + H_BYTES;
+};
+
+struct Tile2 {
+  int kiters;
+  int walk_begin;  // row walk: storage index of row r0's first block; column walk: transpose position
+  int r0;          // SDD/DSD_ROW: first block-row of the pair
+  bool second;     // SDD/DSD_ROW: r0 + 1 belongs to the same expert
+  int c0;          // SDD: first block column; DS_COL/DDS_COL: first column of the pair
+  int v;           // dense tile (DSD_ROW / DS_COL: 256-wide N tile; DDS_COL: 256-row M tile)
+  int q_off;       // DSD_ROW: storage offset of this CTA's row relative to row r0 (= rank * F)
+};
+
+__device__ __forceinline__ int num_tiles2(const GemmParams& p, int mode) {
+  const int pairs = p.sizes[2];
+  switch (mode) {
+    case SDD: return pairs * (p.F / 2);
+    case DSD_ROW: return pairs * p.dense_tiles;
+    default: return (p.n_block_cols / 2) * p.dense_tiles;  // DS_COL, DDS_COL
+  }
+}
+
+// Row pair p -> (first block-row, whether the second row exists), via the
+// per-expert pair offsets (binary search over E).
+__device__ __forceinline__ void row_pair(const GemmParams& p, int pr, int& r0, bool& second) {
+  int lo = 0, hi = p.E - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.pair_bins + mid) > pr) hi = mid; else lo = mid + 1;
+  }
+  const int e = lo;
+  const int pb = __ldg(p.padded_bins + e);
+  const int pc = pb - (e > 0 ? __ldg(p.padded_bins + e - 1) : 0);
+  const int nrows = pc / BM;
+  const int i = pr - (__ldg(p.pair_bins + e) - (nrows + 1) / 2);
+  r0 = (pb - pc) / BM + 2 * i;
+  second = 2 * i + 1 < nrows;
+}
+
+__device__ __forceinline__ Tile2 decode2(const GemmParams& p, int mode, int tile, int rank) {
+  Tile2 t{};
+  if (mode == SDD) {
+    const int pr = tile / (p.F / 2), cp = tile % (p.F / 2);
+    row_pair(p, pr, t.r0, t.second);
+    const int e = __ldg(p.col_indices + (long long)__ldg(p.row_offsets + t.r0)) / p.F;
+    t.c0 = e * p.F + 2 * cp;
+    t.kiters = p.k_dense / BK;
+  } else if (mode == DSD_ROW) {
+    const int pr = tile / p.dense_tiles;
+    t.v = tile % p.dense_tiles;
+    row_pair(p, pr, t.r0, t.second);
+    const int b = __ldg(p.row_offsets + t.r0), e = __ldg(p.row_offsets + t.r0 + 1);
+    t.walk_begin = b;
+    t.kiters = 2 * (e - b);
+    t.q_off = rank * (e - b);
+  } else {  // DS_COL, DDS_COL
+    t.c0 = (tile / p.dense_tiles) * 2;
+    t.v = tile % p.dense_tiles;
+    const int b = __ldg(p.t_col_offsets + t.c0), e = __ldg(p.t_col_offsets + t.c0 + 1);
+    t.walk_begin = b;
+    t.kiters = 2 * (e - b);
+    t.second = true;
+  }
+  return t;
+}
+
+// TMA store coordinates of 32-column chunk c (0..7) for this CTA's rows.
+__device__ __forceinline__ void out_coords2(const GemmParams& p, int mode, const Tile2& t, int rank, int c, int row0,
+                                            int F, int& x, int& y) {
+  const int col = c * EPI_COLS;
+  switch (mode) {
+    case SDD: {  // blocks (r0+rank, c0), (r0+rank, c0+1) in [nnz*128, 128] storage
+      const int r = t.r0 + rank;
+      const int blk = r * F + (t.c0 % F) + col / 128;
+      x = col % 128;
+      y = blk * BM + row0;
+      break;
+    }
+    case DSD_ROW: x = t.v * P_BN + col; y = (t.r0 + rank) * BM + row0; break;
+    case DS_COL: x = t.v * P_BN + col; y = (t.c0 + rank) * BM + row0; break;
+    default: x = t.c0 * 128 + col; y = (2 * t.v + rank) * BM + row0; break;  // DDS_COL
+  }
+}
+
+template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    bsgemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                   const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
+                   const GemmParams p) {
+  using C = Cfg2<EPI_H>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int NCHUNK = P_BN / EPI_COLS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem_a + STAGES * P_A_BYTES;
+  uint8_t* smem_epi = smem_b + STAGES * P_B_BYTES;
+  uint8_t* smem_h = smem_epi + EPI_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* hbar = tempty + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * NUM_EPI_WARPS);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int rank = (int)cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * NUM_EPI_WARPS);
+    }
+    for (int i = 0; i < 2 * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1) tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int ntiles = num_tiles2(p, MODE);
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const Tile2 t = decode2(p, MODE, tile, rank);
+      int idx_a = 0, idx_b = 0;
+      for (int kit = 0; kit < t.kiters; ++kit) {
+        const int blk = kit >> 1, kk = kit & 1;
+        if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
+          const int qq = t.walk_begin + blk + lane;
+          if (qq < t.walk_begin + (t.kiters >> 1)) {
+            if (MODE == DSD_ROW) {
+              idx_a = qq + t.q_off;               // this CTA's row: same column, next row
+              idx_b = __ldg(p.col_indices + qq);  // block column
+            } else {
+              idx_a = __ldg(p.t_block_offsets + qq) + rank;  // this CTA's column of the pair
+              idx_b = __ldg(p.t_row_indices + qq);
+            }
+          }
+        }
+        const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
+        const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          uint8_t* sa = smem_a + stage * P_A_BYTES;
+          uint8_t* sb = smem_b + stage * P_B_BYTES;
+          uint64_t* fb = &full[stage];
+          if (leader) mbar_arrive_expect_tx(fb, 2 * P_STAGE);
+          if (MODE == SDD) {
+            const int k0 = kit * BK;
+            tma_load_2d_pair(sa, &tmap_a, fb, k0, (t.r0 + rank) * BM);
+            if (B_MN) {  // W1 [h, E*f]: this CTA's block column c0 + rank
+              tma_load_2d_pair(sb, &tmap_b, fb, (t.c0 + rank) * 128, k0);
+              tma_load_2d_pair(sb + 8192, &tmap_b, fb, (t.c0 + rank) * 128 + 64, k0);
+            } else {     // W2 [E*f, h]
+              tma_load_2d_pair(sb, &tmap_b, fb, k0, (t.c0 + rank) * 128);
+            }
+          } else if (MODE == DSD_ROW) {
+            tma_load_2d_pair(sa, &tmap_a, fb, kk * BK, sblk * BM);
+            const int n0 = t.v * P_BN + rank * P_BH;
+            if (B_MN) {
+              tma_load_2d_pair(sb, &tmap_b, fb, n0, oblk * BM + kk * BK);
+              tma_load_2d_pair(sb + 8192, &tmap_b, fb, n0 + 64, oblk * BM + kk * BK);
+            } else {
+              tma_load_2d_pair(sb, &tmap_b, fb, oblk * BM + kk * BK, n0);
+            }
+          } else if (MODE == DS_COL) {
+            tma_load_2d_pair(sa, &tmap_a, fb, 0, sblk * BM + kk * BK);
+            tma_load_2d_pair(sa + 8192, &tmap_a, fb, 64, sblk * BM + kk * BK);
+            const int n0 = t.v * P_BN + rank * P_BH;
+            if (B_MN) {
+              tma_load_2d_pair(sb, &tmap_b, fb, n0, oblk * BM + kk * BK);
+              tma_load_2d_pair(sb + 8192, &tmap_b, fb, n0 + 64, oblk * BM + kk * BK);
+            } else {
+              tma_load_2d_pair(sb, &tmap_b, fb, oblk * BM + kk * BK, n0);
+            }
+          } else {  // DDS_COL: A = dense rows (2v + rank) tile, B = block sblk (this CTA's column)
+            const int m0 = (2 * t.v + rank) * BM;
+            if (A_MN) {
+              tma_load_2d_pair(sa, &tmap_a, fb, m0, oblk * BM + kk * BK);
+              tma_load_2d_pair(sa + 8192, &tmap_a, fb, m0 + 64, oblk * BM + kk * BK);
+            } else {
+              tma_load_2d_pair(sa, &tmap_a, fb, oblk * BM + kk * BK, m0);
+            }
+            tma_load_2d_pair(sb, &tmap_b, fb, 0, sblk * BM + kk * BK);
+            tma_load_2d_pair(sb + 8192, &tmap_b, fb, 64, sblk * BM + kk * BK);
+          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, P_BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < ntiles; tile += ncl) {
+        const Tile2 t = decode2(p, MODE, tile, 0);
+        if (t.kiters == 0) continue;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * P_BN;
+        for (int kit = 0; kit < t.kiters; ++kit) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(smem_a + stage * P_A_BYTES);
+          const uint32_t b_base = smem_u32(smem_b + stage * P_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc =
+                A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc =
+                B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+            mma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
+          }
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..9, both CTAs) =====================
+    const int q = warp & 3;
+    const int wq = warp - 2;
+    const int half = wq >> 2;
+    const int row0 = q * 32;
+    uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
+    uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
+    uint64_t* hb = hbar + wq * 2;
+    uint32_t hphase[2] = {0, 0};
+    int hslot = 0;
+    int sbuf = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+
+    auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      stage_row(stg + sbuf * EPI_BUF, lane, v);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
+        bulk_commit();
+      }
+      sbuf ^= 1;
+    };
+    auto load_h = [&](const Tile2& t, int c, int b) {
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        int x, y;
+        out_coords2(p, MODE, t, rank, c, row0, p.F, x, y);
+        mbar_arrive_expect_tx(&hb[b], EPI_BUF);
+        tma_load_2d(hst + b * EPI_BUF, &tmap_d, &hb[b], x, y);
+      }
+    };
+
+    for (int tile = cid; tile < ntiles; tile += ncl) {
+      const Tile2 t = decode2(p, MODE, tile, rank);
+      const bool has_acc = t.kiters > 0;
+      const bool mine = rank == 0 || t.second;  // does this CTA own real output rows?
+      if (EPI_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
+      if (has_acc) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+      }
+      const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * P_BN;
+      if (mine) {
+#pragma unroll 1
+        for (int c = half; c < NCHUNK; c += 2) {
+          float v[32];
+          if (has_acc) {
+            uint32_t r[32];
+            tmem_ld32(taddr + c * EPI_COLS, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          int x, y;
+          out_coords2(p, MODE, t, rank, c, row0, p.F, x, y);
+          if (p.epi == EPI_ACT_FWD) {
+            if (p.has_pre) store_chunk(&tmap_d, v, x, y);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = act_fwd(p.act, v[i]);
+          } else if (EPI_H && p.epi == EPI_ACT_BWD) {
+            mbar_wait(&hb[hslot], hphase[hslot]);
+            hphase[hslot] ^= 1;
+            const uint8_t* hrow = hst + hslot * EPI_BUF + lane * 64;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float hf[8];
+              unpack8(*reinterpret_cast<const uint4*>(hrow + swz64(j, lane)), hf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[8 * j + e] *= act_grad(p.act, hf[e]);
+            }
+            __syncwarp();
+            hslot ^= 1;
+            if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);
+          }
+          store_chunk(&tmap_c, v, x, y);
+        }
+      }
+      if (has_acc) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
+static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
+  using C = Cfg2<EPI_H>;
+  auto kern = bsgemm2_kernel<MODE, A_MN, B_MN, EPI_H>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
+    attr_set = true;
+  }
+  int grid = moe_device_sm_count() & ~1;
+  if (2 * L.max_tiles < grid) grid = 2 * L.max_tiles;
+  if (grid < 2) grid = 2;
+  kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, L.p);
+  MOE_CHECK_LAUNCH(L.name);
+  return MOE_OK;
+}
+
+#define MOE_GEMM2_CASE(MODE, AMN, BMN, H) \
+  if (L.mode == MODE && L.a_mn == AMN && L.b_mn == BMN && L.epi_h == H) return launch2_t<MODE, AMN, BMN, H>(L, stream);
+
+moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream) {
+  MOE_GEMM2_CASE(SDD, false, true, false)      // SDD      X_g . W1 (+act, +pre)
+  MOE_GEMM2_CASE(SDD, false, false, true)      // SDD^T    dY_g . W2^T (+act')
+  MOE_GEMM2_CASE(SDD, false, false, false)
+  MOE_GEMM2_CASE(DSD_ROW, false, true, false)  // DSD      A . W2
+  MOE_GEMM2_CASE(DSD_ROW, false, false, false) // DSD^T    dH . W1^T
+  MOE_GEMM2_CASE(DS_COL, true, true, false)    // DS^TD    A^T . dY_g
+  MOE_GEMM2_CASE(DS_COL, true, false, false)
+  MOE_GEMM2_CASE(DDS_COL, true, true, false)   // DD^TS    X_g^T . dH
+  MOE_GEMM2_CASE(DDS_COL, false, true, false)
+  return set_error(MOE_EUNSUPPORTED, "%s: no CTA-pair kernel for mode=%d a_mn=%d b_mn=%d", L.name, L.mode,
+                   (int)L.a_mn, (int)L.b_mn);
+}
+
+}  // namespace moe

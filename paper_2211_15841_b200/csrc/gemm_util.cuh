@@ -1,0 +1,80 @@
+// gemm_util.cuh — constants and epilogue helpers shared by the 1-CTA
+// (bsgemm.cu) and CTA-pair (bsgemm2.cu) tcgen05 GEMM kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/moe.h"
+#include "sm100.cuh"
+
+namespace moe {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int NUM_EPI_WARPS = 8;                  // 2 per TMEM lane quarter (column halves)
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int EPI_COLS = 32;                      // epilogue chunk: 32 rows x 32 columns per warp
+constexpr int EPI_BUF = 32 * EPI_COLS * 2;        // one warp's chunk, bf16, 64B-swizzled rows
+constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF;  // double buffered
+constexpr int SMEM_LIMIT = 232448;                // 227 KB opt-in
+constexpr int SMEM_FIXED = 1024 + 512;            // alignment slack + barriers
+constexpr int kMaxRouterTopK = 8;
+
+// tanh on the SFU (MUFU.TANH, max rel. error ~2^-11, below the bf16 output ulp)
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// gelu, tanh approximation (reading R2): 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+__device__ __forceinline__ float act_fwd(int kind, float x) {
+  if (kind == MOE_ACT_GELU_TANH) {
+    const float x2 = x * x;
+    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_fast(u), hx);
+  }
+  if (kind == MOE_ACT_RELU) return x > 0.f ? x : 0.f;
+  return x;
+}
+__device__ __forceinline__ float act_grad(int kind, float x) {
+  if (kind == MOE_ACT_GELU_TANH) {
+    const float x2 = x * x;
+    const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
+    const float t = tanh_fast(u);
+    const float du = fmaf(0.7978845608028654f * 3.0f * 0.044715f, x2, 0.7978845608028654f);
+    return fmaf(0.5f * x * du, fmaf(-t, t, 1.0f), 0.5f * (1.0f + t));
+  }
+  if (kind == MOE_ACT_RELU) return x > 0.f ? 1.f : 0.f;
+  return 1.f;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& w, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+
+// 64B swizzle (TMA SWIZZLE_64B): 16-byte chunk j of row r lives at chunk j ^ ((r >> 1) & 3).
+__device__ __forceinline__ int swz64(int j, int row) { return (j ^ ((row >> 1) & 3)) << 4; }
+
+// Write 32 fp32 values of this thread's row as bf16 into a 64B-swizzled
+// [32 rows][64 B] staging buffer (row = lane): conflict-free 16-byte stores.
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
+  uint8_t* row = buf + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 w = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    *reinterpret_cast<uint4*>(row + swz64(j, lane)) = w;
+  }
+}
+
+}  // namespace moe

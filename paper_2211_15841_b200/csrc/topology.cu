@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
   __shared__ int32_t s_counts[1024];
   __shared__ int32_t s_pad[1024];
   __shared__ int32_t s_tmp[32];
-  __shared__ int32_t s_tot[2];
+  __shared__ int32_t s_pairs[1024];
+  __shared__ int32_t s_tot[3];
   // (1) per-expert exclusive scan over chunks (chunk_counts becomes chunk base rank)
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t run = 0;
@@ -87,12 +88,14 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
     }
     s_counts[e] = run;
     s_pad[e] = ((run + bs - 1) / bs) * bs;
+    s_pairs[e] = (s_pad[e] / bs + 1) / 2;  // same-expert block-row pairs
     topo.counts[e] = run;
   }
   __syncthreads();
   // (2) bins / padded_bins = inclusive cumsums (P:297 padding to a multiple of bs)
   block_exclusive_scan(s_counts, E, s_tmp, &s_tot[0]);
   block_exclusive_scan(s_pad, E, s_tmp, &s_tot[1]);
+  block_exclusive_scan(s_pairs, E, s_tmp, &s_tot[2]);
   const int Tp = s_tot[1];
   const int nnz = (Tp / bs) * F;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
     const int32_t pc = ((c + bs - 1) / bs) * bs;
     topo.bins[e] = s_counts[e] + c;
     topo.padded_bins[e] = s_pad[e] + pc;
+    topo.pair_bins[e] = s_pairs[e] + (pc / bs + 1) / 2;
     // transposed offsets of expert e's F block-columns: F*start/bs + j*pc/bs
     for (int j = 0; j < F; ++j) topo.t_col_offsets[e * F + j] = F * (s_pad[e] / bs) + j * (pc / bs);
   }
@@ -108,6 +112,7 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
     topo.row_offsets[Tp / bs] = nnz;
     topo.sizes[0] = Tp;
     topo.sizes[1] = nnz;
+    topo.sizes[2] = s_tot[2];
   }
 }
 

@@ -62,6 +62,10 @@ def check_topology_exact(A, topo_gpu, plan, topo, R):
     np.testing.assert_array_equal(g["t_col_offsets"], topo.t_col_offsets)
     np.testing.assert_array_equal(g["t_block_offsets"][:nnz], topo.t_block_offsets)
     np.testing.assert_array_equal(g["t_row_indices"][:nnz], topo.t_row_indices)
+    # 2-SM tiling helper: per-expert pairs of block-rows, ceil(rows_e / 2), cumulated
+    pairs = np.cumsum((plan.padded_counts // 128 + 1) // 2)
+    np.testing.assert_array_equal(g["pair_bins"], pairs)
+    assert int(g["sizes"][2]) == int(pairs[-1])
 
 
 # ------------------------------------------------------------------ routing
