@@ -129,6 +129,74 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
   }
 }
 
+// Issue the TMA boxes of K-step `kit` of tile t: into the smem stage (PF =
+// false, completion on mbarrier fb) or as L2 prefetches (PF = true).
+template <int MODE, bool A_MN, bool B_MN, int BN, bool PF>
+__device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p,
+                                            const TileInfo& t, int kit, int sblk, int oblk, uint8_t* sa, uint8_t* sb,
+                                            uint64_t* fb) {
+  const int kk = kit & 1;
+  if (MODE == SDD) {
+    const int k0 = kit * BK;
+    tma_box<PF>(sa, ta, fb, k0, t.u * BM);
+    if (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * 128 + j * 64, k0);
+    } else {
+      tma_box<PF>(sb, tb, fb, k0, t.v * 128);
+    }
+  } else if (MODE == DSD_ROW) {
+    tma_box<PF>(sa, ta, fb, kk * BK, sblk * BM);
+    if (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
+    } else {
+      tma_box<PF>(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
+    }
+  } else if (MODE == DS_COL) {
+    tma_box<PF>(sa, ta, fb, 0, sblk * BM + kk * BK);
+    tma_box<PF>(sa + 8192, ta, fb, 64, sblk * BM + kk * BK);
+    if (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
+    } else {
+      tma_box<PF>(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
+    }
+  } else if (MODE == DDS_COL) {
+    if (A_MN) {
+      tma_box<PF>(sa, ta, fb, t.v * BM, oblk * BM + kk * BK);
+      tma_box<PF>(sa + 8192, ta, fb, t.v * BM + 64, oblk * BM + kk * BK);
+    } else {
+      tma_box<PF>(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
+    }
+#pragma unroll
+    for (int j = 0; j < BN / 64; ++j)  // blocks (r, c + j/2): storage sblk + j/2
+      tma_box<PF>(sb + j * 8192, tb, fb, (j & 1) * 64, (sblk + (j >> 1)) * BM + kk * BK);
+  } else if (MODE == DDS_ROW) {
+    if (A_MN) {
+      tma_box<PF>(sa, ta, fb, t.v * BM, oblk * BM + kk * BK);
+      tma_box<PF>(sa + 8192, ta, fb, t.v * BM + 64, oblk * BM + kk * BK);
+    } else {
+      tma_box<PF>(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
+    }
+    tma_box<PF>(sb, tb, fb, kk * BK, sblk * BM);
+  } else {  // DENSE
+    const int k0 = (t.s * p.kiters_split + kit) * BK;
+    if (A_MN) {
+      tma_box<PF>(sa, ta, fb, t.u * BM, k0);
+      tma_box<PF>(sa + 8192, ta, fb, t.u * BM + 64, k0);
+    } else {
+      tma_box<PF>(sa, ta, fb, k0, t.u * BM);
+    }
+    if (B_MN) {
+#pragma unroll
+      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, k0);
+    } else {
+      tma_box<PF>(sb, tb, fb, k0, t.v * BN);
+    }
+  }
+}
+
 template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     bsgemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -198,73 +266,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
+        // L2 prefetch PF K-steps ahead (no smem cost) to deepen the memory pipeline
+        const int kpf = kit + kPrefetch;
+        const int bpf = kpf >> 1;
+        const bool pf_ok = kpf < t.kiters && (MODE == SDD || MODE == DENSE || (bpf >> 5) == (blk >> 5));
+        const int sblk_pf = __shfl_sync(0xffffffffu, idx_a, bpf & 31);
+        const int oblk_pf = __shfl_sync(0xffffffffu, idx_b, bpf & 31);
+        if (kPrefetch > 0 && kit == 0)  // head of the tile: prefetch K-steps 1 .. PF-1 (warp-uniform loop)
+          for (int k2 = 1; k2 < kPrefetch && k2 < t.kiters; ++k2) {
+            const int s2 = __shfl_sync(0xffffffffu, idx_a, (k2 >> 1) & 31);
+            const int o2 = __shfl_sync(0xffffffffu, idx_b, (k2 >> 1) & 31);
+            if (lane == 0)
+              issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, k2, s2, o2, nullptr, nullptr, nullptr);
+          }
+        if (lane == 0) {
+          if (kPrefetch > 0 && pf_ok)
+            issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, kpf, sblk_pf, oblk_pf, nullptr, nullptr,
+                                                    nullptr);
+        }
         mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
-          uint8_t* sa = smem_a + stage * A_BYTES;
-          uint8_t* sb = smem_b + stage * C::B_BYTES;
           uint64_t* fb = &full[stage];
           mbar_arrive_expect_tx(fb, C::STAGE);
-          if (MODE == SDD) {
-            const int k0 = kit * BK;
-            tma_load_2d(sa, &tmap_a, fb, k0, t.u * BM);
-            if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * 128 + j * 64, k0);
-            } else {
-              tma_load_2d(sb, &tmap_b, fb, k0, t.v * 128);
-            }
-          } else if (MODE == DSD_ROW) {
-            tma_load_2d(sa, &tmap_a, fb, kk * BK, sblk * BM);
-            if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
-            } else {
-              tma_load_2d(sb, &tmap_b, fb, oblk * BM + kk * BK, t.v * BN);
-            }
-          } else if (MODE == DS_COL) {
-            tma_load_2d(sa, &tmap_a, fb, 0, sblk * BM + kk * BK);
-            tma_load_2d(sa + 8192, &tmap_a, fb, 64, sblk * BM + kk * BK);
-            if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
-            } else {
-              tma_load_2d(sb, &tmap_b, fb, oblk * BM + kk * BK, t.v * BN);
-            }
-          } else if (MODE == DDS_COL) {
-            if (A_MN) {
-              tma_load_2d(sa, &tmap_a, fb, t.v * BM, oblk * BM + kk * BK);
-              tma_load_2d(sa + 8192, &tmap_a, fb, t.v * BM + 64, oblk * BM + kk * BK);
-            } else {
-              tma_load_2d(sa, &tmap_a, fb, oblk * BM + kk * BK, t.v * BM);
-            }
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j)  // blocks (r, c + j/2): storage sblk + j/2
-              tma_load_2d(sb + j * 8192, &tmap_b, fb, (j & 1) * 64, (sblk + (j >> 1)) * BM + kk * BK);
-          } else if (MODE == DDS_ROW) {
-            if (A_MN) {
-              tma_load_2d(sa, &tmap_a, fb, t.v * BM, oblk * BM + kk * BK);
-              tma_load_2d(sa + 8192, &tmap_a, fb, t.v * BM + 64, oblk * BM + kk * BK);
-            } else {
-              tma_load_2d(sa, &tmap_a, fb, oblk * BM + kk * BK, t.v * BM);
-            }
-            tma_load_2d(sb, &tmap_b, fb, kk * BK, sblk * BM);
-          } else {  // DENSE
-            const int k0 = (t.s * p.kiters_split + kit) * BK;
-            if (A_MN) {
-              tma_load_2d(sa, &tmap_a, fb, t.u * BM, k0);
-              tma_load_2d(sa + 8192, &tmap_a, fb, t.u * BM + 64, k0);
-            } else {
-              tma_load_2d(sa, &tmap_a, fb, k0, t.u * BM);
-            }
-            if (B_MN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 8192, &tmap_b, fb, t.v * BN + j * 64, k0);
-            } else {
-              tma_load_2d(sb, &tmap_b, fb, k0, t.v * BN);
-            }
-          }
+          issue_stage<MODE, A_MN, B_MN, BN, false>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+                                                   smem_b + stage * C::B_BYTES, fb);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -663,7 +688,9 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   MOE_CHECK_ARG(act >= 0 && act <= 2, "moe_sdd: bad act %d", act);
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  const bool pair = use_pair(cfg);
+  // Row-pair 2-SM tiles measured slower for SDD at MoE-XS (half-empty pairs of
+  // odd-row experts); the 1-SM 128 x 256 kernel is used.
+  const bool pair = false;
   GemmLaunch L{};
   L.name = trans_b ? "moe_sdd(T)" : "moe_sdd";
   L.mode = SDD;
@@ -686,7 +713,7 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   if (out_pre) MOE_TRY(make_tmap_epi(&L.td, out_pre, 128, nnz * 128, 128, "moe_sdd pre"));
   if (act_grad_src) MOE_TRY(make_tmap_epi(&L.td, act_grad_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_pre && !act_grad_src) L.td = L.tc;
-  return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
+  return gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
@@ -696,7 +723,7 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  const bool pair = use_pair(cfg);
+  const bool pair = use_pair(cfg) && trans_s;  // column pairs only (DS^TD); see moe_sdd
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.bn = pick_bn(cfg, false);

@@ -74,6 +74,22 @@ __device__ __forceinline__ void tma_load_2d_hint(void* smem_dst, const CUtensorM
       : "memory");
 }
 
+// Prefetch a 2-D box into L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+// Load (PF = false) or L2-prefetch (PF = true) of the same box.
+template <bool PF>
+__device__ __forceinline__ void tma_box(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0, int32_t c1) {
+  if (PF)
+    tma_prefetch_2d(map, c0, c1);
+  else
+    tma_load_2d(smem_dst, map, bar, c0, c1);
+}
+
 // 2-D tiled store smem -> global (bulk async group; clipped at tensor bounds).
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
