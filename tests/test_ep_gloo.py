@@ -36,12 +36,7 @@ def _worker(rank, world, port, cfgd, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import ep_cpu_backend as B
-    import importlib.util
-    spec = importlib.util.spec_from_file_location(
-        "ep_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                               "paper_2211_15841_b200", "ep.py"))
-    ep = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(ep)         # the EP module alone (no libmoe.so needed for host logic)
+    from paper_2211_15841_b200 import ep   # host logic only; compute comes from the test backend
     T, h, f, E, k, act = cfgd["T"], cfgd["h"], cfgd["f"], cfgd["E"], cfgd["k"], cfgd["act"]
     x, wr, w1, w2, dy = _inputs(T * world, h, f, E, 0)
     sl = slice(rank * T, (rank + 1) * T)
@@ -69,7 +64,7 @@ def test_ep_world2_matches_global_oracle(cfgd):
         p.start()
     res = {}
     for _ in range(world):
-        r = q.get(timeout=300)
+        r = q.get(timeout=120)
         res[r[0]] = r[1:]
     for p in procs:
         p.join(timeout=60)
@@ -90,12 +85,7 @@ def test_ep_world2_matches_global_oracle(cfgd):
 
 
 def test_split_helpers():
-    import importlib.util
-    spec = importlib.util.spec_from_file_location(
-        "ep_mod", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                               "paper_2211_15841_b200", "ep.py"))
-    ep = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(ep)
+    from paper_2211_15841_b200 import ep
     counts = np.array([[3, 0, 2, 1], [1, 4, 0, 0]])
     assert ep.send_splits(counts[0], 2) == [3, 3]
     assert ep.send_splits(counts[1], 2) == [5, 0]

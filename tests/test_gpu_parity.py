@@ -440,3 +440,42 @@ def test_c1_full_size_sampled():
     got = f64(dw2[e * f + cols])
     want = Ax[:, cols].T @ dY
     assert rel_fro(got, want) < FRO_TOL
+
+
+def test_expert_parallel_single_rank_nccl():
+    """The expert-parallel layer (ep.py) driving the CUDA kernels through NCCL
+    with one rank (the only multi-process shape one GPU allows): must match the
+    oracle like the single-device layer (dispatch / combine via all_to_all)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2211_15841_b200 import ep
+    d = dev()
+    A = api()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=d)
+    try:
+        shp = S.CONFIGS["C4"]
+        T = 1024
+        inp = S.make_inputs(shp, seed=6, tokens=T)
+        xd, dyd = inp["x"].to(d), inp["dy"].to(d)
+        wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+        y, st = layer.forward(xd, wr, w1, w2)
+        dx, dwr, dw1, dw2 = layer.backward(st, xd, dyd, wr, w1, w2)
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    yo, cache, go = oracle_layer(inp, shp, T)
+    flips = (st.expert_idx.cpu().numpy() != cache.expert_idx).any(axis=1)
+    assert flips.mean() < 1e-3
+    ok = ~flips
+    assert rel_fro(f64(y)[ok], yo[ok]) < FRO_TOL
+    assert rel_fro(f64(dx)[ok], go["dx"][ok]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+    assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
