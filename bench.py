@@ -420,6 +420,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-tokens", type=int, default=4096)
+    ap.add_argument("--ep", action="store_true", help="expert-parallel path even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -430,9 +431,9 @@ def main():
             print(json.dumps(run_reference(args)), flush=True)
         return
     peaks = load_peaks()
-    if world > 1:
+    if world > 1 or args.ep:
         from paper_2211_15841_b200 import ep
-        out = ep.bench_ep(args, peaks)
+        out = ep.bench_ep(args, peaks, ClockSampler)
         if rank == 0 and out is not None:
             print(json.dumps(out), flush=True)
         return

@@ -171,17 +171,20 @@ class ExpertParallelMoE:
 
 # ----------------------------------------------------------------------------- bench (N > 1)
 
-def bench_ep(args, peaks):
+def bench_ep(args, peaks, clock_sampler=None):
     """Weak-scaling EP benchmark: T_local tokens per rank of the BASELINE
     config, experts split over ranks, NCCL all-to-all. Returns rank 0's JSON
-    dict (others None). Timed on the device, max over ranks."""
-    import json  # noqa: F401
+    dict (others None). Timed on the device with CUDA events, max over ranks;
+    e2e through the same public layer with pinned host inputs / outputs."""
     import os
-    import time
 
     from . import api as A
     from synth import inputs as S
 
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -200,40 +203,67 @@ def bench_ep(args, peaks):
     layer = ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act)
     l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
-    def step():
-        y, st = layer.forward(x, wr, w1l, w2l)
-        layer.backward(st, x, dy, wr, w1l, w2l)
+    def step(xd, dyd):
+        y, st = layer.forward(xd, wr, w1l, w2l)
+        dx, _, _, _ = layer.backward(st, xd, dyd, wr, w1l, w2l)
+        return y, dx
+
+    def timed(fn, steps):
+        total = 0.0
+        for _ in range(steps):
+            l2.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record()
+            fn()
+            e_.record()
+            torch.cuda.synchronize()
+            total += s_.elapsed_time(e_)
+        t = torch.tensor([total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     for _ in range(args.warmup):
         l2.zero_()
-        step()
+        step(x, dy)
     torch.cuda.synchronize()
     launches0 = A.lib.moe_total_launch_count()
-    total = 0.0
-    for _ in range(args.steps):
-        l2.zero_()
-        dist.barrier()
-        torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        step()
-        e.record()
-        torch.cuda.synchronize()
-        total += s.elapsed_time(e)
+    clk = clock_sampler(dev.index) if clock_sampler else None
+    if clk:
+        clk.start()
+    ms = timed(lambda: step(x, dy), args.steps)
+    clocks = clk.stop() if clk else None
     launches = A.lib.moe_total_launch_count() - launches0
-    t = torch.tensor([total], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    # end to end: pinned host x, dy in; y, dx out, every step
+    hx, hdy = x.cpu().pin_memory(), dy.cpu().pin_memory()
+    hy = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+    hdx = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+    xd, dyd = torch.empty_like(x), torch.empty_like(dy)
+
+    def e2e_step():
+        xd.copy_(hx, non_blocking=True)
+        dyd.copy_(hdy, non_blocking=True)
+        y, dx = step(xd, dyd)
+        hy.copy_(y, non_blocking=True)
+        hdx.copy_(dx, non_blocking=True)
+
+    e2e_step()
+    ms_e2e = timed(e2e_step, args.steps) if not getattr(args, "no_e2e", False) else None
     out = None
     if rank == 0:
         out = {"metric": "dropless MoE layer fwd+bwd tokens/s", "value": round(T * world * args.steps / (ms / 1e3), 1),
                "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
                "config": {"workload": shp.name, "tokens_per_rank": T, "hidden": h, "ffn_hidden": f,
                           "num_experts": E, "top_k": k, "parallelism": f"ep{world}",
-                          "l2": "flushed between timed steps"},
-               "gpu_launches": int(launches), "roofline": None, "e2e": None}
+                          "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
+               "gpu_launches": int(launches), "clocks": clocks, "roofline": None,
+               "e2e": None if ms_e2e is None else {
+                   "value": round(T * world * args.steps / (ms_e2e / 1e3), 1), "unit": "tokens/s",
+                   "h2d_bytes_per_step": 2 * T * h * 2 * world, "d2h_bytes_per_step": 2 * T * h * 2 * world,
+                   "api": "ExpertParallelMoE.forward/backward over the C ABI + NCCL all_to_all"}}
     dist.barrier()
     dist.destroy_process_group()
     return out

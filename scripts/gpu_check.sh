@@ -21,7 +21,7 @@ for s in $STEPS; do
         python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list_$TAG.log 2>&1
       echo "ncu_list_exit=$?" ;;
     full)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:bsgemm -s 30 -c 10 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:bsgemm -s 27 -c 9 \
         -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$TAG.log 2>&1
       echo "ncu_full_exit=$?" ;;
   esac
