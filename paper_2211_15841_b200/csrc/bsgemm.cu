@@ -39,19 +39,41 @@
 #include "sm100.cuh"
 #include "tma.cuh"
 
+#ifndef MOE_SDD_EPW
+#define MOE_SDD_EPW 16
+#endif
+#ifndef MOE_SDD_NBUF
+#define MOE_SDD_NBUF 2
+#endif
+
 namespace moe {
 
 using namespace sm100;
 
-template <int BN, bool EPI_H>
+// Epilogue warps: 16 (four per TMEM lane quarter) for the wide block-sparse
+// tiles, whose epilogues are store-latency bound; 8 elsewhere (router GEMMs,
+// SDD^T whose H staging would not leave room for the operand ring).
+__host__ __device__ constexpr int epi_warps(int mode, int bn, bool epi_h) {
+  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_EPW : 8;
+}
+// Staging buffers per epilogue warp (stores in flight per warp).
+__host__ __device__ constexpr int epi_bufs(int mode, int bn, bool epi_h) {
+  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_NBUF : 2;
+}
+
+template <int MODE, int BN, bool EPI_H>
 struct Cfg {
+  static constexpr int EPW = epi_warps(MODE, BN, EPI_H);
+  static constexpr int THREADS = 64 + 32 * EPW;
+  static constexpr int NBUF = epi_bufs(MODE, BN, EPI_H);
+  static constexpr int EPI = EPW * NBUF * EPI_BUF;  // per-warp staging ring
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES) / STAGE;
+  static constexpr int H_BYTES = EPI_H ? EPI : 0;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI_BYTES + H_BYTES;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES;
   static_assert(STAGES >= 2, "not enough shared memory for two stages");
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
@@ -198,12 +220,14 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtenso
 }
 
 template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     bsgemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
                   const GemmParams p) {
-  using C = Cfg<BN, EPI_H>;
+  using C = Cfg<MODE, BN, EPI_H>;
   constexpr int STAGES = C::STAGES;
+  constexpr int EPW = C::EPW;
+  constexpr int NG = EPW / 4;  // epilogue warps per TMEM lane quarter
   constexpr int PAIR = (MODE == SDD || MODE == DDS_COL) ? BN / 128 : 1;
   constexpr int NCHUNK = BN / EPI_COLS;
   extern __shared__ uint8_t smem_raw[];
@@ -211,13 +235,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem_a + STAGES * A_BYTES;
   uint8_t* smem_epi = smem_b + STAGES * C::B_BYTES;
-  uint8_t* smem_h = smem_epi + EPI_BYTES;
+  uint8_t* smem_h = smem_epi + C::EPI;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* hbar = tempty + 2;  // [NUM_EPI_WARPS][2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * NUM_EPI_WARPS);
+  uint64_t* hbar = tempty + 2;  // [EPW][2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * EPW);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -229,9 +253,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], NUM_EPI_WARPS);
+      mbar_init(&tempty[i], EPW);
     }
-    for (int i = 0; i < 2 * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
+    for (int i = 0; i < 2 * EPW; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -287,9 +311,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         if (lane == 0) {
           uint64_t* fb = &full[stage];
-          mbar_arrive_expect_tx(fb, C::STAGE);
-          issue_stage<MODE, A_MN, B_MN, BN, false>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
-                                                   smem_b + stage * C::B_BYTES, fb);
+          if (p.dbg & 8) {
+            mbar_arrive(fb);
+          } else {
+            mbar_arrive_expect_tx(fb, C::STAGE);
+            issue_stage<MODE, A_MN, B_MN, BN, false>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+                                                     smem_b + stage * C::B_BYTES, fb);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -309,7 +337,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const TileInfo t = decode(p, MODE, PAIR, tile);
         if (t.kiters == 0) continue;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (!(p.dbg & 64)) mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kit = 0; kit < t.kiters; ++kit) {
@@ -323,7 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bdesc =
                 B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
-            mma_bf16(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
+            if (!(p.dbg & 2)) mma_bf16(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
           }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -337,14 +365,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..9) =====================
+    // ===================== epilogue (warps 2 .. 2+EPW-1) =====================
     // Warp w reads TMEM lane quarter w % 4 (rows 32q..32q+31 of the tile) and
-    // the 32-column chunks c = half, half + 2, ... (half = (w - 2) / 4).
+    // the 32-column chunks c = grp, grp + NG, ... (grp = (w - 2) / 4). The
+    // TMEM load of the next chunk is in flight while the current one is
+    // processed and stored.
     const int q = warp & 3;
     const int wq = warp - 2;
-    const int half = wq >> 2;
+    const int grp = wq >> 2;
     const int row0 = q * 32;
-    uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
+    uint8_t* stg = smem_epi + wq * C::NBUF * EPI_BUF;
     uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
     uint64_t* hb = hbar + wq * 2;
     uint32_t hphase[2] = {0, 0};
@@ -355,7 +385,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool bf16_out = p.epi == EPI_STORE || p.epi == EPI_ACT_FWD || p.epi == EPI_ACT_BWD || p.epi == EPI_ADD_ROWS;
 
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
-      if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer 2 stores ago has read it
+      if (lane == 0) bulk_wait_read<C::NBUF - 1>();  // the store issued from this buffer NBUF stores ago has read it
       __syncwarp();
       stage_row(stg + sbuf * EPI_BUF, lane, v);
       fence_proxy_async_smem();
@@ -364,7 +394,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
         bulk_commit();
       }
-      sbuf ^= 1;
+      sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
     };
     auto load_h = [&](const TileInfo& t, int c, int b) {
       if (lane == 0) {
@@ -378,54 +408,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo t = decode(p, MODE, PAIR, tile);
-      const bool has_acc = t.kiters > 0;
-      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, half, hslot);
+      const bool has_acc = (p.dbg & 64) ? false : t.kiters > 0;
+      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, grp, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
       }
       const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * BN;
 
-      if (bf16_out) {
+      if (p.dbg & 1) {
+        if (has_acc) {
+          uint32_t r[32];
+          tmem_ld32(taddr, r);
+          tmem_ld_wait();
+          if (r[0] == 0x7fffffffu && r[1] == 0x12345u) p.gates[0] = 1.f;
+        }
+      } else if (bf16_out) {
+        uint32_t rn[32];
+        if (has_acc && grp < NCHUNK) {
+          tmem_ld32(taddr + grp * EPI_COLS, rn);
+          tmem_ld_wait();
+        }
 #pragma unroll 1
-        for (int c = half; c < NCHUNK; c += 2) {
+        for (int c = grp; c < NCHUNK; c += NG) {
           float v[32];
-          // rows to add (router backward: dx += ...), issued before the TMEM read
-          uint4 add_raw[4];
-          bool add_ok = false;
-          float add_f[32];
-          if (p.epi == EPI_ADD_ROWS) {
-            const int trow = t.u * BM + row0 + lane;
-            if (trow < p.rows_valid) {
-              add_ok = true;
-              const long long col0 = (long long)t.v * BN + c * EPI_COLS;
-              if (p.addend_map) {  // gathered rows (fused gather backward): sum_j addend[map[trow*k+j]]
-#pragma unroll
-                for (int i = 0; i < 32; ++i) add_f[i] = 0.f;
-                for (int j = 0; j < p.addend_k; ++j) {
-                  const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
-                  const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
-#pragma unroll
-                  for (int q2 = 0; q2 < 4; ++q2) {
-                    float af[8];
-                    unpack8(__ldg(src + q2), af);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) add_f[8 * q2 + e] += af[e];
-                  }
-                }
-              } else {
-                const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + col0);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) add_raw[j] = __ldg(src + j);
-              }
-            }
-          }
           if (has_acc) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c * EPI_COLS, r);
-            tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rn[i]);
+            if (c + NG < NCHUNK) tmem_ld32(taddr + (c + NG) * EPI_COLS, rn);  // next chunk, in flight
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -434,42 +444,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           out_coords(p, MODE, t, c, row0, BN, x, y);
           if (p.epi == EPI_ACT_FWD) {
             if (p.has_pre) store_chunk(&tmap_d, v, x, y);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = act_fwd(p.act, v[i]);
+            if (!(p.dbg & 4)) act_fwd32(p.act, v);
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
             mbar_wait(&hb[hslot], hphase[hslot]);
             hphase[hslot] ^= 1;
-            const uint8_t* hrow = hst + hslot * EPI_BUF + lane * 64;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float hf[8];
-              unpack8(*reinterpret_cast<const uint4*>(hrow + swz64(j, lane)), hf);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[8 * j + e] *= act_grad(p.act, hf[e]);
-            }
+            float hf[32];
+            load_row(hst + hslot * EPI_BUF, lane, hf);
+            if (!(p.dbg & 4)) act_grad_mul32(p.act, v, hf);
             __syncwarp();
             hslot ^= 1;
-            if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);
-          } else if (p.epi == EPI_ADD_ROWS && add_ok) {
-            if (p.addend_map) {
+            if (c + NG < NCHUNK) load_h(t, c + NG, hslot);
+          } else if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
+            // rows to add (router backward: dx += ...)
+            const int trow = t.u * BM + row0 + lane;
+            if (trow < p.rows_valid) {
+              const long long col0 = (long long)t.v * BN + c * EPI_COLS;
+              if (p.addend_map) {  // gathered rows (fused gather backward): sum_j addend[map[trow*k+j]]
+                for (int j = 0; j < p.addend_k; ++j) {
+                  const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
+                  const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += add_f[i];
-            } else {
+                  for (int q2 = 0; q2 < 4; ++q2) {
+                    float af[8];
+                    unpack8(__ldg(src + q2), af);
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                float af[8];
-                unpack8(add_raw[j], af);
+                    for (int e = 0; e < 8; ++e) v[8 * q2 + e] += af[e];
+                  }
+                }
+              } else {
+                const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + col0);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[8 * j + e] += af[e];
+                for (int q2 = 0; q2 < 4; ++q2) {
+                  float af[8];
+                  unpack8(__ldg(src + q2), af);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) v[8 * q2 + e] += af[e];
+                }
               }
             }
           }
           store_chunk(&tmap_c, v, x, y);
+          if (has_acc && c + NG < NCHUNK) tmem_ld_wait();
         }
-      } else if (p.epi == EPI_ROUTER) {
+      } else if (MODE == DENSE && p.epi == EPI_ROUTER) {
         // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e),
-        // softmax gates. Column-half 0 warps own whole rows.
-        if (half == 0) {
+        // softmax gates. Group-0 warps own whole rows.
+        if (grp == 0) {
           const int tok = t.u * BM + row0 + lane;
           const bool valid = tok < p.rows_valid;
           float bv[kMaxRouterTopK];
@@ -533,11 +553,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-      } else {  // EPI_F32: fp32 partial tile (split-K)
+      } else if (MODE == DENSE) {  // EPI_F32: fp32 partial tile (split-K)
         const int r = t.u * BM + row0 + lane;
         float* dst = p.out_f32 + (long long)t.s * p.split_stride + (long long)r * p.ld_f32 + t.v * BN;
 #pragma unroll 1
-        for (int c = half; c < BN / 32; c += 2) {
+        for (int c = grp; c < BN / 32; c += NG) {
           uint32_t rr[32];
           if (has_acc) {  // warp-uniform: every lane takes part in the collective TMEM load
             tmem_ld32(taddr + c * 32, rr);
@@ -576,9 +596,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 
+// Experiment knobs for A/B timing (MOE_GEMM_DBG, see GemmParams::dbg); 0 in production.
+int gemm_dbg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_GEMM_DBG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
-  using C = Cfg<BN, EPI_H>;
+  using C = Cfg<MODE, BN, EPI_H>;
   auto kern = bsgemm_kernel<MODE, A_MN, B_MN, BN, EPI_H>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -589,7 +619,9 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   int grid = moe_device_sm_count();
   if (L.max_tiles < grid) grid = L.max_tiles;
   if (grid < 1) grid = 1;
-  kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, L.p);
+  GemmParams p = L.p;
+  p.dbg = gemm_dbg();
+  kern<<<grid, C::THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, p);
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
 }

@@ -47,6 +47,8 @@ struct GemmParams {
   long long ld_add;
   const int32_t* addend_map;
   int addend_k;
+  int dbg;  // experiment knobs (MOE_GEMM_DBG): 1 = no epilogue work, 2 = no MMA, 4 = no activation
+           // math, 8 = no TMA loads, 64 = epilogue decoupled from the accumulator (timing only)
 };
 
 // Router backward on tcgen05 (router.cu): dWr = x^T . dlogits and
@@ -67,6 +69,7 @@ struct GemmLaunch {
 };
 
 moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
+int gemm_dbg();
 // CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
 // 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);

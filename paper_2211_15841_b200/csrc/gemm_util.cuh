@@ -68,13 +68,51 @@ __device__ __forceinline__ int swz64(int j, int row) { return (j ^ ((row >> 1) &
 
 // Write 32 fp32 values of this thread's row as bf16 into a 64B-swizzled
 // [32 rows][64 B] staging buffer (row = lane): conflict-free 16-byte stores.
+// Explicit st.shared (a generic store would force a full MEMBAR before the
+// async-proxy fence).
 __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
-  uint8_t* row = buf + lane * 64;
+  const uint32_t row = smem_u32(buf) + lane * 64;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint4 w = make_uint4(pack_bf16x2(v[8 * j + 0], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
-                               pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
-    *reinterpret_cast<uint4*>(row + swz64(j, lane)) = w;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + swz64(j, lane)),
+                 "r"(pack_bf16x2(v[8 * j + 0], v[8 * j + 1])), "r"(pack_bf16x2(v[8 * j + 2], v[8 * j + 3])),
+                 "r"(pack_bf16x2(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16x2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+  }
+}
+// Read this thread's 32 bf16 values back from a 64B-swizzled staging row.
+__device__ __forceinline__ void load_row(const uint8_t* buf, int lane, float* f) {
+  const uint32_t row = smem_u32(buf) + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 w;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(row + swz64(j, lane))
+                 : "memory");
+    unpack8(w, f + 8 * j);
+  }
+}
+
+// Activation over a 32-value chunk with the kind hoisted out of the element
+// loop (independent elements -> the SFU latency is overlapped).
+__device__ __forceinline__ void act_fwd32(int kind, float* v) {
+  if (kind == MOE_ACT_GELU_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = act_fwd(MOE_ACT_GELU_TANH, v[i]);
+  } else if (kind == MOE_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = act_fwd(MOE_ACT_RELU, v[i]);
+  }
+}
+// v *= act'(h) over a 32-value chunk.
+__device__ __forceinline__ void act_grad_mul32(int kind, float* v, const float* h) {
+  if (kind == MOE_ACT_GELU_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= act_grad(MOE_ACT_GELU_TANH, h[i]);
+  } else if (kind == MOE_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= act_grad(MOE_ACT_RELU, h[i]);
   }
 }
 
