@@ -145,8 +145,8 @@ class Step:
             ("router", L.moe_router, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), d(sv.gates), ws, s)),
             ("topology", L.moe_topology, (c, d(sv.expert_idx), topo, ws, s)),
             ("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
-            ("sdd", L.moe_sdd, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
-                                None if idn else d(sv.h_pre), s)),
+            ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
+                                      None if idn else d(sv.act_deriv), s)),
             ("dsd", L.moe_dsd, (c, d(sv.a), 0, d(t["w2"]), 0, topo, d(sv.y_g), s)),
             ("scatter", L.moe_scatter, (c, d(sv.y_g), topo, d(sv.gates), d(t["y"]), s)),
         ]
@@ -159,8 +159,8 @@ class Step:
             bwd = [("scatter_bwd", L.moe_scatter_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"],
                                                        wsl["dgates"], s))]
         bwd += [
-            ("sddT", L.moe_sdd, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act, None if idn else d(sv.h_pre),
-                                 wsl["dh"], None, s)),
+            ("sddT", L.moe_sdd_deriv, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act,
+                                       None if idn else d(sv.act_deriv), wsl["dh"], None, s)),
             ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
             ("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
             ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),

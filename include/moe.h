@@ -200,6 +200,17 @@ moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const
 moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b,
                    const moe_topology_t* topo, int32_t act, const void* act_grad_src, void* out_s,
                    void* out_pre, void* stream);
+/* moe_sdd_deriv: the layer's form of moe_sdd, saving the activation
+ * derivative instead of the pre-activation (reading R18 in DESIGN.md).
+ *   deriv_src == NULL (forward): out_s = act(A.B) and, if out_deriv
+ *     != NULL, out_deriv = act'(A.B) [nnz,bs,bs] bf16 (one tanh serves both).
+ *   deriv_src != NULL (SDD^T): out_s = (A.B) * deriv_src, deriv_src
+ *     being the saved act'(H).
+ *   deriv_src and out_deriv are exclusive (MOE_EINVAL). Shapes, layouts and
+ *   errors as moe_sdd. */
+moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                         const moe_topology_t* topo, int32_t act, const void* deriv_src, void* out_s,
+                         void* out_deriv, void* stream);
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream);
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
@@ -252,7 +263,7 @@ typedef struct {
   float* gates;       /* [T, k] fp32 */
   moe_topology_t topo;
   void* x_g;          /* [max_rows, h] bf16 */
-  void* h_pre;        /* [max_nnz, bs, bs] bf16 pre-activation (may equal a for identity) */
+  void* act_deriv;    /* [max_nnz, bs, bs] bf16 act'(pre-activation); unused (NULL) for identity */
   void* a;            /* [max_nnz, bs, bs] bf16 activation */
   void* y_g;          /* [max_rows, h] bf16 */
 } moe_saved;

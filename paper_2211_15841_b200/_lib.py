@@ -39,7 +39,7 @@ class MoeGrads(ctypes.Structure):
 
 class MoeSaved(ctypes.Structure):
     _fields_ = [("logits", ctypes.c_void_p), ("expert_idx", ctypes.c_void_p), ("gates", ctypes.c_void_p),
-                ("topo", MoeTopology), ("x_g", ctypes.c_void_p), ("h_pre", ctypes.c_void_p),
+                ("topo", MoeTopology), ("x_g", ctypes.c_void_p), ("act_deriv", ctypes.c_void_p),
                 ("a", ctypes.c_void_p), ("y_g", ctypes.c_void_p)]
 
 
@@ -69,6 +69,7 @@ SIGNATURES = {
     "moe_unsort_rows_bwd": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
     "moe_sort_rows_bwd": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_sdd": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
+    "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_dds": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),

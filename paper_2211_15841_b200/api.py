@@ -176,6 +176,16 @@ def moe_sdd(cfg, a, b, trans_b, topo: Topology, act=ACT_IDENTITY, act_grad_src=N
     return (out, pre) if want_pre else out
 
 
+def moe_sdd_deriv(cfg, a, b, trans_b, topo: Topology, act=ACT_IDENTITY, deriv_src=None, want_deriv=False, out=None):
+    """moe_sdd_deriv (include/moe.h): forward returns act(A.B) [and act'(A.B)];
+    with deriv_src (the saved act'(H)) returns (A.B) * deriv_src (SDD^T)."""
+    out = out if out is not None else _nnz_values(cfg, a.device)
+    der = _nnz_values(cfg, a.device) if want_deriv else None
+    check("moe_sdd_deriv", lib.moe_sdd_deriv(ctypes.byref(cfg), _p(a), _p(b), int(trans_b), ctypes.byref(topo.struct),
+                                             int(act), _p(deriv_src), _p(out), _p(der), _stream()))
+    return (out, der) if want_deriv else out
+
+
 def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
     rows = moe_max_padded_rows(cfg)
     n_out = cfg.num_experts * cfg.ffn_hidden if trans_s else rows
@@ -209,7 +219,7 @@ class Saved:
     gates: torch.Tensor
     topo: Topology
     x_g: torch.Tensor
-    h_pre: torch.Tensor | None
+    act_deriv: torch.Tensor | None
     a: torch.Tensor
     y_g: torch.Tensor
     struct: MoeSaved = None
@@ -227,7 +237,7 @@ class Saved:
                   _nnz_values(cfg, device),
                   torch.empty(rows, h, dtype=torch.bfloat16, device=device))
         s.struct = MoeSaved(s.logits.data_ptr(), s.expert_idx.data_ptr(), s.gates.data_ptr(), s.topo.struct,
-                            s.x_g.data_ptr(), None if s.h_pre is None else s.h_pre.data_ptr(), s.a.data_ptr(),
+                            s.x_g.data_ptr(), None if s.act_deriv is None else s.act_deriv.data_ptr(), s.a.data_ptr(),
                             s.y_g.data_ptr())
         return s
 

@@ -40,7 +40,7 @@
 #include "tma.cuh"
 
 #ifndef MOE_SDD_EPW
-#define MOE_SDD_EPW 16
+#define MOE_SDD_EPW 8
 #endif
 #ifndef MOE_SDD_NBUF
 #define MOE_SDD_NBUF 2
@@ -443,14 +443,25 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           int x, y;
           out_coords(p, MODE, t, c, row0, BN, x, y);
           if (p.epi == EPI_ACT_FWD) {
-            if (p.has_pre) store_chunk(&tmap_d, v, x, y);
-            if (!(p.dbg & 4)) act_fwd32(p.act, v);
+            if (p.has_pre && p.aux_deriv) {  // save act'(H) beside act(H)
+              float g[32];
+              act_fwd_deriv32(p.act, v, g);
+              store_chunk(&tmap_d, g, x, y);
+            } else {
+              if (p.has_pre) store_chunk(&tmap_d, v, x, y);
+              if (!(p.dbg & 4)) act_fwd32(p.act, v);
+            }
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
             mbar_wait(&hb[hslot], hphase[hslot]);
             hphase[hslot] ^= 1;
             float hf[32];
             load_row(hst + hslot * EPI_BUF, lane, hf);
-            if (!(p.dbg & 4)) act_grad_mul32(p.act, v, hf);
+            if (p.aux_deriv) {  // the source already holds act'(H)
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= hf[i];
+            } else if (!(p.dbg & 4)) {
+              act_grad_mul32(p.act, v, hf);
+            }
             __syncwarp();
             hslot ^= 1;
             if (c + NG < NCHUNK) load_h(t, c + NG, hslot);
@@ -712,17 +723,18 @@ using namespace moe;
 
 extern "C" {
 
-moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b, const moe_topology_t* topo,
-                   int32_t act, const void* act_grad_src, void* out_s, void* out_pre, void* stream) {
+static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                             const moe_topology_t* topo, int32_t act, const void* act_src, void* out_s, void* out_aux,
+                             bool deriv, void* stream) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(a && b && out_s, "moe_sdd: NULL operand");
   MOE_CHECK_ARG(act >= 0 && act <= 2, "moe_sdd: bad act %d", act);
-  const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
+  const int64_t nnz = moe_max_nnz_blocks(cfg);
+  const int64_t rows = moe_max_padded_rows(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
   // Row-pair 2-SM tiles measured slower for SDD at MoE-XS (half-empty pairs of
   // odd-row experts); the 1-SM 128 x 256 kernel is used.
-  const bool pair = false;
   GemmLaunch L{};
   L.name = trans_b ? "moe_sdd(T)" : "moe_sdd";
   L.mode = SDD;
@@ -731,21 +743,33 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
   L.b_mn = !trans_b;
   L.p = gemm_params_topo(cfg, topo);
   L.p.act = act;
-  L.p.epi = act_grad_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_pre) ? EPI_ACT_FWD : EPI_STORE);
-  L.p.has_pre = out_pre != nullptr;
+  L.p.epi = act_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_aux) ? EPI_ACT_FWD : EPI_STORE);
+  L.p.has_pre = out_aux != nullptr;
+  L.p.aux_deriv = deriv ? 1 : 0;
   L.epi_h = L.p.epi == EPI_ACT_BWD;
-  L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
-  const int bbox = pair ? 128 : L.bn;
+  L.max_tiles = (int)(nnz / (L.bn / 128));
   MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 128, "moe_sdd a"));
   if (!trans_b)
     MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, 64, "moe_sdd b"));
   else
-    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, bbox, "moe_sdd b^T"));
+    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
-  if (out_pre) MOE_TRY(make_tmap_epi(&L.td, out_pre, 128, nnz * 128, 128, "moe_sdd pre"));
-  if (act_grad_src) MOE_TRY(make_tmap_epi(&L.td, act_grad_src, 128, nnz * 128, 128, "moe_sdd act src"));
-  if (!out_pre && !act_grad_src) L.td = L.tc;
+  if (out_aux) MOE_TRY(make_tmap_epi(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
+  if (act_src) MOE_TRY(make_tmap_epi(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
+  if (!out_aux && !act_src) L.td = L.tc;
   return gemm_launch(L, as_stream(stream));
+}
+
+moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b, const moe_topology_t* topo,
+                   int32_t act, const void* act_grad_src, void* out_s, void* out_pre, void* stream) {
+  return sdd_launch(cfg, a, b, trans_b, topo, act, act_grad_src, out_s, out_pre, false, stream);
+}
+
+moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                         const moe_topology_t* topo, int32_t act, const void* deriv_src, void* out_s,
+                         void* out_deriv, void* stream) {
+  MOE_CHECK_ARG(!(deriv_src && out_deriv), "moe_sdd_deriv: deriv_src and out_deriv are exclusive");
+  return sdd_launch(cfg, a, b, trans_b, topo, act, deriv_src, out_s, out_deriv, true, stream);
 }
 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,

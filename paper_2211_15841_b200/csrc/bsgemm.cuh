@@ -32,6 +32,7 @@ struct GemmParams {
   int m_tiles, n_tiles, splits, kiters_split, k_iters_total;
   // epilogue
   int epi, act, has_pre;
+  int aux_deriv;  // EPI_ACT_FWD: the aux output is act'(H), not H; EPI_ACT_BWD: the source holds act'(H)
   int rows_valid;  // rows of the output that exist (DENSE: M)
   // EPI_ROUTER
   float* logits;

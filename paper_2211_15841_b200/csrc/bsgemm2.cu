@@ -361,14 +361,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           int x, y;
           out_coords2(p, MODE, t, rank, c, row0, p.F, x, y);
           if (p.epi == EPI_ACT_FWD) {
-            if (p.has_pre) store_chunk(&tmap_d, v, x, y);
-            act_fwd32(p.act, v);
+            if (p.has_pre && p.aux_deriv) {
+              float g[32];
+              act_fwd_deriv32(p.act, v, g);
+              store_chunk(&tmap_d, g, x, y);
+            } else {
+              if (p.has_pre) store_chunk(&tmap_d, v, x, y);
+              act_fwd32(p.act, v);
+            }
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
             mbar_wait(&hb[hslot], hphase[hslot]);
             hphase[hslot] ^= 1;
             float hf[32];
             load_row(hst + hslot * EPI_BUF, lane, hf);
-            act_grad_mul32(p.act, v, hf);
+            if (p.aux_deriv) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= hf[i];
+            } else {
+              act_grad_mul32(p.act, v, hf);
+            }
             __syncwarp();
             hslot ^= 1;
             if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);

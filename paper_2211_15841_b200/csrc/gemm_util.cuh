@@ -105,6 +105,32 @@ __device__ __forceinline__ void act_fwd32(int kind, float* v) {
     for (int i = 0; i < 32; ++i) v[i] = act_fwd(MOE_ACT_RELU, v[i]);
   }
 }
+// v <- act(v) and g <- act'(v) over a 32-value chunk (one tanh per element
+// serves both; the forward saves g for the SDD^T epilogue).
+__device__ __forceinline__ void act_fwd_deriv32(int kind, float* v, float* g) {
+  if (kind == MOE_ACT_GELU_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = v[i];
+      const float x2 = x * x;
+      const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
+      const float t = tanh_fast(u);
+      const float du = fmaf(0.7978845608028654f * 3.0f * 0.044715f, x2, 0.7978845608028654f);
+      const float hx = 0.5f * x;
+      v[i] = fmaf(hx, t, hx);
+      g[i] = fmaf(hx * du, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
+    }
+  } else if (kind == MOE_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      g[i] = v[i] > 0.f ? 1.f : 0.f;
+      v[i] = v[i] > 0.f ? v[i] : 0.f;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) g[i] = 1.f;
+  }
+}
 // v *= act'(h) over a 32-value chunk.
 __device__ __forceinline__ void act_grad_mul32(int kind, float* v, const float* h) {
   if (kind == MOE_ACT_GELU_TANH) {

@@ -18,15 +18,16 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   MOE_CHECK_ARG(sv->logits && sv->expert_idx && sv->gates && sv->x_g && sv->a && sv->y_g,
                 "moe_forward: NULL saved tensor");
   const bool id = cfg->act == MOE_ACT_IDENTITY;
-  MOE_CHECK_ARG(id || sv->h_pre, "moe_forward: saved->h_pre required for a non-identity activation");
+  MOE_CHECK_ARG(id || sv->act_deriv, "moe_forward: saved->act_deriv required for a non-identity activation");
   // (1) indices, weights = router(x)
   MOE_TRY(moe_router(cfg, x, w->wr, sv->logits, sv->expert_idx, sv->gates, ws, stream));
   // (2) topology = make_topology(indices)
   MOE_TRY(moe_topology(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
   MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
-  // (4) x = sdd(x, w1, topology) [+ act]; x = dsd(x, w2)
-  MOE_TRY(moe_sdd(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->h_pre, stream));
+  // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
+  MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
+                        stream));
   MOE_TRY(moe_dsd(cfg, sv->a, 0, w->w2, 0, &sv->topo, sv->y_g, stream));
   // (5) x = padded_scatter(x, indices) * weights
   MOE_TRY(moe_scatter(cfg, sv->y_g, &sv->topo, sv->gates, y, stream));
@@ -57,8 +58,7 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
     MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
   }
   // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
-  MOE_TRY(moe_sdd(cfg, dy_g, w->w2, 1, topo, id ? MOE_ACT_IDENTITY : cfg->act, id ? nullptr : sv->h_pre, dh,
-                  nullptr, stream));
+  MOE_TRY(moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream));
   // b3: DS^TD: dW2 = A^T . dY_g                              "second layer weight gradient"
   MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
   // b4: DSD^T: dX_g = dH . W1^T                              "first layer data gradient"

@@ -72,7 +72,7 @@ class EPState:
     sends: list
     recvs: list
     x_g: torch.Tensor | None
-    h_pre: torch.Tensor | None
+    act_deriv: torch.Tensor | None
     a: torch.Tensor | None
     y_sorted: torch.Tensor
     n_recv: int
@@ -122,14 +122,14 @@ class ExpertParallelMoE:
         self._a2a(recv_x, x_sorted, recvs, sends)
         # (4) local experts: topology over E_l experts, padded gather, SDD(+act), DSD, un-pad
         cfg_e = self._cfg(n_recv, self.El, 1)
-        topo_e = x_g = h_pre = a = None
+        topo_e = x_g = act_deriv = a = None
         y_recv = x.new_empty(n_recv, self.h)
         if n_recv > 0:
             ids = torch.from_numpy(recv_ids).to(x.device)
             topo_e = B.moe_topology(cfg_e, ids)
             x_g = B.moe_gather(cfg_e, recv_x, topo_e)
             if self.act != 0:
-                a, h_pre = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_pre=True)
+                a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
             else:
                 a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
             y_g = B.moe_dsd(cfg_e, a, 0, w2_local, 0, topo_e)
@@ -138,7 +138,7 @@ class ExpertParallelMoE:
         y_sorted = x.new_empty(T * self.k, self.h)
         self._a2a(y_sorted, y_recv, sends, recvs)
         y = B.moe_unsort_rows(cfg_l, y_sorted, topo_l, gates)
-        st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, sends, recvs, x_g, h_pre, a, y_sorted, n_recv)
+        st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, sends, recvs, x_g, act_deriv, a, y_sorted, n_recv)
         return y, st
 
     def backward(self, st: EPState, x, dy, wr, w1_local, w2_local):
@@ -154,7 +154,7 @@ class ExpertParallelMoE:
         if st.n_recv > 0:
             dy_g = B.moe_gather(cfg_e, dy_recv, st.topo_e)
             if self.act != 0:
-                dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, act_grad_src=st.h_pre)
+                dh = B.moe_sdd_deriv(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, deriv_src=st.act_deriv)
             else:
                 dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e)
             B.moe_dsd(cfg_e, st.a, 1, dy_g, 0, st.topo_e, out=dw2)

@@ -63,6 +63,14 @@ def moe_sdd(cfg, a, b, trans_b, topo, act=0, act_grad_src=None, want_pre=False, 
     return (_t(A), _t(H)) if want_pre else _t(A)
 
 
+def moe_sdd_deriv(cfg, a, b, trans_b, topo, act=0, deriv_src=None, want_deriv=False, out=None):
+    H = O.sdd(_np(a), _np(b), topo.topo, trans_b=bool(trans_b))
+    if deriv_src is not None:
+        return _t(H * _np(deriv_src))
+    A = O.act(act, H)
+    return (_t(A), _t(O.act_grad(act, H))) if want_deriv else _t(A)
+
+
 def moe_dsd(cfg, s, trans_s, b, trans_b, topo, out=None):
     r = _t(O.dsd(_np(s), _np(b), topo.topo, trans_s=bool(trans_s), trans_b=bool(trans_b)))
     if out is not None:

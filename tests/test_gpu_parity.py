@@ -278,6 +278,14 @@ def test_six_products(case):
     dA = O.sdd(S.to_f64(dyg[:Tp]), S.to_f64(w2), topo, trans_b=True)
     dH = dA * O.act_grad(O.ACT_GELU, f64(h_s[:nnz]))
     assert rel_fro(f64(dh[:nnz]), dH) < FRO_TOL
+    # the layer's form (reading R18): forward saves act'(H); SDD^T multiplies by it
+    a_d, g_d = A.moe_sdd_deriv(cfg, xg, w1.to(d), 0, tg, act=A.ACT_GELU, want_deriv=True)
+    assert rel_fro(f64(a_d[:nnz]), Aact) < FRO_TOL
+    assert rel_fro(f64(g_d[:nnz]), O.act_grad(O.ACT_GELU, H)) < FRO_TOL
+    dh_d = A.moe_sdd_deriv(cfg, dyg.to(d), w2.to(d), 1, tg, act=A.ACT_GELU, deriv_src=g_d)
+    assert rel_fro(f64(dh_d[:nnz]), dA * O.act_grad(O.ACT_GELU, H)) < FRO_TOL
+    a_r, g_r = A.moe_sdd_deriv(cfg, xg, w1.to(d), 0, tg, act=A.ACT_RELU, want_deriv=True)
+    np.testing.assert_array_equal(f64(g_r[:nnz]), (f64(s_plain[:nnz]) > 0).astype(np.float64))
     # DS^TD: dW2 = A^T . dY_g
     dw2 = A.moe_dsd(cfg, a_s, 1, dyg.to(d), 0, tg)
     want = O.dsd(f64(a_s[:nnz]), S.to_f64(dyg[:Tp]), topo, trans_s=True)
