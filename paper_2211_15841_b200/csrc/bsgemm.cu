@@ -69,7 +69,8 @@ struct Cfg {
   static constexpr int EPI = EPW * NBUF * EPI_BUF;  // per-warp staging ring
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int H_BYTES = EPI_H ? EPI : 0;
+  static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
+  static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
@@ -240,8 +241,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* hbar = tempty + 2;  // [EPW][2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * EPW);
+  uint64_t* hbar = tempty + 2;  // [EPW][NH]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + C::NH * EPW);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], EPW);
     }
-    for (int i = 0; i < 2 * EPW; ++i) mbar_init(&hbar[i], 1);
+    for (int i = 0; i < C::NH * EPW; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -375,10 +376,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     const int grp = wq >> 2;
     const int row0 = q * 32;
     uint8_t* stg = smem_epi + wq * C::NBUF * EPI_BUF;
-    uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
-    uint64_t* hb = hbar + wq * 2;
-    uint32_t hphase[2] = {0, 0};
-    int hslot = 0;
+    uint8_t* hst = smem_h + wq * C::NH * EPI_BUF;
+    uint64_t* hb = hbar + wq * C::NH;
     int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -396,20 +395,30 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       }
       sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
     };
-    auto load_h = [&](const TileInfo& t, int c, int b) {
-      if (lane == 0) {
+    // SDD^T: this warp's act'(H) chunks form one sequence j = 0, 1, ... over
+    // its tiles (tile blockIdx.x + (j / NPW) * gridDim.x, chunk grp + (j % NPW) * NG),
+    // prefetched NH ahead into a ring, so the loads overlap the main loop.
+    constexpr int NPW_ = NCHUNK / NG;
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int hseq_end = my_tiles * NPW_;
+    int hseq = 0;  // next item to consume
+    auto load_h = [&](int j) {
+      if (j < hseq_end && lane == 0) {
         fence_proxy_async_smem();  // prior generic reads of this buffer before the async write
+        const TileInfo tj = decode(p, MODE, PAIR, (int)blockIdx.x + (j / NPW_) * (int)gridDim.x);
         int x, y;
-        out_coords(p, MODE, t, c, row0, BN, x, y);
+        out_coords(p, MODE, tj, grp + (j % NPW_) * NG, row0, BN, x, y);
+        const int b = j % C::NH;
         mbar_arrive_expect_tx(&hb[b], EPI_BUF);
         tma_load_2d(hst + b * EPI_BUF, &tmap_d, &hb[b], x, y);
       }
     };
+    if (EPI_H && p.epi == EPI_ACT_BWD)
+      for (int j = 0; j < C::NH; ++j) load_h(j);
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo t = decode(p, MODE, PAIR, tile);
       const bool has_acc = (p.dbg & 64) ? false : t.kiters > 0;
-      if (EPI_H && p.epi == EPI_ACT_BWD) load_h(t, grp, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -424,21 +433,26 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           if (r[0] == 0x7fffffffu && r[1] == 0x12345u) p.gates[0] = 1.f;
         }
       } else if (bf16_out) {
-        uint32_t rn[32];
-        if (has_acc && grp < NCHUNK) {
-          tmem_ld32(taddr + grp * EPI_COLS, rn);
+        // NPW chunks per warp, fully unrolled with ping-pong TMEM registers
+        // (the next chunk's tcgen05.ld is in flight while this one is processed).
+        constexpr int NPW = NCHUNK / NG;
+        static_assert(NCHUNK % NG == 0, "chunks must divide evenly over the epilogue warps");
+        uint32_t rr[2][32];
+        if (has_acc) {
+          tmem_ld32(taddr + grp * EPI_COLS, rr[0]);
           tmem_ld_wait();
         }
-#pragma unroll 1
-        for (int c = grp; c < NCHUNK; c += NG) {
+#pragma unroll
+        for (int i = 0; i < NPW; ++i) {
+          const int c = grp + i * NG;
           float v[32];
           if (has_acc) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rn[i]);
-            if (c + NG < NCHUNK) tmem_ld32(taddr + (c + NG) * EPI_COLS, rn);  // next chunk, in flight
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[i & 1][e]);
+            if (i + 1 < NPW) tmem_ld32(taddr + (c + NG) * EPI_COLS, rr[(i + 1) & 1]);  // next chunk, in flight
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int e = 0; e < 32; ++e) v[e] = 0.f;
           }
           int x, y;
           out_coords(p, MODE, t, c, row0, BN, x, y);
@@ -452,19 +466,18 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               if (!(p.dbg & 4)) act_fwd32(p.act, v);
             }
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
-            mbar_wait(&hb[hslot], hphase[hslot]);
-            hphase[hslot] ^= 1;
+            const int hb_i = hseq % C::NH;
+            mbar_wait(&hb[hb_i], (uint32_t)(hseq / C::NH) & 1u);
             float hf[32];
-            load_row(hst + hslot * EPI_BUF, lane, hf);
+            load_row(hst + hb_i * EPI_BUF, lane, hf);
             if (p.aux_deriv) {  // the source already holds act'(H)
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= hf[i];
+              mul32(v, hf);
             } else if (!(p.dbg & 4)) {
               act_grad_mul32(p.act, v, hf);
             }
             __syncwarp();
-            hslot ^= 1;
-            if (c + NG < NCHUNK) load_h(t, c + NG, hslot);
+            load_h(hseq + C::NH);  // refill the buffer just read
+            ++hseq;
           } else if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
             // rows to add (router backward: dx += ...)
             const int trow = t.u * BM + row0 + lane;
@@ -495,7 +508,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             }
           }
           store_chunk(&tmap_c, v, x, y);
-          if (has_acc && c + NG < NCHUNK) tmem_ld_wait();
+          if (has_acc && i + 1 < NPW) tmem_ld_wait();
         }
       } else if (MODE == DENSE && p.epi == EPI_ROUTER) {
         // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e),

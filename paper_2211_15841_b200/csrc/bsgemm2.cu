@@ -375,8 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             float hf[32];
             load_row(hst + hslot * EPI_BUF, lane, hf);
             if (p.aux_deriv) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= hf[i];
+              mul32(v, hf);
             } else {
               act_grad_mul32(p.act, v, hf);
             }

@@ -2,6 +2,7 @@
 // (bsgemm.cu) and CTA-pair (bsgemm2.cu) tcgen05 GEMM kernels.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/moe.h"
@@ -106,19 +107,29 @@ __device__ __forceinline__ void act_fwd32(int kind, float* v) {
   }
 }
 // v <- act(v) and g <- act'(v) over a 32-value chunk (one tanh per element
-// serves both; the forward saves g for the SDD^T epilogue).
+// serves both; the forward saves g for the SDD^T epilogue). gelu runs on the
+// packed fp32x2 pipe (FFMA2/FMUL2: half the issue slots, same fp32 rounding).
 __device__ __forceinline__ void act_fwd_deriv32(int kind, float* v, float* g) {
   if (kind == MOE_ACT_GELU_TANH) {
+    const float2 c0 = make_float2(0.7978845608028654f, 0.7978845608028654f);
+    const float2 c1 = make_float2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+    const float2 c3 = make_float2(0.7978845608028654f * 3.0f * 0.044715f, 0.7978845608028654f * 3.0f * 0.044715f);
+    const float2 half = make_float2(0.5f, 0.5f), one = make_float2(1.f, 1.f);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float x = v[i];
-      const float x2 = x * x;
-      const float u = x * fmaf(0.7978845608028654f * 0.044715f, x2, 0.7978845608028654f);
-      const float t = tanh_fast(u);
-      const float du = fmaf(0.7978845608028654f * 3.0f * 0.044715f, x2, 0.7978845608028654f);
-      const float hx = 0.5f * x;
-      v[i] = fmaf(hx, t, hx);
-      g[i] = fmaf(hx * du, fmaf(-t, t, 1.0f), fmaf(0.5f, t, 0.5f));
+    for (int i = 0; i < 32; i += 2) {
+      const float2 x = make_float2(v[i], v[i + 1]);
+      const float2 x2 = __fmul2_rn(x, x);
+      const float2 u = __fmul2_rn(x, __ffma2_rn(c1, x2, c0));
+      const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+      const float2 du = __ffma2_rn(c3, x2, c0);
+      const float2 hx = __fmul2_rn(half, x);
+      const float2 a = __ffma2_rn(hx, t, hx);
+      const float2 omt2 = __ffma2_rn(make_float2(-t.x, -t.y), t, one);
+      const float2 gd = __ffma2_rn(__fmul2_rn(hx, du), omt2, __ffma2_rn(half, t, half));
+      v[i] = a.x;
+      v[i + 1] = a.y;
+      g[i] = gd.x;
+      g[i + 1] = gd.y;
     }
   } else if (kind == MOE_ACT_RELU) {
 #pragma unroll
@@ -129,6 +140,15 @@ __device__ __forceinline__ void act_fwd_deriv32(int kind, float* v, float* g) {
   } else {
 #pragma unroll
     for (int i = 0; i < 32; ++i) g[i] = 1.f;
+  }
+}
+// v *= g over a 32-value chunk (packed fp32x2 multiplies).
+__device__ __forceinline__ void mul32(float* v, const float* g) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float2 r = __fmul2_rn(make_float2(v[i], v[i + 1]), make_float2(g[i], g[i + 1]));
+    v[i] = r.x;
+    v[i + 1] = r.y;
   }
 }
 // v *= act'(h) over a 32-value chunk.
