@@ -31,6 +31,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <float.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "bsgemm.cuh"
@@ -41,6 +42,9 @@
 
 #ifndef MOE_SDD_EPW
 #define MOE_SDD_EPW 8
+#endif
+#ifndef MOE_GEMM_NP
+#define MOE_GEMM_NP 2
 #endif
 #ifndef MOE_SDD_NBUF
 #define MOE_SDD_NBUF 2
@@ -64,7 +68,10 @@ __host__ __device__ constexpr int epi_bufs(int mode, int bn, bool epi_h) {
 template <int MODE, int BN, bool EPI_H>
 struct Cfg {
   static constexpr int EPW = epi_warps(MODE, BN, EPI_H);
-  static constexpr int THREADS = 64 + 32 * EPW;
+  static constexpr int NP = MOE_GEMM_NP;           // TMA producer warps (stage s is issued by warp s % NP)
+  static constexpr int MMA_WARP = NP;
+  static constexpr int EPI_WARP0 = NP + 1;
+  static constexpr int THREADS = 32 * (NP + 1 + EPW);
   static constexpr int NBUF = epi_bufs(MODE, BN, EPI_H);
   static constexpr int EPI = EPW * NBUF * EPI_BUF;  // per-warp staging ring
   static constexpr int B_BYTES = BN * BK * 2;
@@ -78,6 +85,14 @@ struct Cfg {
   static_assert(STAGES >= 2, "not enough shared memory for two stages");
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
+
+__device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev) {
+  if (p.trace && tile_i < kTraceTiles) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[((size_t)blockIdx.x * kTraceTiles + tile_i) * kTraceEvents + ev] = t;
+  }
+}
 
 __device__ __forceinline__ int num_tiles(const GemmParams& p, int mode, int pair) {
   const int Tp = p.sizes ? p.sizes[0] : 0, nnz = p.sizes ? p.sizes[1] : 0;
@@ -152,71 +167,60 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
   }
 }
 
-// Issue the TMA boxes of K-step `kit` of tile t: into the smem stage (PF =
-// false, completion on mbarrier fb) or as L2 prefetches (PF = true).
-template <int MODE, bool A_MN, bool B_MN, int BN, bool PF>
+// Issue the TMA boxes of K-step `kit` of tile t into the smem stage
+// (completion on mbarrier fb). K-major operands are one 2-D box; MN-major
+// operands are one 3-D box {64 elements, 64 K-rows, chunks} whose smem image is
+// the [chunk][64 rows][128 B] layout of the MN-major UMMA descriptor (one TMA
+// instruction per operand: the per-SM TMA issue rate, not bytes, limits small
+// boxes; see scripts/micro/l2_tma_bw.cu).
+template <int MODE, bool A_MN, bool B_MN, int BN>
 __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p,
                                             const TileInfo& t, int kit, int sblk, int oblk, uint8_t* sa, uint8_t* sb,
                                             uint64_t* fb) {
   const int kk = kit & 1;
   if (MODE == SDD) {
     const int k0 = kit * BK;
-    tma_box<PF>(sa, ta, fb, k0, t.u * BM);
-    if (B_MN) {
-#pragma unroll
-      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * 128 + j * 64, k0);
-    } else {
-      tma_box<PF>(sb, tb, fb, k0, t.v * 128);
-    }
+    tma_load_2d(sa, ta, fb, k0, t.u * BM);
+    if (B_MN)
+      tma_load_3d(sb, tb, fb, 0, k0, t.v * 2);
+    else
+      tma_load_2d(sb, tb, fb, k0, t.v * 128);
   } else if (MODE == DSD_ROW) {
-    tma_box<PF>(sa, ta, fb, kk * BK, sblk * BM);
-    if (B_MN) {
-#pragma unroll
-      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
-    } else {
-      tma_box<PF>(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
-    }
+    tma_load_2d(sa, ta, fb, kk * BK, sblk * BM);
+    if (B_MN)
+      tma_load_3d(sb, tb, fb, 0, oblk * BM + kk * BK, t.v * (BN / 64));
+    else
+      tma_load_2d(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
   } else if (MODE == DS_COL) {
-    tma_box<PF>(sa, ta, fb, 0, sblk * BM + kk * BK);
-    tma_box<PF>(sa + 8192, ta, fb, 64, sblk * BM + kk * BK);
-    if (B_MN) {
-#pragma unroll
-      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, oblk * BM + kk * BK);
-    } else {
-      tma_box<PF>(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
-    }
+    tma_load_3d(sa, ta, fb, 0, sblk * BM + kk * BK, 0);
+    if (B_MN)
+      tma_load_3d(sb, tb, fb, 0, oblk * BM + kk * BK, t.v * (BN / 64));
+    else
+      tma_load_2d(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
   } else if (MODE == DDS_COL) {
-    if (A_MN) {
-      tma_box<PF>(sa, ta, fb, t.v * BM, oblk * BM + kk * BK);
-      tma_box<PF>(sa + 8192, ta, fb, t.v * BM + 64, oblk * BM + kk * BK);
-    } else {
-      tma_box<PF>(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
-    }
+    if (A_MN)
+      tma_load_3d(sa, ta, fb, 0, oblk * BM + kk * BK, t.v * 2);
+    else
+      tma_load_2d(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
 #pragma unroll
-    for (int j = 0; j < BN / 64; ++j)  // blocks (r, c + j/2): storage sblk + j/2
-      tma_box<PF>(sb + j * 8192, tb, fb, (j & 1) * 64, (sblk + (j >> 1)) * BM + kk * BK);
+    for (int j = 0; j < BN / 128; ++j)  // blocks (r, c + j): storage sblk + j
+      tma_load_3d(sb + j * 16384, tb, fb, 0, (sblk + j) * BM + kk * BK, 0);
   } else if (MODE == DDS_ROW) {
-    if (A_MN) {
-      tma_box<PF>(sa, ta, fb, t.v * BM, oblk * BM + kk * BK);
-      tma_box<PF>(sa + 8192, ta, fb, t.v * BM + 64, oblk * BM + kk * BK);
-    } else {
-      tma_box<PF>(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
-    }
-    tma_box<PF>(sb, tb, fb, kk * BK, sblk * BM);
+    if (A_MN)
+      tma_load_3d(sa, ta, fb, 0, oblk * BM + kk * BK, t.v * 2);
+    else
+      tma_load_2d(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
+    tma_load_2d(sb, tb, fb, kk * BK, sblk * BM);
   } else {  // DENSE
     const int k0 = (t.s * p.kiters_split + kit) * BK;
-    if (A_MN) {
-      tma_box<PF>(sa, ta, fb, t.u * BM, k0);
-      tma_box<PF>(sa + 8192, ta, fb, t.u * BM + 64, k0);
-    } else {
-      tma_box<PF>(sa, ta, fb, k0, t.u * BM);
-    }
-    if (B_MN) {
-#pragma unroll
-      for (int j = 0; j < BN / 64; ++j) tma_box<PF>(sb + j * 8192, tb, fb, t.v * BN + j * 64, k0);
-    } else {
-      tma_box<PF>(sb, tb, fb, k0, t.v * BN);
-    }
+    if (A_MN)
+      tma_load_3d(sa, ta, fb, 0, k0, t.u * 2);
+    else
+      tma_load_2d(sa, ta, fb, k0, t.u * BM);
+    if (B_MN)
+      tma_load_3d(sb, tb, fb, 0, k0, t.v * (BN / 64));
+    else
+      tma_load_2d(sb, tb, fb, k0, t.v * BN);
   }
 }
 
@@ -261,19 +265,23 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if (warp == C::MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int ntiles = num_tiles(p, MODE, PAIR);
 
-  if (warp == 0) {
-    // ===================== TMA producer (whole warp walks, lane 0 issues) =====================
+  if (warp < C::NP) {
+    // ===================== TMA producers (each warp walks; lane 0 issues its stages) =====================
+    // One issuing thread sustains only a few TMA boxes in flight; NP warps
+    // share the ring (stage s belongs to warp s % NP).
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const TileInfo t = decode(p, MODE, PAIR, tile);
+    int tile_i = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
+      const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
+      if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit >> 1, kk = kit & 1;
@@ -291,32 +299,14 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
-        // L2 prefetch PF K-steps ahead (no smem cost) to deepen the memory pipeline
-        const int kpf = kit + kPrefetch;
-        const int bpf = kpf >> 1;
-        const bool pf_ok = kpf < t.kiters && (MODE == SDD || MODE == DENSE || (bpf >> 5) == (blk >> 5));
-        const int sblk_pf = __shfl_sync(0xffffffffu, idx_a, bpf & 31);
-        const int oblk_pf = __shfl_sync(0xffffffffu, idx_b, bpf & 31);
-        if (kPrefetch > 0 && kit == 0)  // head of the tile: prefetch K-steps 1 .. PF-1 (warp-uniform loop)
-          for (int k2 = 1; k2 < kPrefetch && k2 < t.kiters; ++k2) {
-            const int s2 = __shfl_sync(0xffffffffu, idx_a, (k2 >> 1) & 31);
-            const int o2 = __shfl_sync(0xffffffffu, idx_b, (k2 >> 1) & 31);
-            if (lane == 0)
-              issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, k2, s2, o2, nullptr, nullptr, nullptr);
-          }
-        if (lane == 0) {
-          if (kPrefetch > 0 && pf_ok)
-            issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, kpf, sblk_pf, oblk_pf, nullptr, nullptr,
-                                                    nullptr);
-        }
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
+        if (stage % C::NP == warp) mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0 && stage % C::NP == warp) {
           uint64_t* fb = &full[stage];
           if (p.dbg & 8) {
             mbar_arrive(fb);
           } else {
             mbar_arrive_expect_tx(fb, C::STAGE);
-            issue_stage<MODE, A_MN, B_MN, BN, false>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+            issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
                                                      smem_b + stage * C::B_BYTES, fb);
           }
         }
@@ -327,7 +317,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == C::MMA_WARP) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
@@ -335,11 +325,14 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int tile_i = -1;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const TileInfo t = decode(p, MODE, PAIR, tile);
+        const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
+        ++tile_i;
         if (t.kiters == 0) continue;
         if (!(p.dbg & 64)) mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        trace_ev(p, tile_i, 1);
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kit = 0; kit < t.kiters; ++kit) {
           mbar_wait(&full[stage], phase);
@@ -361,6 +354,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           }
         }
         mma_commit(&tfull[acc]);
+        trace_ev(p, tile_i, 2);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -372,7 +366,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     // TMEM load of the next chunk is in flight while the current one is
     // processed and stored.
     const int q = warp & 3;
-    const int wq = warp - 2;
+    const int wq = warp - C::EPI_WARP0;
     const int grp = wq >> 2;
     const int row0 = q * 32;
     uint8_t* stg = smem_epi + wq * C::NBUF * EPI_BUF;
@@ -405,7 +399,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     auto load_h = [&](int j) {
       if (j < hseq_end && lane == 0) {
         fence_proxy_async_smem();  // prior generic reads of this buffer before the async write
-        const TileInfo tj = decode(p, MODE, PAIR, (int)blockIdx.x + (j / NPW_) * (int)gridDim.x);
+        const int tile_j = (int)blockIdx.x + (j / NPW_) * (int)gridDim.x;
+        const TileInfo tj = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile_j : tile_j);
         int x, y;
         out_coords(p, MODE, tj, grp + (j % NPW_) * NG, row0, BN, x, y);
         const int b = j % C::NH;
@@ -416,13 +411,16 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     if (EPI_H && p.epi == EPI_ACT_BWD)
       for (int j = 0; j < C::NH; ++j) load_h(j);
 
+    int tile_i = -1;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const TileInfo t = decode(p, MODE, PAIR, tile);
+      const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
+      ++tile_i;
       const bool has_acc = (p.dbg & 64) ? false : t.kiters > 0;
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
       }
+      if (wq == 0 && lane == 0) trace_ev(p, tile_i, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * BN;
 
       if (p.dbg & 1) {
@@ -606,13 +604,14 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+      if (wq == 0 && lane == 0) trace_ev(p, tile_i, 4);
     }
     if (lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
@@ -630,6 +629,24 @@ int gemm_dbg() {
   return v;
 }
 
+// Trace buffer: allocated on first use when MOE_GEMM_TRACE is set (debug only);
+// successive launches take successive slots; moe_debug_trace_dump writes them out.
+static unsigned long long* g_trace = nullptr;
+static int g_trace_next = 0;
+static const char* g_trace_names[kTraceLaunches];
+
+unsigned long long* gemm_trace_slot() {
+  static int on = -1;
+  if (on < 0) on = getenv("MOE_GEMM_TRACE") != nullptr;
+  if (!on || g_trace_next >= kTraceLaunches) return nullptr;
+  const size_t per = (size_t)kTraceCtas * kTraceTiles * kTraceEvents;
+  if (!g_trace) {
+    if (cudaMalloc(&g_trace, per * kTraceLaunches * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(g_trace, 0, per * kTraceLaunches * sizeof(unsigned long long));
+  }
+  return g_trace + per * g_trace_next++;
+}
+
 template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   using C = Cfg<MODE, BN, EPI_H>;
@@ -645,6 +662,17 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   if (grid < 1) grid = 1;
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
+  p.trace = gemm_trace_slot();
+  {
+    static int rev = -1;
+    if (rev < 0) {
+      // bit m reverses the tile order of mode m. Default: DSD_ROW (its S operand
+      // was just written by the SDD / SDD^T before it; the tail is still in L2).
+      const char* e = getenv("MOE_GEMM_REVERSE");
+      rev = e ? atoi(e) : (1 << DSD_ROW);
+    }
+    if ((rev >> MODE) & 1) p.reverse = 1;
+  }
   kern<<<grid, C::THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, p);
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
@@ -736,6 +764,28 @@ using namespace moe;
 
 extern "C" {
 
+/* Debug only: synchronise, write the recorded GEMM timelines (MOE_GEMM_TRACE)
+ * as raw uint64 [launch][cta][tile][event] to `path`, reset. Returns launches. */
+int moe_debug_trace_dump(const char* path) {
+  if (!g_trace || !path) return 0;
+  cudaDeviceSynchronize();
+  const size_t per = (size_t)kTraceCtas * kTraceTiles * kTraceEvents;
+  const size_t n = per * g_trace_next;
+  unsigned long long* h = (unsigned long long*)malloc(n * sizeof(unsigned long long));
+  if (!h) return -1;
+  cudaMemcpy(h, g_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  FILE* f = fopen(path, "wb");
+  if (f) {
+    fwrite(h, sizeof(unsigned long long), n, f);
+    fclose(f);
+  }
+  free(h);
+  const int launches = g_trace_next;
+  g_trace_next = 0;
+  cudaMemset(g_trace, 0, per * kTraceLaunches * sizeof(unsigned long long));
+  return launches;
+}
+
 static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b, int trans_b,
                              const moe_topology_t* topo, int32_t act, const void* act_src, void* out_s, void* out_aux,
                              bool deriv, void* stream) {
@@ -763,7 +813,7 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   L.max_tiles = (int)(nnz / (L.bn / 128));
   MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 128, "moe_sdd a"));
   if (!trans_b)
-    MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, 64, "moe_sdd b"));
+    MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, L.bn / 64, "moe_sdd b"));
   else
     MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
@@ -807,7 +857,7 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
                        : (int)(rows / BM * L.p.dense_tiles);
     MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 128, "moe_dsd s"));
     if (!trans_b)
-      MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, 64, "moe_dsd b"));
+      MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, N, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, bbox, "moe_dsd b^T"));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
@@ -816,9 +866,9 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
     L.mode = DS_COL;
     L.a_mn = true;
     L.max_tiles = (pair ? L.p.n_block_cols / 2 : L.p.n_block_cols) * L.p.dense_tiles;
-    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 64, "moe_dsd s^T"));
+    MOE_TRY(make_tmap_bf16_mn(&L.ta, s, 128, nnz * 128, 128, 2, "moe_dsd s^T"));
     if (!trans_b)
-      MOE_TRY(make_tmap_bf16(&L.tb, b, h, rows, h, 64, 64, "moe_dsd b"));
+      MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, rows, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, bbox, "moe_dsd b^T"));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
@@ -846,9 +896,9 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
     L.b_mn = true;
     L.p.dense_tiles = (int)(h / (pair ? 2 * BM : BM));
     L.max_tiles = L.p.n_block_cols / (L.bn / 128) * L.p.dense_tiles;
-    MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 64, "moe_dds s"));
+    MOE_TRY(make_tmap_bf16_mn(&L.tb, s, 128, nnz * 128, 128, 2, "moe_dds s"));
     if (trans_a)
-      MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 64, "moe_dds a^T"));
+      MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, rows, h, 2, "moe_dds a^T"));
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, 64, 128, "moe_dds a"));
     MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
@@ -864,7 +914,7 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
   L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
   MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
   if (trans_a)
-    MOE_TRY(make_tmap_bf16(&L.ta, a, h, N, h, 64, 64, "moe_dds a^T"));
+    MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, N, h, 2, "moe_dds a^T"));
   else
     MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
   MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));

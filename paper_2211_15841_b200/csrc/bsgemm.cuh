@@ -48,6 +48,8 @@ struct GemmParams {
   long long ld_add;
   const int32_t* addend_map;
   int addend_k;
+  unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
+  int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
   int dbg;  // experiment knobs (MOE_GEMM_DBG): 1 = no epilogue work, 2 = no MMA, 4 = no activation
            // math, 8 = no TMA loads, 64 = epilogue decoupled from the accumulator (timing only)
 };
@@ -71,6 +73,11 @@ struct GemmLaunch {
 
 moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
 int gemm_dbg();
+// Timeline tracing of the GEMM engine (debug only, env MOE_GEMM_TRACE=1):
+// slot [launch][cta][tile][event], events: 0 producer first load, 1 MMA start,
+// 2 MMA last commit, 3 epilogue got accumulator, 4 epilogue done.
+constexpr int kTraceLaunches = 16, kTraceCtas = 160, kTraceTiles = 32, kTraceEvents = 5;
+unsigned long long* gemm_trace_slot();
 // CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
 // 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);

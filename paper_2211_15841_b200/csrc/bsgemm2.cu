@@ -208,9 +208,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (MODE == SDD) {
             const int k0 = kit * BK;
             tma_load_2d_pair(sa, &tmap_a, fb, k0, (t.r0 + rank) * BM);
-            if (B_MN) {  // W1 [h, E*f]: this CTA's block column c0 + rank
-              tma_load_2d_pair(sb, &tmap_b, fb, (t.c0 + rank) * 128, k0);
-              tma_load_2d_pair(sb + 8192, &tmap_b, fb, (t.c0 + rank) * 128 + 64, k0);
+            if (B_MN) {  // W1 [h, E*f]: this CTA's block column c0 + rank (3-D MN box, 2 chunks)
+              tma_load_3d_pair(sb, &tmap_b, fb, 0, k0, (t.c0 + rank) * 2);
             } else {     // W2 [E*f, h]
               tma_load_2d_pair(sb, &tmap_b, fb, k0, (t.c0 + rank) * 128);
             }
@@ -218,31 +217,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             tma_load_2d_pair(sa, &tmap_a, fb, kk * BK, sblk * BM);
             const int n0 = t.v * P_BN + rank * P_BH;
             if (B_MN) {
-              tma_load_2d_pair(sb, &tmap_b, fb, n0, oblk * BM + kk * BK);
-              tma_load_2d_pair(sb + 8192, &tmap_b, fb, n0 + 64, oblk * BM + kk * BK);
+              tma_load_3d_pair(sb, &tmap_b, fb, 0, oblk * BM + kk * BK, n0 / 64);
             } else {
               tma_load_2d_pair(sb, &tmap_b, fb, oblk * BM + kk * BK, n0);
             }
           } else if (MODE == DS_COL) {
-            tma_load_2d_pair(sa, &tmap_a, fb, 0, sblk * BM + kk * BK);
-            tma_load_2d_pair(sa + 8192, &tmap_a, fb, 64, sblk * BM + kk * BK);
+            tma_load_3d_pair(sa, &tmap_a, fb, 0, sblk * BM + kk * BK, 0);
             const int n0 = t.v * P_BN + rank * P_BH;
             if (B_MN) {
-              tma_load_2d_pair(sb, &tmap_b, fb, n0, oblk * BM + kk * BK);
-              tma_load_2d_pair(sb + 8192, &tmap_b, fb, n0 + 64, oblk * BM + kk * BK);
+              tma_load_3d_pair(sb, &tmap_b, fb, 0, oblk * BM + kk * BK, n0 / 64);
             } else {
               tma_load_2d_pair(sb, &tmap_b, fb, oblk * BM + kk * BK, n0);
             }
           } else {  // DDS_COL: A = dense rows (2v + rank) tile, B = block sblk (this CTA's column)
             const int m0 = (2 * t.v + rank) * BM;
             if (A_MN) {
-              tma_load_2d_pair(sa, &tmap_a, fb, m0, oblk * BM + kk * BK);
-              tma_load_2d_pair(sa + 8192, &tmap_a, fb, m0 + 64, oblk * BM + kk * BK);
+              tma_load_3d_pair(sa, &tmap_a, fb, 0, oblk * BM + kk * BK, m0 / 64);
             } else {
               tma_load_2d_pair(sa, &tmap_a, fb, oblk * BM + kk * BK, m0);
             }
-            tma_load_2d_pair(sb, &tmap_b, fb, 0, sblk * BM + kk * BK);
-            tma_load_2d_pair(sb + 8192, &tmap_b, fb, 64, sblk * BM + kk * BK);
+            tma_load_3d_pair(sb, &tmap_b, fb, 0, sblk * BM + kk * BK, 0);
           }
         }
         __syncwarp();

@@ -23,7 +23,6 @@ constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF;  // double buffered
 constexpr int SMEM_LIMIT = 232448;                // 227 KB opt-in
 constexpr int SMEM_FIXED = 1024 + 512;            // alignment slack + barriers
 constexpr int kMaxRouterTopK = 8;
-constexpr int kPrefetch = 0;  // L2 prefetch distance in K-steps (0: off; measured slower at 8)
 
 // tanh on the SFU (MUFU.TANH, max rel. error ~2^-11, below the bf16 output ulp)
 __device__ __forceinline__ float tanh_fast(float x) {

@@ -244,8 +244,8 @@ moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat
   L.p.ld_f32 = E;
   L.p.split_stride = (long long)h * E;
   L.max_tiles = parts * L.p.m_tiles;
-  MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 64, "router dWr x^T"));
-  MOE_TRY(make_tmap_bf16(&L.tb, dlogits, E, T, E, 64, 64, "router dWr dlogits"));
+  MOE_TRY(make_tmap_bf16_mn(&L.ta, x, h, T, h, 2, "router dWr x^T"));
+  MOE_TRY(make_tmap_bf16_mn(&L.tb, dlogits, E, T, E, L.bn / 64, "router dWr dlogits"));
   L.tc = L.td = L.ta;
   MOE_TRY(gemm_launch(L, s));
   router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
@@ -329,7 +329,7 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.p.topk = (int)cfg->top_k;
     L.max_tiles = L.p.m_tiles;
     MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 128, "moe_router x"));
-    MOE_TRY(make_tmap_bf16(&L.tb, wr, E, h, E, 64, 64, "moe_router wr"));
+    MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
     L.tc = L.td = L.ta;
     return gemm_launch(L, as_stream(stream));
   }

@@ -49,4 +49,27 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
   return MOE_OK;
 }
 
+moe_status make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
+                             uint32_t nchunk, const char* what) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  if (!base) return set_error(MOE_EINVAL, "%s: NULL pointer", what);
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return set_error(MOE_EINVAL, "%s: pointer must be 16-byte aligned for TMA", what);
+  if (inner % 64) return set_error(MOE_ESHAPE, "%s: MN extent %llu must be a multiple of 64", what,
+                                   (unsigned long long)inner);
+  if (outer == 0) outer = 1;
+  cuuint64_t dims[3] = {64, outer, inner / 64};
+  cuuint64_t strides[2] = {row_elems * 2, 128};
+  cuuint32_t box[3] = {64, 64, nchunk};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(MOE_ECUDA, "%s: cuTensorMapEncodeTiled (3-D MN) failed (%d) dims=[64,%llu,%llu] box=[64,64,%u]",
+                     what, (int)r, (unsigned long long)outer, (unsigned long long)(inner / 64), nchunk);
+  return MOE_OK;
+}
+
 }  // namespace moe

@@ -9,6 +9,12 @@ namespace moe {
 // swizzle span (64 elements for 128 B, 32 for 64 B).
 moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
                           uint32_t box_inner, uint32_t box_outer, const char* what, int swizzle_bytes = 128);
+// MN-major operand map: the row-major [outer, inner] matrix viewed as 3-D
+// {64, outer, inner/64} (strides: row pitch, 128 B) with box {64, 64, nchunk}:
+// one TMA box fills nchunk MN-chunks of 64 K-rows ([chunk][64][128 B] in smem,
+// SWIZZLE_128B). inner must be a multiple of 64.
+moe_status make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
+                             uint32_t nchunk, const char* what);
 // Epilogue store / H-prefetch maps: 32 x 32 boxes, 64 B swizzle.
 inline moe_status make_tmap_epi(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                                 uint64_t row_elems, const char* what) {

@@ -1,0 +1,85 @@
+"""Timeline of the tcgen05 GEMM launches of one layer step (debug tool).
+
+Run on the GPU box:  MOE_GEMM_TRACE=1 python scripts/trace_gemm.py [out.bin]
+Every GEMM launch records %globaltimer per CTA and tile (bsgemm.cu trace_ev):
+0 producer starts the tile, 1 MMA starts (accumulator free), 2 MMA done
+(last commit), 3 epilogue has the accumulator, 4 epilogue done. Prints, per
+launch, the kernel span and the mean per-tile phase times.
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("MOE_GEMM_TRACE", "1")
+
+import bench  # noqa: E402
+
+L, C, TT, EV = 16, 160, 32, 5
+
+
+def main(out):
+    from paper_2211_15841_b200 import api as A
+    from paper_2211_15841_b200._lib import lib
+    from synth import inputs as S
+    lib.moe_debug_trace_dump.restype = ctypes.c_int
+    lib.moe_debug_trace_dump.argtypes = [ctypes.c_char_p]
+    dev = torch.device("cuda", 0)
+    shp = S.CONFIGS["C1"]
+    T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
+    inp = S.make_inputs(shp, seed=0)
+    cfg = A.make_config(T, h, E, k, f, act=shp.act)
+    x, dy = inp["x"].to(dev), inp["dy"].to(dev)
+    wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
+    saved = A.Saved.allocate(cfg, dev)
+    ws = A.workspace(cfg, dev)
+    t = {"x": x, "dy": dy, "wr": wr, "w1": w1, "w2": w2, "saved": saved, "ws": ws,
+         "y": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
+         "dx": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
+         "dwr": torch.empty(h, E, dtype=torch.float32, device=dev),
+         "dw1": torch.empty(h, E * f, dtype=torch.bfloat16, device=dev),
+         "dw2": torch.empty(E * f, h, dtype=torch.bfloat16, device=dev)}
+    t["ws_layout"] = bench.ws_views(A, cfg, ws)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    step = bench.Step(A, cfg, t, stream)
+    l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        l2.zero_()
+        step.run()
+    torch.cuda.synchronize()
+    lib.moe_debug_trace_dump(out.encode())   # discard warm-up slots
+    l2.zero_()
+    torch.cuda.synchronize()
+    step.run()
+    n = lib.moe_debug_trace_dump(out.encode())
+    tr = np.fromfile(out, dtype=np.uint64).reshape(n, C, TT, EV).astype(np.float64)
+    gemm_names = [nm for nm in step.names if nm in ("router", "sdd", "dsd", "sddT", "dsTd", "dsdT", "ddTs",
+                                                   "router_dwr", "router_dx")]
+    for li in range(n):
+        a = tr[li]
+        valid = a[..., 1] > 0
+        if not valid.any():
+            print(f"launch {li}: no 1-SM trace (CTA-pair kernel)")
+            continue
+        t0 = a[a > 0].min()
+        span = (a.max() - t0) / 1e3
+        mma = (a[..., 2] - a[..., 1])[valid] / 1e3
+        epi = (a[..., 4] - a[..., 3])[valid & (a[..., 4] > 0)] / 1e3
+        wait_acc = (a[..., 3] - a[..., 2])[valid & (a[..., 3] > 0)] / 1e3
+        first = (a[:, 0, 1] - t0)[a[:, 0, 1] > 0] / 1e3
+        last_end = (a[..., 4].max(axis=1) - t0) / 1e3
+        ntile = valid.sum(axis=1)
+        nm = gemm_names[li] if li < len(gemm_names) else "?"
+        print(f"launch {li} ({nm}): span {span:.1f} us | tiles/CTA {ntile.min()}-{ntile.max()} | "
+              f"mainloop/tile {mma.mean():.2f} us (max {mma.max():.2f}) | epilogue/tile {epi.mean():.2f} us | "
+              f"commit->epi {wait_acc.mean():.2f} us | first MMA start {first.mean():.2f} us (max {first.max():.2f}) | "
+              f"CTA end min {last_end[last_end > 0].min():.1f} max {last_end.max():.1f}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/trace.bin")
