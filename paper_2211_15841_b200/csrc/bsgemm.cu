@@ -411,11 +411,39 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     if (EPI_H && p.epi == EPI_ACT_BWD)
       for (int j = 0; j < C::NH; ++j) load_h(j);
 
+    uint4 pre_next[MODE == DENSE ? NCHUNK / NG : 1][4];
+    auto addend_prefetch = [&](int tl, uint4 (&dst)[MODE == DENSE ? NCHUNK / NG : 1][4]) {
+      if (tl >= ntiles) return;
+      const TileInfo tn = decode(p, MODE, PAIR, tl);
+      const int trow = tn.u * BM + row0 + lane;
+      if (trow >= p.rows_valid) return;
+      const int m = p.addend_map ? __ldg(p.addend_map + (long long)trow * p.addend_k) : trow;
+      const __nv_bfloat16* rowp = p.addend + (long long)m * p.ld_add + (long long)tn.v * BN;
+#pragma unroll
+      for (int i = 0; i < (MODE == DENSE ? NCHUNK / NG : 1); ++i) {
+        const uint4* src = reinterpret_cast<const uint4*>(rowp + (grp + i * NG) * EPI_COLS);
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) dst[i][q2] = __ldg(src + q2);
+      }
+    };
     int tile_i = -1;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       ++tile_i;
       const bool has_acc = (p.dbg & 64) ? false : t.kiters > 0;
+      // DENSE + EPI_ADD_ROWS: this lane's addend rows for all of its chunks are
+      // in registers before the accumulator is waited for; the next tile's rows
+      // are loaded now, so the gather latency overlaps this tile's epilogue.
+      constexpr int NPW0 = NCHUNK / NG;
+      uint4 pre[MODE == DENSE ? NPW0 : 1][4];
+      if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
+        if (tile_i == 0) addend_prefetch(tile, pre_next);
+#pragma unroll
+        for (int i = 0; i < (MODE == DENSE ? NPW0 : 1); ++i)
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) pre[i][q2] = pre_next[i][q2];
+        addend_prefetch(tile + (int)gridDim.x, pre_next);
+      }
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -435,8 +463,10 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         // (the next chunk's tcgen05.ld is in flight while this one is processed).
         constexpr int NPW = NCHUNK / NG;
         static_assert(NCHUNK % NG == 0, "chunks must divide evenly over the epilogue warps");
-        uint32_t rr[2][32];
-        if (has_acc) {
+        // DENSE kernels keep registers for the prefetched addend rows instead
+        constexpr bool PP = MODE != DENSE;
+        uint32_t rr[PP ? 2 : 1][32];
+        if (has_acc && PP) {
           tmem_ld32(taddr + grp * EPI_COLS, rr[0]);
           tmem_ld_wait();
         }
@@ -445,9 +475,13 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           const int c = grp + i * NG;
           float v[32];
           if (has_acc) {
+            if (!PP) {
+              tmem_ld32(taddr + c * EPI_COLS, rr[0]);
+              tmem_ld_wait();
+            }
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[i & 1][e]);
-            if (i + 1 < NPW) tmem_ld32(taddr + (c + NG) * EPI_COLS, rr[(i + 1) & 1]);  // next chunk, in flight
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(rr[PP ? (i & 1) : 0][e]);
+            if (PP && i + 1 < NPW) tmem_ld32(taddr + (c + NG) * EPI_COLS, rr[PP ? ((i + 1) & 1) : 0]);  // next chunk, in flight
           } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = 0.f;
@@ -477,24 +511,21 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             load_h(hseq + C::NH);  // refill the buffer just read
             ++hseq;
           } else if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
-            // rows to add (router backward: dx += ...)
+            // rows to add (router backward: dx += ...): the first term was
+            // prefetched at the tile start; further top-k terms load here
             const int trow = t.u * BM + row0 + lane;
             if (trow < p.rows_valid) {
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2) {
+                float af[8];
+                unpack8(pre[i][q2], af);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[8 * q2 + e] += af[e];
+              }
               const long long col0 = (long long)t.v * BN + c * EPI_COLS;
-              if (p.addend_map) {  // gathered rows (fused gather backward): sum_j addend[map[trow*k+j]]
-                for (int j = 0; j < p.addend_k; ++j) {
-                  const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
-                  const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
-#pragma unroll
-                  for (int q2 = 0; q2 < 4; ++q2) {
-                    float af[8];
-                    unpack8(__ldg(src + q2), af);
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) v[8 * q2 + e] += af[e];
-                  }
-                }
-              } else {
-                const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)trow * p.ld_add + col0);
+              for (int j = 1; j < (p.addend_map ? p.addend_k : 1); ++j) {
+                const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
+                const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
 #pragma unroll
                 for (int q2 = 0; q2 < 4; ++q2) {
                   float af[8];
@@ -506,7 +537,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             }
           }
           store_chunk(&tmap_c, v, x, y);
-          if (has_acc && i + 1 < NPW) tmem_ld_wait();
+          if (PP && has_acc && i + 1 < NPW) tmem_ld_wait();
         }
       } else if (MODE == DENSE && p.epi == EPI_ROUTER) {
         // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e),

@@ -263,7 +263,7 @@ moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, con
   GemmLaunch D{};
   D.name = "router dx";
   D.mode = DENSE;
-  D.bn = h % 256 == 0 ? 256 : 128;
+  D.bn = 128;  // two 32-column chunks per epilogue warp: its gathered addend rows are prefetched in registers
   D.a_mn = false;
   D.b_mn = false;
   D.p.m_tiles = (int)ceil_div(T, 128);
