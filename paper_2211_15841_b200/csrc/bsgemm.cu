@@ -270,6 +270,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+  pdl_wait();  // operands and device-side sizes come from the previous kernels
   const int ntiles = num_tiles(p, MODE, PAIR);
 
   if (warp < C::NP) {
@@ -704,7 +706,8 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
     }
     if ((rev >> MODE) & 1) p.reverse = 1;
   }
-  kern<<<grid, C::THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, p);
+  cudaError_t le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
+  if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
 }

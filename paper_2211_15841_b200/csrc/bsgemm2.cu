@@ -174,6 +174,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+  pdl_wait();
   const int ntiles = num_tiles2(p, MODE);
 
   if (warp == 0) {
@@ -414,7 +416,8 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   if (grid < 2) grid = 2;
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
-  kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(L.ta, L.tb, L.tc, L.td, p);
+  cudaError_t le = launch_k(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
+  if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
 }

@@ -6,9 +6,38 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <utility>
+
 #include "../../include/moe.h"
 
 namespace moe {
+
+// ---- programmatic dependent launch (PDL) ----
+// With MOE_PDL=1 every kernel of the library is launched with programmatic
+// stream serialisation: kernel N+1's CTAs may be scheduled while kernel N
+// drains. Each kernel triggers its dependents at entry and executes
+// griddepcontrol.wait before it touches global memory a previous kernel wrote;
+// without the launch attribute (default) both instructions are no-ops.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 moe_status set_error(moe_status st, const char* fmt, ...);
 void clear_error();
@@ -25,6 +54,16 @@ void reset_launch_count();
     cudaError_t _e = cudaGetLastError();                                               \
     if (_e != cudaSuccess)                                                             \
       return ::moe::set_error(MOE_ECUDA, "%s: %s", name, cudaGetErrorString(_e));      \
+    ::moe::count_launch();                                                             \
+  } while (0)
+
+// Launch through launch_k and account for it (errors -> MOE_ECUDA).
+#define MOE_LAUNCH(name, ...)                                                         \
+  do {                                                                                 \
+    cudaError_t _le = ::moe::launch_k(__VA_ARGS__);                                    \
+    if (_le == cudaSuccess) _le = cudaGetLastError();                                  \
+    if (_le != cudaSuccess)                                                            \
+      return ::moe::set_error(MOE_ECUDA, "%s: %s", name, cudaGetErrorString(_le));     \
     ::moe::count_launch();                                                             \
   } while (0)
 

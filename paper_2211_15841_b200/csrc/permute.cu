@@ -65,6 +65,8 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restri
                                                             uint4* __restrict__ dst, int R, int k,
                                                             const int32_t* __restrict__ counts,
                                                             const int32_t* __restrict__ padded_bins, int E, int bs) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int ROWS = 8 / VEC;
   constexpr int RV = VEC * 32;  // uint4 per row
   const int lane = threadIdx.x & 31;
@@ -99,6 +101,8 @@ template <int VEC>
 __global__ void __launch_bounds__(256) combine_kernel(const uint4* __restrict__ rows, const int32_t* __restrict__ map,
                                                        const float* __restrict__ gates, uint4* __restrict__ y, int T,
                                                        int k) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int ROWS = 8 / VEC;
   constexpr int RV = VEC * 32;
   const int lane = threadIdx.x & 31;
@@ -160,6 +164,8 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
     const float* __restrict__ logits, const int32_t* __restrict__ expert_idx, int E,
     __nv_bfloat16* __restrict__ dlogits_bf16, float* __restrict__ dlogits_f32, const int32_t* __restrict__ counts,
     const int32_t* __restrict__ padded_bins, int bs) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int RV = VEC * 32;
   const int lane = threadIdx.x & 31;
   const bool want_dg = dgates != nullptr;
@@ -269,16 +275,18 @@ static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, 
   return MOE_OK;
 }
 
-#define MOE_VEC_DISPATCH(VEC_EXPR, KERNEL, ...)                                                         \
-  switch (VEC_EXPR) {                                                                                   \
-    case 1: KERNEL<1><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 2: KERNEL<2><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 3: KERNEL<3><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 4: KERNEL<4><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 5: KERNEL<5><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 6: KERNEL<6><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    case 7: KERNEL<7><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                     \
-    default: KERNEL<8><<<row_grid(), 32 * kWarpsPerCta, 0, s>>>(__VA_ARGS__); break;                    \
+#define MOE_VEC_CASE(V, NAME, KERNEL, ...) \
+  case V: MOE_LAUNCH(NAME, KERNEL<V>, dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break;
+#define MOE_VEC_DISPATCH(VEC_EXPR, NAME, KERNEL, ...)  \
+  switch (VEC_EXPR) {                                  \
+    MOE_VEC_CASE(1, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(2, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(3, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(4, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(5, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(6, NAME, KERNEL, __VA_ARGS__)         \
+    MOE_VEC_CASE(7, NAME, KERNEL, __VA_ARGS__)         \
+    default: MOE_LAUNCH(NAME, KERNEL<8>, dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break; \
   }
 
 moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* y_rows, const int32_t* map,
@@ -289,10 +297,9 @@ moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* 
   const int T = (int)cfg->tokens, k = (int)cfg->top_k, E = (int)cfg->num_experts, bs = (int)cfg->block_size;
   const int32_t* counts = pad_topo ? pad_topo->counts : nullptr;
   const int32_t* pbins = pad_topo ? pad_topo->padded_bins : nullptr;
-  MOE_VEC_DISPATCH(vec, scatter_bwd_kernel, reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows),
+  MOE_VEC_DISPATCH(vec, "scatter_bwd", scatter_bwd_kernel, reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows),
                    map, gates, reinterpret_cast<uint4*>(dy_rows), dgates, T, k, logits, expert_idx, E, dlogits_bf16,
                    dlogits_f32, counts, pbins, bs);
-  MOE_CHECK_LAUNCH("scatter_bwd");
   return MOE_OK;
 }
 
@@ -307,10 +314,9 @@ moe_status moe_gather(const moe_config* cfg, const void* x, const moe_topology_t
   MOE_CHECK_ARG(x && x_g, "moe_gather: NULL pointer");
   cudaStream_t s = as_stream(stream);
   const int R = (int)(cfg->tokens * cfg->top_k);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->pos,
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_gather", scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->pos,
                    reinterpret_cast<uint4*>(x_g), R, (int)cfg->top_k, topo->counts, topo->padded_bins,
                    (int)cfg->num_experts, (int)cfg->block_size);
-  MOE_CHECK_LAUNCH("moe_gather");
   return MOE_OK;
 }
 
@@ -319,9 +325,8 @@ moe_status moe_scatter(const moe_config* cfg, const void* y_g, const moe_topolog
   MOE_TRY(check_rows(cfg, topo, "moe_scatter"));
   MOE_CHECK_ARG(y_g && y, "moe_scatter: NULL pointer");
   cudaStream_t s = as_stream(stream);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(y_g), topo->pos, gates,
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_scatter", combine_kernel, reinterpret_cast<const uint4*>(y_g), topo->pos, gates,
                    reinterpret_cast<uint4*>(y), (int)cfg->tokens, (int)cfg->top_k);
-  MOE_CHECK_LAUNCH("moe_scatter");
   return MOE_OK;
 }
 
@@ -338,9 +343,8 @@ moe_status moe_gather_bwd(const moe_config* cfg, const void* dx_g, const moe_top
   MOE_TRY(check_rows(cfg, topo, "moe_gather_bwd"));
   MOE_CHECK_ARG(dx_g && dx, "moe_gather_bwd: NULL pointer");
   cudaStream_t s = as_stream(stream);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(dx_g), topo->pos, nullptr,
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_gather_bwd", combine_kernel, reinterpret_cast<const uint4*>(dx_g), topo->pos, nullptr,
                    reinterpret_cast<uint4*>(dx), (int)cfg->tokens, (int)cfg->top_k);
-  MOE_CHECK_LAUNCH("moe_gather_bwd");
   return MOE_OK;
 }
 
@@ -350,9 +354,8 @@ moe_status moe_sort_rows(const moe_config* cfg, const void* x, const moe_topolog
   MOE_CHECK_ARG(x && x_sorted, "moe_sort_rows: NULL pointer");
   cudaStream_t s = as_stream(stream);
   const int R = (int)(cfg->tokens * cfg->top_k);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->sorted_pos,
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_sort_rows", scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->sorted_pos,
                    reinterpret_cast<uint4*>(x_sorted), R, (int)cfg->top_k, nullptr, nullptr, 0, 1);
-  MOE_CHECK_LAUNCH("moe_sort_rows");
   return MOE_OK;
 }
 
@@ -361,9 +364,8 @@ moe_status moe_unsort_rows(const moe_config* cfg, const void* y_sorted, const mo
   MOE_TRY(check_rows(cfg, topo, "moe_unsort_rows"));
   MOE_CHECK_ARG(y_sorted && y, "moe_unsort_rows: NULL pointer");
   cudaStream_t s = as_stream(stream);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), combine_kernel, reinterpret_cast<const uint4*>(y_sorted),
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_unsort_rows", combine_kernel, reinterpret_cast<const uint4*>(y_sorted),
                    topo->sorted_pos, gates, reinterpret_cast<uint4*>(y), (int)cfg->tokens, (int)cfg->top_k);
-  MOE_CHECK_LAUNCH("moe_unsort_rows");
   return MOE_OK;
 }
 

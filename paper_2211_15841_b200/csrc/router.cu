@@ -23,6 +23,8 @@ constexpr int RT_K = 32;     // contraction chunk
 __global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16* __restrict__ x,
                                                              const __nv_bfloat16* __restrict__ wr,
                                                              float* __restrict__ logits, int T, int h, int E) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sx[RT_K][RT_TOK + 1];
   __shared__ float sw[RT_K][RT_EXP];
   const int t0 = blockIdx.x * RT_TOK, e0 = blockIdx.y * RT_EXP;
@@ -71,6 +73,8 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16*
 constexpr int kMaxTopK = 32;
 __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ gates,
                             int T, int E, int k) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (t >= T) return;
@@ -115,6 +119,8 @@ __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restric
 __global__ void router_dlogits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                                       const float* __restrict__ dgates, float* __restrict__ dlogits,
                                       __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k) {
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (t >= T) return;
@@ -150,6 +156,8 @@ __global__ void __launch_bounds__(256) router_dwr_part_kernel(const __nv_bfloat1
                                                                const float* __restrict__ dlogits,
                                                                float* __restrict__ part, int T, int h, int E,
                                                                int tok_per_part) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sx[32][33];
   __shared__ float sd[32][64];
   const int q = blockIdx.x, i0 = blockIdx.y * 32;
@@ -189,6 +197,8 @@ __global__ void __launch_bounds__(256) router_dwr_part_kernel(const __nv_bfloat1
 }
 
 __global__ void router_dwr_reduce_kernel(const float* __restrict__ part, float* __restrict__ dwr, int parts, int n) {
+  pdl_trigger();
+  pdl_wait();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= n) return;
   float s = 0.f;
@@ -200,6 +210,8 @@ __global__ void router_dwr_reduce_kernel(const float* __restrict__ part, float* 
 __global__ void __launch_bounds__(256) router_dx_kernel(const float* __restrict__ dlogits,
                                                          const __nv_bfloat16* __restrict__ wr,
                                                          __nv_bfloat16* __restrict__ dx, int T, int h, int E) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float s_dl[];  // [8 warps][E]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
@@ -248,8 +260,7 @@ moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat
   MOE_TRY(make_tmap_bf16_mn(&L.tb, dlogits, E, T, E, L.bn / 64, "router dWr dlogits"));
   L.tc = L.td = L.ta;
   MOE_TRY(gemm_launch(L, s));
-  router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
-  MOE_CHECK_LAUNCH("router_dwr_reduce");
+  MOE_LAUNCH("router_dwr_reduce", router_dwr_reduce_kernel, dim3((int)ceil_div((int64_t)h * E, 256)), dim3(256), 0, s, part, dwr, parts, h * E);
   return MOE_OK;
 }
 
@@ -295,9 +306,7 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
   MOE_CHECK_ARG(logits && expert_idx && gates, "moe_topk: NULL pointer");
   if (cfg->top_k > kMaxTopK) return set_error(MOE_EUNSUPPORTED, "top_k=%lld > %d", (long long)cfg->top_k, kMaxTopK);
   const int T = (int)cfg->tokens;
-  topk_kernel<<<(int)ceil_div(T, 8), 256, 0, as_stream(stream)>>>(logits, expert_idx, gates, T,
-                                                                   (int)cfg->num_experts, (int)cfg->top_k);
-  MOE_CHECK_LAUNCH("moe_topk");
+  MOE_LAUNCH("moe_topk", topk_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, as_stream(stream), logits, expert_idx, gates, T, (int)cfg->num_experts, (int)cfg->top_k);
   return MOE_OK;
 }
 
@@ -334,10 +343,7 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     return gemm_launch(L, as_stream(stream));
   }
   dim3 grid((unsigned)ceil_div(T, RT_TOK), (unsigned)ceil_div(E, RT_EXP));
-  router_logits_kernel<<<grid, 256, 0, as_stream(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x),
-                                                            reinterpret_cast<const __nv_bfloat16*>(wr), logits, T, h,
-                                                            E);
-  MOE_CHECK_LAUNCH("router_logits");
+  MOE_LAUNCH("router_logits", router_logits_kernel, dim3(grid), dim3(256), 0, as_stream(stream), reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wr), logits, T, h, E);
   return moe_topk(cfg, logits, expert_idx, gates, stream);
 }
 
@@ -354,24 +360,17 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
   const int parts = router_bwd_parts(cfg);
   if (router_on_tensor_cores(cfg)) {
     __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(dlogits);
-    router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, nullptr, dl16, T, E, k);
-    MOE_CHECK_LAUNCH("router_dlogits");
+    MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, nullptr, dl16, T, E, k);
     MOE_TRY(router_dwr_tc(cfg, x, dl16, dwr, ws, s));
     return router_dx_tc(cfg, dl16, wr, dx, dx, nullptr, 1, h, s);  // dx += dlogits . Wr^T (in place)
   }
-  router_dlogits_kernel<<<(int)ceil_div(T, 8), 256, 0, s>>>(logits, expert_idx, dgates, dlogits, nullptr, T, E, k);
-  MOE_CHECK_LAUNCH("router_dlogits");
+  MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, dlogits, nullptr, T, E, k);
   const int tpp = (int)ceil_div(T, parts);
-  router_dwr_part_kernel<<<dim3(parts, (unsigned)ceil_div(h, 32)), 256, 0, s>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);
-  MOE_CHECK_LAUNCH("router_dwr_part");
-  router_dwr_reduce_kernel<<<(int)ceil_div((int64_t)h * E, 256), 256, 0, s>>>(part, dwr, parts, h * E);
-  MOE_CHECK_LAUNCH("router_dwr_reduce");
+  MOE_LAUNCH("router_dwr_part", router_dwr_part_kernel, dim3(dim3(parts, (unsigned)ceil_div(h, 32))), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);
+  MOE_LAUNCH("router_dwr_reduce", router_dwr_reduce_kernel, dim3((int)ceil_div((int64_t)h * E, 256)), dim3(256), 0, s, part, dwr, parts, h * E);
   const size_t smem = 8 * E * sizeof(float);
   if (smem > 48 * 1024) return set_error(MOE_EUNSUPPORTED, "router_bwd: num_experts too large");
-  router_dx_kernel<<<(int)ceil_div(T, 8), 256, smem, s>>>(dlogits, reinterpret_cast<const __nv_bfloat16*>(wr),
-                                                          reinterpret_cast<__nv_bfloat16*>(dx), T, h, E);
-  MOE_CHECK_LAUNCH("router_dx");
+  MOE_LAUNCH("router_dx", router_dx_kernel, dim3((int)ceil_div(T, 8)), dim3(256), smem, s, dlogits, reinterpret_cast<const __nv_bfloat16*>(wr), reinterpret_cast<__nv_bfloat16*>(dx), T, h, E);
   return MOE_OK;
 }
 

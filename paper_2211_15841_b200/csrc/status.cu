@@ -1,5 +1,6 @@
 // status.cu — error reporting, config validation and size queries of the C ABI
 // (include/moe.h). Host only; no CUDA calls except the SM-count query.
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -7,6 +8,18 @@
 #include "common.cuh"
 
 namespace moe {
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    // measured no gain inside a CUDA graph at MoE-XS (the kernel tails are
+    // short and the persistent GEMMs leave no room to co-schedule): opt-in
+    const char* e = getenv("MOE_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 
 static thread_local char g_err[512] = "";
 static thread_local int g_launches = 0;

@@ -21,6 +21,8 @@
 namespace moe {
 
 __global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, int32_t* __restrict__ chunk_counts) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ int32_t s_cnt[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_cnt[e] = 0;
   __syncthreads();
@@ -68,6 +70,8 @@ __device__ void block_exclusive_scan(int32_t* data, int n, int32_t* s_tmp, int32
 
 __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ chunk_counts, int n_chunks, int E,
                                                           int bs, int F, moe_topology_t topo) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int32_t s_counts[1024];
   __shared__ int32_t s_pad[1024];
   __shared__ int32_t s_tmp[32];
@@ -121,6 +125,8 @@ __global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ c
 __global__ void __launch_bounds__(1024) topo_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs, int F,
                                                           int n_chunks, const int32_t* __restrict__ chunk_base,
                                                           moe_topology_t topo) {
+  pdl_trigger();
+  pdl_wait();
   if ((int)blockIdx.x < n_chunks) {
     extern __shared__ int32_t s_w[];  // [32 warps][E] counts -> exclusive prefix over warps
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,10 +198,8 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   const WsLayout L = ws_layout(cfg);
   int32_t* chunk_counts = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + L.topo_chunk_counts);
   cudaStream_t s = as_stream(stream);
-  topo_hist_kernel<<<n_chunks, kTopoChunk, E * sizeof(int32_t), s>>>(expert_idx, R, E, chunk_counts);
-  MOE_CHECK_LAUNCH("topo_hist");
-  topo_scan_kernel<<<1, 1024, 0, s>>>(chunk_counts, n_chunks, E, bs, F, *topo);
-  MOE_CHECK_LAUNCH("topo_scan");
+  MOE_LAUNCH("topo_hist", topo_hist_kernel, dim3(n_chunks), dim3(kTopoChunk), E * sizeof(int32_t), s, expert_idx, R, E, chunk_counts);
+  MOE_LAUNCH("topo_scan", topo_scan_kernel, dim3(1), dim3(1024), 0, s, chunk_counts, n_chunks, E, bs, F, *topo);
   const int emit_smem = 32 * E * (int)sizeof(int32_t);
   static int smem_set = 0;
   if (emit_smem > 48 * 1024 && smem_set < emit_smem) {
@@ -204,8 +208,6 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   }
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
-  topo_emit_kernel<<<n_chunks + blk_ctas, 1024, emit_smem, s>>>(expert_idx, R, E, bs, F, n_chunks, chunk_counts,
-                                                                 *topo);
-  MOE_CHECK_LAUNCH("topo_emit");
+  MOE_LAUNCH("topo_emit", topo_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R, E, bs, F, n_chunks, chunk_counts, *topo);
   return MOE_OK;
 }
