@@ -77,11 +77,12 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
+  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 : 0;  // router epilogue exchange
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES) / STAGE;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES + XCH;
   static_assert(STAGES >= 2, "not enough shared memory for two stages");
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
@@ -241,7 +242,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
   uint8_t* smem_b = smem_a + STAGES * A_BYTES;
   uint8_t* smem_epi = smem_b + STAGES * C::B_BYTES;
   uint8_t* smem_h = smem_epi + C::EPI;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES);
+  uint8_t* smem_x = smem_h + C::H_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_x + C::XCH);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -542,42 +544,74 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           if (PP && has_acc && i + 1 < NPW) tmem_ld_wait();
         }
       } else if (MODE == DENSE && p.epi == EPI_ROUTER) {
-        // logits row of token t -> fp32 logits, greedy top-k (ties -> lower e),
-        // softmax gates. Group-0 warps own whole rows.
-        if (grp == 0) {
-          const int tok = t.u * BM + row0 + lane;
-          const bool valid = tok < p.rows_valid;
-          float bv[kMaxRouterTopK];
-          int be[kMaxRouterTopK];
+        // logits row of token t -> fp32 logits (TMA store), greedy top-k (ties ->
+        // lower e), softmax gates. The two warps of a lane quarter split
+        // the experts; each keeps an online (max, sum exp) and a local top-k,
+        // group 1 hands its partials to group 0 through shared memory.
+        constexpr int CG = BN / NG;  // experts per warp
+        const int tok = t.u * BM + row0 + lane;
+        const bool valid = tok < p.rows_valid;
+        const int topk = p.topk;
+        float bv[kMaxRouterTopK];
+        int be[kMaxRouterTopK];
 #pragma unroll
-          for (int j = 0; j < kMaxRouterTopK; ++j) {
-            bv[j] = -FLT_MAX;
-            be[j] = 0x7fffffff;
-          }
-          float mx = -FLT_MAX;
+        for (int j = 0; j < kMaxRouterTopK; ++j) {
+          bv[j] = -FLT_MAX;
+          be[j] = 0x7fffffff;
+        }
+        float mx = -FLT_MAX, ssum = 0.f;
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c * 32, r);
-            tmem_ld_wait();
-            if (valid) {
-              float4* lrow = reinterpret_cast<float4*>(p.logits + (long long)tok * p.E + c * 32);
+        for (int c = 0; c < CG / 32; ++c) {
+          const int col0 = grp * CG + c * 32;
+          uint32_t r[32];
+          tmem_ld32(taddr + col0, r);
+          tmem_ld_wait();
+          // stage the 32 x 32 fp32 chunk (128B-swizzled rows) and TMA-store it
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          {
+            const uint32_t row = smem_u32(stg) + lane * 128;
 #pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                lrow[i / 4] = make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                                          __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-            }
+            for (int j = 0; j < 8; ++j)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((j ^ (lane & 7)) << 4)),
+                           "r"(r[4 * j]), "r"(r[4 * j + 1]), "r"(r[4 * j + 2]), "r"(r[4 * j + 3])
+                           : "memory");
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_c, stg, col0, t.u * BM + row0);
+            bulk_commit();
+          }
+          float cm = -FLT_MAX;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cm = fmaxf(cm, __uint_as_float(r[i]));
+          float cs = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cs += __expf(__uint_as_float(r[i]) - cm);
+          const float nm = fmaxf(mx, cm);
+          ssum = ssum * __expf(mx - nm) + cs * __expf(cm - nm);
+          mx = nm;
+          if (topk == 1) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float x = __uint_as_float(r[i]);
-              const int e = c * 32 + i;
-              mx = fmaxf(mx, x);
+              if (x > bv[0]) {
+                bv[0] = x;
+                be[0] = col0 + i;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(r[i]);
+              const int e = col0 + i;
               // stable insertion into the descending list (experts arrive in ascending e;
               // strict '>' keeps the lower e first on ties). Back to front, reading the
               // not-yet-updated predecessor.
 #pragma unroll
               for (int j = kMaxRouterTopK - 1; j >= 0; --j) {
-                if (j < p.topk && x > bv[j]) {
+                if (j < topk && x > bv[j]) {
                   if (j > 0 && x > bv[j - 1]) {
                     bv[j] = bv[j - 1];
                     be[j] = be[j - 1];
@@ -589,25 +623,51 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               }
             }
           }
-          float ssum = 0.f;
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(taddr + c * 32, r);
-            tmem_ld_wait();
+        }
+        // group 1 -> group 0 through shared memory (per row: max, sum, k values, k experts)
+        float* xr = reinterpret_cast<float*>(smem_x) + (row0 + lane) * (2 + 2 * kMaxRouterTopK);
+        if (grp == 1) {
+          xr[0] = mx;
+          xr[1] = ssum;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ssum += __expf(__uint_as_float(r[i]) - mx);
+          for (int j = 0; j < kMaxRouterTopK; ++j) {
+            xr[2 + j] = bv[j];
+            xr[2 + kMaxRouterTopK + j] = __int_as_float(be[j]);
           }
-          if (valid) {
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (grp == 0) {
+          const float m1 = xr[0], s1 = xr[1];
+          const float M = fmaxf(mx, m1);
+          const float S = ssum * __expf(mx - M) + s1 * __expf(m1 - M);
+          // merge the two descending lists; on equal values list 0 (lower experts) first
+          int i0 = 0, i1 = 0;
 #pragma unroll
-            for (int j = 0; j < kMaxRouterTopK; ++j) {
-              if (j < p.topk) {
-                p.idx[(long long)tok * p.topk + j] = be[j];
-                p.gates[(long long)tok * p.topk + j] = __expf(bv[j] - mx) / ssum;
+          for (int j = 0; j < kMaxRouterTopK; ++j) {
+            if (j < topk) {
+              float v0 = -FLT_MAX, v1 = -FLT_MAX;
+              int e0 = 0x7fffffff, e1 = 0x7fffffff;
+#pragma unroll
+              for (int u = 0; u < kMaxRouterTopK; ++u) {
+                if (u == i0) { v0 = bv[u]; e0 = be[u]; }
+              }
+              if (i1 < kMaxRouterTopK) {
+                v1 = xr[2 + i1];
+                e1 = __float_as_int(xr[2 + kMaxRouterTopK + i1]);
+              }
+              const bool take1 = v1 > v0;
+              const float v = take1 ? v1 : v0;
+              const int e = take1 ? e1 : e0;
+              i1 += take1 ? 1 : 0;
+              i0 += take1 ? 0 : 1;
+              if (valid) {
+                p.idx[(long long)tok * topk + j] = e;
+                p.gates[(long long)tok * topk + j] = __expf(v - M) / S;
               }
             }
           }
         }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // xr reused by the next tile
       } else if (MODE == DENSE) {  // EPI_F32: fp32 partial tile (split-K)
         const int r = t.u * BM + row0 + lane;
         float* dst = p.out_f32 + (long long)t.s * p.split_stride + (long long)r * p.ld_f32 + t.v * BN;

@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "permute.cuh"
@@ -154,10 +155,13 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint4* __restrict__ 
   }
 }
 
-// Per token t (one warp): dy_rows[map[i]] = g_i * dy[t]; dgates[i] = <y_rows[map[i]], dy[t]>,
-// i = t*k + j. Optionally fused router backward (P:98 softmax chain rule):
+// dy_rows[map[i]] = g_i * dy[t]; dgates[i] = <y_rows[map[i]], dy[t]>, i = t*k + j.
+// Optionally fused router backward (P:98 softmax chain rule):
 // dlogits[t,:] = p * (dp - <p,dp>), p = softmax(logits[t,:]), dp[e] = sum_{j: idx_j = e} dgates_j.
-template <int VEC>
+// Each warp owns TPW tokens at once: all index, gate, dy-row and logit loads
+// are issued together, then the gathered y rows of every slot, so a warp keeps
+// ~TPW*(2 + k) row loads in flight instead of a dependent chain per token.
+template <int VEC, int TPW, int EQ>
 __global__ void __launch_bounds__(256) scatter_bwd_kernel(
     const uint4* __restrict__ dy, const uint4* __restrict__ y_rows, const int32_t* __restrict__ map,
     const float* __restrict__ gates, uint4* __restrict__ dy_rows, float* __restrict__ dgates, int T, int k,
@@ -167,96 +171,120 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
   pdl_trigger();
   pdl_wait();
   constexpr int RV = VEC * 32;
+  // EQ: logits per lane per token (E <= 32 * EQ)
   const int lane = threadIdx.x & 31;
   const bool want_dg = dgates != nullptr;
-  for (int t = warp_global(); t < T; t += warps_total()) {
-    uint4 d[VEC];
-    const uint4* ds = dy + (size_t)t * RV;
+  const bool want_dl = logits && (dlogits_bf16 || dlogits_f32);
+  const int EQn = (E + 31) / 32;
+  for (int base = warp_global() * TPW; base < T; base += warps_total() * TPW) {
+    // lane l < TPW*k holds slot (token base + l / k, j = l % k)
+    const int tl = lane / k, jl = lane - tl * k;
+    const bool sl = lane < TPW * k && base + tl < T;
+    const int midx = sl ? __ldg(map + (size_t)(base + tl) * k + jl) : 0;
+    const float gl = sl ? (gates ? __ldg(gates + (size_t)(base + tl) * k + jl) : 1.0f) : 0.f;
+    const int eidx = (sl && want_dl) ? __ldg(expert_idx + (size_t)(base + tl) * k + jl) : -1;
+    uint4 d[TPW][VEC];
 #pragma unroll
-    for (int u = 0; u < VEC; ++u) d[u] = __ldg(ds + lane + 32 * u);
-    float df[VEC][8];
+    for (int r = 0; r < TPW; ++r)
+      if (base + r < T) {
+        const uint4* ds = dy + (size_t)(base + r) * RV;
 #pragma unroll
-    for (int u = 0; u < VEC; ++u) bf16x8_to_f32(d[u], df[u]);
-    const int midx = lane < k ? __ldg(map + (size_t)t * k + lane) : 0;
-    const float gl = lane < k ? (gates ? __ldg(gates + (size_t)t * k + lane) : 1.0f) : 0.f;
-    float dg_lane = 0.f;  // lane j holds dgates[t, j]
+        for (int u = 0; u < VEC; ++u) d[r][u] = __ldg(ds + lane + 32 * u);
+      }
+    float lv[TPW][EQ];
+    if (want_dl) {
+#pragma unroll
+      for (int r = 0; r < TPW; ++r)
+#pragma unroll
+        for (int q = 0; q < EQ; ++q) {
+          const int e = lane + 32 * q;
+          lv[r][q] = (q < EQn && e < E && base + r < T) ? __ldg(logits + (size_t)(base + r) * E + e) : -FLT_MAX;
+        }
+    }
+    float dg_lane = 0.f;  // lane l holds dgates of its slot
     for (int j = 0; j < k; ++j) {
-      const int m = __shfl_sync(0xffffffffu, midx, j);
-      const float g = __shfl_sync(0xffffffffu, gl, j);
-      uint4 yv[VEC];
-      if (want_dg) {
-        const uint4* ys = y_rows + (size_t)m * RV;
+      uint4 yv[TPW][VEC];
+      int m[TPW];
+      float g[TPW];
 #pragma unroll
-        for (int u = 0; u < VEC; ++u) yv[u] = __ldg(ys + lane + 32 * u);
+      for (int r = 0; r < TPW; ++r) {
+        m[r] = __shfl_sync(0xffffffffu, midx, r * k + j);
+        g[r] = __shfl_sync(0xffffffffu, gl, r * k + j);
+        if (want_dg && base + r < T) {
+          const uint4* ys = y_rows + (size_t)m[r] * RV;
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) yv[r][u] = __ldg(ys + lane + 32 * u);
+        }
       }
-      uint4* o = dy_rows + (size_t)m * RV;
 #pragma unroll
-      for (int u = 0; u < VEC; ++u) {
-        float f[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) f[q] = g * df[u][q];
-        o[lane + 32 * u] = f32_to_bf16x8(f);
-      }
-      if (want_dg) {
+      for (int r = 0; r < TPW; ++r) {
+        if (base + r >= T) continue;
+        uint4* o = dy_rows + (size_t)m[r] * RV;
         float dot = 0.f;
 #pragma unroll
         for (int u = 0; u < VEC; ++u) {
-          float fy[8];
-          bf16x8_to_f32(yv[u], fy);
+          float f[8];
+          bf16x8_to_f32(d[r][u], f);
+          if (want_dg) {
+            float fy[8];
+            bf16x8_to_f32(yv[r][u], fy);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) dot = fmaf(fy[q], df[u][q], dot);
+            for (int q = 0; q < 8; ++q) dot = fmaf(fy[q], f[q], dot);
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) f[q] *= g[r];
+          o[lane + 32 * u] = f32_to_bf16x8(f);
         }
+        if (want_dg) {
 #pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
-        if (lane == j) dg_lane = dot;
+          for (int o2 = 16; o2 > 0; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+          if (lane == r * k + j) dg_lane = dot;
+        }
       }
     }
-    if (want_dg && lane < k) dgates[(size_t)t * k + lane] = dg_lane;
-    if (logits && (dlogits_bf16 || dlogits_f32)) {  // E <= 256 (checked on the host)
-      const float* row = logits + (size_t)t * E;
-      float lv[8];
-      float m = -FLT_MAX;
+    if (want_dg && sl) dgates[(size_t)(base + tl) * k + jl] = dg_lane;
+    if (want_dl) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = lane + 32 * q;
-        lv[q] = e < E ? row[e] : -FLT_MAX;
-        m = fmaxf(m, lv[q]);
-      }
+      for (int r = 0; r < TPW; ++r) {
+        if (base + r >= T) continue;  // warp-uniform
+        float mx = -FLT_MAX;
 #pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o2));
-      float ssum = 0.f, pv[8], dpl[8];
+        for (int q = 0; q < EQ; ++q) mx = fmaxf(mx, lv[r][q]);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        pv[q] = lane + 32 * q < E ? __expf(lv[q] - m) : 0.f;
-        ssum += pv[q];
-        dpl[q] = 0.f;
-      }
+        for (int o2 = 16; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+        float ssum = 0.f, pv[EQ], dpl[EQ];
 #pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o2);
-      const float inv = 1.f / ssum;
-      const int ej = lane < k ? __ldg(expert_idx + (size_t)t * k + lane) : -1;
-      float pdp = 0.f;
-      for (int j = 0; j < k; ++j) {  // warp-uniform
-        const int ejj = __shfl_sync(0xffffffffu, ej, j);
-        const float dgj = __shfl_sync(0xffffffffu, dg_lane, j);
+        for (int q = 0; q < EQ; ++q) {
+          pv[q] = (q < EQn && lane + 32 * q < E) ? __expf(lv[r][q] - mx) : 0.f;
+          ssum += pv[q];
+          dpl[q] = 0.f;
+        }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (lane + 32 * q == ejj) {
-            dpl[q] += dgj;
-            pdp += pv[q] * inv * dgj;
+        for (int o2 = 16; o2 > 0; o2 >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o2);
+        const float inv = 1.f / ssum;
+        float pdp = 0.f;
+        for (int j = 0; j < k; ++j) {  // warp-uniform
+          const int ejj = __shfl_sync(0xffffffffu, eidx, r * k + j);
+          const float dgj = __shfl_sync(0xffffffffu, dg_lane, r * k + j);
+#pragma unroll
+          for (int q = 0; q < EQ; ++q)
+            if (lane + 32 * q == ejj) {
+              dpl[q] += dgj;
+              pdp += pv[q] * inv * dgj;
+            }
+        }
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) pdp += __shfl_xor_sync(0xffffffffu, pdp, o2);
+#pragma unroll
+        for (int q = 0; q < EQ; ++q) {
+          const int e = lane + 32 * q;
+          if (q < EQn && e < E) {
+            const float dl = pv[q] * inv * (dpl[q] - pdp);
+            if (dlogits_bf16)
+              dlogits_bf16[(size_t)(base + r) * E + e] = __float2bfloat16_rn(dl);
+            else
+              dlogits_f32[(size_t)(base + r) * E + e] = dl;
           }
-      }
-#pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) pdp += __shfl_xor_sync(0xffffffffu, pdp, o2);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int e = lane + 32 * q;
-        if (e < E) {
-          const float dl = pv[q] * inv * (dpl[q] - pdp);
-          if (dlogits_bf16)
-            dlogits_bf16[(size_t)t * E + e] = __float2bfloat16_rn(dl);
-          else
-            dlogits_f32[(size_t)t * E + e] = dl;
         }
       }
     }
@@ -289,18 +317,58 @@ static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, 
     default: MOE_LAUNCH(NAME, KERNEL<8>, dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break; \
   }
 
+struct SbwdArgs {
+  const uint4* dy;
+  const uint4* y_rows;
+  const int32_t* map;
+  const float* gates;
+  uint4* dy_rows;
+  float* dgates;
+  int T, k;
+  const float* logits;
+  const int32_t* expert_idx;
+  int E;
+  __nv_bfloat16* dl16;
+  float* dl32;
+  const int32_t* counts;
+  const int32_t* pbins;
+  int bs;
+};
+
+template <int V, int TPW>
+static moe_status sbwd_launch(const SbwdArgs& a, cudaStream_t s) {
+  if (a.E <= 64)
+    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 2>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
+               a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
+               a.counts, a.pbins, a.bs);
+  else
+    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 8>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
+               a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
+               a.counts, a.pbins, a.bs);
+  return MOE_OK;
+}
+
 moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* y_rows, const int32_t* map,
                              const float* gates, void* dy_rows, float* dgates, const float* logits,
                              const int32_t* expert_idx, __nv_bfloat16* dlogits_bf16, float* dlogits_f32,
                              const moe_topology_t* pad_topo, cudaStream_t s) {
   const int vec = (int)(cfg->hidden / 256);
-  const int T = (int)cfg->tokens, k = (int)cfg->top_k, E = (int)cfg->num_experts, bs = (int)cfg->block_size;
-  const int32_t* counts = pad_topo ? pad_topo->counts : nullptr;
-  const int32_t* pbins = pad_topo ? pad_topo->padded_bins : nullptr;
-  MOE_VEC_DISPATCH(vec, "scatter_bwd", scatter_bwd_kernel, reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows),
-                   map, gates, reinterpret_cast<uint4*>(dy_rows), dgates, T, k, logits, expert_idx, E, dlogits_bf16,
-                   dlogits_f32, counts, pbins, bs);
-  return MOE_OK;
+  SbwdArgs a{reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows), map, gates,
+             reinterpret_cast<uint4*>(dy_rows), dgates, (int)cfg->tokens, (int)cfg->top_k, logits, expert_idx,
+             (int)cfg->num_experts, dlogits_bf16, dlogits_f32, pad_topo ? pad_topo->counts : nullptr,
+             pad_topo ? pad_topo->padded_bins : nullptr, (int)cfg->block_size};
+  // one token per warp: measured faster than 2-4 tokens per warp (whose register
+  // footprint halves the occupancy) at MoE-XS
+  switch (vec) {
+    case 1: return sbwd_launch<1, 1>(a, s);
+    case 2: return sbwd_launch<2, 1>(a, s);
+    case 3: return sbwd_launch<3, 1>(a, s);
+    case 4: return sbwd_launch<4, 1>(a, s);
+    case 5: return sbwd_launch<5, 1>(a, s);
+    case 6: return sbwd_launch<6, 1>(a, s);
+    case 7: return sbwd_launch<7, 1>(a, s);
+    default: return sbwd_launch<8, 1>(a, s);
+  }
 }
 
 }  // namespace moe

@@ -339,7 +339,8 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.max_tiles = L.p.m_tiles;
     MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 128, "moe_router x"));
     MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
-    L.tc = L.td = L.ta;
+    MOE_TRY(make_tmap_f32(&L.tc, logits, E, T, E, "moe_router logits"));
+    L.td = L.tc;
     return gemm_launch(L, as_stream(stream));
   }
   dim3 grid((unsigned)ceil_div(T, RT_TOK), (unsigned)ceil_div(E, RT_EXP));

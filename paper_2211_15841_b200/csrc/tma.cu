@@ -49,6 +49,26 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
   return MOE_OK;
 }
 
+moe_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
+                         const char* what) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(MOE_ECUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  if (!base) return set_error(MOE_EINVAL, "%s: NULL pointer", what);
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return set_error(MOE_EINVAL, "%s: pointer must be 16-byte aligned for TMA", what);
+  if ((row_elems * 4) % 16) return set_error(MOE_ESHAPE, "%s: row pitch must be a multiple of 16 bytes", what);
+  if (outer == 0) outer = 1;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_elems * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(MOE_ECUDA, "%s: cuTensorMapEncodeTiled (f32) failed (%d)", what, (int)r);
+  return MOE_OK;
+}
+
 moe_status make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
                              uint32_t nchunk, const char* what) {
   EncodeTiledFn enc = get_encode();

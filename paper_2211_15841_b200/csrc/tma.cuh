@@ -15,6 +15,9 @@ moe_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, ui
 // SWIZZLE_128B). inner must be a multiple of 64.
 moe_status make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
                              uint32_t nchunk, const char* what);
+// fp32 [outer, inner] map with 32 x 32 boxes, SWIZZLE_128B (router logits store).
+moe_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t row_elems,
+                         const char* what);
 // Epilogue store / H-prefetch maps: 32 x 32 boxes, 64 B swizzle.
 inline moe_status make_tmap_epi(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                                 uint64_t row_elems, const char* what) {
