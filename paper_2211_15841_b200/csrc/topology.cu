@@ -5,15 +5,16 @@
 // using a custom CUDA kernel ... construct the transposed metadata at this
 // time"; P:242 COO row indices; P:290 transpose indices).
 //
-// Three launches:
-//  1. topo_hist:   per-chunk expert histograms (shared-memory integer atomics:
-//                  order-independent, so deterministic).
-//  2. topo_scan:   one CTA: per-expert exclusive scan over chunks, counts, bins,
-//                  padded_bins, {Tp, nnz}, t_col_offsets, row_offsets[end].
-//  3. topo_emit:   (a) stable rank of every assignment within its expert
-//                  (warp match_any + per-warp prefix) -> sorted_idx, pos,
-//                  sorted_pos; (b) one thread per nonzero block emits the BCSR,
-//                  COO and transpose entries in closed form.
+// Two launches:
+//  1. topo_hist:       per-chunk expert histograms (shared-memory integer
+//                      atomics: order-independent, so deterministic).
+//  2. topo_scan_emit:  every CTA rescans the chunk histograms in shared memory
+//                      (counts, bins, padded_bins, pair_bins; CTA 0 publishes
+//                      them with {Tp, nnz}, t_col_offsets, row_offsets[end]),
+//                      then (a) ranks assignments stably within their expert
+//                      (warp match_any + per-warp prefix) -> sorted_idx, pos,
+//                      sorted_pos, or (b) emits the BCSR, COO and transpose
+//                      entries, one thread per nonzero block, in closed form.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -68,116 +69,122 @@ __device__ void block_exclusive_scan(int32_t* data, int n, int32_t* s_tmp, int32
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) topo_scan_kernel(int32_t* __restrict__ chunk_counts, int n_chunks, int E,
-                                                          int bs, int F, moe_topology_t topo) {
+// Scan + emit in one launch. Every CTA first recomputes, from the per-chunk
+// histograms (G x E ints, L2-resident), the per-expert totals, the chunk
+// prefix it needs and the E-long scans (bins, padded_bins, pair_bins) in
+// shared memory; CTA 0 also publishes the global arrays. Then blocks
+// [0, n_chunks) rank assignments stably (warp match_any + per-warp prefix) ->
+// sorted_idx, pos, sorted_pos, and the remaining blocks emit the BCSR, COO and
+// transpose entries, one thread per nonzero block, in closed form.
+__global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs,
+                                                               int F, int n_chunks,
+                                                               const int32_t* __restrict__ chunk_counts,
+                                                               moe_topology_t topo) {
   pdl_trigger();
   pdl_wait();
-  __shared__ int32_t s_counts[1024];
-  __shared__ int32_t s_pad[1024];
+  extern __shared__ int32_t s_dyn[];           // [32 warps][E] per-warp counts (ranking CTAs)
+  __shared__ int32_t s_cnt[1024], s_start[1024], s_pstart[1024], s_pair[1024], s_base[1024];
   __shared__ int32_t s_tmp[32];
-  __shared__ int32_t s_pairs[1024];
   __shared__ int32_t s_tot[3];
-  // (1) per-expert exclusive scan over chunks (chunk_counts becomes chunk base rank)
+  const bool ranking = (int)blockIdx.x < n_chunks;
+  // (1) per-expert totals and (ranking CTAs) this chunk's exclusive base
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int32_t run = 0;
+    int32_t run = 0, base = 0;
     for (int c0 = 0; c0 < n_chunks; c0 += 16) {
       int32_t v[16];  // batch the loads so they are in flight together
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = c0 + u < n_chunks ? chunk_counts[(size_t)(c0 + u) * E + e] : 0;
+      for (int u = 0; u < 16; ++u) v[u] = c0 + u < n_chunks ? __ldg(chunk_counts + (size_t)(c0 + u) * E + e) : 0;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        if (c0 + u < n_chunks) chunk_counts[(size_t)(c0 + u) * E + e] = run;
+        if (c0 + u == (int)blockIdx.x) base = run;
         run += v[u];
       }
     }
-    s_counts[e] = run;
-    s_pad[e] = ((run + bs - 1) / bs) * bs;
-    s_pairs[e] = (s_pad[e] / bs + 1) / 2;  // same-expert block-row pairs
-    topo.counts[e] = run;
+    s_base[e] = base;
+    s_cnt[e] = run;
+    const int32_t pc = ((run + bs - 1) / bs) * bs;
+    s_start[e] = run;
+    s_pstart[e] = pc;
+    s_pair[e] = (pc / bs + 1) / 2;  // same-expert block-row pairs
   }
   __syncthreads();
-  // (2) bins / padded_bins = inclusive cumsums (P:297 padding to a multiple of bs)
-  block_exclusive_scan(s_counts, E, s_tmp, &s_tot[0]);
-  block_exclusive_scan(s_pad, E, s_tmp, &s_tot[1]);
-  block_exclusive_scan(s_pairs, E, s_tmp, &s_tot[2]);
+  // (2) exclusive scans over experts: unpadded and padded group starts
+  block_exclusive_scan(s_start, E, s_tmp, &s_tot[0]);
+  block_exclusive_scan(s_pstart, E, s_tmp, &s_tot[1]);
+  block_exclusive_scan(s_pair, E, s_tmp, &s_tot[2]);
   const int Tp = s_tot[1];
   const int nnz = (Tp / bs) * F;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int32_t c = topo.counts[e];
-    const int32_t pc = ((c + bs - 1) / bs) * bs;
-    topo.bins[e] = s_counts[e] + c;
-    topo.padded_bins[e] = s_pad[e] + pc;
-    topo.pair_bins[e] = s_pairs[e] + (pc / bs + 1) / 2;
+  if (blockIdx.x == 0) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      const int32_t c = s_cnt[e], pc = ((c + bs - 1) / bs) * bs;
+      topo.counts[e] = c;
+      topo.bins[e] = s_start[e] + c;
+      topo.padded_bins[e] = s_pstart[e] + pc;
+      topo.pair_bins[e] = s_pair[e] + (pc / bs + 1) / 2;
+    }
     // transposed offsets of expert e's F block-columns: F*start/bs + j*pc/bs
-    for (int j = 0; j < F; ++j) topo.t_col_offsets[e * F + j] = F * (s_pad[e] / bs) + j * (pc / bs);
+    for (int q = threadIdx.x; q < E * F; q += blockDim.x) {
+      const int e = q / F, j = q - e * F;
+      const int32_t pc = ((s_cnt[e] + bs - 1) / bs) * bs;
+      topo.t_col_offsets[q] = F * (s_pstart[e] / bs) + j * (pc / bs);
+    }
+    if (threadIdx.x == 0) {
+      topo.t_col_offsets[E * F] = nnz;
+      topo.row_offsets[Tp / bs] = nnz;
+      topo.sizes[0] = Tp;
+      topo.sizes[1] = nnz;
+      topo.sizes[2] = s_tot[2];
+    }
   }
-  if (threadIdx.x == 0) {
-    topo.t_col_offsets[E * F] = nnz;
-    topo.row_offsets[Tp / bs] = nnz;
-    topo.sizes[0] = Tp;
-    topo.sizes[1] = nnz;
-    topo.sizes[2] = s_tot[2];
-  }
-}
-
-// Part (a): blocks [0, n_chunks) rank assignments; part (b): remaining blocks
-// emit the topology, one thread per potential nonzero block.
-__global__ void __launch_bounds__(1024) topo_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs, int F,
-                                                          int n_chunks, const int32_t* __restrict__ chunk_base,
-                                                          moe_topology_t topo) {
-  pdl_trigger();
-  pdl_wait();
-  if ((int)blockIdx.x < n_chunks) {
-    extern __shared__ int32_t s_w[];  // [32 warps][E] counts -> exclusive prefix over warps
+  if (ranking) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_w[i] = 0;
+    for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_dyn[i] = 0;
     __syncthreads();
     const int i = blockIdx.x * kTopoChunk + threadIdx.x;
     const bool valid = i < R;
-    const int e = valid ? idx[i] : E + lane;  // unique sentinel for inactive lanes
+    const int e = valid ? __ldg(idx + i) : E + lane;  // unique sentinel for inactive lanes
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const unsigned lt = (1u << lane) - 1u;
     const int rank_w = __popc(peers & lt);
-    if (valid && rank_w == 0) s_w[warp * E + e] = __popc(peers);
+    if (valid && rank_w == 0) s_dyn[warp * E + e] = __popc(peers);
     __syncthreads();
     for (int x = threadIdx.x; x < E; x += blockDim.x) {
       int32_t run = 0;
       for (int w = 0; w < 32; ++w) {
-        int32_t v = s_w[w * E + x];
-        s_w[w * E + x] = run;
+        int32_t v = s_dyn[w * E + x];
+        s_dyn[w * E + x] = run;
         run += v;
       }
     }
     __syncthreads();
     if (valid) {
-      const int rank = chunk_base[(size_t)blockIdx.x * E + e] + s_w[warp * E + e] + rank_w;
-      const int c = topo.counts[e];
-      const int pc = ((c + bs - 1) / bs) * bs;
-      const int u = topo.bins[e] - c + rank;
-      const int p = topo.padded_bins[e] - pc + rank;
+      const int rank = s_base[e] + s_dyn[warp * E + e] + rank_w;
+      const int u = s_start[e] + rank;
+      const int p = s_pstart[e] + rank;
       topo.sorted_idx[u] = i;
       topo.sorted_pos[i] = u;
       topo.pos[i] = p;
     }
   } else {
     const int s = (blockIdx.x - n_chunks) * blockDim.x + threadIdx.x;
-    const int nnz = topo.sizes[1];
     if (s >= nnz) return;
     const int r = s / F, j = s - r * F;
-    // expert of block-row r: first e with padded_bins[e] > r*bs
+    // expert of block-row r: last e with padded start <= r*bs (empty experts have no rows)
     int lo = 0, hi = E - 1;
     const int row0 = r * bs;
     while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (topo.padded_bins[mid] > row0) hi = mid; else lo = mid + 1;
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pstart[mid] <= row0) lo = mid; else hi = mid - 1;
     }
+    // (an empty expert e < E-1 starts where e+1 starts, so the last start <= row0
+    // belongs to the non-empty owner of the row)
     const int e = lo;
-    const int pc = topo.padded_bins[e] - (e > 0 ? topo.padded_bins[e - 1] : 0);
-    const int r0 = (topo.padded_bins[e] - pc) / bs;
+    const int r0 = s_pstart[e] / bs;
     topo.row_indices[s] = r;
     topo.col_indices[s] = e * F + j;
     if (j == 0) topo.row_offsets[r] = s;
-    const int qpos = topo.t_col_offsets[e * F + j] + (r - r0);
+    const int32_t pc = ((s_cnt[e] + bs - 1) / bs) * bs;
+    const int qpos = F * (s_pstart[e] / bs) + j * (pc / bs) + (r - r0);
     topo.t_block_offsets[qpos] = s;
     topo.t_row_indices[qpos] = r;
   }
@@ -199,15 +206,15 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   int32_t* chunk_counts = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + L.topo_chunk_counts);
   cudaStream_t s = as_stream(stream);
   MOE_LAUNCH("topo_hist", topo_hist_kernel, dim3(n_chunks), dim3(kTopoChunk), E * sizeof(int32_t), s, expert_idx, R, E, chunk_counts);
-  MOE_LAUNCH("topo_scan", topo_scan_kernel, dim3(1), dim3(1024), 0, s, chunk_counts, n_chunks, E, bs, F, *topo);
   const int emit_smem = 32 * E * (int)sizeof(int32_t);
   static int smem_set = 0;
-  if (emit_smem > 48 * 1024 && smem_set < emit_smem) {
-    cudaFuncSetAttribute(topo_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem);
+  if (emit_smem > 48 * 1024 - 21 * 1024 && smem_set < emit_smem) {
+    cudaFuncSetAttribute(topo_scan_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem);
     smem_set = emit_smem;
   }
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
-  MOE_LAUNCH("topo_emit", topo_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R, E, bs, F, n_chunks, chunk_counts, *topo);
+  MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
+             E, bs, F, n_chunks, chunk_counts, *topo);
   return MOE_OK;
 }
