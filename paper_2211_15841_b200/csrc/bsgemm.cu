@@ -50,6 +50,10 @@
 #define MOE_SDD_NBUF 2
 #endif
 
+#ifndef MOE_MAX_STAGES
+#define MOE_MAX_STAGES 16
+#endif
+
 namespace moe {
 
 using namespace sm100;
@@ -80,20 +84,12 @@ struct Cfg {
   static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 : 0;  // router epilogue exchange
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
   static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES + XCH;
   static_assert(STAGES >= 2, "not enough shared memory for two stages");
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
-
-__device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev) {
-  if (p.trace && tile_i < kTraceTiles) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[((size_t)blockIdx.x * kTraceTiles + tile_i) * kTraceEvents + ev] = t;
-  }
-}
 
 __device__ __forceinline__ int num_tiles(const GemmParams& p, int mode, int pair) {
   const int Tp = p.sizes ? p.sizes[0] : 0, nnz = p.sizes ? p.sizes[1] : 0;
@@ -129,13 +125,13 @@ __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pa
     t.v = tile % p.dense_tiles;
     const int b = __ldg(p.row_offsets + t.u), e = __ldg(p.row_offsets + t.u + 1);
     t.walk_begin = b;
-    t.kiters = 2 * (e - b);
+    t.kiters = KPB * (e - b);
   } else if (mode == DS_COL || mode == DDS_COL) {
     t.u = (tile / p.dense_tiles) * (mode == DDS_COL ? pair : 1);
     t.v = tile % p.dense_tiles;
     const int b = __ldg(p.t_col_offsets + t.u), e = __ldg(p.t_col_offsets + t.u + 1);
     t.walk_begin = b;
-    t.kiters = 2 * (e - b);
+    t.kiters = KPB * (e - b);
   } else {  // DENSE: tile = (split * m_tiles + m) * n_tiles + n
     t.v = tile % p.n_tiles;
     const int rest = tile / p.n_tiles;
@@ -174,11 +170,25 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
 // the [chunk][64 rows][128 B] layout of the MN-major UMMA descriptor (one TMA
 // instruction per operand: the per-SM TMA issue rate, not bytes, limits small
 // boxes; see scripts/micro/l2_tma_bw.cu).
-template <int MODE, bool A_MN, bool B_MN, int BN>
+template <bool PF>
+__device__ __forceinline__ void ld2(void* dst, const CUtensorMap* m, uint64_t* fb, int c0, int c1) {
+  if (!m) return;
+  if (PF) tma_prefetch_2d(m, c0, c1); else tma_load_2d(dst, m, fb, c0, c1);
+}
+template <bool PF>
+__device__ __forceinline__ void ld3(void* dst, const CUtensorMap* m, uint64_t* fb, int c0, int c1, int c2) {
+  if (!m) return;
+  if (PF) tma_prefetch_3d(m, c0, c1, c2); else tma_load_3d(dst, m, fb, c0, c1, c2);
+}
+#define tma_load_2d ld2<PF>
+#define tma_load_3d ld3<PF>
+template <int MODE, bool A_MN, bool B_MN, int BN, bool PF = false>
 __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p,
                                             const TileInfo& t, int kit, int sblk, int oblk, uint8_t* sa, uint8_t* sb,
-                                            uint64_t* fb) {
-  const int kk = kit & 1;
+                                            uint64_t* fb, int part = 3) {
+  const int kk = kit % KPB;
+  if (!(part & 1)) ta = nullptr;  // A boxes skipped below
+  if (!(part & 2)) tb = nullptr;
   if (MODE == SDD) {
     const int k0 = kit * BK;
     tma_load_2d(sa, ta, fb, k0, t.u * BM);
@@ -205,7 +215,7 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtenso
       tma_load_2d(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
 #pragma unroll
     for (int j = 0; j < BN / 128; ++j)  // blocks (r, c + j): storage sblk + j
-      tma_load_3d(sb + j * 16384, tb, fb, 0, (sblk + j) * BM + kk * BK, 0);
+      tma_load_3d(sb + j * (2 * BK * 128), tb, fb, 0, (sblk + j) * BM + kk * BK, 0);
   } else if (MODE == DDS_ROW) {
     if (A_MN)
       tma_load_3d(sa, ta, fb, 0, oblk * BM + kk * BK, t.v * 2);
@@ -224,6 +234,8 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtenso
       tma_load_2d(sb, tb, fb, k0, t.v * BN);
   }
 }
+#undef tma_load_2d
+#undef tma_load_3d
 
 template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
@@ -283,15 +295,20 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tile_i = 0;
+    // L2-prefetch mode (MOE_GEMM_DBG & 128, NP == 2): warp 0 issues every stage,
+    // warp 1 prefetches the K-step STAGES ahead of it into L2
+    const bool pf_mode = C::NP == 2 && (p.dbg & 128);
+    const bool prefetcher = pf_mode && warp == 1;
+    long long g = 0;  // global K-step index of this CTA
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
       for (int kit = 0; kit < t.kiters; ++kit) {
-        const int blk = kit >> 1, kk = kit & 1;
+        const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0) {
           const int q = t.walk_begin + blk + lane;
-          if (q < t.walk_begin + (t.kiters >> 1)) {
+          if (q < t.walk_begin + (t.kiters / KPB)) {
             if (MODE == DSD_ROW || MODE == DDS_ROW) {
               idx_a = q;
               idx_b = __ldg(p.col_indices + q);
@@ -303,15 +320,29 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
-        if (stage % C::NP == warp) mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0 && stage % C::NP == warp) {
+        if (prefetcher) {
+          const long long h = g - STAGES;  // the stage warp 0 fills while we prefetch step g
+          if (h >= 0) mbar_wait(&empty[h % STAGES], (uint32_t)((h / STAGES) & 1) ^ 1u);
+          if (lane == 0)
+            issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, nullptr, nullptr, nullptr);
+          __syncwarp();
+          ++g;
+          continue;
+        }
+        const bool mine = pf_mode ? true : stage % C::NP == warp;
+        if (mine) mbar_wait(&empty[stage], phase ^ 1);
+        // lane 0 issues the A box(es), lane 1 the B box(es): each thread keeps
+        // its own TMA requests in flight (MOE_GEMM_DBG & 256 -> lane 0 issues both)
+        const bool split = !(p.dbg & 256);
+        if (mine && (lane == 0 || (split && lane == 1))) {
           uint64_t* fb = &full[stage];
           if (p.dbg & 8) {
-            mbar_arrive(fb);
+            if (lane == 0) mbar_arrive(fb);
           } else {
-            mbar_arrive_expect_tx(fb, C::STAGE);
+            if (lane == 0) mbar_arrive_expect_tx(fb, C::STAGE);
+            const int part = split ? (lane == 0 ? 1 : 2) : 3;
             issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
-                                                     smem_b + stage * C::B_BYTES, fb);
+                                              smem_b + stage * C::B_BYTES, fb, part);
           }
         }
         __syncwarp();
@@ -346,9 +377,9 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t adesc =
-                A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+                A_MN ? make_sdesc(a_base + k * 2048, BK * 128, 1024) : make_sdesc(a_base + k * 32, 16, KSW * 8, KSW);
             const uint64_t bdesc =
-                B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+                B_MN ? make_sdesc(b_base + k * 2048, BK * 128, 1024) : make_sdesc(b_base + k * 32, 16, KSW * 8, KSW);
             if (!(p.dbg & 2)) mma_bf16(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
           }
           mma_commit(&empty[stage]);
@@ -905,11 +936,11 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   L.p.aux_deriv = deriv ? 1 : 0;
   L.epi_h = L.p.epi == EPI_ACT_BWD;
   L.max_tiles = (int)(nnz / (L.bn / 128));
-  MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, 64, 128, "moe_sdd a"));
+  MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, BK, 128, "moe_sdd a", KSW));
   if (!trans_b)
     MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, L.bn / 64, "moe_sdd b"));
   else
-    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, 64, L.bn, "moe_sdd b^T"));
+    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, L.bn, "moe_sdd b^T", KSW));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   if (out_aux) MOE_TRY(make_tmap_epi(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
   if (act_src) MOE_TRY(make_tmap_epi(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
@@ -936,7 +967,9 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  const bool pair = use_pair(cfg) && trans_s;  // column pairs only (DS^TD); see moe_sdd
+  static int pair_rows = -1;
+  if (pair_rows < 0) pair_rows = getenv("MOE_GEMM_PAIR_ROWS") != nullptr;  // experiment: row pairs for DSD / DSD^T
+  const bool pair = use_pair(cfg) && (trans_s || pair_rows);
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.bn = pick_bn(cfg, false);
@@ -949,11 +982,11 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
     L.a_mn = false;
     L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * L.p.dense_tiles)
                        : (int)(rows / BM * L.p.dense_tiles);
-    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, 64, 128, "moe_dsd s"));
+    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, BK, 128, "moe_dsd s", KSW));
     if (!trans_b)
       MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, N, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
-      MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, 64, bbox, "moe_dsd b^T"));
+      MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
   } else {
     L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
@@ -964,7 +997,7 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
     if (!trans_b)
       MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, rows, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
-      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, 64, bbox, "moe_dsd b^T"));
+      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
   }
   L.td = L.tc;
@@ -994,7 +1027,7 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
     if (trans_a)
       MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, rows, h, 2, "moe_dds a^T"));
     else
-      MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, 64, 128, "moe_dds a"));
+      MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, BK, 128, "moe_dds a", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
     L.td = L.tc;
     return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
@@ -1006,11 +1039,11 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
   L.bn = 128;
   L.b_mn = false;
   L.max_tiles = (int)(rows / BM * L.p.dense_tiles);
-  MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, 64, 128, "moe_dds s^T"));
+  MOE_TRY(make_tmap_bf16(&L.tb, s, 128, nnz * 128, 128, BK, 128, "moe_dds s^T", KSW));
   if (trans_a)
     MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, N, h, 2, "moe_dds a^T"));
   else
-    MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, 64, 128, "moe_dds a"));
+    MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, BK, 128, "moe_dds a", KSW));
   MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));
   L.td = L.tc;
   return gemm_launch(L, as_stream(stream));

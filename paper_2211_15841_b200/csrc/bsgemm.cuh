@@ -78,6 +78,17 @@ int gemm_dbg();
 // 2 MMA last commit, 3 epilogue got accumulator, 4 epilogue done.
 constexpr int kTraceLaunches = 16, kTraceCtas = 160, kTraceTiles = 32, kTraceEvents = 5;
 unsigned long long* gemm_trace_slot();
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev) {
+  if (p.trace && tile_i < kTraceTiles) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[((size_t)blockIdx.x * kTraceTiles + tile_i) * kTraceEvents + ev] = t;
+  }
+}
+
+#endif
 // CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
 // 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);

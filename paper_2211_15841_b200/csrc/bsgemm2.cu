@@ -30,6 +30,10 @@
 #include "sm100.cuh"
 #include "tma.cuh"
 
+#ifndef MOE_MAX_STAGES
+#define MOE_MAX_STAGES 16
+#endif
+
 namespace moe {
 
 constexpr int P_BN = 256;                      // N of the pair MMA
@@ -42,7 +46,7 @@ template <bool EPI_H>
 struct Cfg2 {
   static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES) / P_STAGE;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * P_BN;
   static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + EPI_BYTES + H_BYTES;
 };
@@ -97,14 +101,14 @@ __device__ __forceinline__ Tile2 decode2(const GemmParams& p, int mode, int tile
     row_pair(p, pr, t.r0, t.second);
     const int b = __ldg(p.row_offsets + t.r0), e = __ldg(p.row_offsets + t.r0 + 1);
     t.walk_begin = b;
-    t.kiters = 2 * (e - b);
+    t.kiters = KPB * (e - b);
     t.q_off = rank * (e - b);
   } else {  // DS_COL, DDS_COL
     t.c0 = (tile / p.dense_tiles) * 2;
     t.v = tile % p.dense_tiles;
     const int b = __ldg(p.t_col_offsets + t.c0), e = __ldg(p.t_col_offsets + t.c0 + 1);
     t.walk_begin = b;
-    t.kiters = 2 * (e - b);
+    t.kiters = KPB * (e - b);
     t.second = true;
   }
   return t;
@@ -182,14 +186,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ===================== TMA producer (both CTAs) =====================
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = cid; tile < ntiles; tile += ncl) {
+    int tile_i = 0;
+    for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
       const Tile2 t = decode2(p, MODE, tile, rank);
+      if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;
       for (int kit = 0; kit < t.kiters; ++kit) {
-        const int blk = kit >> 1, kk = kit & 1;
+        const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
           const int qq = t.walk_begin + blk + lane;
-          if (qq < t.walk_begin + (t.kiters >> 1)) {
+          if (qq < t.walk_begin + (t.kiters / KPB)) {
             if (MODE == DSD_ROW) {
               idx_a = qq + t.q_off;               // this CTA's row: same column, next row
               idx_b = __ldg(p.col_indices + qq);  // block column
@@ -256,11 +262,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int tile_i = -1;
       for (int tile = cid; tile < ntiles; tile += ncl) {
         const Tile2 t = decode2(p, MODE, tile, 0);
+        ++tile_i;
         if (t.kiters == 0) continue;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        trace_ev(p, tile_i, 1);
         const uint32_t d_tmem = tmem_base + acc * P_BN;
         for (int kit = 0; kit < t.kiters; ++kit) {
           mbar_wait(&full[stage], phase);
@@ -270,9 +279,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t adesc =
-                A_MN ? make_sdesc(a_base + k * 2048, 8192, 1024) : make_sdesc(a_base + k * 32, 16, 1024);
+                A_MN ? make_sdesc(a_base + k * 2048, BK * 128, 1024) : make_sdesc(a_base + k * 32, 16, KSW * 8, KSW);
             const uint64_t bdesc =
-                B_MN ? make_sdesc(b_base + k * 2048, 8192, 1024) : make_sdesc(b_base + k * 32, 16, 1024);
+                B_MN ? make_sdesc(b_base + k * 2048, BK * 128, 1024) : make_sdesc(b_base + k * 32, 16, KSW * 8, KSW);
             if (!(p.dbg & 2)) mma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
           }
           mma_commit_pair(&empty[stage], 0x3);
@@ -282,6 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit_pair(&tfull[acc], 0x3);
+        trace_ev(p, tile_i, 2);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -323,8 +333,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     };
 
+    int tile_i = -1;
     for (int tile = cid; tile < ntiles; tile += ncl) {
       const Tile2 t = decode2(p, MODE, tile, rank);
+      ++tile_i;
       const bool has_acc = t.kiters > 0;
       const bool mine = rank == 0 || t.second;  // does this CTA own real output rows?
       if (EPI_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
@@ -332,6 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
       }
+      if (wq == 0 && lane == 0) trace_ev(p, tile_i, 3);
       const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * P_BN;
       if (p.dbg & 1) {
         if (has_acc) {
@@ -389,6 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+      if (wq == 0 && lane == 0) trace_ev(p, tile_i, 4);
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -416,6 +430,7 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   if (grid < 2) grid = 2;
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
+  p.trace = gemm_trace_slot();
   cudaError_t le = launch_k(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
   if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);

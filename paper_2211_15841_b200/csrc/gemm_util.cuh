@@ -13,7 +13,13 @@ namespace moe {
 using namespace sm100;
 
 constexpr int BM = 128;
-constexpr int BK = 64;
+#ifndef MOE_BK
+#define MOE_BK 64
+#endif
+constexpr int BK = MOE_BK;        // K per pipeline stage (64: 128B-swizzled K-major rows; 32: 64B-swizzled)
+constexpr int KPB = 128 / BK;     // stages per 128 x 128 sparse block
+constexpr int KSW = BK * 2;       // K-major row bytes = TMA / UMMA swizzle span
+static_assert(BK == 32 || BK == 64, "BK must be 32 or 64");
 constexpr int NUM_EPI_WARPS = 8;                  // 2 per TMEM lane quarter (column halves)
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;

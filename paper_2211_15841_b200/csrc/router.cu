@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "permute.cuh"
 #include "tma.cuh"
+#include "gemm_util.cuh"
 
 namespace moe {
 
@@ -248,7 +249,7 @@ moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat
   L.p.m_tiles = (int)ceil_div(h, 128);
   L.p.n_tiles = 1;
   L.p.splits = parts;
-  L.p.k_iters_total = (int)ceil_div(T, 64);
+  L.p.k_iters_total = (int)ceil_div(T, BK);
   L.p.kiters_split = (int)ceil_div(L.p.k_iters_total, parts);
   L.p.epi = EPI_F32;
   L.p.rows_valid = h;
@@ -280,7 +281,7 @@ moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, con
   D.p.m_tiles = (int)ceil_div(T, 128);
   D.p.n_tiles = h / D.bn;
   D.p.splits = 1;
-  D.p.k_iters_total = D.p.kiters_split = E / 64;
+  D.p.k_iters_total = D.p.kiters_split = E / BK;
   D.p.epi = EPI_ADD_ROWS;
   D.p.rows_valid = T;
   D.p.addend = reinterpret_cast<const __nv_bfloat16*>(addend);
@@ -288,8 +289,8 @@ moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, con
   D.p.addend_map = addend_map;
   D.p.addend_k = addend_k;
   D.max_tiles = D.p.m_tiles * D.p.n_tiles;
-  MOE_TRY(make_tmap_bf16(&D.ta, dlogits, E, T, E, 64, 128, "router dx dlogits"));
-  MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, 64, D.bn, "router dx wr"));
+  MOE_TRY(make_tmap_bf16(&D.ta, dlogits, E, T, E, BK, 128, "router dx dlogits", KSW));
+  MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, BK, D.bn, "router dx wr", KSW));
   MOE_TRY(make_tmap_epi(&D.tc, dx, h, T, h, "router dx out"));
   D.td = D.tc;
   return gemm_launch(D, s);
@@ -328,7 +329,7 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.p.m_tiles = (int)ceil_div(T, 128);
     L.p.n_tiles = 1;
     L.p.splits = 1;
-    L.p.k_iters_total = L.p.kiters_split = (int)ceil_div(h, 64);
+    L.p.k_iters_total = L.p.kiters_split = (int)ceil_div(h, BK);
     L.p.epi = EPI_ROUTER;
     L.p.rows_valid = T;
     L.p.logits = logits;
@@ -337,7 +338,7 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.p.E = E;
     L.p.topk = (int)cfg->top_k;
     L.max_tiles = L.p.m_tiles;
-    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, 64, 128, "moe_router x"));
+    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, BK, 128, "moe_router x", KSW));
     MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
     MOE_TRY(make_tmap_f32(&L.tc, logits, E, T, E, "moe_router logits"));
     L.td = L.tc;

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "tma.cuh"
+#include "gemm_util.cuh"
 
 namespace moe {
 
@@ -81,7 +82,7 @@ moe_status make_tmap_bf16_mn(CUtensorMap* map, const void* base, uint64_t inner,
   if (outer == 0) outer = 1;
   cuuint64_t dims[3] = {64, outer, inner / 64};
   cuuint64_t strides[2] = {row_elems * 2, 128};
-  cuuint32_t box[3] = {64, 64, nchunk};
+  cuuint32_t box[3] = {64, (cuuint32_t)BK, nchunk};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

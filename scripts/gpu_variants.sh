@@ -4,7 +4,7 @@
 mkdir -p gpurun_out; TAG=$1; shift
 i=0
 for v in "$@"; do
-  rm -f build/bsgemm.o
+  rm -f build/*.o
   make -s EXTRA="$v" > gpurun_out/build_${TAG}_$i.log 2>&1 || { echo "build $v failed"; continue; }
   timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_${TAG}_$i.json 2> gpurun_out/bench_${TAG}_$i.err
   python - "$TAG" "$i" "$v" <<'PY'
@@ -17,4 +17,4 @@ except Exception as e:
 PY
   i=$((i+1))
 done
-rm -f build/bsgemm.o; make -s > /dev/null 2>&1
+rm -f build/*.o; make -s > /dev/null 2>&1

@@ -49,7 +49,7 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-constexpr int S = 16;  // max ring stages
+constexpr int S = 32;  // max ring stages
 
 // mode 0 distinct, 1 shared(G), 2 multicast cluster C (launched with cluster dims C)
 struct Maps { CUtensorMap m[4]; };
@@ -72,7 +72,21 @@ __global__ void __launch_bounds__(128, 1) bw_kernel(const __grid_constant__ Maps
   if (C > 1) cluster_sync(); else __syncthreads();
   const int b = blockIdx.x;
   mode &= 3;
-  if (G == 555 || G == 556 || G == 557) {
+  if (G == 900) {
+    // every lane of warp 0 owns one stage and issues its own boxes
+    if (warp == 0 && lane < NS) {
+      const int s = lane;
+      for (int i = 0; i < iters / NS; ++i) {
+        if (i > 0) mbar_wait(&full[s], (i - 1) & 1);
+        const int box = (int)(((long long)(b * NS + lane) * iters + i) % nboxes);
+        mbar_expect(&full[s], BOX);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(su32(buf + s * BOX)), "l"(&maps.m[0]), "r"(0), "r"(box * rows_per_box), "r"(su32(&full[s])) : "memory");
+      }
+      mbar_wait(&full[s], ((iters / NS) - 1) & 1);
+    }
+  } else if (G == 555 || G == 556 || G == 557) {
     const int P = G - 553;  // 2, 3, 4 producer warps
     if (warp < P && lane == 0) {
       const int ns = NS / P;
@@ -136,7 +150,7 @@ int main() {
   cudaEvent_t a, e;
   cudaEventCreate(&a);
   cudaEventCreate(&e);
-  for (int rows : {64, 256}) {
+  for (int rows : {32, 64}) {
     const int inner = 64;
     const int BOX = rows * inner * 2;
     const int nboxes = (int)(bytes / BOX);
@@ -151,7 +165,7 @@ int main() {
     const int NS = ring_kb * 1024 / BOX;
     const int smem = ring_kb * 1024 + 1024;
     cudaFuncSetAttribute(bw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int G : {777, 555, 557}) {
+    for (int G : {777, 557, 900}) {
       const int grid = sms;
       const int iters = (int)((1LL << 30) / ((long long)grid * BOX)) / 16 * 16;
       for (int rep = 0; rep < 2; ++rep) {
@@ -164,7 +178,7 @@ int main() {
       cudaEventElapsedTime(&ms, a, e);
       const double delivered = (double)grid * iters * BOX;
       printf("box %5d B ring %3d KB producers %d : %8.1f GB/s total (%.1f GB/s per CTA) %s\n", BOX, ring_kb,
-             G == 777 ? 1 : G - 553, delivered / ms / 1e6, delivered / ms / 1e6 / grid,
+             G == 777 ? 1 : (G == 900 ? 32 : G - 553), delivered / ms / 1e6, delivered / ms / 1e6 / grid,
              cudaGetErrorString(cudaGetLastError()));
     }
   }

@@ -58,8 +58,8 @@ def main(out):
     step.run()
     n = lib.moe_debug_trace_dump(out.encode())
     tr = np.fromfile(out, dtype=np.uint64).reshape(n, C, TT, EV).astype(np.float64)
-    # 1-SM GEMM launches in step order (the CTA-pair DS^TD / DD^TS kernels do not trace)
-    gemm_names = [nm for nm in step.names if nm in ("router", "sdd", "dsd", "sddT", "dsdT", "router_dwr", "router_dx")]
+    gemm_names = [nm for nm in step.names if nm in ("router", "sdd", "dsd", "sddT", "dsTd", "dsdT", "ddTs",
+                                                   "router_dwr", "router_dx")]
     for li in range(n):
         a = tr[li]
         valid = a[..., 1] > 0
