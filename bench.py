@@ -111,7 +111,8 @@ def work_model(T, h, f, E, k, Tp):
         "prod_flop": prod_flop,
         "prod_bytes": prod_bytes,
         "sddt_bytes": prod_bytes + 2 * R * f,      # + read of the saved pre-activation H
-        "sdd_bytes": prod_bytes + 2 * R * f,       # + write of H (kept for act' in the backward)
+        "sdd_bytes": prod_bytes + 2 * R * f,       # + write of act'(H) (kept for the backward)
+        "dsd_scatter_bytes": prod_bytes + 2 * T * h + 4 * R,  # + the gate-weighted rows scattered to y
         "gather_bytes": 2 * (T * h + R * h) + 4 * R,
         "scatter_bytes": 2 * (R * h + T * h) + 8 * R,
         "scatter_bwd_bytes": 2 * (T * h + 2 * R * h) + 4 * R,
@@ -147,8 +148,8 @@ class Step:
             ("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
             ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
                                       None if idn else d(sv.act_deriv), s)),
-            ("dsd", L.moe_dsd, (c, d(sv.a), 0, d(t["w2"]), 0, topo, d(sv.y_g), s)),
-            ("scatter", L.moe_scatter, (c, d(sv.y_g), topo, d(sv.gates), d(t["y"]), s)),
+            ("dsd+scatter", L.moe_dsd_scatter, (c, d(sv.a), d(t["w2"]), topo, d(sv.gates), d(sv.y_g),
+                                                 d(t["y"]), s)),
         ]
         fused =cfg.num_experts % 64 == 0 and cfg.num_experts <= 256 and cfg.top_k <= 8
         if fused:   # moe_backward's tensor-core router path (layer.cu)
@@ -305,7 +306,7 @@ def run_ours_single(args, peaks):
     shares = mean_call / mean_call.sum()
     dom = int(np.argmax(mean_call))
     dname = step.names[dom]
-    prod_names = {"sdd": "sdd_bytes", "dsd": "prod_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
+    prod_names = {"sdd": "sdd_bytes", "dsd+scatter": "dsd_scatter_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
                   "dsdT": "prod_bytes", "ddTs": "prod_bytes"}
     byte_names = {"gather": "gather_bytes", "scatter": "scatter_bytes", "scatter_bwd": "scatter_bwd_bytes",
                   "gather_bwd": "gather_bwd_bytes"}

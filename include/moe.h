@@ -116,6 +116,8 @@ typedef struct {
   int32_t* t_row_indices;   /* [max_nnz]          row of each block in transposed order      */
   int32_t* pair_bins;       /* [E]  inclusive cumsum of ceil(block_rows_e / 2): pairs of
                                     same-expert block-rows (2-SM tiles of the GEMMs)          */
+  int32_t* row_src;         /* [max_rows] flat id i = t*k + j held by padded row p (the
+                                    inverse of pos), -1 for pad rows                          */
   int32_t* sizes;           /* [3] = {Tp, nnz, row pairs}, written on the device             */
 } moe_topology_t;
 
@@ -213,6 +215,14 @@ moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, in
                          void* out_deriv, void* stream);
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream);
+/* moe_dsd_scatter: the layer's DSD fused with the weighted
+ * un-permutation: y_g [max_rows, h] = S . b (b = W2 [E*f, h]) and
+ * y [T, h] with y[t] = sum_j gates[t,j] * y_g[pos[t*k+j]]. For top-1 the
+ * DSD epilogue writes the gate-scaled rows straight to y[t] with TMA
+ * tile::scatter4 (rows via topo->row_src, pad rows dropped); for k > 1 it is
+ * moe_dsd followed by moe_scatter. y_g is still written (the backward needs it). */
+moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
+                           const float* gates, void* y_g, void* y, void* stream);
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
                    const moe_topology_t* topo, void* out, void* stream);
 

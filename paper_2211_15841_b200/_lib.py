@@ -22,7 +22,8 @@ class MoeConfig(ctypes.Structure):
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",
-               "col_indices", "row_indices", "t_col_offsets", "t_block_offsets", "t_row_indices", "pair_bins", "sizes"]
+               "col_indices", "row_indices", "t_col_offsets", "t_block_offsets", "t_row_indices", "pair_bins", "row_src",
+               "sizes"]
 
 
 class MoeTopology(ctypes.Structure):
@@ -71,6 +72,7 @@ SIGNATURES = {
     "moe_sdd": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
+    "moe_dsd_scatter": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
     "moe_dds": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),
     "moe_scatter_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),

@@ -63,7 +63,8 @@ class Topology:
         F = cfg.ffn_hidden // bs
         shapes = {"counts": E, "bins": E, "padded_bins": E, "sorted_idx": R, "pos": R, "sorted_pos": R,
                   "row_offsets": rows // bs + 1, "col_indices": nnz, "row_indices": nnz,
-                  "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "pair_bins": E, "sizes": 3}
+                  "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "pair_bins": E,
+                  "row_src": rows, "sizes": 3}
         self.t = {n: torch.empty(max(int(shapes[n]), 1), dtype=torch.int32, device=device) for n in TOPO_FIELDS}
         self.struct = MoeTopology(*[self.t[n].data_ptr() for n in TOPO_FIELDS])
 
@@ -193,6 +194,16 @@ def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
     check("moe_dsd", lib.moe_dsd(ctypes.byref(cfg), _p(s), int(trans_s), _p(b), int(trans_b),
                                  ctypes.byref(topo.struct), _p(out), _stream()))
     return out
+
+
+def moe_dsd_scatter(cfg, s, w2, topo: Topology, gates, y_g=None, y=None):
+    """moe_dsd_scatter (include/moe.h): Y_g = S . W2 and y = weighted un-permutation of Y_g."""
+    rows = moe_max_padded_rows(cfg)
+    y_g = y_g if y_g is not None else torch.empty(rows, cfg.hidden, dtype=torch.bfloat16, device=s.device)
+    y = y if y is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device=s.device)
+    check("moe_dsd_scatter", lib.moe_dsd_scatter(ctypes.byref(cfg), _p(s), _p(w2), ctypes.byref(topo.struct),
+                                                 _p(gates), _p(y_g), _p(y), _stream()))
+    return y_g, y
 
 
 def moe_dds(cfg, a, trans_a, s, trans_s, topo: Topology, out=None):

@@ -471,6 +471,15 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       // are loaded now, so the gather latency overlaps this tile's epilogue.
       constexpr int NPW0 = NCHUNK / NG;
       uint4 pre[MODE == DENSE ? NPW0 : 1][4];
+      int my_tok = 0x7fffffff;  // scatter target row (out of range: dropped)
+      float my_gate = 0.f;
+      if (MODE == DSD_ROW && p.scatter_y) {
+        const int src = __ldg(p.row_src + t.u * BM + row0 + lane);
+        if (src >= 0) {
+          my_tok = src;
+          my_gate = __ldg(p.scatter_gates + src);
+        }
+      }
       if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
         if (tile_i == 0) addend_prefetch(tile, pre_next);
 #pragma unroll
@@ -572,6 +581,28 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             }
           }
           store_chunk(&tmap_c, v, x, y);
+          if (MODE == DSD_ROW && p.scatter_y) {
+            // the weighted un-permutation of the layer (top-1): the
+            // gate-scaled rows go straight to y[token] by tile::scatter4
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] *= my_gate;
+            int tk[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) tk[u] = __shfl_sync(0xffffffffu, my_tok, u);
+            if (lane == 0) bulk_wait_read<C::NBUF - 1>();
+            __syncwarp();
+            stage_row(stg + sbuf * EPI_BUF, lane, v);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+              for (int g4 = 0; g4 < 8; ++g4)
+                tma_scatter4(&tmap_d, stg + sbuf * EPI_BUF + g4 * 4 * 64, x, tk[4 * g4], tk[4 * g4 + 1],
+                             tk[4 * g4 + 2], tk[4 * g4 + 3]);
+              bulk_commit();
+            }
+            sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
+          }
           if (PP && has_acc && i + 1 < NPW) tmem_ld_wait();
         }
       } else if (MODE == DENSE && p.epi == EPI_ROUTER) {
@@ -871,6 +902,14 @@ static int pick_bn(const moe_config* cfg, bool pairs_columns) {
   return (cfg->hidden % 256 == 0) ? 256 : 128;
 }
 
+// Experiment switch MOE_GEMM_PAIR_ROWS: row-pair 2-SM tiles for DSD / DSD^T
+// (measured slower at MoE-XS: half-empty pairs of odd-row experts).
+static bool use_pair_rows() {
+  static int v = -1;
+  if (v < 0) v = getenv("MOE_GEMM_PAIR_ROWS") != nullptr;
+  return v == 1;
+}
+
 // 2-SM (cta_group::2) 256 x 256 tiles: needs even F and h % 256 == 0.
 // MOE_GEMM_PAIR=0 in the environment selects the 1-SM kernels (A/B testing).
 static bool use_pair(const moe_config* cfg) {
@@ -960,16 +999,14 @@ moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, in
   return sdd_launch(cfg, a, b, trans_b, topo, act, deriv_src, out_s, out_deriv, true, stream);
 }
 
-moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
-                   const moe_topology_t* topo, void* out, void* stream) {
+static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
+                             const moe_topology_t* topo, void* out, const float* gates, void* y, void* stream) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  static int pair_rows = -1;
-  if (pair_rows < 0) pair_rows = getenv("MOE_GEMM_PAIR_ROWS") != nullptr;  // experiment: row pairs for DSD / DSD^T
-  const bool pair = use_pair(cfg) && (trans_s || pair_rows);
+  const bool pair = use_pair(cfg) && (trans_s || use_pair_rows());
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.bn = pick_bn(cfg, false);
@@ -988,6 +1025,13 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
+    if (y) {  // fused weighted un-permutation (top-1): rows scattered to y[token] by tile::scatter4
+      MOE_TRY(make_tmap_bf16(&L.td, y, h, cfg->tokens, h, 32, 1, "moe_dsd_scatter y", 64));
+      L.p.scatter_y = 1;
+      L.p.scatter_T = (int)cfg->tokens;
+      L.p.row_src = topo->row_src;
+      L.p.scatter_gates = gates;
+    }
   } else {
     L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
     L.mode = DS_COL;
@@ -1000,8 +1044,22 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
       MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
   }
-  L.td = L.tc;
+  if (!L.p.scatter_y) L.td = L.tc;
   return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
+}
+
+moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
+                   const moe_topology_t* topo, void* out, void* stream) {
+  return dsd_launch(cfg, s, trans_s, b, trans_b, topo, out, nullptr, nullptr, stream);
+}
+
+moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
+                           const float* gates, void* y_g, void* y, void* stream) {
+  MOE_CHECK_ARG(gates && y, "moe_dsd_scatter: NULL gates or y");
+  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && !use_pair_rows())
+    return dsd_launch(cfg, s, 0, b, 0, topo, y_g, gates, y, stream);
+  MOE_TRY(moe_dsd(cfg, s, 0, b, 0, topo, y_g, stream));  // k > 1: slots are summed by the combine kernel
+  return moe_scatter(cfg, y_g, topo, gates, y, stream);
 }
 
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,

@@ -32,7 +32,12 @@ struct GemmParams {
   int m_tiles, n_tiles, splits, kiters_split, k_iters_total;
   // epilogue
   int epi, act, has_pre;
-  int aux_deriv;  // EPI_ACT_FWD: the aux output is act'(H), not H; EPI_ACT_BWD: the source holds act'(H)
+  int aux_deriv;
+  // DSD_ROW + scatter_y (top-1 only): y[t] = gate[t] * row p of the output, t = row_src[p]
+  // (tile::scatter4 through tmap_d; pad rows dropped)
+  int scatter_y, scatter_T;
+  const int32_t* row_src;
+  const float* scatter_gates;  // EPI_ACT_FWD: the aux output is act'(H), not H; EPI_ACT_BWD: the source holds act'(H)
   int rows_valid;  // rows of the output that exist (DENSE: M)
   // EPI_ROUTER
   float* logits;

@@ -28,9 +28,8 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
   MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
                         stream));
-  MOE_TRY(moe_dsd(cfg, sv->a, 0, w->w2, 0, &sv->topo, sv->y_g, stream));
-  // (5) x = padded_scatter(x, indices) * weights
-  MOE_TRY(moe_scatter(cfg, sv->y_g, &sv->topo, sv->gates, y, stream));
+  // (5) x = padded_scatter(x, indices) * weights            P:279-280 (fused into the DSD for top-1)
+  MOE_TRY(moe_dsd_scatter(cfg, sv->a, w->w2, &sv->topo, sv->gates, sv->y_g, y, stream));
   return MOE_OK;
 }
 

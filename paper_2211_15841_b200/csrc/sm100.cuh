@@ -103,6 +103,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// TMA scatter of 4 rows (tile::scatter4): smem [4 rows][box bytes] -> rows r0..r3
+// of a 2-D tensor whose map has box {inner, 1}; out-of-range rows are dropped.
+__device__ __forceinline__ void tma_scatter4(const CUtensorMap* map, const void* smem_src, int32_t c0, int32_t r0,
+                                             int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::
+                   "l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(smem_src))
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

@@ -48,7 +48,7 @@ moe_status check_topo(const moe_topology_t* t) {
   if (!t) return set_error(MOE_EINVAL, "topology pointer is NULL");
   if (!t->counts || !t->bins || !t->padded_bins || !t->sorted_idx || !t->pos || !t->sorted_pos ||
       !t->row_offsets || !t->col_indices || !t->row_indices || !t->t_col_offsets || !t->t_block_offsets ||
-      !t->t_row_indices || !t->pair_bins || !t->sizes)
+      !t->t_row_indices || !t->pair_bins || !t->row_src || !t->sizes)
     return set_error(MOE_EINVAL, "topology has a NULL array");
   return MOE_OK;
 }

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
       topo.sorted_idx[u] = i;
       topo.sorted_pos[i] = u;
       topo.pos[i] = p;
+      topo.row_src[p] = i;
     }
   } else {
     const int s = (blockIdx.x - n_chunks) * blockDim.x + threadIdx.x;
@@ -182,8 +183,13 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     const int r0 = s_pstart[e] / bs;
     topo.row_indices[s] = r;
     topo.col_indices[s] = e * F + j;
-    if (j == 0) topo.row_offsets[r] = s;
     const int32_t pc = ((s_cnt[e] + bs - 1) / bs) * bs;
+    if (j == 0) {
+      topo.row_offsets[r] = s;
+      // pad rows of this block-row (the tail of expert e's group) hold no assignment
+      const int pad0 = s_pstart[e] + s_cnt[e];
+      for (int q = max(row0, pad0); q < row0 + bs && q < s_pstart[e] + pc; ++q) topo.row_src[q] = -1;
+    }
     const int qpos = F * (s_pstart[e] / bs) + j * (pc / bs) + (r - r0);
     topo.t_block_offsets[qpos] = s;
     topo.t_row_indices[qpos] = r;

@@ -66,6 +66,10 @@ def check_topology_exact(A, topo_gpu, plan, topo, R):
     pairs = np.cumsum((plan.padded_counts // 128 + 1) // 2)
     np.testing.assert_array_equal(g["pair_bins"], pairs)
     assert int(g["sizes"][2]) == int(pairs[-1])
+    # row_src: the inverse of pos over the padded rows, -1 on pad rows
+    src = np.full(Tp, -1, np.int64)
+    src[plan.pos] = np.arange(R)
+    np.testing.assert_array_equal(g["row_src"][:Tp], src)
 
 
 # ------------------------------------------------------------------ routing
@@ -170,7 +174,7 @@ def test_topology_deterministic_repeat():
     Tp, nnz = t1.sizes()
     assert (Tp, nnz) == t2.sizes()
     valid = {"row_offsets": Tp // 128 + 1, "col_indices": nnz, "row_indices": nnz, "t_block_offsets": nnz,
-             "t_row_indices": nnz}   # contents beyond the device-side sizes are unspecified (moe.h)
+             "t_row_indices": nnz, "row_src": Tp}   # contents beyond the device-side sizes are unspecified (moe.h)
     for name in t1.t:
         n = valid.get(name, t1[name].numel())
         assert torch.equal(t1[name][:n], t2[name][:n]), name
@@ -247,6 +251,31 @@ def product_case(T, h, f, E, k, zipf, seed):
 
 
 PRODUCT_CASES = [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2), (2500, 768, 384, 8, 1, 0.5, 3)]
+
+
+@pytest.mark.parametrize("case", PRODUCT_CASES + [(4100, 512, 2048, 64, 1, 0.0, 4)])
+def test_dsd_scatter(case):
+    """DSD fused with the weighted un-permutation (moe_dsd_scatter): Y_g and y
+    against the oracle's DSD and padded_scatter; top-1 takes
+    the tile::scatter4 epilogue, top-2 the DSD + combine path."""
+    d = dev()
+    A = api()
+    T, h, f, E, k, zipf, seed = case
+    idx, plan, topo, x, w1, w2, dyg = product_case(*case)
+    Tp, nnz = plan.Tp, topo.nnz
+    cfg = A.make_config(T, h, E, k, f, act=A.ACT_GELU)
+    tg = A.moe_topology(cfg, idx.to(d))
+    g = torch.Generator().manual_seed(seed + 100)
+    svals = torch.randn(A.moe_max_nnz_blocks(cfg), 128, 128, generator=g).to(torch.bfloat16)
+    gates = torch.rand(T, k, generator=g, dtype=torch.float32)
+    y = torch.full((T, h), float("nan"), dtype=torch.bfloat16)
+    yg, yy = A.moe_dsd_scatter(cfg, svals.to(d), w2.to(d), tg, gates.to(d), y=y.to(d))
+    Y = O.dsd(f64(svals[:nnz]), S.to_f64(w2), topo)
+    assert rel_fro(f64(yg[:Tp]), Y) < FRO_TOL
+    want = O.padded_scatter(f64(yg[:Tp]), plan, gates.double().numpy(), T, k)
+    got = f64(yy)
+    assert np.isfinite(got).all()          # every token row written exactly by its scatter
+    assert rel_fro(got, want) < FRO_TOL
 
 
 @pytest.mark.parametrize("case", PRODUCT_CASES)
