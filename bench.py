@@ -113,6 +113,8 @@ def work_model(T, h, f, E, k, Tp):
         "sddt_bytes": prod_bytes + 2 * R * f,      # + read of the saved pre-activation H
         "sdd_bytes": prod_bytes + 2 * R * f,       # + write of act'(H) (kept for the backward)
         "dsd_scatter_bytes": prod_bytes + 2 * T * h + 4 * R,  # + the gate-weighted rows scattered to y
+        # DSD^T writing dx rows instead of dX_g, + dlogits rows and Wr for the router term
+        "dsdt_dx_bytes": prod_bytes - 2 * R * h + 2 * T * h + 2 * T * E + 2 * h * E + 4 * R,
         "gather_bytes": 2 * (T * h + R * h) + 4 * R,
         "scatter_bytes": 2 * (R * h + T * h) + 8 * R,
         "scatter_bwd_bytes": 2 * (T * h + 2 * R * h) + 4 * R,
@@ -163,14 +165,16 @@ class Step:
             ("sddT", L.moe_sdd_deriv, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act,
                                        None if idn else d(sv.act_deriv), wsl["dh"], None, s)),
             ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
-            ("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
-            ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
         ]
-        if fused:
-            bwd += [("router_dwr", L.moe_router_dwr, (c, d(t["x"]), wsl["dlogits"], d(t["dwr"]), ws, s)),
-                    ("router_dx", L.moe_router_dx, (c, wsl["dlogits"], d(t["wr"]), wsl["dx_g"], topo, d(t["dx"]), s))]
+        if fused:   # layer.cu order: DD^TS, dWr, then DSD^T fused with the gather backward + router dx
+            bwd += [("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
+                    ("router_dwr", L.moe_router_dwr, (c, d(t["x"]), wsl["dlogits"], d(t["dwr"]), ws, s)),
+                    ("dsdT+dx", L.moe_dsd_dx, (c, wsl["dh"], d(t["w1"]), topo, wsl["dlogits"], d(t["wr"]), d(t["dx"]),
+                                               wsl["dx_g"], s))]
         else:
-            bwd += [("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
+            bwd += [("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
+                    ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
+                    ("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
                     ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
                                                       wsl["dgates"], d(t["dwr"]), d(t["dx"]), ws, s))]
         self.calls += bwd
@@ -307,7 +311,7 @@ def run_ours_single(args, peaks):
     dom = int(np.argmax(mean_call))
     dname = step.names[dom]
     prod_names = {"sdd": "sdd_bytes", "dsd+scatter": "dsd_scatter_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
-                  "dsdT": "prod_bytes", "ddTs": "prod_bytes"}
+                  "dsdT": "prod_bytes", "ddTs": "prod_bytes", "dsdT+dx": "dsdt_dx_bytes"}
     byte_names = {"gather": "gather_bytes", "scatter": "scatter_bytes", "scatter_bwd": "scatter_bwd_bytes",
                   "gather_bwd": "gather_bwd_bytes"}
     dur_s = mean_call[dom] / 1e3
@@ -334,7 +338,7 @@ def run_ours_single(args, peaks):
     roof["traffic"] = load_traffic(dname)
     breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4)}
                  for nm, m, s_ in zip(step.names, mean_call, shares)}
-    gemm_ms = sum(mean_call[step.names.index(p)] for p in prod_names)
+    gemm_ms = sum(mean_call[step.names.index(p)] for p in prod_names if p in step.names)
     gemm = {"ms": round(float(gemm_ms), 4),
             "useful_tflops": round(6 * wm["prod_flop"] / (gemm_ms / 1e3) / 1e12, 1),
             "executed_tflops": round(wm["executed_flop_step"] / (gemm_ms / 1e3) / 1e12, 1)}

@@ -253,6 +253,16 @@ moe_status moe_router_dwr(const moe_config* cfg, const void* x, const void* dlog
 moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const void* wr, const void* dx_g,
                          const moe_topology_t* topo, void* dx, void* stream);
 
+/* b4 + b6 + b7 fused: dx [T,h] bf16 = sum_j (dh . w1^T)[pos[t*k+j]] + dlogits . wr^T,
+ * i.e. DSD^T with the padded-gather backward and the router term of
+ * dx. For top-1 one tcgen05 kernel: each DSD^T tile appends E/64 dense K-steps
+ * whose A rows are the tile's tokens' dlogits (TMA tile::gather4 through
+ * topo->row_src) and writes its rows straight to dx[token] (tile::scatter4;
+ * pad rows dropped). For k > 1: moe_dsd into dx_g [max_rows, h] (caller
+ * scratch, required), then moe_router_dx. dlogits bf16 [T,E]; wr [h,E]. */
+moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, const moe_topology_t* topo,
+                      const void* dlogits_bf16, const void* wr, void* dx, void* dx_g, void* stream);
+
 /* ---- the layer: Fig. 5 forward, §5.1 backward ---- */
 typedef struct {
   const void* wr; /* [h, E]   bf16 */

@@ -73,6 +73,7 @@ SIGNATURES = {
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_dsd_scatter": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
+    "moe_dsd_dx": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P]),
     "moe_dds": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),
     "moe_scatter_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),

@@ -126,6 +126,8 @@ __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pa
     const int b = __ldg(p.row_offsets + t.u), e = __ldg(p.row_offsets + t.u + 1);
     t.walk_begin = b;
     t.kiters = KPB * (e - b);
+    t.s = t.kiters;  // sparse K-steps; DSD_ROW appends p.extra_k dense ones
+    if (mode == DSD_ROW) t.kiters += p.extra_k;
   } else if (mode == DS_COL || mode == DDS_COL) {
     t.u = (tile / p.dense_tiles) * (mode == DDS_COL ? pair : 1);
     t.v = tile % p.dense_tiles;
@@ -241,6 +243,7 @@ template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     bsgemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
+                  const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_f,
                   const GemmParams p) {
   using C = Cfg<MODE, BN, EPI_H>;
   constexpr int STAGES = C::STAGES;
@@ -295,18 +298,20 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tile_i = 0;
-    // L2-prefetch mode (MOE_GEMM_DBG & 128, NP == 2): warp 0 issues every stage,
-    // warp 1 prefetches the K-step STAGES ahead of it into L2
-    const bool pf_mode = C::NP == 2 && (p.dbg & 128);
-    const bool prefetcher = pf_mode && warp == 1;
-    long long g = 0;  // global K-step index of this CTA
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
+      int4 gtok = make_int4(0, 0, 0, 0);
+      if (MODE == DSD_ROW && p.extra_k) {  // tokens of the tile's rows 4*lane .. 4*lane+3
+        const int4 src = __ldg(reinterpret_cast<const int4*>(p.row_src + t.u * BM) + lane);
+        const int oob = p.scatter_T;
+        gtok = make_int4(src.x >= 0 ? src.x : oob, src.y >= 0 ? src.y : oob, src.z >= 0 ? src.z : oob,
+                         src.w >= 0 ? src.w : oob);
+      }
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit / KPB, kk = kit % KPB;
-        if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0) {
+        if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0 && kit < t.s) {
           const int q = t.walk_begin + blk + lane;
           if (q < t.walk_begin + (t.kiters / KPB)) {
             if (MODE == DSD_ROW || MODE == DDS_ROW) {
@@ -320,29 +325,26 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
-        if (prefetcher) {
-          const long long h = g - STAGES;  // the stage warp 0 fills while we prefetch step g
-          if (h >= 0) mbar_wait(&empty[h % STAGES], (uint32_t)((h / STAGES) & 1) ^ 1u);
-          if (lane == 0)
-            issue_stage<MODE, A_MN, B_MN, BN, true>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, nullptr, nullptr, nullptr);
-          __syncwarp();
-          ++g;
-          continue;
-        }
-        const bool mine = pf_mode ? true : stage % C::NP == warp;
+        const bool mine = stage % C::NP == warp;
         if (mine) mbar_wait(&empty[stage], phase ^ 1);
-        // lane 0 issues the A box(es), lane 1 the B box(es): each thread keeps
-        // its own TMA requests in flight (MOE_GEMM_DBG & 256 -> lane 0 issues both)
-        const bool split = !(p.dbg & 256);
-        if (mine && (lane == 0 || (split && lane == 1))) {
+        if (mine && MODE == DSD_ROW && kit >= t.s) {
+          // appended dense K-steps (dsdT + router dx): A = dlogits rows of the
+          // tile's tokens, gathered 4 rows per lane (tile::gather4; pad rows are
+          // out of range -> zeros), B = Wr^T
+          const int ke = kit - t.s;
+          if (lane == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE);
+          __syncwarp();
+          tma_gather4(smem_a + stage * A_BYTES + lane * 512, &tmap_e, &full[stage], ke * BK, gtok.x, gtok.y, gtok.z,
+                      gtok.w);
+          if (lane == 0) tma_load_2d(smem_b + stage * C::B_BYTES, &tmap_f, &full[stage], ke * BK, t.v * BN);
+        } else if (mine && lane == 0) {
           uint64_t* fb = &full[stage];
           if (p.dbg & 8) {
-            if (lane == 0) mbar_arrive(fb);
+            mbar_arrive(fb);
           } else {
-            if (lane == 0) mbar_arrive_expect_tx(fb, C::STAGE);
-            const int part = split ? (lane == 0 ? 1 : 2) : 3;
+            mbar_arrive_expect_tx(fb, C::STAGE);
             issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
-                                              smem_b + stage * C::B_BYTES, fb, part);
+                                              smem_b + stage * C::B_BYTES, fb);
           }
         }
         __syncwarp();
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
         const int src = __ldg(p.row_src + t.u * BM + row0 + lane);
         if (src >= 0) {
           my_tok = src;
-          my_gate = __ldg(p.scatter_gates + src);
+          my_gate = p.scatter_gates ? __ldg(p.scatter_gates + src) : 1.f;
         }
       }
       if (MODE == DENSE && p.epi == EPI_ADD_ROWS) {
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               }
             }
           }
-          store_chunk(&tmap_c, v, x, y);
+          if (!(MODE == DSD_ROW && p.scatter_only)) store_chunk(&tmap_c, v, x, y);
           if (MODE == DSD_ROW && p.scatter_y) {
             // the weighted un-permutation of the layer (top-1): the
             // gate-scaled rows go straight to y[token] by tile::scatter4
@@ -828,7 +830,7 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
     }
     if ((rev >> MODE) & 1) p.reverse = 1;
   }
-  cudaError_t le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
+  cudaError_t le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
   if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
@@ -999,8 +1001,13 @@ moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, in
   return sdd_launch(cfg, a, b, trans_b, topo, act, deriv_src, out_s, out_deriv, true, stream);
 }
 
+// DSD launcher. With y: the output rows are also (or, with dl16, only) scattered
+// to y[row_src[p]] by tile::scatter4, scaled by gates (NULL: 1). With dl16 and wr:
+// each tile appends E/BK dense K-steps dl16[token rows] . wr^T (the router term
+// of dx, P:98 chain rule) and writes only y.
 static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
-                             const moe_topology_t* topo, void* out, const float* gates, void* y, void* stream) {
+                             const moe_topology_t* topo, void* out, const float* gates, void* y, void* stream,
+                             const void* dl16 = nullptr, const void* wr = nullptr) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
@@ -1032,6 +1039,13 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
       L.p.row_src = topo->row_src;
       L.p.scatter_gates = gates;
     }
+    if (dl16 && wr) {  // + dlogits . Wr^T on the gathered token rows, only the scatter is written
+      const int64_t E = cfg->num_experts;
+      MOE_TRY(make_tmap_bf16(&L.te, dl16, E, cfg->tokens, E, 64, 1, "moe_dsd_dx dlogits", 128));
+      MOE_TRY(make_tmap_bf16(&L.tf, wr, E, h, E, BK, L.bn, "moe_dsd_dx wr", KSW));
+      L.p.extra_k = (int)(E / BK);
+      L.p.scatter_only = 1;
+    }
   } else {
     L.name = trans_b ? "moe_dsd(S^T,T)" : "moe_dsd(S^T)";
     L.mode = DS_COL;
@@ -1051,6 +1065,18 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream) {
   return dsd_launch(cfg, s, trans_s, b, trans_b, topo, out, nullptr, nullptr, stream);
+}
+
+moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, const moe_topology_t* topo,
+                      const void* dlogits_bf16, const void* wr, void* dx, void* dx_g, void* stream) {
+  MOE_CHECK_ARG(dh && w1 && dlogits_bf16 && wr && dx, "moe_dsd_dx: NULL pointer");
+  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && cfg->num_experts % 64 == 0 && cfg->num_experts <= 256 &&
+      cfg->hidden % 256 == 0 && !use_pair_rows())
+    return dsd_launch(cfg, dh, 0, w1, 1, topo, dx, nullptr, dx, stream, dlogits_bf16, wr);
+  // general k: dX_g = dH . W1^T, then dx = sum_j dX_g[pos] + dlogits . Wr^T
+  MOE_CHECK_ARG(dx_g, "moe_dsd_dx: top_k > 1 needs the dx_g scratch buffer");
+  MOE_TRY(moe_dsd(cfg, dh, 0, w1, 1, topo, dx_g, stream));
+  return moe_router_dx(cfg, dlogits_bf16, wr, dx_g, topo, dx, stream);
 }
 
 moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,

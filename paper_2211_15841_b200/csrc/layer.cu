@@ -60,15 +60,18 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   MOE_TRY(moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream));
   // b3: DS^TD: dW2 = A^T . dY_g                              "second layer weight gradient"
   MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
+  if (fused_router) {
+    // b5: DD^TS: dW1 = X_g^T . dH                            "first layer weight gradient"
+    MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
+    // b7: dWr = x^T . dlogits
+    MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
+    // b4 + b6 + b7: dx = sum_j (dH . W1^T)[pos[t*k+j]] + dlogits . Wr^T   "first layer data gradient"
+    return moe_dsd_dx(cfg, dh, w->w1, topo, dl16, w->wr, dx, dx_g, stream);
+  }
   // b4: DSD^T: dX_g = dH . W1^T                              "first layer data gradient"
   MOE_TRY(moe_dsd(cfg, dh, 0, w->w1, 1, topo, dx_g, stream));
   // b5: DD^TS: dW1 = X_g^T . dH                              "first layer weight gradient"
   MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
-  if (fused_router) {
-    // b7: dWr = x^T . dlogits; b6+b7: dx = sum_j dX_g[pos[t*k+j]] + dlogits . Wr^T
-    MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
-    return moe_router_dx(cfg, dl16, w->wr, dx_g, topo, dx, stream);
-  }
   // b6: dx = sum_j dX_g[pos]
   MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
   // b7: router backward (dWr, dx += dlogits . Wr^T)

@@ -253,6 +253,35 @@ def product_case(T, h, f, E, k, zipf, seed):
 PRODUCT_CASES = [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2), (2500, 768, 384, 8, 1, 0.5, 3)]
 
 
+@pytest.mark.parametrize("case", [(1000, 256, 512, 64, 1, 0.0, 1), (4100, 512, 2048, 64, 1, 0.5, 4),
+                                  (3000, 512, 1024, 128, 2, 1.2, 2), (2000, 768, 384, 64, 1, 0.0, 5)])
+def test_dsd_dx(case):
+    """DSD^T fused with the gather backward and the router term of dx
+    (moe_dsd_dx): dx = sum_j (dH . W1^T)[pos[t*k+j]] + dlogits . Wr^T (P:206
+    b4, b6; P:98 chain rule b7) against the oracle's DSD^T. Top-1 takes the
+    gather4 / scatter4 kernel, top-2 the DSD^T + router-dx path."""
+    d = dev()
+    A = api()
+    T, h, f, E, k, zipf, seed = case
+    idx, plan, topo, x, w1, w2, dyg = product_case(T, h, f, E, k, zipf, seed)
+    Tp, nnz = plan.Tp, topo.nnz
+    cfg = A.make_config(T, h, E, k, f, act=A.ACT_GELU)
+    tg = A.moe_topology(cfg, idx.to(d))
+    g = torch.Generator().manual_seed(seed + 200)
+    dh = torch.randn(A.moe_max_nnz_blocks(cfg), 128, 128, generator=g).to(torch.bfloat16)
+    dl = (torch.randn(T, E, generator=g) * 0.1).to(torch.bfloat16)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16)
+    dx = torch.full((T, h), float("nan"), dtype=torch.bfloat16)
+    got = f64(A.moe_dsd_dx(cfg, dh.to(d), w1.to(d), tg, dl.to(d), wr.to(d), dx=dx.to(d)))
+    dxg = O.dsd(f64(dh[:nnz]), S.to_f64(w1), topo, trans_b=True)
+    want = S.to_f64(dl) @ S.to_f64(wr).T
+    for t in range(T):
+        for j in range(k):
+            want[t] += dxg[plan.pos[t * k + j]]
+    assert np.isfinite(got).all()
+    assert rel_fro(got, want) < FRO_TOL
+
+
 @pytest.mark.parametrize("case", PRODUCT_CASES + [(4100, 512, 2048, 64, 1, 0.0, 4)])
 def test_dsd_scatter(case):
     """DSD fused with the weighted un-permutation (moe_dsd_scatter): Y_g and y
