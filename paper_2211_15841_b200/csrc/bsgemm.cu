@@ -901,7 +901,9 @@ GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo) {
 static int pick_bn(const moe_config* cfg, bool pairs_columns) {
   const int64_t F = cfg->ffn_hidden / cfg->block_size;
   if (pairs_columns) return (F % 2 == 0) ? 256 : 128;
-  return (cfg->hidden % 256 == 0) ? 256 : 128;
+  static int force128 = -1;
+  if (force128 < 0) force128 = getenv("MOE_DSD_BN128") != nullptr;  // experiment: 128-wide DSD tiles
+  return (cfg->hidden % 256 == 0 && !force128) ? 256 : 128;
 }
 
 // Experiment switch MOE_GEMM_PAIR_ROWS: row-pair 2-SM tiles for DSD / DSD^T
