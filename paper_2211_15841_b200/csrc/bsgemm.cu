@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       }
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit / KPB, kk = kit % KPB;
-        if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0 && kit < t.s) {
+        if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0 && (MODE != DSD_ROW || kit < t.s)) {
           const int q = t.walk_begin + blk + lane;
           if (q < t.walk_begin + (t.kiters / KPB)) {
             if (MODE == DSD_ROW || MODE == DDS_ROW) {
