@@ -33,42 +33,6 @@ __global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, 
   for (int e = threadIdx.x; e < E; e += blockDim.x) chunk_counts[(size_t)blockIdx.x * E + e] = s_cnt[e];
 }
 
-// Block-wide exclusive scan helper over `n` ints in shared memory (n <= 4096),
-// single CTA of 1024 threads, sequential per-thread segments + warp scan.
-__device__ void block_exclusive_scan(int32_t* data, int n, int32_t* s_tmp, int32_t* total_out) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (n + nt - 1) / nt;
-  const int b = tid * per, e = min(n, b + per);
-  int32_t local = 0;
-  for (int i = b; i < e; ++i) local += data[i];
-  // warp inclusive scan
-  const int lane = tid & 31, w = tid >> 5;
-  int32_t v = local;
-  for (int o = 1; o < 32; o <<= 1) {
-    int32_t y = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += y;
-  }
-  if (lane == 31) s_tmp[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    int32_t x = lane < (nt >> 5) ? s_tmp[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    s_tmp[lane] = x;  // inclusive per-warp totals
-  }
-  __syncthreads();
-  int32_t run = (w > 0 ? s_tmp[w - 1] : 0) + v - local;  // exclusive start of this thread's segment
-  for (int i = b; i < e; ++i) {
-    int32_t d = data[i];
-    data[i] = run;
-    run += d;
-  }
-  if (total_out && tid == nt - 1) *total_out = run;
-  __syncthreads();
-}
-
 // Scan + emit in one launch. Every CTA first recomputes, from the per-chunk
 // histograms (G x E ints, L2-resident), the per-expert totals, the chunk
 // prefix it needs and the E-long scans (bins, padded_bins, pair_bins) in
@@ -84,34 +48,72 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
   pdl_wait();
   extern __shared__ int32_t s_dyn[];           // [32 warps][E] per-warp counts (ranking CTAs)
   __shared__ int32_t s_cnt[1024], s_start[1024], s_pstart[1024], s_pair[1024], s_base[1024];
-  __shared__ int32_t s_tmp[32];
   __shared__ int32_t s_tot[3];
   const bool ranking = (int)blockIdx.x < n_chunks;
-  // (1) per-expert totals and (ranking CTAs) this chunk's exclusive base
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  const int warp_id = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+  // (1) per-expert totals and (ranking CTAs) this chunk's exclusive base: one
+  //     warp per expert, lanes over chunks (coalesced-enough L2 reads, warp scan)
+  for (int e = warp_id; e < E; e += 32) {
     int32_t run = 0, base = 0;
-    for (int c0 = 0; c0 < n_chunks; c0 += 16) {
-      int32_t v[16];  // batch the loads so they are in flight together
+    for (int c0 = 0; c0 < n_chunks; c0 += 32) {
+      const int c = c0 + lane_id;
+      const int32_t v = c < n_chunks ? __ldg(chunk_counts + (size_t)c * E + e) : 0;
+      int32_t incl = v;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = c0 + u < n_chunks ? __ldg(chunk_counts + (size_t)(c0 + u) * E + e) : 0;
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        if (c0 + u == (int)blockIdx.x) base = run;
-        run += v[u];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane_id >= o) incl += y;
       }
+      if (c == (int)blockIdx.x) base = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_base[e] = base;
-    s_cnt[e] = run;
-    const int32_t pc = ((run + bs - 1) / bs) * bs;
-    s_start[e] = run;
-    s_pstart[e] = pc;
-    s_pair[e] = (pc / bs + 1) / 2;  // same-expert block-row pairs
+    base = __reduce_max_sync(0xffffffffu, (unsigned)base);  // the one lane holding it (others 0)
+    if (lane_id == 0) {
+      s_base[e] = base;
+      s_cnt[e] = run;
+    }
   }
   __syncthreads();
-  // (2) exclusive scans over experts: unpadded and padded group starts
-  block_exclusive_scan(s_start, E, s_tmp, &s_tot[0]);
-  block_exclusive_scan(s_pstart, E, s_tmp, &s_tot[1]);
-  block_exclusive_scan(s_pair, E, s_tmp, &s_tot[2]);
+  // (2) exclusive scans over experts (unpadded, padded group starts P:297, row
+  //     pairs) by warp 0: lane l owns experts [l*per, (l+1)*per)
+  if (warp_id == 0) {
+    const int per = (E + 31) / 32;
+    const int e0 = min(E, lane_id * per), e1 = min(E, e0 + per);
+    int32_t a0 = 0, a1 = 0, a2 = 0;
+    for (int e = e0; e < e1; ++e) {
+      const int32_t c = s_cnt[e], pc = ((c + bs - 1) / bs) * bs;
+      a0 += c;
+      a1 += pc;
+      a2 += (pc / bs + 1) / 2;
+    }
+    int32_t i0 = a0, i1 = a1, i2 = a2;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o),
+                    y2 = __shfl_up_sync(0xffffffffu, i2, o);
+      if (lane_id >= o) {
+        i0 += y0;
+        i1 += y1;
+        i2 += y2;
+      }
+    }
+    int32_t r0 = i0 - a0, r1 = i1 - a1, r2 = i2 - a2;
+    for (int e = e0; e < e1; ++e) {
+      const int32_t c = s_cnt[e], pc = ((c + bs - 1) / bs) * bs;
+      s_start[e] = r0;
+      s_pstart[e] = r1;
+      s_pair[e] = r2;
+      r0 += c;
+      r1 += pc;
+      r2 += (pc / bs + 1) / 2;
+    }
+    if (lane_id == 31) {
+      s_tot[0] = i0;
+      s_tot[1] = i1;
+      s_tot[2] = i2;
+    }
+  }
+  __syncthreads();
   const int Tp = s_tot[1];
   const int nnz = (Tp / bs) * F;
   if (blockIdx.x == 0) {
