@@ -414,6 +414,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     uint32_t acc_phase = 0;
     const bool bf16_out = p.epi == EPI_STORE || p.epi == EPI_ACT_FWD || p.epi == EPI_ACT_BWD || p.epi == EPI_ADD_ROWS;
 
+    // L2 priority of the two epilogue outputs (GemmParams::l2_c / l2_d)
+    const uint64_t pol_c = l2_policy(p.l2_c), pol_d = l2_policy(p.l2_d);
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
       if (lane == 0) bulk_wait_read<C::NBUF - 1>();  // the store issued from this buffer NBUF stores ago has read it
       __syncwarp();
@@ -421,7 +423,11 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
+        const int kind = map == &tmap_c ? p.l2_c : p.l2_d;
+        if (kind)
+          tma_store_2d_hint(map, stg + sbuf * EPI_BUF, x, y, map == &tmap_c ? pol_c : pol_d);
+        else
+          tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
         bulk_commit();
       }
       sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
@@ -977,6 +983,23 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   L.p.epi = act_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_aux) ? EPI_ACT_FWD : EPI_STORE);
   L.p.has_pre = out_aux != nullptr;
   L.p.aux_deriv = deriv ? 1 : 0;
+  {
+    // L2 priorities of the SDD outputs: act(H) (read next by the DSD) kept,
+    // act'(H) (read only in the backward) streamed; SDD^T: dH kept.
+    static int mode = -1;
+    if (mode < 0) {
+      const char* e = getenv("MOE_L2_HINTS");
+      mode = e ? atoi(e) : 0;  // measured neutral at MoE-XS: opt-in
+    }
+    if (mode) {
+      if (act_src) {
+        L.p.l2_c = 1;
+      } else {
+        L.p.l2_c = 1;
+        L.p.l2_d = 2;
+      }
+    }
+  }
   L.epi_h = L.p.epi == EPI_ACT_BWD;
   L.max_tiles = (int)(nnz / (L.bn / 128));
   MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, BK, 128, "moe_sdd a", KSW));

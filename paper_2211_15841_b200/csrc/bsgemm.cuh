@@ -33,6 +33,7 @@ struct GemmParams {
   // epilogue
   int epi, act, has_pre;
   int aux_deriv;
+  int l2_c, l2_d;  // L2 priority of the tmap_c / tmap_d epilogue stores: 0 normal, 1 evict_last, 2 evict_first
   // DSD_ROW + scatter_y (top-1 only): y[t] = gate[t] * row p of the output, t = row_src[p]
   // (tile::scatter4 through tmap_d; pad rows dropped)
   int scatter_y, scatter_T, scatter_only;
