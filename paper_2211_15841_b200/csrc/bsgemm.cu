@@ -1001,17 +1001,20 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
     }
   }
   L.epi_h = L.p.epi == EPI_ACT_BWD;
-  L.max_tiles = (int)(nnz / (L.bn / 128));
+  static int pair_env = -1;  // experiment: row-pair 2-SM tiles for SDD / SDD^T (MOE_SDD_PAIR=1)
+  if (pair_env < 0) pair_env = getenv("MOE_SDD_PAIR") != nullptr;
+  const bool pair = pair_env && use_pair(cfg);
+  L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
   MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, BK, 128, "moe_sdd a", KSW));
   if (!trans_b)
-    MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, L.bn / 64, "moe_sdd b"));
+    MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, pair ? 2 : L.bn / 64, "moe_sdd b"));
   else
-    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, L.bn, "moe_sdd b^T", KSW));
+    MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, pair ? 128 : L.bn, "moe_sdd b^T", KSW));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   if (out_aux) MOE_TRY(make_tmap_epi(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
   if (act_src) MOE_TRY(make_tmap_epi(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_aux && !act_src) L.td = L.tc;
-  return gemm_launch(L, as_stream(stream));
+  return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
 }
 
 moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b, const moe_topology_t* topo,
