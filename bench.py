@@ -147,9 +147,16 @@ class Step:
         self.calls = [
             ("router", L.moe_router, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), d(sv.gates), ws, s)),
             ("topology", L.moe_topology, (c, d(sv.expert_idx), topo, ws, s)),
-            ("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
-            ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
-                                      None if idn else d(sv.act_deriv), s)),
+        ]
+        gfused = bool(L.moe_gather_is_fused(c))   # layer.cu: the padded gather inside the SDD / DD^TS loads
+        if gfused:
+            self.calls += [("sdd+gather", L.moe_sdd_gather, (c, d(t["x"]), d(t["w1"]), topo, cfg.act, d(sv.a),
+                                                            None if idn else d(sv.act_deriv), d(sv.x_g), s))]
+        else:
+            self.calls += [("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
+                           ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
+                                                     None if idn else d(sv.act_deriv), s))]
+        self.calls += [
             ("dsd+scatter", L.moe_dsd_scatter, (c, d(sv.a), d(t["w2"]), topo, d(sv.gates), d(sv.y_g),
                                                  d(t["y"]), s)),
         ]
@@ -166,14 +173,16 @@ class Step:
                                        None if idn else d(sv.act_deriv), wsl["dh"], None, s)),
             ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
         ]
+        ddts = (("ddTs+gather", L.moe_dds_gather, (c, d(t["x"]), wsl["dh"], topo, d(t["dw1"]), d(sv.x_g), s)) if gfused
+                else ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)))
         if fused:   # layer.cu order: DD^TS, dWr, then DSD^T fused with the gather backward + router dx
-            bwd += [("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
+            bwd += [ddts,
                     ("router_dwr", L.moe_router_dwr, (c, d(t["x"]), wsl["dlogits"], d(t["dwr"]), ws, s)),
                     ("dsdT+dx", L.moe_dsd_dx, (c, wsl["dh"], d(t["w1"]), topo, wsl["dlogits"], d(t["wr"]), d(t["dx"]),
                                                wsl["dx_g"], s))]
         else:
             bwd += [("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
-                    ("ddTs", L.moe_dds, (c, d(sv.x_g), 1, wsl["dh"], 0, topo, d(t["dw1"]), s)),
+                    ddts,
                     ("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
                     ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
                                                       wsl["dgates"], d(t["dwr"]), d(t["dx"]), ws, s))]
@@ -310,7 +319,8 @@ def run_ours_single(args, peaks):
     shares = mean_call / mean_call.sum()
     dom = int(np.argmax(mean_call))
     dname = step.names[dom]
-    prod_names = {"sdd": "sdd_bytes", "dsd+scatter": "dsd_scatter_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
+    prod_names = {"sdd": "sdd_bytes", "sdd+gather": "sdd_bytes", "ddTs+gather": "prod_bytes",
+                  "dsd+scatter": "dsd_scatter_bytes", "sddT": "sddt_bytes", "dsTd": "prod_bytes",
                   "dsdT": "prod_bytes", "ddTs": "prod_bytes", "dsdT+dx": "dsdt_dx_bytes"}
     byte_names = {"gather": "gather_bytes", "scatter": "scatter_bytes", "scatter_bwd": "scatter_bwd_bytes",
                   "gather_bwd": "gather_bwd_bytes"}

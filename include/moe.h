@@ -215,6 +215,25 @@ moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, in
                          void* out_deriv, void* stream);
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream);
+/* The padded gather fused into the products that read X_g: the A rows
+ * are fetched from x [T, h] by token (topo->row_src / k) with TMA
+ * tile::gather4, pad rows read as zeros, so X_g is never materialised.
+ * moe_sdd_gather: out_s = act(X_g . w1), out_deriv (optional) = act'(X_g . w1)
+ *   (forward SDD, as moe_sdd_deriv with trans_b = 0).
+ * moe_dds_gather: dw1 [h, E*f] = X_g^T . dh (DD^TS).
+ * Both need even f/bs and h % 256 == 0 (CTA-pair column tiles); otherwise they
+ * run moe_gather into x_g [max_rows, h] (caller scratch, then required) and the
+ * unfused product. */
+moe_status moe_sdd_gather(const moe_config* cfg, const void* x, const void* w1, const moe_topology_t* topo,
+                          int32_t act, void* out_s, void* out_deriv, void* x_g, void* stream);
+/* 1 if moe_forward / moe_backward use the gather-fused products for this config
+ * (off unless MOE_GATHER_FUSED=1: the gather4 requests are issue-rate bound at
+ * one 128 B row each, slower than a separate coalesced gather at MoE-XS). The
+ * two entry points above always gather inside the product when the config allows. */
+int moe_gather_is_fused(const moe_config* cfg);
+moe_status moe_dds_gather(const moe_config* cfg, const void* x, const void* dh, const moe_topology_t* topo, void* dw1,
+                          void* x_g, void* stream);
+
 /* moe_dsd_scatter: the layer's DSD fused with the weighted
  * un-permutation: y_g [max_rows, h] = S . b (b = W2 [E*f, h]) and
  * y [T, h] with y[t] = sum_j gates[t,j] * y_g[pos[t*k+j]]. For top-1 the
@@ -282,7 +301,8 @@ typedef struct {
   int32_t* expert_idx;/* [T, k] */
   float* gates;       /* [T, k] fp32 */
   moe_topology_t topo;
-  void* x_g;          /* [max_rows, h] bf16 */
+  void* x_g;          /* [max_rows, h] bf16 padded gather of x; written only when the config
+                         cannot gather inside the products (moe_sdd_gather) */
   void* act_deriv;    /* [max_nnz, bs, bs] bf16 act'(pre-activation); unused (NULL) for identity */
   void* a;            /* [max_nnz, bs, bs] bf16 activation */
   void* y_g;          /* [max_rows, h] bf16 */

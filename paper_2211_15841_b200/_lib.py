@@ -73,6 +73,9 @@ SIGNATURES = {
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_dsd_scatter": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
+    "moe_sdd_gather": (STATUS, [CFG, P, P, TOPO, ctypes.c_int32, P, P, P, P]),
+    "moe_dds_gather": (STATUS, [CFG, P, P, TOPO, P, P, P]),
+    "moe_gather_is_fused": (ctypes.c_int, [CFG]),
     "moe_dsd_dx": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P]),
     "moe_dds": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),

@@ -196,6 +196,32 @@ def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
     return out
 
 
+def moe_gather_is_fused(cfg) -> bool:
+    return bool(lib.moe_gather_is_fused(ctypes.byref(cfg)))
+
+
+def moe_sdd_gather(cfg, x, w1, topo: Topology, act=ACT_IDENTITY, want_deriv=False, out=None, x_g=None):
+    """moe_sdd_gather (include/moe.h): act(X_g . W1) [and act'] with X_g gathered from x inside the product."""
+    out = out if out is not None else _nnz_values(cfg, x.device)
+    der = _nnz_values(cfg, x.device) if want_deriv else None
+    if x_g is None:   # scratch for configs the kernels cannot gather in
+        x_g = torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=torch.bfloat16, device=x.device)
+    check("moe_sdd_gather", lib.moe_sdd_gather(ctypes.byref(cfg), _p(x), _p(w1), ctypes.byref(topo.struct), int(act),
+                                               _p(out), _p(der), _p(x_g), _stream()))
+    return (out, der) if want_deriv else out
+
+
+def moe_dds_gather(cfg, x, dh, topo: Topology, dw1=None, x_g=None):
+    """moe_dds_gather (include/moe.h): dW1 = X_g^T . dH with X_g gathered from x inside the product."""
+    dw1 = dw1 if dw1 is not None else torch.empty(cfg.hidden, cfg.num_experts * cfg.ffn_hidden, dtype=torch.bfloat16,
+                                                  device=x.device)
+    if x_g is None:
+        x_g = torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=torch.bfloat16, device=x.device)
+    check("moe_dds_gather", lib.moe_dds_gather(ctypes.byref(cfg), _p(x), _p(dh), ctypes.byref(topo.struct), _p(dw1),
+                                               _p(x_g), _stream()))
+    return dw1
+
+
 def moe_dsd_scatter(cfg, s, w2, topo: Topology, gates, y_g=None, y=None):
     """moe_dsd_scatter (include/moe.h): Y_g = S . W2 and y = weighted un-permutation of Y_g."""
     rows = moe_max_padded_rows(cfg)

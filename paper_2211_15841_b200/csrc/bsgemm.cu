@@ -73,6 +73,7 @@ template <int MODE, int BN, bool EPI_H>
 struct Cfg {
   static constexpr int EPW = epi_warps(MODE, BN, EPI_H);
   static constexpr int NP = MOE_GEMM_NP;           // TMA producer warps (stage s is issued by warp s % NP)
+  static_assert(NP >= 1, "at least one producer warp");
   static constexpr int MMA_WARP = NP;
   static constexpr int EPI_WARP0 = NP + 1;
   static constexpr int THREADS = 32 * (NP + 1 + EPW);
@@ -81,7 +82,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
-  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 : 0;  // router epilogue exchange
+  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4
+                             : (MODE == SDD ? NP * 2 * 32 * 16 : 0);  // router exchange / SDD gather tokens
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
@@ -298,10 +300,33 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tile_i = 0;
+    // SDD with gathered A (p.gather_a): the 128 token ids of a tile's rows come
+    // from row_src (4 per lane) through a cp.async double buffer, one tile ahead
+    int4* tokring = reinterpret_cast<int4*>(smem_x) + warp * 64;
+    auto tok_fetch = [&](int tl) {  // async copy of tile tl's row_src entries (4 per lane)
+      if (tl < ntiles) {
+        const int s0 = (p.reverse ? ntiles - 1 - tl : tl) * PAIR;
+        const int32_t* src = p.row_src + (size_t)(s0 / p.F) * BM + 4 * lane;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(tokring + ((tl / gridDim.x) & 1) * 32 + lane)),
+                     "l"(src)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (MODE == SDD && p.gather_a) tok_fetch(blockIdx.x);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
+      int4 atok = make_int4(0, 0, 0, 0);
+      if (MODE == SDD && p.gather_a) {
+        tok_fetch(tile + gridDim.x);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        const int4 r = tokring[(tile_i & 1) * 32 + lane];
+        const int oob = p.gather_T, kq = p.gather_k;
+        atok = make_int4(r.x >= 0 ? r.x / kq : oob, r.y >= 0 ? r.y / kq : oob, r.z >= 0 ? r.z / kq : oob,
+                         r.w >= 0 ? r.w / kq : oob);
+      }
       int4 gtok = make_int4(0, 0, 0, 0);
       if (MODE == DSD_ROW && p.extra_k) {  // tokens of the tile's rows 4*lane .. 4*lane+3
         const int4 src = __ldg(reinterpret_cast<const int4*>(p.row_src + t.u * BM) + lane);
@@ -337,6 +362,15 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           tma_gather4(smem_a + stage * A_BYTES + lane * 512, &tmap_e, &full[stage], ke * BK, gtok.x, gtok.y, gtok.z,
                       gtok.w);
           if (lane == 0) tma_load_2d(smem_b + stage * C::B_BYTES, &tmap_f, &full[stage], ke * BK, t.v * BN);
+        } else if (mine && MODE == SDD && p.gather_a) {
+          // A rows gathered from x by token (tile::gather4, 4 rows per lane; pad rows -> zeros)
+          if (lane == 0) mbar_arrive_expect_tx(&full[stage], C::STAGE);
+          __syncwarp();
+          tma_gather4(smem_a + stage * A_BYTES + lane * 4 * KSW, &tmap_a, &full[stage], kit * BK, atok.x, atok.y,
+                      atok.z, atok.w);
+          if (lane == 0)
+            issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+                                              smem_b + stage * C::B_BYTES, &full[stage], 2);
         } else if (mine && lane == 0) {
           uint64_t* fb = &full[stage];
           if (p.dbg & 8) {
@@ -962,7 +996,7 @@ int moe_debug_trace_dump(const char* path) {
 
 static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b, int trans_b,
                              const moe_topology_t* topo, int32_t act, const void* act_src, void* out_s, void* out_aux,
-                             bool deriv, void* stream) {
+                             bool deriv, void* stream, const void* x_gather = nullptr) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(a && b && out_s, "moe_sdd: NULL operand");
@@ -1005,7 +1039,15 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   if (pair_env < 0) pair_env = getenv("MOE_SDD_PAIR") != nullptr;
   const bool pair = pair_env && use_pair(cfg);
   L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
-  MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, BK, 128, "moe_sdd a", KSW));
+  if (x_gather) {  // A rows = x[row_src / k] by tile::gather4 (X_g never materialised)
+    MOE_TRY(make_tmap_bf16(&L.ta, x_gather, h, cfg->tokens, h, BK, 1, "moe_sdd_gather x", KSW));
+    L.p.gather_a = 1;
+    L.p.gather_k = (int)cfg->top_k;
+    L.p.gather_T = (int)cfg->tokens;
+    L.p.row_src = topo->row_src;
+  } else {
+    MOE_TRY(make_tmap_bf16(&L.ta, a, h, rows, h, BK, 128, "moe_sdd a", KSW));
+  }
   if (!trans_b)
     MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, pair ? 2 : L.bn / 64, "moe_sdd b"));
   else
@@ -1020,6 +1062,32 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
 moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int trans_b, const moe_topology_t* topo,
                    int32_t act, const void* act_grad_src, void* out_s, void* out_pre, void* stream) {
   return sdd_launch(cfg, a, b, trans_b, topo, act, act_grad_src, out_s, out_pre, false, stream);
+}
+
+// The fused-gather products need the CTA-pair column kernels (even F, h % 256 == 0) and 64-wide K-steps.
+static bool gather_fusable(const moe_config* cfg) { return use_pair(cfg) && BK == 64 && cfg->block_size == 128; }
+
+// Whether the layer (moe_forward / moe_backward) gathers inside the products.
+// Off by default: the 32 tile::gather4 requests per stage (one 128 B row each
+// per 4-row op) are issue-rate bound — measured SDD 160 vs 100 + 14 us and
+// DD^TS 269 vs 74 us at MoE-XS; MOE_GATHER_FUSED=1 enables it.
+int moe_gather_is_fused(const moe_config* cfg) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MOE_GATHER_FUSED");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on && cfg && gather_fusable(cfg) ? 1 : 0;
+}
+
+moe_status moe_sdd_gather(const moe_config* cfg, const void* x, const void* w1, const moe_topology_t* topo,
+                          int32_t act, void* out_s, void* out_deriv, void* x_g, void* stream) {
+  MOE_CHECK_ARG(x && w1 && out_s, "moe_sdd_gather: NULL pointer");
+  if (cfg && gather_fusable(cfg))
+    return sdd_launch(cfg, x, w1, 0, topo, act, nullptr, out_s, out_deriv, true, stream, x);
+  MOE_CHECK_ARG(x_g, "moe_sdd_gather: this config needs the x_g scratch (padded gather + SDD)");
+  MOE_TRY(moe_gather(cfg, x, topo, x_g, stream));
+  return sdd_launch(cfg, x_g, w1, 0, topo, act, nullptr, out_s, out_deriv, true, stream);
 }
 
 moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, int trans_b,
@@ -1116,8 +1184,25 @@ moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, 
   return moe_scatter(cfg, y_g, topo, gates, y, stream);
 }
 
+static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
+                             const moe_topology_t* topo, void* out, void* stream, const void* x_gather);
+
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
                    const moe_topology_t* topo, void* out, void* stream) {
+  return dds_launch(cfg, a, trans_a, s, trans_s, topo, out, stream, nullptr);
+}
+
+moe_status moe_dds_gather(const moe_config* cfg, const void* x, const void* dh, const moe_topology_t* topo, void* dw1,
+                          void* x_g, void* stream) {
+  MOE_CHECK_ARG(x && dh && dw1, "moe_dds_gather: NULL pointer");
+  if (cfg && gather_fusable(cfg)) return dds_launch(cfg, x, 1, dh, 0, topo, dw1, stream, x);
+  MOE_CHECK_ARG(x_g, "moe_dds_gather: this config needs the x_g scratch (padded gather + DD^TS)");
+  MOE_TRY(moe_gather(cfg, x, topo, x_g, stream));
+  return moe_dds(cfg, x_g, 1, dh, 0, topo, dw1, stream);
+}
+
+static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
+                             const moe_topology_t* topo, void* out, void* stream, const void* x_gather) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(a && s && out, "moe_dds: NULL operand");
@@ -1136,7 +1221,13 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
     L.p.dense_tiles = (int)(h / (pair ? 2 * BM : BM));
     L.max_tiles = L.p.n_block_cols / (L.bn / 128) * L.p.dense_tiles;
     MOE_TRY(make_tmap_bf16_mn(&L.tb, s, 128, nnz * 128, 128, 2, "moe_dds s"));
-    if (trans_a)
+    if (x_gather) {  // A = X_g^T with the K-rows gathered from x (pair kernel only, see gather_fusable)
+      MOE_TRY(make_tmap_bf16(&L.ta, x_gather, h, cfg->tokens, h, 64, 1, "moe_dds_gather x", 128));
+      L.p.gather_a = 1;
+      L.p.gather_k = (int)cfg->top_k;
+      L.p.gather_T = (int)cfg->tokens;
+      L.p.row_src = topo->row_src;
+    } else if (trans_a)
       MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, rows, h, 2, "moe_dds a^T"));
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, BK, 128, "moe_dds a", KSW));

@@ -37,7 +37,8 @@ struct GemmParams {
   // DSD_ROW + scatter_y (top-1 only): y[t] = gate[t] * row p of the output, t = row_src[p]
   // (tile::scatter4 through tmap_d; pad rows dropped)
   int scatter_y, scatter_T, scatter_only;
-  int extra_k;  // DSD_ROW: dense K-steps appended per tile (A: tmap_e gathered by row_src, B: tmap_f)
+  int extra_k;
+  int gather_a, gather_k, gather_T;  // SDD / DDS_COL: A rows gathered from x [T, h] by row_src / k (OOB: zeros)  // DSD_ROW: dense K-steps appended per tile (A: tmap_e gathered by row_src, B: tmap_f)
   const int32_t* row_src;
   const float* scatter_gates;  // EPI_ACT_FWD: the aux output is act'(H), not H; EPI_ACT_BWD: the source holds act'(H)
   int rows_valid;  // rows of the output that exist (DENSE: M)

@@ -45,10 +45,11 @@ constexpr int P_STAGE = P_A_BYTES + P_B_BYTES;
 template <bool EPI_H>
 struct Cfg2 {
   static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES) / P_STAGE;
+  static constexpr int TOK = 4 * 16 * 16;  // DDS_COL gather: token ring, 4 K-steps x 16 lanes x int4
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES - TOK) / P_STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * P_BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + EPI_BYTES + H_BYTES;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + EPI_BYTES + H_BYTES + TOK;
 };
 
 struct Tile2 {
@@ -146,7 +147,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem_b = smem_a + STAGES * P_A_BYTES;
   uint8_t* smem_epi = smem_b + STAGES * P_B_BYTES;
   uint8_t* smem_h = smem_epi + EPI_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES);
+  int4* tokring = reinterpret_cast<int4*>(smem_h + C::H_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES + C::TOK);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -187,6 +189,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tile_i = 0;
+    // DDS_COL with gathered A (p.gather_a): the K-rows of a column tile are the
+    // contiguous padded rows of its expert; their token ids (row_src / k) are
+    // copied by cp.async into a 4-slot ring TD = 3 K-steps ahead of use.
+    constexpr int TD = 3;
+    const bool gat = MODE == DDS_COL && p.gather_a;
+    int la_j = 0, la_kit = 0, la_kiters = 0, la_pstart = 0;  // look-ahead cursor over (tile, K-step)
+    long long la_g = 0;                                     // global K-step index of the cursor
+    auto la_decode = [&]() {  // settle the cursor on a tile with K-steps (or past the end)
+      while (true) {
+        const int tl = cid + la_j * ncl;
+        if (tl >= ntiles) {
+          la_kiters = -1;
+          return;
+        }
+        const int c0 = (tl / p.dense_tiles) * 2;
+        const int e = c0 / p.F;
+        const int pend = __ldg(p.padded_bins + e);
+        la_pstart = e > 0 ? __ldg(p.padded_bins + e - 1) : 0;
+        la_kiters = (pend - la_pstart) / (BM / KPB);
+        if (la_kiters > 0) return;
+        ++la_j;
+      }
+    };
+    auto la_issue = [&]() {  // copy the cursor's 64 row ids (16 lanes x 4), then advance
+      if (la_kiters > 0 && lane < 16) {
+        const int32_t* src = p.row_src + la_pstart + la_kit * (BM / KPB) + 4 * lane;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(tokring + (la_g & 3) * 16 + lane)),
+                     "l"(src)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (la_kiters > 0) {
+        ++la_g;
+        if (++la_kit == la_kiters) {
+          la_kit = 0;
+          ++la_j;
+          la_decode();
+        }
+      }
+    };
+    long long g_step = 0;
+    if (gat) {
+      la_decode();
+      for (int i = 0; i < TD; ++i) la_issue();
+    }
     for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
       const Tile2 t = decode2(p, MODE, tile, rank);
       if (lane == 0) trace_ev(p, tile_i, 0);
@@ -207,8 +254,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
+        int4 atok = make_int4(0, 0, 0, 0);
+        if (gat) {
+          la_issue();  // K-step g_step + TD
+          asm volatile("cp.async.wait_group %0;" ::"n"(TD) : "memory");
+          __syncwarp();
+          const int4 r = tokring[(g_step & 3) * 16 + (lane & 15)];
+          const int oob = p.gather_T, kq = p.gather_k;
+          atok = make_int4(r.x >= 0 ? r.x / kq : oob, r.y >= 0 ? r.y / kq : oob, r.z >= 0 ? r.z / kq : oob,
+                           r.w >= 0 ? r.w / kq : oob);
+          ++g_step;
+        }
         mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
+        if (gat) {
+          // A = X_g^T: 64 gathered K-rows x this CTA's 128 h-columns (two 64-wide
+          // MN chunks); lane l: chunk l / 16, rows 4 (l % 16) .. +3
+          uint8_t* sa = smem_a + stage * P_A_BYTES;
+          uint64_t* fb = &full[stage];
+          if (leader && lane == 0) mbar_arrive_expect_tx(fb, 2 * P_STAGE);
+          __syncwarp();
+          const int m0 = (2 * t.v + rank) * BM;
+          tma_gather4_pair(sa + (lane >> 4) * (BK * 128) + (lane & 15) * 512, &tmap_a, fb, m0 + (lane >> 4) * 64,
+                           atok.x, atok.y, atok.z, atok.w);
+          if (lane == 0) tma_load_3d_pair(smem_b + stage * P_B_BYTES, &tmap_b, fb, 0, sblk * BM + kk * BK, 0);
+        } else if (lane == 0) {
           uint8_t* sa = smem_a + stage * P_A_BYTES;
           uint8_t* sb = smem_b + stage * P_B_BYTES;
           uint64_t* fb = &full[stage];

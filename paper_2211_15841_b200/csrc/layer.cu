@@ -24,10 +24,14 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   // (2) topology = make_topology(indices)
   MOE_TRY(moe_topology(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
-  MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
-  MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
-                        stream));
+  if (moe_gather_is_fused(cfg)) {  // the gather happens inside the SDD's loads (tile::gather4)
+    MOE_TRY(moe_sdd_gather(cfg, x, w->w1, &sv->topo, cfg->act, sv->a, id ? nullptr : sv->act_deriv, sv->x_g, stream));
+  } else {
+    MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
+    MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
+                          stream));
+  }
   // (5) x = padded_scatter(x, indices) * weights            P:279-280 (fused into the DSD for top-1)
   MOE_TRY(moe_dsd_scatter(cfg, sv->a, w->w2, &sv->topo, sv->gates, sv->y_g, y, stream));
   return MOE_OK;
@@ -62,7 +66,10 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
   if (fused_router) {
     // b5: DD^TS: dW1 = X_g^T . dH                            "first layer weight gradient"
-    MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
+    if (moe_gather_is_fused(cfg))
+      MOE_TRY(moe_dds_gather(cfg, x, dh, topo, g->dw1, sv->x_g, stream));
+    else
+      MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
     // b7: dWr = x^T . dlogits
     MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
     // b4 + b6 + b7: dx = sum_j (dH . W1^T)[pos[t*k+j]] + dlogits . Wr^T   "first layer data gradient"
@@ -71,7 +78,10 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   // b4: DSD^T: dX_g = dH . W1^T                              "first layer data gradient"
   MOE_TRY(moe_dsd(cfg, dh, 0, w->w1, 1, topo, dx_g, stream));
   // b5: DD^TS: dW1 = X_g^T . dH                              "first layer weight gradient"
-  MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
+  if (moe_gather_is_fused(cfg))
+    MOE_TRY(moe_dds_gather(cfg, x, dh, topo, g->dw1, sv->x_g, stream));
+  else
+    MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
   // b6: dx = sum_j dX_g[pos]
   MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
   // b7: router backward (dWr, dx += dlogits . Wr^T)

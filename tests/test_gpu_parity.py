@@ -253,6 +253,35 @@ def product_case(T, h, f, E, k, zipf, seed):
 PRODUCT_CASES = [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2), (2500, 768, 384, 8, 1, 0.5, 3)]
 
 
+@pytest.mark.parametrize("case", [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2),
+                                  (2500, 768, 384, 8, 1, 0.5, 3), (4100, 512, 2048, 64, 1, 0.0, 4)])
+def test_gather_fused_products(case):
+    """SDD and DD^TS with the padded gather inside the product (moe_sdd_gather /
+    moe_dds_gather: TMA tile::gather4 of x rows by row_src, P:297) against the
+    oracle on the explicitly gathered X_g; the odd-F case takes the unfused path."""
+    d = dev()
+    A = api()
+    T, h, f, E, k, zipf, seed = case
+    idx, plan, topo, x, w1, w2, dyg = product_case(*case)
+    Tp, nnz = plan.Tp, topo.nnz
+    cfg = A.make_config(T, h, E, k, f, act=A.ACT_GELU)
+    tg = A.moe_topology(cfg, idx.to(d))
+    xg64 = O.padded_gather(S.to_f64(x), plan, k)
+    a_s, g_s = A.moe_sdd_gather(cfg, x.to(d), w1.to(d), tg, act=A.ACT_GELU, want_deriv=True)
+    H = O.sdd(xg64, S.to_f64(w1), topo)
+    assert rel_fro(f64(a_s[:nnz]), O.act(O.ACT_GELU, H)) < FRO_TOL
+    assert rel_fro(f64(g_s[:nnz]), O.act_grad(O.ACT_GELU, H)) < FRO_TOL
+    g = torch.Generator().manual_seed(seed + 300)
+    dh = torch.randn(A.moe_max_nnz_blocks(cfg), 128, 128, generator=g).to(torch.bfloat16)
+    dw1 = A.moe_dds_gather(cfg, x.to(d), dh.to(d), tg)
+    want = O.dds(xg64, f64(dh[:nnz]), topo, trans_a=True)
+    assert rel_fro(f64(dw1), want) < FRO_TOL
+    if E * f // 128 > 0:   # columns of experts without tokens are exact zeros
+        empty = np.where(plan.counts == 0)[0]
+        for e in empty:
+            assert not f64(dw1[:, e * f:(e + 1) * f]).any()
+
+
 @pytest.mark.parametrize("case", [(1000, 256, 512, 64, 1, 0.0, 1), (4100, 512, 2048, 64, 1, 0.5, 4),
                                   (3000, 512, 1024, 128, 2, 1.2, 2), (2000, 768, 384, 64, 1, 0.0, 5)])
 def test_dsd_dx(case):
