@@ -82,8 +82,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
-  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4
-                             : (MODE == SDD ? NP * 2 * 32 * 16 : 0);  // router exchange / SDD gather tokens
+  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 : 0;  // router epilogue exchange
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
@@ -301,28 +300,23 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     uint32_t phase = 0;
     int tile_i = 0;
     // SDD with gathered A (p.gather_a): the 128 token ids of a tile's rows come
-    // from row_src (4 per lane) through a cp.async double buffer, one tile ahead
-    int4* tokring = reinterpret_cast<int4*>(smem_x) + warp * 64;
-    auto tok_fetch = [&](int tl) {  // async copy of tile tl's row_src entries (4 per lane)
-      if (tl < ntiles) {
-        const int s0 = (p.reverse ? ntiles - 1 - tl : tl) * PAIR;
-        const int32_t* src = p.row_src + (size_t)(s0 / p.F) * BM + 4 * lane;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(tokring + ((tl / gridDim.x) & 1) * 32 + lane)),
-                     "l"(src)
-                     : "memory");
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+    // from row_src (4 per lane), loaded one tile ahead into registers (the load
+    // is only waited for at the next tile)
+    auto tok_load = [&](int tl) -> int4 {
+      if (tl >= ntiles) return make_int4(-1, -1, -1, -1);
+      const int s0 = (p.reverse ? ntiles - 1 - tl : tl) * PAIR;
+      return __ldg(reinterpret_cast<const int4*>(p.row_src + (size_t)(s0 / p.F) * BM) + lane);
     };
-    if (MODE == SDD && p.gather_a) tok_fetch(blockIdx.x);
+    int4 tok_next = make_int4(-1, -1, -1, -1);
+    if (MODE == SDD && p.gather_a) tok_next = tok_load(blockIdx.x);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
       int4 atok = make_int4(0, 0, 0, 0);
       if (MODE == SDD && p.gather_a) {
-        tok_fetch(tile + gridDim.x);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        const int4 r = tokring[(tile_i & 1) * 32 + lane];
+        const int4 r = tok_next;
+        tok_next = tok_load(tile + gridDim.x);
         const int oob = p.gather_T, kq = p.gather_k;
         atok = make_int4(r.x >= 0 ? r.x / kq : oob, r.y >= 0 ? r.y / kq : oob, r.z >= 0 ? r.z / kq : oob,
                          r.w >= 0 ? r.w / kq : oob);
@@ -816,6 +810,13 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 
+static thread_local int t_sm_budget = 0;
+void set_gemm_sm_budget(int sms) { t_sm_budget = sms; }
+int gemm_sm_budget() {
+  const int all = moe_device_sm_count();
+  return (t_sm_budget > 0 && t_sm_budget < all) ? t_sm_budget : all;
+}
+
 // Experiment knobs for A/B timing (MOE_GEMM_DBG, see GemmParams::dbg); 0 in production.
 int gemm_dbg() {
   static int v = -1;
@@ -854,7 +855,7 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
     if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
     attr_set = true;
   }
-  int grid = moe_device_sm_count();
+  int grid = gemm_sm_budget();
   if (L.max_tiles < grid) grid = L.max_tiles;
   if (grid < 1) grid = 1;
   GemmParams p = L.p;

@@ -80,6 +80,11 @@ struct GemmLaunch {
 };
 
 moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
+// Persistent-grid size control for concurrent kernels (host, per thread):
+// gemm_sm_budget() = SMs the next GEMM launches may use (default: all);
+// set by moe_backward around the GEMMs that share the GPU with the router dWr.
+int gemm_sm_budget();
+void set_gemm_sm_budget(int sms);  // <= 0: all SMs
 int gemm_dbg();
 // Timeline tracing of the GEMM engine (debug only, env MOE_GEMM_TRACE=1):
 // slot [launch][cta][tile][event], events: 0 producer first load, 1 MMA start,

@@ -494,7 +494,7 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
     if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
     attr_set = true;
   }
-  int grid = moe_device_sm_count() & ~1;
+  int grid = gemm_sm_budget() & ~1;
   if (2 * L.max_tiles < grid) grid = 2 * L.max_tiles;
   if (grid < 2) grid = 2;
   GemmParams p = L.p;

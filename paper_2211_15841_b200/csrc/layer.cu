@@ -2,11 +2,49 @@
 // above. Forward follows Fig. 5; backward follows the operation
 // list of §5.1. No host synchronisation: data-dependent sizes live
 // in saved->topo.sizes on the device.
+#include <stdlib.h>
+
 #include "bsgemm.cuh"
 #include "common.cuh"
 #include "permute.cuh"
 
 using namespace moe;
+
+namespace {
+// Side stream (per thread and device) on which moe_backward runs the router's
+// dWr while the SDD^T uses the remaining SMs; fork/join by events, so the
+// whole backward stays one stream-ordered, graph-capturable call.
+struct SideStream {
+  int device = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+thread_local SideStream t_side;
+
+moe_status side_stream(SideStream** out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(MOE_ECUDA, "cudaGetDevice failed");
+  if (t_side.device != dev) {
+    if (cudaStreamCreateWithFlags(&t_side.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&t_side.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&t_side.join, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: side stream creation failed");
+    t_side.device = dev;
+  }
+  *out = &t_side;
+  return MOE_OK;
+}
+
+// SMs given to the router dWr GEMM while the SDD^T runs beside it (MOE_DWR_SMS, 0 = serial).
+int dwr_side_sms() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_DWR_SMS");
+    v = e ? atoi(e) : 8;
+  }
+  return v;
+}
+}  // namespace
 
 extern "C" {
 
@@ -60,8 +98,30 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   } else {
     MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
   }
+  // b7 (dWr = x^T . dlogits) only needs the scatter backward's dlogits: it runs
+  // on a side stream on dwr_side_sms() SMs while the SDD^T takes the others.
+  const int side_sms = fused_router ? dwr_side_sms() : 0;
+  SideStream* side = nullptr;
+  if (side_sms > 0) {
+    MOE_TRY(side_stream(&side));
+    if (cudaEventRecord(side->fork, as_stream(stream)) != cudaSuccess ||
+        cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: fork failed");
+    set_gemm_sm_budget(side_sms);
+    const moe_status st = moe_router_dwr(cfg, x, dl16, g->dwr, ws, side->s);
+    set_gemm_sm_budget(0);
+    MOE_TRY(st);
+    if (cudaEventRecord(side->join, side->s) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: join record failed");
+    set_gemm_sm_budget(moe_device_sm_count() - side_sms);
+  }
   // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
-  MOE_TRY(moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream));
+  {
+    const moe_status st =
+        moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream);
+    set_gemm_sm_budget(0);
+    MOE_TRY(st);
+  }
   // b3: DS^TD: dW2 = A^T . dY_g                              "second layer weight gradient"
   MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
   if (fused_router) {
@@ -70,10 +130,13 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
       MOE_TRY(moe_dds_gather(cfg, x, dh, topo, g->dw1, sv->x_g, stream));
     else
       MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
-    // b7: dWr = x^T . dlogits
-    MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
+    // b7: dWr = x^T . dlogits (unless it already runs on the side stream)
+    if (!side) MOE_TRY(moe_router_dwr(cfg, x, dl16, g->dwr, ws, stream));
     // b4 + b6 + b7: dx = sum_j (dH . W1^T)[pos[t*k+j]] + dlogits . Wr^T   "first layer data gradient"
-    return moe_dsd_dx(cfg, dh, w->w1, topo, dl16, w->wr, dx, dx_g, stream);
+    MOE_TRY(moe_dsd_dx(cfg, dh, w->w1, topo, dl16, w->wr, dx, dx_g, stream));
+    if (side && cudaStreamWaitEvent(as_stream(stream), side->join, 0) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: join failed");
+    return MOE_OK;
   }
   // b4: DSD^T: dX_g = dH . W1^T                              "first layer data gradient"
   MOE_TRY(moe_dsd(cfg, dh, 0, w->w1, 1, topo, dx_g, stream));
