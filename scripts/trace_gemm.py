@@ -58,7 +58,8 @@ def main(out):
     step.run()
     n = lib.moe_debug_trace_dump(out.encode())
     tr = np.fromfile(out, dtype=np.uint64).reshape(n, C, TT, EV).astype(np.float64)
-    gemm_names = [nm for nm in step.names if nm in ("router", "sdd", "dsd+scatter", "sddT", "dsTd", "dsdT", "ddTs",
+    gemm_names = [nm for nm in step.names if nm in ("router", "sdd", "sdd+gather", "dsd+scatter", "sddT", "dsTd", "dsdT",
+                                                   "ddTs", "ddTs+gather", "dsdT+dx",
                                                    "router_dwr", "router_dx")]
     for li in range(n):
         a = tr[li]
