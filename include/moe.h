@@ -239,7 +239,8 @@ moe_status moe_dds_gather(const moe_config* cfg, const void* x, const void* dh, 
  * y [T, h] with y[t] = sum_j gates[t,j] * y_g[pos[t*k+j]]. For top-1 the
  * DSD epilogue writes the gate-scaled rows straight to y[t] with TMA
  * tile::scatter4 (rows via topo->row_src, pad rows dropped); for k > 1 it is
- * moe_dsd followed by moe_scatter. y_g is still written (the backward needs it). */
+ * moe_dsd followed by moe_scatter. y_g is still written (the backward needs it).
+ * gates = NULL: unit weights (the un-permutation alone). */
 moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
                            const float* gates, void* y_g, void* y, void* stream);
 moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void* s, int trans_s,
@@ -278,7 +279,9 @@ moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const 
  * whose A rows are the tile's tokens' dlogits (TMA tile::gather4 through
  * topo->row_src) and writes its rows straight to dx[token] (tile::scatter4;
  * pad rows dropped). For k > 1: moe_dsd into dx_g [max_rows, h] (caller
- * scratch, required), then moe_router_dx. dlogits bf16 [T,E]; wr [h,E]. */
+ * scratch, required), then moe_router_dx. dlogits bf16 [T,E]; wr [h,E].
+ * dlogits = wr = NULL drops the router term (DSD^T + gather backward only; then
+ * dx_g is required and also receives dX_g). */
 moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, const moe_topology_t* topo,
                       const void* dlogits_bf16, const void* wr, void* dx, void* dx_g, void* stream);
 

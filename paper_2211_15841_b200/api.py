@@ -232,10 +232,10 @@ def moe_dsd_scatter(cfg, s, w2, topo: Topology, gates, y_g=None, y=None):
     return y_g, y
 
 
-def moe_dsd_dx(cfg, dh, w1, topo: Topology, dlogits_bf16, wr, dx=None, dx_g=None):
-    """moe_dsd_dx (include/moe.h): dx = sum_j (dH . W1^T)[pos] + dlogits . Wr^T."""
+def moe_dsd_dx(cfg, dh, w1, topo: Topology, dlogits_bf16=None, wr=None, dx=None, dx_g=None):
+    """moe_dsd_dx (include/moe.h): dx = sum_j (dH . W1^T)[pos] (+ dlogits . Wr^T)."""
     dx = dx if dx is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=torch.bfloat16, device=dh.device)
-    if dx_g is None and cfg.top_k > 1:
+    if dx_g is None and (cfg.top_k > 1 or dlogits_bf16 is None):
         dx_g = torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=torch.bfloat16, device=dh.device)
     check("moe_dsd_dx", lib.moe_dsd_dx(ctypes.byref(cfg), _p(dh), _p(w1), ctypes.byref(topo.struct), _p(dlogits_bf16),
                                        _p(wr), _p(dx), _p(dx_g), _stream()))

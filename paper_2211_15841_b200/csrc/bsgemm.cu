@@ -1166,19 +1166,25 @@ moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void
 
 moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, const moe_topology_t* topo,
                       const void* dlogits_bf16, const void* wr, void* dx, void* dx_g, void* stream) {
-  MOE_CHECK_ARG(dh && w1 && dlogits_bf16 && wr && dx, "moe_dsd_dx: NULL pointer");
-  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && cfg->num_experts % 64 == 0 && cfg->num_experts <= 256 &&
-      cfg->hidden % 256 == 0 && !use_pair_rows())
-    return dsd_launch(cfg, dh, 0, w1, 1, topo, dx, nullptr, dx, stream, dlogits_bf16, wr);
-  // general k: dX_g = dH . W1^T, then dx = sum_j dX_g[pos] + dlogits . Wr^T
+  MOE_CHECK_ARG(dh && w1 && dx, "moe_dsd_dx: NULL pointer");
+  MOE_CHECK_ARG((dlogits_bf16 == nullptr) == (wr == nullptr), "moe_dsd_dx: dlogits and wr come together");
+  const bool router_term = dlogits_bf16 != nullptr;
+  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && cfg->hidden % 256 == 0 && !use_pair_rows() &&
+      (!router_term || (cfg->num_experts % 64 == 0 && cfg->num_experts <= 256))) {
+    if (router_term) return dsd_launch(cfg, dh, 0, w1, 1, topo, dx, nullptr, dx, stream, dlogits_bf16, wr);
+    MOE_CHECK_ARG(dx_g, "moe_dsd_dx: the un-permutation-only form needs the dx_g buffer");
+    return dsd_launch(cfg, dh, 0, w1, 1, topo, dx_g, nullptr, dx, stream);  // dX_g kept, rows also to dx
+  }
+  // general k: dX_g = dH . W1^T, then dx = sum_j dX_g[pos] (+ dlogits . Wr^T)
   MOE_CHECK_ARG(dx_g, "moe_dsd_dx: top_k > 1 needs the dx_g scratch buffer");
   MOE_TRY(moe_dsd(cfg, dh, 0, w1, 1, topo, dx_g, stream));
+  if (!router_term) return moe_gather_bwd(cfg, dx_g, topo, dx, stream);
   return moe_router_dx(cfg, dlogits_bf16, wr, dx_g, topo, dx, stream);
 }
 
 moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
                            const float* gates, void* y_g, void* y, void* stream) {
-  MOE_CHECK_ARG(gates && y, "moe_dsd_scatter: NULL gates or y");
+  MOE_CHECK_ARG(y, "moe_dsd_scatter: NULL y");  // gates may be NULL: unit weights (un-permutation only)
   if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && !use_pair_rows())
     return dsd_launch(cfg, s, 0, b, 0, topo, y_g, gates, y, stream);
   MOE_TRY(moe_dsd(cfg, s, 0, b, 0, topo, y_g, stream));  // k > 1: slots are summed by the combine kernel

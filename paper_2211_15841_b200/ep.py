@@ -132,8 +132,7 @@ class ExpertParallelMoE:
                 a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
             else:
                 a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
-            y_g = B.moe_dsd(cfg_e, a, 0, w2_local, 0, topo_e)
-            B.moe_scatter(cfg_e, y_g, topo_e, None, y=y_recv)
+            B.moe_dsd_scatter(cfg_e, a, w2_local, topo_e, None, y=y_recv)   # DSD + un-pad in one kernel
         # (5) combine: reverse exchange, then gate-weighted sum in token order
         y_sorted = x.new_empty(T * self.k, self.h)
         self._a2a(y_sorted, y_recv, sends, recvs)
@@ -158,9 +157,8 @@ class ExpertParallelMoE:
             else:
                 dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e)
             B.moe_dsd(cfg_e, st.a, 1, dy_g, 0, st.topo_e, out=dw2)
-            dx_g = B.moe_dsd(cfg_e, dh, 0, w1_local, 1, st.topo_e)
             B.moe_dds(cfg_e, st.x_g, 1, dh, 0, st.topo_e, out=dw1)
-            B.moe_gather_bwd(cfg_e, dx_g, st.topo_e, dx=dx_recv)
+            B.moe_dsd_dx(cfg_e, dh, w1_local, st.topo_e, dx=dx_recv)          # DSD^T + un-pad in one kernel
         dx_sorted = dy.new_empty(cfg_l.tokens * self.k, self.h)
         self._a2a(dx_sorted, dx_recv, st.sends, st.recvs)
         dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)

@@ -71,6 +71,31 @@ def moe_sdd_deriv(cfg, a, b, trans_b, topo, act=0, deriv_src=None, want_deriv=Fa
     return (_t(A), _t(O.act_grad(act, H))) if want_deriv else _t(A)
 
 
+def moe_dsd_scatter(cfg, s, w2, topo, gates, y_g=None, y=None):
+    yg = O.dsd(_np(s), _np(w2), topo.topo)
+    g = np.ones((cfg.tokens, cfg.top_k)) if gates is None else _np(gates).reshape(cfg.tokens, cfg.top_k)
+    r = _t(O.padded_scatter(yg, topo.plan, g, cfg.tokens, cfg.top_k))
+    if y is not None:
+        y.copy_(r)
+        return _t(yg), y
+    return _t(yg), r
+
+
+def moe_dsd_dx(cfg, dh, w1, topo, dlogits_bf16=None, wr=None, dx=None, dx_g=None):
+    dxg = O.dsd(_np(dh), _np(w1), topo.topo, trans_b=True)
+    T, k = cfg.tokens, cfg.top_k
+    r = np.zeros((T, dxg.shape[1]))
+    for t in range(T):
+        for j in range(k):
+            r[t] += dxg[topo.plan.pos[t * k + j]]
+    if dlogits_bf16 is not None:
+        r = r + _np(dlogits_bf16) @ _np(wr).T
+    if dx is not None:
+        dx.copy_(_t(r))
+        return dx
+    return _t(r)
+
+
 def moe_dsd(cfg, s, trans_s, b, trans_b, topo, out=None):
     r = _t(O.dsd(_np(s), _np(b), topo.topo, trans_s=bool(trans_s), trans_b=bool(trans_b)))
     if out is not None:

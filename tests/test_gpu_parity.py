@@ -303,12 +303,18 @@ def test_dsd_dx(case):
     dx = torch.full((T, h), float("nan"), dtype=torch.bfloat16)
     got = f64(A.moe_dsd_dx(cfg, dh.to(d), w1.to(d), tg, dl.to(d), wr.to(d), dx=dx.to(d)))
     dxg = O.dsd(f64(dh[:nnz]), S.to_f64(w1), topo, trans_b=True)
-    want = S.to_f64(dl) @ S.to_f64(wr).T
+    gathered = np.zeros((T, h))
     for t in range(T):
         for j in range(k):
-            want[t] += dxg[plan.pos[t * k + j]]
+            gathered[t] += dxg[plan.pos[t * k + j]]
+    want = gathered + S.to_f64(dl) @ S.to_f64(wr).T
     assert np.isfinite(got).all()
     assert rel_fro(got, want) < FRO_TOL
+    # without the router term: DSD^T + gather backward (the expert-parallel form)
+    got2 = f64(A.moe_dsd_dx(cfg, dh.to(d), w1.to(d), tg, dx=torch.full((T, h), float("nan"),
+                                                                     dtype=torch.bfloat16).to(d)))
+    assert np.isfinite(got2).all()
+    assert rel_fro(got2, gathered) < FRO_TOL
 
 
 @pytest.mark.parametrize("case", PRODUCT_CASES + [(4100, 512, 2048, 64, 1, 0.0, 4)])
@@ -334,6 +340,10 @@ def test_dsd_scatter(case):
     got = f64(yy)
     assert np.isfinite(got).all()          # every token row written exactly by its scatter
     assert rel_fro(got, want) < FRO_TOL
+    # unit weights (gates = NULL): the un-permutation alone
+    _, y1 = A.moe_dsd_scatter(cfg, svals.to(d), w2.to(d), tg, None, y=y.to(d))
+    want1 = O.padded_scatter(f64(yg[:Tp]), plan, np.ones((T, k)), T, k)
+    assert rel_fro(f64(y1), want1) < FRO_TOL
 
 
 @pytest.mark.parametrize("case", PRODUCT_CASES)
