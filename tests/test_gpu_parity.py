@@ -547,6 +547,68 @@ def test_c1_full_size_sampled():
     assert rel_fro(got, want) < FRO_TOL
 
 
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_full_size_sampled_rows(name):
+    """BASELINE configs[2] (MoE-Small, skewed router: empty and overloaded
+    experts) and configs[4] (MoE-Medium top-2) at full size through
+    moe_forward / moe_backward: sampled y and dx rows recomputed one token at
+    a time by the oracle's per-token definition (P:98, P:157, P:206 chain rule),
+    and sampled dW2 rows of the most loaded expert."""
+    d = dev()
+    A = api()
+    shp = S.CONFIGS[name]
+    T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
+    inp = S.make_inputs(shp, seed=0)
+    cfg = A.make_config(T, h, E, k, f, act=shp.act)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    L = O.router_logits(x64, wr64)
+    idx_o, gates_o = O.topk(L, k)
+    idx_g = saved.expert_idx.cpu().numpy()
+    assert (idx_g != idx_o).any(axis=1).sum() <= 4       # fp32-vs-fp64 near-ties only
+    P = O.softmax(L)
+    yg, dxg = f64(y), f64(dx)
+    rng = np.random.default_rng(1)
+    checked = 0
+    for t in rng.choice(T, 24, replace=False):
+        if (idx_g[t] != idx_o[t]).any():
+            continue
+        yt = np.zeros(h)
+        dxt = np.zeros(h)
+        dp = np.zeros(E)
+        for j in range(k):
+            e = idx_o[t, j]
+            hp = x64[t] @ w164[:, e * f:(e + 1) * f]
+            yj = O.act(shp.act, hp) @ w264[e * f:(e + 1) * f]
+            yt += gates_o[t, j] * yj
+            dA = gates_o[t, j] * (dy64[t] @ w264[e * f:(e + 1) * f].T)
+            dxt += (dA * O.act_grad(shp.act, hp)) @ w164[:, e * f:(e + 1) * f].T
+            dp[e] += yj @ dy64[t]
+        dlog = P[t] * (dp - P[t] @ dp)
+        dxt += dlog @ wr64.T
+        assert rel_fro(yg[t], yt) < FRO_TOL
+        assert rel_fro(dxg[t], dxt) < FRO_TOL
+        checked += 1
+    assert checked >= 16
+    # sampled dW2 rows of the most loaded expert
+    counts = np.bincount(idx_o.reshape(-1), minlength=E)
+    e = int(np.argmax(counts))
+    ti, ji = np.nonzero(idx_o == e)
+    Hx = x64[ti] @ w164[:, e * f:(e + 1) * f]
+    Ax = O.act(shp.act, Hx)
+    dY = gates_o[ti, ji][:, None] * dy64[ti]
+    cols = rng.choice(f, 6, replace=False)
+    assert rel_fro(f64(dw2[e * f + cols]), Ax[:, cols].T @ dY) < FRO_TOL
+    # experts without tokens: exact zero weight-gradient columns / rows
+    for e0 in np.nonzero(counts == 0)[0][:4]:
+        assert not f64(dw1[:, e0 * f:(e0 + 1) * f]).any()
+        assert not f64(dw2[e0 * f:(e0 + 1) * f]).any()
+
+
 def test_expert_parallel_single_rank_nccl():
     """The expert-parallel layer (ep.py) driving the CUDA kernels through NCCL
     with one rank (the only multi-process shape one GPU allows): must match the
