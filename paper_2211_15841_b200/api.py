@@ -65,7 +65,13 @@ class Topology:
                   "row_offsets": rows // bs + 1, "col_indices": nnz, "row_indices": nnz,
                   "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "pair_bins": E,
                   "row_src": rows, "sizes": 3}
-        self.t = {n: torch.empty(max(int(shapes[n]), 1), dtype=torch.int32, device=device) for n in TOPO_FIELDS}
+        # one allocation, 16-byte aligned views (TMA / int4 loads read row_src)
+        sizes = [((max(int(shapes[n]), 1) + 3) // 4) * 4 for n in TOPO_FIELDS]
+        self.buf = torch.empty(sum(sizes), dtype=torch.int32, device=device)
+        self.t, o = {}, 0
+        for n, sz in zip(TOPO_FIELDS, sizes):
+            self.t[n] = self.buf[o:o + max(int(shapes[n]), 1)]
+            o += sz
         self.struct = MoeTopology(*[self.t[n].data_ptr() for n in TOPO_FIELDS])
 
     def __getitem__(self, name):

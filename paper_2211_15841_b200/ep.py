@@ -98,6 +98,19 @@ class ExpertParallelMoE:
     def _cfg(self, tokens, experts, k):
         return self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
 
+    def _topology(self, cfg, ids, slot):
+        """moe_topology with a workspace cached per slot and shape (scratch only:
+        the topology arrays themselves are per step, they belong to the EPState)."""
+        cache = self.__dict__.setdefault("_ws_cache", {})
+        key = (slot, cfg.tokens, cfg.num_experts, cfg.top_k)
+        if not hasattr(self.B, "workspace"):
+            return self.B.moe_topology(cfg, ids)
+        if key not in cache:
+            for k_old in [k_ for k_ in cache if k_[0] == slot]:
+                del cache[k_old]
+            cache[key] = self.B.workspace(cfg, ids.device)
+        return self.B.moe_topology(cfg, ids, ws=cache[key])
+
     def _a2a(self, out, inp, out_splits, in_splits):
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
@@ -107,7 +120,7 @@ class ExpertParallelMoE:
         cfg_l = self._cfg(T, self.E, self.k)
         # (1) local router + top-k, grouped by GLOBAL expert
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
-        topo_l = B.moe_topology(cfg_l, idx)
+        topo_l = self._topology(cfg_l, idx, "local")
         x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
         # (2) count exchange -> split sizes (the one host synchronisation)
         counts = topo_l["counts"][: self.E].to(torch.int64)
@@ -126,7 +139,7 @@ class ExpertParallelMoE:
         y_recv = x.new_empty(n_recv, self.h)
         if n_recv > 0:
             ids = torch.from_numpy(recv_ids).to(x.device)
-            topo_e = B.moe_topology(cfg_e, ids)
+            topo_e = self._topology(cfg_e, ids, "experts")
             x_g = B.moe_gather(cfg_e, recv_x, topo_e)
             if self.act != 0:
                 a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
@@ -147,8 +160,12 @@ class ExpertParallelMoE:
         dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
         dy_recv = dy.new_empty(st.n_recv, self.h)
         self._a2a(dy_recv, dy_sorted, st.recvs, st.sends)
-        dw1 = torch.zeros(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device)
-        dw2 = torch.zeros(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device)
+        # every column / row is written by the products (experts without tokens get exact zeros)
+        dw1 = torch.empty(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device)
+        dw2 = torch.empty(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device)
+        if st.n_recv == 0:
+            dw1.zero_()
+            dw2.zero_()
         dx_recv = dy.new_empty(st.n_recv, self.h)
         if st.n_recv > 0:
             dy_g = B.moe_gather(cfg_e, dy_recv, st.topo_e)
