@@ -20,13 +20,15 @@
 // BN = 256 tiles pair two adjacent block-columns of the same expert (F even):
 // they share their row set, so one walk of the transpose index serves both.
 //
-// Warp roles (192 threads, 1 CTA/SM): warp 0 = TMA producer, warp 1 = TMEM
-// allocator + single-thread MMA issuer, warps 2-5 = epilogue. Pipelines:
-// STAGES-deep smem ring (full/empty mbarriers), double-buffered TMEM
-// accumulator (tfull/tempty) so the epilogue of tile i overlaps the main loop
-// of tile i+1. The epilogue stages bf16 results in 128B-swizzled shared memory
-// and writes them with TMA bulk stores (coalesced, asynchronous); the SDD^T
-// epilogue prefetches the saved pre-activation H by TMA.
+// Warp roles (1 CTA/SM): warps 0..NP-1 = TMA producers (stage s issued by warp
+// s % NP), warp NP = TMEM allocator + single-thread MMA issuer, the next EPW
+// warps = epilogue (two per TMEM lane quarter). Pipelines: STAGES-deep smem
+// ring (full/empty mbarriers), double-buffered TMEM accumulator (tfull/tempty)
+// so the epilogue of tile i overlaps the main loop of tile i+1. The epilogue
+// stages bf16 results in 64B-swizzled shared memory and writes them with TMA
+// bulk stores (or tile::scatter4 to token rows); the SDD forward writes act(H)
+// and act'(H), the SDD^T epilogue prefetches the saved act'(H) by TMA. DSD_ROW
+// tiles may append dense K-steps whose A rows are tile::gather4-ed (router dx).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -173,19 +175,16 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
 // the [chunk][64 rows][128 B] layout of the MN-major UMMA descriptor (one TMA
 // instruction per operand: the per-SM TMA issue rate, not bytes, limits small
 // boxes; see scripts/micro/l2_tma_bw.cu).
-template <bool PF>
+// Loads of one operand side; a null map skips them (issue_stage's `part` mask).
 __device__ __forceinline__ void ld2(void* dst, const CUtensorMap* m, uint64_t* fb, int c0, int c1) {
-  if (!m) return;
-  if (PF) tma_prefetch_2d(m, c0, c1); else tma_load_2d(dst, m, fb, c0, c1);
+  if (m) tma_load_2d(dst, m, fb, c0, c1);
 }
-template <bool PF>
 __device__ __forceinline__ void ld3(void* dst, const CUtensorMap* m, uint64_t* fb, int c0, int c1, int c2) {
-  if (!m) return;
-  if (PF) tma_prefetch_3d(m, c0, c1, c2); else tma_load_3d(dst, m, fb, c0, c1, c2);
+  if (m) tma_load_3d(dst, m, fb, c0, c1, c2);
 }
-#define tma_load_2d ld2<PF>
-#define tma_load_3d ld3<PF>
-template <int MODE, bool A_MN, bool B_MN, int BN, bool PF = false>
+#define tma_load_2d ld2
+#define tma_load_3d ld3
+template <int MODE, bool A_MN, bool B_MN, int BN>
 __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p,
                                             const TileInfo& t, int kit, int sblk, int oblk, uint8_t* sa, uint8_t* sb,
                                             uint64_t* fb, int part = 3) {
