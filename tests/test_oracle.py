@@ -454,3 +454,26 @@ def test_max_padded_rows_bound_is_tight():
     idx = np.arange(8).reshape(8, 1).astype(np.int32)
     plan = O.make_plan(idx, E, bs)
     assert plan.Tp == O.max_padded_rows(T, k, E, bs) == 32
+
+
+def test_product_sweep_layout_conversion():
+    """scripts/product_sweep.py compares the library's BCSR values with torch.bmm
+    through blocks_to_dense / dense_to_blocks; pin both against the oracle's SDD
+    under exact-uniform routing (block (r, e*F+j) = rows r*bs.. of expert e's
+    batched product, columns j*bs..)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "product_sweep", os.path.join(os.path.dirname(__file__), "..", "scripts", "product_sweep.py"))
+    ps = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ps)
+    T, h, f, E, bs = 512, 8, 256, 2, 128
+    x, wr, w1, w2, _ = small_inputs(T, h, f, E, 5)
+    idx = S.uniform_expert_idx(T, E, 1).numpy()
+    plan = O.make_plan(idx, E, bs)
+    topo = O.make_topology(plan, bs, f)
+    hs = O.sdd(O.padded_gather(x, plan, 1), w1, topo)
+    dense = ps.blocks_to_dense(torch.from_numpy(hs), E, T // E, f, bs)
+    want = torch.bmm(t64(x).reshape(E, T // E, h), torch.stack([t64(w1)[:, e * f:(e + 1) * f] for e in range(E)]))
+    np.testing.assert_allclose(dense.numpy(), want.numpy(), atol=1e-12)
+    np.testing.assert_array_equal(ps.dense_to_blocks(dense, E, T // E, f, bs).numpy(), hs)
