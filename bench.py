@@ -544,8 +544,20 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
-    # NCCL's version / debug lines go to stderr so stdout carries only the JSON line
+    # NCCL's version / debug lines go to stderr so stdout carries only the JSON line:
+    # native libraries print to fd 1 directly (NCCL's "NCCL version" line ignores
+    # NCCL_DEBUG_FILE), so fd 1 is pointed at stderr and the JSON goes to a dup
+    # of the original stdout.
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    sys.stdout.flush()
+    out_fd = os.dup(1)
+    os.dup2(2, 1)
+    emit = os.fdopen(out_fd, "w")
+
+    def print(line, flush=True):  # noqa: A001 - the one JSON line, to the real stdout
+        emit.write(line + "\n")
+        emit.flush()
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":

@@ -178,6 +178,31 @@ moe_status moe_unsort_rows_bwd(const moe_config* cfg, const void* dy, const void
 moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
                              void* dx, void* stream);
 
+/* Expert-parallel forms of the fused router backward (P:98 softmax, P:355
+ * expert parallelism; the token owner's side of b1 / b6 / b7). Same
+ * arithmetic as moe_scatter_bwd_router / moe_router_dx, on the unpadded
+ * expert-order rows (sorted_pos instead of pos, no pad rows):
+ *   moe_unsort_rows_bwd_router: dy_sorted, dgates as moe_unsort_rows_bwd, and
+ *     dlogits_bf16 [T,E] = p * (dp - <p,dp>) rounded to bf16.
+ *   moe_sort_rows_bwd_router: dx [T,h] = sum_j dx_sorted[sorted_pos[t*k+j]]
+ *     + dlogits . wr^T (tcgen05; wr [h,E] bf16).
+ * Tensor-core router configs only (E % 64 == 0, E <= 256, top_k <= 8), else
+ * MOE_EUNSUPPORTED. All pointers device, caller-owned; stream-ordered. */
+moe_status moe_unsort_rows_bwd_router(const moe_config* cfg, const void* dy, const void* y_sorted,
+                                      const moe_topology_t* topo, const float* gates, const float* logits,
+                                      const int32_t* expert_idx, void* dy_sorted, float* dgates,
+                                      void* dlogits_bf16, void* stream);
+moe_status moe_sort_rows_bwd_router(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
+                                    const void* dlogits_bf16, const void* wr, void* dx, void* stream);
+
+/* Expert-parallel receive ids (DESIGN.md §7 ordering contract): rows
+ * arrive ordered (source rank q, local expert l, token); ids[i] = l of arrival
+ * row i, i < sum over q, l of counts_all[q*E + e0 + l]. counts_all [P,E] int32
+ * device (the all-gathered per-rank histograms), ids int32 device with room for
+ * every received row. One small kernel, no host synchronisation. */
+moe_status moe_ep_recv_ids(const int32_t* counts_all, int nranks, int num_experts, int e0, int local_experts,
+                           int32_t* ids, int64_t max_rows, void* stream);
+
 /* ---- block-sparse products, Triton notation, §5.1 ----
  * The sparse operand has the MoE topology: logical shape [Tp, E*f] with
  * 128x128 blocks. bf16 in, fp32 accumulate on the tensor cores, bf16 out.

@@ -69,6 +69,9 @@ SIGNATURES = {
     "moe_unsort_rows": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_unsort_rows_bwd": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
     "moe_sort_rows_bwd": (STATUS, [CFG, P, TOPO, P, P]),
+    "moe_unsort_rows_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),
+    "moe_sort_rows_bwd_router": (STATUS, [CFG, P, TOPO, P, P, P, P]),
+    "moe_ep_recv_ids": (STATUS, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P]),
     "moe_sdd": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),

@@ -170,6 +170,51 @@ def moe_sort_rows_bwd(cfg, dx_sorted, topo: Topology, dx=None):
     return dx
 
 
+def router_on_tensor_cores(cfg) -> bool:
+    """The fused tensor-core router path's condition (include/moe.h)."""
+    return cfg.num_experts % 64 == 0 and cfg.num_experts <= 256 and cfg.top_k <= 8
+
+
+def moe_unsort_rows_bwd_router(cfg, dy, y_sorted, topo: Topology, gates, logits, expert_idx, dy_sorted=None,
+                               dgates=None, dlogits=None):
+    """moe_unsort_rows_bwd_router (include/moe.h): dy_sorted, dgates and the bf16 dlogits [T,E]."""
+    T, k = cfg.tokens, cfg.top_k
+    dy_sorted = dy_sorted if dy_sorted is not None else torch.empty(T * k, cfg.hidden, dtype=dy.dtype, device=dy.device)
+    dgates = dgates if dgates is not None else torch.empty(T, k, dtype=torch.float32, device=dy.device)
+    dlogits = dlogits if dlogits is not None else torch.empty(T, cfg.num_experts, dtype=torch.bfloat16,
+                                                              device=dy.device)
+    check("moe_unsort_rows_bwd_router", lib.moe_unsort_rows_bwd_router(
+        ctypes.byref(cfg), _p(dy), _p(y_sorted), ctypes.byref(topo.struct), _p(gates), _p(logits), _p(expert_idx),
+        _p(dy_sorted), _p(dgates), _p(dlogits), _stream()))
+    return dy_sorted, dgates, dlogits
+
+
+def moe_sort_rows_bwd_router(cfg, dx_sorted, topo: Topology, dlogits, wr, dx=None):
+    """moe_sort_rows_bwd_router (include/moe.h): dx = sum_j dx_sorted[sorted_pos] + dlogits . wr^T."""
+    dx = dx if dx is not None else torch.empty(cfg.tokens, cfg.hidden, dtype=dx_sorted.dtype, device=dx_sorted.device)
+    check("moe_sort_rows_bwd_router", lib.moe_sort_rows_bwd_router(
+        ctypes.byref(cfg), _p(dx_sorted), ctypes.byref(topo.struct), _p(dlogits), _p(wr), _p(dx), _stream()))
+    return dx
+
+
+def moe_router_dwr(cfg, x, dlogits, dwr=None, ws=None):
+    """moe_router_dwr (include/moe.h): dWr [h,E] fp32 = x^T . dlogits (tcgen05)."""
+    dwr = dwr if dwr is not None else torch.empty(cfg.hidden, cfg.num_experts, dtype=torch.float32, device=x.device)
+    ws = ws if ws is not None else workspace(cfg, x.device)
+    check("moe_router_dwr", lib.moe_router_dwr(ctypes.byref(cfg), _p(x), _p(dlogits), _p(dwr), _p(ws), _stream()))
+    return dwr
+
+
+def moe_ep_recv_ids(counts_all, rank_e0, local_experts, n_rows, ids=None):
+    """moe_ep_recv_ids (include/moe.h): local expert id of every received row, in
+    arrival order (source, local expert, token), from the [P, E] int32 counts."""
+    P, E = counts_all.shape
+    ids = ids if ids is not None else torch.empty(max(int(n_rows), 1), dtype=torch.int32, device=counts_all.device)
+    check("moe_ep_recv_ids", lib.moe_ep_recv_ids(_p(counts_all), int(P), int(E), int(rank_e0), int(local_experts),
+                                                 _p(ids), int(n_rows), _stream()))
+    return ids
+
+
 def _nnz_values(cfg, device, dtype=torch.bfloat16):
     bs = cfg.block_size
     return torch.empty(moe_max_nnz_blocks(cfg), bs, bs, dtype=dtype, device=device)

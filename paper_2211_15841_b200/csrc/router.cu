@@ -414,3 +414,33 @@ moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const 
 }
 
 }  // extern "C"
+
+extern "C" {
+
+moe_status moe_unsort_rows_bwd_router(const moe_config* cfg, const void* dy, const void* y_sorted,
+                                      const moe_topology_t* topo, const float* gates, const float* logits,
+                                      const int32_t* expert_idx, void* dy_sorted, float* dgates,
+                                      void* dlogits_bf16, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(dy && y_sorted && gates && logits && expert_idx && dy_sorted && dgates && dlogits_bf16,
+                "moe_unsort_rows_bwd_router: NULL pointer");
+  if (!router_on_tensor_cores(cfg))
+    return set_error(MOE_EUNSUPPORTED, "moe_unsort_rows_bwd_router: needs E %% 64 == 0, E <= 256, top_k <= 8");
+  // unpadded expert-order rows: sorted_pos map, no pad rows to zero
+  return scatter_bwd_fused(cfg, dy, y_sorted, topo->sorted_pos, gates, dy_sorted, dgates, logits, expert_idx,
+                           reinterpret_cast<__nv_bfloat16*>(dlogits_bf16), nullptr, nullptr, as_stream(stream));
+}
+
+moe_status moe_sort_rows_bwd_router(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
+                                    const void* dlogits_bf16, const void* wr, void* dx, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(dx_sorted && dlogits_bf16 && wr && dx, "moe_sort_rows_bwd_router: NULL pointer");
+  if (!router_on_tensor_cores(cfg))
+    return set_error(MOE_EUNSUPPORTED, "moe_sort_rows_bwd_router: needs E %% 64 == 0, E <= 256, top_k <= 8");
+  return router_dx_tc(cfg, reinterpret_cast<const __nv_bfloat16*>(dlogits_bf16), wr, dx, dx_sorted, topo->sorted_pos,
+                      (int)cfg->top_k, cfg->hidden, as_stream(stream));
+}
+
+}  // extern "C"

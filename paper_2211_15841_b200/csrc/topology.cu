@@ -17,6 +17,8 @@
 //                      entries, one thread per nonzero block, in closed form.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace moe {
@@ -198,6 +200,35 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
   }
 }
 
+
+// Expert-parallel receive ids (moe_ep_recv_ids): segments (source q, local
+// expert l) in arrival order, segment length counts_all[q*E + e0 + l]; every
+// CTA rescans the P*E_l segment lengths in shared memory (E_l*P = E entries at
+// most), then writes ids grid-stride with a binary search over the prefix.
+__global__ void ep_recv_ids_kernel(const int32_t* __restrict__ counts_all, int P, int E, int e0, int El,
+                                   int32_t* __restrict__ ids, long long max_rows) {
+  extern __shared__ int32_t s_pre[];  // [P*El + 1] exclusive prefix
+  const int nseg = P * El;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < nseg; ++g) {
+      s_pre[g] = acc;
+      acc += __ldg(counts_all + (size_t)(g / El) * E + e0 + g % El);
+    }
+    s_pre[nseg] = acc;
+  }
+  __syncthreads();
+  const long long total = min((long long)s_pre[nseg], max_rows);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg - 1;   // last segment with s_pre[g] <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    ids[i] = lo % El;
+  }
+}
+
 }  // namespace moe
 
 using namespace moe;
@@ -224,5 +255,19 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
              E, bs, F, n_chunks, chunk_counts, *topo);
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ep_recv_ids(const int32_t* counts_all, int nranks, int num_experts, int e0, int local_experts,
+                                      int32_t* ids, int64_t max_rows, void* stream) {
+  MOE_CHECK_ARG(counts_all && ids, "moe_ep_recv_ids: NULL pointer");
+  MOE_CHECK_ARG(nranks >= 1 && local_experts >= 1 && e0 >= 0 && e0 + local_experts <= num_experts && max_rows >= 0,
+                "moe_ep_recv_ids: bad ranks/experts (P=%d E=%d e0=%d E_l=%d)", nranks, num_experts, e0, local_experts);
+  const int nseg = nranks * local_experts;
+  MOE_CHECK_ARG(nseg + 1 <= 12 * 1024, "moe_ep_recv_ids: %d segments exceed the shared-memory scan", nseg);
+  if (max_rows == 0) return MOE_OK;
+  const int ctas = (int)std::min<int64_t>(ceil_div(max_rows, 256), 4 * 148);
+  MOE_LAUNCH("ep_recv_ids", ep_recv_ids_kernel, dim3(ctas), dim3(256), (nseg + 1) * sizeof(int32_t),
+             as_stream(stream), counts_all, nranks, num_experts, e0, local_experts, ids, (long long)max_rows);
   return MOE_OK;
 }

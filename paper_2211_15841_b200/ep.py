@@ -99,20 +99,39 @@ class ExpertParallelMoE:
         return self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
 
     def _topology(self, cfg, ids, slot):
-        """moe_topology with a workspace cached per slot and shape (scratch only:
-        the topology arrays themselves are per step, they belong to the EPState)."""
-        cache = self.__dict__.setdefault("_ws_cache", {})
-        key = (slot, cfg.tokens, cfg.num_experts, cfg.top_k)
-        if not hasattr(self.B, "workspace"):
+        """moe_topology into device arrays and a workspace cached per slot. The
+        expert side's row count changes every step, so its arrays are sized for
+        a capacity (grown geometrically) rather than the exact count: the
+        library only reads and writes the first R entries / device-side sizes."""
+        if not hasattr(self.B, "Topology"):
             return self.B.moe_topology(cfg, ids)
-        if key not in cache:
-            for k_old in [k_ for k_ in cache if k_[0] == slot]:
-                del cache[k_old]
-            cache[key] = self.B.workspace(cfg, ids.device)
-        return self.B.moe_topology(cfg, ids, ws=cache[key])
+        cache = self.__dict__.setdefault("_topo_cache", {})
+        need = int(cfg.tokens) * int(cfg.top_k)
+        ent = cache.get(slot)
+        if ent is None or ent[0] < need or ent[1] != (cfg.num_experts, cfg.top_k):
+            cap = max(need, int(ent[0] * 1.25) if ent is not None else need)
+            cap = -(-cap // 1024) * 1024
+            cap_cfg = self.B.cfg_replace(cfg, tokens=cap // int(cfg.top_k))
+            ent = (cap, (cfg.num_experts, cfg.top_k), self.B.Topology(cap_cfg, ids.device),
+                   self.B.workspace(cap_cfg, ids.device))
+            cache[slot] = ent
+        return self.B.moe_topology(cfg, ids, topo=ent[2], ws=ent[3])
 
     def _a2a(self, out, inp, out_splits, in_splits):
         dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+
+    def _gather_counts(self, counts):
+        """[P, E] int32 per-rank histograms on every rank (one collective)."""
+        out = counts.new_empty(self.world, counts.numel())
+        try:
+            dist.all_gather_into_tensor(out, counts, group=self.group)
+        except (RuntimeError, NotImplementedError, AttributeError):
+            dist.all_gather(list(out.unbind(0)), counts, group=self.group)
+        return out
+
+    def _fused_router(self, cfg):
+        f = getattr(self.B, "router_on_tensor_cores", None)
+        return bool(f and f(cfg))
 
     def forward(self, x, wr, w1_local, w2_local):
         B = self.B
@@ -123,12 +142,10 @@ class ExpertParallelMoE:
         topo_l = self._topology(cfg_l, idx, "local")
         x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
         # (2) count exchange -> split sizes (the one host synchronisation)
-        counts = topo_l["counts"][: self.E].to(torch.int64)
-        gathered = [torch.empty_like(counts) for _ in range(self.world)]
-        dist.all_gather(gathered, counts, group=self.group)
-        counts_all = torch.stack(gathered).cpu().numpy()
+        counts_dev = self._gather_counts(topo_l["counts"][: self.E].to(torch.int32).contiguous())
+        counts_all = counts_dev.cpu().numpy()
         sends = send_splits(counts_all[self.rank], self.world)
-        recvs, recv_ids = recv_plan(counts_all, self.rank, self.world)
+        recvs = [int(counts_all[q, self.e0:self.e1].sum()) for q in range(self.world)]
         n_recv = int(sum(recvs))
         # (3) dispatch
         recv_x = x.new_empty(n_recv, self.h)
@@ -138,7 +155,10 @@ class ExpertParallelMoE:
         topo_e = x_g = act_deriv = a = None
         y_recv = x.new_empty(n_recv, self.h)
         if n_recv > 0:
-            ids = torch.from_numpy(recv_ids).to(x.device)
+            if hasattr(B, "moe_ep_recv_ids"):   # arrival-order expert ids built on the device
+                ids = B.moe_ep_recv_ids(counts_dev, self.e0, self.El, n_recv)
+            else:
+                ids = torch.from_numpy(recv_plan(counts_all, self.rank, self.world)[1]).to(x.device)
             topo_e = self._topology(cfg_e, ids, "experts")
             x_g = B.moe_gather(cfg_e, recv_x, topo_e)
             if self.act != 0:
@@ -156,8 +176,24 @@ class ExpertParallelMoE:
     def backward(self, st: EPState, x, dy, wr, w1_local, w2_local):
         B = self.B
         cfg_l, cfg_e = st.cfg_local, st.cfg_e
-        # b1 on the token owner: dY rows in expert order, dgates
-        dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
+        fused = self._fused_router(cfg_l)
+        side = None
+        # b1 on the token owner: dY rows in expert order, dgates (+ the router's dlogits)
+        if fused:
+            dy_sorted, dgates, dlogits = B.moe_unsort_rows_bwd_router(cfg_l, dy, st.y_sorted, st.topo_local, st.gates,
+                                                                      st.logits, st.expert_idx)
+            # b7 dWr = x^T . dlogits needs nothing else: on a side stream beside the exchange
+            if dy.is_cuda:
+                side = self.__dict__.setdefault("_side", torch.cuda.Stream(device=dy.device))
+                side.wait_stream(torch.cuda.current_stream(dy.device))
+                dlogits.record_stream(side)
+                ws_l = self._topo_cache["local"][3]      # the local topology's scratch: idle until the next step
+                with torch.cuda.stream(side):
+                    dwr = B.moe_router_dwr(cfg_l, x, dlogits, ws=ws_l)
+            else:
+                dwr = B.moe_router_dwr(cfg_l, x, dlogits)
+        else:
+            dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
         dy_recv = dy.new_empty(st.n_recv, self.h)
         self._a2a(dy_recv, dy_sorted, st.recvs, st.sends)
         # every column / row is written by the products (experts without tokens get exact zeros)
@@ -178,8 +214,14 @@ class ExpertParallelMoE:
             B.moe_dsd_dx(cfg_e, dh, w1_local, st.topo_e, dx=dx_recv)          # DSD^T + un-pad in one kernel
         dx_sorted = dy.new_empty(cfg_l.tokens * self.k, self.h)
         self._a2a(dx_sorted, dx_recv, st.sends, st.recvs)
-        dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
-        dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
+        if fused:   # b6 + b7: un-sort fused with dx += dlogits . Wr^T (tcgen05)
+            dx = B.moe_sort_rows_bwd_router(cfg_l, dx_sorted, st.topo_local, dlogits, wr)
+            if side is not None:
+                torch.cuda.current_stream(dy.device).wait_stream(side)
+                dwr.record_stream(torch.cuda.current_stream(dy.device))
+        else:
+            dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
         dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
 

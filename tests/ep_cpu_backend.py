@@ -172,3 +172,39 @@ def moe_router_bwd(cfg, x, wr, logits, expert_idx, dgates, dx):
     dl = p * (dp - (p * dp).sum(1, keepdims=True))
     dx += _t(dl @ _np(wr).T)
     return _t(_np(x).T @ dl)
+
+
+# ---- fused tensor-core router forms (same arithmetic, unpadded expert order)
+
+def router_on_tensor_cores(cfg):
+    return True
+
+
+def _dlogits(cfg, logits, expert_idx, dgates):
+    L, idx, dg = _np(logits), expert_idx.numpy(), _np(dgates)
+    p = O.softmax(L)
+    dp = np.zeros_like(p)
+    for t in range(L.shape[0]):
+        for j in range(cfg.top_k):
+            dp[t, idx[t, j]] += dg[t, j]
+    return p * (dp - (p * dp).sum(1, keepdims=True))
+
+
+def moe_unsort_rows_bwd_router(cfg, dy, y_sorted, topo, gates, logits, expert_idx):
+    dys, dg = moe_unsort_rows_bwd(cfg, dy, y_sorted, topo, gates)
+    return dys, dg, _t(_dlogits(cfg, logits, expert_idx, dg))
+
+
+def moe_router_dwr(cfg, x, dlogits, ws=None):
+    return _t(_np(x).T @ _np(dlogits))
+
+
+def moe_sort_rows_bwd_router(cfg, dx_sorted, topo, dlogits, wr):
+    return _t(_np(moe_sort_rows_bwd(cfg, dx_sorted, topo)) + _np(dlogits) @ _np(wr).T)
+
+
+def moe_ep_recv_ids(counts_all, e0, local_experts, n_rows):
+    c = counts_all.numpy()
+    ids = np.concatenate([np.repeat(np.arange(local_experts), c[q, e0:e0 + local_experts]) for q in range(c.shape[0])])
+    assert ids.size == n_rows
+    return torch.from_numpy(ids.astype(np.int32))

@@ -235,6 +235,76 @@ def test_permutation_kernels(T, h, E, k):
     np.testing.assert_allclose(f64(yb), k * S.to_f64(x), rtol=1e-2)
 
 
+@pytest.mark.parametrize("T,h,E,k", [(1000, 512, 64, 1), (777, 256, 128, 2)])
+def test_ep_router_fused_forms(T, h, E, k):
+    """Expert-parallel token-owner backward (moe_unsort_rows_bwd_router,
+    moe_sort_rows_bwd_router): the unpadded expert-order rows with the router's
+    softmax backward and dx += dlogits . Wr^T, vs the oracle."""
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(T, E, k, seed=T + 7, zipf=0.5)
+    cfg = A.make_config(T, h, E, k, 128)
+    g = torch.Generator().manual_seed(T + 1)
+    logits = torch.randn(T, E, generator=g)
+    gates = torch.rand(T, k, generator=g)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    ys = torch.randn(T * k, h, generator=g).to(torch.bfloat16)
+    dy = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    dxs = torch.randn(T * k, h, generator=g).to(torch.bfloat16)
+    topo = A.moe_topology(cfg, idx.to(d))
+    plan, _ = oracle_plan_topo(idx.numpy(), E, 128)
+    spos = np.empty(T * k, np.int64)
+    spos[plan.sorted_idx] = np.arange(T * k)
+    dys, dg, dl = A.moe_unsort_rows_bwd_router(cfg, dy.to(d), ys.to(d), topo, gates.to(d), logits.to(d), idx.to(d))
+    want_dys = np.zeros((T * k, h))
+    want_dg = np.zeros((T, k))
+    for t in range(T):
+        for j in range(k):
+            u = spos[t * k + j]
+            want_dys[u] = float(gates[t, j]) * S.to_f64(dy[t])
+            want_dg[t, j] = f64(ys[u]) @ S.to_f64(dy[t])
+    assert rel_fro(f64(dys), want_dys) < 4e-3
+    assert rel_fro(dg.cpu().double().numpy(), want_dg) < 1e-4
+    # dlogits by the oracle's softmax backward, on the GPU's own dgates
+    prob = O.softmax(logits.double().numpy())
+    dp = np.zeros((T, E))
+    dgn = dg.cpu().double().numpy()
+    for t in range(T):
+        for j in range(k):
+            dp[t, int(idx[t, j])] += dgn[t, j]
+    want_dl = prob * (dp - (prob * dp).sum(1, keepdims=True))       # b7, oracle dmoe_backward's form
+    assert rel_fro(f64(dl), want_dl) < FRO_TOL
+    dx = A.moe_sort_rows_bwd_router(cfg, dxs.to(d), topo, dl, wr.to(d))
+    want_dx = np.zeros((T, h))
+    for i in range(T * k):
+        want_dx[i // k] += f64(dxs[spos[i]])
+    want_dx += f64(dl) @ S.to_f64(wr).T
+    assert rel_fro(f64(dx), want_dx) < FRO_TOL
+    dwr = A.moe_router_dwr(cfg, x.to(d), dl)
+    assert rel_fro(dwr.cpu().double().numpy(), S.to_f64(x).T @ f64(dl)) < FRO_TOL
+
+
+@pytest.mark.parametrize("P,E,zero", [(2, 64, False), (8, 64, True), (4, 16, True), (1, 8, False)])
+def test_ep_recv_ids_bit_exact(P, E, zero):
+    """moe_ep_recv_ids vs the host plan (ep.recv_plan): arrival order
+    (source rank, local expert, token), bit-exact, empty segments included."""
+    from paper_2211_15841_b200 import ep
+    d = dev()
+    A = api()
+    rng = np.random.default_rng(P * E)
+    counts = rng.integers(0, 300, size=(P, E)).astype(np.int32)
+    if zero:
+        counts[:, ::3] = 0
+        counts[0] = 0
+    for r in range(P):
+        e0, e1 = ep.local_expert_range(r, P, E)
+        splits, want = ep.recv_plan(counts, r, P)
+        n = int(sum(splits))
+        got = A.moe_ep_recv_ids(torch.from_numpy(counts).to(d), e0, e1 - e0, n)
+        np.testing.assert_array_equal(got[:n].cpu().numpy(), want)
+
+
 # ------------------------------------------------------------------ block-sparse products
 
 def product_case(T, h, f, E, k, zipf, seed):
