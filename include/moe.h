@@ -195,6 +195,65 @@ moe_status moe_unsort_rows_bwd_router(const moe_config* cfg, const void* dy, con
 moe_status moe_sort_rows_bwd_router(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
                                     const void* dlogits_bf16, const void* wr, void* dx, void* stream);
 
+/* ---- expert parallelism over peer memory (NVLink 5 / NVSwitch; SURVEY §8(f)
+ *      NEXT-1): device-initiated dispatch / combine, no host
+ *      synchronisation. Each rank owns one window (moe_ep_window_alloc, a
+ *      cudaMalloc'd region exported with moe_ipc_get_handle and mapped by every
+ *      peer with moe_ipc_open_handle). Window layout (moe_ep_window_offset):
+ *      cumulative arrival counters, an error word, the all-gathered [P,E]
+ *      int32 histograms and four bf16 row regions: receive x / dy
+ *      [cap_rows, hidden] (rows this rank's experts get, arrival order source
+ *      rank, local expert, token) and return y / dx [owner_rows = T*k, hidden]
+ *      (rows coming back, in this rank's expert-sorted order, moe_sort_rows).
+ *      Every exchange bumps per-source arrival counters at its destinations;
+ *      `epoch` = how many exchanges of that region this rank has done (all
+ *      ranks call the same sequence, so epochs agree). A wait spins with
+ *      acquire loads and gives up after 20 s, writing 1 + region to the error
+ *      word (read it to detect a broken peer) instead of hanging. ---- */
+enum { MOE_EP_ARRIVE = 0, MOE_EP_ERROR = 1, MOE_EP_COUNTS = 2, MOE_EP_RECV_X = 3, MOE_EP_RECV_DY = 4,
+       MOE_EP_RET_Y = 5, MOE_EP_RET_DX = 6 };
+
+typedef struct {
+  int32_t nranks, rank, num_experts, hidden;  /* E % nranks == 0: rank r owns experts [r E/P, (r+1) E/P) */
+  int64_t cap_rows;                           /* receive-region rows (>= rows any step can bring) */
+  int64_t owner_rows;                         /* T_local * top_k */
+  const void* peers;                          /* DEVICE uint64 [nranks]: every rank's window base as mapped here */
+  int32_t* plan;                              /* DEVICE int32 [moe_ep_plan_ints]: counts_all [P,E], n_recv,
+                                                 offsets (written by moe_ep_exchange_counts); the last
+                                                 int mirrors the error word (0 = no timeout) */
+} moe_ep_t;
+
+size_t  moe_ep_window_bytes(int nranks, int num_experts, int64_t hidden, int64_t cap_rows, int64_t owner_rows);
+int64_t moe_ep_window_offset(int nranks, int num_experts, int64_t hidden, int64_t cap_rows, int64_t owner_rows,
+                             int which);   /* which = MOE_EP_*; -1 if unknown */
+int     moe_ep_plan_ints(int nranks, int num_experts);
+moe_status moe_ep_window_alloc(size_t bytes, void** window);   /* setup only: cudaMalloc + zero */
+moe_status moe_ep_window_free(void* window);
+moe_status moe_ipc_get_handle(const void* window, void* handle /* 64 bytes out */);
+moe_status moe_ipc_open_handle(const void* handle /* 64 bytes */, void** window);
+moe_status moe_ipc_close_handle(void* window);
+/* counts_local [E] int32 device: this rank's per-global-expert histogram
+ * (moe_topology counts). Stores it into every peer, waits for all P rows, and
+ * writes ep->plan; plan[P*E] = rows this rank receives (the device-side row
+ * count for moe_topology_rows / moe_gather_rows). One CTA. */
+moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, uint32_t epoch, void* stream);
+/* region MOE_EP_RECV_X / MOE_EP_RECV_DY: rows [T*k, hidden] bf16 in this
+ * rank's expert-sorted order go to their experts' owners' receive regions. */
+moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream);
+/* region MOE_EP_RET_Y / MOE_EP_RET_DX: received rows [n_recv, hidden] bf16
+ * (arrival order) go back to their source ranks' return regions. */
+moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream);
+/* Stream-ordered wait until every source's exchange `epoch` of `region` landed here. */
+moe_status moe_ep_wait(const moe_ep_t* ep, int region, uint32_t epoch, void* stream);
+
+/* Device-side row count variants for the receiving side of the exchange:
+ * cfg->tokens * top_k is the capacity (buffer sizes, grids); the live count is
+ * *rows_dev (device int32, <= capacity), read by the kernels. */
+moe_status moe_topology_rows(const moe_config* cfg, const int32_t* expert_idx, const int32_t* rows_dev,
+                             const moe_topology_t* topo, void* ws, void* stream);
+moe_status moe_gather_rows(const moe_config* cfg, const void* x, const moe_topology_t* topo, const int32_t* rows_dev,
+                           void* x_g, void* stream);
+
 /* Expert-parallel receive ids (DESIGN.md §7 ordering contract): rows
  * arrive ordered (source rank q, local expert l, token); ids[i] = l of arrival
  * row i, i < sum over q, l of counts_all[q*E + e0 + l]. counts_all [P,E] int32

@@ -38,6 +38,12 @@ class MoeGrads(ctypes.Structure):
     _fields_ = [("dwr", ctypes.c_void_p), ("dw1", ctypes.c_void_p), ("dw2", ctypes.c_void_p)]
 
 
+class MoeEp(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("num_experts", ctypes.c_int32),
+                ("hidden", ctypes.c_int32), ("cap_rows", ctypes.c_int64), ("owner_rows", ctypes.c_int64),
+                ("peers", ctypes.c_void_p), ("plan", ctypes.c_void_p)]
+
+
 class MoeSaved(ctypes.Structure):
     _fields_ = [("logits", ctypes.c_void_p), ("expert_idx", ctypes.c_void_p), ("gates", ctypes.c_void_p),
                 ("topo", MoeTopology), ("x_g", ctypes.c_void_p), ("act_deriv", ctypes.c_void_p),
@@ -71,6 +77,22 @@ SIGNATURES = {
     "moe_sort_rows_bwd": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_unsort_rows_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),
     "moe_sort_rows_bwd_router": (STATUS, [CFG, P, TOPO, P, P, P, P]),
+    "moe_ep_window_bytes": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64]),
+    "moe_ep_window_offset": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int]),
+    "moe_ep_plan_ints": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "moe_ep_window_alloc": (STATUS, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "moe_ep_window_free": (STATUS, [P]),
+    "moe_ipc_get_handle": (STATUS, [P, P]),
+    "moe_ipc_open_handle": (STATUS, [P, ctypes.POINTER(ctypes.c_void_p)]),
+    "moe_ipc_close_handle": (STATUS, [P]),
+    "moe_ep_exchange_counts": (STATUS, [ctypes.POINTER(MoeEp), P, ctypes.c_uint32, P]),
+    "moe_ep_dispatch": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, ctypes.c_uint32, P]),
+    "moe_ep_combine": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, ctypes.c_uint32, P]),
+    "moe_ep_wait": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, ctypes.c_uint32, P]),
+    "moe_topology_rows": (STATUS, [CFG, P, P, TOPO, P, P]),
+    "moe_gather_rows": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_ep_recv_ids": (STATUS, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P]),
     "moe_sdd": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),

@@ -1,0 +1,337 @@
+// ep_p2p.cu — expert-parallel token exchange over peer memory (NVLink 5 /
+// NVSwitch), device-initiated, no host synchronisation (SURVEY.md §8(f)
+// NEXT-1; the paper's expert parallelism P:197).
+//
+// Every rank owns one "window" (cudaMalloc'd, IPC-exported, mapped by every
+// peer): cumulative arrival counters, the all-gathered histograms and four
+// row regions. A step's exchanges are plain peer stores issued by kernels:
+//
+//   counts   each rank stores its [E] histogram row into every peer's
+//            counts[rank, :], then bumps the peer's arrival counter; one CTA
+//            waits for all P rows and derives the exchange plan on the device
+//            (rows received, chunk offsets) — no device->host copy.
+//   dispatch sender row j of the expert-ordered rows (moe_sort_rows) goes to
+//            the owner q of its expert, at q's receive offset for this source
+//            (arrival order: source rank, local expert, token — the ordering
+//            contract of DESIGN.md §7, identical to the NCCL all-to-all path).
+//   combine  receiver row i (from source s) goes back to s's return region at
+//            the position s sorted it from.
+//
+// Completion: each CTA fences its peer stores (fence.sc.sys), counts itself
+// on a local counter; the last CTA bumps every destination's arrival counter
+// for this source (release, system scope). A one-CTA wait kernel spins with
+// acquire loads until every source's counter reaches the exchange's epoch,
+// bounded by a 20 s timeout that writes 1 + region to the window's error word
+// instead of hanging the GPU. Counters are cumulative (never reset), so epochs are just
+// the per-region exchange count every rank tracks identically on the host.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace moe {
+
+constexpr int kEpRegions = 6;          // arrive counters: counts, x, dy, y, dx, (spare)
+constexpr int kEpCtas = 148;           // CTAs of every copy kernel (fixed: the completion count)
+constexpr unsigned long long kEpTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+struct WinLayout {
+  size_t arrive, done, error, counts, recv_x, recv_dy, ret_y, ret_dx, total;
+};
+
+__host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+__host__ __device__ inline WinLayout win_layout(int P, int E, long long h, long long cap, long long owner) {
+  WinLayout L;
+  size_t o = 0;
+  L.arrive = o; o = align256(o + sizeof(uint32_t) * kEpRegions * P);   // [region][source]
+  L.done = o;   o = align256(o + sizeof(uint32_t) * kEpRegions);       // local CTA completion counters
+  L.error = o;  o = align256(o + sizeof(uint32_t) * 4);
+  L.counts = o; o = align256(o + sizeof(int32_t) * (size_t)P * E);
+  L.recv_x = o; o = align256(o + 2ull * cap * h);
+  L.recv_dy = o; o = align256(o + 2ull * cap * h);
+  L.ret_y = o;  o = align256(o + 2ull * owner * h);
+  L.ret_dx = o; o = align256(o + 2ull * owner * h);
+  L.total = o;
+  return L;
+}
+
+// plan (int32, local): [0, P*E) counts_all | n_recv | recv_start[P+1] | send_dst[P] | send_src[P+1] | ret_off[P]
+// | error (mirror of the window's error word)
+__host__ __device__ inline int plan_ints(int P, int E) { return P * E + 1 + (P + 1) + P + (P + 1) + P + 1; }  // + error
+struct PlanView {
+  int32_t *counts, *n_recv, *recv_start, *send_dst, *send_src, *ret_off;
+};
+__device__ inline PlanView plan_view(int32_t* plan, int P, int E) {
+  PlanView v;
+  v.counts = plan;
+  v.n_recv = plan + P * E;
+  v.recv_start = v.n_recv + 1;
+  v.send_dst = v.recv_start + P + 1;
+  v.send_src = v.send_dst + P;
+  v.ret_off = v.send_src + P + 1;
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct EpArgs {
+  int P, rank, E, El;
+  long long h, cap, owner;
+  const uint64_t* peers;  // device [P] window bases
+  int32_t* plan;
+};
+
+__device__ inline uint8_t* peer_win(const EpArgs& a, int q) { return reinterpret_cast<uint8_t*>(a.peers[q]); }
+
+// Last-CTA completion: every CTA fences its peer stores and counts itself; the
+// CTA completing the count bumps arrive[region][rank] at every destination.
+__device__ void signal_peers(const EpArgs& a, int region, uint32_t epoch) {
+  __shared__ bool s_last;
+  __threadfence_system();  // every thread: its peer stores before the CTA's completion
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
+    uint32_t* done = reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.done) + region;
+    const uint32_t prev = atomicAdd(done, 1u);
+    s_last = prev + 1 == epoch * (uint32_t)gridDim.x;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x < a.P) {
+    __threadfence_system();
+    const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
+    uint32_t* arr = reinterpret_cast<uint32_t*>(peer_win(a, threadIdx.x) + L.arrive);
+    red_release_sys(arr + region * a.P + a.rank, 1u);
+  }
+}
+
+// Spin (acquire, system scope) until every source's counter of `region`
+// reaches epoch; timeout -> error word set, return.
+__device__ bool wait_arrivals(const EpArgs& a, int region, uint32_t epoch) {
+  const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
+  const uint32_t* arr = reinterpret_cast<const uint32_t*>(peer_win(a, a.rank) + L.arrive) + region * a.P;
+  uint32_t* err = reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.error);
+  bool ok = true;
+  if (threadIdx.x < a.P) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(arr + threadIdx.x) < epoch) {
+      if (globaltimer() - t0 > kEpTimeoutNs) {
+        atomicExch(err, 1u + region);
+        a.plan[plan_ints(a.P, a.E) - 1] = 1 + region;
+        ok = false;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  return __syncthreads_and(ok);
+}
+
+__global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_local, uint32_t epoch) {
+  const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
+  for (int i = threadIdx.x; i < a.P * a.E; i += blockDim.x) {
+    const int q = i / a.E, e = i % a.E;
+    int32_t* dst = reinterpret_cast<int32_t*>(peer_win(a, q) + L.counts) + (size_t)a.rank * a.E + e;
+    *reinterpret_cast<volatile int32_t*>(dst) = __ldg(counts_local + e);
+  }
+  signal_peers(a, 0, epoch);
+  if (!wait_arrivals(a, 0, epoch)) return;
+  // the plan, derived identically on every rank from the same [P, E] histograms
+  const volatile int32_t* cnt = reinterpret_cast<const volatile int32_t*>(peer_win(a, a.rank) + L.counts);
+  PlanView v = plan_view(a.plan, a.P, a.E);
+  for (int i = threadIdx.x; i < a.P * a.E; i += blockDim.x) v.counts[i] = cnt[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int P = a.P, E = a.E, El = a.El, r = a.rank;
+    auto chunk = [&](int s, int q) {  // rows source s sends to rank q
+      int32_t c = 0;
+      for (int e = q * El; e < (q + 1) * El; ++e) c += v.counts[s * E + e];
+      return c;
+    };
+    int32_t acc = 0;
+    for (int s = 0; s < P; ++s) {
+      v.recv_start[s] = acc;
+      acc += chunk(s, r);
+    }
+    v.recv_start[P] = acc;
+    *v.n_recv = acc;
+    int32_t so = 0;
+    for (int q = 0; q < P; ++q) {
+      int32_t d = 0;
+      for (int s = 0; s < r; ++s) d += chunk(s, q);
+      v.send_dst[q] = d;   // where my chunk lands in q's receive region
+      v.send_src[q] = so;  // where my chunk for q starts in my expert-ordered rows
+      so += chunk(r, q);
+    }
+    v.send_src[P] = so;
+    for (int s = 0; s < P; ++s) {  // where my rows from s go back in s's return region
+      int32_t o = 0;
+      for (int q = 0; q < r; ++q) o += chunk(s, q);
+      v.ret_off[s] = o;
+    }
+  }
+}
+
+// Row copy to peers. dispatch: rows [0, send_src[P]) of src by destination;
+// combine: rows [0, n_recv) of src back to their source ranks.
+template <bool COMBINE>
+__global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
+                                                      size_t region_off, uint32_t epoch) {
+  PlanView v = plan_view(a.plan, a.P, a.E);
+  const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
+  const int RV = (int)(a.h * 2 / 16);  // uint4 per row
+  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * warps + threadIdx.x / 32; j < rows; j += gridDim.x * warps) {
+    int q = 0;
+    const int32_t* starts = COMBINE ? v.recv_start : v.send_src;
+    while (q + 1 < a.P && starts[q + 1] <= j) ++q;
+    const int drow = (COMBINE ? v.ret_off[q] : v.send_dst[q]) + (j - starts[q]);
+    uint4* dst = reinterpret_cast<uint4*>(peer_win(a, q) + region_off) + (size_t)drow * RV;
+    const uint4* s = src + (size_t)j * RV;
+    for (int u = lane; u < RV; u += 32) dst[u] = __ldg(s + u);
+  }
+  signal_peers(a, region, epoch);
+}
+
+__global__ void ep_wait_kernel(EpArgs a, int region, uint32_t epoch) { wait_arrivals(a, region, epoch); }
+
+EpArgs ep_args(const moe_ep_t* ep) {
+  EpArgs a;
+  a.P = ep->nranks;
+  a.rank = ep->rank;
+  a.E = ep->num_experts;
+  a.El = ep->num_experts / ep->nranks;
+  a.h = ep->hidden;
+  a.cap = ep->cap_rows;
+  a.owner = ep->owner_rows;
+  a.peers = reinterpret_cast<const uint64_t*>(ep->peers);
+  a.plan = ep->plan;
+  return a;
+}
+
+moe_status check_ep(const moe_ep_t* ep, const char* fn) {
+  MOE_CHECK_ARG(ep && ep->peers && ep->plan, "%s: NULL ep / peers / plan", fn);
+  MOE_CHECK_ARG(ep->nranks >= 1 && ep->rank >= 0 && ep->rank < ep->nranks && ep->num_experts % ep->nranks == 0,
+                "%s: bad ranks (P=%d rank=%d E=%d)", fn, ep->nranks, ep->rank, ep->num_experts);
+  MOE_CHECK_ARG(ep->nranks <= 64 && ep->hidden % 8 == 0 && ep->cap_rows >= 0 && ep->owner_rows >= 0,
+                "%s: unsupported (P=%d <= 64, hidden %% 8 == 0)", fn, ep->nranks);
+  return MOE_OK;
+}
+
+}  // namespace moe
+
+using namespace moe;
+
+extern "C" {
+
+size_t moe_ep_window_bytes(int nranks, int num_experts, int64_t hidden, int64_t cap_rows, int64_t owner_rows) {
+  return win_layout(nranks, num_experts, hidden, cap_rows, owner_rows).total;
+}
+
+int64_t moe_ep_window_offset(int nranks, int num_experts, int64_t hidden, int64_t cap_rows, int64_t owner_rows,
+                             int which) {
+  const WinLayout L = win_layout(nranks, num_experts, hidden, cap_rows, owner_rows);
+  switch (which) {
+    case MOE_EP_ARRIVE: return (int64_t)L.arrive;
+    case MOE_EP_ERROR: return (int64_t)L.error;
+    case MOE_EP_COUNTS: return (int64_t)L.counts;
+    case MOE_EP_RECV_X: return (int64_t)L.recv_x;
+    case MOE_EP_RECV_DY: return (int64_t)L.recv_dy;
+    case MOE_EP_RET_Y: return (int64_t)L.ret_y;
+    case MOE_EP_RET_DX: return (int64_t)L.ret_dx;
+    default: return -1;
+  }
+}
+
+int moe_ep_plan_ints(int nranks, int num_experts) { return plan_ints(nranks, num_experts); }
+
+moe_status moe_ep_window_alloc(size_t bytes, void** window) {
+  MOE_CHECK_ARG(window && bytes > 0, "moe_ep_window_alloc: bad arguments");
+  cudaError_t e = cudaMalloc(window, bytes);
+  if (e == cudaSuccess) e = cudaMemset(*window, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_error(MOE_ECUDA, "moe_ep_window_alloc: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ep_window_free(void* window) {
+  cudaError_t e = cudaFree(window);
+  if (e != cudaSuccess) return set_error(MOE_ECUDA, "moe_ep_window_free: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ipc_get_handle(const void* window, void* handle) {
+  MOE_CHECK_ARG(window && handle, "moe_ipc_get_handle: NULL pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  cudaError_t e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), const_cast<void*>(window));
+  if (e != cudaSuccess) return set_error(MOE_ECUDA, "moe_ipc_get_handle: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ipc_open_handle(const void* handle, void** window) {
+  MOE_CHECK_ARG(window && handle, "moe_ipc_open_handle: NULL pointer");
+  cudaIpcMemHandle_t hnd;
+  memcpy(&hnd, handle, sizeof(hnd));
+  cudaError_t e = cudaIpcOpenMemHandle(window, hnd, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return set_error(MOE_ECUDA, "moe_ipc_open_handle: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ipc_close_handle(void* window) {
+  cudaError_t e = cudaIpcCloseMemHandle(window);
+  if (e != cudaSuccess) return set_error(MOE_ECUDA, "moe_ipc_close_handle: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, uint32_t epoch, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_exchange_counts"));
+  MOE_CHECK_ARG(counts_local && epoch > 0, "moe_ep_exchange_counts: NULL counts or epoch 0");
+  MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), 0, as_stream(stream), ep_args(ep), counts_local, epoch);
+  return MOE_OK;
+}
+
+moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_dispatch"));
+  MOE_CHECK_ARG(rows && epoch > 0 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
+                "moe_ep_dispatch: NULL rows, epoch 0 or region %d not a receive region", region);
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
+  MOE_LAUNCH("ep_dispatch", ep_copy_kernel<false>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
+             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off, epoch);
+  return MOE_OK;
+}
+
+moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_combine"));
+  MOE_CHECK_ARG(rows && epoch > 0 && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
+                "moe_ep_combine: NULL rows, epoch 0 or region %d not a return region", region);
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
+  MOE_LAUNCH("ep_combine", ep_copy_kernel<true>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
+             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off, epoch);
+  return MOE_OK;
+}
+
+moe_status moe_ep_wait(const moe_ep_t* ep, int region, uint32_t epoch, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_wait"));
+  MOE_CHECK_ARG(region >= MOE_EP_RECV_X && region <= MOE_EP_RET_DX && epoch > 0, "moe_ep_wait: bad region %d / epoch",
+                region);
+  MOE_LAUNCH("ep_wait", ep_wait_kernel, dim3(1), dim3(64), 0, as_stream(stream), ep_args(ep), region - MOE_EP_COUNTS,
+             epoch);
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -86,9 +86,14 @@ class ExpertParallelMoE:
     w2_local [E_l*f, h] of this rank's experts.
     """
 
-    def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128):
+    def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128,
+                 transport="nccl"):
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.B = backend
         self.group = group
+        self.transport = transport
+        self.win = None
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.h, self.E, self.k, self.f, self.act, self.bs = hidden, num_experts, top_k, ffn_hidden, act, block_size
@@ -134,6 +139,8 @@ class ExpertParallelMoE:
         return bool(f and f(cfg))
 
     def forward(self, x, wr, w1_local, w2_local):
+        if self.transport == "p2p":
+            return self._forward_p2p(x, wr, w1_local, w2_local)
         B = self.B
         T = x.shape[0]
         cfg_l = self._cfg(T, self.E, self.k)
@@ -174,6 +181,8 @@ class ExpertParallelMoE:
         return y, st
 
     def backward(self, st: EPState, x, dy, wr, w1_local, w2_local):
+        if self.transport == "p2p":
+            return self._backward_p2p(st, x, dy, wr, w1_local, w2_local)
         B = self.B
         cfg_l, cfg_e = st.cfg_local, st.cfg_e
         fused = self._fused_router(cfg_l)
@@ -226,6 +235,110 @@ class ExpertParallelMoE:
         return dx, dwr, dw1, dw2
 
 
+    # ------------------------------------------------------------------ peer-memory transport (NEXT-1)
+    def _windows(self, T, device):
+        """Windows sized for T local tokens: every rank can receive at most all
+        P*T*k assignments (the capacity of the receiving side's buffers)."""
+        from .ep_p2p import PeerWindows
+        owner = T * self.k
+        if self.win is None or self.win.owner != owner:
+            if self.win is not None:
+                self.win.close()
+            self.win = PeerWindows(self.group, self.E, self.h, self.world * owner, owner, device)
+        return self.win
+
+    def _expert_bufs(self, cfg_cap, device):
+        """Receive-side scratch at capacity, allocated once per shape."""
+        key = (cfg_cap.tokens, cfg_cap.num_experts)
+        c = self.__dict__.setdefault("_ebufs", {})
+        if key not in c:
+            c.clear()
+            c[key] = {"ids": torch.empty(cfg_cap.tokens, dtype=torch.int32, device=device),
+                      "y": torch.empty(cfg_cap.tokens, self.h, dtype=torch.bfloat16, device=device),
+                      "dx": torch.empty(cfg_cap.tokens, self.h, dtype=torch.bfloat16, device=device)}
+        return c[key]
+
+    def _forward_p2p(self, x, wr, w1_local, w2_local):
+        """Forward with device-initiated exchanges: nothing here waits for the
+        device; the receiving side runs at capacity with the live row count
+        read on the device (moe_topology_rows / moe_gather_rows)."""
+        B = self.B
+        T = x.shape[0]
+        W = self._windows(T, x.device)
+        cfg_l = self._cfg(T, self.E, self.k)
+        logits, idx, gates = B.moe_router(cfg_l, x, wr)
+        topo_l = self._topology(cfg_l, idx, "local")
+        x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
+        W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
+        recv_x = W.dispatch("x", x_sorted)                      # rows into the owners' windows
+        cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
+        buf = self._expert_bufs(cfg_e, x.device)
+        rows = W.n_recv()
+        ids = B.moe_ep_recv_ids(W.counts_all(), self.e0, self.El, W.cap, ids=buf["ids"])
+        topo_e = self._topology_rows(cfg_e, ids, rows)
+        x_g = B.moe_gather_rows(cfg_e, recv_x, topo_e, rows)
+        act_deriv = None
+        if self.act != 0:
+            a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
+        else:
+            a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
+        B.moe_dsd_scatter(cfg_e, a, w2_local, topo_e, None, y=buf["y"])   # DSD + un-pad (live rows only)
+        y_sorted = W.combine("y", buf["y"])                     # back to the token owners
+        y = B.moe_unsort_rows(cfg_l, y_sorted, topo_l, gates, y=torch.empty_like(x))
+        st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, None, None, x_g, act_deriv, a, y_sorted, -1)
+        return y, st
+
+    def _topology_rows(self, cfg, ids, rows):
+        cache = self.__dict__.setdefault("_topo_cache", {})
+        key = ("experts_rows", cfg.tokens, cfg.num_experts)
+        if key not in cache:
+            cache[key] = (self.B.Topology(cfg, ids.device), self.B.workspace(cfg, ids.device))
+        tp, ws = cache[key]
+        return self.B.moe_topology_rows(cfg, ids, rows, topo=tp, ws=ws)
+
+    def _backward_p2p(self, st: EPState, x, dy, wr, w1_local, w2_local):
+        B = self.B
+        W = self.win
+        cfg_l, cfg_e = st.cfg_local, st.cfg_e
+        buf = self._expert_bufs(cfg_e, dy.device)
+        rows = W.n_recv()
+        fused = self._fused_router(cfg_l)
+        side = None
+        if fused:
+            dy_sorted, dgates, dlogits = B.moe_unsort_rows_bwd_router(cfg_l, dy, st.y_sorted, st.topo_local, st.gates,
+                                                                      st.logits, st.expert_idx)
+            side = self.__dict__.setdefault("_side", torch.cuda.Stream(device=dy.device))
+            side.wait_stream(torch.cuda.current_stream(dy.device))
+            dlogits.record_stream(side)
+            ws_l = self._topo_cache["local"][3]
+            with torch.cuda.stream(side):
+                dwr = B.moe_router_dwr(cfg_l, x, dlogits, ws=ws_l)
+        else:
+            dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
+        recv_dy = W.dispatch("dy", dy_sorted)
+        dy_g = B.moe_gather_rows(cfg_e, recv_dy, st.topo_e, rows)
+        if self.act != 0:
+            dh = B.moe_sdd_deriv(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, deriv_src=st.act_deriv)
+        else:
+            dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e)
+        # every dW column / row is written by the products (zeros for experts without rows)
+        dw2 = B.moe_dsd(cfg_e, st.a, 1, dy_g, 0, st.topo_e,
+                        out=torch.empty(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device))
+        dw1 = B.moe_dds(cfg_e, st.x_g, 1, dh, 0, st.topo_e,
+                        out=torch.empty(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device))
+        B.moe_dsd_dx(cfg_e, dh, w1_local, st.topo_e, dx=buf["dx"])          # DSD^T + un-pad (live rows only)
+        dx_sorted = W.combine("dx", buf["dx"])
+        if fused:
+            dx = B.moe_sort_rows_bwd_router(cfg_l, dx_sorted, st.topo_local, dlogits, wr, dx=torch.empty_like(dy))
+            torch.cuda.current_stream(dy.device).wait_stream(side)
+            dwr.record_stream(torch.cuda.current_stream(dy.device))
+        else:
+            dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local, dx=torch.empty_like(dy))
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
+        dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
+        return dx, dwr, dw1, dw2
+
+
 # ----------------------------------------------------------------------------- bench (N > 1)
 
 def bench_ep(args, peaks, clock_sampler=None):
@@ -257,7 +370,8 @@ def bench_ep(args, peaks, clock_sampler=None):
     w2l = wts["w2"][e0 * f:e1 * f].contiguous().to(dev)
     x, dy = inp["x"].to(dev), inp["dy"].to(dev)
     del wts
-    layer = ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act)
+    transport = getattr(args, "transport", "nccl")
+    layer = ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act, transport=transport)
     l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step(xd, dyd):
@@ -314,13 +428,14 @@ def bench_ep(args, peaks, clock_sampler=None):
                "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
                "config": {"workload": shp.name, "tokens_per_rank": T, "hidden": h, "ffn_hidden": f,
-                          "num_experts": E, "top_k": k, "parallelism": f"ep{world}",
+                          "num_experts": E, "top_k": k, "parallelism": f"ep{world}", "transport": transport,
                           "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
                "gpu_launches": int(launches), "clocks": clocks, "roofline": None,
                "e2e": None if ms_e2e is None else {
                    "value": round(T * world * args.steps / (ms_e2e / 1e3), 1), "unit": "tokens/s",
                    "h2d_bytes_per_step": 2 * T * h * 2 * world, "d2h_bytes_per_step": 2 * T * h * 2 * world,
-                   "api": "ExpertParallelMoE.forward/backward over the C ABI + NCCL all_to_all"}}
+                   "api": "ExpertParallelMoE.forward/backward over the C ABI + "
+                          + ("NCCL all_to_all" if transport == "nccl" else "peer-memory dispatch / combine")}}
     dist.barrier()
     dist.destroy_process_group()
     return out

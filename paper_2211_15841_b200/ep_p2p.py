@@ -1,0 +1,126 @@
+"""Peer-memory transport for expert parallelism (
+P:197): the token dispatch / combine of ExpertParallelMoE as kernels
+that store rows straight into the owners' windows over NVLink (csrc/ep_p2p.cu,
+include/moe.h "expert parallelism over peer memory"), with the per-rank
+histograms exchanged the same way — no NCCL all-to-all and no host round
+trip, so the host enqueues a whole step without waiting for the device.
+
+Plumbing only: the window is allocated by the library (cudaMalloc), exported
+with CUDA IPC and mapped by every peer once; the process group only carries
+the 64-byte handles at setup (all_gather_object) and a barrier.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from ._lib import MoeEp, check, lib
+
+REGION = {"x": 3, "dy": 4, "y": 5, "dx": 6}   # MOE_EP_RECV_X, _RECV_DY, _RET_Y, _RET_DX
+ERROR = 1
+
+
+class RawRows:
+    """A [rows, hidden] bf16 view of window memory for the binding (which only
+    needs data_ptr / dtype / device / shape)."""
+
+    def __init__(self, ptr: int, rows: int, hidden: int, device):
+        self.ptr, self.shape, self.device, self.dtype = int(ptr), (int(rows), int(hidden)), device, torch.bfloat16
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+
+class PeerWindows:
+    """This rank's window, every peer's window mapped here, the device plan and
+    the per-region exchange epochs."""
+
+    def __init__(self, group, num_experts: int, hidden: int, cap_rows: int, owner_rows: int, device):
+        self.group = group
+        self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.E, self.h, self.cap, self.owner, self.device = num_experts, hidden, int(cap_rows), int(owner_rows), device
+        args = (self.P, self.E, self.h, self.cap, self.owner)
+        nbytes = lib.moe_ep_window_bytes(*args)
+        win = ctypes.c_void_p()
+        check("moe_ep_window_alloc", lib.moe_ep_window_alloc(nbytes, ctypes.byref(win)))
+        self.win = win.value
+        handle = (ctypes.c_char * 64)()
+        check("moe_ipc_get_handle", lib.moe_ipc_get_handle(ctypes.c_void_p(self.win), handle))
+        handles = [None] * self.P
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.mapped = []
+        ptrs = []
+        for q, hq in enumerate(handles):
+            if q == self.rank:
+                ptrs.append(self.win)
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_char * 64).from_buffer_copy(hq)
+            check("moe_ipc_open_handle", lib.moe_ipc_open_handle(buf, ctypes.byref(p)))
+            self.mapped.append(p.value)
+            ptrs.append(p.value)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.plan = torch.zeros(lib.moe_ep_plan_ints(self.P, self.E), dtype=torch.int32, device=device)
+        self.ep = MoeEp(self.P, self.rank, self.E, self.h, self.cap, self.owner, self.peers.data_ptr(),
+                        self.plan.data_ptr())
+        self.off = {n: int(lib.moe_ep_window_offset(*args, r)) for n, r in REGION.items()}
+        self.err_off = int(lib.moe_ep_window_offset(*args, ERROR))
+        self.epoch = {"counts": 0, **{n: 0 for n in REGION}}
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+
+    # ---- views
+    def counts_all(self) -> torch.Tensor:
+        return self.plan[: self.P * self.E].view(self.P, self.E)
+
+    def n_recv(self) -> torch.Tensor:
+        return self.plan[self.P * self.E: self.P * self.E + 1]
+
+    def rows(self, name: str) -> RawRows:
+        n = self.cap if name in ("x", "dy") else self.owner
+        return RawRows(self.win + self.off[name], n, self.h, self.device)
+
+    # ---- exchanges (stream-ordered on the current stream)
+    @staticmethod
+    def _s():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def exchange_counts(self, counts_local: torch.Tensor):
+        self.epoch["counts"] += 1
+        check("moe_ep_exchange_counts", lib.moe_ep_exchange_counts(ctypes.byref(self.ep),
+                                                                   ctypes.c_void_p(counts_local.data_ptr()),
+                                                                   self.epoch["counts"], self._s()))
+
+    def dispatch(self, name: str, rows: torch.Tensor):
+        """rows [T*k, h] in this rank's expert order -> owners' receive regions; waits for this rank's."""
+        self.epoch[name] += 1
+        e = self.epoch[name]
+        check("moe_ep_dispatch", lib.moe_ep_dispatch(ctypes.byref(self.ep), REGION[name],
+                                                     ctypes.c_void_p(rows.data_ptr()), e, self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], e, self._s()))
+        return self.rows(name)
+
+    def combine(self, name: str, rows):
+        """received rows [n_recv, h] -> their sources' return regions; waits for this rank's."""
+        self.epoch[name] += 1
+        e = self.epoch[name]
+        check("moe_ep_combine", lib.moe_ep_combine(ctypes.byref(self.ep), REGION[name],
+                                                   ctypes.c_void_p(rows.data_ptr()), e, self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], e, self._s()))
+        return self.rows(name)
+
+    def error_word(self) -> int:
+        """0, or 1 + the arrival region whose wait timed out (the plan's last
+        int, mirrored from the window's error word). Reads the device."""
+        return int(self.plan[-1].item())
+
+    def close(self):
+        for p in self.mapped:
+            lib.moe_ipc_close_handle(ctypes.c_void_p(p))
+        self.mapped = []
+        if self.win:
+            torch.cuda.synchronize(self.device)
+            lib.moe_ep_window_free(ctypes.c_void_p(self.win))
+            self.win = 0
