@@ -541,8 +541,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=4096)
     ap.add_argument("--ep", action="store_true", help="expert-parallel path even at one rank")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
-    ap.add_argument("--transport", default=os.environ.get("MOE_EP_TRANSPORT", "nccl"), choices=["nccl", "p2p"],
-                    help="expert-parallel token exchange: NCCL all-to-all or device-initiated peer stores")
+    ap.add_argument("--transport", default=os.environ.get("MOE_EP_TRANSPORT", "auto"), choices=["auto", "nccl", "p2p"],
+                    help="expert-parallel token exchange: device-initiated peer stores (p2p; auto = p2p with an "
+                         "NCCL fallback if peer memory is unusable) or NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

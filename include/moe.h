@@ -206,10 +206,12 @@ moe_status moe_sort_rows_bwd_router(const moe_config* cfg, const void* dx_sorted
  *      rank, local expert, token) and return y / dx [owner_rows = T*k, hidden]
  *      (rows coming back, in this rank's expert-sorted order, moe_sort_rows).
  *      Every exchange bumps per-source arrival counters at its destinations;
- *      `epoch` = how many exchanges of that region this rank has done (all
- *      ranks call the same sequence, so epochs agree). A wait spins with
- *      acquire loads and gives up after 20 s, writing 1 + region to the error
- *      word (read it to detect a broken peer) instead of hanging. ---- */
+ *      a wait spins with acquire loads until every source reached this rank's
+ *      next epoch of the region (kept in the window: calls carry no host
+ *      state, so a step can be captured in a CUDA graph; all ranks must issue
+ *      the same sequence of exchanges). A wait gives up after 20 s, writing
+ *      1 + region to the error word (mirrored in the plan's last int) instead
+ *      of hanging. ---- */
 enum { MOE_EP_ARRIVE = 0, MOE_EP_ERROR = 1, MOE_EP_COUNTS = 2, MOE_EP_RECV_X = 3, MOE_EP_RECV_DY = 4,
        MOE_EP_RET_Y = 5, MOE_EP_RET_DX = 6 };
 
@@ -236,15 +238,15 @@ moe_status moe_ipc_close_handle(void* window);
  * (moe_topology counts). Stores it into every peer, waits for all P rows, and
  * writes ep->plan; plan[P*E] = rows this rank receives (the device-side row
  * count for moe_topology_rows / moe_gather_rows). One CTA. */
-moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, uint32_t epoch, void* stream);
+moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, void* stream);
 /* region MOE_EP_RECV_X / MOE_EP_RECV_DY: rows [T*k, hidden] bf16 in this
  * rank's expert-sorted order go to their experts' owners' receive regions. */
-moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream);
+moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, void* stream);
 /* region MOE_EP_RET_Y / MOE_EP_RET_DX: received rows [n_recv, hidden] bf16
  * (arrival order) go back to their source ranks' return regions. */
-moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream);
-/* Stream-ordered wait until every source's exchange `epoch` of `region` landed here. */
-moe_status moe_ep_wait(const moe_ep_t* ep, int region, uint32_t epoch, void* stream);
+moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream);
+/* Stream-ordered wait until every source's next exchange of `region` landed here. */
+moe_status moe_ep_wait(const moe_ep_t* ep, int region, void* stream);
 
 /* Device-side row count variants for the receiving side of the exchange:
  * cfg->tokens * top_k is the capacity (buffer sizes, grids); the live count is

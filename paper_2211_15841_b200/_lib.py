@@ -87,10 +87,10 @@ SIGNATURES = {
     "moe_ipc_get_handle": (STATUS, [P, P]),
     "moe_ipc_open_handle": (STATUS, [P, ctypes.POINTER(ctypes.c_void_p)]),
     "moe_ipc_close_handle": (STATUS, [P]),
-    "moe_ep_exchange_counts": (STATUS, [ctypes.POINTER(MoeEp), P, ctypes.c_uint32, P]),
-    "moe_ep_dispatch": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, ctypes.c_uint32, P]),
-    "moe_ep_combine": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, ctypes.c_uint32, P]),
-    "moe_ep_wait": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, ctypes.c_uint32, P]),
+    "moe_ep_exchange_counts": (STATUS, [ctypes.POINTER(MoeEp), P, P]),
+    "moe_ep_dispatch": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
+    "moe_ep_combine": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
+    "moe_ep_wait": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P]),
     "moe_topology_rows": (STATUS, [CFG, P, P, TOPO, P, P]),
     "moe_gather_rows": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_ep_recv_ids": (STATUS, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P]),

@@ -18,12 +18,13 @@
 //            the position s sorted it from.
 //
 // Completion: each CTA fences its peer stores (fence.sc.sys), counts itself
-// on a local counter; the last CTA bumps every destination's arrival counter
-// for this source (release, system scope). A one-CTA wait kernel spins with
-// acquire loads until every source's counter reaches the exchange's epoch,
-// bounded by a 20 s timeout that writes 1 + region to the window's error word
-// instead of hanging the GPU. Counters are cumulative (never reset), so epochs are just
-// the per-region exchange count every rank tracks identically on the host.
+// on a local counter; the last CTA resets it and bumps every destination's
+// arrival counter for this source (release, system scope). A one-CTA wait
+// kernel spins with acquire loads until every source's counter reaches the
+// region's next epoch, then records that epoch; the wait is bounded by a 20 s
+// timeout that writes 1 + region to the window's error word instead of hanging
+// the GPU. Arrival counters are cumulative and the expected epochs live in the
+// window, so no call carries host state: a step is capturable in a CUDA graph.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -37,7 +38,7 @@ constexpr int kEpCtas = 148;           // CTAs of every copy kernel (fixed: the 
 constexpr unsigned long long kEpTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 struct WinLayout {
-  size_t arrive, done, error, counts, recv_x, recv_dy, ret_y, ret_dx, total;
+  size_t arrive, done, expect, error, counts, recv_x, recv_dy, ret_y, ret_dx, total;
 };
 
 __host__ __device__ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -47,6 +48,7 @@ __host__ __device__ inline WinLayout win_layout(int P, int E, long long h, long 
   size_t o = 0;
   L.arrive = o; o = align256(o + sizeof(uint32_t) * kEpRegions * P);   // [region][source]
   L.done = o;   o = align256(o + sizeof(uint32_t) * kEpRegions);       // local CTA completion counters
+  L.expect = o; o = align256(o + sizeof(uint32_t) * kEpRegions);       // epochs this rank has completed
   L.error = o;  o = align256(o + sizeof(uint32_t) * 4);
   L.counts = o; o = align256(o + sizeof(int32_t) * (size_t)P * E);
   L.recv_x = o; o = align256(o + 2ull * cap * h);
@@ -99,7 +101,7 @@ __device__ inline uint8_t* peer_win(const EpArgs& a, int q) { return reinterpret
 
 // Last-CTA completion: every CTA fences its peer stores and counts itself; the
 // CTA completing the count bumps arrive[region][rank] at every destination.
-__device__ void signal_peers(const EpArgs& a, int region, uint32_t epoch) {
+__device__ void signal_peers(const EpArgs& a, int region) {
   __shared__ bool s_last;
   __threadfence_system();  // every thread: its peer stores before the CTA's completion
   __syncthreads();
@@ -107,7 +109,8 @@ __device__ void signal_peers(const EpArgs& a, int region, uint32_t epoch) {
     const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
     uint32_t* done = reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.done) + region;
     const uint32_t prev = atomicAdd(done, 1u);
-    s_last = prev + 1 == epoch * (uint32_t)gridDim.x;
+    s_last = prev + 1 == (uint32_t)gridDim.x;
+    if (s_last) atomicExch(done, 0u);  // every CTA of this launch has counted: ready for the next one
   }
   __syncthreads();
   if (s_last && threadIdx.x < a.P) {
@@ -119,11 +122,14 @@ __device__ void signal_peers(const EpArgs& a, int region, uint32_t epoch) {
 }
 
 // Spin (acquire, system scope) until every source's counter of `region`
-// reaches epoch; timeout -> error word set, return.
-__device__ bool wait_arrivals(const EpArgs& a, int region, uint32_t epoch) {
+// reaches this rank's next epoch of the region; record it. Timeout -> error
+// word set, epoch not advanced, return false.
+__device__ bool wait_arrivals(const EpArgs& a, int region) {
   const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
   const uint32_t* arr = reinterpret_cast<const uint32_t*>(peer_win(a, a.rank) + L.arrive) + region * a.P;
   uint32_t* err = reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.error);
+  volatile uint32_t* expect = reinterpret_cast<volatile uint32_t*>(peer_win(a, a.rank) + L.expect) + region;
+  const uint32_t epoch = *expect + 1;  // written only by this rank's (stream-ordered) waits
   bool ok = true;
   if (threadIdx.x < a.P) {
     const unsigned long long t0 = globaltimer();
@@ -137,18 +143,20 @@ __device__ bool wait_arrivals(const EpArgs& a, int region, uint32_t epoch) {
       __nanosleep(64);
     }
   }
-  return __syncthreads_and(ok);
+  ok = __syncthreads_and(ok);
+  if (ok && threadIdx.x == 0) *expect = epoch;
+  return ok;
 }
 
-__global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_local, uint32_t epoch) {
+__global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_local) {
   const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
   for (int i = threadIdx.x; i < a.P * a.E; i += blockDim.x) {
     const int q = i / a.E, e = i % a.E;
     int32_t* dst = reinterpret_cast<int32_t*>(peer_win(a, q) + L.counts) + (size_t)a.rank * a.E + e;
     *reinterpret_cast<volatile int32_t*>(dst) = __ldg(counts_local + e);
   }
-  signal_peers(a, 0, epoch);
-  if (!wait_arrivals(a, 0, epoch)) return;
+  signal_peers(a, 0);
+  if (!wait_arrivals(a, 0)) return;
   // the plan, derived identically on every rank from the same [P, E] histograms
   const volatile int32_t* cnt = reinterpret_cast<const volatile int32_t*>(peer_win(a, a.rank) + L.counts);
   PlanView v = plan_view(a.plan, a.P, a.E);
@@ -189,7 +197,7 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
 // combine: rows [0, n_recv) of src back to their source ranks.
 template <bool COMBINE>
 __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
-                                                      size_t region_off, uint32_t epoch) {
+                                                      size_t region_off) {
   PlanView v = plan_view(a.plan, a.P, a.E);
   const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
   const int RV = (int)(a.h * 2 / 16);  // uint4 per row
@@ -203,10 +211,10 @@ __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __r
     const uint4* s = src + (size_t)j * RV;
     for (int u = lane; u < RV; u += 32) dst[u] = __ldg(s + u);
   }
-  signal_peers(a, region, epoch);
+  signal_peers(a, region);
 }
 
-__global__ void ep_wait_kernel(EpArgs a, int region, uint32_t epoch) { wait_arrivals(a, region, epoch); }
+__global__ void ep_wait_kernel(EpArgs a, int region) { wait_arrivals(a, region); }
 
 EpArgs ep_args(const moe_ep_t* ep) {
   EpArgs a;
@@ -296,41 +304,39 @@ moe_status moe_ipc_close_handle(void* window) {
   return MOE_OK;
 }
 
-moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, uint32_t epoch, void* stream) {
+moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_exchange_counts"));
-  MOE_CHECK_ARG(counts_local && epoch > 0, "moe_ep_exchange_counts: NULL counts or epoch 0");
-  MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), 0, as_stream(stream), ep_args(ep), counts_local, epoch);
+  MOE_CHECK_ARG(counts_local, "moe_ep_exchange_counts: NULL counts");
+  MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), 0, as_stream(stream), ep_args(ep), counts_local);
   return MOE_OK;
 }
 
-moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream) {
+moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_dispatch"));
-  MOE_CHECK_ARG(rows && epoch > 0 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
-                "moe_ep_dispatch: NULL rows, epoch 0 or region %d not a receive region", region);
+  MOE_CHECK_ARG(rows && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
+                "moe_ep_dispatch: NULL rows or region %d not a receive region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
   MOE_LAUNCH("ep_dispatch", ep_copy_kernel<false>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
-             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off, epoch);
+             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off);
   return MOE_OK;
 }
 
-moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, uint32_t epoch, void* stream) {
+moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_combine"));
-  MOE_CHECK_ARG(rows && epoch > 0 && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
-                "moe_ep_combine: NULL rows, epoch 0 or region %d not a return region", region);
+  MOE_CHECK_ARG(rows && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
+                "moe_ep_combine: NULL rows or region %d not a return region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
   MOE_LAUNCH("ep_combine", ep_copy_kernel<true>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
-             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off, epoch);
+             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off);
   return MOE_OK;
 }
 
-moe_status moe_ep_wait(const moe_ep_t* ep, int region, uint32_t epoch, void* stream) {
+moe_status moe_ep_wait(const moe_ep_t* ep, int region, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_wait"));
-  MOE_CHECK_ARG(region >= MOE_EP_RECV_X && region <= MOE_EP_RET_DX && epoch > 0, "moe_ep_wait: bad region %d / epoch",
-                region);
-  MOE_LAUNCH("ep_wait", ep_wait_kernel, dim3(1), dim3(64), 0, as_stream(stream), ep_args(ep), region - MOE_EP_COUNTS,
-             epoch);
+  MOE_CHECK_ARG(region >= MOE_EP_RECV_X && region <= MOE_EP_RET_DX, "moe_ep_wait: bad region %d", region);
+  MOE_LAUNCH("ep_wait", ep_wait_kernel, dim3(1), dim3(64), 0, as_stream(stream), ep_args(ep), region - MOE_EP_COUNTS);
   return MOE_OK;
 }
 

@@ -23,6 +23,7 @@ synchronisation at all.
 """
 from __future__ import annotations
 
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -180,9 +181,11 @@ class ExpertParallelMoE:
         st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, sends, recvs, x_g, act_deriv, a, y_sorted, n_recv)
         return y, st
 
-    def backward(self, st: EPState, x, dy, wr, w1_local, w2_local):
+    def backward(self, st: EPState, x, dy, wr, w1_local, w2_local, reduce_dwr=True):
+        """reduce_dwr=False leaves the router gradient rank-local (the caller
+        sums it, e.g. after replaying a captured step)."""
         if self.transport == "p2p":
-            return self._backward_p2p(st, x, dy, wr, w1_local, w2_local)
+            return self._backward_p2p(st, x, dy, wr, w1_local, w2_local, reduce_dwr)
         B = self.B
         cfg_l, cfg_e = st.cfg_local, st.cfg_e
         fused = self._fused_router(cfg_l)
@@ -231,9 +234,9 @@ class ExpertParallelMoE:
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
             dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
-        dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
+        if reduce_dwr:
+            dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
-
 
     # ------------------------------------------------------------------ peer-memory transport (NEXT-1)
     def _windows(self, T, device):
@@ -296,7 +299,7 @@ class ExpertParallelMoE:
         tp, ws = cache[key]
         return self.B.moe_topology_rows(cfg, ids, rows, topo=tp, ws=ws)
 
-    def _backward_p2p(self, st: EPState, x, dy, wr, w1_local, w2_local):
+    def _backward_p2p(self, st: EPState, x, dy, wr, w1_local, w2_local, reduce_dwr=True):
         B = self.B
         W = self.win
         cfg_l, cfg_e = st.cfg_local, st.cfg_e
@@ -335,7 +338,8 @@ class ExpertParallelMoE:
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local, dx=torch.empty_like(dy))
             dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
-        dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
+        if reduce_dwr:
+            dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
 
 
@@ -371,10 +375,69 @@ def bench_ep(args, peaks, clock_sampler=None):
     x, dy = inp["x"].to(dev), inp["dy"].to(dev)
     del wts
     transport = getattr(args, "transport", "nccl")
-    layer = ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act, transport=transport)
+    transport = "p2p" if transport == "auto" else transport
     l2 = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    note = None
+
+    def make_layer(tr):
+        return ExpertParallelMoE(A, dist.group.WORLD, h, E, k, f, act=shp.act, transport=tr)
+
+    def warm(lay, n):
+        for _ in range(n):
+            l2.zero_()
+            y_, st_ = lay.forward(x, wr, w1l, w2l)
+            lay.backward(st_, x, dy, wr, w1l, w2l)
+        torch.cuda.synchronize()
+
+    layer = make_layer(transport)
+    if transport == "p2p":   # fall back to NCCL, on every rank alike, if peer memory is unusable
+        ok = torch.ones(1, device=dev)
+        try:
+            warm(layer, args.warmup)
+            if layer.win.error_word() != 0:
+                raise RuntimeError(f"exchange wait timed out (region {layer.win.error_word() - 1})")
+        except RuntimeError as exc:
+            ok.zero_()
+            note = f"p2p unavailable ({exc}); NCCL all-to-all used"
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 0:
+            print(f"[bench] {note or 'p2p failed on a peer rank; NCCL all-to-all used'}", file=sys.stderr)
+            transport = "nccl"
+            layer = make_layer("nccl")
+    warm(layer, args.warmup)
+    launches0 = A.lib.moe_total_launch_count()
+    warm(layer, 1)
+    launches_per_step = A.lib.moe_total_launch_count() - launches0
+
+    # the p2p step has no host synchronisation: capture forward + backward in a
+    # CUDA graph (the router-gradient sum stays an eager NCCL all-reduce)
+    graph = None
+    if transport == "p2p" and not getattr(args, "no_graph", False):
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                y_, st_ = layer.forward(x, wr, w1l, w2l)
+                layer.backward(st_, x, dy, wr, w1l, w2l, reduce_dwr=False)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                g_y, g_st = layer.forward(x, wr, w1l, w2l)
+                g_dx, g_dwr, _, _ = layer.backward(g_st, x, dy, wr, w1l, w2l, reduce_dwr=False)
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 - eager launches are still correct
+            print(f"[bench] graph capture unavailable ({exc}); timing eager launches", file=sys.stderr)
+            graph = None
 
     def step(xd, dyd):
+        if graph is not None:   # captured on the static x, dy
+            if xd is not x:
+                x.copy_(xd)
+                dy.copy_(dyd)
+            graph.replay()
+            dist.all_reduce(g_dwr, op=dist.ReduceOp.SUM)
+            return g_y, g_dx
         y, st = layer.forward(xd, wr, w1l, w2l)
         dx, _, _, _ = layer.backward(st, xd, dyd, wr, w1l, w2l)
         return y, dx
@@ -395,17 +458,17 @@ def bench_ep(args, peaks, clock_sampler=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
-        l2.zero_()
+    for _ in range(2):
         step(x, dy)
     torch.cuda.synchronize()
-    launches0 = A.lib.moe_total_launch_count()
     clk = clock_sampler(dev.index) if clock_sampler else None
     if clk:
         clk.start()
     ms = timed(lambda: step(x, dy), args.steps)
     clocks = clk.stop() if clk else None
-    launches = A.lib.moe_total_launch_count() - launches0
+    launches = launches_per_step * args.steps
+    if transport == "p2p" and layer.win.error_word() != 0:
+        raise RuntimeError(f"p2p exchange wait timed out during the timed steps (region {layer.win.error_word() - 1})")
     # end to end: pinned host x, dy in; y, dx out, every step
     hx, hdy = x.cpu().pin_memory(), dy.cpu().pin_memory()
     hy = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
@@ -429,6 +492,8 @@ def bench_ep(args, peaks, clock_sampler=None):
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded inputs, random-init weights)",
                "config": {"workload": shp.name, "tokens_per_rank": T, "hidden": h, "ffn_hidden": f,
                           "num_experts": E, "top_k": k, "parallelism": f"ep{world}", "transport": transport,
+                          "launch_mode": "cuda_graph" if graph is not None else "eager",
+                          **({"transport_note": note} if note else {}),
                           "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
                "gpu_launches": int(launches), "clocks": clocks, "roofline": None,
                "e2e": None if ms_e2e is None else {

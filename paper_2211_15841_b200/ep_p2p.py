@@ -34,40 +34,58 @@ class RawRows:
 
 
 class PeerWindows:
-    """This rank's window, every peer's window mapped here, the device plan and
-    the per-region exchange epochs."""
+    """This rank's window, every peer's window mapped here and the device plan.
+    Exchange epochs live in the window (device side), so these calls are
+    graph-capturable."""
 
     def __init__(self, group, num_experts: int, hidden: int, cap_rows: int, owner_rows: int, device):
         self.group = group
         self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
         self.E, self.h, self.cap, self.owner, self.device = num_experts, hidden, int(cap_rows), int(owner_rows), device
         args = (self.P, self.E, self.h, self.cap, self.owner)
-        nbytes = lib.moe_ep_window_bytes(*args)
-        win = ctypes.c_void_p()
-        check("moe_ep_window_alloc", lib.moe_ep_window_alloc(nbytes, ctypes.byref(win)))
-        self.win = win.value
-        handle = (ctypes.c_char * 64)()
-        check("moe_ipc_get_handle", lib.moe_ipc_get_handle(ctypes.c_void_p(self.win), handle))
+        self.win, self.mapped = 0, []
+        # every rank reaches every collective below, failures included, and all
+        # ranks agree on the outcome (so a caller can fall back consistently)
+        err, handle = None, None
+        try:
+            win = ctypes.c_void_p()
+            check("moe_ep_window_alloc", lib.moe_ep_window_alloc(lib.moe_ep_window_bytes(*args), ctypes.byref(win)))
+            self.win = win.value
+            hb = (ctypes.c_char * 64)()
+            check("moe_ipc_get_handle", lib.moe_ipc_get_handle(ctypes.c_void_p(self.win), hb))
+            handle = bytes(hb)
+        except Exception as exc:  # noqa: BLE001 - reported collectively below
+            err = f"window: {exc}"
         handles = [None] * self.P
-        dist.all_gather_object(handles, bytes(handle), group=group)
-        self.mapped = []
+        dist.all_gather_object(handles, handle, group=group)
         ptrs = []
-        for q, hq in enumerate(handles):
-            if q == self.rank:
-                ptrs.append(self.win)
-                continue
-            p = ctypes.c_void_p()
-            buf = (ctypes.c_char * 64).from_buffer_copy(hq)
-            check("moe_ipc_open_handle", lib.moe_ipc_open_handle(buf, ctypes.byref(p)))
-            self.mapped.append(p.value)
-            ptrs.append(p.value)
+        if err is None:
+            try:
+                for q, hq in enumerate(handles):
+                    if q == self.rank:
+                        ptrs.append(self.win)
+                        continue
+                    if hq is None:
+                        raise RuntimeError(f"rank {q} has no window")
+                    p = ctypes.c_void_p()
+                    buf = (ctypes.c_char * 64).from_buffer_copy(hq)
+                    check("moe_ipc_open_handle", lib.moe_ipc_open_handle(buf, ctypes.byref(p)))
+                    self.mapped.append(p.value)
+                    ptrs.append(p.value)
+            except Exception as exc:  # noqa: BLE001
+                err = f"peer mapping: {exc}"
+        errs = [None] * self.P
+        dist.all_gather_object(errs, err, group=group)
+        bad = [f"rank {q}: {e}" for q, e in enumerate(errs) if e]
+        if bad:
+            self.close()
+            raise RuntimeError("peer-memory windows unavailable: " + "; ".join(bad))
         self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
         self.plan = torch.zeros(lib.moe_ep_plan_ints(self.P, self.E), dtype=torch.int32, device=device)
         self.ep = MoeEp(self.P, self.rank, self.E, self.h, self.cap, self.owner, self.peers.data_ptr(),
                         self.plan.data_ptr())
         self.off = {n: int(lib.moe_ep_window_offset(*args, r)) for n, r in REGION.items()}
         self.err_off = int(lib.moe_ep_window_offset(*args, ERROR))
-        self.epoch = {"counts": 0, **{n: 0 for n in REGION}}
         torch.cuda.synchronize(device)
         dist.barrier(group=group)
 
@@ -88,27 +106,21 @@ class PeerWindows:
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def exchange_counts(self, counts_local: torch.Tensor):
-        self.epoch["counts"] += 1
         check("moe_ep_exchange_counts", lib.moe_ep_exchange_counts(ctypes.byref(self.ep),
-                                                                   ctypes.c_void_p(counts_local.data_ptr()),
-                                                                   self.epoch["counts"], self._s()))
+                                                                   ctypes.c_void_p(counts_local.data_ptr()), self._s()))
 
     def dispatch(self, name: str, rows: torch.Tensor):
         """rows [T*k, h] in this rank's expert order -> owners' receive regions; waits for this rank's."""
-        self.epoch[name] += 1
-        e = self.epoch[name]
         check("moe_ep_dispatch", lib.moe_ep_dispatch(ctypes.byref(self.ep), REGION[name],
-                                                     ctypes.c_void_p(rows.data_ptr()), e, self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], e, self._s()))
+                                                     ctypes.c_void_p(rows.data_ptr()), self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
         return self.rows(name)
 
     def combine(self, name: str, rows):
         """received rows [n_recv, h] -> their sources' return regions; waits for this rank's."""
-        self.epoch[name] += 1
-        e = self.epoch[name]
         check("moe_ep_combine", lib.moe_ep_combine(ctypes.byref(self.ep), REGION[name],
-                                                   ctypes.c_void_p(rows.data_ptr()), e, self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], e, self._s()))
+                                                   ctypes.c_void_p(rows.data_ptr()), self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
         return self.rows(name)
 
     def error_word(self) -> int:
