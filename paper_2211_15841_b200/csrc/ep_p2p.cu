@@ -34,7 +34,7 @@
 namespace moe {
 
 constexpr int kEpRegions = 6;          // arrive counters: counts, x, dy, y, dx, (spare)
-constexpr int kEpCtas = 148;           // CTAs of every copy kernel (fixed: the completion count)
+constexpr int kEpCtas = 4 * 148;       // CTAs of every copy kernel
 constexpr unsigned long long kEpTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 struct WinLayout {
@@ -193,27 +193,6 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
   }
 }
 
-// Row copy to peers. dispatch: rows [0, send_src[P]) of src by destination;
-// combine: rows [0, n_recv) of src back to their source ranks.
-template <bool COMBINE>
-__global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
-                                                      size_t region_off) {
-  PlanView v = plan_view(a.plan, a.P, a.E);
-  const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
-  const int RV = (int)(a.h * 2 / 16);  // uint4 per row
-  const int warps = blockDim.x / 32, lane = threadIdx.x & 31;
-  for (int j = blockIdx.x * warps + threadIdx.x / 32; j < rows; j += gridDim.x * warps) {
-    int q = 0;
-    const int32_t* starts = COMBINE ? v.recv_start : v.send_src;
-    while (q + 1 < a.P && starts[q + 1] <= j) ++q;
-    const int drow = (COMBINE ? v.ret_off[q] : v.send_dst[q]) + (j - starts[q]);
-    uint4* dst = reinterpret_cast<uint4*>(peer_win(a, q) + region_off) + (size_t)drow * RV;
-    const uint4* s = src + (size_t)j * RV;
-    for (int u = lane; u < RV; u += 32) dst[u] = __ldg(s + u);
-  }
-  signal_peers(a, region);
-}
-
 __global__ void ep_wait_kernel(EpArgs a, int region) { wait_arrivals(a, region); }
 
 EpArgs ep_args(const moe_ep_t* ep) {
@@ -230,12 +209,70 @@ EpArgs ep_args(const moe_ep_t* ep) {
   return a;
 }
 
+// Row copy to peers. dispatch: rows [0, send_src[P]) of src by destination;
+// combine: rows [0, n_recv) of src back to their source ranks. Each warp moves
+// kRowsPerWarp rows per iteration (all loads, then all stores) so enough bytes
+// are in flight per SM to run at bandwidth rather than at load latency.
+constexpr int kRowsPerWarp = 4;
+template <bool COMBINE, int VEC>
+__global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
+                                                      size_t region_off) {
+  PlanView v = plan_view(a.plan, a.P, a.E);
+  const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
+  const int32_t* starts = COMBINE ? v.recv_start : v.send_src;
+  const int32_t* dbase = COMBINE ? v.ret_off : v.send_dst;
+  constexpr int RV = VEC * 32;  // uint4 per row (hidden = 256 * VEC)
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j0 = warp * kRowsPerWarp; j0 < rows; j0 += nwarps * kRowsPerWarp) {
+    uint4 val[kRowsPerWarp][VEC];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (j0 + r < rows) {
+        const uint4* sp = src + (size_t)(j0 + r) * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) val[r][u] = __ldg(sp + lane + 32 * u);
+      }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int j = j0 + r;
+      if (j < rows) {
+        int q = 0;
+        while (q + 1 < a.P && starts[q + 1] <= j) ++q;
+        uint4* dst = reinterpret_cast<uint4*>(peer_win(a, q) + region_off) + (size_t)(dbase[q] + (j - starts[q])) * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) dst[lane + 32 * u] = val[r][u];
+      }
+    }
+  }
+  signal_peers(a, region);
+}
+
+template <bool COMBINE>
+moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream) {
+  const EpArgs a = ep_args(ep);
+  const uint4* src = reinterpret_cast<const uint4*>(rows);
+  const int r = region - MOE_EP_COUNTS;
+  const dim3 grid(kEpCtas), block(256);
+  cudaStream_t s = as_stream(stream);
+  switch (ep->hidden / 256) {
+    case 1: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off); break;
+    case 2: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off); break;
+    case 3: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off); break;
+    case 4: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off); break;
+    case 6: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off); break;
+    case 8: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off); break;
+    default: return set_error(MOE_EUNSUPPORTED, "moe_ep exchange: hidden=%d must be 256 * {1,2,3,4,6,8}", ep->hidden);
+  }
+  return MOE_OK;
+}
+
 moe_status check_ep(const moe_ep_t* ep, const char* fn) {
   MOE_CHECK_ARG(ep && ep->peers && ep->plan, "%s: NULL ep / peers / plan", fn);
   MOE_CHECK_ARG(ep->nranks >= 1 && ep->rank >= 0 && ep->rank < ep->nranks && ep->num_experts % ep->nranks == 0,
                 "%s: bad ranks (P=%d rank=%d E=%d)", fn, ep->nranks, ep->rank, ep->num_experts);
-  MOE_CHECK_ARG(ep->nranks <= 64 && ep->hidden % 8 == 0 && ep->cap_rows >= 0 && ep->owner_rows >= 0,
-                "%s: unsupported (P=%d <= 64, hidden %% 8 == 0)", fn, ep->nranks);
+  MOE_CHECK_ARG(ep->nranks <= 64 && ep->hidden % 256 == 0 && ep->cap_rows >= 0 && ep->owner_rows >= 0,
+                "%s: unsupported (P=%d <= 64, hidden %% 256 == 0)", fn, ep->nranks);
   return MOE_OK;
 }
 
@@ -317,9 +354,7 @@ moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, voi
                 "moe_ep_dispatch: NULL rows or region %d not a receive region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
-  MOE_LAUNCH("ep_dispatch", ep_copy_kernel<false>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
-             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off);
-  return MOE_OK;
+  return ep_copy_launch<false>(ep, rows, region, off, stream);
 }
 
 moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream) {
@@ -328,9 +363,7 @@ moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void
                 "moe_ep_combine: NULL rows or region %d not a return region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
-  MOE_LAUNCH("ep_combine", ep_copy_kernel<true>, dim3(kEpCtas), dim3(256), 0, as_stream(stream), ep_args(ep),
-             reinterpret_cast<const uint4*>(rows), region - MOE_EP_COUNTS, off);
-  return MOE_OK;
+  return ep_copy_launch<true>(ep, rows, region, off, stream);
 }
 
 moe_status moe_ep_wait(const moe_ep_t* ep, int region, void* stream) {

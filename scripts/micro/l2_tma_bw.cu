@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(128, 1) bw_kernel(const __grid_constant__ Maps
   if (C > 1) cluster_sync();
 }
 
+#ifndef MODES_MAIN
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -184,3 +185,73 @@ int main() {
   }
   return 0;
 }
+#else
+// MODES_MAIN: distinct vs shared (G CTAs read the same box sequence) vs
+// multicast (cluster of C CTAs, each issues 1/C of the box to all): is the
+// ~98 GB/s per SM TMA delivery limit on the SM side or the L2 side?
+template <int C>
+static double run(const Maps& maps, int sms, int mode, int G, int BOX, int NS, int rows, int nboxes, int smem) {
+  cudaFuncSetAttribute(bw_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int grid = sms / C * C;
+  const int iters = (int)((1LL << 30) / ((long long)grid * BOX)) / 16 * 16;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaEvent_t a, e;
+  cudaEventCreate(&a);
+  cudaEventCreate(&e);
+  float ms = 0;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(a);
+    cudaLaunchKernelEx(&cfg, bw_kernel<C>, maps, 1, iters, nboxes, mode, G, BOX, NS, rows);
+    cudaEventRecord(e);
+    cudaEventSynchronize(e);
+    cudaEventElapsedTime(&ms, a, e);
+  }
+  const double delivered = (double)grid * iters * BOX;  // bytes landed in shared memory
+  printf("mode %d G %d C %d: %8.1f GB/s delivered to smem (%.1f GB/s per CTA) %s\n", mode, G, C, delivered / ms / 1e6,
+         delivered / ms / 1e6 / grid, cudaGetErrorString(cudaGetLastError()));
+  return delivered / ms / 1e6;
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long bytes = 32LL << 20;
+  void* src;
+  cudaMalloc(&src, bytes);
+  cudaMemset(src, 1, bytes);
+  const int rows = 128, inner = 64, BOX = rows * inner * 2;
+  const int nboxes = (int)(bytes / BOX);
+  Maps maps;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)nboxes * rows};
+  cuuint64_t strides[1] = {(cuuint64_t)inner * 2};
+  cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)rows}, es[2] = {1, 1};
+  cuTensorMapEncodeTiled(&maps.m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t box2[2] = {(cuuint32_t)inner, (cuuint32_t)(rows / 2)}, box4[2] = {(cuuint32_t)inner, (cuuint32_t)(rows / 4)};
+  Maps m2 = maps, m4 = maps;
+  cuTensorMapEncodeTiled(&m2.m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box2, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuTensorMapEncodeTiled(&m4.m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, src, dims, strides, box4, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const int ring = 128 * 1024, NS = ring / BOX, smem = ring + 1024;
+  run<1>(maps, sms, 0, 1, BOX, NS, rows, nboxes, smem);
+  run<1>(maps, sms, 1, 2, BOX, NS, rows, nboxes, smem);
+  run<1>(maps, sms, 1, 4, BOX, NS, rows, nboxes, smem);
+  run<2>(m2, sms, 2, 1, BOX, NS, rows, nboxes, smem);
+  run<4>(m4, sms, 2, 1, BOX, NS, rows, nboxes, smem);
+  return 0;
+}
+#endif
