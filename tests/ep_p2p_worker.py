@@ -7,6 +7,25 @@ import os
 import sys
 
 
+def make_global_inputs(shp, cfg, tokens):
+    """The global batch; cfg["starve"] routes no token to the experts of the
+    last rank (x[:, h-1] = 1, Wr[h-1, e] = -30 there), so that rank receives
+    zero rows and its expert gradients must come out exactly zero."""
+    from synth import inputs as S
+    import torch
+    inp = S.make_inputs(shp, seed=cfg["seed"], tokens=tokens)
+    if cfg.get("starve"):
+        E, h = shp.experts, shp.hidden
+        world = cfg["world"]
+        x = inp["x"].clone()
+        wr = inp["wr"].clone()
+        x[:, h - 1] = 1.0
+        wr[h - 1, :] = 0.0
+        wr[h - 1, E - E // world:] = -30.0
+        inp["x"], inp["wr"] = x.to(torch.bfloat16), wr.to(torch.bfloat16)
+    return inp
+
+
 def run(rank, world, port, cfg, q):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import numpy as np
@@ -22,7 +41,7 @@ def run(rank, world, port, cfg, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         shp = S.CONFIGS[cfg["shape"]]
         T = cfg["T"]
-        inp = S.make_inputs(shp, seed=cfg["seed"], tokens=T * world)     # the global batch
+        inp = make_global_inputs(shp, cfg, T * world)
         E, f = shp.experts, shp.ffn
         e0, e1 = ep.local_expert_range(rank, world, E)
         sl = slice(rank * T, (rank + 1) * T)

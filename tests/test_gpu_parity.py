@@ -722,8 +722,9 @@ def test_expert_parallel_single_rank_nccl():
 
 # ------------------------------------------------------------------ expert parallelism over peer memory
 
-def _check_ep_against_oracle(res, world, T, shp, seed):
-    inp = S.make_inputs(shp, seed=seed, tokens=T * world)
+def _check_ep_against_oracle(res, world, T, shp, cfg):
+    import ep_p2p_worker
+    inp = ep_p2p_worker.make_global_inputs(shp, cfg, T * world)
     yo, cache, go = oracle_layer(inp, shp, T * world)
     E, f = shp.experts, shp.ffn
     El = E // world
@@ -738,12 +739,17 @@ def _check_ep_against_oracle(res, world, T, shp, seed):
         assert rel_fro(y[ok], yo[sl][ok]) < FRO_TOL
         assert rel_fro(dx[ok], go["dx"][sl][ok]) < FRO_TOL
         assert rel_fro(dwr, go["dwr"]) < FRO_TOL
-        assert rel_fro(dw1, go["dw1"][:, r * El * f:(r + 1) * El * f]) < FRO_TOL
-        assert rel_fro(dw2, go["dw2"][r * El * f:(r + 1) * El * f]) < FRO_TOL
+        want1, want2 = go["dw1"][:, r * El * f:(r + 1) * El * f], go["dw2"][r * El * f:(r + 1) * El * f]
+        if not want1.any():              # a rank whose experts received nothing: exact zeros
+            assert not dw1.any() and not dw2.any()
+        else:
+            assert rel_fro(dw1, want1) < FRO_TOL
+            assert rel_fro(dw2, want2) < FRO_TOL
 
 
-@pytest.mark.parametrize("world,shape,T", [(1, "C4", 512), (2, "C4", 384), (2, "C0", 500), (4, "C1", 256)])
-def test_expert_parallel_p2p(world, shape, T):
+@pytest.mark.parametrize("world,shape,T,starve", [(1, "C4", 512, False), (2, "C4", 384, False), (2, "C0", 500, False),
+                                                  (4, "C1", 256, False), (2, "C1", 300, True)])
+def test_expert_parallel_p2p(world, shape, T, starve):
     """ExpertParallelMoE with the peer-memory transport (device-initiated
     dispatch / combine through CUDA IPC windows, device-side row counts on the
     receiving side, no host synchronisation): `world` processes share cuda:0
@@ -760,7 +766,7 @@ def test_expert_parallel_p2p(world, shape, T):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    cfg = dict(shape=shape, T=T, seed=21, steps=2)
+    cfg = dict(shape=shape, T=T, seed=21, steps=2, starve=starve, world=world)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=ep_p2p_worker.run, args=(r, world, port, cfg, q)) for r in range(world)]
@@ -777,4 +783,4 @@ def test_expert_parallel_p2p(world, shape, T):
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
-    _check_ep_against_oracle(res, world, T, S.CONFIGS[shape], 21)
+    _check_ep_against_oracle(res, world, T, S.CONFIGS[shape], cfg)
