@@ -86,39 +86,51 @@ def topk(logits: np.ndarray, k: int):
 
 @dataclass
 class Plan:
-    counts: np.ndarray          # [E] assignments per expert
+    counts: np.ndarray          # [E] assignments per expert (kept ones, with a capacity)
     bins: np.ndarray            # [E] inclusive cumsum of counts
     padded_counts: np.ndarray   # [E] counts rounded up to a multiple of bs
     padded_bins: np.ndarray     # [E] inclusive cumsum of padded_counts
-    sorted_idx: np.ndarray      # [R] flat ids i = t*k + j in expert order (stable)
-    pos: np.ndarray             # [R] padded row of flat id i
+    sorted_idx: np.ndarray      # [R_kept] kept flat ids i = t*k + j in expert order (stable)
+    pos: np.ndarray             # [R] padded row of flat id i; -1 for a dropped assignment
     Tp: int                     # total padded rows
+    dropped: np.ndarray = None  # [R] bool, assignment i dropped by the capacity (all False dropless)
 
 
-def make_plan(expert_idx: np.ndarray, num_experts: int, bs: int) -> Plan:
+def make_plan(expert_idx: np.ndarray, num_experts: int, bs: int, capacity: int | None = None) -> Plan:
     """Histogram, bins, stable expert-grouped order and padded positions.
 
     counts[e] = #{(t,j): idx[t,j] = e}; bins = inclusive cumsum (R7: grouping is
     stable by flat id t*k+j); padded_counts = ceil(counts/bs)*bs, pad rows at the
     tail of each expert's group and zero-token experts get zero rows (R8).
-    """
+
+    capacity (the token-dropping formulation the paper compares against, §2.2
+    P:112-116): each expert keeps at most `capacity`
+    assignments, the earliest in flat-id order (S:284 keep-earliest); the others
+    are dropped (pos = -1) and contribute nothing ("tokens are dropped").
+    None = dropless, the method of the paper."""
     flat = np.asarray(expert_idx, np.int64).reshape(-1)
     R = flat.size
+    order = np.argsort(flat, kind="stable")         # stable: ascending flat id within expert
+    rank_all = np.zeros(R, np.int64)
+    seen = np.zeros(num_experts, np.int64)
+    for i in order:                                  # rank of each assignment within its expert
+        rank_all[i] = seen[flat[i]]
+        seen[flat[i]] += 1
+    dropped = np.zeros(R, bool) if capacity is None else rank_all >= capacity
     counts = np.zeros(num_experts, np.int64)
-    for e in flat:                                  # histogram
-        counts[e] += 1
+    for i in range(R):                               # histogram of the kept assignments
+        if not dropped[i]:
+            counts[flat[i]] += 1
     bins = np.cumsum(counts)
     padded_counts = ((counts + bs - 1) // bs) * bs
     padded_bins = np.cumsum(padded_counts)
-    sorted_idx = np.argsort(flat, kind="stable")    # stable: ascending flat id within expert
-    pos = np.empty(R, np.int64)
-    rank = np.zeros(num_experts, np.int64)
+    sorted_idx = np.array([i for i in order if not dropped[i]], np.int64)
+    pos = np.full(R, -1, np.int64)
     for i in sorted_idx:
         e = flat[i]
-        pos[i] = (padded_bins[e] - padded_counts[e]) + rank[e]
-        rank[e] += 1
+        pos[i] = (padded_bins[e] - padded_counts[e]) + rank_all[i]
     Tp = int(padded_bins[-1]) if num_experts > 0 else 0
-    return Plan(counts, bins, padded_counts, padded_bins, sorted_idx.astype(np.int64), pos, Tp)
+    return Plan(counts, bins, padded_counts, padded_bins, sorted_idx, pos, Tp, dropped)
 
 
 def padded_gather(x: np.ndarray, plan: Plan, k: int) -> np.ndarray:
@@ -127,7 +139,8 @@ def padded_gather(x: np.ndarray, plan: Plan, k: int) -> np.ndarray:
     x = np.asarray(x, np.float64)
     xg = np.zeros((plan.Tp, x.shape[1]), np.float64)
     for i in range(plan.pos.size):
-        xg[plan.pos[i]] = x[i // k]
+        if plan.pos[i] >= 0:                        # dropped assignments are not gathered
+            xg[plan.pos[i]] = x[i // k]
     return xg
 
 
@@ -140,7 +153,8 @@ def padded_scatter(yg: np.ndarray, plan: Plan, gates: np.ndarray, T: int, k: int
     y = np.zeros((T, yg.shape[1]), np.float64)
     for t in range(T):
         for j in range(k):
-            y[t] += g[t, j] * yg[plan.pos[t * k + j]]
+            if plan.pos[t * k + j] >= 0:            # a dropped slot contributes zero
+                y[t] += g[t, j] * yg[plan.pos[t * k + j]]
     return y
 
 
@@ -388,7 +402,7 @@ class Cache:
 
 
 def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = ACT_GELU,
-                 logits: np.ndarray | None = None):
+                 logits: np.ndarray | None = None, capacity: int | None = None):
     """Fig. 5 'dmoe_forward', step by step:
     (1) indices, weights = router(x)              P:260
     (2) topology = make_topology(indices)         P:265
@@ -396,13 +410,14 @@ def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = A
     (4) x = sdd(x, w1, topology); act; dsd(x, w2) P:275-276 (+ R2 activation)
     (5) padded_scatter(x, indices) * weights
     `logits` may be given to route from a fixed score matrix (tests of the
-    routing-independent part)."""
+    routing-independent part). `capacity` selects the token-dropping
+    formulation (make_plan); None = dropless."""
     x = np.asarray(x, np.float64)
     T = x.shape[0]
     E = np.asarray(wr).shape[1]
     L = router_logits(x, wr) if logits is None else np.asarray(logits, np.float64)
     idx, gates = topk(L, top_k)
-    plan = make_plan(idx, E, bs)
+    plan = make_plan(idx, E, bs, capacity)
     topo = make_topology(plan, bs, ffn)
     xg = padded_gather(x, plan, top_k)
     h_pre = sdd(xg, w1, topo)
@@ -436,6 +451,8 @@ def dmoe_backward(cache: Cache, dy, wr, w1, w2):
     for t in range(T):
         for j in range(k):
             p = plan.pos[t * k + j]
+            if p < 0:                               # dropped: y does not depend on it, dgate = 0
+                continue
             dyg[p] = c.gates[t, j] * dy[t]
             dgates[t, j] = float(c.yg[p] @ dy[t])
     # b2
@@ -451,7 +468,8 @@ def dmoe_backward(cache: Cache, dy, wr, w1, w2):
     dx = np.zeros((T, h), np.float64)
     for t in range(T):
         for j in range(k):
-            dx[t] += dxg[plan.pos[t * k + j]]
+            if plan.pos[t * k + j] >= 0:
+                dx[t] += dxg[plan.pos[t * k + j]]
     # b7
     E = c.logits.shape[1]
     dp = np.zeros((T, E), np.float64)

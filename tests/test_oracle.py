@@ -477,3 +477,52 @@ def test_product_sweep_layout_conversion():
     want = torch.bmm(t64(x).reshape(E, T // E, h), torch.stack([t64(w1)[:, e * f:(e + 1) * f] for e in range(E)]))
     np.testing.assert_allclose(dense.numpy(), want.numpy(), atol=1e-12)
     np.testing.assert_array_equal(ps.dense_to_blocks(dense, E, T // E, f, bs).numpy(), hs)
+
+
+# ------------------------------------------------------------------ token-dropping formulation (NEXT-4)
+
+def test_capacity_plan_spec_example_keep_earliest():
+    # 8 tokens all to expert 0 of 4 experts, cf 1 -> capacity 2: tokens 2..7 dropped
+    idx = np.zeros((8, 1), np.int64)
+    C = O.expert_capacity(8, 4, 1.0)
+    assert C == 2
+    plan = O.make_plan(idx, 4, 4, capacity=C)
+    assert plan.dropped.tolist() == [False, False] + [True] * 6
+    assert plan.counts.tolist() == [2, 0, 0, 0] and plan.Tp == 4
+    assert plan.pos.tolist() == [0, 1] + [-1] * 6
+    assert plan.sorted_idx.tolist() == [0, 1]
+
+
+def test_capacity_large_enough_equals_dropless():
+    # no expert overflows -> identical to the dropless plan and layer, bit for bit
+    T, h, f, E, k = 40, 8, 8, 4, 2
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 11)
+    y0, c0 = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU)
+    y1, c1 = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU, capacity=int(c0.plan.counts.max()))
+    np.testing.assert_array_equal(c0.plan.pos, c1.plan.pos)
+    np.testing.assert_array_equal(y0, y1)
+    g0, g1 = O.dmoe_backward(c0, dy, wr, w1, w2), O.dmoe_backward(c1, dy, wr, w1, w2)
+    for n in ("dx", "dwr", "dw1", "dw2"):
+        np.testing.assert_array_equal(g0[n], g1[n])
+
+
+@pytest.mark.parametrize("T,h,f,E,k,cf", [(32, 6, 8, 4, 1, 1.0), (30, 4, 8, 4, 2, 1.5), (24, 8, 4, 3, 1, 0.5)])
+def test_capacity_layer_equals_batched_dropping_moe_and_autograd(T, h, f, E, k, cf):
+    """The block-sparse layer with a capacity (make_plan keep-earliest, pos = -1
+    for dropped slots) against formulation (ii), the batched-matmul token-dropping
+    MoE (Fig. 3A), forward and — through torch autograd of (ii) —
+    every gradient."""
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 13)
+    C = O.expert_capacity(T, E, cf)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU, capacity=C)
+    assert cache.plan.dropped.any()                      # the case really drops
+    tx, twr, tw1, tw2 = (t64(a).requires_grad_(True) for a in (x, wr, w1, w2))
+    yt, kept = dropping_moe_cf(tx, twr, tw1, tw2, k, f, O.ACT_GELU, cf)
+    assert kept == int((~cache.plan.dropped).sum())
+    np.testing.assert_allclose(y, yt.detach().numpy(), atol=1e-10)
+    (yt * t64(dy)).sum().backward()
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    np.testing.assert_allclose(g["dx"], tx.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
