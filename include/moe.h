@@ -65,7 +65,12 @@ typedef struct {
   int64_t ffn_hidden;
   int64_t block_size;
   int32_t act;      /* moe_act */
-  int32_t reserved; /* must be 0 */
+  int32_t capacity; /* 0: dropless (the paper's method). > 0: the token-dropping
+                       formulation it is compared against (§2.2): each
+                       expert keeps at most `capacity` assignments, the earliest
+                       by flat id t*k+j; the others are dropped (pos = -1,
+                       sorted_pos = -1) and contribute nothing to y, dx or the
+                       gradients (their dgates are 0). See moe_expert_capacity. */
 } moe_config;
 
 /* ---- configuration and size queries (host only, no CUDA calls) ---------- */
@@ -80,6 +85,10 @@ moe_status moe_check_config(const moe_config* cfg);
 /* Worst-case padded rows: Tp = sum_e bs*ceil(c_e/bs) <= bs*floor((R + min(E,R)*(bs-1))/bs),
  * R = T*k (P:297 padding to a multiple of the block size). */
 int64_t moe_max_padded_rows(const moe_config* cfg);
+
+/* Capacity of the token-dropping formulation (§2.2):
+ * ceil(tokens * capacity_factor / num_experts); 0 if capacity_factor <= 0. */
+int64_t moe_expert_capacity(int64_t tokens, int64_t num_experts, double capacity_factor);
 
 /* Worst-case nonzero blocks: max_padded_rows/bs * f/bs (Fig. 3C). */
 int64_t moe_max_nnz_blocks(const moe_config* cfg);

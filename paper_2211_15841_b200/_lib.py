@@ -18,7 +18,7 @@ c_float_p = ctypes.POINTER(ctypes.c_float)
 class MoeConfig(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int64), ("num_experts", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("ffn_hidden", ctypes.c_int64), ("block_size", ctypes.c_int64),
-                ("act", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("act", ctypes.c_int32), ("capacity", ctypes.c_int32)]
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",
@@ -61,6 +61,7 @@ SIGNATURES = {
     "moe_check_config": (STATUS, [CFG]),
     "moe_max_padded_rows": (ctypes.c_int64, [CFG]),
     "moe_max_nnz_blocks": (ctypes.c_int64, [CFG]),
+    "moe_expert_capacity": (ctypes.c_int64, [ctypes.c_int64, ctypes.c_int64, ctypes.c_double]),
     "moe_workspace_bytes": (ctypes.c_size_t, [CFG]),
     "moe_device_sm_count": (ctypes.c_int, []),
     "moe_workspace_offset": (ctypes.c_size_t, [CFG, ctypes.c_int]),

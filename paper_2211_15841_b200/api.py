@@ -14,9 +14,17 @@ from ._lib import (MoeConfig, MoeGrads, MoeSaved, MoeTopology, MoeWeights, TOPO_
 ACT_IDENTITY, ACT_GELU, ACT_RELU = 0, 1, 2
 
 
-def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU) -> MoeConfig:
+def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU,
+                capacity=0) -> MoeConfig:
+    """capacity = 0: dropless (the method). > 0: the token-dropping formulation
+    with that many assignments kept per expert (moe_expert_capacity)."""
     return MoeConfig(int(tokens), int(hidden), int(num_experts), int(top_k), int(ffn_hidden), int(block_size),
-                     int(act), 0)
+                     int(act), int(capacity))
+
+
+def moe_expert_capacity(tokens, num_experts, capacity_factor) -> int:
+    """ceil(tokens * capacity_factor / num_experts) (§2.2)."""
+    return int(lib.moe_expert_capacity(int(tokens), int(num_experts), float(capacity_factor)))
 
 
 def cfg_replace(cfg: MoeConfig, **kw) -> MoeConfig:

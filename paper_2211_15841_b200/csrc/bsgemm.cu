@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       for (int i = 0; i < (MODE == DENSE ? NCHUNK / NG : 1); ++i) {
         const uint4* src = reinterpret_cast<const uint4*>(rowp + (grp + i * NG) * EPI_COLS);
 #pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) dst[i][q2] = __ldg(src + q2);
+        for (int q2 = 0; q2 < 4; ++q2) dst[i][q2] = m >= 0 ? __ldg(src + q2) : make_uint4(0u, 0u, 0u, 0u);
       }
     };
     int tile_i = -1;
@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               const long long col0 = (long long)t.v * BN + c * EPI_COLS;
               for (int j = 1; j < (p.addend_map ? p.addend_k : 1); ++j) {
                 const int m = __ldg(p.addend_map + (long long)trow * p.addend_k + j);
+                if (m < 0) continue;  // slot dropped by a capacity
                 const uint4* src = reinterpret_cast<const uint4*>(p.addend + (long long)m * p.ld_add + col0);
 #pragma unroll
                 for (int q2 = 0; q2 < 4; ++q2) {
@@ -1168,8 +1169,8 @@ moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, con
   MOE_CHECK_ARG(dh && w1 && dx, "moe_dsd_dx: NULL pointer");
   MOE_CHECK_ARG((dlogits_bf16 == nullptr) == (wr == nullptr), "moe_dsd_dx: dlogits and wr come together");
   const bool router_term = dlogits_bf16 != nullptr;
-  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && cfg->hidden % 256 == 0 && !use_pair_rows() &&
-      (!router_term || (cfg->num_experts % 64 == 0 && cfg->num_experts <= 256))) {
+  if (cfg && cfg->top_k == 1 && cfg->capacity == 0 && cfg->block_size == 128 && cfg->hidden % 256 == 0 &&
+      !use_pair_rows() && (!router_term || (cfg->num_experts % 64 == 0 && cfg->num_experts <= 256))) {
     if (router_term) return dsd_launch(cfg, dh, 0, w1, 1, topo, dx, nullptr, dx, stream, dlogits_bf16, wr);
     MOE_CHECK_ARG(dx_g, "moe_dsd_dx: the un-permutation-only form needs the dx_g buffer");
     return dsd_launch(cfg, dh, 0, w1, 1, topo, dx_g, nullptr, dx, stream);  // dX_g kept, rows also to dx
@@ -1184,7 +1185,8 @@ moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, con
 moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
                            const float* gates, void* y_g, void* y, void* stream) {
   MOE_CHECK_ARG(y, "moe_dsd_scatter: NULL y");  // gates may be NULL: unit weights (un-permutation only)
-  if (cfg && cfg->top_k == 1 && cfg->block_size == 128 && !use_pair_rows())
+  // the fused form writes y only for tokens that own a padded row: dropless top-1 only
+  if (cfg && cfg->top_k == 1 && cfg->capacity == 0 && cfg->block_size == 128 && !use_pair_rows())
     return dsd_launch(cfg, s, 0, b, 0, topo, y_g, gates, y, stream);
   MOE_TRY(moe_dsd(cfg, s, 0, b, 0, topo, y_g, stream));  // k > 1: slots are summed by the combine kernel
   return moe_scatter(cfg, y_g, topo, gates, y, stream);

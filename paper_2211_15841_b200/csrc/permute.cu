@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restri
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       const int d = __shfl_sync(0xffffffffu, midx, r);
-      if (base + r < R) {
+      if (base + r < R && d >= 0) {  // d < 0: assignment dropped by a capacity
         uint4* o = dst + (size_t)d * RV;
 #pragma unroll
         for (int u = 0; u < VEC; ++u) o[lane + 32 * u] = v[r][u];
@@ -126,10 +126,13 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint4* __restrict__ 
 #pragma unroll
       for (int r = 0; r < ROWS; ++r) {
         const int m = __shfl_sync(0xffffffffu, midx, r);
-        if (base + r < T) {
+        if (base + r < T && m >= 0) {
           const uint4* s = rows + (size_t)m * RV;
 #pragma unroll
           for (int u = 0; u < VEC; ++u) v[r][u] = __ldg(s + lane + 32 * u);
+        } else {  // a dropped slot (capacity) contributes zero
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) v[r][u] = make_uint4(0u, 0u, 0u, 0u);
         }
       }
 #pragma unroll
@@ -212,10 +215,13 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
       for (int r = 0; r < TPW; ++r) {
         m[r] = __shfl_sync(0xffffffffu, midx, r * k + j);
         g[r] = __shfl_sync(0xffffffffu, gl, r * k + j);
-        if (want_dg && base + r < T) {
+        if (want_dg && base + r < T && m[r] >= 0) {
           const uint4* ys = y_rows + (size_t)m[r] * RV;
 #pragma unroll
           for (int u = 0; u < VEC; ++u) yv[r][u] = __ldg(ys + lane + 32 * u);
+        } else {
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) yv[r][u] = make_uint4(0u, 0u, 0u, 0u);
         }
       }
 #pragma unroll
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q) f[q] *= g[r];
-          o[lane + 32 * u] = f32_to_bf16x8(f);
+          if (m[r] >= 0) o[lane + 32 * u] = f32_to_bf16x8(f);  // dropped slot: no row, dgate 0
         }
         if (want_dg) {
 #pragma unroll

@@ -1,5 +1,6 @@
 // status.cu — error reporting, config validation and size queries of the C ABI
 // (include/moe.h). Host only; no CUDA calls except the SM-count query.
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -129,7 +130,7 @@ moe_status moe_check_config(const moe_config* cfg) {
                      (long long)cfg->ffn_hidden, (long long)cfg->block_size);
   if (cfg->act < MOE_ACT_IDENTITY || cfg->act > MOE_ACT_RELU)
     return set_error(MOE_EINVAL, "act=%d is not a moe_act", cfg->act);
-  if (cfg->reserved != 0) return set_error(MOE_EINVAL, "reserved field must be 0");
+  if (cfg->capacity < 0) return set_error(MOE_EINVAL, "capacity=%d must be >= 0 (0 = dropless)", cfg->capacity);
   if (cfg->block_size != 128)
     return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
                      (long long)cfg->block_size);
@@ -141,6 +142,11 @@ moe_status moe_check_config(const moe_config* cfg) {
   if (cfg->tokens * cfg->top_k > (int64_t)1 << 30)
     return set_error(MOE_EUNSUPPORTED, "tokens*top_k too large for int32 indices");
   return MOE_OK;
+}
+
+int64_t moe_expert_capacity(int64_t tokens, int64_t num_experts, double capacity_factor) {
+  if (tokens < 1 || num_experts < 1 || !(capacity_factor > 0)) return 0;
+  return (int64_t)ceil((double)tokens * capacity_factor / (double)num_experts - 1e-12);
 }
 
 int64_t moe_max_padded_rows(const moe_config* cfg) {

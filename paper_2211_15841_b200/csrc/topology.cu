@@ -47,7 +47,8 @@ __global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, 
 __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs,
                                                                int F, int n_chunks,
                                                                const int32_t* __restrict__ chunk_counts,
-                                                               moe_topology_t topo, const int32_t* __restrict__ R_dev) {
+                                                               moe_topology_t topo, const int32_t* __restrict__ R_dev,
+                                                               int capacity) {
   pdl_trigger();
   pdl_wait();
   if (R_dev) R = min(R, __ldg(R_dev));
@@ -75,7 +76,7 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     base = __reduce_max_sync(0xffffffffu, (unsigned)base);  // the one lane holding it (others 0)
     if (lane_id == 0) {
       s_base[e] = base;
-      s_cnt[e] = run;
+      s_cnt[e] = capacity > 0 ? min(run, capacity) : run;    // kept assignments (token dropping)
     }
   }
   __syncthreads();
@@ -165,7 +166,12 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     }
     __syncthreads();
     if (valid) {
-      const int rank = s_base[e] + s_dyn[warp * E + e] + rank_w;
+      const int rank = s_base[e] + s_dyn[warp * E + e] + rank_w;  // within expert e, by flat id
+      if (capacity > 0 && rank >= capacity) {  // dropped (keep-earliest)
+        topo.sorted_pos[i] = -1;
+        topo.pos[i] = -1;
+        return;
+      }
       const int u = s_start[e] + rank;
       const int p = s_pstart[e] + rank;
       topo.sorted_idx[u] = i;
@@ -258,7 +264,7 @@ static moe_status topology_impl(const moe_config* cfg, const int32_t* expert_idx
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
-             E, bs, F, n_chunks, chunk_counts, *topo, rows_dev);
+             E, bs, F, n_chunks, chunk_counts, *topo, rows_dev, (int)cfg->capacity);
   return MOE_OK;
 }
 

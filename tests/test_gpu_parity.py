@@ -784,3 +784,82 @@ def test_expert_parallel_p2p(world, shape, T, starve):
             if p.is_alive():
                 p.kill()
     _check_ep_against_oracle(res, world, T, S.CONFIGS[shape], cfg)
+
+
+# ------------------------------------------------------------------ token-dropping formulation (NEXT-4)
+
+@pytest.mark.parametrize("T,E,k,f,zipf,cf", [(1000, 4, 1, 512, 1.0, 1.0), (8192, 64, 2, 1024, 0.8, 1.5),
+                                             (5000, 64, 1, 256, 1.5, 0.5), (777, 16, 3, 128, 0.0, 1.0),
+                                             (4096, 64, 1, 256, 0.0, 64.0)])
+def test_topology_capacity_bit_exact(T, E, k, f, zipf, cf):
+    """moe_topology with cfg.capacity (keep-earliest by flat id): kept
+    counts, bins, positions (-1 = dropped), sorted order and every BCSR / COO /
+    transpose index bit-exact against the oracle's capacity plan."""
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(T, E, k, seed=T + 3, zipf=zipf)
+    C = A.moe_expert_capacity(T, E, cf)
+    assert C == O.expert_capacity(T, E, cf)
+    cfg = A.make_config(T, 256, E, k, f, capacity=C)
+    tg = A.moe_topology(cfg, idx.to(d))
+    plan = O.make_plan(idx.numpy(), E, 128, capacity=C)
+    topo = O.make_topology_closed_form(plan, 128, f)
+    R, Rk = T * k, plan.sorted_idx.size
+    Tp, nnz = tg.sizes()
+    assert Tp == plan.Tp and nnz == topo.nnz
+    g = {n: v.cpu().numpy() for n, v in tg.t.items()}
+    np.testing.assert_array_equal(g["counts"], plan.counts)
+    np.testing.assert_array_equal(g["bins"], plan.bins)
+    np.testing.assert_array_equal(g["padded_bins"], plan.padded_bins)
+    np.testing.assert_array_equal(g["pos"][:R], plan.pos)
+    np.testing.assert_array_equal(g["sorted_idx"][:Rk], plan.sorted_idx)
+    spos = np.full(R, -1, np.int64)
+    spos[plan.sorted_idx] = np.arange(Rk)
+    np.testing.assert_array_equal(g["sorted_pos"][:R], spos)
+    src = np.full(Tp, -1, np.int64)
+    kept = plan.pos >= 0
+    src[plan.pos[kept]] = np.nonzero(kept)[0]
+    np.testing.assert_array_equal(g["row_src"][:Tp], src)
+    np.testing.assert_array_equal(g["row_offsets"][:Tp // 128 + 1], topo.row_offsets)
+    np.testing.assert_array_equal(g["col_indices"][:nnz], topo.col_indices)
+    np.testing.assert_array_equal(g["t_col_offsets"], topo.t_col_offsets)
+    np.testing.assert_array_equal(g["t_block_offsets"][:nnz], topo.t_block_offsets)
+    if cf >= E:
+        assert not plan.dropped.any()
+
+
+CAPACITY_CASES = [("C0-cf1", 1024, 1, S.CONFIGS["C0"], 1.0), ("C0-k2-cf1.5", 1000, 2, S.CONFIGS["C0"].replace(top_k=2), 1.5),
+                  ("C2-skew-cf1", 4096, 1, S.CONFIGS["C2"], 1.0), ("C4-cf1", 2048, 2, S.CONFIGS["C4"], 1.0)]
+
+
+@pytest.mark.parametrize("name,T,k,shp,cf", CAPACITY_CASES)
+def test_layer_capacity_forward_backward(name, T, k, shp, cf):
+    """moe_forward / moe_backward in the token-dropping formulation (cfg.capacity
+    > 0) against the oracle: dropped slots contribute nothing, fully
+    dropped tokens get y = 0 and only the router term in dx."""
+    d = dev()
+    A = api()
+    inp = S.make_inputs(shp, seed=4, tokens=T)
+    C = A.moe_expert_capacity(T, shp.experts, cf)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, capacity=C)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    # the oracle routes from the GPU's fp32 logits (R6), so both drop the same slots
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act,
+                               logits=saved.logits.cpu().double().numpy(), capacity=C)
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
+    np.testing.assert_array_equal(saved.expert_idx.cpu().numpy(), cache.expert_idx)
+    assert cache.plan.dropped.any(), "case must drop"
+    np.testing.assert_array_equal(saved.topo["pos"][:T * shp.top_k].cpu().numpy(), cache.plan.pos)
+    gone = cache.plan.dropped.reshape(T, shp.top_k).all(axis=1)
+    if gone.any():
+        assert not f64(y)[gone].any()                      # fully dropped tokens: exact zero rows
+    assert rel_fro(f64(y), yo) < FRO_TOL
+    assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+    assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
