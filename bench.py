@@ -221,7 +221,8 @@ def run_ours_single(args, peaks):
     shp = S.CONFIGS[args.config]
     T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
     inp = S.make_inputs(shp, seed=0)
-    cfg = A.make_config(T, h, E, k, f, act=shp.act)
+    cap = A.moe_expert_capacity(T, E, args.capacity_factor) if args.capacity_factor > 0 else 0
+    cfg = A.make_config(T, h, E, k, f, act=shp.act, capacity=cap)   # capacity 0: dropless (the headline)
     stream = torch.cuda.current_stream()
     x = inp["x"].to(dev)
     dy = inp["dy"].to(dev)
@@ -383,6 +384,9 @@ def run_ours_single(args, peaks):
                    "block_size": 128, "act": "gelu_tanh", "routing": shp.routing, "parallelism": "ep1",
                    "padded_rows": Tp, "nnz_blocks": nnz,
                    "expert_load_max_over_mean": round(float(counts.max() / counts.mean()), 3),
+                   **({"formulation": "token-dropping", "capacity_factor": args.capacity_factor, "capacity": cap,
+                       "dropped_fraction": round(1.0 - float(counts.sum()) / (T * k), 4)} if cap else
+                      {"formulation": "dropless"}),
                    "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
         "roofline": roof,
         "gemm": gemm,
@@ -540,6 +544,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-tokens", type=int, default=4096)
     ap.add_argument("--ep", action="store_true", help="expert-parallel path even at one rank")
+    ap.add_argument("--capacity-factor", type=float, default=0.0,
+                    help="> 0: time the token-dropping formulation (P:112-116) with this capacity factor "
+                         "instead of the dropless layer (context only; the headline is dropless)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--transport", default=os.environ.get("MOE_EP_TRANSPORT", "auto"), choices=["auto", "nccl", "p2p"],
                     help="expert-parallel token exchange: device-initiated peer stores (p2p; auto = p2p with an "

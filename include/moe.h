@@ -146,7 +146,11 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
 /* Topology + permutation plan from expert_idx [T*k].
  * Writes every array of *topo (caller-allocated, sized by the max queries)
  * and topo->sizes = {Tp, nnz}. Integer outputs are bit-exact (closed form of
- * the block-diagonal pattern). ws: moe_workspace_bytes. */
+ * the block-diagonal pattern). ws: moe_workspace_bytes.
+ * With cfg->capacity > 0 (token-dropping formulation) counts are
+ * the kept assignments per expert (at most capacity, the earliest by flat id),
+ * dropped assignments get pos = sorted_pos = -1 and appear in no other array;
+ * every later entry point skips them. */
 moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
                         void* ws, void* stream);
 
