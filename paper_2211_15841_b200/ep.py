@@ -360,9 +360,19 @@ def bench_ep(args, peaks, clock_sampler=None):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29517")
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # test hooks (not used by the driver): MOE_EP_SAME_DEVICE=1 puts every rank
+    # on cuda:0 and MOE_EP_BACKEND=gloo replaces NCCL for the process group, so
+    # the N > 1 bench flow (windows, graphs, e2e, max over ranks) can be run on
+    # a one-GPU box; numbers from such a run are not measurements
+    if os.environ.get("MOE_EP_SAME_DEVICE") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl", device_id=dev)
+    backend = os.environ.get("MOE_EP_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
     rank, world = dist.get_rank(), dist.get_world_size()
     shp = S.CONFIGS[args.config]
     T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k

@@ -863,3 +863,31 @@ def test_layer_capacity_forward_backward(name, T, k, shp, cf):
     assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
     assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
     assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
+
+
+def test_bench_ep_multi_rank_flow():
+    """The N > 1 bench path end to end (torchrun, peer-memory windows, captured
+    graphs, pipelined e2e, max over ranks) with 2 ranks sharing cuda:0 through
+    the test hooks (gloo process group); checks the JSON contract, not speed."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    dev()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, MOE_EP_SAME_DEVICE="1", MOE_EP_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+                          "--steps", "2", "--warmup", "3"], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout            # one JSON line on stdout, from rank 0
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "ep2" and d["value"] > 0
+    assert d["config"]["transport"] == "p2p" and d["config"]["launch_mode"] == "cuda_graph"
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
