@@ -55,14 +55,16 @@ def softmax(logits: np.ndarray) -> np.ndarray:
     return e / e.sum(axis=1, keepdims=True)
 
 
-def topk(logits: np.ndarray, k: int):
+def topk(logits: np.ndarray, k: int, renormalize: bool = False):
     """Greedy top-k (P:98 'greedily selecting the top_k scoring experts').
 
     R6: selection is made on the logits (softmax is monotone, so this is the
     same set as selecting on the probabilities in exact arithmetic); slots are
     in descending score order; exact ties go to the lower expert index.
     Gates are the softmax probabilities of the chosen experts, not
-    renormalised (R4, P:96 'probabilities for each assignment').
+    renormalised (R4, P:96 'probabilities for each assignment'); with
+    `renormalize` each token's k gates are divided by
+    their sum.
     Returns (expert_idx [T,k] int32, gates [T,k] float64).
     """
     L = np.asarray(logits, np.float64)
@@ -76,6 +78,8 @@ def topk(logits: np.ndarray, k: int):
         idx[t] = order[:k]
     p = softmax(L)
     gates = np.take_along_axis(p, idx.astype(np.int64), axis=1)
+    if renormalize:
+        gates = gates / gates.sum(axis=1, keepdims=True)
     return idx, gates
 
 
@@ -399,10 +403,11 @@ class Cache:
     yg: np.ndarray
     k: int
     act: int
+    renormalize: bool = False
 
 
 def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = ACT_GELU,
-                 logits: np.ndarray | None = None, capacity: int | None = None):
+                 logits: np.ndarray | None = None, capacity: int | None = None, renormalize: bool = False):
     """Fig. 5 'dmoe_forward', step by step:
     (1) indices, weights = router(x)              P:260
     (2) topology = make_topology(indices)         P:265
@@ -416,7 +421,7 @@ def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = A
     T = x.shape[0]
     E = np.asarray(wr).shape[1]
     L = router_logits(x, wr) if logits is None else np.asarray(logits, np.float64)
-    idx, gates = topk(L, top_k)
+    idx, gates = topk(L, top_k, renormalize)
     plan = make_plan(idx, E, bs, capacity)
     topo = make_topology(plan, bs, ffn)
     xg = padded_gather(x, plan, top_k)
@@ -424,7 +429,7 @@ def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = A
     a = act(act_kind, h_pre)
     yg = dsd(a, w2, topo)
     y = padded_scatter(yg, plan, gates, T, top_k)
-    cache = Cache(x, L, softmax(L), idx, gates, plan, topo, xg, h_pre, a, yg, top_k, act_kind)
+    cache = Cache(x, L, softmax(L), idx, gates, plan, topo, xg, h_pre, a, yg, top_k, act_kind, renormalize)
     return y, cache
 
 
@@ -473,10 +478,17 @@ def dmoe_backward(cache: Cache, dy, wr, w1, w2):
     # b7
     E = c.logits.shape[1]
     dp = np.zeros((T, E), np.float64)
-    for t in range(T):
-        for j in range(k):
-            dp[t, c.expert_idx[t, j]] += dgates[t, j]
     p = c.probs
+    for t in range(T):
+        if c.renormalize:
+            # g_j = p_j / S, S = sum_i p_i over the chosen: dL/dp_j = (dg_j - sum_i dg_i g_i) / S
+            S = sum(p[t, c.expert_idx[t, i]] for i in range(k))
+            gd = sum(dgates[t, i] * c.gates[t, i] for i in range(k))
+            for j in range(k):
+                dp[t, c.expert_idx[t, j]] += (dgates[t, j] - gd) / S
+        else:
+            for j in range(k):
+                dp[t, c.expert_idx[t, j]] += dgates[t, j]
     dlogits = p * (dp - (p * dp).sum(axis=1, keepdims=True))
     dwr = c.x.T @ dlogits
     dx = dx + dlogits @ np.asarray(wr, np.float64).T

@@ -526,3 +526,46 @@ def test_capacity_layer_equals_batched_dropping_moe_and_autograd(T, h, f, E, k, 
     np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
+
+
+# ------------------------------------------------------------------ top-k gate renormalisation (NEXT-4)
+
+def test_renormalized_gates_invariants():
+    # gates in (0, 1]; k = E with renormalisation -> each token's gates sum to 1; k = 1 -> gate 1
+    rng = np.random.default_rng(5)
+    L = rng.normal(size=(50, 6))
+    _, g = O.topk(L, 6, renormalize=True)
+    np.testing.assert_allclose(g.sum(axis=1), 1.0, atol=1e-12)
+    _, g1 = O.topk(L, 1, renormalize=True)
+    np.testing.assert_array_equal(g1, np.ones((50, 1)))
+    idx, g3 = O.topk(L, 3, renormalize=True)
+    _, raw = O.topk(L, 3)
+    np.testing.assert_allclose(g3, raw / raw.sum(axis=1, keepdims=True), atol=1e-15)
+    assert (g3 > 0).all() and (g3 <= 1).all()
+
+
+@pytest.mark.parametrize("T,h,f,E,k", [(20, 6, 8, 4, 2), (17, 4, 4, 5, 3), (12, 5, 8, 3, 1)])
+def test_renormalized_layer_backward_vs_autograd(T, h, f, E, k):
+    """Formulation (i) with renormalised gates (every expert on every token,
+    masked, weight p_e / sum of the chosen p) under torch autograd against the
+    oracle layer with renormalize=True, forward and every gradient."""
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 17)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU, renormalize=True)
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    tx, twr, tw1, tw2 = (t64(a).requires_grad_(True) for a in (x, wr, w1, w2))
+    L = tx @ twr
+    p = torch.softmax(L, dim=1)
+    idx = torch.topk(L, k, dim=1).indices
+    sel = torch.zeros_like(p).scatter(1, idx, 1.0)
+    wsel = p * sel
+    wsel = wsel / wsel.sum(dim=1, keepdim=True)
+    yt = torch.zeros_like(tx)
+    for e in range(E):
+        ye = torch_act(O.ACT_GELU, tx @ tw1[:, e * f:(e + 1) * f]) @ tw2[e * f:(e + 1) * f]
+        yt = yt + wsel[:, e:e + 1] * ye
+    np.testing.assert_allclose(y, yt.detach().numpy(), atol=1e-10)
+    (yt * t64(dy)).sum().backward()
+    np.testing.assert_allclose(g["dx"], tx.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
