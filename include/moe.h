@@ -71,6 +71,10 @@ typedef struct {
                        by flat id t*k+j; the others are dropped (pos = -1,
                        sorted_pos = -1) and contribute nothing to y, dx or the
                        gradients (their dgates are 0). See moe_expert_capacity. */
+  int32_t renormalize; /* 0: gate = softmax probability of the chosen expert (R4, the
+                          paper's Fig. 5 reading). 1: each token's k gates divided by
+                          their sum; the router backward follows it. */
+  int32_t reserved;    /* must be 0 */
 } moe_config;
 
 /* ---- configuration and size queries (host only, no CUDA calls) ---------- */

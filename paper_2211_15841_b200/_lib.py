@@ -18,7 +18,8 @@ c_float_p = ctypes.POINTER(ctypes.c_float)
 class MoeConfig(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int64), ("num_experts", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("ffn_hidden", ctypes.c_int64), ("block_size", ctypes.c_int64),
-                ("act", ctypes.c_int32), ("capacity", ctypes.c_int32)]
+                ("act", ctypes.c_int32), ("capacity", ctypes.c_int32),
+                ("renormalize", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",

@@ -15,11 +15,12 @@ ACT_IDENTITY, ACT_GELU, ACT_RELU = 0, 1, 2
 
 
 def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU,
-                capacity=0) -> MoeConfig:
+                capacity=0, renormalize=False) -> MoeConfig:
     """capacity = 0: dropless (the method). > 0: the token-dropping formulation
-    with that many assignments kept per expert (moe_expert_capacity)."""
+    with that many assignments kept per expert (moe_expert_capacity).
+    renormalize: divide each token's k gates by their sum."""
     return MoeConfig(int(tokens), int(hidden), int(num_experts), int(top_k), int(ffn_hidden), int(block_size),
-                     int(act), int(capacity))
+                     int(act), int(capacity), int(bool(renormalize)), 0)
 
 
 def moe_expert_capacity(tokens, num_experts, capacity_factor) -> int:

@@ -740,6 +740,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           const float S = ssum * __expf(mx - M) + s1 * __expf(m1 - M);
           // merge the two descending lists; on equal values list 0 (lower experts) first
           int i0 = 0, i1 = 0;
+          float gsel[kMaxRouterTopK];
+          float gsum = 0.f;
 #pragma unroll
           for (int j = 0; j < kMaxRouterTopK; ++j) {
             if (j < topk) {
@@ -758,12 +760,15 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               const int e = take1 ? e1 : e0;
               i1 += take1 ? 1 : 0;
               i0 += take1 ? 0 : 1;
-              if (valid) {
-                p.idx[(long long)tok * topk + j] = e;
-                p.gates[(long long)tok * topk + j] = __expf(v - M) / S;
-              }
+              gsel[j] = __expf(v - M) / S;
+              gsum += gsel[j];
+              if (valid) p.idx[(long long)tok * topk + j] = e;
             }
           }
+          const float gscale = p.renorm ? 1.f / gsum : 1.f;  // NEXT-4 renormalisation over the k chosen
+#pragma unroll
+          for (int j = 0; j < kMaxRouterTopK; ++j)
+            if (j < topk && valid) p.gates[(long long)tok * topk + j] = gsel[j] * gscale;
         }
         asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // xr reused by the next tile
       } else if (MODE == DENSE) {  // EPI_F32: fp32 partial tile (split-K)

@@ -47,6 +47,7 @@ struct GemmParams {
   int32_t* idx;
   float* gates;
   int E, topk;
+  int renorm;  // gates divided by the sum of the token's k gates
   // EPI_F32
   float* out_f32;
   long long ld_f32, split_stride;

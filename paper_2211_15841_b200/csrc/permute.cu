@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
     const float* __restrict__ gates, uint4* __restrict__ dy_rows, float* __restrict__ dgates, int T, int k,
     const float* __restrict__ logits, const int32_t* __restrict__ expert_idx, int E,
     __nv_bfloat16* __restrict__ dlogits_bf16, float* __restrict__ dlogits_f32, const int32_t* __restrict__ counts,
-    const int32_t* __restrict__ padded_bins, int bs) {
+    const int32_t* __restrict__ padded_bins, int bs, int renorm) {
   pdl_trigger();
   pdl_wait();
   constexpr int RV = VEC * 32;
@@ -270,10 +270,34 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
 #pragma unroll
         for (int o2 = 16; o2 > 0; o2 >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o2);
         const float inv = 1.f / ssum;
+        // renormalised gates g_j = p_j / S (NEXT-4): the gradient reaching p_j is
+        // (dg_j - sum_i dg_i g_i) / S
+        float rs = 1.f, gd = 0.f;
+        if (renorm) {
+          float sp = 0.f, gp = 0.f;
+          for (int j = 0; j < k; ++j) {
+            const int ejj = __shfl_sync(0xffffffffu, eidx, r * k + j);
+            const float dgj = __shfl_sync(0xffffffffu, dg_lane, r * k + j);
+#pragma unroll
+            for (int q = 0; q < EQ; ++q)
+              if (lane + 32 * q == ejj) {
+                sp += pv[q] * inv;
+                gp += pv[q] * inv * dgj;
+              }
+          }
+#pragma unroll
+          for (int o2 = 16; o2 > 0; o2 >>= 1) {
+            sp += __shfl_xor_sync(0xffffffffu, sp, o2);
+            gp += __shfl_xor_sync(0xffffffffu, gp, o2);
+          }
+          rs = 1.f / sp;
+          gd = gp * rs;
+        }
         float pdp = 0.f;
         for (int j = 0; j < k; ++j) {  // warp-uniform
           const int ejj = __shfl_sync(0xffffffffu, eidx, r * k + j);
-          const float dgj = __shfl_sync(0xffffffffu, dg_lane, r * k + j);
+          float dgj = __shfl_sync(0xffffffffu, dg_lane, r * k + j);
+          if (renorm) dgj = (dgj - gd) * rs;
 #pragma unroll
           for (int q = 0; q < EQ; ++q)
             if (lane + 32 * q == ejj) {
@@ -341,6 +365,7 @@ struct SbwdArgs {
   const int32_t* counts;
   const int32_t* pbins;
   int bs;
+  int renorm;
 };
 
 template <int V, int TPW>
@@ -348,11 +373,11 @@ static moe_status sbwd_launch(const SbwdArgs& a, cudaStream_t s) {
   if (a.E <= 64)
     MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 2>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
-               a.counts, a.pbins, a.bs);
+               a.counts, a.pbins, a.bs, a.renorm);
   else
     MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 8>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
-               a.counts, a.pbins, a.bs);
+               a.counts, a.pbins, a.bs, a.renorm);
   return MOE_OK;
 }
 
@@ -364,7 +389,7 @@ moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* 
   SbwdArgs a{reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows), map, gates,
              reinterpret_cast<uint4*>(dy_rows), dgates, (int)cfg->tokens, (int)cfg->top_k, logits, expert_idx,
              (int)cfg->num_experts, dlogits_bf16, dlogits_f32, pad_topo ? pad_topo->counts : nullptr,
-             pad_topo ? pad_topo->padded_bins : nullptr, (int)cfg->block_size};
+             pad_topo ? pad_topo->padded_bins : nullptr, (int)cfg->block_size, cfg->renormalize};
   // one token per warp: measured faster than 2-4 tokens per warp (whose register
   // footprint halves the occupancy) at MoE-XS
   switch (vec) {

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16*
 // then gates = softmax probabilities of the chosen experts.
 constexpr int kMaxTopK = 32;
 __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restrict__ idx, float* __restrict__ gates,
-                            int T, int E, int k) {
+                            int T, int E, int k, int renorm) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
@@ -114,12 +114,19 @@ __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restric
       gates[(size_t)t * k + j] = expf(bv - m) / ssum;
     }
   }
+  if (renorm && lane == 0) {  // NEXT-4: the k gates divided by their sum
+    float gs = 0.f;
+    for (int j = 0; j < k; ++j) gs += gates[(size_t)t * k + j];
+    for (int j = 0; j < k; ++j) gates[(size_t)t * k + j] /= gs;
+  }
 }
 
 // dlogits[t,:] = p * (dp - <p, dp>) with p = softmax(logits[t,:]), dp sparse from dgates.
+// With renorm (gates g_j = p_j / S, S = sum of the chosen p): the gradient
+// reaching p_j is (dg_j - sum_i dg_i g_i) / S.
 __global__ void router_dlogits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                                       const float* __restrict__ dgates, float* __restrict__ dlogits,
-                                      __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k) {
+                                      __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k, int renorm) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
@@ -133,16 +140,24 @@ __global__ void router_dlogits_kernel(const float* __restrict__ logits, const in
   for (int e = lane; e < E; e += 32) ssum += expf(row[e] - m);
   for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
   const float inv = 1.f / ssum;
-  // <p, dp> = sum_j p[idx_j] * dgates_j
+  float rs = 1.f, gd = 0.f;  // renorm: 1/S and sum_i dg_i g_i
+  if (renorm) {
+    float S = 0.f;
+    for (int j = 0; j < k; ++j) S += expf(row[idx[(size_t)t * k + j]] - m) * inv;
+    rs = 1.f / S;
+    for (int j = 0; j < k; ++j) gd += dgates[(size_t)t * k + j] * expf(row[idx[(size_t)t * k + j]] - m) * inv * rs;
+  }
+  auto dgp = [&](int j) { return renorm ? (dgates[(size_t)t * k + j] - gd) * rs : dgates[(size_t)t * k + j]; };
+  // <p, dp> = sum_j p[idx_j] * dp_j
   float pdp = 0.f;
   for (int j = 0; j < k; ++j) {
     const int e = idx[(size_t)t * k + j];
-    pdp += expf(row[e] - m) * inv * dgates[(size_t)t * k + j];
+    pdp += expf(row[e] - m) * inv * dgp(j);
   }
   for (int e = lane; e < E; e += 32) {
     float dp = 0.f;
     for (int j = 0; j < k; ++j)
-      if (idx[(size_t)t * k + j] == e) dp += dgates[(size_t)t * k + j];
+      if (idx[(size_t)t * k + j] == e) dp += dgp(j);
     const float p = expf(row[e] - m) * inv;
     if (dlogits_bf16)
       dlogits_bf16[(size_t)t * E + e] = __float2bfloat16_rn(p * (dp - pdp));
@@ -307,7 +322,7 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
   MOE_CHECK_ARG(logits && expert_idx && gates, "moe_topk: NULL pointer");
   if (cfg->top_k > kMaxTopK) return set_error(MOE_EUNSUPPORTED, "top_k=%lld > %d", (long long)cfg->top_k, kMaxTopK);
   const int T = (int)cfg->tokens;
-  MOE_LAUNCH("moe_topk", topk_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, as_stream(stream), logits, expert_idx, gates, T, (int)cfg->num_experts, (int)cfg->top_k);
+  MOE_LAUNCH("moe_topk", topk_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, as_stream(stream), logits, expert_idx, gates, T, (int)cfg->num_experts, (int)cfg->top_k, cfg->renormalize);
   return MOE_OK;
 }
 
@@ -337,6 +352,7 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.p.gates = gates;
     L.p.E = E;
     L.p.topk = (int)cfg->top_k;
+    L.p.renorm = cfg->renormalize;
     L.max_tiles = L.p.m_tiles;
     MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, BK, 128, "moe_router x", KSW));
     MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
@@ -362,11 +378,13 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
   const int parts = router_bwd_parts(cfg);
   if (router_on_tensor_cores(cfg)) {
     __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(dlogits);
-    MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, nullptr, dl16, T, E, k);
+    MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, nullptr, dl16, T, E, k,
+               cfg->renormalize);
     MOE_TRY(router_dwr_tc(cfg, x, dl16, dwr, ws, s));
     return router_dx_tc(cfg, dl16, wr, dx, dx, nullptr, 1, h, s);  // dx += dlogits . Wr^T (in place)
   }
-  MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, dlogits, nullptr, T, E, k);
+  MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, dlogits, nullptr, T, E, k,
+             cfg->renormalize);
   const int tpp = (int)ceil_div(T, parts);
   MOE_LAUNCH("router_dwr_part", router_dwr_part_kernel, dim3(dim3(parts, (unsigned)ceil_div(h, 32))), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);
   MOE_LAUNCH("router_dwr_reduce", router_dwr_reduce_kernel, dim3((int)ceil_div((int64_t)h * E, 256)), dim3(256), 0, s, part, dwr, parts, h * E);

@@ -131,6 +131,9 @@ moe_status moe_check_config(const moe_config* cfg) {
   if (cfg->act < MOE_ACT_IDENTITY || cfg->act > MOE_ACT_RELU)
     return set_error(MOE_EINVAL, "act=%d is not a moe_act", cfg->act);
   if (cfg->capacity < 0) return set_error(MOE_EINVAL, "capacity=%d must be >= 0 (0 = dropless)", cfg->capacity);
+  if (cfg->renormalize != 0 && cfg->renormalize != 1)
+    return set_error(MOE_EINVAL, "renormalize=%d must be 0 or 1", cfg->renormalize);
+  if (cfg->reserved != 0) return set_error(MOE_EINVAL, "reserved field must be 0");
   if (cfg->block_size != 128)
     return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
                      (long long)cfg->block_size);

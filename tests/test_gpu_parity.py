@@ -891,3 +891,42 @@ def test_bench_ep_multi_rank_flow():
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "ep2" and d["value"] > 0
     assert d["config"]["transport"] == "p2p" and d["config"]["launch_mode"] == "cuda_graph"
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+# ------------------------------------------------------------------ top-k gate renormalisation (NEXT-4)
+
+RENORM_CASES = [("C0-k2", 1000, S.CONFIGS["C0"].replace(top_k=2), 0.0), ("C4-k2", 2048, S.CONFIGS["C4"], 0.0),
+                ("E64-k4", 1024, S.MoEShape("E64-k4", 1024, 256, 256, 64, 4), 0.0),
+                ("C4-k2-cf1", 2048, S.CONFIGS["C4"], 1.0)]
+
+
+@pytest.mark.parametrize("name,T,shp,cf", RENORM_CASES)
+def test_layer_renormalized_gates(name, T, shp, cf):
+    """cfg.renormalize = 1: the router writes each token's k gates divided by
+    their sum (tensor-core epilogue for E % 64 == 0, SIMT top-k otherwise) and
+    the router backward follows the renormalisation (fused scatter-backward /
+    SIMT dlogits); layer fwd+bwd vs the oracle with renormalize=True, also
+    combined with a capacity."""
+    d = dev()
+    A = api()
+    inp = S.make_inputs(shp, seed=8, tokens=T)
+    C = A.moe_expert_capacity(T, shp.experts, cf) if cf > 0 else 0
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, capacity=C, renormalize=True)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    g = saved.gates.cpu().double().numpy()
+    np.testing.assert_allclose(g.sum(axis=1), 1.0, rtol=2e-6)
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act,
+                               logits=saved.logits.cpu().double().numpy(), capacity=C or None, renormalize=True)
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
+    np.testing.assert_array_equal(saved.expert_idx.cpu().numpy(), cache.expert_idx)
+    assert rel_fro(g, cache.gates) < 1e-5
+    assert rel_fro(f64(y), yo) < FRO_TOL
+    assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+    assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
