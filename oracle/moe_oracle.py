@@ -83,6 +83,24 @@ def topk(logits: np.ndarray, k: int, renormalize: bool = False):
     return idx, gates
 
 
+def load_balance_loss(probs: np.ndarray, expert_idx: np.ndarray, coeff: float):
+    """Auxiliary load-balancing loss (§2.2 P:118 names it without a formula;
+    SURVEY NEXT-4 takes S:354's): loss = coeff * E * sum_e f_e * P_e, f_e = the
+    fraction of tokens whose top-1 choice is e (treated as a constant), P_e =
+    the mean router probability of e. Returns (loss, dloss/dprobs [T,E])."""
+    p = np.asarray(probs, np.float64)
+    T, E = p.shape
+    top1 = np.asarray(expert_idx).reshape(T, -1)[:, 0]
+    f = np.zeros(E, np.float64)
+    for t in range(T):
+        f[top1[t]] += 1.0
+    f /= T
+    P = p.sum(axis=0) / T
+    loss = coeff * E * float((f * P).sum())
+    dprobs = np.broadcast_to(coeff * E * f / T, (T, E)).copy()
+    return loss, dprobs
+
+
 # ----------------------------------------------------------------------------
 # Permutation plan: §2.2 (P:110) + §5.2 "we pad each group of tokens with zeros
 # to the nearest multiple of 128" (P:297) + Fig. 5 padded_gather (P:267-268).
@@ -404,10 +422,13 @@ class Cache:
     k: int
     act: int
     renormalize: bool = False
+    aux_coeff: float = 0.0
+    aux_loss: float = 0.0
 
 
 def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = ACT_GELU,
-                 logits: np.ndarray | None = None, capacity: int | None = None, renormalize: bool = False):
+                 logits: np.ndarray | None = None, capacity: int | None = None, renormalize: bool = False,
+                 aux_coeff: float = 0.0):
     """Fig. 5 'dmoe_forward', step by step:
     (1) indices, weights = router(x)              P:260
     (2) topology = make_topology(indices)         P:265
@@ -429,7 +450,9 @@ def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = A
     a = act(act_kind, h_pre)
     yg = dsd(a, w2, topo)
     y = padded_scatter(yg, plan, gates, T, top_k)
-    cache = Cache(x, L, softmax(L), idx, gates, plan, topo, xg, h_pre, a, yg, top_k, act_kind, renormalize)
+    aux = load_balance_loss(softmax(L), idx, aux_coeff)[0] if aux_coeff else 0.0
+    cache = Cache(x, L, softmax(L), idx, gates, plan, topo, xg, h_pre, a, yg, top_k, act_kind, renormalize,
+                  aux_coeff, aux)
     return y, cache
 
 
@@ -489,6 +512,8 @@ def dmoe_backward(cache: Cache, dy, wr, w1, w2):
         else:
             for j in range(k):
                 dp[t, c.expert_idx[t, j]] += dgates[t, j]
+    if c.aux_coeff:                                 # + the auxiliary loss's gradient (d total / d aux = 1)
+        dp = dp + load_balance_loss(p, c.expert_idx, c.aux_coeff)[1]
     dlogits = p * (dp - (p * dp).sum(axis=1, keepdims=True))
     dwr = c.x.T @ dlogits
     dx = dx + dlogits @ np.asarray(wr, np.float64).T

@@ -569,3 +569,50 @@ def test_renormalized_layer_backward_vs_autograd(T, h, f, E, k):
     np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
+
+
+# ------------------------------------------------------------------ auxiliary load-balancing loss (NEXT-4)
+
+def test_load_balance_loss_closed_forms():
+    # uniform f and P -> loss = coefficient; all tokens to one expert with prob 1 -> coefficient * E
+    E, T = 4, 8
+    p = np.full((T, E), 1.0 / E)
+    idx = np.array([[t % E] for t in range(T)])
+    assert abs(O.load_balance_loss(p, idx, 0.3)[0] - 0.3) < 1e-15
+    p1 = np.zeros((T, E)); p1[:, 2] = 1.0
+    assert abs(O.load_balance_loss(p1, np.full((T, 1), 2), 0.3)[0] - 0.3 * E) < 1e-15
+
+
+def test_load_balance_loss_grad_finite_differences_and_layer_autograd():
+    # d loss / d probs by finite differences (f held fixed); then the layer's
+    # dlogits / dWr / dx with the aux term against torch autograd of the masked formulation
+    rng = np.random.default_rng(3)
+    T, E = 6, 5
+    p = rng.random((T, E)); p /= p.sum(1, keepdims=True)
+    idx = p.argmax(1)[:, None]
+    loss, g = O.load_balance_loss(p, idx, 0.7)
+    eps = 1e-6
+    for t in range(T):
+        for e in range(E):
+            q = p.copy(); q[t, e] += eps
+            fd = (O.load_balance_loss(q, idx, 0.7)[0] - loss) / eps
+            assert abs(fd - g[t, e]) <= 1e-6 * max(1.0, abs(g[t, e]))
+    T, h, f, E, k = 16, 6, 8, 4, 2
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 23)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU, aux_coeff=0.05)
+    gr = O.dmoe_backward(cache, dy, wr, w1, w2)
+    tx, twr, tw1, tw2 = (t64(a).requires_grad_(True) for a in (x, wr, w1, w2))
+    L = tx @ twr
+    pt = torch.softmax(L, dim=1)
+    ti = torch.topk(L, k, dim=1).indices
+    fe = torch.bincount(ti[:, 0], minlength=E).double() / T           # constant (no gradient)
+    aux = 0.05 * E * (fe * pt.mean(0)).sum()
+    assert abs(aux.item() - cache.aux_loss) < 1e-12
+    yt = torch.zeros_like(tx)
+    for e in range(E):
+        ye = torch_act(O.ACT_GELU, tx @ tw1[:, e * f:(e + 1) * f]) @ tw2[e * f:(e + 1) * f]
+        sel = (ti == e).any(dim=1).double()
+        yt = yt + (sel * pt[:, e])[:, None] * ye
+    ((yt * t64(dy)).sum() + aux).backward()
+    np.testing.assert_allclose(gr["dx"], tx.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(gr["dwr"], twr.grad.numpy(), atol=1e-10)
