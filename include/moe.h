@@ -74,7 +74,11 @@ typedef struct {
   int32_t renormalize; /* 0: gate = softmax probability of the chosen expert (R4, the
                           paper's Fig. 5 reading). 1: each token's k gates divided by
                           their sum; the router backward follows it. */
-  int32_t reserved;    /* must be 0 */
+  float aux_loss_coeff; /* 0: none. > 0: auxiliary load-balancing loss (P:118 names it, no formula;
+                           S:354: coeff * E * sum_e f_e P_e, f_e = fraction of tokens whose top-1
+                           expert is e, held constant; P_e = mean router probability). moe_forward
+                           writes it to the workspace (moe_workspace_offset 5) and moe_backward
+                           adds its gradient (d total / d aux = 1) to the router's. */
 } moe_config;
 
 /* ---- configuration and size queries (host only, no CUDA calls) ---------- */
@@ -105,7 +109,10 @@ size_t moe_workspace_bytes(const moe_config* cfg);
 /* Byte offset inside the workspace of the scratch tensors moe_backward uses:
  * which = 0 dY_g [max_rows,h] bf16, 1 dH [max_nnz,bs,bs] bf16, 2 dX_g
  * [max_rows,h] bf16, 3 dgates [T,k] fp32, 4 dlogits [T,E] (bf16 on the
- * tensor-core router path). Returns (size_t)-1 for an unknown `which`. */
+ * tensor-core router path), 5 the auxiliary loss: float [1 + E] = {loss,
+ * per-expert logit-gradient coefficients coeff*E*f_e/T} (written by
+ * moe_load_balance_loss / moe_forward, read by moe_backward; kept between
+ * them). Returns (size_t)-1 for an unknown `which`. */
 size_t moe_workspace_offset(const moe_config* cfg, int which);
 
 /* Number of SMs the library sizes its persistent grids for (queried once). */
@@ -355,6 +362,13 @@ moe_status moe_dds(const moe_config* cfg, const void* a, int trans_a, const void
 moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, const float* logits,
                           const int32_t* expert_idx, const float* dgates, float* dwr, void* dx,
                           void* ws, void* stream);
+
+/* Auxiliary load-balancing loss (cfg->aux_loss_coeff): from the
+ * fp32 logits [T,E] and expert_idx [T,k] (top-1 = slot 0) writes {loss,
+ * coeff*E*f_e/T for every e} to the workspace's aux region (offset 5).
+ * Deterministic: fixed token partition, fixed-order reductions. */
+moe_status moe_load_balance_loss(const moe_config* cfg, const float* logits, const int32_t* expert_idx, void* ws,
+                                 void* stream);
 
 /* ---- fused backward pieces used by moe_backward when the router runs on the
  *      tensor cores (E % 64 == 0, E <= 256, top_k <= 8; else MOE_EUNSUPPORTED) --- */

@@ -19,7 +19,7 @@ class MoeConfig(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int64), ("num_experts", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("ffn_hidden", ctypes.c_int64), ("block_size", ctypes.c_int64),
                 ("act", ctypes.c_int32), ("capacity", ctypes.c_int32),
-                ("renormalize", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("renormalize", ctypes.c_int32), ("aux_loss_coeff", ctypes.c_float)]
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",
@@ -108,6 +108,7 @@ SIGNATURES = {
     "moe_router_bwd": (STATUS, [CFG, P, P, P, P, P, P, P, P, P]),
     "moe_scatter_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),
     "moe_router_dwr": (STATUS, [CFG, P, P, P, P, P]),
+    "moe_load_balance_loss": (STATUS, [CFG, P, P, P, P]),
     "moe_router_dx": (STATUS, [CFG, P, P, P, TOPO, P, P]),
     "moe_forward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), P, P, ctypes.POINTER(MoeSaved), P, P]),
     "moe_backward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), ctypes.POINTER(MoeSaved), P, P, P,

@@ -15,12 +15,27 @@ ACT_IDENTITY, ACT_GELU, ACT_RELU = 0, 1, 2
 
 
 def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU,
-                capacity=0, renormalize=False) -> MoeConfig:
+                capacity=0, renormalize=False, aux_loss_coeff=0.0) -> MoeConfig:
     """capacity = 0: dropless (the method). > 0: the token-dropping formulation
     with that many assignments kept per expert (moe_expert_capacity).
-    renormalize: divide each token's k gates by their sum."""
+    renormalize: divide each token's k gates by their sum. aux_loss_coeff > 0:
+    auxiliary load-balancing loss (moe_load_balance_loss)."""
     return MoeConfig(int(tokens), int(hidden), int(num_experts), int(top_k), int(ffn_hidden), int(block_size),
-                     int(act), int(capacity), int(bool(renormalize)), 0)
+                     int(act), int(capacity), int(bool(renormalize)), float(aux_loss_coeff))
+
+
+def aux_region(cfg, ws) -> torch.Tensor:
+    """float [1 + E] view of the workspace's auxiliary-loss region: {loss, coeff*E*f_e/T}."""
+    off = int(lib.moe_workspace_offset(ctypes.byref(cfg), 5))
+    return ws[off: off + 4 * (1 + cfg.num_experts)].view(torch.float32)
+
+
+def moe_load_balance_loss(cfg, logits, expert_idx, ws=None):
+    """moe_load_balance_loss (include/moe.h): returns (loss [1] tensor view, the workspace)."""
+    ws = ws if ws is not None else workspace(cfg, logits.device)
+    check("moe_load_balance_loss", lib.moe_load_balance_loss(ctypes.byref(cfg), _p(logits), _p(expert_idx), _p(ws),
+                                                             _stream()))
+    return aux_region(cfg, ws)[:1], ws
 
 
 def moe_expert_capacity(tokens, num_experts, capacity_factor) -> int:
@@ -347,6 +362,7 @@ class Saved:
     a: torch.Tensor
     y_g: torch.Tensor
     struct: MoeSaved = None
+    ws: torch.Tensor | None = None   # the forward's workspace when it holds the auxiliary loss (aux_loss_coeff > 0)
 
     @staticmethod
     def allocate(cfg, device="cuda") -> "Saved":
@@ -377,6 +393,8 @@ def moe_forward(cfg, wr, w1, w2, x, y=None, saved: Saved | None = None, ws=None)
     w = weights_struct(wr, w1, w2)
     check("moe_forward", lib.moe_forward(ctypes.byref(cfg), ctypes.byref(w), _p(x), _p(y), ctypes.byref(saved.struct),
                                          _p(ws), _stream()))
+    if cfg.aux_loss_coeff > 0:
+        saved.ws = ws   # its aux region (loss, gradient coefficients) is read by moe_backward
     return y, saved
 
 
@@ -387,7 +405,8 @@ def moe_backward(cfg, wr, w1, w2, saved: Saved, x, dy, dx=None, grads=None, ws=N
         grads = (torch.empty(cfg.hidden, cfg.num_experts, dtype=torch.float32, device=dev),
                  torch.empty(cfg.hidden, cfg.num_experts * cfg.ffn_hidden, dtype=torch.bfloat16, device=dev),
                  torch.empty(cfg.num_experts * cfg.ffn_hidden, cfg.hidden, dtype=torch.bfloat16, device=dev))
-    ws = ws if ws is not None else workspace(cfg, dev)
+    if ws is None:
+        ws = saved.ws if saved.ws is not None else workspace(cfg, dev)
     w = weights_struct(wr, w1, w2)
     g = MoeGrads(grads[0].data_ptr(), grads[1].data_ptr(), grads[2].data_ptr())
     check("moe_backward", lib.moe_backward(ctypes.byref(cfg), ctypes.byref(w), ctypes.byref(saved.struct), _p(x),

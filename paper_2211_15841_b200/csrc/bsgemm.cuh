@@ -67,6 +67,9 @@ struct GemmParams {
 // dx = dlogits . Wr^T + addend (optionally gathered through addend_map).
 moe_status router_dwr_tc(const moe_config* cfg, const void* x, const __nv_bfloat16* dlogits, float* dwr, void* ws,
                          cudaStream_t s);
+moe_status scatter_bwd_router_aux(const moe_config* cfg, const void* dy, const void* y_g, const moe_topology_t* topo,
+                                  const float* gates, const float* logits, const int32_t* expert_idx, void* dy_g,
+                                  float* dgates, void* dlogits_bf16, const float* aux_c, cudaStream_t s);
 moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, const void* wr, void* dx,
                         const void* addend, const int32_t* addend_map, int addend_k, long long ld_add,
                         cudaStream_t s);

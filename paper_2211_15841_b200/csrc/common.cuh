@@ -92,9 +92,11 @@ struct WsLayout {
   size_t dgates;    // f32 [T, k]
   size_t dlogits;   // f32 [T, E]
   size_t dwr_part;  // f32 [n_parts, h, E]
+  size_t aux;       // f32 [1 + E] {aux loss, per-expert gradient coefficients} + partials
   size_t total;
 };
 constexpr int kTopoChunk = 1024;  // assignments per topology CTA
+constexpr int kAuxParts = 148;    // fixed token partition of the auxiliary-loss reduction
 int router_bwd_parts(const moe_config* cfg);
 bool router_on_tensor_cores(const moe_config* cfg);
 WsLayout ws_layout(const moe_config* cfg);

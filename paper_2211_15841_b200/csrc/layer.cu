@@ -59,6 +59,8 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   MOE_CHECK_ARG(id || sv->act_deriv, "moe_forward: saved->act_deriv required for a non-identity activation");
   // (1) indices, weights = router(x)
   MOE_TRY(moe_router(cfg, x, w->wr, sv->logits, sv->expert_idx, sv->gates, ws, stream));
+  //     + the auxiliary load-balancing loss into the workspace
+  if (cfg->aux_loss_coeff > 0.f) MOE_TRY(moe_load_balance_loss(cfg, sv->logits, sv->expert_idx, ws, stream));
   // (2) topology = make_topology(indices)
   MOE_TRY(moe_topology(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
@@ -93,8 +95,9 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   // b1: dY_g = gates * dy (un-permuted rows), dgates = <Y_g, dy>
   //     [+ b7's dlogits = p * (dp - <p,dp>) in the same pass]
   if (fused_router) {
-    MOE_TRY(moe_scatter_bwd_router(cfg, dy, sv->y_g, topo, sv->gates, sv->logits, sv->expert_idx, dy_g, dgates,
-                                   dl16, stream));
+    const float* aux_c = cfg->aux_loss_coeff > 0.f ? reinterpret_cast<const float*>(wsb + L.aux) + 1 : nullptr;
+    MOE_TRY(scatter_bwd_router_aux(cfg, dy, sv->y_g, topo, sv->gates, sv->logits, sv->expert_idx, dy_g, dgates,
+                                   dl16, aux_c, as_stream(stream)));
   } else {
     MOE_TRY(moe_scatter_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
   }

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
     const float* __restrict__ gates, uint4* __restrict__ dy_rows, float* __restrict__ dgates, int T, int k,
     const float* __restrict__ logits, const int32_t* __restrict__ expert_idx, int E,
     __nv_bfloat16* __restrict__ dlogits_bf16, float* __restrict__ dlogits_f32, const int32_t* __restrict__ counts,
-    const int32_t* __restrict__ padded_bins, int bs, int renorm) {
+    const int32_t* __restrict__ padded_bins, int bs, int renorm, const float* __restrict__ aux_c) {
   pdl_trigger();
   pdl_wait();
   constexpr int RV = VEC * 32;
@@ -305,6 +305,17 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
               pdp += pv[q] * inv * dgj;
             }
         }
+        if (aux_c) {  // + the auxiliary loss's d/dp (every expert)
+#pragma unroll
+          for (int q = 0; q < EQ; ++q) {
+            const int e = lane + 32 * q;
+            if (q < EQn && e < E) {
+              const float c = __ldg(aux_c + e);
+              dpl[q] += c;
+              pdp += pv[q] * inv * c;
+            }
+          }
+        }
 #pragma unroll
         for (int o2 = 16; o2 > 0; o2 >>= 1) pdp += __shfl_xor_sync(0xffffffffu, pdp, o2);
 #pragma unroll
@@ -366,6 +377,7 @@ struct SbwdArgs {
   const int32_t* pbins;
   int bs;
   int renorm;
+  const float* aux_c;
 };
 
 template <int V, int TPW>
@@ -373,23 +385,23 @@ static moe_status sbwd_launch(const SbwdArgs& a, cudaStream_t s) {
   if (a.E <= 64)
     MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 2>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
-               a.counts, a.pbins, a.bs, a.renorm);
+               a.counts, a.pbins, a.bs, a.renorm, a.aux_c);
   else
     MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 8>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
-               a.counts, a.pbins, a.bs, a.renorm);
+               a.counts, a.pbins, a.bs, a.renorm, a.aux_c);
   return MOE_OK;
 }
 
 moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* y_rows, const int32_t* map,
                              const float* gates, void* dy_rows, float* dgates, const float* logits,
                              const int32_t* expert_idx, __nv_bfloat16* dlogits_bf16, float* dlogits_f32,
-                             const moe_topology_t* pad_topo, cudaStream_t s) {
+                             const moe_topology_t* pad_topo, cudaStream_t s, const float* aux_c) {
   const int vec = (int)(cfg->hidden / 256);
   SbwdArgs a{reinterpret_cast<const uint4*>(dy), reinterpret_cast<const uint4*>(y_rows), map, gates,
              reinterpret_cast<uint4*>(dy_rows), dgates, (int)cfg->tokens, (int)cfg->top_k, logits, expert_idx,
              (int)cfg->num_experts, dlogits_bf16, dlogits_f32, pad_topo ? pad_topo->counts : nullptr,
-             pad_topo ? pad_topo->padded_bins : nullptr, (int)cfg->block_size, cfg->renormalize};
+             pad_topo ? pad_topo->padded_bins : nullptr, (int)cfg->block_size, cfg->renormalize, aux_c};
   // one token per warp: measured faster than 2-4 tokens per warp (whose register
   // footprint halves the occupancy) at MoE-XS
   switch (vec) {

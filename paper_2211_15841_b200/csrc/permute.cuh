@@ -13,5 +13,5 @@ namespace moe {
 moe_status scatter_bwd_fused(const moe_config* cfg, const void* dy, const void* y_rows, const int32_t* map,
                              const float* gates, void* dy_rows, float* dgates, const float* logits,
                              const int32_t* expert_idx, __nv_bfloat16* dlogits_bf16, float* dlogits_f32,
-                             const moe_topology_t* pad_topo, cudaStream_t s);
+                             const moe_topology_t* pad_topo, cudaStream_t s, const float* aux_c = nullptr);
 }  // namespace moe

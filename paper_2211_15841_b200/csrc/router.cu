@@ -124,9 +124,11 @@ __global__ void topk_kernel(const float* __restrict__ logits, int32_t* __restric
 // dlogits[t,:] = p * (dp - <p, dp>) with p = softmax(logits[t,:]), dp sparse from dgates.
 // With renorm (gates g_j = p_j / S, S = sum of the chosen p): the gradient
 // reaching p_j is (dg_j - sum_i dg_i g_i) / S.
+// aux_c (optional, [E]): the auxiliary loss's d/dp, added to every expert's dp.
 __global__ void router_dlogits_kernel(const float* __restrict__ logits, const int32_t* __restrict__ idx,
                                       const float* __restrict__ dgates, float* __restrict__ dlogits,
-                                      __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k, int renorm) {
+                                      __nv_bfloat16* __restrict__ dlogits_bf16, int T, int E, int k, int renorm,
+                                      const float* __restrict__ aux_c) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
@@ -154,8 +156,14 @@ __global__ void router_dlogits_kernel(const float* __restrict__ logits, const in
     const int e = idx[(size_t)t * k + j];
     pdp += expf(row[e] - m) * inv * dgp(j);
   }
+  if (aux_c) {  // + <p, c>
+    float pa = 0.f;
+    for (int e = lane; e < E; e += 32) pa += expf(row[e] - m) * inv * __ldg(aux_c + e);
+    for (int o = 16; o > 0; o >>= 1) pa += __shfl_xor_sync(0xffffffffu, pa, o);
+    pdp += pa;
+  }
   for (int e = lane; e < E; e += 32) {
-    float dp = 0.f;
+    float dp = aux_c ? __ldg(aux_c + e) : 0.f;
     for (int j = 0; j < k; ++j)
       if (idx[(size_t)t * k + j] == e) dp += dgp(j);
     const float p = expf(row[e] - m) * inv;
@@ -374,17 +382,19 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
   const WsLayout WL = ws_layout(cfg);
   float* dlogits = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WL.dlogits);
   float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + WL.dwr_part);
+  const float* aux_c =
+      cfg->aux_loss_coeff > 0.f ? reinterpret_cast<const float*>(reinterpret_cast<char*>(ws) + WL.aux) + 1 : nullptr;
   cudaStream_t s = as_stream(stream);
   const int parts = router_bwd_parts(cfg);
   if (router_on_tensor_cores(cfg)) {
     __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(dlogits);
     MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, nullptr, dl16, T, E, k,
-               cfg->renormalize);
+               cfg->renormalize, aux_c);
     MOE_TRY(router_dwr_tc(cfg, x, dl16, dwr, ws, s));
     return router_dx_tc(cfg, dl16, wr, dx, dx, nullptr, 1, h, s);  // dx += dlogits . Wr^T (in place)
   }
   MOE_LAUNCH("router_dlogits", router_dlogits_kernel, dim3((int)ceil_div(T, 8)), dim3(256), 0, s, logits, expert_idx, dgates, dlogits, nullptr, T, E, k,
-             cfg->renormalize);
+             cfg->renormalize, aux_c);
   const int tpp = (int)ceil_div(T, parts);
   MOE_LAUNCH("router_dwr_part", router_dwr_part_kernel, dim3(dim3(parts, (unsigned)ceil_div(h, 32))), dim3(256), 0, s, reinterpret_cast<const __nv_bfloat16*>(x), dlogits, part, T, h, E, tpp);
   MOE_LAUNCH("router_dwr_reduce", router_dwr_reduce_kernel, dim3((int)ceil_div((int64_t)h * E, 256)), dim3(256), 0, s, part, dwr, parts, h * E);
@@ -409,6 +419,99 @@ moe_status moe_scatter_bwd_router(const moe_config* cfg, const void* dy, const v
     return set_error(MOE_EUNSUPPORTED, "moe_scatter_bwd_router: needs E %% 64 == 0, E <= 256, top_k <= 8");
   return scatter_bwd_fused(cfg, dy, y_g, topo->pos, gates, dy_g, dgates, logits, expert_idx,
                            reinterpret_cast<__nv_bfloat16*>(dlogits_bf16), nullptr, topo, as_stream(stream));
+}
+
+}  // extern "C"
+
+namespace moe {
+// moe_scatter_bwd_router + the auxiliary loss's gradient (the layer's form)
+moe_status scatter_bwd_router_aux(const moe_config* cfg, const void* dy, const void* y_g, const moe_topology_t* topo,
+                                  const float* gates, const float* logits, const int32_t* expert_idx, void* dy_g,
+                                  float* dgates, void* dlogits_bf16, const float* aux_c, cudaStream_t s) {
+  return scatter_bwd_fused(cfg, dy, y_g, topo->pos, gates, dy_g, dgates, logits, expert_idx,
+                           reinterpret_cast<__nv_bfloat16*>(dlogits_bf16), nullptr, topo, s, aux_c);
+}
+
+// Auxiliary load-balancing loss. Partials: CTA q owns tokens
+// [q*T/P, (q+1)*T/P); each warp accumulates softmax probabilities of its tokens
+// per expert in registers-backed shared rows, reduced in warp order.
+__global__ void __launch_bounds__(256) aux_partial_kernel(const float* __restrict__ logits,
+                                                          const int32_t* __restrict__ idx, int T, int E, int k,
+                                                          float* __restrict__ part_p, int* __restrict__ part_c) {
+  extern __shared__ float s_acc[];  // [8 warps][E] probabilities, then int [E] top-1 counts
+  int* s_cnt = reinterpret_cast<int*>(s_acc + 8 * E);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * E; i += blockDim.x) s_acc[i] = 0.f;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int t0 = (int)((long long)blockIdx.x * T / gridDim.x), t1 = (int)((long long)(blockIdx.x + 1) * T / gridDim.x);
+  for (int t = t0 + warp; t < t1; t += 8) {
+    const float* row = logits + (size_t)t * E;
+    float m = -FLT_MAX;
+    for (int e = lane; e < E; e += 32) m = fmaxf(m, row[e]);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float ssum = 0.f;
+    for (int e = lane; e < E; e += 32) ssum += expf(row[e] - m);
+    for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+    const float inv = 1.f / ssum;
+    for (int e = lane; e < E; e += 32) s_acc[warp * E + e] += expf(row[e] - m) * inv;
+    if (lane == 0) atomicAdd(&s_cnt[idx[(size_t)t * k]], 1);  // integer: order-free
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float a = 0.f;
+    for (int w = 0; w < 8; ++w) a += s_acc[w * E + e];
+    part_p[(size_t)blockIdx.x * E + e] = a;
+    part_c[(size_t)blockIdx.x * E + e] = s_cnt[e];
+  }
+}
+
+__global__ void __launch_bounds__(256) aux_final_kernel(const float* __restrict__ part_p,
+                                                        const int* __restrict__ part_c, int parts, int T, int E,
+                                                        float coeff, float* __restrict__ aux) {
+  __shared__ float s_red[256];
+  float acc = 0.f;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float P = 0.f;
+    long long c = 0;
+    for (int q = 0; q < parts; ++q) {
+      P += part_p[(size_t)q * E + e];
+      c += part_c[(size_t)q * E + e];
+    }
+    const float f = (float)c / (float)T;
+    aux[1 + e] = coeff * (float)E * f / (float)T;  // d loss / d p[t, e]
+    acc += f * (P / (float)T);
+  }
+  s_red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {  // fixed-shape tree: deterministic
+    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) aux[0] = coeff * (float)E * s_red[0];
+}
+}  // namespace moe
+
+extern "C" {
+
+moe_status moe_load_balance_loss(const moe_config* cfg, const float* logits, const int32_t* expert_idx, void* ws,
+                                 void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(logits && expert_idx && ws, "moe_load_balance_loss: NULL pointer");
+  const int T = (int)cfg->tokens, E = (int)cfg->num_experts, k = (int)cfg->top_k;
+  const WsLayout WL = ws_layout(cfg);
+  char* base = reinterpret_cast<char*>(ws) + WL.aux;
+  float* aux = reinterpret_cast<float*>(base);
+  float* part_p = aux + 1 + E;
+  int* part_c = reinterpret_cast<int*>(part_p + (size_t)kAuxParts * E);
+  const size_t smem = (size_t)8 * E * sizeof(float) + (size_t)E * sizeof(int);
+  if (smem > 48 * 1024) return set_error(MOE_EUNSUPPORTED, "moe_load_balance_loss: num_experts=%d too large", E);
+  cudaStream_t s = as_stream(stream);
+  MOE_LAUNCH("aux_partial", aux_partial_kernel, dim3(kAuxParts), dim3(256), smem, s, logits, expert_idx, T, E, k, part_p,
+             part_c);
+  MOE_LAUNCH("aux_final", aux_final_kernel, dim3(1), dim3(256), 0, s, part_p, part_c, kAuxParts, T, E,
+             cfg->aux_loss_coeff, aux);
+  return MOE_OK;
 }
 
 moe_status moe_router_dwr(const moe_config* cfg, const void* x, const void* dlogits_bf16, float* dwr, void* ws,

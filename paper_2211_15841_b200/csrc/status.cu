@@ -99,6 +99,8 @@ WsLayout ws_layout(const moe_config* cfg) {
   off = align256(off + 4 * cfg->tokens * E);
   L.dwr_part = off;
   off = align256(off + 4 * (size_t)router_bwd_parts(cfg) * h * E);
+  L.aux = off;  // {loss, c[E]}, then per-part column sums and top-1 counts
+  off = align256(off + 4 * (size_t)(1 + E) + 8 * (size_t)kAuxParts * E);
   L.total = off;
   return L;
 }
@@ -133,7 +135,8 @@ moe_status moe_check_config(const moe_config* cfg) {
   if (cfg->capacity < 0) return set_error(MOE_EINVAL, "capacity=%d must be >= 0 (0 = dropless)", cfg->capacity);
   if (cfg->renormalize != 0 && cfg->renormalize != 1)
     return set_error(MOE_EINVAL, "renormalize=%d must be 0 or 1", cfg->renormalize);
-  if (cfg->reserved != 0) return set_error(MOE_EINVAL, "reserved field must be 0");
+  if (!(cfg->aux_loss_coeff >= 0.f) || isinf(cfg->aux_loss_coeff))
+    return set_error(MOE_EINVAL, "aux_loss_coeff=%g must be finite and >= 0", (double)cfg->aux_loss_coeff);
   if (cfg->block_size != 128)
     return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
                      (long long)cfg->block_size);
@@ -178,6 +181,7 @@ size_t moe_workspace_offset(const moe_config* cfg, int which) {
     case 2: return L.dx_g;
     case 3: return L.dgates;
     case 4: return L.dlogits;
+    case 5: return L.aux;
     default: return (size_t)-1;
   }
 }

@@ -930,3 +930,37 @@ def test_layer_renormalized_gates(name, T, shp, cf):
     assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
     assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
     assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
+
+
+# ------------------------------------------------------------------ auxiliary load-balancing loss (NEXT-4)
+
+@pytest.mark.parametrize("name,T,shp", [("C0", 1024, S.CONFIGS["C0"]), ("C1-reduced", 4096, S.CONFIGS["C1"]),
+                                        ("C4-k2", 2048, S.CONFIGS["C4"]), ("C2-skew", 4096, S.CONFIGS["C2"])])
+def test_layer_aux_load_balance_loss(name, T, shp):
+    """cfg.aux_loss_coeff > 0: moe_forward writes the auxiliary loss to
+    the workspace and moe_backward adds its router gradient; loss value and
+    dx / dWr against the oracle routed from the GPU's logits."""
+    d = dev()
+    A = api()
+    coeff = 0.01
+    inp = S.make_inputs(shp, seed=12, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, aux_loss_coeff=coeff)
+    ws = A.workspace(cfg, d)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd, ws=ws)
+    loss = float(A.aux_region(cfg, ws)[0].item())
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d), ws=ws)
+    torch.cuda.synchronize()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    L = saved.logits.cpu().double().numpy()
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act, logits=L, aux_coeff=coeff)
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
+    assert abs(loss - cache.aux_loss) <= 1e-5 * abs(cache.aux_loss)
+    # the standalone entry agrees with what the forward wrote
+    l2, _ = A.moe_load_balance_loss(cfg, saved.logits, saved.expert_idx)
+    assert float(l2.item()) == loss
+    assert rel_fro(f64(y), yo) < FRO_TOL
+    assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
