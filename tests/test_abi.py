@@ -82,3 +82,26 @@ def test_null_arguments_rejected_without_launch():
     cfg = _cfg()
     st = lib.moe_gather(ctypes.byref(cfg), None, None, None, None)
     assert st == 1 and b"NULL" in lib.moe_last_error()
+
+
+def test_check_config_formulation_fields():
+    """capacity / renormalize / aux_loss_coeff (NEXT-4) are validated on the host;
+    moe_expert_capacity matches the oracle's ceil(T*cf/E)."""
+    import math
+    from oracle import moe_oracle as O
+    from paper_2211_15841_b200 import api
+    from paper_2211_15841_b200._lib import lib
+    assert api.moe_check_config(_cfg(capacity=3, renormalize=True, aux_loss_coeff=0.01)) == 0
+    assert api.moe_check_config(_cfg(capacity=-1)) == 1 and b"capacity" in lib.moe_last_error()
+    cfg = _cfg()
+    cfg.renormalize = 2
+    assert api.moe_check_config(cfg) == 1 and b"renormalize" in lib.moe_last_error()
+    for bad in (-0.5, math.nan, math.inf):
+        assert api.moe_check_config(_cfg(aux_loss_coeff=bad)) == 1
+    for T, E, cf in [(8, 4, 1.0), (1000, 64, 1.5), (32768, 64, 2.0), (7, 3, 0.5), (10, 4, 0.0)]:
+        want = O.expert_capacity(T, E, cf) if cf > 0 else 0
+        assert api.moe_expert_capacity(T, E, cf) == want
+    # workspace offset 5 (aux region) exists and leaves room for {loss, E coefficients}
+    cfg = _cfg(num_experts=64, hidden=512, ffn_hidden=2048)
+    off = lib.moe_workspace_offset(ctypes.byref(cfg), 5)
+    assert 0 < off and off + 4 * 65 <= api.moe_workspace_bytes(cfg)
