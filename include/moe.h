@@ -266,6 +266,11 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
 /* region MOE_EP_RECV_X / MOE_EP_RECV_DY: rows [T*k, hidden] bf16 in this
  * rank's expert-sorted order go to their experts' owners' receive regions. */
 moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, void* stream);
+/* moe_ep_dispatch fused with moe_sort_rows: x [T, hidden] in token order;
+ * row j of the expert-sorted order is x[sorted_idx[j] / top_k] (sorted_idx of
+ * the rank's moe_topology over the global experts). */
+moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+                                  int top_k, void* stream);
 /* region MOE_EP_RET_Y / MOE_EP_RET_DX: received rows [n_recv, hidden] bf16
  * (arrival order) go back to their source ranks' return regions. */
 moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream);

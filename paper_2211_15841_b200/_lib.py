@@ -92,6 +92,7 @@ SIGNATURES = {
     "moe_ep_exchange_counts": (STATUS, [ctypes.POINTER(MoeEp), P, P]),
     "moe_ep_dispatch": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
     "moe_ep_combine": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
+    "moe_ep_dispatch_tokens": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P, ctypes.c_int, P]),
     "moe_ep_wait": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P]),
     "moe_topology_rows": (STATUS, [CFG, P, P, TOPO, P, P]),
     "moe_gather_rows": (STATUS, [CFG, P, TOPO, P, P, P]),

@@ -214,9 +214,12 @@ EpArgs ep_args(const moe_ep_t* ep) {
 // kRowsPerWarp rows per iteration (all loads, then all stores) so enough bytes
 // are in flight per SM to run at bandwidth rather than at load latency.
 constexpr int kRowsPerWarp = 4;
+// src_map (dispatch only, optional): row j of the expert-sorted order is source
+// row src_map[j] / src_k (moe_topology's sorted_idx: the sort is fused here).
 template <bool COMBINE, int VEC>
 __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
-                                                      size_t region_off) {
+                                                      size_t region_off, const int32_t* __restrict__ src_map,
+                                                      int src_k) {
   PlanView v = plan_view(a.plan, a.P, a.E);
   const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
   const int32_t* starts = COMBINE ? v.recv_start : v.send_src;
@@ -229,7 +232,8 @@ __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __r
 #pragma unroll
     for (int r = 0; r < kRowsPerWarp; ++r)
       if (j0 + r < rows) {
-        const uint4* sp = src + (size_t)(j0 + r) * RV;
+        const int srow = src_map ? __ldg(src_map + j0 + r) / src_k : j0 + r;
+        const uint4* sp = src + (size_t)srow * RV;
 #pragma unroll
         for (int u = 0; u < VEC; ++u) val[r][u] = __ldg(sp + lane + 32 * u);
       }
@@ -249,19 +253,20 @@ __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __r
 }
 
 template <bool COMBINE>
-moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream) {
+moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream,
+                          const int32_t* src_map = nullptr, int src_k = 1) {
   const EpArgs a = ep_args(ep);
   const uint4* src = reinterpret_cast<const uint4*>(rows);
   const int r = region - MOE_EP_COUNTS;
   const dim3 grid(kEpCtas), block(256);
   cudaStream_t s = as_stream(stream);
   switch (ep->hidden / 256) {
-    case 1: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off); break;
-    case 2: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off); break;
-    case 3: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off); break;
-    case 4: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off); break;
-    case 6: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off); break;
-    case 8: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off); break;
+    case 1: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 2: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 3: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 4: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 6: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 8: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
     default: return set_error(MOE_EUNSUPPORTED, "moe_ep exchange: hidden=%d must be 256 * {1,2,3,4,6,8}", ep->hidden);
   }
   return MOE_OK;
@@ -355,6 +360,16 @@ moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, voi
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
   return ep_copy_launch<false>(ep, rows, region, off, stream);
+}
+
+moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+                                  int top_k, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_dispatch_tokens"));
+  MOE_CHECK_ARG(x && sorted_idx && top_k >= 1 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
+                "moe_ep_dispatch_tokens: NULL x / sorted_idx, top_k < 1 or region %d not a receive region", region);
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
+  return ep_copy_launch<false>(ep, x, region, off, stream, sorted_idx, top_k);
 }
 
 moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream) {

@@ -271,9 +271,8 @@ class ExpertParallelMoE:
         cfg_l = self._cfg(T, self.E, self.k)
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
         topo_l = self._topology(cfg_l, idx, "local")
-        x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
         W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
-        recv_x = W.dispatch("x", x_sorted)                      # rows into the owners' windows
+        recv_x = W.dispatch_tokens("x", x, topo_l["sorted_idx"], self.k)   # sorted rows into the owners' windows
         cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
         buf = self._expert_bufs(cfg_e, x.device)
         rows = W.n_recv()

@@ -116,6 +116,15 @@ class PeerWindows:
         check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
         return self.rows(name)
 
+    def dispatch_tokens(self, name: str, x: torch.Tensor, sorted_idx: torch.Tensor, top_k: int):
+        """x [T, h] in token order, sent in expert-sorted order (sorted_idx): the
+        sort fused into the dispatch; waits for this rank's receive region."""
+        check("moe_ep_dispatch_tokens", lib.moe_ep_dispatch_tokens(
+            ctypes.byref(self.ep), REGION[name], ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(sorted_idx.data_ptr()),
+            int(top_k), self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
+        return self.rows(name)
+
     def combine(self, name: str, rows):
         """received rows [n_recv, h] -> their sources' return regions; waits for this rank's."""
         check("moe_ep_combine", lib.moe_ep_combine(ctypes.byref(self.ep), REGION[name],
