@@ -271,6 +271,32 @@ moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, voi
  * the rank's moe_topology over the global experts). */
 moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
                                   int top_k, void* stream);
+/* Padded exchange (the receiving side needs no gather): rows land directly in
+ * the owner's padded expert-grouped layout (local expert, then source
+ * rank, then token; pad rows at each expert's tail are NOT written — zero them
+ * with moe_zero_pad_rows). x [T, hidden] in token order read through
+ * sorted_idx (or, with sorted_idx NULL, rows already in expert order).
+ * moe_ep_combine_padded sends this rank's padded rows [n_padded, hidden] back
+ * to their sources' return regions (pad rows skipped). The receiving side's
+ * topology comes from the per-source counts (moe_topology_counts with the
+ * plan's compact counts, moe_ep_plan_offset 0); plan offset 1 holds its
+ * padded row count. */
+moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+                                  int top_k, void* stream);
+moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream);
+int moe_ep_plan_offset(int nranks, int num_experts, int which);
+
+/* Topology of assignments that are already grouped by expert and, within an
+ * expert, by source (expert parallelism's receiving side): counts_per_source
+ * [nsources, E] int32 device. Writes counts, bins, padded_bins, pair_bins,
+ * sizes and every BCSR / COO / transpose index (bit-identical to moe_topology
+ * of the same grouping); the per-assignment arrays (sorted_idx, pos,
+ * sorted_pos, row_src of real rows) are not written. */
+moe_status moe_topology_counts(const moe_config* cfg, const int32_t* counts_per_source, int nsources,
+                               const moe_topology_t* topo, void* stream);
+/* Zero the pad rows (tail of each expert group) of a padded [max_rows, h] buffer. */
+moe_status moe_zero_pad_rows(const moe_config* cfg, const moe_topology_t* topo, void* x_g, void* stream);
+
 /* region MOE_EP_RET_Y / MOE_EP_RET_DX: received rows [n_recv, hidden] bf16
  * (arrival order) go back to their source ranks' return regions. */
 moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream);

@@ -152,6 +152,21 @@ def moe_gather_rows(cfg, x, topo: Topology, rows_dev, x_g=None):
     return x_g
 
 
+def moe_topology_counts(cfg, counts_per_source, topo: Topology | None = None) -> Topology:
+    """moe_topology_counts (include/moe.h): topology of rows grouped by expert
+    then source, from the [nsources, E] int32 device counts."""
+    topo = topo if topo is not None else Topology(cfg, counts_per_source.device)
+    check("moe_topology_counts", lib.moe_topology_counts(ctypes.byref(cfg), _p(counts_per_source),
+                                                         int(counts_per_source.shape[0]), ctypes.byref(topo.struct),
+                                                         _stream()))
+    return topo
+
+
+def moe_zero_pad_rows(cfg, topo: Topology, x_g):
+    check("moe_zero_pad_rows", lib.moe_zero_pad_rows(ctypes.byref(cfg), ctypes.byref(topo.struct), _p(x_g), _stream()))
+    return x_g
+
+
 def moe_gather(cfg, x, topo: Topology, x_g=None):
     x_g = x_g if x_g is not None else torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=x.dtype,
                                                   device=x.device)

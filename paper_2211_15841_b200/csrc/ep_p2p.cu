@@ -51,8 +51,10 @@ __host__ __device__ inline WinLayout win_layout(int P, int E, long long h, long 
   L.expect = o; o = align256(o + sizeof(uint32_t) * kEpRegions);       // epochs this rank has completed
   L.error = o;  o = align256(o + sizeof(uint32_t) * 4);
   L.counts = o; o = align256(o + sizeof(int32_t) * (size_t)P * E);
-  L.recv_x = o; o = align256(o + 2ull * cap * h);
-  L.recv_dy = o; o = align256(o + 2ull * cap * h);
+  // receive regions hold the padded expert-grouped layout (up to 127 pad rows per local expert)
+  const long long rrows = cap + (long long)(E / P) * 128;
+  L.recv_x = o; o = align256(o + 2ull * rrows * h);
+  L.recv_dy = o; o = align256(o + 2ull * rrows * h);
   L.ret_y = o;  o = align256(o + 2ull * owner * h);
   L.ret_dx = o; o = align256(o + 2ull * owner * h);
   L.total = o;
@@ -60,12 +62,19 @@ __host__ __device__ inline WinLayout win_layout(int P, int E, long long h, long 
 }
 
 // plan (int32, local): [0, P*E) counts_all | n_recv | recv_start[P+1] | send_dst[P] | send_src[P+1] | ret_off[P]
+// (arrival-order exchange) | ccomp[P*El] (this rank's experts' counts per source, compact) | n_padded |
+// my_start[E+1] | dst_base[E] | seg_pstart[El*P] | seg_len[El*P] | seg_dst[El*P] (padded exchange)
 // | error (mirror of the window's error word)
-__host__ __device__ inline int plan_ints(int P, int E) { return P * E + 1 + (P + 1) + P + (P + 1) + P + 1; }  // + error
+__host__ __device__ inline int plan_ints(int P, int E) {
+  const int El = E / P;
+  return P * E + 1 + (P + 1) + P + (P + 1) + P + P * El + 1 + (E + 1) + E + 3 * El * P + 1;
+}
 struct PlanView {
   int32_t *counts, *n_recv, *recv_start, *send_dst, *send_src, *ret_off;
+  int32_t *ccomp, *n_padded, *my_start, *dst_base, *seg_pstart, *seg_len, *seg_dst;
 };
 __device__ inline PlanView plan_view(int32_t* plan, int P, int E) {
+  const int El = E / P;
   PlanView v;
   v.counts = plan;
   v.n_recv = plan + P * E;
@@ -73,6 +82,13 @@ __device__ inline PlanView plan_view(int32_t* plan, int P, int E) {
   v.send_dst = v.recv_start + P + 1;
   v.send_src = v.send_dst + P;
   v.ret_off = v.send_src + P + 1;
+  v.ccomp = v.ret_off + P;
+  v.n_padded = v.ccomp + P * El;
+  v.my_start = v.n_padded + 1;
+  v.dst_base = v.my_start + E + 1;
+  v.seg_pstart = v.dst_base + E;
+  v.seg_len = v.seg_pstart + El * P;
+  v.seg_dst = v.seg_len + El * P;
   return v;
 }
 
@@ -158,16 +174,30 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
   signal_peers(a, 0);
   if (!wait_arrivals(a, 0)) return;
   // the plan, derived identically on every rank from the same [P, E] histograms
+  // The plan, derived identically on every rank from the same [P, E] histograms,
+  // in shared memory. Arrival-order exchange: chunk offsets (thread 0). Padded
+  // exchange: rows land directly in the owner's padded expert-grouped layout
+  // (local expert l, then source rank s, then token — the order the
+  // arrival-order path reaches after its topology), so the receiving side needs
+  // no gather and its topology follows from the counts alone.
   const volatile int32_t* cnt = reinterpret_cast<const volatile int32_t*>(peer_win(a, a.rank) + L.counts);
   PlanView v = plan_view(a.plan, a.P, a.E);
-  for (int i = threadIdx.x; i < a.P * a.E; i += blockDim.x) v.counts[i] = cnt[i];
+  extern __shared__ int32_t s_pl[];
+  const int P = a.P, E = a.E, El = a.El, r = a.rank;
+  int32_t* c = s_pl;                 // [P][E] counts
+  int32_t* pre = c + P * E;          // [P][E] exclusive prefix over e of c[s][*] (source s's sorted order)
+  int32_t* tot = pre + P * E;        // [E] over sources
+  int32_t* ps = tot + E;             // [E] padded start of global expert e in its owner's layout
+  for (int i = threadIdx.x; i < P * E; i += blockDim.x) {
+    c[i] = cnt[i];
+    v.counts[i] = c[i];
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int P = a.P, E = a.E, El = a.El, r = a.rank;
     auto chunk = [&](int s, int q) {  // rows source s sends to rank q
-      int32_t c = 0;
-      for (int e = q * El; e < (q + 1) * El; ++e) c += v.counts[s * E + e];
-      return c;
+      int32_t n = 0;
+      for (int e = q * El; e < (q + 1) * El; ++e) n += c[s * E + e];
+      return n;
     };
     int32_t acc = 0;
     for (int s = 0; s < P; ++s) {
@@ -190,6 +220,46 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
       for (int q = 0; q < r; ++q) o += chunk(s, q);
       v.ret_off[s] = o;
     }
+  }
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    int32_t t = 0;
+    for (int s2 = 0; s2 < P; ++s2) t += c[s2 * E + i];
+    tot[i] = t;
+  }
+  for (int s2 = threadIdx.x; s2 < P; s2 += blockDim.x) {
+    int32_t acc2 = 0;
+    for (int e = 0; e < E; ++e) {
+      pre[s2 * E + e] = acc2;
+      acc2 += c[s2 * E + e];
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+    int32_t acc2 = 0;
+    for (int l = 0; l < El; ++l) {
+      ps[q * El + l] = acc2;
+      acc2 += ((tot[q * El + l] + 127) / 128) * 128;
+    }
+    if (q == r) *v.n_padded = acc2;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) v.my_start[e] = e < E ? pre[r * E + e] : pre[r * E + E - 1] + c[r * E + E - 1];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t before = 0;
+    for (int s2 = 0; s2 < r; ++s2) before += c[s2 * E + e];
+    v.dst_base[e] = ps[e] + before;
+  }
+  for (int i = threadIdx.x; i < P * El; i += blockDim.x) {
+    const int s2 = i / El, l = i % El;
+    v.ccomp[i] = c[s2 * E + r * El + l];
+  }
+  for (int i = threadIdx.x; i < El * P; i += blockDim.x) {  // my segments (l, s)
+    const int l = i / P, s2 = i % P, e = r * El + l;
+    int32_t within = 0;
+    for (int s3 = 0; s3 < s2; ++s3) within += c[s3 * E + e];
+    v.seg_pstart[i] = ps[e] + within;
+    v.seg_len[i] = c[s2 * E + e];
+    v.seg_dst[i] = pre[s2 * E + e];
   }
 }
 
@@ -252,21 +322,119 @@ __global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __r
   signal_peers(a, region);
 }
 
-template <bool COMBINE>
+// Padded exchange. Dispatch: row j of this rank's expert-sorted order (source
+// row src_map[j] / src_k) belongs to global expert e (my_start) and lands in
+// the owner's padded layout at dst_base[e] + (j - my_start[e]). Combine: padded
+// row p of this rank belongs to segment (l, s) (seg_pstart; pad rows skipped)
+// and goes back to source s's return region at seg_dst + (p - seg_pstart).
+template <bool COMBINE, int VEC>
+__global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uint4* __restrict__ src, int region,
+                                                             size_t region_off, const int32_t* __restrict__ src_map,
+                                                             int src_k) {
+  PlanView v = plan_view(a.plan, a.P, a.E);
+  const int rows = COMBINE ? *v.n_padded : v.my_start[a.E];
+  const int nseg = COMBINE ? a.El * a.P : a.E;
+  // the segment tables in shared memory: the per-row binary search stays on-chip
+  extern __shared__ int32_t s_tab[];
+  int32_t* starts = s_tab;             // [nseg]
+  int32_t* lens_or_base = s_tab + nseg;  // combine: seg_len; dispatch: dst_base
+  int32_t* dsts = s_tab + 2 * nseg;      // combine: seg_dst
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    starts[i] = COMBINE ? v.seg_pstart[i] : v.my_start[i];
+    lens_or_base[i] = COMBINE ? v.seg_len[i] : v.dst_base[i];
+    if (COMBINE) dsts[i] = v.seg_dst[i];
+  }
+  __syncthreads();
+  constexpr int RV = VEC * 32;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int j0 = warp * kRowsPerWarp; j0 < rows; j0 += nwarps * kRowsPerWarp) {
+    uint4 val[kRowsPerWarp][VEC];
+    int dq[kRowsPerWarp], drow[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const int j = j0 + r;
+      dq[r] = -1;
+      if (j < rows) {
+        int lo = 0, hi = nseg - 1;  // last segment starting at or before j
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (starts[mid] <= j) lo = mid; else hi = mid - 1;
+        }
+        if (COMBINE) {
+          if (j < starts[lo] + lens_or_base[lo]) {  // else a pad row
+            dq[r] = lo % a.P;
+            drow[r] = dsts[lo] + (j - starts[lo]);
+          }
+        } else {
+          dq[r] = lo / a.El;
+          drow[r] = lens_or_base[lo] + (j - starts[lo]);
+        }
+      }
+      if (dq[r] >= 0) {
+        const int srow = src_map ? __ldg(src_map + j) / src_k : j;
+        const uint4* sp = src + (size_t)srow * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) val[r][u] = __ldg(sp + lane + 32 * u);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r)
+      if (dq[r] >= 0) {
+        uint4* dst = reinterpret_cast<uint4*>(peer_win(a, dq[r]) + region_off) + (size_t)drow[r] * RV;
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) dst[lane + 32 * u] = val[r][u];
+      }
+  }
+  signal_peers(a, region);
+}
+
+template <bool COMBINE, bool PADDED = false>
 moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream,
                           const int32_t* src_map = nullptr, int src_k = 1) {
   const EpArgs a = ep_args(ep);
   const uint4* src = reinterpret_cast<const uint4*>(rows);
   const int r = region - MOE_EP_COUNTS;
   const dim3 grid(kEpCtas), block(256);
+  const size_t tab = 3 * sizeof(int32_t) * (size_t)ep->num_experts;  // segment tables (El * P == E entries)
   cudaStream_t s = as_stream(stream);
   switch (ep->hidden / 256) {
-    case 1: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
-    case 2: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
-    case 3: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
-    case 4: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
-    case 6: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
-    case 8: MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off, src_map, src_k); break;
+    case 1:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 1>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
+    case 2:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 2>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
+    case 3:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 3>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
+    case 4:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 4>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
+    case 6:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 6>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
+    case 8:
+      if (PADDED)
+        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 8>), grid, block, tab, s, a, src, r, off, src_map, src_k);
+      else
+        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off, src_map, src_k);
+      break;
     default: return set_error(MOE_EUNSUPPORTED, "moe_ep exchange: hidden=%d must be 256 * {1,2,3,4,6,8}", ep->hidden);
   }
   return MOE_OK;
@@ -349,7 +517,15 @@ moe_status moe_ipc_close_handle(void* window) {
 moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_exchange_counts"));
   MOE_CHECK_ARG(counts_local, "moe_ep_exchange_counts: NULL counts");
-  MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), 0, as_stream(stream), ep_args(ep), counts_local);
+  const size_t smem = sizeof(int32_t) * (2 * (size_t)ep->nranks * ep->num_experts + 2 * (size_t)ep->num_experts);
+  MOE_CHECK_ARG(smem <= 200 * 1024, "moe_ep_exchange_counts: nranks * num_experts too large (%d x %d)", ep->nranks,
+                ep->num_experts);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaFuncSetAttribute(ep_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
+  MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), smem, as_stream(stream), ep_args(ep), counts_local);
   return MOE_OK;
 }
 
@@ -370,6 +546,36 @@ moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x,
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
   return ep_copy_launch<false>(ep, x, region, off, stream, sorted_idx, top_k);
+}
+
+moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+                                  int top_k, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_dispatch_padded"));
+  MOE_CHECK_ARG(x && top_k >= 1 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
+                "moe_ep_dispatch_padded: NULL x, top_k < 1 or region %d not a receive region", region);
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
+  return ep_copy_launch<false, true>(ep, x, region, off, stream, sorted_idx, sorted_idx ? top_k : 1);
+}
+
+moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_combine_padded"));
+  MOE_CHECK_ARG(rows_padded && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
+                "moe_ep_combine_padded: NULL rows or region %d not a return region", region);
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
+  return ep_copy_launch<true, true>(ep, rows_padded, region, off, stream);
+}
+
+int moe_ep_plan_offset(int nranks, int num_experts, int which) {
+  // 0 compact counts [P, E/P], 1 padded rows of this rank; computed as plan_view does
+  const int P = nranks, E = num_experts, El = E / P;
+  const int ccomp = P * E + 1 + (P + 1) + P + (P + 1) + P;
+  switch (which) {
+    case 0: return ccomp;
+    case 1: return ccomp + P * El;
+    default: return -1;
+  }
 }
 
 moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream) {

@@ -335,6 +335,12 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
   if (counts) zero_pad_rows<VEC>(dy_rows, counts, padded_bins, E, bs);
 }
 
+template <int VEC>
+__global__ void __launch_bounds__(256) zero_pad_kernel(uint4* __restrict__ dst, const int32_t* __restrict__ counts,
+                                                       const int32_t* __restrict__ padded_bins, int E, int bs) {
+  zero_pad_rows<VEC>(dst, counts, padded_bins, E, bs);
+}
+
 static int row_grid() { return moe_device_sm_count() * 8; }
 
 static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, const char* name) {
@@ -506,6 +512,15 @@ moe_status moe_unsort_rows_bwd(const moe_config* cfg, const void* dy, const void
 moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo, void* dx,
                              void* stream) {
   return moe_unsort_rows(cfg, dx_sorted, topo, nullptr, dx, stream);
+}
+
+moe_status moe_zero_pad_rows(const moe_config* cfg, const moe_topology_t* topo, void* x_g, void* stream) {
+  MOE_TRY(check_rows(cfg, topo, "moe_zero_pad_rows"));
+  MOE_CHECK_ARG(x_g, "moe_zero_pad_rows: NULL x_g");
+  cudaStream_t s = as_stream(stream);
+  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_zero_pad_rows", zero_pad_kernel, reinterpret_cast<uint4*>(x_g),
+                   topo->counts, topo->padded_bins, (int)cfg->num_experts, (int)cfg->block_size);
+  return MOE_OK;
 }
 
 }  // extern "C"

@@ -292,3 +292,24 @@ extern "C" moe_status moe_ep_recv_ids(const int32_t* counts_all, int nranks, int
              as_stream(stream), counts_all, nranks, num_experts, e0, local_experts, ids, (long long)max_rows);
   return MOE_OK;
 }
+
+extern "C" moe_status moe_topology_counts(const moe_config* cfg, const int32_t* counts_per_source, int nsources,
+                                          const moe_topology_t* topo, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(counts_per_source && nsources >= 1, "moe_topology_counts: NULL counts or nsources < 1");
+  const int E = (int)cfg->num_experts, bs = (int)cfg->block_size, F = (int)(cfg->ffn_hidden / cfg->block_size);
+  const int emit_smem = 32 * E * (int)sizeof(int32_t);
+  static int smem_set = 0;
+  if (emit_smem > 48 * 1024 - 21 * 1024 && smem_set < emit_smem) {
+    cudaFuncSetAttribute(topo_scan_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem);
+    smem_set = emit_smem;
+  }
+  const int64_t max_nnz = moe_max_nnz_blocks(cfg);
+  const int blk_ctas = (int)ceil_div(max_nnz, 1024);
+  // the per-source histograms play the per-chunk ones; no assignment is ranked (R = 0)
+  MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(nsources + blk_ctas), dim3(1024), emit_smem,
+             as_stream(stream), (const int32_t*)nullptr, 0, E, bs, F, nsources, counts_per_source, *topo,
+             (const int32_t*)nullptr, 0);
+  return MOE_OK;
+}

@@ -256,15 +256,18 @@ class ExpertParallelMoE:
         c = self.__dict__.setdefault("_ebufs", {})
         if key not in c:
             c.clear()
-            c[key] = {"ids": torch.empty(cfg_cap.tokens, dtype=torch.int32, device=device),
-                      "y": torch.empty(cfg_cap.tokens, self.h, dtype=torch.bfloat16, device=device),
-                      "dx": torch.empty(cfg_cap.tokens, self.h, dtype=torch.bfloat16, device=device)}
+            rows = self.B.moe_max_padded_rows(cfg_cap)
+            c[key] = {"topo": self.B.Topology(cfg_cap, device),
+                      "y_g": torch.empty(rows, self.h, dtype=torch.bfloat16, device=device),
+                      "dx_g": torch.empty(rows, self.h, dtype=torch.bfloat16, device=device)}
         return c[key]
 
     def _forward_p2p(self, x, wr, w1_local, w2_local):
         """Forward with device-initiated exchanges: nothing here waits for the
-        device; the receiving side runs at capacity with the live row count
-        read on the device (moe_topology_rows / moe_gather_rows)."""
+        device. Rows land directly in the owners' padded expert-grouped layout
+        (no gather on the receiving side); its topology follows from the
+        exchanged counts (moe_topology_counts) and the receiving side runs at
+        capacity with device-side sizes."""
         B = self.B
         T = x.shape[0]
         W = self._windows(T, x.device)
@@ -272,20 +275,18 @@ class ExpertParallelMoE:
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
         topo_l = self._topology(cfg_l, idx, "local")
         W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
-        recv_x = W.dispatch_tokens("x", x, topo_l["sorted_idx"], self.k)   # sorted rows into the owners' windows
+        x_g = W.dispatch_padded("x", x, topo_l["sorted_idx"], self.k)   # X_g of the owners, in their windows
         cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
         buf = self._expert_bufs(cfg_e, x.device)
-        rows = W.n_recv()
-        ids = B.moe_ep_recv_ids(W.counts_all(), self.e0, self.El, W.cap, ids=buf["ids"])
-        topo_e = self._topology_rows(cfg_e, ids, rows)
-        x_g = B.moe_gather_rows(cfg_e, recv_x, topo_e, rows)
+        topo_e = B.moe_topology_counts(cfg_e, W.compact_counts(), topo=buf["topo"])
+        B.moe_zero_pad_rows(cfg_e, topo_e, x_g)
         act_deriv = None
         if self.act != 0:
             a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
         else:
             a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
-        B.moe_dsd_scatter(cfg_e, a, w2_local, topo_e, None, y=buf["y"])   # DSD + un-pad (live rows only)
-        y_sorted = W.combine("y", buf["y"])                     # back to the token owners
+        y_g = B.moe_dsd(cfg_e, a, 0, w2_local, 0, topo_e, out=buf["y_g"])
+        y_sorted = W.combine_padded("y", y_g)                   # back to the token owners (pad rows skipped)
         y = B.moe_unsort_rows(cfg_l, y_sorted, topo_l, gates, y=torch.empty_like(x))
         st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, None, None, x_g, act_deriv, a, y_sorted, -1)
         return y, st
@@ -303,7 +304,6 @@ class ExpertParallelMoE:
         W = self.win
         cfg_l, cfg_e = st.cfg_local, st.cfg_e
         buf = self._expert_bufs(cfg_e, dy.device)
-        rows = W.n_recv()
         fused = self._fused_router(cfg_l)
         side = None
         if fused:
@@ -317,8 +317,8 @@ class ExpertParallelMoE:
                 dwr = B.moe_router_dwr(cfg_l, x, dlogits, ws=ws_l)
         else:
             dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
-        recv_dy = W.dispatch("dy", dy_sorted)
-        dy_g = B.moe_gather_rows(cfg_e, recv_dy, st.topo_e, rows)
+        dy_g = W.dispatch_padded("dy", dy_sorted, None, 1)    # already in expert order
+        B.moe_zero_pad_rows(cfg_e, st.topo_e, dy_g)
         if self.act != 0:
             dh = B.moe_sdd_deriv(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, deriv_src=st.act_deriv)
         else:
@@ -328,8 +328,8 @@ class ExpertParallelMoE:
                         out=torch.empty(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device))
         dw1 = B.moe_dds(cfg_e, st.x_g, 1, dh, 0, st.topo_e,
                         out=torch.empty(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device))
-        B.moe_dsd_dx(cfg_e, dh, w1_local, st.topo_e, dx=buf["dx"])          # DSD^T + un-pad (live rows only)
-        dx_sorted = W.combine("dx", buf["dx"])
+        dx_g = B.moe_dsd(cfg_e, dh, 0, w1_local, 1, st.topo_e, out=buf["dx_g"])   # DSD^T
+        dx_sorted = W.combine_padded("dx", dx_g)
         if fused:
             dx = B.moe_sort_rows_bwd_router(cfg_l, dx_sorted, st.topo_local, dlogits, wr, dx=torch.empty_like(dy))
             torch.cuda.current_stream(dy.device).wait_stream(side)

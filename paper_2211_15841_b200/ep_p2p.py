@@ -97,8 +97,32 @@ class PeerWindows:
         return self.plan[self.P * self.E: self.P * self.E + 1]
 
     def rows(self, name: str) -> RawRows:
-        n = self.cap if name in ("x", "dy") else self.owner
+        # receive regions hold the padded layout: up to 127 pad rows per local expert
+        n = self.cap + (self.E // self.P) * 128 if name in ("x", "dy") else self.owner
         return RawRows(self.win + self.off[name], n, self.h, self.device)
+
+    def compact_counts(self) -> torch.Tensor:
+        """[P, E/P] int32: rows of each of this rank's experts from each source (device)."""
+        o = lib.moe_ep_plan_offset(self.P, self.E, 0)
+        El = self.E // self.P
+        return self.plan[o: o + self.P * El].view(self.P, El)
+
+    def dispatch_padded(self, name: str, x: torch.Tensor, sorted_idx, top_k: int):
+        """Rows (x read through sorted_idx, or already in expert order with
+        sorted_idx None) straight into the owners' padded layouts; waits for
+        this rank's region (its pad rows still need zeroing)."""
+        check("moe_ep_dispatch_padded", lib.moe_ep_dispatch_padded(
+            ctypes.byref(self.ep), REGION[name], ctypes.c_void_p(x.data_ptr()),
+            None if sorted_idx is None else ctypes.c_void_p(sorted_idx.data_ptr()), int(top_k), self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
+        return self.rows(name)
+
+    def combine_padded(self, name: str, rows_padded):
+        """This rank's padded rows back to their sources' return regions; waits for this rank's."""
+        check("moe_ep_combine_padded", lib.moe_ep_combine_padded(ctypes.byref(self.ep), REGION[name],
+                                                                 ctypes.c_void_p(rows_padded.data_ptr()), self._s()))
+        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
+        return self.rows(name)
 
     # ---- exchanges (stream-ordered on the current stream)
     @staticmethod

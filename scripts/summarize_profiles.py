@@ -98,7 +98,47 @@ def gemm_full(tag, label):
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
 
 
+def perm_full(tag, label):
+    """ncu --set full of the HBM-bound non-GEMM kernels (topology, permutations,
+    scatter backward): achieved DRAM GB/s against the measured copy bandwidth."""
+    rep = os.path.join(ROOT, "gpurun_out", f"prof_perm_{tag}.ncu-rep")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, data = rows[0], rows[2:]
+    ix = {h: i for i, h in enumerate(hdr)}
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    bw = float(peaks["hbm_gbs"])
+
+    def g(d, k):
+        try:
+            return float(d[ix[k]])
+        except (KeyError, ValueError):
+            return float("nan")
+    out = [f"# {label} — ncu --set full, one C1 (MoE-XS) step, non-GEMM kernels", "",
+           f"Source: `gpurun_out/prof_perm_{tag}.ncu-rep` (ncu --set full --clock-control none, kernels topo_*, "
+           "scatter_rows (padded gather), scatter_bwd (+ router dlogits)). DRAM GB/s = (read + write bytes) / ncu "
+           f"duration, against the measured {bw:.0f} GB/s copy (MEASURED_PEAKS.json). Cold-cache, serialised.", "",
+           "| kernel | ncu us | DRAM read MB | DRAM write MB | DRAM GB/s | frac of copy BW | DRAM % peak (ncu) | issue % |",
+           "|---|---|---|---|---|---|---|---|"]
+    seen = set()
+    for d in data:
+        k = re.sub(r"[(].*", "", d[ix["Kernel Name"]]).replace("moe::", "")
+        if k in seen:
+            continue
+        seen.add(k)
+        us = g(d, "gpu__time_duration.sum")
+        rd, wr = g(d, "dram__bytes_read.sum"), g(d, "dram__bytes_write.sum")
+        gbs = (rd + wr) * 1e6 / (us * 1e-6) / 1e9 if us > 0 else float("nan")
+        out.append(f"| `{k[:48]}` | {us:.1f} | {rd:.1f} | {wr:.1f} | {gbs:.0f} | {gbs / bw:.2f} | "
+                   f"{g(d, 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
+                   f"{g(d, 'sm__inst_issued.avg.pct_of_peak_sustained_active'):.1f} |")
+    open(os.path.join(ROOT, "profiles", f"{label}_permute_ncu_full.md"), "w").write("\n".join(out) + "\n")
+
+
 if __name__ == "__main__":
     tag, label = sys.argv[1], sys.argv[2]
-    launches(tag, label)
-    gemm_full(tag, label)
+    if len(sys.argv) > 3 and sys.argv[3] == "perm":
+        perm_full(tag, label)
+    else:
+        launches(tag, label)
+        gemm_full(tag, label)
