@@ -260,17 +260,8 @@ moe_status moe_ipc_open_handle(const void* handle /* 64 bytes */, void** window)
 moe_status moe_ipc_close_handle(void* window);
 /* counts_local [E] int32 device: this rank's per-global-expert histogram
  * (moe_topology counts). Stores it into every peer, waits for all P rows, and
- * writes ep->plan; plan[P*E] = rows this rank receives (the device-side row
- * count for moe_topology_rows / moe_gather_rows). One CTA. */
+ * writes ep->plan; plan[P*E] = rows this rank receives. One CTA. */
 moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_local, void* stream);
-/* region MOE_EP_RECV_X / MOE_EP_RECV_DY: rows [T*k, hidden] bf16 in this
- * rank's expert-sorted order go to their experts' owners' receive regions. */
-moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, void* stream);
-/* moe_ep_dispatch fused with moe_sort_rows: x [T, hidden] in token order;
- * row j of the expert-sorted order is x[sorted_idx[j] / top_k] (sorted_idx of
- * the rank's moe_topology over the global experts). */
-moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
-                                  int top_k, void* stream);
 /* Padded exchange (the receiving side needs no gather): rows land directly in
  * the owner's padded expert-grouped layout (local expert, then source
  * rank, then token; pad rows at each expert's tail are NOT written — zero them
@@ -297,19 +288,8 @@ moe_status moe_topology_counts(const moe_config* cfg, const int32_t* counts_per_
 /* Zero the pad rows (tail of each expert group) of a padded [max_rows, h] buffer. */
 moe_status moe_zero_pad_rows(const moe_config* cfg, const moe_topology_t* topo, void* x_g, void* stream);
 
-/* region MOE_EP_RET_Y / MOE_EP_RET_DX: received rows [n_recv, hidden] bf16
- * (arrival order) go back to their source ranks' return regions. */
-moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream);
 /* Stream-ordered wait until every source's next exchange of `region` landed here. */
 moe_status moe_ep_wait(const moe_ep_t* ep, int region, void* stream);
-
-/* Device-side row count variants for the receiving side of the exchange:
- * cfg->tokens * top_k is the capacity (buffer sizes, grids); the live count is
- * *rows_dev (device int32, <= capacity), read by the kernels. */
-moe_status moe_topology_rows(const moe_config* cfg, const int32_t* expert_idx, const int32_t* rows_dev,
-                             const moe_topology_t* topo, void* ws, void* stream);
-moe_status moe_gather_rows(const moe_config* cfg, const void* x, const moe_topology_t* topo, const int32_t* rows_dev,
-                           void* x_g, void* stream);
 
 /* Expert-parallel receive ids (DESIGN.md §7 ordering contract): rows
  * arrive ordered (source rank q, local expert l, token); ids[i] = l of arrival

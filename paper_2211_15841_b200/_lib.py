@@ -90,17 +90,12 @@ SIGNATURES = {
     "moe_ipc_open_handle": (STATUS, [P, ctypes.POINTER(ctypes.c_void_p)]),
     "moe_ipc_close_handle": (STATUS, [P]),
     "moe_ep_exchange_counts": (STATUS, [ctypes.POINTER(MoeEp), P, P]),
-    "moe_ep_dispatch": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
-    "moe_ep_combine": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
-    "moe_ep_dispatch_tokens": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P, ctypes.c_int, P]),
     "moe_ep_dispatch_padded": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P, ctypes.c_int, P]),
     "moe_ep_combine_padded": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, P]),
     "moe_ep_plan_offset": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "moe_topology_counts": (STATUS, [CFG, P, ctypes.c_int, TOPO, P]),
     "moe_zero_pad_rows": (STATUS, [CFG, TOPO, P, P]),
     "moe_ep_wait": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P]),
-    "moe_topology_rows": (STATUS, [CFG, P, P, TOPO, P, P]),
-    "moe_gather_rows": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_ep_recv_ids": (STATUS, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P]),
     "moe_sdd": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_sdd_deriv": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P, P]),

@@ -135,23 +135,6 @@ def moe_topology(cfg, expert_idx, topo: Topology | None = None, ws=None) -> Topo
     return topo
 
 
-def moe_topology_rows(cfg, expert_idx, rows_dev, topo: Topology | None = None, ws=None) -> Topology:
-    """moe_topology_rows (include/moe.h): cfg.tokens is the capacity, rows_dev
-    (device int32 scalar tensor) the live assignment count."""
-    topo = topo if topo is not None else Topology(cfg, expert_idx.device)
-    ws = ws if ws is not None else workspace(cfg, expert_idx.device)
-    check("moe_topology_rows", lib.moe_topology_rows(ctypes.byref(cfg), _p(expert_idx), _p(rows_dev),
-                                                     ctypes.byref(topo.struct), _p(ws), _stream()))
-    return topo
-
-
-def moe_gather_rows(cfg, x, topo: Topology, rows_dev, x_g=None):
-    x_g = x_g if x_g is not None else torch.empty(moe_max_padded_rows(cfg), cfg.hidden, dtype=x.dtype, device=x.device)
-    check("moe_gather_rows", lib.moe_gather_rows(ctypes.byref(cfg), _p(x), ctypes.byref(topo.struct), _p(rows_dev),
-                                                 _p(x_g), _stream()))
-    return x_g
-
-
 def moe_topology_counts(cfg, counts_per_source, topo: Topology | None = None) -> Topology:
     """moe_topology_counts (include/moe.h): topology of rows grouped by expert
     then source, from the [nsources, E] int32 device counts."""

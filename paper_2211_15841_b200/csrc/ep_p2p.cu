@@ -10,12 +10,13 @@
 //            counts[rank, :], then bumps the peer's arrival counter; one CTA
 //            waits for all P rows and derives the exchange plan on the device
 //            (rows received, chunk offsets) — no device->host copy.
-//   dispatch sender row j of the expert-ordered rows (moe_sort_rows) goes to
-//            the owner q of its expert, at q's receive offset for this source
-//            (arrival order: source rank, local expert, token — the ordering
-//            contract of DESIGN.md §7, identical to the NCCL all-to-all path).
-//   combine  receiver row i (from source s) goes back to s's return region at
-//            the position s sorted it from.
+//   dispatch sender row j of its expert-ordered rows (x read through the
+//            topology's sorted_idx) goes to the owner of its expert, straight
+//            into the owner's padded expert-grouped layout (local expert, then
+//            source rank, then token — DESIGN.md §7), so the owner needs no
+//            gather and builds its topology from the counts alone.
+//   combine  the owner's padded rows (pad rows skipped) go back to their source
+//            ranks' return regions at the positions the sources sorted them from.
 //
 // Completion: each CTA fences its peer stores (fence.sc.sys), counts itself
 // on a local counter; the last CTA resets it and bumps every destination's
@@ -61,28 +62,22 @@ __host__ __device__ inline WinLayout win_layout(int P, int E, long long h, long 
   return L;
 }
 
-// plan (int32, local): [0, P*E) counts_all | n_recv | recv_start[P+1] | send_dst[P] | send_src[P+1] | ret_off[P]
-// (arrival-order exchange) | ccomp[P*El] (this rank's experts' counts per source, compact) | n_padded |
-// my_start[E+1] | dst_base[E] | seg_pstart[El*P] | seg_len[El*P] | seg_dst[El*P] (padded exchange)
-// | error (mirror of the window's error word)
+// plan (int32, local): [0, P*E) counts_all | n_recv | ccomp[P*El] (this rank's experts' counts per
+// source, compact) | n_padded | my_start[E+1] | dst_base[E] | seg_pstart[El*P] | seg_len[El*P] |
+// seg_dst[El*P] | error (mirror of the window's error word)
 __host__ __device__ inline int plan_ints(int P, int E) {
   const int El = E / P;
-  return P * E + 1 + (P + 1) + P + (P + 1) + P + P * El + 1 + (E + 1) + E + 3 * El * P + 1;
+  return P * E + 1 + P * El + 1 + (E + 1) + E + 3 * El * P + 1;
 }
 struct PlanView {
-  int32_t *counts, *n_recv, *recv_start, *send_dst, *send_src, *ret_off;
-  int32_t *ccomp, *n_padded, *my_start, *dst_base, *seg_pstart, *seg_len, *seg_dst;
+  int32_t *counts, *n_recv, *ccomp, *n_padded, *my_start, *dst_base, *seg_pstart, *seg_len, *seg_dst;
 };
 __device__ inline PlanView plan_view(int32_t* plan, int P, int E) {
   const int El = E / P;
   PlanView v;
   v.counts = plan;
   v.n_recv = plan + P * E;
-  v.recv_start = v.n_recv + 1;
-  v.send_dst = v.recv_start + P + 1;
-  v.send_src = v.send_dst + P;
-  v.ret_off = v.send_src + P + 1;
-  v.ccomp = v.ret_off + P;
+  v.ccomp = v.n_recv + 1;
   v.n_padded = v.ccomp + P * El;
   v.my_start = v.n_padded + 1;
   v.dst_base = v.my_start + E + 1;
@@ -175,8 +170,7 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
   if (!wait_arrivals(a, 0)) return;
   // the plan, derived identically on every rank from the same [P, E] histograms
   // The plan, derived identically on every rank from the same [P, E] histograms,
-  // in shared memory. Arrival-order exchange: chunk offsets (thread 0). Padded
-  // exchange: rows land directly in the owner's padded expert-grouped layout
+  // in shared memory: rows land directly in the owner's padded expert-grouped layout
   // (local expert l, then source rank s, then token — the order the
   // arrival-order path reaches after its topology), so the receiving side needs
   // no gather and its topology follows from the counts alone.
@@ -193,33 +187,11 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
     v.counts[i] = c[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    auto chunk = [&](int s, int q) {  // rows source s sends to rank q
-      int32_t n = 0;
-      for (int e = q * El; e < (q + 1) * El; ++e) n += c[s * E + e];
-      return n;
-    };
-    int32_t acc = 0;
-    for (int s = 0; s < P; ++s) {
-      v.recv_start[s] = acc;
-      acc += chunk(s, r);
-    }
-    v.recv_start[P] = acc;
-    *v.n_recv = acc;
-    int32_t so = 0;
-    for (int q = 0; q < P; ++q) {
-      int32_t d = 0;
-      for (int s = 0; s < r; ++s) d += chunk(s, q);
-      v.send_dst[q] = d;   // where my chunk lands in q's receive region
-      v.send_src[q] = so;  // where my chunk for q starts in my expert-ordered rows
-      so += chunk(r, q);
-    }
-    v.send_src[P] = so;
-    for (int s = 0; s < P; ++s) {  // where my rows from s go back in s's return region
-      int32_t o = 0;
-      for (int q = 0; q < r; ++q) o += chunk(s, q);
-      v.ret_off[s] = o;
-    }
+  if (threadIdx.x == 0) {  // rows this rank receives
+    int32_t n = 0;
+    for (int s2 = 0; s2 < P; ++s2)
+      for (int e = r * El; e < (r + 1) * El; ++e) n += c[s2 * E + e];
+    *v.n_recv = n;
   }
   for (int i = threadIdx.x; i < E; i += blockDim.x) {
     int32_t t = 0;
@@ -279,48 +251,7 @@ EpArgs ep_args(const moe_ep_t* ep) {
   return a;
 }
 
-// Row copy to peers. dispatch: rows [0, send_src[P]) of src by destination;
-// combine: rows [0, n_recv) of src back to their source ranks. Each warp moves
-// kRowsPerWarp rows per iteration (all loads, then all stores) so enough bytes
-// are in flight per SM to run at bandwidth rather than at load latency.
-constexpr int kRowsPerWarp = 4;
-// src_map (dispatch only, optional): row j of the expert-sorted order is source
-// row src_map[j] / src_k (moe_topology's sorted_idx: the sort is fused here).
-template <bool COMBINE, int VEC>
-__global__ void __launch_bounds__(256) ep_copy_kernel(EpArgs a, const uint4* __restrict__ src, int region,
-                                                      size_t region_off, const int32_t* __restrict__ src_map,
-                                                      int src_k) {
-  PlanView v = plan_view(a.plan, a.P, a.E);
-  const int rows = COMBINE ? *v.n_recv : v.send_src[a.P];
-  const int32_t* starts = COMBINE ? v.recv_start : v.send_src;
-  const int32_t* dbase = COMBINE ? v.ret_off : v.send_dst;
-  constexpr int RV = VEC * 32;  // uint4 per row (hidden = 256 * VEC)
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int j0 = warp * kRowsPerWarp; j0 < rows; j0 += nwarps * kRowsPerWarp) {
-    uint4 val[kRowsPerWarp][VEC];
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r)
-      if (j0 + r < rows) {
-        const int srow = src_map ? __ldg(src_map + j0 + r) / src_k : j0 + r;
-        const uint4* sp = src + (size_t)srow * RV;
-#pragma unroll
-        for (int u = 0; u < VEC; ++u) val[r][u] = __ldg(sp + lane + 32 * u);
-      }
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
-      const int j = j0 + r;
-      if (j < rows) {
-        int q = 0;
-        while (q + 1 < a.P && starts[q + 1] <= j) ++q;
-        uint4* dst = reinterpret_cast<uint4*>(peer_win(a, q) + region_off) + (size_t)(dbase[q] + (j - starts[q])) * RV;
-#pragma unroll
-        for (int u = 0; u < VEC; ++u) dst[lane + 32 * u] = val[r][u];
-      }
-    }
-  }
-  signal_peers(a, region);
-}
+constexpr int kRowsPerWarp = 4;  // rows in flight per warp (all loads, then all stores)
 
 // Padded exchange. Dispatch: row j of this rank's expert-sorted order (source
 // row src_map[j] / src_k) belongs to global expert e (my_start) and lands in
@@ -389,7 +320,7 @@ __global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uin
   signal_peers(a, region);
 }
 
-template <bool COMBINE, bool PADDED = false>
+template <bool COMBINE>
 moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream,
                           const int32_t* src_map = nullptr, int src_k = 1) {
   const EpArgs a = ep_args(ep);
@@ -399,42 +330,12 @@ moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size
   const size_t tab = 3 * sizeof(int32_t) * (size_t)ep->num_experts;  // segment tables (El * P == E entries)
   cudaStream_t s = as_stream(stream);
   switch (ep->hidden / 256) {
-    case 1:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 1>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 1>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
-    case 2:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 2>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 2>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
-    case 3:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 3>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 3>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
-    case 4:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 4>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 4>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
-    case 6:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 6>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 6>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
-    case 8:
-      if (PADDED)
-        MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 8>), grid, block, tab, s, a, src, r, off, src_map, src_k);
-      else
-        MOE_LAUNCH("ep_copy", (ep_copy_kernel<COMBINE, 8>), grid, block, 0, s, a, src, r, off, src_map, src_k);
-      break;
+    case 1: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 1>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
+    case 2: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 2>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
+    case 3: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 3>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
+    case 4: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 4>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
+    case 6: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 6>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
+    case 8: MOE_LAUNCH("ep_copy", (ep_copy_padded_kernel<COMBINE, 8>), grid, block, tab, s, a, src, r, off, src_map, src_k); break;
     default: return set_error(MOE_EUNSUPPORTED, "moe_ep exchange: hidden=%d must be 256 * {1,2,3,4,6,8}", ep->hidden);
   }
   return MOE_OK;
@@ -529,25 +430,6 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
   return MOE_OK;
 }
 
-moe_status moe_ep_dispatch(const moe_ep_t* ep, int region, const void* rows, void* stream) {
-  MOE_TRY(check_ep(ep, "moe_ep_dispatch"));
-  MOE_CHECK_ARG(rows && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
-                "moe_ep_dispatch: NULL rows or region %d not a receive region", region);
-  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
-  const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
-  return ep_copy_launch<false>(ep, rows, region, off, stream);
-}
-
-moe_status moe_ep_dispatch_tokens(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
-                                  int top_k, void* stream) {
-  MOE_TRY(check_ep(ep, "moe_ep_dispatch_tokens"));
-  MOE_CHECK_ARG(x && sorted_idx && top_k >= 1 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
-                "moe_ep_dispatch_tokens: NULL x / sorted_idx, top_k < 1 or region %d not a receive region", region);
-  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
-  const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
-  return ep_copy_launch<false>(ep, x, region, off, stream, sorted_idx, top_k);
-}
-
 moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
                                   int top_k, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_dispatch_padded"));
@@ -555,7 +437,7 @@ moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x,
                 "moe_ep_dispatch_padded: NULL x, top_k < 1 or region %d not a receive region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
-  return ep_copy_launch<false, true>(ep, x, region, off, stream, sorted_idx, sorted_idx ? top_k : 1);
+  return ep_copy_launch<false>(ep, x, region, off, stream, sorted_idx, sorted_idx ? top_k : 1);
 }
 
 moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream) {
@@ -564,27 +446,18 @@ moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* row
                 "moe_ep_combine_padded: NULL rows or region %d not a return region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
-  return ep_copy_launch<true, true>(ep, rows_padded, region, off, stream);
+  return ep_copy_launch<true>(ep, rows_padded, region, off, stream);
 }
 
 int moe_ep_plan_offset(int nranks, int num_experts, int which) {
   // 0 compact counts [P, E/P], 1 padded rows of this rank; computed as plan_view does
   const int P = nranks, E = num_experts, El = E / P;
-  const int ccomp = P * E + 1 + (P + 1) + P + (P + 1) + P;
+  const int ccomp = P * E + 1;
   switch (which) {
     case 0: return ccomp;
     case 1: return ccomp + P * El;
     default: return -1;
   }
-}
-
-moe_status moe_ep_combine(const moe_ep_t* ep, int region, const void* rows, void* stream) {
-  MOE_TRY(check_ep(ep, "moe_ep_combine"));
-  MOE_CHECK_ARG(rows && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
-                "moe_ep_combine: NULL rows or region %d not a return region", region);
-  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
-  const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
-  return ep_copy_launch<true>(ep, rows, region, off, stream);
 }
 
 moe_status moe_ep_wait(const moe_ep_t* ep, int region, void* stream) {

@@ -65,11 +65,9 @@ template <int VEC>
 __global__ void __launch_bounds__(256) scatter_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ map,
                                                             uint4* __restrict__ dst, int R, int k,
                                                             const int32_t* __restrict__ counts,
-                                                            const int32_t* __restrict__ padded_bins, int E, int bs,
-                                                            const int32_t* __restrict__ R_dev) {
+                                                            const int32_t* __restrict__ padded_bins, int E, int bs) {
   pdl_trigger();
   pdl_wait();
-  if (R_dev) R = min(R, __ldg(R_dev));   // live row count known only on the device (expert parallelism)
   constexpr int ROWS = 8 / VEC;
   constexpr int RV = VEC * 32;  // uint4 per row
   const int lane = threadIdx.x & 31;
@@ -435,19 +433,7 @@ moe_status moe_gather(const moe_config* cfg, const void* x, const moe_topology_t
   const int R = (int)(cfg->tokens * cfg->top_k);
   MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_gather", scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->pos,
                    reinterpret_cast<uint4*>(x_g), R, (int)cfg->top_k, topo->counts, topo->padded_bins,
-                   (int)cfg->num_experts, (int)cfg->block_size, (const int32_t*)nullptr);
-  return MOE_OK;
-}
-
-moe_status moe_gather_rows(const moe_config* cfg, const void* x, const moe_topology_t* topo, const int32_t* rows_dev,
-                           void* x_g, void* stream) {
-  MOE_TRY(check_rows(cfg, topo, "moe_gather_rows"));
-  MOE_CHECK_ARG(x && x_g && rows_dev, "moe_gather_rows: NULL pointer");
-  cudaStream_t s = as_stream(stream);
-  const int R = (int)(cfg->tokens * cfg->top_k);
-  MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_gather_rows", scatter_rows_kernel, reinterpret_cast<const uint4*>(x),
-                   topo->pos, reinterpret_cast<uint4*>(x_g), R, (int)cfg->top_k, topo->counts, topo->padded_bins,
-                   (int)cfg->num_experts, (int)cfg->block_size, rows_dev);
+                   (int)cfg->num_experts, (int)cfg->block_size);
   return MOE_OK;
 }
 
@@ -486,8 +472,7 @@ moe_status moe_sort_rows(const moe_config* cfg, const void* x, const moe_topolog
   cudaStream_t s = as_stream(stream);
   const int R = (int)(cfg->tokens * cfg->top_k);
   MOE_VEC_DISPATCH((int)(cfg->hidden / 256), "moe_sort_rows", scatter_rows_kernel, reinterpret_cast<const uint4*>(x), topo->sorted_pos,
-                   reinterpret_cast<uint4*>(x_sorted), R, (int)cfg->top_k, nullptr, nullptr, 0, 1,
-                   (const int32_t*)nullptr);
+                   reinterpret_cast<uint4*>(x_sorted), R, (int)cfg->top_k, nullptr, nullptr, 0, 1);
   return MOE_OK;
 }
 

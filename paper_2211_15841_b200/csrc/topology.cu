@@ -23,11 +23,9 @@
 
 namespace moe {
 
-__global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, int32_t* __restrict__ chunk_counts,
-                                 const int32_t* __restrict__ R_dev) {
+__global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, int32_t* __restrict__ chunk_counts) {
   pdl_trigger();
   pdl_wait();
-  if (R_dev) R = min(R, __ldg(R_dev));   // live row count known only on the device (expert parallelism)
   extern __shared__ int32_t s_cnt[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_cnt[e] = 0;
   __syncthreads();
@@ -47,11 +45,9 @@ __global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, 
 __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs,
                                                                int F, int n_chunks,
                                                                const int32_t* __restrict__ chunk_counts,
-                                                               moe_topology_t topo, const int32_t* __restrict__ R_dev,
-                                                               int capacity) {
+                                                               moe_topology_t topo, int capacity) {
   pdl_trigger();
   pdl_wait();
-  if (R_dev) R = min(R, __ldg(R_dev));
   extern __shared__ int32_t s_dyn[];           // [32 warps][E] per-warp counts (ranking CTAs)
   __shared__ int32_t s_cnt[1024], s_start[1024], s_pstart[1024], s_pair[1024], s_base[1024];
   __shared__ int32_t s_tot[3];
@@ -242,8 +238,8 @@ __global__ void ep_recv_ids_kernel(const int32_t* __restrict__ counts_all, int P
 
 using namespace moe;
 
-static moe_status topology_impl(const moe_config* cfg, const int32_t* expert_idx, const int32_t* rows_dev,
-                                const moe_topology_t* topo, void* ws, void* stream) {
+extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
+                                   void* ws, void* stream) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(expert_idx && ws, "moe_topology: NULL expert_idx or workspace");
@@ -254,7 +250,7 @@ static moe_status topology_impl(const moe_config* cfg, const int32_t* expert_idx
   int32_t* chunk_counts = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + L.topo_chunk_counts);
   cudaStream_t s = as_stream(stream);
   MOE_LAUNCH("topo_hist", topo_hist_kernel, dim3(n_chunks), dim3(kTopoChunk), E * sizeof(int32_t), s, expert_idx, R, E,
-             chunk_counts, rows_dev);
+             chunk_counts);
   const int emit_smem = 32 * E * (int)sizeof(int32_t);
   static int smem_set = 0;
   if (emit_smem > 48 * 1024 - 21 * 1024 && smem_set < emit_smem) {
@@ -264,19 +260,8 @@ static moe_status topology_impl(const moe_config* cfg, const int32_t* expert_idx
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
-             E, bs, F, n_chunks, chunk_counts, *topo, rows_dev, (int)cfg->capacity);
+             E, bs, F, n_chunks, chunk_counts, *topo, (int)cfg->capacity);
   return MOE_OK;
-}
-
-extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
-                                   void* ws, void* stream) {
-  return topology_impl(cfg, expert_idx, nullptr, topo, ws, stream);
-}
-
-extern "C" moe_status moe_topology_rows(const moe_config* cfg, const int32_t* expert_idx, const int32_t* rows_dev,
-                                        const moe_topology_t* topo, void* ws, void* stream) {
-  MOE_CHECK_ARG(rows_dev, "moe_topology_rows: NULL rows_dev");
-  return topology_impl(cfg, expert_idx, rows_dev, topo, ws, stream);
 }
 
 extern "C" moe_status moe_ep_recv_ids(const int32_t* counts_all, int nranks, int num_experts, int e0, int local_experts,
@@ -309,7 +294,6 @@ extern "C" moe_status moe_topology_counts(const moe_config* cfg, const int32_t* 
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   // the per-source histograms play the per-chunk ones; no assignment is ranked (R = 0)
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(nsources + blk_ctas), dim3(1024), emit_smem,
-             as_stream(stream), (const int32_t*)nullptr, 0, E, bs, F, nsources, counts_per_source, *topo,
-             (const int32_t*)nullptr, 0);
+             as_stream(stream), (const int32_t*)nullptr, 0, E, bs, F, nsources, counts_per_source, *topo, 0);
   return MOE_OK;
 }

@@ -291,14 +291,6 @@ class ExpertParallelMoE:
         st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, None, None, x_g, act_deriv, a, y_sorted, -1)
         return y, st
 
-    def _topology_rows(self, cfg, ids, rows):
-        cache = self.__dict__.setdefault("_topo_cache", {})
-        key = ("experts_rows", cfg.tokens, cfg.num_experts)
-        if key not in cache:
-            cache[key] = (self.B.Topology(cfg, ids.device), self.B.workspace(cfg, ids.device))
-        tp, ws = cache[key]
-        return self.B.moe_topology_rows(cfg, ids, rows, topo=tp, ws=ws)
-
     def _backward_p2p(self, st: EPState, x, dy, wr, w1_local, w2_local, reduce_dwr=True):
         B = self.B
         W = self.win

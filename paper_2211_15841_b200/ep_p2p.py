@@ -133,29 +133,6 @@ class PeerWindows:
         check("moe_ep_exchange_counts", lib.moe_ep_exchange_counts(ctypes.byref(self.ep),
                                                                    ctypes.c_void_p(counts_local.data_ptr()), self._s()))
 
-    def dispatch(self, name: str, rows: torch.Tensor):
-        """rows [T*k, h] in this rank's expert order -> owners' receive regions; waits for this rank's."""
-        check("moe_ep_dispatch", lib.moe_ep_dispatch(ctypes.byref(self.ep), REGION[name],
-                                                     ctypes.c_void_p(rows.data_ptr()), self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
-        return self.rows(name)
-
-    def dispatch_tokens(self, name: str, x: torch.Tensor, sorted_idx: torch.Tensor, top_k: int):
-        """x [T, h] in token order, sent in expert-sorted order (sorted_idx): the
-        sort fused into the dispatch; waits for this rank's receive region."""
-        check("moe_ep_dispatch_tokens", lib.moe_ep_dispatch_tokens(
-            ctypes.byref(self.ep), REGION[name], ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(sorted_idx.data_ptr()),
-            int(top_k), self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
-        return self.rows(name)
-
-    def combine(self, name: str, rows):
-        """received rows [n_recv, h] -> their sources' return regions; waits for this rank's."""
-        check("moe_ep_combine", lib.moe_ep_combine(ctypes.byref(self.ep), REGION[name],
-                                                   ctypes.c_void_p(rows.data_ptr()), self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
-        return self.rows(name)
-
     def error_word(self) -> int:
         """0, or 1 + the arrival region whose wait timed out (the plan's last
         int, mirrored from the window's error word). Reads the device."""
