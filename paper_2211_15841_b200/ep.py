@@ -88,9 +88,12 @@ class ExpertParallelMoE:
     """
 
     def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128,
-                 transport="nccl"):
+                 transport="nccl", renormalize=False):
+        """renormalize: top-k gates divided by their sum (the token owner's
+        router and its backward; the expert side is unaffected)."""
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        self.renormalize = bool(renormalize)
         self.B = backend
         self.group = group
         self.transport = transport
@@ -102,7 +105,10 @@ class ExpertParallelMoE:
         self.El = self.e1 - self.e0
 
     def _cfg(self, tokens, experts, k):
-        return self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
+        cfg = self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
+        if self.renormalize and experts == self.E:   # the token owner's (router) config
+            cfg.renormalize = 1
+        return cfg
 
     def _topology(self, cfg, ids, slot):
         """moe_topology into device arrays and a workspace cached per slot. The

@@ -38,7 +38,7 @@ class Topo:
 
 def moe_router(cfg, x, wr):
     L = O.router_logits(_np(x), _np(wr))
-    idx, g = O.topk(L, cfg.top_k)
+    idx, g = O.topk(L, cfg.top_k, bool(getattr(cfg, "renormalize", 0)))
     return _t(L), torch.from_numpy(idx), _t(g)
 
 
@@ -184,9 +184,12 @@ def _dlogits(cfg, logits, expert_idx, dgates):
     L, idx, dg = _np(logits), expert_idx.numpy(), _np(dgates)
     p = O.softmax(L)
     dp = np.zeros_like(p)
+    renorm = bool(getattr(cfg, "renormalize", 0))
     for t in range(L.shape[0]):
+        S = sum(p[t, idx[t, i]] for i in range(cfg.top_k))
+        gd = sum(dg[t, i] * p[t, idx[t, i]] / S for i in range(cfg.top_k))
         for j in range(cfg.top_k):
-            dp[t, idx[t, j]] += dg[t, j]
+            dp[t, idx[t, j]] += (dg[t, j] - gd) / S if renorm else dg[t, j]
     return p * (dp - (p * dp).sum(1, keepdims=True))
 
 

@@ -49,7 +49,8 @@ def run(rank, world, port, cfg, q):
         wr = inp["wr"].to(d)
         w1 = inp["w1"][:, e0 * f:e1 * f].contiguous().to(d)
         w2 = inp["w2"][e0 * f:e1 * f].contiguous().to(d)
-        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, E, shp.top_k, f, act=shp.act, transport="p2p")
+        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, E, shp.top_k, f, act=shp.act, transport="p2p",
+                                     renormalize=cfg.get("renorm", False))
         outs = []
         for _ in range(cfg.get("steps", 2)):   # repeated steps exercise the cumulative epochs
             y, st = layer.forward(x, wr, w1, w2)

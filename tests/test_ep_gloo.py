@@ -42,7 +42,8 @@ def _worker(rank, world, port, cfgd, q):
     sl = slice(rank * T, (rank + 1) * T)
     e0, e1 = ep.local_expert_range(rank, world, E)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
-    layer = ep.ExpertParallelMoE(B, dist.group.WORLD, h, E, k, f, act=act, block_size=4)
+    layer = ep.ExpertParallelMoE(B, dist.group.WORLD, h, E, k, f, act=act, block_size=4,
+                                 renormalize=cfgd.get("renorm", False))
     xl, dyl = t(x[sl]), t(dy[sl])
     w1l, w2l = t(w1[:, e0 * f:e1 * f]), t(w2[e0 * f:e1 * f])
     y, st = layer.forward(xl, t(wr), w1l, w2l)
@@ -53,7 +54,7 @@ def _worker(rank, world, port, cfgd, q):
 
 
 @pytest.mark.parametrize("cfgd", [dict(T=24, h=6, f=8, E=4, k=1, act=1), dict(T=17, h=4, f=4, E=6, k=2, act=2),
-                                  dict(T=9, h=4, f=4, E=2, k=1, act=0)])
+                                  dict(T=9, h=4, f=4, E=2, k=1, act=0), dict(T=15, h=4, f=4, E=4, k=2, act=1, renorm=True)])
 def test_ep_world2_matches_global_oracle(cfgd):
     world = 2
     ctx = mp.get_context("spawn")
@@ -71,7 +72,7 @@ def test_ep_world2_matches_global_oracle(cfgd):
         assert p.exitcode == 0
     T, h, f, E, k, act = cfgd["T"], cfgd["h"], cfgd["f"], cfgd["E"], cfgd["k"], cfgd["act"]
     x, wr, w1, w2, dy = _inputs(T * world, h, f, E, 0)
-    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, act)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, act, renormalize=cfgd.get("renorm", False))
     g = O.dmoe_backward(cache, dy, wr, w1, w2)
     El = E // world
     for r in range(world):

@@ -725,7 +725,9 @@ def test_expert_parallel_single_rank_nccl():
 def _check_ep_against_oracle(res, world, T, shp, cfg):
     import ep_p2p_worker
     inp = ep_p2p_worker.make_global_inputs(shp, cfg, T * world)
-    yo, cache, go = oracle_layer(inp, shp, T * world)
+    x, wr, w1, w2, dy = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    yo, cache = O.dmoe_forward(x, wr, w1, w2, shp.top_k, 128, shp.ffn, shp.act, renormalize=cfg.get("renorm", False))
+    go = O.dmoe_backward(cache, dy, wr, w1, w2)
     E, f = shp.experts, shp.ffn
     El = E // world
     for r in range(world):
@@ -747,9 +749,10 @@ def _check_ep_against_oracle(res, world, T, shp, cfg):
             assert rel_fro(dw2, want2) < FRO_TOL
 
 
-@pytest.mark.parametrize("world,shape,T,starve", [(1, "C4", 512, False), (2, "C4", 384, False), (2, "C0", 500, False),
-                                                  (4, "C1", 256, False), (2, "C1", 300, True)])
-def test_expert_parallel_p2p(world, shape, T, starve):
+@pytest.mark.parametrize("world,shape,T,starve,renorm", [(1, "C4", 512, False, False), (2, "C4", 384, False, False),
+                                                         (2, "C0", 500, False, False), (4, "C1", 256, False, False),
+                                                         (2, "C1", 300, True, False), (2, "C4", 256, False, True)])
+def test_expert_parallel_p2p(world, shape, T, starve, renorm):
     """ExpertParallelMoE with the peer-memory transport (device-initiated
     dispatch / combine through CUDA IPC windows, device-side row counts on the
     receiving side, no host synchronisation): `world` processes share cuda:0
@@ -766,7 +769,7 @@ def test_expert_parallel_p2p(world, shape, T, starve):
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    cfg = dict(shape=shape, T=T, seed=21, steps=2, starve=starve, world=world)
+    cfg = dict(shape=shape, T=T, seed=21, steps=2, starve=starve, world=world, renorm=renorm)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=ep_p2p_worker.run, args=(r, world, port, cfg, q)) for r in range(world)]
