@@ -366,6 +366,15 @@ def run_ours_single(args, peaks):
         roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
     roof["peak_source"] = peaks.get("source", "measured") + " (burst)"
     roof["traffic"] = load_traffic(dname)
+    if dname == "sdd":
+        # context: the SDD's tiles move A (128 x h) and B (h x 256)
+        # into shared memory and act(H), act'(H) (2 x 128 x 256) out of it, per
+        # 128 x 256 tile; against the measured TMA L2->SMEM delivery ceiling
+        # (scripts/micro/l2_tma_bw.cu, profiles/r1s5_l2_tma_bw.txt)
+        tile_bytes = 2 * (128 * h + h * 256) + 2 * 2 * 128 * 256
+        feed = tile_bytes * (nnz // 2) / dur_s / 1e12
+        roof["sm_port"] = {"bytes_per_tile": tile_bytes, "tiles": nnz // 2, "achieved_tbs": round(feed, 2),
+                           "tma_l2_to_smem_ceiling_tbs": 14.59, "frac": round(feed / 14.59, 3)}
     breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4)}
                  for nm, m, s_ in zip(step.names, mean_call, shares)}
     gemm_ms = sum(mean_call[step.names.index(p)] for p in prod_names if p in step.names)
