@@ -342,6 +342,76 @@ class ExpertParallelMoE:
 
 # ----------------------------------------------------------------------------- bench (N > 1)
 
+class _TimedBackend:
+    """Wraps the binding: CUDA events around every moe_* call on the current
+    stream (one extra eager EP step, outside the timed region)."""
+
+    def __init__(self, mod):
+        self.mod, self.marks = mod, []
+
+    def __getattr__(self, name):
+        f = getattr(self.mod, name)
+        if not callable(f) or not name.startswith("moe_"):
+            return f
+
+        def w(*a, **k):
+            self.marks.append((name, f, a, k))
+            return f(*a, **k)
+        return w
+
+
+def _ep_roofline(layer, A, x, dy, wr, w1l, w2l, peaks, dev, shp):
+    """Roofline of the expert side's dominant kernel (the SDD, act and act'
+    written) in one extra eager step on this rank: algorithmic bytes of the
+    rank's received rows (2(Rh + Rf + E_l h f) + 2 R f) / its
+    event-timed duration; the max over ranks of the duration is reported."""
+    B0 = layer.B
+    tb = _TimedBackend(B0)
+    layer.B = tb
+    try:
+        torch.cuda.synchronize()
+        y, st = layer.forward(x, wr, w1l, w2l)
+        layer.backward(st, x, dy, wr, w1l, w2l)
+        torch.cuda.synchronize()
+    finally:
+        layer.B = B0
+    calls = [(f, a, k) for n, f, a, k in tb.marks if n in ("moe_sdd_deriv", "moe_sdd")]
+    if not calls:
+        return None
+    f, a, k = calls[0]          # the forward SDD, re-issued back to back on the same operands
+
+    def timed_ms(fn, reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+    sdd_ms = timed_ms(lambda: f(*a, **k), 10)
+    ms = torch.tensor([sdd_ms, 1.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if layer.transport == "p2p":
+        R = int(layer.win.n_recv().item())
+    else:
+        R = int(st.n_recv)
+    Rmax = torch.tensor([R], dtype=torch.float64, device=dev)
+    dist.all_reduce(Rmax, op=dist.ReduceOp.MAX)
+    R = int(Rmax.item())
+    h, f, El = layer.h, layer.f, layer.El
+    bytes_ = 2 * (R * h + R * f + El * h * f) + (2 * R * f if layer.act != 0 else 0)
+    dur = float(ms[0].item()) * 1e-3
+    ach = bytes_ / dur / 1e9
+    return {"kernel": "sdd (expert side)", "launch_ms": round(float(ms[0].item()), 4), "bound": "hbm",
+            "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(ach / peaks["hbm_gbs"], 4), "peak_source": peaks.get("source", "measured") + " (burst)",
+            "traffic": None, "rows_received_max": R,
+            "note": "after the timed region: the forward SDD of one extra eager step re-issued 10x back to back "
+                    "on its operands, CUDA events on the launching stream, max over ranks"}
+
+
 def bench_ep(args, peaks, clock_sampler=None):
     """Weak-scaling EP benchmark: T_local tokens per rank of the BASELINE
     config, experts split over ranks, NCCL all-to-all. Returns rank 0's JSON
@@ -476,6 +546,7 @@ def bench_ep(args, peaks, clock_sampler=None):
     launches = launches_per_step * args.steps
     if transport == "p2p" and layer.win.error_word() != 0:
         raise RuntimeError(f"p2p exchange wait timed out during the timed steps (region {layer.win.error_word() - 1})")
+    roof = _ep_roofline(layer, A, x, dy, wr, w1l, w2l, peaks, dev, shp)
     # end to end: pinned host x, dy in; y, dx out, every step. Host->device
     # copies of step i+1 and device->host copies of step i-1 overlap step i's
     # compute (double-buffered device inputs / outputs, three streams), as in
@@ -557,7 +628,7 @@ def bench_ep(args, peaks, clock_sampler=None):
                           "launch_mode": "cuda_graph" if graph is not None else "eager",
                           **({"transport_note": note} if note else {}),
                           "l2": "flushed between timed steps (512 MiB memset, outside the events)"},
-               "gpu_launches": int(launches), "clocks": clocks, "roofline": None,
+               "gpu_launches": int(launches), "clocks": clocks, "roofline": roof,
                "e2e": None if ms_e2e is None else {
                    "value": round(T * world * args.steps / (ms_e2e / 1e3), 1), "unit": "tokens/s",
                    "h2d_bytes_per_step": 2 * T * h * 2 * world, "d2h_bytes_per_step": 2 * T * h * 2 * world,

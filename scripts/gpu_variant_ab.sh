@@ -1,10 +1,10 @@
 #!/bin/bash
-# A/B of library builds: bash scripts/gpu_variant_ab.sh name1 name2 ... (build/variants/libmoe_<name>.so)
+# A/B of library builds: bash scripts/gpu_variant_ab.sh name1 name2 ... (abvariants/libmoe_<name>.so)
 mkdir -p gpurun_out
 cp paper_2211_15841_b200/libmoe.so /tmp/libmoe_current.so
 for v in "$@"; do
   for rep in 1 2; do
-    cp build/variants/libmoe_$v.so paper_2211_15841_b200/libmoe.so
+    cp abvariants/libmoe_$v.so paper_2211_15841_b200/libmoe.so
     timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/ab_$v.json 2>/dev/null
     python - "$v" <<'PY'
 import json, sys
