@@ -967,3 +967,34 @@ def test_layer_aux_load_balance_loss(name, T, shp):
     assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
     assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
     assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+
+
+@pytest.mark.parametrize("T,shp", [(1, S.CONFIGS["C0"]), (3, S.CONFIGS["C1"]), (129, S.CONFIGS["C4"]),
+                                   (2, S.CONFIGS["C0"].replace(top_k=2))])
+def test_layer_degenerate_token_counts(T, shp):
+    """Degenerate batches through moe_forward / moe_backward: one token, fewer
+    tokens than experts (most experts empty, a single partial block), one block
+    plus one row; against the oracle routed from the GPU's logits."""
+    d = dev()
+    A = api()
+    inp = S.make_inputs(shp, seed=31, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act,
+                               logits=saved.logits.cpu().double().numpy())
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
+    assert rel_fro(f64(y), yo) < FRO_TOL
+    assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
+    assert rel_fro(f64(dw1), go["dw1"]) < FRO_TOL
+    assert rel_fro(f64(dw2), go["dw2"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
+    E, f = shp.experts, shp.ffn
+    used = np.unique(cache.expert_idx)
+    for e in range(E):   # experts without tokens: exact zero gradient slices
+        if e not in used:
+            assert not f64(dw1[:, e * f:(e + 1) * f]).any() and not f64(dw2[e * f:(e + 1) * f]).any()
