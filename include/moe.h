@@ -265,14 +265,16 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
 /* Padded exchange (the receiving side needs no gather): rows land directly in
  * the owner's padded expert-grouped layout (local expert, then source
  * rank, then token; pad rows at each expert's tail are NOT written — zero them
- * with moe_zero_pad_rows). x [T, hidden] in token order read through
- * sorted_idx (or, with sorted_idx NULL, rows already in expert order).
+ * with moe_zero_pad_rows). x [T, hidden] in token order: assignment i =
+ * t*k+j sends x[i / k] to its sorted position sorted_pos[i] (the rank's
+ * moe_topology sorted_pos; input-driven, sequential reads), or, with
+ * sorted_pos NULL, x holds rows already in expert order.
  * moe_ep_combine_padded sends this rank's padded rows [n_padded, hidden] back
  * to their sources' return regions (pad rows skipped). The receiving side's
  * topology comes from the per-source counts (moe_topology_counts with the
  * plan's compact counts, moe_ep_plan_offset 0); plan offset 1 holds its
  * padded row count. */
-moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_pos,
                                   int top_k, void* stream);
 moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream);
 int moe_ep_plan_offset(int nranks, int num_experts, int which);

@@ -253,9 +253,11 @@ EpArgs ep_args(const moe_ep_t* ep) {
 
 constexpr int kRowsPerWarp = 4;  // rows in flight per warp (all loads, then all stores)
 
-// Padded exchange. Dispatch: row j of this rank's expert-sorted order (source
-// row src_map[j] / src_k) belongs to global expert e (my_start) and lands in
-// the owner's padded layout at dst_base[e] + (j - my_start[e]). Combine: padded
+// Padded exchange. Dispatch: sorted position u of this rank's expert order
+// belongs to global expert e (my_start) and lands in the owner's padded layout
+// at dst_base[e] + (u - my_start[e]); with src_map (the topology's sorted_pos)
+// the kernel is input-driven — assignment j reads source row j / src_k
+// sequentially and u = src_map[j] — else row j is u. Combine: padded
 // row p of this rank belongs to segment (l, s) (seg_pstart; pad rows skipped)
 // and goes back to source s's return region at seg_dst + (p - seg_pstart).
 template <bool COMBINE, int VEC>
@@ -287,23 +289,24 @@ __global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uin
       const int j = j0 + r;
       dq[r] = -1;
       if (j < rows) {
-        int lo = 0, hi = nseg - 1;  // last segment starting at or before j
+        const int u = (!COMBINE && src_map) ? __ldg(src_map + j) : j;
+        int lo = 0, hi = nseg - 1;  // last segment starting at or before u
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
-          if (starts[mid] <= j) lo = mid; else hi = mid - 1;
+          if (starts[mid] <= u) lo = mid; else hi = mid - 1;
         }
         if (COMBINE) {
-          if (j < starts[lo] + lens_or_base[lo]) {  // else a pad row
+          if (u < starts[lo] + lens_or_base[lo]) {  // else a pad row
             dq[r] = lo % a.P;
-            drow[r] = dsts[lo] + (j - starts[lo]);
+            drow[r] = dsts[lo] + (u - starts[lo]);
           }
         } else {
           dq[r] = lo / a.El;
-          drow[r] = lens_or_base[lo] + (j - starts[lo]);
+          drow[r] = lens_or_base[lo] + (u - starts[lo]);
         }
       }
       if (dq[r] >= 0) {
-        const int srow = src_map ? __ldg(src_map + j) / src_k : j;
+        const int srow = src_map ? j / src_k : j;
         const uint4* sp = src + (size_t)srow * RV;
 #pragma unroll
         for (int u = 0; u < VEC; ++u) val[r][u] = __ldg(sp + lane + 32 * u);
@@ -430,14 +433,14 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
   return MOE_OK;
 }
 
-moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_idx,
+moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_pos,
                                   int top_k, void* stream) {
   MOE_TRY(check_ep(ep, "moe_ep_dispatch_padded"));
   MOE_CHECK_ARG(x && top_k >= 1 && (region == MOE_EP_RECV_X || region == MOE_EP_RECV_DY),
                 "moe_ep_dispatch_padded: NULL x, top_k < 1 or region %d not a receive region", region);
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RECV_X ? L.recv_x : L.recv_dy;
-  return ep_copy_launch<false>(ep, x, region, off, stream, sorted_idx, sorted_idx ? top_k : 1);
+  return ep_copy_launch<false>(ep, x, region, off, stream, sorted_pos, sorted_pos ? top_k : 1);
 }
 
 moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream) {

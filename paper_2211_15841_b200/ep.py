@@ -281,7 +281,7 @@ class ExpertParallelMoE:
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
         topo_l = self._topology(cfg_l, idx, "local")
         W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
-        x_g = W.dispatch_padded("x", x, topo_l["sorted_idx"], self.k)   # X_g of the owners, in their windows
+        x_g = W.dispatch_padded("x", x, topo_l["sorted_pos"], self.k)   # X_g of the owners, in their windows
         cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
         buf = self._expert_bufs(cfg_e, x.device)
         topo_e = B.moe_topology_counts(cfg_e, W.compact_counts(), topo=buf["topo"])

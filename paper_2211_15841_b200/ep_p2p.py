@@ -107,13 +107,14 @@ class PeerWindows:
         El = self.E // self.P
         return self.plan[o: o + self.P * El].view(self.P, El)
 
-    def dispatch_padded(self, name: str, x: torch.Tensor, sorted_idx, top_k: int):
-        """Rows (x read through sorted_idx, or already in expert order with
-        sorted_idx None) straight into the owners' padded layouts; waits for
-        this rank's region (its pad rows still need zeroing)."""
+    def dispatch_padded(self, name: str, x: torch.Tensor, sorted_pos, top_k: int):
+        """Rows straight into the owners' padded layouts: x [T, h] in token order
+        sent to the sorted positions sorted_pos (input-driven), or, with
+        sorted_pos None, rows already in expert order; waits for this rank's
+        region (its pad rows still need zeroing)."""
         check("moe_ep_dispatch_padded", lib.moe_ep_dispatch_padded(
             ctypes.byref(self.ep), REGION[name], ctypes.c_void_p(x.data_ptr()),
-            None if sorted_idx is None else ctypes.c_void_p(sorted_idx.data_ptr()), int(top_k), self._s()))
+            None if sorted_pos is None else ctypes.c_void_p(sorted_pos.data_ptr()), int(top_k), self._s()))
         check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
         return self.rows(name)
 
