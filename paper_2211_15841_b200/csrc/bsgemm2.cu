@@ -369,7 +369,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ===================== epilogue (warps 2..9, both CTAs) =====================
     const int q = warp & 3;
     const int wq = warp - 2;
-    const int half = wq >> 2;
+    const int half = wq >> 2;                  // this warp's first chunk; it takes every EPG-th
+    constexpr int EPG = NUM_EPI_WARPS / 4;     // epilogue warps per TMEM lane quarter
     const int row0 = q * 32;
     uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
     uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
@@ -424,7 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       } else if (mine) {
 #pragma unroll 1
-        for (int c = half; c < NCHUNK; c += 2) {
+        for (int c = half; c < NCHUNK; c += EPG) {
           float v[32];
           if (has_acc) {
             uint32_t r[32];
@@ -459,7 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             }
             __syncwarp();
             hslot ^= 1;
-            if (c + 2 < NCHUNK) load_h(t, c + 2, hslot);
+            if (c + EPG < NCHUNK) load_h(t, c + EPG, hslot);
           }
           store_chunk(&tmap_c, v, x, y);
         }

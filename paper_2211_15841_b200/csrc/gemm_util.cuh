@@ -20,7 +20,10 @@ constexpr int BK = MOE_BK;        // K per pipeline stage (64: 128B-swizzled K-m
 constexpr int KPB = 128 / BK;     // stages per 128 x 128 sparse block
 constexpr int KSW = BK * 2;       // K-major row bytes = TMA / UMMA swizzle span
 static_assert(BK == 32 || BK == 64, "BK must be 32 or 64");
-constexpr int NUM_EPI_WARPS = 8;                  // 2 per TMEM lane quarter (column halves)
+#ifndef MOE_PAIR_EPW
+#define MOE_PAIR_EPW 8
+#endif
+constexpr int NUM_EPI_WARPS = MOE_PAIR_EPW;       // CTA-pair kernels: NUM_EPI_WARPS / 4 per TMEM lane quarter
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int EPI_COLS = 32;                      // epilogue chunk: 32 rows x 32 columns per warp
