@@ -1184,7 +1184,18 @@ moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, con
   MOE_CHECK_ARG(dx_g, "moe_dsd_dx: top_k > 1 needs the dx_g scratch buffer");
   MOE_TRY(moe_dsd(cfg, dh, 0, w1, 1, topo, dx_g, stream));
   if (!router_term) return moe_gather_bwd(cfg, dx_g, topo, dx, stream);
-  return moe_router_dx(cfg, dlogits_bf16, wr, dx_g, topo, dx, stream);
+  static int gathered = -1;  // MOE_ROUTER_DX_GATHERED=1: the router-dx GEMM gathers the k rows itself
+  if (gathered < 0) {
+    const char* e = getenv("MOE_ROUTER_DX_GATHERED");
+    gathered = e && e[0] == '1';
+  }
+  if (gathered) return moe_router_dx(cfg, dlogits_bf16, wr, dx_g, topo, dx, stream);
+  // the k-row sum by the coalesced combine kernel, then dx += dlogits . Wr^T with
+  // contiguous addend rows (in place)
+  MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
+  MOE_CHECK_ARG(router_on_tensor_cores(cfg), "moe_dsd_dx: the router term needs E %% 64 == 0, E <= 256, top_k <= 8");
+  return router_dx_tc(cfg, reinterpret_cast<const __nv_bfloat16*>(dlogits_bf16), wr, dx, dx, nullptr, 1,
+                      cfg->hidden, as_stream(stream));
 }
 
 moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, const moe_topology_t* topo,
