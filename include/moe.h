@@ -176,13 +176,14 @@ moe_status moe_gather(const moe_config* cfg, const void* x, const moe_topology_t
 moe_status moe_scatter(const moe_config* cfg, const void* y_g, const moe_topology_t* topo,
                        const float* gates, void* y, void* stream);
 
-/* Backward of moe_scatter: dy_g[pos[t*k+j]] = gates[t,j]*dy[t] (pad rows 0);
+/* Backward of moe_scatter (chain rule of Fig. 5's weighted un-permutation):
+ * dy_g[pos[t*k+j]] = gates[t,j]*dy[t] (pad rows 0);
  * dgates[t,j] = <y_g[pos[t*k+j]], dy[t]> (fp32). dgates may be NULL. */
 moe_status moe_scatter_bwd(const moe_config* cfg, const void* dy, const void* y_g,
                            const moe_topology_t* topo, const float* gates, void* dy_g, float* dgates,
                            void* stream);
 
-/* Backward of moe_gather: dx[t] = sum_j dx_g[pos[t*k+j]] (bf16 out). */
+/* Backward of moe_gather (P:268 padded_gather): dx[t] = sum_j dx_g[pos[t*k+j]] (bf16 out). */
 moe_status moe_gather_bwd(const moe_config* cfg, const void* dx_g, const moe_topology_t* topo, void* dx,
                           void* stream);
 
@@ -190,15 +191,16 @@ moe_status moe_gather_bwd(const moe_config* cfg, const void* dx_g, const moe_top
  * x_sorted[j] = x[sorted_idx[j] / k], j < T*k. */
 moe_status moe_sort_rows(const moe_config* cfg, const void* x, const moe_topology_t* topo, void* x_sorted,
                          void* stream);
-/* y[t] = sum_j gates[t,j] * y_sorted[sorted_pos[t*k+j]] (gates may be NULL). */
+/* Un-permutation on the token owner under expert parallelism:
+ * y[t] = sum_j gates[t,j] * y_sorted[sorted_pos[t*k+j]] (gates may be NULL). */
 moe_status moe_unsort_rows(const moe_config* cfg, const void* y_sorted, const moe_topology_t* topo,
                            const float* gates, void* y, void* stream);
-/* Backward of moe_unsort_rows: dy_sorted[sorted_pos[i]] = g*dy[t];
+/* Backward of moe_unsort_rows (chain rule of P:280): dy_sorted[sorted_pos[i]] = g*dy[t];
  * dgates[t,j] = <y_sorted[sorted_pos[i]], dy[t]>. */
 moe_status moe_unsort_rows_bwd(const moe_config* cfg, const void* dy, const void* y_sorted,
                                const moe_topology_t* topo, const float* gates, void* dy_sorted,
                                float* dgates, void* stream);
-/* Backward of moe_sort_rows: dx[t] = sum_j dx_sorted[sorted_pos[t*k+j]]. */
+/* Backward of moe_sort_rows (P:268, P:355): dx[t] = sum_j dx_sorted[sorted_pos[t*k+j]]. */
 moe_status moe_sort_rows_bwd(const moe_config* cfg, const void* dx_sorted, const moe_topology_t* topo,
                              void* dx, void* stream);
 
@@ -279,7 +281,8 @@ moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x,
 moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream);
 int moe_ep_plan_offset(int nranks, int num_experts, int which);
 
-/* Topology of assignments that are already grouped by expert and, within an
+/* Topology (P:235-242 hybrid blocked-CSR-COO, P:290 transpose indices, P:297
+ * padding) of assignments that are already grouped by expert and, within an
  * expert, by source (expert parallelism's receiving side): counts_per_source
  * [nsources, E] int32 device. Writes counts, bins, padded_bins, pair_bins,
  * sizes and every BCSR / COO / transpose index (bit-identical to moe_topology
@@ -386,19 +389,19 @@ moe_status moe_load_balance_loss(const moe_config* cfg, const float* logits, con
 /* ---- fused backward pieces used by moe_backward when the router runs on the
  *      tensor cores (E % 64 == 0, E <= 256, top_k <= 8; else MOE_EUNSUPPORTED) --- */
 
-/* b1 + the softmax part of b7 in one pass per token: dy_g and dgates exactly as
+/* b1 + the softmax part of b7 (P:98 softmax router, chain rule of P:280) in one pass per token: dy_g and dgates exactly as
  * moe_scatter_bwd, and dlogits_bf16 [T,E] = p * (dp - <p,dp>) rounded to bf16,
  * p = softmax(logits[t,:]), dp[e] = sum_{j: expert_idx[t,j] = e} dgates[t,j]. */
 moe_status moe_scatter_bwd_router(const moe_config* cfg, const void* dy, const void* y_g, const moe_topology_t* topo,
                                   const float* gates, const float* logits, const int32_t* expert_idx, void* dy_g,
                                   float* dgates, void* dlogits_bf16, void* stream);
 
-/* b7: dwr [h,E] fp32 = x^T . dlogits (tcgen05, token dimension split into a
+/* b7 (P:98 router projection, backward): dwr [h,E] fp32 = x^T . dlogits (tcgen05, token dimension split into a
  * fixed number of ranges, partials reduced in a fixed order). ws as above. */
 moe_status moe_router_dwr(const moe_config* cfg, const void* x, const void* dlogits_bf16, float* dwr, void* ws,
                           void* stream);
 
-/* b6 + b7: dx [T,h] bf16 = sum_j dx_g[pos[t*k+j]] + dlogits . wr^T (tcgen05,
+/* b6 + b7 (P:268 gather, P:98 router, backward): dx [T,h] bf16 = sum_j dx_g[pos[t*k+j]] + dlogits . wr^T (tcgen05,
  * the padded-gather backward fused into the GEMM epilogue). */
 moe_status moe_router_dx(const moe_config* cfg, const void* dlogits_bf16, const void* wr, const void* dx_g,
                          const moe_topology_t* topo, void* dx, void* stream);
