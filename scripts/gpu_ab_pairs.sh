@@ -1,3 +1,5 @@
+#!/bin/bash
+# A/B of the CTA-pair experiment switches (MOE_SDD_PAIR, MOE_GEMM_PAIR_ROWS) on the product sweep and the bench
 mkdir -p gpurun_out
 for v in base MOE_SDD_PAIR MOE_GEMM_PAIR_ROWS; do
   if [ $v = base ]; then E=""; else E="$v=1"; fi
