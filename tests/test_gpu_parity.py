@@ -793,7 +793,7 @@ def test_expert_parallel_p2p(world, shape, T, starve, renorm):
 
 @pytest.mark.parametrize("T,E,k,f,zipf,cf", [(1000, 4, 1, 512, 1.0, 1.0), (8192, 64, 2, 1024, 0.8, 1.5),
                                              (5000, 64, 1, 256, 1.5, 0.5), (777, 16, 3, 128, 0.0, 1.0),
-                                             (4096, 64, 1, 256, 0.0, 64.0)])
+                                             (4096, 64, 1, 256, 0.0, 64.0), (32768, 64, 1, 2048, 0.5, 1.0)])
 def test_topology_capacity_bit_exact(T, E, k, f, zipf, cf):
     """moe_topology with cfg.capacity (keep-earliest by flat id): kept
     counts, bins, positions (-1 = dropped), sorted order and every BCSR / COO /
@@ -998,3 +998,25 @@ def test_layer_degenerate_token_counts(T, shp):
     for e in range(E):   # experts without tokens: exact zero gradient slices
         if e not in used:
             assert not f64(dw1[:, e * f:(e + 1) * f]).any() and not f64(dw2[e * f:(e + 1) * f]).any()
+
+
+
+@pytest.mark.parametrize("E,k", [(64, 2), (128, 4), (64, 8)])
+def test_router_renormalized_gates_tensor_core(E, k):
+    """Tensor-core router epilogue with renormalize = 1: the chosen experts are
+    the same as without renormalisation (bit-exact), and each token's gates are
+    the raw softmax probabilities divided by their sum."""
+    d = dev()
+    A = api()
+    T, h = 1000, 256
+    g = torch.Generator().manual_seed(E + k)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16).to(d)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16).to(d)
+    cfg0 = A.make_config(T, h, E, k, 128)
+    cfg1 = A.make_config(T, h, E, k, 128, renormalize=True)
+    L0, i0, g0 = A.moe_router(cfg0, x, wr)
+    L1, i1, g1 = A.moe_router(cfg1, x, wr)
+    assert torch.equal(L0, L1) and torch.equal(i0, i1)
+    want = g0.double() / g0.double().sum(1, keepdim=True)
+    assert (g1.double() - want).abs().max().item() < 1e-6
+    np.testing.assert_allclose(g1.double().sum(1).cpu().numpy(), 1.0, rtol=1e-6)
