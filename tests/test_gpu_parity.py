@@ -681,7 +681,8 @@ def test_full_size_sampled_rows(name):
         assert not f64(dw2[e0 * f:(e0 + 1) * f]).any()
 
 
-def test_expert_parallel_single_rank_nccl():
+@pytest.mark.parametrize("renorm", [False, True])
+def test_expert_parallel_single_rank_nccl(renorm):
     """The expert-parallel layer (ep.py) driving the CUDA kernels through NCCL
     with one rank (the only multi-process shape one GPU allows): must match the
     oracle like the single-device layer (dispatch / combine via all_to_all)."""
@@ -703,13 +704,16 @@ def test_expert_parallel_single_rank_nccl():
         inp = S.make_inputs(shp, seed=6, tokens=T)
         xd, dyd = inp["x"].to(d), inp["dy"].to(d)
         wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
-        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act,
+                                     renormalize=renorm)
         y, st = layer.forward(xd, wr, w1, w2)
         dx, dwr, dw1, dw2 = layer.backward(st, xd, dyd, wr, w1, w2)
         torch.cuda.synchronize()
     finally:
         dist.destroy_process_group()
-    yo, cache, go = oracle_layer(inp, shp, T)
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act, renormalize=renorm)
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
     flips = (st.expert_idx.cpu().numpy() != cache.expert_idx).any(axis=1)
     assert flips.mean() < 1e-3
     ok = ~flips
