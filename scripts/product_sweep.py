@@ -40,6 +40,8 @@ PROBLEMS = {
     "Small": dict(E=8, n=4096, h=768, f=3072, k=1),
     "Medium": dict(E=8, n=1024, h=1024, f=4096, k=1),
     "Medium-top2": dict(E=8, n=2048, h=1024, f=4096, k=2),   # C4 per-GPU: T=8192 tokens, k=2
+    # bench.py's N = 8 weak-scaling run: 32768 tokens per rank of C1, 8 local experts
+    "C1-EP8": dict(E=8, n=4096, h=512, f=2048, k=1),
 }
 PRODUCTS = ["sdd", "dsd", "sddT", "dsTd", "dsdT", "ddTs"]
 
