@@ -1,8 +1,9 @@
 """Per-phase device timeline of the expert-parallel layer at one rank (debug tool).
 
-Run on the GPU box: python scripts/ep_profile.py  — prints ms per phase of one
-forward + backward (CUDA events recorded between the phases by monkey-patching
-the binding calls)."""
+Run on the GPU box: python scripts/ep_profile.py [nccl|p2p] — prints ms per
+phase of one eager forward + backward (CUDA events recorded between the phases
+by monkey-patching the binding calls; the p2p exchanges are PeerWindows'
+direct library calls and show up in the gaps before the call that follows)."""
 import os
 import sys
 import time
@@ -53,7 +54,8 @@ def main():
     x, dy = inp["x"].to(dev), inp["dy"].to(dev)
     wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
     B = Timed(A)
-    layer = ep.ExpertParallelMoE(B, dist.group.WORLD, h, E, k, f, act=shp.act)
+    transport = sys.argv[1] if len(sys.argv) > 1 else "nccl"
+    layer = ep.ExpertParallelMoE(B, dist.group.WORLD, h, E, k, f, act=shp.act, transport=transport)
     for it in range(4):
         B.marks.clear()
         torch.cuda.synchronize()
