@@ -386,6 +386,14 @@ moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, 
 moe_status moe_load_balance_loss(const moe_config* cfg, const float* logits, const int32_t* expert_idx, void* ws,
                                  void* stream);
 
+/* The auxiliary loss's router gradient added to an existing bf16 dlogits [T,E]
+ * in place: dlogits += p * (c - <p,c>), p = softmax(logits), c = the per-expert
+ * coefficients moe_load_balance_loss left in ws. A no-op when
+ * cfg->aux_loss_coeff == 0. For callers that compose the router backward from
+ * the pieces below (expert parallelism); moe_backward folds it in itself. */
+moe_status moe_add_aux_dlogits(const moe_config* cfg, const float* logits, void* dlogits_bf16, const void* ws,
+                               void* stream);
+
 /* ---- fused backward pieces used by moe_backward when the router runs on the
  *      tensor cores (E % 64 == 0, E <= 256, top_k <= 8; else MOE_EUNSUPPORTED) --- */
 

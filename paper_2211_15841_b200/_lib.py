@@ -110,6 +110,7 @@ SIGNATURES = {
     "moe_scatter_bwd_router": (STATUS, [CFG, P, P, TOPO, P, P, P, P, P, P, P]),
     "moe_router_dwr": (STATUS, [CFG, P, P, P, P, P]),
     "moe_load_balance_loss": (STATUS, [CFG, P, P, P, P]),
+    "moe_add_aux_dlogits": (STATUS, [CFG, P, P, P, P]),
     "moe_router_dx": (STATUS, [CFG, P, P, P, TOPO, P, P]),
     "moe_forward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), P, P, ctypes.POINTER(MoeSaved), P, P]),
     "moe_backward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), ctypes.POINTER(MoeSaved), P, P, P,

@@ -30,6 +30,13 @@ def aux_region(cfg, ws) -> torch.Tensor:
     return ws[off: off + 4 * (1 + cfg.num_experts)].view(torch.float32)
 
 
+def moe_add_aux_dlogits(cfg, logits, dlogits, ws):
+    """moe_add_aux_dlogits (include/moe.h): dlogits += the auxiliary loss's gradient, in place."""
+    check("moe_add_aux_dlogits", lib.moe_add_aux_dlogits(ctypes.byref(cfg), _p(logits), _p(dlogits), _p(ws),
+                                                         _stream()))
+    return dlogits
+
+
 def moe_load_balance_loss(cfg, logits, expert_idx, ws=None):
     """moe_load_balance_loss (include/moe.h): returns (loss [1] tensor view, the workspace)."""
     ws = ws if ws is not None else workspace(cfg, logits.device)

@@ -490,6 +490,35 @@ __global__ void __launch_bounds__(256) aux_final_kernel(const float* __restrict_
   }
   if (threadIdx.x == 0) aux[0] = coeff * (float)E * s_red[0];
 }
+
+// dlogits[t, :] += p * (c - <p, c>) in place (bf16), c = the aux coefficients
+__global__ void aux_dlogits_kernel(const float* __restrict__ logits, const float* __restrict__ aux_c,
+                                   __nv_bfloat16* __restrict__ dlogits, int T, int E) {
+  const int lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= T) return;
+  const float* row = logits + (size_t)t * E;
+  float m = -FLT_MAX;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, row[e]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float ssum = 0.f, pc = 0.f;
+  for (int e = lane; e < E; e += 32) {
+    const float q = expf(row[e] - m);
+    ssum += q;
+    pc += q * __ldg(aux_c + e);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  const float inv = 1.f / ssum;
+  pc *= inv;
+  for (int e = lane; e < E; e += 32) {
+    __nv_bfloat16* d = dlogits + (size_t)t * E + e;
+    const float pe = expf(row[e] - m) * inv;
+    *d = __float2bfloat16_rn(__bfloat162float(*d) + pe * (__ldg(aux_c + e) - pc));
+  }
+}
 }  // namespace moe
 
 extern "C" {
@@ -565,3 +594,16 @@ moe_status moe_sort_rows_bwd_router(const moe_config* cfg, const void* dx_sorted
 }
 
 }  // extern "C"
+
+extern "C" moe_status moe_add_aux_dlogits(const moe_config* cfg, const float* logits, void* dlogits_bf16, const void* ws,
+                                          void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_CHECK_ARG(logits && dlogits_bf16 && ws, "moe_add_aux_dlogits: NULL pointer");
+  if (!(cfg->aux_loss_coeff > 0.f)) return MOE_OK;
+  const WsLayout WL = ws_layout(cfg);
+  const float* aux_c = reinterpret_cast<const float*>(reinterpret_cast<const char*>(ws) + WL.aux) + 1;
+  const int T = (int)cfg->tokens;
+  MOE_LAUNCH("aux_dlogits", aux_dlogits_kernel, dim3((unsigned)ceil_div(T, 8)), dim3(256), 0, as_stream(stream),
+             logits, aux_c, reinterpret_cast<__nv_bfloat16*>(dlogits_bf16), T, (int)cfg->num_experts);
+  return MOE_OK;
+}

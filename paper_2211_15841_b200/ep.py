@@ -88,12 +88,18 @@ class ExpertParallelMoE:
     """
 
     def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128,
-                 transport="nccl", renormalize=False):
+                 transport="nccl", renormalize=False, aux_loss_coeff=0.0):
         """renormalize: top-k gates divided by their sum (the token owner's
-        router and its backward; the expert side is unaffected)."""
+        router and its backward; the expert side is unaffected).
+        aux_loss_coeff > 0: the auxiliary load-balancing loss of this rank's
+        tokens (f_e and P_e over the local batch, as data parallelism
+        computes it per micro-batch), its value in `self.aux_loss` (device
+        scalar) after each forward and its gradient added to the router's."""
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.renormalize = bool(renormalize)
+        self.aux_loss_coeff = float(aux_loss_coeff)
+        self.aux_loss = None
         self.B = backend
         self.group = group
         self.transport = transport
@@ -106,9 +112,25 @@ class ExpertParallelMoE:
 
     def _cfg(self, tokens, experts, k):
         cfg = self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
-        if self.renormalize and experts == self.E:   # the token owner's (router) config
-            cfg.renormalize = 1
+        if experts == self.E:   # the token owner's (router) config
+            cfg.renormalize = int(self.renormalize)
+            cfg.aux_loss_coeff = self.aux_loss_coeff
         return cfg
+
+    def _aux_forward(self, cfg_l, logits, idx):
+        """The auxiliary loss into the local topology's workspace (kept until the backward)."""
+        if self.aux_loss_coeff > 0:
+            ws = self._topo_cache["local"][3]
+            loss, _ = self.B.moe_load_balance_loss(cfg_l, logits, idx, ws=ws)
+            self.aux_loss = loss
+
+    def _aux_dlogits(self, cfg_l, logits, dlogits):
+        if self.aux_loss_coeff > 0:
+            self.B.moe_add_aux_dlogits(cfg_l, logits, dlogits, self._topo_cache["local"][3])
+
+    def _router_bwd_ws(self):
+        c = self.__dict__.get("_topo_cache", {})
+        return c["local"][3] if "local" in c and self.aux_loss_coeff > 0 else None
 
     def _topology(self, cfg, ids, slot):
         """moe_topology into device arrays and a workspace cached per slot. The
@@ -154,6 +176,7 @@ class ExpertParallelMoE:
         # (1) local router + top-k, grouped by GLOBAL expert
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
         topo_l = self._topology(cfg_l, idx, "local")
+        self._aux_forward(cfg_l, logits, idx)
         x_sorted = B.moe_sort_rows(cfg_l, x, topo_l)
         # (2) count exchange -> split sizes (the one host synchronisation)
         counts_dev = self._gather_counts(topo_l["counts"][: self.E].to(torch.int32).contiguous())
@@ -200,6 +223,7 @@ class ExpertParallelMoE:
         if fused:
             dy_sorted, dgates, dlogits = B.moe_unsort_rows_bwd_router(cfg_l, dy, st.y_sorted, st.topo_local, st.gates,
                                                                       st.logits, st.expert_idx)
+            self._aux_dlogits(cfg_l, st.logits, dlogits)
             # b7 dWr = x^T . dlogits needs nothing else: on a side stream beside the exchange
             if dy.is_cuda:
                 side = self.__dict__.setdefault("_side", torch.cuda.Stream(device=dy.device))
@@ -239,7 +263,7 @@ class ExpertParallelMoE:
                 dwr.record_stream(torch.cuda.current_stream(dy.device))
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
-            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws())
         if reduce_dwr:
             dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
@@ -280,6 +304,7 @@ class ExpertParallelMoE:
         cfg_l = self._cfg(T, self.E, self.k)
         logits, idx, gates = B.moe_router(cfg_l, x, wr)
         topo_l = self._topology(cfg_l, idx, "local")
+        self._aux_forward(cfg_l, logits, idx)
         W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
         x_g = W.dispatch_padded("x", x, topo_l["sorted_pos"], self.k)   # X_g of the owners, in their windows
         cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
@@ -307,6 +332,7 @@ class ExpertParallelMoE:
         if fused:
             dy_sorted, dgates, dlogits = B.moe_unsort_rows_bwd_router(cfg_l, dy, st.y_sorted, st.topo_local, st.gates,
                                                                       st.logits, st.expert_idx)
+            self._aux_dlogits(cfg_l, st.logits, dlogits)
             side = self.__dict__.setdefault("_side", torch.cuda.Stream(device=dy.device))
             side.wait_stream(torch.cuda.current_stream(dy.device))
             dlogits.record_stream(side)
@@ -334,7 +360,7 @@ class ExpertParallelMoE:
             dwr.record_stream(torch.cuda.current_stream(dy.device))
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local, dx=torch.empty_like(dy))
-            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx)
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws())
         if reduce_dwr:
             dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2

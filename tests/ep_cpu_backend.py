@@ -162,7 +162,7 @@ def moe_sort_rows_bwd(cfg, dx_sorted, topo):
     return moe_unsort_rows(cfg, dx_sorted, topo, None)
 
 
-def moe_router_bwd(cfg, x, wr, logits, expert_idx, dgates, dx):
+def moe_router_bwd(cfg, x, wr, logits, expert_idx, dgates, dx, ws=None):
     L, idx, dg = _np(logits), expert_idx.numpy(), _np(dgates)
     p = O.softmax(L)
     dp = np.zeros_like(p)

@@ -1024,3 +1024,51 @@ def test_router_renormalized_gates_tensor_core(E, k):
     want = g0.double() / g0.double().sum(1, keepdim=True)
     assert (g1.double() - want).abs().max().item() < 1e-6
     np.testing.assert_allclose(g1.double().sum(1).cpu().numpy(), 1.0, rtol=1e-6)
+
+
+@pytest.mark.parametrize("transport,shape", [("p2p", "C4"), ("nccl", "C4"), ("p2p", "C0")])
+def test_expert_parallel_aux_loss_single_rank(transport, shape):
+    """ExpertParallelMoE(aux_loss_coeff=...) at one rank (in-process): the
+    auxiliary loss over the rank's tokens and its router gradient (through
+    moe_add_aux_dlogits on the fused path, moe_router_bwd's workspace on the
+    SIMT one) against the oracle."""
+    import socket
+    import torch.distributed as dist
+    from paper_2211_15841_b200 import ep
+    d = dev()
+    A = api()
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    backend = "nccl" if transport == "nccl" else "gloo"
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=d)
+    else:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    coeff = 0.02
+    try:
+        shp = S.CONFIGS[shape]
+        T = 1024
+        inp = S.make_inputs(shp, seed=41, tokens=T)
+        xd, dyd = inp["x"].to(d), inp["dy"].to(d)
+        wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+        layer = ep.ExpertParallelMoE(A, dist.group.WORLD, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act,
+                                     transport=transport, aux_loss_coeff=coeff)
+        y, st = layer.forward(xd, wr, w1, w2)
+        loss = float(layer.aux_loss.item())
+        dx, dwr, dw1, dw2 = layer.backward(st, xd, dyd, wr, w1, w2)
+        torch.cuda.synchronize()
+        if layer.win is not None:
+            layer.win.close()
+    finally:
+        dist.destroy_process_group()
+    x64, wr64, w164, w264, dy64 = (S.to_f64(inp[n]) for n in ("x", "wr", "w1", "w2", "dy"))
+    yo, cache = O.dmoe_forward(x64, wr64, w164, w264, shp.top_k, 128, shp.ffn, shp.act,
+                               logits=st.logits.cpu().double().numpy(), aux_coeff=coeff)
+    go = O.dmoe_backward(cache, dy64, wr64, w164, w264)
+    assert abs(loss - cache.aux_loss) <= 1e-5 * abs(cache.aux_loss)
+    assert rel_fro(f64(y), yo) < FRO_TOL
+    assert rel_fro(f64(dx), go["dx"]) < FRO_TOL
+    assert rel_fro(dwr.cpu().double().numpy(), go["dwr"]) < FRO_TOL
