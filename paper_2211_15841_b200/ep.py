@@ -117,20 +117,28 @@ class ExpertParallelMoE:
             cfg.aux_loss_coeff = self.aux_loss_coeff
         return cfg
 
+    def _aux_ws(self, cfg_l, device):
+        """The workspace holding the auxiliary loss between forward and backward:
+        the local topology's cached one when there is one."""
+        c = self.__dict__.get("_topo_cache", {})
+        if "local" in c:
+            return c["local"][3]
+        if getattr(self, "_aux_ws_buf", None) is None:
+            self._aux_ws_buf = self.B.workspace(cfg_l, device)
+        return self._aux_ws_buf
+
     def _aux_forward(self, cfg_l, logits, idx):
-        """The auxiliary loss into the local topology's workspace (kept until the backward)."""
+        """The auxiliary loss of this rank's tokens (kept in the workspace until the backward)."""
         if self.aux_loss_coeff > 0:
-            ws = self._topo_cache["local"][3]
-            loss, _ = self.B.moe_load_balance_loss(cfg_l, logits, idx, ws=ws)
+            loss, _ = self.B.moe_load_balance_loss(cfg_l, logits, idx, ws=self._aux_ws(cfg_l, logits.device))
             self.aux_loss = loss
 
     def _aux_dlogits(self, cfg_l, logits, dlogits):
         if self.aux_loss_coeff > 0:
-            self.B.moe_add_aux_dlogits(cfg_l, logits, dlogits, self._topo_cache["local"][3])
+            self.B.moe_add_aux_dlogits(cfg_l, logits, dlogits, self._aux_ws(cfg_l, logits.device))
 
-    def _router_bwd_ws(self):
-        c = self.__dict__.get("_topo_cache", {})
-        return c["local"][3] if "local" in c and self.aux_loss_coeff > 0 else None
+    def _router_bwd_ws(self, cfg_l, device):
+        return self._aux_ws(cfg_l, device) if self.aux_loss_coeff > 0 else None
 
     def _topology(self, cfg, ids, slot):
         """moe_topology into device arrays and a workspace cached per slot. The
@@ -263,7 +271,7 @@ class ExpertParallelMoE:
                 dwr.record_stream(torch.cuda.current_stream(dy.device))
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local)
-            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws())
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws(cfg_l, dy.device))
         if reduce_dwr:
             dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
@@ -360,7 +368,7 @@ class ExpertParallelMoE:
             dwr.record_stream(torch.cuda.current_stream(dy.device))
         else:
             dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local, dx=torch.empty_like(dy))
-            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws())
+            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws(cfg_l, dy.device))
         if reduce_dwr:
             dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2

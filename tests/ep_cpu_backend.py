@@ -211,3 +211,25 @@ def moe_ep_recv_ids(counts_all, e0, local_experts, n_rows):
     ids = np.concatenate([np.repeat(np.arange(local_experts), c[q, e0:e0 + local_experts]) for q in range(c.shape[0])])
     assert ids.size == n_rows
     return torch.from_numpy(ids.astype(np.int32))
+
+
+# ---- auxiliary load-balancing loss (per rank's tokens; ws is a dict here)
+
+def workspace(cfg, device=None):
+    return {}
+
+
+def moe_load_balance_loss(cfg, logits, expert_idx, ws=None):
+    ws = ws if ws is not None else {}
+    p = O.softmax(_np(logits))
+    loss, dprobs = O.load_balance_loss(p, expert_idx.numpy(), cfg.aux_loss_coeff)
+    ws["aux_c"] = dprobs[0] * 1.0      # the per-expert coefficient (same for every token)
+    return torch.tensor([loss], dtype=torch.float64), ws
+
+
+def moe_add_aux_dlogits(cfg, logits, dlogits, ws):
+    p = O.softmax(_np(logits))
+    c = ws["aux_c"][None, :]
+    add = p * (c - (p * c).sum(1, keepdims=True))
+    dlogits.copy_(_t(_np(dlogits) + add))
+    return dlogits
