@@ -106,12 +106,14 @@ def work_model(T, h, f, E, k, Tp):
     prod_flop = 2 * R * h * f                       # useful, per product
     prod_bytes = 2 * (R * h + R * f + E * h * f)    # minimal bytes, per product
     return {
+        "T": T, "h": h, "E": E, "R": R, "nnz": (Tp // 128) * (f // 128),
         "useful_flop_step": 6 * prod_flop + 2 * T * h * E + 4 * T * h * E,
         "executed_flop_step": 6 * 2 * Tp * h * f,
         "prod_flop": prod_flop,
         "prod_bytes": prod_bytes,
-        "sddt_bytes": prod_bytes + 2 * R * f,      # + read of the saved pre-activation H
-        "sdd_bytes": prod_bytes + 2 * R * f,       # + write of act'(H) (kept for the backward)
+        "sddt_bytes": prod_bytes + 2 * R * f,      # + read of the saved pre-activation H (SURVEY §8(d))
+        "sdd_bytes": prod_bytes,                   # one sparse output
+        "sdd_design_bytes": prod_bytes + 2 * R * f,  # this design's SDD also writes act'(H) (reading R18)
         "dsd_scatter_bytes": prod_bytes + 2 * T * h + 4 * R,  # + the gate-weighted rows scattered to y
         # DSD^T writing dx rows instead of dX_g, + dlogits rows and Wr for the router term
         "dsdt_dx_bytes": prod_bytes - 2 * R * h + 2 * T * h + 2 * T * E + 2 * h * E + 4 * R,
@@ -346,27 +348,19 @@ def run_ours_single(args, peaks):
                   "gather_bwd": "gather_bwd_bytes"}
     dur_s = mean_call[dom] / 1e3
     roof = {"kernel": dname, "launch_ms": round(float(mean_call[dom]), 4), "share_of_step": round(float(shares[dom]), 4)}
-    if dname in prod_names:
-        bytes_ = wm[prod_names[dname]]
-        flop = wm["prod_flop"]
-        t_mem, t_flop = bytes_ / (peaks["hbm_gbs"] * 1e9), flop / (peaks["bf16_tflops"] * 1e12)
-        if t_mem >= t_flop:
-            roof.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s")
-        else:
-            roof.update(bound="tensor", achieved=round(flop / dur_s / 1e12, 1), peak=peaks["bf16_tflops"],
-                        unit="TFLOP/s")
-        roof["tflops_useful"] = round(flop / dur_s / 1e12, 1)
-        roof["tflops_frac_of_bf16_peak"] = round(flop / dur_s / 1e12 / peaks["bf16_tflops"], 4)
-    elif dname in byte_names:
-        bytes_ = wm[byte_names[dname]]
-        roof.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s")
-    else:
-        roof.update(bound="hbm", achieved=None, peak=peaks["hbm_gbs"], unit="GB/s")
-    if roof.get("achieved") is not None:
-        roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    kinfo = kernel_roofline(dname, wm, dur_s, peaks, prod_names, byte_names)
+    roof.update({kk: vv for kk, vv in kinfo.items() if kk != "ms"})
     roof["peak_source"] = peaks.get("source", "measured") + " (burst)"
-    roof["traffic"] = load_traffic(dname)
+    tr = load_traffic(dname)
+    roof["traffic"] = tr.get("bytes") if tr else None
+    if tr:
+        roof["traffic_source"] = tr.get("source")
     if dname == "sdd":
+        # this design writes act(H) AND act'(H) (reading R18): the same launch
+        # against its own two-output byte count, beside the §8(d) figure above
+        b2 = wm["sdd_design_bytes"]
+        roof["design_two_outputs"] = {"bytes": b2, "achieved": round(b2 / dur_s / 1e9, 1),
+                                      "frac": round(b2 / dur_s / 1e9 / peaks["hbm_gbs"], 4)}
         # context: the SDD's tiles move A (128 x h) and B (h x 256)
         # into shared memory and act(H), act'(H) (2 x 128 x 256) out of it, per
         # 128 x 256 tile; against the measured TMA L2->SMEM delivery ceiling
@@ -375,7 +369,8 @@ def run_ours_single(args, peaks):
         feed = tile_bytes * (nnz // 2) / dur_s / 1e12
         roof["sm_port"] = {"bytes_per_tile": tile_bytes, "tiles": nnz // 2, "achieved_tbs": round(feed, 2),
                            "tma_l2_to_smem_ceiling_tbs": 14.59, "frac": round(feed / 14.59, 3)}
-    breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4)}
+    breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4),
+                      **kernel_roofline(nm, wm, m / 1e3, peaks, prod_names, byte_names)}
                  for nm, m, s_ in zip(step.names, mean_call, shares)}
     gemm_ms = sum(mean_call[step.names.index(p)] for p in prod_names if p in step.names)
     gemm = {"ms": round(float(gemm_ms), 4),
@@ -415,12 +410,51 @@ def run_ours_single(args, peaks):
     return out
 
 
+def kernel_roofline(name, wm, dur_s, peaks, prod_names, byte_names):
+    """Roofline entry of one launch: SURVEY §8(d) algorithmic bytes (and FLOPs
+    for the products) / its event-timed duration, against the measured peaks.
+    The router and topology are reported against HBM too (the topology is
+    latency-bound: a tiny frac is expected)."""
+    T, h, E, R = wm["T"], wm["h"], wm["E"], wm["R"]
+    extra = {"router": 2 * T * h + 4 * T * E + 8 * R + 2 * h * E,
+             "router_dwr": 2 * T * h + 2 * T * E + 4 * h * E,
+             "topology": 12 * R + 12 * wm["nnz"]}
+    out = {}
+    if dur_s <= 0:
+        return out
+    if name in prod_names:
+        bytes_ = wm[prod_names[name]]
+        flop = wm["prod_flop"]
+        t_mem, t_flop = bytes_ / (peaks["hbm_gbs"] * 1e9), flop / (peaks["bf16_tflops"] * 1e12)
+        if t_mem >= t_flop:
+            out.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s")
+        else:
+            out.update(bound="tensor", achieved=round(flop / dur_s / 1e12, 1), peak=peaks["bf16_tflops"],
+                       unit="TFLOP/s")
+        out["alg_bytes"] = int(bytes_)
+        out["tflops_useful"] = round(flop / dur_s / 1e12, 1)
+        out["tflops_frac_of_bf16_peak"] = round(flop / dur_s / 1e12 / peaks["bf16_tflops"], 4)
+    elif name in byte_names or name in extra:
+        bytes_ = wm[byte_names[name]] if name in byte_names else extra[name]
+        out.update(bound="hbm", achieved=round(bytes_ / dur_s / 1e9, 1), peak=peaks["hbm_gbs"], unit="GB/s",
+                   alg_bytes=int(bytes_))
+    if out.get("achieved") is not None:
+        out["frac"] = round(out["achieved"] / out["peak"], 4)
+    return out
+
+
 def load_traffic(kernel_name):
     """dram bytes per launch for the dominant kernel from the committed ncu
-    capture summary (profiles/traffic.json), else null."""
+    --set full capture summary (profiles/traffic.json, which names its capture
+    and date), else null. ncu cannot run inside the timed bench, so this is the
+    latest committed capture of the same kernel, stamped with its source."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel_name)
+            d = json.load(f)
+        v = d.get(kernel_name)
+        if v is None:
+            return None
+        return {"bytes": v, "source": d.get("source", "profiles/traffic.json")}
     except Exception:
         return None
 
@@ -508,14 +542,29 @@ def cpu_threads():
     return os.cpu_count()
 
 
-def cpu_baseline(shp, T_sample=16384):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(shp, T_sample=None):
+    """The oracle as it stands, one fwd+bwd of the whole bench workload (all
+    T tokens: no extrapolation) on the host cores."""
     from synth import inputs as S
+    T_sample = T_sample or shp.tokens
     inp = S.make_inputs(shp, seed=0, tokens=T_sample)
     t0 = time.perf_counter()
     oracle_step(inp, shp, T_sample)
     dt = time.perf_counter() - t0
     return {"value": round(T_sample / dt, 1), "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"first {T_sample} tokens of the {shp.name} workload, one fwd+bwd of oracle/moe_oracle.py "
+            "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+            "sample": f"all {T_sample} tokens of the {shp.name} workload, one fwd+bwd of oracle/moe_oracle.py "
                       f"(numpy fp64, OpenBLAS matmul per block) in {dt:.2f} s"}
 
 
@@ -538,6 +587,7 @@ def run_reference(args):
                                            "hidden": shp.hidden, "ffn_hidden": shp.ffn,
                                            "num_experts": shp.experts, "top_k": shp.top_k},
             "cpu_baseline": {"value": round(value, 2), "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                             "nproc": os.cpu_count(), "cpu_model": cpu_model(),
                              "sample": f"{T_sample} tokens of {shp.name} per step (full h, f, E)"},
             "e2e": {"value": round(value, 2), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 

@@ -428,7 +428,7 @@ class Cache:
 
 def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = ACT_GELU,
                  logits: np.ndarray | None = None, capacity: int | None = None, renormalize: bool = False,
-                 aux_coeff: float = 0.0):
+                 aux_coeff: float = 0.0, expert_idx: np.ndarray | None = None):
     """Fig. 5 'dmoe_forward', step by step:
     (1) indices, weights = router(x)              P:260
     (2) topology = make_topology(indices)         P:265
@@ -437,12 +437,21 @@ def dmoe_forward(x, wr, w1, w2, top_k: int, bs: int, ffn: int, act_kind: int = A
     (5) padded_scatter(x, indices) * weights
     `logits` may be given to route from a fixed score matrix (tests of the
     routing-independent part). `capacity` selects the token-dropping
-    formulation (make_plan); None = dropless."""
+    formulation (make_plan); None = dropless. `expert_idx` [T, k] replaces
+    the greedy selection of step (1) (R6: a test resolving a near-tie token
+    the other valid way); the gates are still this oracle's softmax
+    probabilities of the given experts (renormalised if asked)."""
     x = np.asarray(x, np.float64)
     T = x.shape[0]
     E = np.asarray(wr).shape[1]
     L = router_logits(x, wr) if logits is None else np.asarray(logits, np.float64)
-    idx, gates = topk(L, top_k, renormalize)
+    if expert_idx is None:
+        idx, gates = topk(L, top_k, renormalize)
+    else:
+        idx = np.asarray(expert_idx, np.int32).reshape(T, top_k)
+        gates = np.take_along_axis(softmax(L), idx.astype(np.int64), axis=1)
+        if renormalize:
+            gates = gates / gates.sum(axis=1, keepdims=True)
     plan = make_plan(idx, E, bs, capacity)
     topo = make_topology(plan, bs, ffn)
     xg = padded_gather(x, plan, top_k)

@@ -854,11 +854,11 @@ template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
 static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   using C = Cfg<MODE, BN, EPI_H>;
   auto kern = bsgemm_kernel<MODE, A_MN, B_MN, BN, EPI_H>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  {
+    static unsigned long long smem_mask = 0;  // per device (the attribute is per device)
+    static int smem_set = 0;
+    cudaError_t e = set_smem_attr_once(kern, (int)C::SMEM, smem_mask, smem_set);
     if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
-    attr_set = true;
   }
   int grid = gemm_sm_budget();
   if (L.max_tiles < grid) grid = L.max_tiles;

@@ -39,6 +39,25 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Raise a kernel's dynamic shared-memory limit once per device (the attribute
+// is per device: a process driving several GPUs must set it on each). `mask`
+// is a per-call-site static holding one bit per device id; the value set is
+// the maximum ever requested at that site.
+template <typename K>
+cudaError_t set_smem_attr_once(K* kern, int bytes, unsigned long long& mask, int& set_bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if ((mask & bit) && bytes <= set_bytes) return cudaSuccess;
+  if (bytes > set_bytes) {
+    set_bytes = bytes;
+    mask = 0;  // a larger request re-applies on every device
+  }
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, set_bytes);
+  if (e == cudaSuccess) mask |= bit;
+  return e;
+}
+
 moe_status set_error(moe_status st, const char* fmt, ...);
 void clear_error();
 void count_launch(int n = 1);

@@ -160,6 +160,8 @@ __device__ bool wait_arrivals(const EpArgs& a, int region) {
 }
 
 __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_local) {
+  pdl_trigger();
+  pdl_wait();  // counts_local comes from the topology kernel before it
   const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
   for (int i = threadIdx.x; i < a.P * a.E; i += blockDim.x) {
     const int q = i / a.E, e = i % a.E;
@@ -235,7 +237,11 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
   }
 }
 
-__global__ void ep_wait_kernel(EpArgs a, int region) { wait_arrivals(a, region); }
+__global__ void ep_wait_kernel(EpArgs a, int region) {
+  pdl_trigger();
+  pdl_wait();
+  wait_arrivals(a, region);
+}
 
 EpArgs ep_args(const moe_ep_t* ep) {
   EpArgs a;
@@ -264,6 +270,8 @@ template <bool COMBINE, int VEC>
 __global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uint4* __restrict__ src, int region,
                                                              size_t region_off, const int32_t* __restrict__ src_map,
                                                              int src_k) {
+  pdl_trigger();
+  pdl_wait();  // the plan, the source rows and src_map come from earlier kernels
   PlanView v = plan_view(a.plan, a.P, a.E);
   const int rows = COMBINE ? *v.n_padded : v.my_start[a.E];
   const int nseg = COMBINE ? a.El * a.P : a.E;
@@ -424,11 +432,9 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
   const size_t smem = sizeof(int32_t) * (2 * (size_t)ep->nranks * ep->num_experts + 2 * (size_t)ep->num_experts);
   MOE_CHECK_ARG(smem <= 200 * 1024, "moe_ep_exchange_counts: nranks * num_experts too large (%d x %d)", ep->nranks,
                 ep->num_experts);
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaFuncSetAttribute(ep_counts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    smem_set = smem;
-  }
+  static unsigned long long smem_mask = 0;
+  static int smem_set = 0;
+  if (smem > 48 * 1024) set_smem_attr_once(ep_counts_kernel, (int)smem, smem_mask, smem_set);
   MOE_LAUNCH("ep_counts", ep_counts_kernel, dim3(1), dim3(256), smem, as_stream(stream), ep_args(ep), counts_local);
   return MOE_OK;
 }

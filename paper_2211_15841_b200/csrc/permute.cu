@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(256) scatter_bwd_kernel(
 template <int VEC>
 __global__ void __launch_bounds__(256) zero_pad_kernel(uint4* __restrict__ dst, const int32_t* __restrict__ counts,
                                                        const int32_t* __restrict__ padded_bins, int E, int bs) {
+  pdl_trigger();
+  pdl_wait();  // counts / padded_bins come from the topology kernel before it
   zero_pad_rows<VEC>(dst, counts, padded_bins, E, bs);
 }
 

@@ -438,6 +438,8 @@ moe_status scatter_bwd_router_aux(const moe_config* cfg, const void* dy, const v
 __global__ void __launch_bounds__(256) aux_partial_kernel(const float* __restrict__ logits,
                                                           const int32_t* __restrict__ idx, int T, int E, int k,
                                                           float* __restrict__ part_p, int* __restrict__ part_c) {
+  pdl_trigger();
+  pdl_wait();  // logits / idx come from the router before it
   extern __shared__ float s_acc[];  // [8 warps][E] probabilities, then int [E] top-1 counts
   int* s_cnt = reinterpret_cast<int*>(s_acc + 8 * E);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -469,6 +471,8 @@ __global__ void __launch_bounds__(256) aux_partial_kernel(const float* __restric
 __global__ void __launch_bounds__(256) aux_final_kernel(const float* __restrict__ part_p,
                                                         const int* __restrict__ part_c, int parts, int T, int E,
                                                         float coeff, float* __restrict__ aux) {
+  pdl_trigger();
+  pdl_wait();  // the partials of aux_partial_kernel
   __shared__ float s_red[256];
   float acc = 0.f;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -494,6 +498,8 @@ __global__ void __launch_bounds__(256) aux_final_kernel(const float* __restrict_
 // dlogits[t, :] += p * (c - <p, c>) in place (bf16), c = the aux coefficients
 __global__ void aux_dlogits_kernel(const float* __restrict__ logits, const float* __restrict__ aux_c,
                                    __nv_bfloat16* __restrict__ dlogits, int T, int E) {
+  pdl_trigger();
+  pdl_wait();  // dlogits from the scatter backward, aux_c from aux_final_kernel
   const int lane = threadIdx.x & 31;
   const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (t >= T) return;

@@ -212,6 +212,8 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
 // most), then writes ids grid-stride with a binary search over the prefix.
 __global__ void ep_recv_ids_kernel(const int32_t* __restrict__ counts_all, int P, int E, int e0, int El,
                                    int32_t* __restrict__ ids, long long max_rows) {
+  pdl_trigger();
+  pdl_wait();  // the gathered counts come from earlier kernels / copies
   extern __shared__ int32_t s_pre[];  // [P*El + 1] exclusive prefix
   const int nseg = P * El;
   if (threadIdx.x == 0) {
@@ -252,11 +254,9 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   MOE_LAUNCH("topo_hist", topo_hist_kernel, dim3(n_chunks), dim3(kTopoChunk), E * sizeof(int32_t), s, expert_idx, R, E,
              chunk_counts);
   const int emit_smem = 32 * E * (int)sizeof(int32_t);
+  static unsigned long long smem_mask = 0;
   static int smem_set = 0;
-  if (emit_smem > 48 * 1024 - 21 * 1024 && smem_set < emit_smem) {
-    cudaFuncSetAttribute(topo_scan_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem);
-    smem_set = emit_smem;
-  }
+  if (emit_smem > 48 * 1024 - 21 * 1024) set_smem_attr_once(topo_scan_emit_kernel, emit_smem, smem_mask, smem_set);
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
@@ -285,11 +285,9 @@ extern "C" moe_status moe_topology_counts(const moe_config* cfg, const int32_t* 
   MOE_CHECK_ARG(counts_per_source && nsources >= 1, "moe_topology_counts: NULL counts or nsources < 1");
   const int E = (int)cfg->num_experts, bs = (int)cfg->block_size, F = (int)(cfg->ffn_hidden / cfg->block_size);
   const int emit_smem = 32 * E * (int)sizeof(int32_t);
+  static unsigned long long smem_mask = 0;
   static int smem_set = 0;
-  if (emit_smem > 48 * 1024 - 21 * 1024 && smem_set < emit_smem) {
-    cudaFuncSetAttribute(topo_scan_emit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, emit_smem);
-    smem_set = emit_smem;
-  }
+  if (emit_smem > 48 * 1024 - 21 * 1024) set_smem_attr_once(topo_scan_emit_kernel, emit_smem, smem_mask, smem_set);
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   // the per-source histograms play the per-chunk ones; no assignment is ranked (R = 0)

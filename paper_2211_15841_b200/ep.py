@@ -77,6 +77,7 @@ class EPState:
     a: torch.Tensor | None
     y_sorted: torch.Tensor
     n_recv: int
+    step: int = 0     # which forward produced this state (one forward in flight per layer)
 
 
 class ExpertParallelMoE:
@@ -88,13 +89,22 @@ class ExpertParallelMoE:
     """
 
     def __init__(self, backend, group, hidden, num_experts, top_k, ffn_hidden, act=1, block_size=128,
-                 transport="nccl", renormalize=False, aux_loss_coeff=0.0):
+                 transport="nccl", renormalize=False, aux_loss_coeff=0.0, max_tokens=None):
         """renormalize: top-k gates divided by their sum (the token owner's
         router and its backward; the expert side is unaffected).
         aux_loss_coeff > 0: the auxiliary load-balancing loss of this rank's
         tokens (f_e and P_e over the local batch, as data parallelism
         computes it per micro-batch), its value in `self.aux_loss` (device
-        scalar) after each forward and its gradient added to the router's."""
+        scalar) after each forward and its gradient added to the router's.
+        max_tokens: the most tokens any rank will pass to one forward (p2p
+        transport: the peer windows are sized once, collectively, for the
+        maximum over ranks of this and of the first forward's token counts;
+        a later forward with more tokens raises).
+
+        One forward in flight: the state a forward returns refers to buffers
+        the layer reuses (cached topologies, the peer windows), so each
+        backward must follow its own forward before the next forward; a
+        stale state raises instead of silently computing wrong gradients."""
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.renormalize = bool(renormalize)
@@ -109,6 +119,9 @@ class ExpertParallelMoE:
         self.h, self.E, self.k, self.f, self.act, self.bs = hidden, num_experts, top_k, ffn_hidden, act, block_size
         self.e0, self.e1 = local_expert_range(self.rank, self.world, num_experts)
         self.El = self.e1 - self.e0
+        self.max_tokens = int(max_tokens) if max_tokens else 0
+        self.t_max = 0
+        self._fwd_step = 0
 
     def _cfg(self, tokens, experts, k):
         cfg = self.B.make_config(max(int(tokens), 1), self.h, experts, k, self.f, self.bs, self.act)
@@ -176,8 +189,15 @@ class ExpertParallelMoE:
         return bool(f and f(cfg))
 
     def forward(self, x, wr, w1_local, w2_local):
+        self._fwd_step += 1
         if self.transport == "p2p":
-            return self._forward_p2p(x, wr, w1_local, w2_local)
+            y, st = self._forward_p2p(x, wr, w1_local, w2_local)
+        else:
+            y, st = self._forward_nccl(x, wr, w1_local, w2_local)
+        st.step = self._fwd_step
+        return y, st
+
+    def _forward_nccl(self, x, wr, w1_local, w2_local):
         B = self.B
         T = x.shape[0]
         cfg_l = self._cfg(T, self.E, self.k)
@@ -221,6 +241,10 @@ class ExpertParallelMoE:
     def backward(self, st: EPState, x, dy, wr, w1_local, w2_local, reduce_dwr=True):
         """reduce_dwr=False leaves the router gradient rank-local (the caller
         sums it, e.g. after replaying a captured step)."""
+        if st.step != self._fwd_step:
+            raise RuntimeError(f"ExpertParallelMoE: backward of forward #{st.step} after forward #{self._fwd_step}; "
+                               "the layer reuses its topology and window buffers, so each backward must follow "
+                               "its own forward (one forward in flight)")
         if self.transport == "p2p":
             return self._backward_p2p(st, x, dy, wr, w1_local, w2_local, reduce_dwr)
         B = self.B
@@ -278,14 +302,22 @@ class ExpertParallelMoE:
 
     # ------------------------------------------------------------------ peer-memory transport (NEXT-1)
     def _windows(self, T, device):
-        """Windows sized for T local tokens: every rank can receive at most all
-        P*T*k assignments (the capacity of the receiving side's buffers)."""
+        """Windows sized for t_max local tokens on EVERY rank: the peers write
+        at offsets of their own window layout, so all layouts must agree.
+        t_max = the maximum over ranks of max_tokens and the first forward's T
+        (agreed collectively once; every rank reaches its first forward). Every
+        rank can receive at most all P*t_max*k assignments (the capacity of the
+        receiving side's buffers)."""
         from .ep_p2p import PeerWindows
-        owner = T * self.k
-        if self.win is None or self.win.owner != owner:
-            if self.win is not None:
-                self.win.close()
+        if self.win is None:
+            ts = [None] * self.world
+            dist.all_gather_object(ts, max(int(T), self.max_tokens), group=self.group)
+            self.t_max = max(ts)
+            owner = self.t_max * self.k
             self.win = PeerWindows(self.group, self.E, self.h, self.world * owner, owner, device)
+        elif T > self.t_max:
+            raise ValueError(f"ExpertParallelMoE: {T} tokens on rank {self.rank} exceed the {self.t_max} per rank the "
+                             "peer windows were sized for at the first forward; pass max_tokens= to the constructor")
         return self.win
 
     def _expert_bufs(self, cfg_cap, device):
@@ -435,13 +467,16 @@ def _ep_roofline(layer, A, x, dy, wr, w1l, w2l, peaks, dev, shp):
     dist.all_reduce(Rmax, op=dist.ReduceOp.MAX)
     R = int(Rmax.item())
     h, f, El = layer.h, layer.f, layer.El
-    bytes_ = 2 * (R * h + R * f + El * h * f) + (2 * R * f if layer.act != 0 else 0)
+    bytes_ = 2 * (R * h + R * f + El * h * f)                     # one sparse output
+    bytes2 = bytes_ + (2 * R * f if layer.act != 0 else 0)       # this design also writes act'(H) (R18)
     dur = float(ms[0].item()) * 1e-3
     ach = bytes_ / dur / 1e9
     return {"kernel": "sdd (expert side)", "launch_ms": round(float(ms[0].item()), 4), "bound": "hbm",
             "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(ach / peaks["hbm_gbs"], 4), "peak_source": peaks.get("source", "measured") + " (burst)",
-            "traffic": None, "rows_received_max": R,
+            "traffic": None, "rows_received_max": R, "alg_bytes": bytes_,
+            "design_two_outputs": {"bytes": bytes2, "achieved": round(bytes2 / dur / 1e9, 1),
+                                   "frac": round(bytes2 / dur / 1e9 / peaks["hbm_gbs"], 4)},
             "note": "after the timed region: the forward SDD of one extra eager step re-issued 10x back to back "
                     "on its operands, CUDA events on the launching stream, max over ranks"}
 

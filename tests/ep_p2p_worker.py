@@ -26,6 +26,12 @@ def make_global_inputs(shp, cfg, tokens):
     return inp
 
 
+def rank_tokens(cfg, world):
+    """Tokens of each rank: cfg["T"], minus cfg["uneven"] * rank (ranks with
+    different batch sizes share one window layout sized for the largest)."""
+    return [cfg["T"] - cfg.get("uneven", 0) * r for r in range(world)]
+
+
 def run(rank, world, port, cfg, q):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import numpy as np
@@ -40,11 +46,11 @@ def run(rank, world, port, cfg, q):
         d = torch.device("cuda", 0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         shp = S.CONFIGS[cfg["shape"]]
-        T = cfg["T"]
-        inp = make_global_inputs(shp, cfg, T * world)
+        Ts = rank_tokens(cfg, world)
+        inp = make_global_inputs(shp, cfg, sum(Ts))
         E, f = shp.experts, shp.ffn
         e0, e1 = ep.local_expert_range(rank, world, E)
-        sl = slice(rank * T, (rank + 1) * T)
+        sl = slice(sum(Ts[:rank]), sum(Ts[:rank + 1]))
         x, dy = inp["x"][sl].to(d), inp["dy"][sl].to(d)
         wr = inp["wr"].to(d)
         w1 = inp["w1"][:, e0 * f:e1 * f].contiguous().to(d)

@@ -616,3 +616,38 @@ def test_load_balance_loss_grad_finite_differences_and_layer_autograd():
     ((yt * t64(dy)).sum() + aux).backward()
     np.testing.assert_allclose(gr["dx"], tx.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(gr["dwr"], twr.grad.numpy(), atol=1e-10)
+
+
+@pytest.mark.parametrize("T,h,f,E,k,renorm", [(24, 6, 8, 4, 2, False), (19, 4, 4, 5, 3, True), (16, 5, 8, 3, 1, False)])
+def test_forward_given_expert_idx_vs_autograd(T, h, f, E, k, renorm):
+    """dmoe_forward(expert_idx=...) (R6: a test resolving a near-tie token the
+    other valid way) with an arbitrary, non-greedy choice of distinct experts:
+    y[t] = sum_j g[t,j] act(x_t W1_e) W2_e with g = softmax(x Wr)[t, e_j]
+    (renormalised over the k if asked), written per token in torch; and its
+    backward against torch autograd of that formulation (the routing is a
+    constant, the gates carry the router gradient)."""
+    x, wr, w1, w2, dy = small_inputs(T, h, f, E, 13)
+    rng = np.random.default_rng(5)
+    idx = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    y, cache = O.dmoe_forward(x, wr, w1, w2, k, 4, f, O.ACT_GELU, renormalize=renorm, expert_idx=idx)
+    assert (cache.expert_idx == idx).all()
+    g = O.dmoe_backward(cache, dy, wr, w1, w2)
+    tx, twr, tw1, tw2 = (t64(v).requires_grad_() for v in (x, wr, w1, w2))
+    p = torch.softmax(tx @ twr, dim=1)
+    rows = []
+    for t in range(T):
+        gs = torch.stack([p[t, int(e)] for e in idx[t]])
+        if renorm:
+            gs = gs / gs.sum()
+        yt = torch.zeros(h, dtype=torch.float64)
+        for j, e in enumerate(idx[t]):
+            e = int(e)
+            yt = yt + gs[j] * (torch_act(O.ACT_GELU, tx[t] @ tw1[:, e * f:(e + 1) * f]) @ tw2[e * f:(e + 1) * f])
+        rows.append(yt)
+    yt = torch.stack(rows)
+    np.testing.assert_allclose(y, yt.detach().numpy(), atol=1e-12)
+    (yt * t64(dy)).sum().backward()
+    np.testing.assert_allclose(g["dx"], tx.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
+    np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
