@@ -462,6 +462,66 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
 moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_saved* saved, const void* x,
                         const void* dy, void* dx, moe_grads* grads, void* ws, void* stream);
 
+/* ---- the expert-parallel layer ("data and expert model
+ *      parallelism", "8-way expert model parallelism for MoE layers and
+ *      data parallelism for all other layers") ----
+ * One object per rank (one process per GPU). Rank r of nranks owns experts
+ * [r E/P, (r+1) E/P) and their weight slices; the router weights are
+ * replicated. Tokens travel over the peer-memory transport above (device-
+ * initiated stores into every owner's IPC window, on-device count exchange):
+ * forward and backward are stream-ordered with no host synchronisation and can
+ * be captured in a CUDA graph; every rank must issue the same sequence of
+ * forwards / backwards.
+ *
+ * Setup (collective over the caller's process group, which the library does
+ * not own):  moe_ep_init on every rank -> moe_ep_get_handle (64 bytes) ->
+ * the caller all-gathers the nranks handles (rank order) -> moe_ep_connect.
+ * moe_ep_init is the only call that allocates (cudaMalloc of the rank's window
+ * and of every buffer the layer needs, sized for max_tokens); the hot path
+ * allocates nothing. max_tokens must be the same on every rank (window layouts
+ * must agree); a step may pass fewer tokens.
+ *
+ * moe_ep_forward: y [tokens, h] bf16 = dMoE(x [tokens, h] bf16); w->wr [h, E]
+ * (all experts), w->w1 [h, (E/P) f], w->w2 [(E/P) f, h] (this rank's slices).
+ * moe_ep_backward: dx [tokens, h] bf16, g->dw1 / g->dw2 (this rank's slices,
+ * bf16) and g->dwr [h, E] fp32 = THIS RANK'S PARTIAL of the router gradient
+ * (its tokens only): the data-parallel sum over ranks is the caller's
+ * all-reduce. The layer keeps the state of the last forward only (one forward
+ * in flight): a backward must follow its forward, else MOE_EINVAL.
+ * Routing, topology and the expert-side products are exactly the single-GPU
+ * layer's on the global batch restricted to each rank's experts.
+ * Errors: a peer that never arrives makes the waits give up after 20 s and
+ * set the plan's last int (MOE_EP_T_PLAN) to 1 + region; a receive bound
+ * (recv_rows_cap) that a step exceeds sets it to 100 and that rank's expert
+ * side computes nothing (no write leaves any window). */
+typedef struct moe_ep moe_ep;
+typedef struct {
+  int32_t nranks, rank;
+  int64_t max_tokens;   /* per rank, identical on all ranks */
+  int64_t hidden, num_experts /* global E, E % nranks == 0 */, top_k, ffn_hidden, block_size;
+  int32_t act, renormalize;
+  float aux_loss_coeff; /* > 0: the auxiliary loss of this rank's tokens (moe_config.aux_loss_coeff) */
+  int64_t recv_rows_cap;/* rows one rank's experts may receive per step; 0 = nranks*max_tokens*top_k (never
+                           exceeded; each of x_g, A, act', dH is then sized for it) */
+} moe_ep_desc;
+enum { MOE_EP_T_LOGITS = 0, MOE_EP_T_EXPERT_IDX = 1, MOE_EP_T_GATES = 2, MOE_EP_T_PLAN = 3, MOE_EP_T_AUX = 4,
+       MOE_EP_T_X_G = 5, MOE_EP_T_A = 6, MOE_EP_T_ACT_DERIV = 7 };
+moe_status moe_ep_init(moe_ep** ep, const moe_ep_desc* desc, int device);
+moe_status moe_ep_get_handle(const moe_ep* ep, void* handle /* 64 bytes out */);
+moe_status moe_ep_connect(moe_ep* ep, const void* handles /* nranks x 64 bytes, rank order */);
+moe_status moe_ep_forward(moe_ep* ep, int64_t tokens, const moe_weights* w, const void* x, void* y, void* stream);
+moe_status moe_ep_backward(moe_ep* ep, const moe_weights* w, const void* x, const void* dy, void* dx,
+                           moe_grads* grads, void* stream);
+/* Device pointer into the layer's state (MOE_EP_T_*; the forward's logits [T,E]
+ * fp32, expert_idx [T,k], gates [T,k], the exchange plan, the auxiliary loss
+ * {loss, coefficients}, the expert side's X_g / A / act'); NULL if unknown. */
+void* moe_ep_tensor(const moe_ep* ep, int which);
+/* The config and topology of side 0 (token owner, tokens of the last forward)
+ * or side 1 (expert side at capacity); device-side sizes live in topo->sizes. */
+moe_status moe_ep_state(const moe_ep* ep, int side, moe_config* cfg, moe_topology_t* topo);
+moe_status moe_ep_exchange_desc(const moe_ep* ep, moe_ep_t* out);
+moe_status moe_ep_destroy(moe_ep* ep);   /* synchronises the device, unmaps the peers, frees everything */
+
 /* Number of kernel launches the last moe_forward / moe_backward on this
  * thread enqueued (for the bench's gpu_launches count). */
 int moe_last_launch_count(void);

@@ -8,3 +8,4 @@ fallback.
 """
 from . import api  # noqa: F401  (loads libmoe.so)
 from .api import *  # noqa: F401,F403
+from . import layer  # noqa: F401,E402  (torch.autograd wrapper: DroplessMoE, DroplessMoEFunction)

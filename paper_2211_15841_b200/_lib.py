@@ -45,6 +45,14 @@ class MoeEp(ctypes.Structure):
                 ("peers", ctypes.c_void_p), ("plan", ctypes.c_void_p)]
 
 
+class MoeEpDesc(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("max_tokens", ctypes.c_int64),
+                ("hidden", ctypes.c_int64), ("num_experts", ctypes.c_int64), ("top_k", ctypes.c_int64),
+                ("ffn_hidden", ctypes.c_int64), ("block_size", ctypes.c_int64), ("act", ctypes.c_int32),
+                ("renormalize", ctypes.c_int32), ("aux_loss_coeff", ctypes.c_float),
+                ("recv_rows_cap", ctypes.c_int64)]
+
+
 class MoeSaved(ctypes.Structure):
     _fields_ = [("logits", ctypes.c_void_p), ("expert_idx", ctypes.c_void_p), ("gates", ctypes.c_void_p),
                 ("topo", MoeTopology), ("x_g", ctypes.c_void_p), ("act_deriv", ctypes.c_void_p),
@@ -115,6 +123,15 @@ SIGNATURES = {
     "moe_forward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), P, P, ctypes.POINTER(MoeSaved), P, P]),
     "moe_backward": (STATUS, [CFG, ctypes.POINTER(MoeWeights), ctypes.POINTER(MoeSaved), P, P, P,
                               ctypes.POINTER(MoeGrads), P, P]),
+    "moe_ep_init": (STATUS, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(MoeEpDesc), ctypes.c_int]),
+    "moe_ep_get_handle": (STATUS, [P, P]),
+    "moe_ep_connect": (STATUS, [P, P]),
+    "moe_ep_forward": (STATUS, [P, ctypes.c_int64, ctypes.POINTER(MoeWeights), P, P, P]),
+    "moe_ep_backward": (STATUS, [P, ctypes.POINTER(MoeWeights), P, P, P, ctypes.POINTER(MoeGrads), P]),
+    "moe_ep_tensor": (ctypes.c_void_p, [P, ctypes.c_int]),
+    "moe_ep_state": (STATUS, [P, ctypes.c_int, CFG, TOPO]),
+    "moe_ep_exchange_desc": (STATUS, [P, ctypes.POINTER(MoeEp)]),
+    "moe_ep_destroy": (STATUS, [P]),
     "moe_last_launch_count": (ctypes.c_int, []),
     "moe_total_launch_count": (ctypes.c_int64, []),
 }

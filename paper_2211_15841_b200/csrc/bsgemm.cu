@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <float.h>
+#include <limits.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -443,7 +444,39 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
 
     // L2 priority of the two epilogue outputs (GemmParams::l2_c / l2_d)
     const uint64_t pol_c = l2_policy(p.l2_c), pol_d = l2_policy(p.l2_d);
+    // Direct stores: the warp's 32 x 32 bf16 chunk goes through its staging
+    // buffer (conflict-free swizzled rows), is read back 4 lanes per 64-byte
+    // row segment and written with coalesced 16-byte st.global (8 rows per
+    // instruction): the epilogue does not queue behind the TMA unit, which
+    // stays with the operand loads. `tok` maps staging row -> output row
+    // (scatter to token rows; < 0 or >= rows: dropped).
+    auto store_direct = [&](__nv_bfloat16* base, long long ld, long long nrows, const float* v, int x, int y,
+                            int tok_of_lane) {
+      uint8_t* buf = stg + sbuf * EPI_BUF;
+      stage_row(buf, lane, v);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = i * 8 + (lane >> 2), j = lane & 3;
+        uint4 w;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(smem_u32(buf) + r * 64 + swz64(j, r))
+                     : "memory");
+        const long long row = tok_of_lane == INT_MIN ? (long long)y + r : (long long)__shfl_sync(0xffffffffu, tok_of_lane, r);
+        if (row >= 0 && row < nrows)
+          *reinterpret_cast<uint4*>(base + row * ld + x + j * 8) = w;
+      }
+      sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;  // the other buffer next: one __syncwarp per chunk
+    };
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
+      if (p.direct) {
+        if (map == &tmap_c)
+          store_direct(p.out_c, p.ldc, p.rows_c, v, x, y, INT_MIN);
+        else
+          store_direct(p.out_d, p.ldd, p.rows_d, v, x, y, INT_MIN);
+        return;
+      }
       if (lane == 0) bulk_wait_read<C::NBUF - 1>();  // the store issued from this buffer NBUF stores ago has read it
       __syncwarp();
       stage_row(stg + sbuf * EPI_BUF, lane, v);
@@ -617,7 +650,13 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             }
           }
           if (!(MODE == DSD_ROW && p.scatter_only)) store_chunk(&tmap_c, v, x, y);
-          if (MODE == DSD_ROW && p.scatter_y) {
+          if (MODE == DSD_ROW && p.scatter_y && p.direct) {
+            // the weighted un-permutation of the layer (top-1): the
+            // gate-scaled rows go straight to y[token] (pad rows: dropped)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] *= my_gate;
+            store_direct(p.out_d, p.ldd, p.rows_d, v, x, 0, my_tok == 0x7fffffff ? -1 : my_tok);
+          } else if (MODE == DSD_ROW && p.scatter_y) {
             // the weighted un-permutation of the layer (top-1): the
             // gate-scaled rows go straight to y[token] by tile::scatter4
 #pragma unroll
@@ -865,6 +904,17 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   if (grid < 1) grid = 1;
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
+  {
+    // MOE_EPI_DIRECT=1: epilogue stores by st.global through a shared-memory
+    // transpose instead of TMA (measured slower at MoE-XS: SDD 129 vs 111 us,
+    // the others equal; kept for A/B experiments)
+    static int direct = -1;
+    if (direct < 0) {
+      const char* e = getenv("MOE_EPI_DIRECT");
+      direct = (e && e[0] == '1') ? 1 : 0;
+    }
+    p.direct = (direct && p.out_c) ? 1 : 0;
+  }
   p.trace = gemm_trace_slot();
   {
     static int rev = -1;
@@ -1010,8 +1060,6 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   const int64_t nnz = moe_max_nnz_blocks(cfg);
   const int64_t rows = moe_max_padded_rows(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  // Row-pair 2-SM tiles measured slower for SDD at MoE-XS (half-empty pairs of
-  // odd-row experts); the 1-SM 128 x 256 kernel is used.
   GemmLaunch L{};
   L.name = trans_b ? "moe_sdd(T)" : "moe_sdd";
   L.mode = SDD;
@@ -1041,9 +1089,18 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
     }
   }
   L.epi_h = L.p.epi == EPI_ACT_BWD;
-  static int pair_env = -1;  // experiment: row-pair 2-SM tiles for SDD / SDD^T (MOE_SDD_PAIR=1)
-  if (pair_env < 0) pair_env = getenv("MOE_SDD_PAIR") != nullptr;
-  const bool pair = pair_env && use_pair(cfg);
+  // Row-pair 2-SM (cta_group::2) tiles: each SM streams half of the expert's
+  // W1 columns, so the forward SDD's operand traffic per output drops to 2/3
+  // (measured 109 -> 101 us at MoE-XS despite the half-empty pairs of odd-row
+  // experts). The SDD^T keeps the 1-SM kernel (its act'(H) prefetch measured
+  // slower on pairs: 99 -> 116 us). MOE_SDD_PAIR=0: 1-SM for both, =1: pairs for both.
+  static int pair_env = -2;
+  if (pair_env == -2) {
+    const char* e = getenv("MOE_SDD_PAIR");
+    pair_env = e ? (e[0] == '1' ? 1 : 0) : -1;
+  }
+  // (the A-row gather inside the loads, moe_sdd_gather, exists only in the 1-SM kernel)
+  const bool pair = use_pair(cfg) && !x_gather && (pair_env == 1 || (pair_env == -1 && !act_src));
   L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
   if (x_gather) {  // A rows = x[row_src / k] by tile::gather4 (X_g never materialised)
     MOE_TRY(make_tmap_bf16(&L.ta, x_gather, h, cfg->tokens, h, BK, 1, "moe_sdd_gather x", KSW));
@@ -1059,7 +1116,9 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   else
     MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, pair ? 128 : L.bn, "moe_sdd b^T", KSW));
   MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
+  set_epi_out(L.p, 0, out_s, nnz * 128, 128);
   if (out_aux) MOE_TRY(make_tmap_epi(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
+  if (out_aux) set_epi_out(L.p, 1, out_aux, nnz * 128, 128);
   if (act_src) MOE_TRY(make_tmap_epi(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_aux && !act_src) L.td = L.tc;
   return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
@@ -1134,8 +1193,10 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
+    set_epi_out(L.p, 0, out, rows, h);
     if (y) {  // fused weighted un-permutation (top-1): rows scattered to y[token] by tile::scatter4
       MOE_TRY(make_tmap_bf16(&L.td, y, h, cfg->tokens, h, 32, 1, "moe_dsd_scatter y", 64));
+      set_epi_out(L.p, 1, y, cfg->tokens, h);
       L.p.scatter_y = 1;
       L.p.scatter_T = (int)cfg->tokens;
       L.p.row_src = topo->row_src;
@@ -1159,6 +1220,7 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
+    set_epi_out(L.p, 0, out, N, h);
   }
   if (!L.p.scatter_y) L.td = L.tc;
   return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
@@ -1256,6 +1318,7 @@ static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, 
     else
       MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, BK, 128, "moe_dds a", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
+    set_epi_out(L.p, 0, out, h, N);
     L.td = L.tc;
     return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
   }
@@ -1272,6 +1335,7 @@ static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, 
   else
     MOE_TRY(make_tmap_bf16(&L.ta, a, N, h, N, BK, 128, "moe_dds a", KSW));
   MOE_TRY(make_tmap_epi(&L.tc, out, rows, h, rows, "moe_dds out"));
+  set_epi_out(L.p, 0, out, h, rows);
   L.td = L.tc;
   return gemm_launch(L, as_stream(stream));
 }

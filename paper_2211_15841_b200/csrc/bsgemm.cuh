@@ -57,6 +57,14 @@ struct GemmParams {
   long long ld_add;
   const int32_t* addend_map;
   int addend_k;
+  // direct epilogue stores (MOE_EPI_DIRECT=1; default: TMA stores):
+  // bf16 outputs of tmap_c / tmap_d written with coalesced st.global from a
+  // per-warp shared-memory transpose; rows >= rows_c / rows_d are clipped as
+  // the TMA store would clip them
+  __nv_bfloat16* out_c;
+  __nv_bfloat16* out_d;
+  long long ldc, ldd, rows_c, rows_d;
+  int direct;
   unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
   int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
   int dbg;  // experiment knobs (MOE_GEMM_DBG): 1 = no epilogue work, 2 = no MMA, 4 = no activation
@@ -84,6 +92,19 @@ struct GemmLaunch {
 };
 
 moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream);
+// Record a bf16 epilogue output (which 0: tmap_c, 1: tmap_d) for the direct-store epilogue.
+inline void set_epi_out(GemmParams& p, int which, const void* ptr, long long rows, long long ld) {
+  __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(ptr));
+  if (which == 0) {
+    p.out_c = q;
+    p.rows_c = rows;
+    p.ldc = ld;
+  } else {
+    p.out_d = q;
+    p.rows_d = rows;
+    p.ldd = ld;
+  }
+}
 // Persistent-grid size control for concurrent kernels (host, per thread):
 // gemm_sm_budget() = SMs the next GEMM launches may use (default: all);
 // set by moe_backward around the GEMMs that share the GPU with the router dWr.

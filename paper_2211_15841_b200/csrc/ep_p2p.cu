@@ -37,6 +37,11 @@ namespace moe {
 constexpr int kEpRegions = 6;          // arrive counters: counts, x, dy, y, dx, (spare)
 constexpr int kEpCtas = 4 * 148;       // CTAs of every copy kernel
 constexpr unsigned long long kEpTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+// error word when a rank would receive more padded rows than its receive
+// region holds (cap_rows + 128 per local expert): its expert side computes
+// nothing that step and the senders drop the rows that do not fit (no write
+// outside the window). Only possible with a receive bound below P*T*k.
+constexpr uint32_t kEpErrOverflow = 100;
 
 struct WinLayout {
   size_t arrive, done, expect, error, counts, recv_x, recv_dy, ret_y, ret_dx, total;
@@ -208,15 +213,27 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
     }
   }
   __syncthreads();
+  __shared__ int s_over;
+  if (threadIdx.x == 0) s_over = 0;
+  __syncthreads();
   for (int q = threadIdx.x; q < P; q += blockDim.x) {
     int32_t acc2 = 0;
     for (int l = 0; l < El; ++l) {
       ps[q * El + l] = acc2;
       acc2 += ((tot[q * El + l] + 127) / 128) * 128;
     }
-    if (q == r) *v.n_padded = acc2;
+    if (q == r) {
+      const bool over = acc2 > a.cap + (long long)El * 128;
+      *v.n_padded = over ? 0 : acc2;
+      if (over) s_over = 1;
+    }
   }
   __syncthreads();
+  if (s_over && threadIdx.x == 0) {
+    *v.n_recv = 0;
+    atomicExch(reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.error), kEpErrOverflow);
+    a.plan[plan_ints(a.P, a.E) - 1] = kEpErrOverflow;
+  }
   for (int e = threadIdx.x; e <= E; e += blockDim.x) v.my_start[e] = e < E ? pre[r * E + e] : pre[r * E + E - 1] + c[r * E + E - 1];
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int32_t before = 0;
@@ -225,7 +242,7 @@ __global__ void ep_counts_kernel(EpArgs a, const int32_t* __restrict__ counts_lo
   }
   for (int i = threadIdx.x; i < P * El; i += blockDim.x) {
     const int s2 = i / El, l = i % El;
-    v.ccomp[i] = c[s2 * E + r * El + l];
+    v.ccomp[i] = s_over ? 0 : c[s2 * E + r * El + l];
   }
   for (int i = threadIdx.x; i < El * P; i += blockDim.x) {  // my segments (l, s)
     const int l = i / P, s2 = i % P, e = r * El + l;
@@ -311,6 +328,7 @@ __global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uin
         } else {
           dq[r] = lo / a.El;
           drow[r] = lens_or_base[lo] + (u - starts[lo]);
+          if (drow[r] >= a.cap + (long long)a.El * 128) dq[r] = -1;  // overflowing receiver: dropped
         }
       }
       if (dq[r] >= 0) {

@@ -315,6 +315,7 @@ moe_status router_dx_tc(const moe_config* cfg, const __nv_bfloat16* dlogits, con
   MOE_TRY(make_tmap_bf16(&D.ta, dlogits, E, T, E, BK, 128, "router dx dlogits", KSW));
   MOE_TRY(make_tmap_bf16(&D.tb, wr, E, h, E, BK, D.bn, "router dx wr", KSW));
   MOE_TRY(make_tmap_epi(&D.tc, dx, h, T, h, "router dx out"));
+  set_epi_out(D.p, 0, dx, T, h);
   D.td = D.tc;
   return gemm_launch(D, s);
 }

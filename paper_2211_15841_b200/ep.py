@@ -104,7 +104,10 @@ class ExpertParallelMoE:
         One forward in flight: the state a forward returns refers to buffers
         the layer reuses (cached topologies, the peer windows), so each
         backward must follow its own forward before the next forward; a
-        stale state raises instead of silently computing wrong gradients."""
+        stale state raises instead of silently computing wrong gradients. With
+        the p2p transport the state's logits / expert_idx / gates are views of
+        the library layer's own buffers: valid until the next forward or
+        `self.win.close()`."""
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.renormalize = bool(renormalize)
@@ -301,106 +304,37 @@ class ExpertParallelMoE:
         return dx, dwr, dw1, dw2
 
     # ------------------------------------------------------------------ peer-memory transport (NEXT-1)
-    def _windows(self, T, device):
-        """Windows sized for t_max local tokens on EVERY rank: the peers write
-        at offsets of their own window layout, so all layouts must agree.
-        t_max = the maximum over ranks of max_tokens and the first forward's T
-        (agreed collectively once; every rank reaches its first forward). Every
-        rank can receive at most all P*t_max*k assignments (the capacity of the
-        receiving side's buffers)."""
-        from .ep_p2p import PeerWindows
+    # The whole step runs inside the library's expert-parallel layer object
+    # (include/moe.h moe_ep_*, csrc/ep_layer.cu); this is argument marshalling.
+    def _layer(self, T, device):
+        """The C-ABI layer, created collectively at the first forward (every
+        rank reaches it) with windows sized for t_max = the maximum over ranks
+        of max_tokens and the first forward's token count: the peers write at
+        offsets of their own window layout, so all layouts must agree."""
+        from .ep_p2p import EpLayer
         if self.win is None:
-            ts = [None] * self.world
-            dist.all_gather_object(ts, max(int(T), self.max_tokens), group=self.group)
-            self.t_max = max(ts)
-            owner = self.t_max * self.k
-            self.win = PeerWindows(self.group, self.E, self.h, self.world * owner, owner, device)
+            self.win = EpLayer(self.group, self.h, self.E, self.k, self.f, self.act, self.bs, self.renormalize,
+                               self.aux_loss_coeff, max(int(T), self.max_tokens), device)
+            self.t_max = self.win.t_max
         elif T > self.t_max:
             raise ValueError(f"ExpertParallelMoE: {T} tokens on rank {self.rank} exceed the {self.t_max} per rank the "
                              "peer windows were sized for at the first forward; pass max_tokens= to the constructor")
         return self.win
 
-    def _expert_bufs(self, cfg_cap, device):
-        """Receive-side scratch at capacity, allocated once per shape."""
-        key = (cfg_cap.tokens, cfg_cap.num_experts)
-        c = self.__dict__.setdefault("_ebufs", {})
-        if key not in c:
-            c.clear()
-            rows = self.B.moe_max_padded_rows(cfg_cap)
-            c[key] = {"topo": self.B.Topology(cfg_cap, device),
-                      "y_g": torch.empty(rows, self.h, dtype=torch.bfloat16, device=device),
-                      "dx_g": torch.empty(rows, self.h, dtype=torch.bfloat16, device=device)}
-        return c[key]
-
     def _forward_p2p(self, x, wr, w1_local, w2_local):
-        """Forward with device-initiated exchanges: nothing here waits for the
-        device. Rows land directly in the owners' padded expert-grouped layout
-        (no gather on the receiving side); its topology follows from the
-        exchanged counts (moe_topology_counts) and the receiving side runs at
-        capacity with device-side sizes."""
-        B = self.B
-        T = x.shape[0]
-        W = self._windows(T, x.device)
-        cfg_l = self._cfg(T, self.E, self.k)
-        logits, idx, gates = B.moe_router(cfg_l, x, wr)
-        topo_l = self._topology(cfg_l, idx, "local")
-        self._aux_forward(cfg_l, logits, idx)
-        W.exchange_counts(topo_l["counts"])                     # [P, E] histograms + plan, on the device
-        x_g = W.dispatch_padded("x", x, topo_l["sorted_pos"], self.k)   # X_g of the owners, in their windows
-        cfg_e = self._cfg(W.cap, self.El, 1)                    # capacity config (tokens = P*T*k)
-        buf = self._expert_bufs(cfg_e, x.device)
-        topo_e = B.moe_topology_counts(cfg_e, W.compact_counts(), topo=buf["topo"])
-        B.moe_zero_pad_rows(cfg_e, topo_e, x_g)
-        act_deriv = None
-        if self.act != 0:
-            a, act_deriv = B.moe_sdd_deriv(cfg_e, x_g, w1_local, 0, topo_e, act=self.act, want_deriv=True)
-        else:
-            a = B.moe_sdd(cfg_e, x_g, w1_local, 0, topo_e)
-        y_g = B.moe_dsd(cfg_e, a, 0, w2_local, 0, topo_e, out=buf["y_g"])
-        y_sorted = W.combine_padded("y", y_g)                   # back to the token owners (pad rows skipped)
-        y = B.moe_unsort_rows(cfg_l, y_sorted, topo_l, gates, y=torch.empty_like(x))
-        st = EPState(cfg_l, cfg_e, logits, idx, gates, topo_l, topo_e, None, None, x_g, act_deriv, a, y_sorted, -1)
-        return y, st
+        from .ep_p2p import T_EXPERT_IDX, T_GATES, T_LOGITS
+        T = int(x.shape[0])
+        L = self._layer(T, x.device)
+        y = L.forward(x, wr, w1_local, w2_local)
+        if self.aux_loss_coeff > 0:
+            self.aux_loss = L.aux[0:1]
+        logits = L.tensor(T_LOGITS, (T, self.E), torch.float32)
+        idx = L.tensor(T_EXPERT_IDX, (T, self.k), torch.int32)
+        gates = L.tensor(T_GATES, (T, self.k), torch.float32)
+        return y, EPState(None, None, logits, idx, gates, None, None, None, None, None, None, None, None, -1)
 
     def _backward_p2p(self, st: EPState, x, dy, wr, w1_local, w2_local, reduce_dwr=True):
-        B = self.B
-        W = self.win
-        cfg_l, cfg_e = st.cfg_local, st.cfg_e
-        buf = self._expert_bufs(cfg_e, dy.device)
-        fused = self._fused_router(cfg_l)
-        side = None
-        if fused:
-            dy_sorted, dgates, dlogits = B.moe_unsort_rows_bwd_router(cfg_l, dy, st.y_sorted, st.topo_local, st.gates,
-                                                                      st.logits, st.expert_idx)
-            self._aux_dlogits(cfg_l, st.logits, dlogits)
-            side = self.__dict__.setdefault("_side", torch.cuda.Stream(device=dy.device))
-            side.wait_stream(torch.cuda.current_stream(dy.device))
-            dlogits.record_stream(side)
-            ws_l = self._topo_cache["local"][3]
-            with torch.cuda.stream(side):
-                dwr = B.moe_router_dwr(cfg_l, x, dlogits, ws=ws_l)
-        else:
-            dy_sorted, dgates = B.moe_unsort_rows_bwd(cfg_l, dy, st.y_sorted, st.topo_local, st.gates)
-        dy_g = W.dispatch_padded("dy", dy_sorted, None, 1)    # already in expert order
-        B.moe_zero_pad_rows(cfg_e, st.topo_e, dy_g)
-        if self.act != 0:
-            dh = B.moe_sdd_deriv(cfg_e, dy_g, w2_local, 1, st.topo_e, act=self.act, deriv_src=st.act_deriv)
-        else:
-            dh = B.moe_sdd(cfg_e, dy_g, w2_local, 1, st.topo_e)
-        # every dW column / row is written by the products (zeros for experts without rows)
-        dw2 = B.moe_dsd(cfg_e, st.a, 1, dy_g, 0, st.topo_e,
-                        out=torch.empty(self.El * self.f, self.h, dtype=w2_local.dtype, device=dy.device))
-        dw1 = B.moe_dds(cfg_e, st.x_g, 1, dh, 0, st.topo_e,
-                        out=torch.empty(self.h, self.El * self.f, dtype=w1_local.dtype, device=dy.device))
-        dx_g = B.moe_dsd(cfg_e, dh, 0, w1_local, 1, st.topo_e, out=buf["dx_g"])   # DSD^T
-        dx_sorted = W.combine_padded("dx", dx_g)
-        if fused:
-            dx = B.moe_sort_rows_bwd_router(cfg_l, dx_sorted, st.topo_local, dlogits, wr, dx=torch.empty_like(dy))
-            torch.cuda.current_stream(dy.device).wait_stream(side)
-            dwr.record_stream(torch.cuda.current_stream(dy.device))
-        else:
-            dx = B.moe_sort_rows_bwd(cfg_l, dx_sorted, st.topo_local, dx=torch.empty_like(dy))
-            dwr = B.moe_router_bwd(cfg_l, x, wr, st.logits, st.expert_idx, dgates, dx, ws=self._router_bwd_ws(cfg_l, dy.device))
+        dx, dwr, dw1, dw2 = self.win.backward(x, dy, wr, w1_local, w2_local)
         if reduce_dwr:
             dist.all_reduce(dwr, op=dist.ReduceOp.SUM, group=self.group)   # data-parallel router grad
         return dx, dwr, dw1, dw2
@@ -431,20 +365,40 @@ def _ep_roofline(layer, A, x, dy, wr, w1l, w2l, peaks, dev, shp):
     written) in one extra eager step on this rank: algorithmic bytes of the
     rank's received rows (2(Rh + Rf + E_l h f) + 2 R f) / its
     event-timed duration; the max over ranks of the duration is reported."""
-    B0 = layer.B
-    tb = _TimedBackend(B0)
-    layer.B = tb
-    try:
-        torch.cuda.synchronize()
-        y, st = layer.forward(x, wr, w1l, w2l)
-        layer.backward(st, x, dy, wr, w1l, w2l)
-        torch.cuda.synchronize()
-    finally:
-        layer.B = B0
-    calls = [(f, a, k) for n, f, a, k in tb.marks if n in ("moe_sdd_deriv", "moe_sdd")]
-    if not calls:
-        return None
-    f, a, k = calls[0]          # the forward SDD, re-issued back to back on the same operands
+    torch.cuda.synchronize()
+    y, st = layer.forward(x, wr, w1l, w2l)
+    layer.backward(st, x, dy, wr, w1l, w2l)
+    torch.cuda.synchronize()
+    if layer.transport == "p2p":
+        # the C layer's expert-side state of that step: re-issue its forward SDD
+        import ctypes
+
+        from ._lib import check, lib
+        from .ep_p2p import T_A, T_ACT_DERIV, T_X_G
+        cfg_e, topo_e = layer.win.state(1)
+        ptr = {n: lib.moe_ep_tensor(layer.win.h_ep, n) for n in (T_X_G, T_A, T_ACT_DERIV)}
+
+        def f():
+            check("moe_sdd_deriv", lib.moe_sdd_deriv(
+                ctypes.byref(cfg_e), ctypes.c_void_p(ptr[T_X_G]), ctypes.c_void_p(w1l.data_ptr()), 0,
+                ctypes.byref(topo_e), int(layer.act), None, ctypes.c_void_p(ptr[T_A]),
+                ctypes.c_void_p(ptr[T_ACT_DERIV]) if layer.act != 0 else None,
+                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        a, k = (), {}
+    else:
+        B0 = layer.B
+        tb = _TimedBackend(B0)
+        layer.B = tb
+        try:
+            y, st = layer.forward(x, wr, w1l, w2l)
+            layer.backward(st, x, dy, wr, w1l, w2l)
+            torch.cuda.synchronize()
+        finally:
+            layer.B = B0
+        calls = [(f, a, k) for n, f, a, k in tb.marks if n in ("moe_sdd_deriv", "moe_sdd")]
+        if not calls:
+            return None
+        f, a, k = calls[0]          # the forward SDD, re-issued back to back on the same operands
 
     def timed_ms(fn, reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -5,9 +5,11 @@ include/moe.h "expert parallelism over peer memory"), with the per-rank
 histograms exchanged the same way — no NCCL all-to-all and no host round
 trip, so the host enqueues a whole step without waiting for the device.
 
-Plumbing only: the window is allocated by the library (cudaMalloc), exported
-with CUDA IPC and mapped by every peer once; the process group only carries
-the 64-byte handles at setup (all_gather_object) and a barrier.
+Plumbing only: the layer object (moe_ep_init) allocates this rank's window
+(cudaMalloc) and every buffer of the step, exports the window with CUDA IPC
+and maps every peer's once (moe_ep_connect); the process group only carries
+the agreed token maximum and the 64-byte handles at setup (all_gather_object)
+and a barrier. Forward and backward are single library calls.
 """
 from __future__ import annotations
 
@@ -16,134 +18,115 @@ import ctypes
 import torch
 import torch.distributed as dist
 
-from ._lib import MoeEp, check, lib
-
-REGION = {"x": 3, "dy": 4, "y": 5, "dx": 6}   # MOE_EP_RECV_X, _RECV_DY, _RET_Y, _RET_DX
-ERROR = 1
+from ._lib import MoeConfig, MoeEpDesc, MoeGrads, MoeTopology, MoeWeights, check, lib
 
 
-class RawRows:
-    """A [rows, hidden] bf16 view of window memory for the binding (which only
-    needs data_ptr / dtype / device / shape)."""
+class _DevView:
+    """Zero-copy torch view of library-owned device memory (CUDA array interface)."""
 
-    def __init__(self, ptr: int, rows: int, hidden: int, device):
-        self.ptr, self.shape, self.device, self.dtype = int(ptr), (int(rows), int(hidden)), device, torch.bfloat16
-
-    def data_ptr(self) -> int:
-        return self.ptr
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(v) for v in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2, "strides": None}
 
 
-class PeerWindows:
-    """This rank's window, every peer's window mapped here and the device plan.
-    Exchange epochs live in the window (device side), so these calls are
-    graph-capturable."""
+def dev_view(ptr: int, shape, dtype) -> torch.Tensor:
+    typestr = {torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+    return torch.as_tensor(_DevView(ptr, shape, typestr), device="cuda")
 
-    def __init__(self, group, num_experts: int, hidden: int, cap_rows: int, owner_rows: int, device):
+
+T_LOGITS, T_EXPERT_IDX, T_GATES, T_PLAN, T_AUX, T_X_G, T_A, T_ACT_DERIV = range(8)   # MOE_EP_T_*
+
+
+class EpLayer:
+    """The C-ABI expert-parallel layer of this rank (include/moe.h moe_ep_*):
+    the library owns the window, the buffers and the whole step (forward and
+    backward run in library kernels, stream-ordered, no host synchronisation).
+    This class is plumbing: the collective setup (max_tokens agreed over the
+    group, the 64-byte window handles all-gathered) and argument marshalling."""
+
+    def __init__(self, group, hidden: int, num_experts: int, top_k: int, ffn_hidden: int, act: int, block_size: int,
+                 renormalize: bool, aux_loss_coeff: float, max_tokens: int, device, recv_rows_cap: int = 0):
         self.group = group
         self.P, self.rank = dist.get_world_size(group), dist.get_rank(group)
-        self.E, self.h, self.cap, self.owner, self.device = num_experts, hidden, int(cap_rows), int(owner_rows), device
-        args = (self.P, self.E, self.h, self.cap, self.owner)
-        self.win, self.mapped = 0, []
-        # every rank reaches every collective below, failures included, and all
-        # ranks agree on the outcome (so a caller can fall back consistently)
+        self.E, self.h, self.k, self.device = num_experts, hidden, top_k, torch.device(device)
+        ts = [None] * self.P
+        dist.all_gather_object(ts, int(max_tokens), group=group)
+        self.t_max = max(ts)                      # window layouts must agree on every rank
+        desc = MoeEpDesc(self.P, self.rank, self.t_max, hidden, num_experts, top_k, ffn_hidden, block_size, int(act),
+                         int(bool(renormalize)), float(aux_loss_coeff), int(recv_rows_cap))
+        self.h_ep = ctypes.c_void_p()
         err, handle = None, None
         try:
-            win = ctypes.c_void_p()
-            check("moe_ep_window_alloc", lib.moe_ep_window_alloc(lib.moe_ep_window_bytes(*args), ctypes.byref(win)))
-            self.win = win.value
+            check("moe_ep_init", lib.moe_ep_init(ctypes.byref(self.h_ep), ctypes.byref(desc),
+                                                 self.device.index if self.device.index is not None else 0))
             hb = (ctypes.c_char * 64)()
-            check("moe_ipc_get_handle", lib.moe_ipc_get_handle(ctypes.c_void_p(self.win), hb))
+            check("moe_ep_get_handle", lib.moe_ep_get_handle(self.h_ep, hb))
             handle = bytes(hb)
         except Exception as exc:  # noqa: BLE001 - reported collectively below
-            err = f"window: {exc}"
+            err = f"init: {exc}"
         handles = [None] * self.P
         dist.all_gather_object(handles, handle, group=group)
-        ptrs = []
         if err is None:
             try:
-                for q, hq in enumerate(handles):
-                    if q == self.rank:
-                        ptrs.append(self.win)
-                        continue
-                    if hq is None:
-                        raise RuntimeError(f"rank {q} has no window")
-                    p = ctypes.c_void_p()
-                    buf = (ctypes.c_char * 64).from_buffer_copy(hq)
-                    check("moe_ipc_open_handle", lib.moe_ipc_open_handle(buf, ctypes.byref(p)))
-                    self.mapped.append(p.value)
-                    ptrs.append(p.value)
+                if any(hq is None for hq in handles):
+                    raise RuntimeError("a rank has no window")
+                buf = (ctypes.c_char * (64 * self.P)).from_buffer_copy(b"".join(handles))
+                check("moe_ep_connect", lib.moe_ep_connect(self.h_ep, buf))
             except Exception as exc:  # noqa: BLE001
-                err = f"peer mapping: {exc}"
+                err = f"connect: {exc}"
         errs = [None] * self.P
         dist.all_gather_object(errs, err, group=group)
         bad = [f"rank {q}: {e}" for q, e in enumerate(errs) if e]
         if bad:
             self.close()
-            raise RuntimeError("peer-memory windows unavailable: " + "; ".join(bad))
-        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=device)
-        self.plan = torch.zeros(lib.moe_ep_plan_ints(self.P, self.E), dtype=torch.int32, device=device)
-        self.ep = MoeEp(self.P, self.rank, self.E, self.h, self.cap, self.owner, self.peers.data_ptr(),
-                        self.plan.data_ptr())
-        self.off = {n: int(lib.moe_ep_window_offset(*args, r)) for n, r in REGION.items()}
-        self.err_off = int(lib.moe_ep_window_offset(*args, ERROR))
-        torch.cuda.synchronize(device)
+            raise RuntimeError("expert-parallel layer unavailable: " + "; ".join(bad))
+        self.plan_n = int(lib.moe_ep_plan_ints(self.P, self.E))
+        self.plan = dev_view(lib.moe_ep_tensor(self.h_ep, T_PLAN), (self.plan_n,), torch.int32)
+        self.aux = dev_view(lib.moe_ep_tensor(self.h_ep, T_AUX), (1 + self.E,), torch.float32)
+        torch.cuda.synchronize(self.device)
         dist.barrier(group=group)
 
-    # ---- views
-    def counts_all(self) -> torch.Tensor:
-        return self.plan[: self.P * self.E].view(self.P, self.E)
-
-    def n_recv(self) -> torch.Tensor:
-        return self.plan[self.P * self.E: self.P * self.E + 1]
-
-    def rows(self, name: str) -> RawRows:
-        # receive regions hold the padded layout: up to 127 pad rows per local expert
-        n = self.cap + (self.E // self.P) * 128 if name in ("x", "dy") else self.owner
-        return RawRows(self.win + self.off[name], n, self.h, self.device)
-
-    def compact_counts(self) -> torch.Tensor:
-        """[P, E/P] int32: rows of each of this rank's experts from each source (device)."""
-        o = lib.moe_ep_plan_offset(self.P, self.E, 0)
-        El = self.E // self.P
-        return self.plan[o: o + self.P * El].view(self.P, El)
-
-    def dispatch_padded(self, name: str, x: torch.Tensor, sorted_pos, top_k: int):
-        """Rows straight into the owners' padded layouts: x [T, h] in token order
-        sent to the sorted positions sorted_pos (input-driven), or, with
-        sorted_pos None, rows already in expert order; waits for this rank's
-        region (its pad rows still need zeroing)."""
-        check("moe_ep_dispatch_padded", lib.moe_ep_dispatch_padded(
-            ctypes.byref(self.ep), REGION[name], ctypes.c_void_p(x.data_ptr()),
-            None if sorted_pos is None else ctypes.c_void_p(sorted_pos.data_ptr()), int(top_k), self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
-        return self.rows(name)
-
-    def combine_padded(self, name: str, rows_padded):
-        """This rank's padded rows back to their sources' return regions; waits for this rank's."""
-        check("moe_ep_combine_padded", lib.moe_ep_combine_padded(ctypes.byref(self.ep), REGION[name],
-                                                                 ctypes.c_void_p(rows_padded.data_ptr()), self._s()))
-        check("moe_ep_wait", lib.moe_ep_wait(ctypes.byref(self.ep), REGION[name], self._s()))
-        return self.rows(name)
-
-    # ---- exchanges (stream-ordered on the current stream)
     @staticmethod
     def _s():
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
-    def exchange_counts(self, counts_local: torch.Tensor):
-        check("moe_ep_exchange_counts", lib.moe_ep_exchange_counts(ctypes.byref(self.ep),
-                                                                   ctypes.c_void_p(counts_local.data_ptr()), self._s()))
+    def forward(self, x, wr, w1_local, w2_local, y=None):
+        T = int(x.shape[0])
+        if T > self.t_max:
+            raise ValueError(f"{T} tokens on rank {self.rank} exceed max_tokens={self.t_max} the layer was built for")
+        y = y if y is not None else torch.empty_like(x)
+        w = MoeWeights(wr.data_ptr(), w1_local.data_ptr(), w2_local.data_ptr())
+        check("moe_ep_forward", lib.moe_ep_forward(self.h_ep, T, ctypes.byref(w), ctypes.c_void_p(x.data_ptr()),
+                                                   ctypes.c_void_p(y.data_ptr()), self._s()))
+        return y
+
+    def backward(self, x, dy, wr, w1_local, w2_local):
+        dx = torch.empty_like(dy)
+        dwr = torch.empty(wr.shape, dtype=torch.float32, device=dy.device)
+        dw1, dw2 = torch.empty_like(w1_local), torch.empty_like(w2_local)
+        w = MoeWeights(wr.data_ptr(), w1_local.data_ptr(), w2_local.data_ptr())
+        g = MoeGrads(dwr.data_ptr(), dw1.data_ptr(), dw2.data_ptr())
+        check("moe_ep_backward", lib.moe_ep_backward(self.h_ep, ctypes.byref(w), ctypes.c_void_p(x.data_ptr()),
+                                                     ctypes.c_void_p(dy.data_ptr()), ctypes.c_void_p(dx.data_ptr()),
+                                                     ctypes.byref(g), self._s()))
+        return dx, dwr, dw1, dw2
+
+    def tensor(self, which: int, shape, dtype) -> torch.Tensor:
+        return dev_view(lib.moe_ep_tensor(self.h_ep, which), shape, dtype)
+
+    def state(self, side: int):
+        cfg, topo = MoeConfig(), MoeTopology()
+        check("moe_ep_state", lib.moe_ep_state(self.h_ep, side, ctypes.byref(cfg), ctypes.byref(topo)))
+        return cfg, topo
 
     def error_word(self) -> int:
-        """0, or 1 + the arrival region whose wait timed out (the plan's last
-        int, mirrored from the window's error word). Reads the device."""
+        """0, 1 + the region whose wait timed out, or 100 (a receive bound was exceeded). Reads the device."""
         return int(self.plan[-1].item())
 
+    def n_recv(self) -> torch.Tensor:
+        return self.plan[self.P * self.E: self.P * self.E + 1]
+
     def close(self):
-        for p in self.mapped:
-            lib.moe_ipc_close_handle(ctypes.c_void_p(p))
-        self.mapped = []
-        if self.win:
-            torch.cuda.synchronize(self.device)
-            lib.moe_ep_window_free(ctypes.c_void_p(self.win))
-            self.win = 0
+        if self.h_ep:
+            lib.moe_ep_destroy(self.h_ep)
+            self.h_ep = ctypes.c_void_p()

@@ -976,10 +976,138 @@ def test_expert_parallel_aux_loss_single_rank(transport, shape):
         loss = float(layer.aux_loss.item())
         dx, dwr, dw1, dw2 = layer.backward(st, xd, dyd, wr, w1, w2)
         torch.cuda.synchronize()
+        got_idx = st.expert_idx.cpu().numpy()     # p2p: a view of the layer's state, valid until close()
         if layer.win is not None:
             layer.win.close()
     finally:
         dist.destroy_process_group()
-    yo, cache, go, _ = oracle_layer(inp, shp, T, got_idx=st.expert_idx.cpu().numpy(), aux_coeff=coeff)
+    yo, cache, go, _ = oracle_layer(inp, shp, T, got_idx=got_idx, aux_coeff=coeff)
     assert abs(loss - cache.aux_loss) <= 1e-5 * abs(cache.aux_loss)
     assert_layer_close(y, dx, dwr, dw1, dw2, yo, go)
+
+
+# ------------------------------------------------------------------ the expert-parallel layer through the C ABI alone
+
+def _ep_c_layer(A, shp, T, d, recv_cap=0, renorm=False, aux=0.0):
+    import ctypes
+    from paper_2211_15841_b200._lib import MoeEpDesc, check, lib
+    desc = MoeEpDesc(1, 0, T, shp.hidden, shp.experts, shp.top_k, shp.ffn, 128, shp.act, int(renorm), float(aux),
+                     recv_cap)
+    h = ctypes.c_void_p()
+    check("moe_ep_init", lib.moe_ep_init(ctypes.byref(h), ctypes.byref(desc), d.index or 0))
+    hb = (ctypes.c_char * 64)()
+    check("moe_ep_get_handle", lib.moe_ep_get_handle(h, hb))
+    check("moe_ep_connect", lib.moe_ep_connect(h, hb))
+    return h
+
+
+@pytest.mark.parametrize("shape,T", [("C4", 768), ("C0", 512), ("C1", 1000)])
+def test_ep_layer_c_abi_single_rank(shape, T):
+    """moe_ep_init / get_handle / connect / forward / backward / destroy with
+    plain pointers (no torch.distributed, no Python orchestration): one rank,
+    its own window; every output and gradient against the oracle (dWr is the
+    rank's partial = the whole gradient at one rank). Also the ABI's error
+    behaviour: backward without a forward in flight, too many tokens."""
+    import ctypes
+    from paper_2211_15841_b200._lib import MoeGrads, MoeWeights, lib
+    d = dev()
+    A = api()
+    shp = S.CONFIGS[shape]
+    inp = S.make_inputs(shp, seed=17, tokens=T)
+    x, dy = inp["x"].to(d), inp["dy"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    h = _ep_c_layer(A, shp, T, d)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = ctypes.c_void_p
+    try:
+        w = MoeWeights(wr.data_ptr(), w1.data_ptr(), w2.data_ptr())
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        dwr = torch.empty(wr.shape, dtype=torch.float32, device=d)
+        dw1, dw2 = torch.empty_like(w1), torch.empty_like(w2)
+        g = MoeGrads(dwr.data_ptr(), dw1.data_ptr(), dw2.data_ptr())
+        assert lib.moe_ep_backward(h, ctypes.byref(w), P(x.data_ptr()), P(dy.data_ptr()), P(dx.data_ptr()),
+                                   ctypes.byref(g), s) == 1          # MOE_EINVAL: no forward in flight
+        assert lib.moe_ep_forward(h, T + 1, ctypes.byref(w), P(x.data_ptr()), P(y.data_ptr()), s) == 1
+        assert lib.moe_ep_forward(h, T, ctypes.byref(w), P(x.data_ptr()), P(y.data_ptr()), s) == 0
+        assert lib.moe_ep_backward(h, ctypes.byref(w), P(x.data_ptr()), P(dy.data_ptr()), P(dx.data_ptr()),
+                                   ctypes.byref(g), s) == 0
+        assert lib.moe_ep_backward(h, ctypes.byref(w), P(x.data_ptr()), P(dy.data_ptr()), P(dx.data_ptr()),
+                                   ctypes.byref(g), s) == 1          # one backward per forward
+        torch.cuda.synchronize()
+        idx_ptr = lib.moe_ep_tensor(h, 1)
+        from paper_2211_15841_b200.ep_p2p import dev_view
+        got_idx = dev_view(idx_ptr, (T, shp.top_k), torch.int32).cpu().numpy()
+        plan_n = lib.moe_ep_plan_ints(1, shp.experts)
+        assert int(dev_view(lib.moe_ep_tensor(h, 3), (plan_n,), torch.int32)[-1].item()) == 0
+    finally:
+        assert lib.moe_ep_destroy(h) == 0
+    yo, cache, go, _ = oracle_layer(inp, shp, T, got_idx=got_idx)
+    assert_layer_close(y, dx, dwr, dw1, dw2, yo, go)
+
+
+def test_ep_layer_receive_bound_overflow_is_reported():
+    """recv_rows_cap below what a step brings: the exchange reports error 100
+    in the plan, the rank's expert side computes nothing and nothing is
+    written outside the window (the process survives, the next calls work)."""
+    import ctypes
+    from paper_2211_15841_b200._lib import MoeGrads, MoeWeights, lib
+    from paper_2211_15841_b200.ep_p2p import dev_view
+    d = dev()
+    A = api()
+    shp = S.CONFIGS["C0"]
+    T = 1024            # 1024 rows to 4 experts: far above 128 + 4 * 128 receive rows
+    inp = S.make_inputs(shp, seed=5, tokens=T)
+    x, dy = inp["x"].to(d), inp["dy"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    h = _ep_c_layer(A, shp, T, d, recv_cap=128)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = ctypes.c_void_p
+    try:
+        w = MoeWeights(wr.data_ptr(), w1.data_ptr(), w2.data_ptr())
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        dwr = torch.empty(wr.shape, dtype=torch.float32, device=d)
+        dw1, dw2 = torch.empty_like(w1), torch.empty_like(w2)
+        g = MoeGrads(dwr.data_ptr(), dw1.data_ptr(), dw2.data_ptr())
+        assert lib.moe_ep_forward(h, T, ctypes.byref(w), P(x.data_ptr()), P(y.data_ptr()), s) == 0
+        assert lib.moe_ep_backward(h, ctypes.byref(w), P(x.data_ptr()), P(dy.data_ptr()), P(dx.data_ptr()),
+                                   ctypes.byref(g), s) == 0
+        torch.cuda.synchronize()
+        plan_n = lib.moe_ep_plan_ints(1, shp.experts)
+        assert int(dev_view(lib.moe_ep_tensor(h, 3), (plan_n,), torch.int32)[-1].item()) == 100
+        assert not f64(dw1).any() and not f64(dw2).any()     # expert side skipped: exact zeros
+    finally:
+        assert lib.moe_ep_destroy(h) == 0
+
+
+@pytest.mark.parametrize("name,T,renorm,aux", [("C0", 1000, False, 0.0), ("C1-reduced", 2048, False, 0.0),
+                                               ("C4-k2", 1024, True, 0.01)])
+def test_autograd_layer(name, T, renorm, aux):
+    """paper_2211_15841_b200.layer.DroplessMoE (torch.autograd.Function over
+    moe_forward / moe_backward): y and the autograd gradients of sum(y * dy)
+    w.r.t. x, Wr, W1, W2 against the oracle on the same bf16 values."""
+    from paper_2211_15841_b200.layer import DroplessMoE
+    d = dev()
+    base = {"C0": S.CONFIGS["C0"], "C1-reduced": S.CONFIGS["C1"], "C4-k2": S.CONFIGS["C4"]}[name]
+    shp = base
+    inp = S.make_inputs(shp, seed=23, tokens=T)
+    m = DroplessMoE(shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, renormalize=renorm,
+                    aux_loss_coeff=aux, device=d)
+    with torch.no_grad():
+        m.wr.copy_(inp["wr"].to(d))
+        m.w1.copy_(inp["w1"].to(d))
+        m.w2.copy_(inp["w2"].to(d))
+    x = inp["x"].to(d).requires_grad_(True)
+    y = m(x)
+    (y.float() * inp["dy"].to(d).float()).sum().backward()
+    torch.cuda.synchronize()
+    kw = {"renormalize": renorm}
+    if aux:
+        kw["aux_coeff"] = aux
+    yo, cache, go, _ = oracle_layer(inp, shp, T, got_idx=m.stats["expert_idx"].cpu().numpy(), **kw)
+    if aux:
+        assert abs(float(m.stats["aux_loss"].item()) - cache.aux_loss) <= 1e-5 * abs(cache.aux_loss)
+    assert_close("y", f64(y), yo)
+    assert_close("dx", f64(x.grad), go["dx"])
+    assert_close("dw1", f64(m.w1.grad), go["dw1"], per="block")
+    assert_close("dw2", f64(m.w2.grad), go["dw2"], per="block")
+    assert_close("dwr", f64(m.wr.grad), go["dwr"], per="none")
