@@ -56,8 +56,39 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.nvml = None
+
+    # NVML polled every ~2 ms from a thread: the timed region of a default run
+    # is only tens of ms, shorter than nvidia-smi's start-up and 100 ms period
+    _BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+
+    def _nvml_poll(self):
+        import pynvml
+        while not self._stop:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.nv.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            phys = self.gpu
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            if vis and all(v.strip().isdigit() for v in vis.split(",")):
+                phys = int(vis.split(",")[self.gpu])     # NVML counts physical GPUs
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.nv, self._stop = [], False
+            self.nvml = threading.Thread(target=self._nvml_poll, daemon=True)
+            self.nvml.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -72,6 +103,15 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            time.sleep(0.01)
+            self._stop = True
+            self.nvml.join(timeout=2)
+            sm = [v for v, _ in self.nv]
+            reasons = sorted(n for n, b in self._BITS.items() if any(r & b for _, r in self.nv))
+            load = [v for v in sm if self.mx and v > 0.5 * self.mx] or sm
+            return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": self.mx,
+                    "reasons": reasons, "samples": len(sm), "source": "nvml, polled every 2 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -148,7 +188,7 @@ class Step:
         wsl = t["ws_layout"]
         self.calls = [
             ("router", L.moe_router, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), d(sv.gates), ws, s)),
-            ("topology", L.moe_topology, (c, d(sv.expert_idx), topo, ws, s)),
+            ("topology", L.moe_topology_from_router, (c, d(sv.expert_idx), topo, ws, s)),
         ]
         gfused = bool(L.moe_gather_is_fused(c))   # layer.cu: the padded gather inside the SDD / DD^TS loads
         if gfused:

@@ -162,6 +162,13 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
  * the kept assignments per expert (at most capacity, the earliest by flat id),
  * dropped assignments get pos = sorted_pos = -1 and appear in no other array;
  * every later entry point skips them. */
+/* moe_topology after moe_router ran with the same cfg and ws: on the
+ * tensor-core router path (E % 64 == 0, E <= 256, top_k <= 8) the router's
+ * epilogue already wrote per-128-token expert histograms into ws, so the
+ * whole topology is one launch ("custom CUDA kernel"); otherwise it is
+ * moe_topology. Same outputs, bit for bit. */
+moe_status moe_topology_from_router(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
+                                    void* ws, void* stream);
 moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
                         void* ws, void* stream);
 

@@ -77,6 +77,7 @@ SIGNATURES = {
     "moe_router": (STATUS, [CFG, P, P, P, P, P, P, P]),
     "moe_topk": (STATUS, [CFG, P, P, P, P]),
     "moe_topology": (STATUS, [CFG, P, TOPO, P, P]),
+    "moe_topology_from_router": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_gather": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_scatter": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_scatter_bwd": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),

@@ -142,6 +142,15 @@ def moe_topology(cfg, expert_idx, topo: Topology | None = None, ws=None) -> Topo
     return topo
 
 
+def moe_topology_from_router(cfg, expert_idx, ws, topo: Topology | None = None) -> Topology:
+    """moe_topology_from_router (include/moe.h): the topology from the per-tile
+    histograms moe_router(cfg, ..., ws) left in ws (tensor-core router), else moe_topology."""
+    topo = topo if topo is not None else Topology(cfg, expert_idx.device)
+    check("moe_topology_from_router", lib.moe_topology_from_router(ctypes.byref(cfg), _p(expert_idx),
+                                                                   ctypes.byref(topo.struct), _p(ws), _stream()))
+    return topo
+
+
 def moe_topology_counts(cfg, counts_per_source, topo: Topology | None = None) -> Topology:
     """moe_topology_counts (include/moe.h): topology of rows grouped by expert
     then source, from the [nsources, E] int32 device counts."""

@@ -85,7 +85,8 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
-  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 : 0;  // router epilogue exchange
+  // router epilogue exchange (+ the tile's expert histogram, E <= 256)
+  static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 + 256 * 4 : 0;
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
@@ -697,6 +698,14 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           be[j] = 0x7fffffff;
         }
         float mx = -FLT_MAX, ssum = 0.f;
+        // the tile's expert histogram (topology input): zeroed by the
+        // 128 group-0 threads, each owning entries e = its index mod 128
+        int32_t* s_hist = reinterpret_cast<int32_t*>(smem_x + 128 * (2 + 2 * kMaxRouterTopK) * 4);
+        const int ht = q * 32 + lane;  // 0..127 over the group-0 warps
+        if (p.hist_out && grp == 0) {
+          for (int e = ht; e < p.E; e += 128) s_hist[e] = 0;
+          asm volatile("bar.sync 5, 128;" ::: "memory");
+        }
 #pragma unroll 1
         for (int c = 0; c < CG / 32; ++c) {
           const int col0 = grp * CG + c * 32;
@@ -801,13 +810,20 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               i0 += take1 ? 0 : 1;
               gsel[j] = __expf(v - M) / S;
               gsum += gsel[j];
-              if (valid) p.idx[(long long)tok * topk + j] = e;
+              if (valid) {
+                p.idx[(long long)tok * topk + j] = e;
+                if (p.hist_out) atomicAdd(&s_hist[e], 1);  // integer: order-independent
+              }
             }
           }
           const float gscale = p.renorm ? 1.f / gsum : 1.f;  // NEXT-4 renormalisation over the k chosen
 #pragma unroll
           for (int j = 0; j < kMaxRouterTopK; ++j)
             if (j < topk && valid) p.gates[(long long)tok * topk + j] = gsel[j] * gscale;
+          if (p.hist_out) {
+            asm volatile("bar.sync 5, 128;" ::: "memory");
+            for (int e = ht; e < p.E; e += 128) p.hist_out[(long long)t.u * p.E + e] = s_hist[e];
+          }
         }
         asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // xr reused by the next tile
       } else if (MODE == DENSE) {  // EPI_F32: fp32 partial tile (split-K)

@@ -48,6 +48,7 @@ struct GemmParams {
   float* gates;
   int E, topk;
   int renorm;  // gates divided by the sum of the token's k gates
+  int32_t* hist_out;  // optional: per-tile expert histogram [m_tiles][E] of the selected experts (topology input)
   // EPI_F32
   float* out_f32;
   long long ld_f32, split_stride;

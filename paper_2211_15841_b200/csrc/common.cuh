@@ -103,6 +103,7 @@ moe_status check_topo(const moe_topology_t* t);
 // Workspace layout (byte offsets inside the caller's ws buffer).
 struct WsLayout {
   size_t topo_chunk_counts;  // int32 [n_chunks][E]
+  size_t router_hist;        // int32 [ceil(T/128)][E]: per-router-tile expert histograms (tensor-core router)
   size_t topo_end;
   // backward scratch
   size_t dy_g;      // bf16 [max_rows, h]
@@ -119,5 +120,10 @@ constexpr int kAuxParts = 148;    // fixed token partition of the auxiliary-loss
 int router_bwd_parts(const moe_config* cfg);
 bool router_on_tensor_cores(const moe_config* cfg);
 WsLayout ws_layout(const moe_config* cfg);
+// moe_topology from per-row expert histograms hist [n_rows][E] of consecutive
+// row_chunk-assignment ranges (the tensor-core router's per-tile histograms):
+// one launch (topo_scan_emit) instead of topo_hist + topo_scan_emit.
+moe_status topology_from_hist(const moe_config* cfg, const int32_t* expert_idx, const int32_t* hist, int n_rows,
+                              int row_chunk, const moe_topology_t* topo, cudaStream_t s);
 
 }  // namespace moe

@@ -62,7 +62,8 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   //     + the auxiliary load-balancing loss into the workspace
   if (cfg->aux_loss_coeff > 0.f) MOE_TRY(moe_load_balance_loss(cfg, sv->logits, sv->expert_idx, ws, stream));
   // (2) topology = make_topology(indices)
-  MOE_TRY(moe_topology(cfg, sv->expert_idx, &sv->topo, ws, stream));
+  //     (tensor-core router: from the per-tile histograms its epilogue wrote)
+  MOE_TRY(moe_topology_from_router(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
   if (moe_gather_is_fused(cfg)) {  // the gather happens inside the SDD's loads (tile::gather4)

@@ -339,7 +339,6 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
                       float* gates, void* ws, void* stream) {
   MOE_TRY(moe_check_config(cfg));
   MOE_CHECK_ARG(x && wr && logits && expert_idx && gates, "moe_router: NULL pointer");
-  (void)ws;
   const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
   if (router_on_tensor_cores(cfg)) {
     // logits = x . Wr on tcgen05 (M = tokens, N = E, K = h) with the greedy
@@ -362,6 +361,8 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
     L.p.E = E;
     L.p.topk = (int)cfg->top_k;
     L.p.renorm = cfg->renormalize;
+    // per-tile expert histograms for the topology (moe_forward: topology_from_hist)
+    L.p.hist_out = ws ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + ws_layout(cfg).router_hist) : nullptr;
     L.max_tiles = L.p.m_tiles;
     MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, BK, 128, "moe_router x", KSW));
     MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));

@@ -86,6 +86,8 @@ WsLayout ws_layout(const moe_config* cfg) {
   size_t off = 0;
   L.topo_chunk_counts = off;
   off = align256(off + sizeof(int32_t) * n_chunks * E);
+  L.router_hist = off;
+  off = align256(off + sizeof(int32_t) * ceil_div(cfg->tokens > 0 ? cfg->tokens : 1, 128) * E);
   L.topo_end = off;
   L.dy_g = off;
   off = align256(off + 2 * rows * h);

@@ -45,34 +45,51 @@ __global__ void topo_hist_kernel(const int32_t* __restrict__ idx, int R, int E, 
 __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __restrict__ idx, int R, int E, int bs,
                                                                int F, int n_chunks,
                                                                const int32_t* __restrict__ chunk_counts,
-                                                               moe_topology_t topo, int capacity) {
+                                                               moe_topology_t topo, int capacity, int n_rows,
+                                                               int row_chunk, int rows_per_cta) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ int32_t s_dyn[];           // [32 warps][E] per-warp counts (ranking CTAs)
   __shared__ int32_t s_cnt[1024], s_start[1024], s_pstart[1024], s_pair[1024], s_base[1024];
   __shared__ int32_t s_tot[3];
+  // n_chunks ranking CTAs; CTA b ranks assignments [b * span, (b+1) * span),
+  // span = rows_per_cta * row_chunk <= 1024, i.e. histogram rows
+  // [b * rows_per_cta, (b+1) * rows_per_cta) of chunk_counts [n_rows][E]
+  // (row_chunk assignments per row: kTopoChunk from topo_hist, 128 tokens x k
+  // from the router epilogue)
   const bool ranking = (int)blockIdx.x < n_chunks;
+  const int span = rows_per_cta * row_chunk;
   const int warp_id = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
-  // (1) per-expert totals and (ranking CTAs) this chunk's exclusive base: one
-  //     warp per expert, lanes over chunks (coalesced-enough L2 reads, warp scan)
-  for (int e = warp_id; e < E; e += 32) {
-    int32_t run = 0, base = 0;
-    for (int c0 = 0; c0 < n_chunks; c0 += 32) {
-      const int c = c0 + lane_id;
-      const int32_t v = c < n_chunks ? __ldg(chunk_counts + (size_t)c * E + e) : 0;
-      int32_t incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane_id >= o) incl += y;
+  // (1) per-expert totals and (ranking CTAs) the exclusive base of the CTA's
+  //     first row: the threads split into S = 1024 / E row slices x E experts
+  //     (coalesced over e), each summing its slice's rows with independent
+  //     loads; partial sums reduced over the slices in shared memory
+  {
+    const int S = 1024 / E;
+    const int first = ranking ? (int)blockIdx.x * rows_per_cta : 0;
+    const int t = threadIdx.x;
+    if (t < S * E) {
+      const int sl = t / E, e = t - sl * E;
+      const int r0 = (int)((long long)n_rows * sl / S), r1 = (int)((long long)n_rows * (sl + 1) / S);
+      int32_t tot = 0, pre = 0;
+#pragma unroll 8
+      for (int c = r0; c < r1; ++c) {
+        const int32_t v = __ldg(chunk_counts + (size_t)c * E + e);
+        tot += v;
+        pre += c < first ? v : 0;
       }
-      if (c == (int)blockIdx.x) base = run + incl - v;
-      run += __shfl_sync(0xffffffffu, incl, 31);
+      s_start[t] = tot;
+      s_pstart[t] = pre;
     }
-    base = __reduce_max_sync(0xffffffffu, (unsigned)base);  // the one lane holding it (others 0)
-    if (lane_id == 0) {
-      s_base[e] = base;
-      s_cnt[e] = capacity > 0 ? min(run, capacity) : run;    // kept assignments (token dropping)
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      int32_t tot = 0, pre = 0;
+      for (int sl = 0; sl < S; ++sl) {
+        tot += s_start[sl * E + e];
+        pre += s_pstart[sl * E + e];
+      }
+      s_base[e] = pre;
+      s_cnt[e] = capacity > 0 ? min(tot, capacity) : tot;    // kept assignments (token dropping)
     }
   }
   __syncthreads();
@@ -144,8 +161,8 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_dyn[i] = 0;
     __syncthreads();
-    const int i = blockIdx.x * kTopoChunk + threadIdx.x;
-    const bool valid = i < R;
+    const int i = blockIdx.x * span + threadIdx.x;
+    const bool valid = (int)threadIdx.x < span && i < R;
     const int e = valid ? __ldg(idx + i) : E + lane;  // unique sentinel for inactive lanes
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const unsigned lt = (1u << lane) - 1u;
@@ -193,12 +210,11 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     topo.row_indices[s] = r;
     topo.col_indices[s] = e * F + j;
     const int32_t pc = ((s_cnt[e] + bs - 1) / bs) * bs;
-    if (j == 0) {
-      topo.row_offsets[r] = s;
-      // pad rows of this block-row (the tail of expert e's group) hold no assignment
-      const int pad0 = s_pstart[e] + s_cnt[e];
-      for (int q = max(row0, pad0); q < row0 + bs && q < s_pstart[e] + pc; ++q) topo.row_src[q] = -1;
-    }
+    if (j == 0) topo.row_offsets[r] = s;
+    // pad rows of this block-row (the tail of expert e's group) hold no
+    // assignment: the row's F threads write them strided
+    const int pad0 = s_pstart[e] + s_cnt[e];
+    for (int q = max(row0, pad0) + j; q < row0 + bs && q < s_pstart[e] + pc; q += F) topo.row_src[q] = -1;
     const int qpos = F * (s_pstart[e] / bs) + j * (pc / bs) + (r - r0);
     topo.t_block_offsets[qpos] = s;
     topo.t_row_indices[qpos] = r;
@@ -260,8 +276,40 @@ extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_
   const int64_t max_nnz = moe_max_nnz_blocks(cfg);
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_chunks + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
-             E, bs, F, n_chunks, chunk_counts, *topo, (int)cfg->capacity);
+             E, bs, F, n_chunks, chunk_counts, *topo, (int)cfg->capacity, n_chunks, kTopoChunk, 1);
   return MOE_OK;
+}
+
+namespace moe {
+
+moe_status topology_from_hist(const moe_config* cfg, const int32_t* expert_idx, const int32_t* hist, int n_rows,
+                              int row_chunk, const moe_topology_t* topo, cudaStream_t s) {
+  const int E = (int)cfg->num_experts, bs = (int)cfg->block_size, F = (int)(cfg->ffn_hidden / cfg->block_size);
+  const int R = (int)(cfg->tokens * cfg->top_k);
+  MOE_CHECK_ARG(row_chunk >= 1 && row_chunk <= 1024, "topology_from_hist: row_chunk=%d", row_chunk);
+  const int rows_per_cta = 1024 / row_chunk;
+  const int n_rank = (n_rows + rows_per_cta - 1) / rows_per_cta;
+  const int emit_smem = 32 * E * (int)sizeof(int32_t);
+  static unsigned long long smem_mask = 0;
+  static int smem_set = 0;
+  if (emit_smem > 48 * 1024 - 21 * 1024) set_smem_attr_once(topo_scan_emit_kernel, emit_smem, smem_mask, smem_set);
+  const int blk_ctas = (int)ceil_div(moe_max_nnz_blocks(cfg), 1024);
+  MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(n_rank + blk_ctas), dim3(1024), emit_smem, s, expert_idx, R,
+             E, bs, F, n_rank, hist, *topo, (int)cfg->capacity, n_rows, row_chunk, rows_per_cta);
+  return MOE_OK;
+}
+
+}  // namespace moe
+
+extern "C" moe_status moe_topology_from_router(const moe_config* cfg, const int32_t* expert_idx,
+                                               const moe_topology_t* topo, void* ws, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(expert_idx && ws, "moe_topology_from_router: NULL pointer");
+  if (!router_on_tensor_cores(cfg)) return moe_topology(cfg, expert_idx, topo, ws, stream);
+  const int32_t* hist = reinterpret_cast<const int32_t*>(reinterpret_cast<char*>(ws) + ws_layout(cfg).router_hist);
+  return topology_from_hist(cfg, expert_idx, hist, (int)((cfg->tokens + 127) / 128), (int)(128 * cfg->top_k), topo,
+                            as_stream(stream));
 }
 
 extern "C" moe_status moe_ep_recv_ids(const int32_t* counts_all, int nranks, int num_experts, int e0, int local_experts,
@@ -292,6 +340,6 @@ extern "C" moe_status moe_topology_counts(const moe_config* cfg, const int32_t* 
   const int blk_ctas = (int)ceil_div(max_nnz, 1024);
   // the per-source histograms play the per-chunk ones; no assignment is ranked (R = 0)
   MOE_LAUNCH("topo_scan_emit", topo_scan_emit_kernel, dim3(nsources + blk_ctas), dim3(1024), emit_smem,
-             as_stream(stream), (const int32_t*)nullptr, 0, E, bs, F, nsources, counts_per_source, *topo, 0);
+             as_stream(stream), (const int32_t*)nullptr, 0, E, bs, F, nsources, counts_per_source, *topo, 0, nsources, 1, 1);
   return MOE_OK;
 }

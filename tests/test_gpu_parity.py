@@ -1111,3 +1111,28 @@ def test_autograd_layer(name, T, renorm, aux):
     assert_close("dw1", f64(m.w1.grad), go["dw1"], per="block")
     assert_close("dw2", f64(m.w2.grad), go["dw2"], per="block")
     assert_close("dwr", f64(m.wr.grad), go["dwr"], per="none")
+
+
+@pytest.mark.parametrize("T,E,k,h", [(32768, 64, 1, 512), (1000, 64, 2, 256), (777, 128, 3, 256), (129, 256, 8, 256),
+                                     (5000, 64, 1, 768)])
+def test_topology_from_router_histograms(T, E, k, h):
+    """moe_router (tensor-core epilogue writing per-128-token expert
+    histograms) + moe_topology_from_router (one scan/emit launch): every
+    topology array bit-exact against the oracle's plan of the oracle's routing
+    (near-ties resolved the GPU's way, R6), ragged last router tile included."""
+    d = dev()
+    A = api()
+    g = torch.Generator().manual_seed(T + E + k)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16)
+    cfg = A.make_config(T, h, E, k, 256)
+    ws = A.workspace(cfg, d)
+    logits, idx, gates = A.moe_router(cfg, x.to(d), wr.to(d), ws=ws)
+    topo = A.moe_topology_from_router(cfg, idx, ws)
+    torch.cuda.synchronize()
+    x64, wr64 = S.to_f64(x), S.to_f64(wr)
+    L = O.router_logits(x64, wr64)
+    want_idx, _ = O.topk(L, k)
+    ridx, _ = resolved_routing(L, logit_error_bound(x64, wr64), idx.cpu().numpy(), want_idx)
+    plan, tt = oracle_plan_topo(ridx, E, 256)
+    check_topology_exact(A, topo, plan, tt, T * k)
