@@ -919,7 +919,7 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   if (L.max_tiles < grid) grid = L.max_tiles;
   if (grid < 1) grid = 1;
   GemmParams p = L.p;
-  p.dbg = gemm_dbg();
+  p.dbg = MODE == DENSE ? 0 : gemm_dbg();  // experiment knobs act on the products only (routing stays valid)
   {
     // MOE_EPI_DIRECT=1: epilogue stores by st.global through a shared-memory
     // transpose instead of TMA (measured slower at MoE-XS: SDD 129 vs 111 us,
@@ -1022,7 +1022,10 @@ static int pick_bn(const moe_config* cfg, bool pairs_columns) {
 // (measured slower at MoE-XS: half-empty pairs of odd-row experts).
 static bool use_pair_rows() {
   static int v = -1;
-  if (v < 0) v = getenv("MOE_GEMM_PAIR_ROWS") != nullptr;
+  if (v < 0) {
+    const char* e = getenv("MOE_GEMM_PAIR_ROWS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
   return v == 1;
 }
 

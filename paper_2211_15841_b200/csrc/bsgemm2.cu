@@ -36,6 +36,14 @@
 
 namespace moe {
 
+#ifndef MOE_PAIR_NP
+#define MOE_PAIR_NP 2
+#endif
+constexpr int P_NP = MOE_PAIR_NP;              // TMA producer warps per CTA (stage s issued by warp s % P_NP):
+                                               // one issuing thread keeps too few boxes in flight
+constexpr int P_MMA_WARP = P_NP;
+constexpr int P_EPI_WARP0 = P_NP + 1;
+constexpr int P_THREADS = 32 * (P_NP + 1 + NUM_EPI_WARPS);
 constexpr int P_BN = 256;                      // N of the pair MMA
 constexpr int P_BH = 128;                      // B columns held per CTA
 constexpr int P_A_BYTES = A_BYTES;             // 128 x 64
@@ -134,7 +142,7 @@ __device__ __forceinline__ void out_coords2(const GemmParams& p, int mode, const
 }
 
 template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     bsgemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
                    const GemmParams p) {
@@ -175,7 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
   }
-  if (warp == 1) tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
+  if (warp == P_MMA_WARP) tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -184,8 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   pdl_wait();
   const int ntiles = num_tiles2(p, MODE);
 
-  if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
+  if (warp < P_NP) {
+    // ===================== TMA producers (both CTAs; warp s % P_NP issues stage s) =====================
     int stage = 0;
     uint32_t phase = 0;
     int tile_i = 0;
@@ -230,11 +238,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     };
     long long g_step = 0;
-    if (gat) {
+    // the gathered form keeps its token ring in one warp: warp 0 issues every stage, the others idle
+    const bool idle = gat && warp != 0;
+    if (gat && !idle) {
       la_decode();
       for (int i = 0; i < TD; ++i) la_issue();
     }
-    for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
+    for (int tile = cid; tile < ntiles && !idle; tile += ncl, ++tile_i) {
       const Tile2 t = decode2(p, MODE, tile, rank);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0;
@@ -265,7 +275,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                            r.w >= 0 ? r.w / kq : oob);
           ++g_step;
         }
-        mbar_wait(&empty[stage], phase ^ 1);
+        const bool mine = gat || stage % P_NP == warp;
+        if (mine) mbar_wait(&empty[stage], phase ^ 1);
         if (gat) {
           // A = X_g^T: 64 gathered K-rows x this CTA's 128 h-columns (two 64-wide
           // MN chunks); lane l: chunk l / 16, rows 4 (l % 16) .. +3
@@ -277,7 +288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tma_gather4_pair(sa + (lane >> 4) * (BK * 128) + (lane & 15) * 512, &tmap_a, fb, m0 + (lane >> 4) * 64,
                            atok.x, atok.y, atok.z, atok.w);
           if (lane == 0) tma_load_3d_pair(smem_b + stage * P_B_BYTES, &tmap_b, fb, 0, sblk * BM + kk * BK, 0);
-        } else if (lane == 0) {
+        } else if (mine && lane == 0) {
           uint8_t* sa = smem_a + stage * P_A_BYTES;
           uint8_t* sb = smem_b + stage * P_B_BYTES;
           uint64_t* fb = &full[stage];
@@ -323,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == P_MMA_WARP) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
     if (leader && lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(2 * BM, P_BN, A_MN, B_MN);
@@ -368,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ===================== epilogue (warps 2..9, both CTAs) =====================
     const int q = warp & 3;
-    const int wq = warp - 2;
+    const int wq = warp - P_EPI_WARP0;
     const int half = wq >> 2;                  // this warp's first chunk; it takes every EPG-th
     constexpr int EPG = NUM_EPI_WARPS / 4;     // epilogue warps per TMEM lane quarter
     const int row0 = q * 32;
@@ -479,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   cluster_sync();
-  if (warp == 1) {
+  if (warp == P_MMA_WARP) {
     tc_fence_after();
     tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
   }
@@ -501,7 +512,7 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
   p.trace = gemm_trace_slot();
-  cudaError_t le = launch_k(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
+  cudaError_t le = launch_k(kern, dim3(grid), dim3(P_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
   if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;
