@@ -297,6 +297,30 @@ def make_topology_closed_form(plan: Plan, bs: int, ffn: int) -> Topology:
                     t_col_offsets, t_block_offsets, t_row_indices)
 
 
+def fringe_rows(plan: Plan, bs: int):
+    """Partial blocks at the fringe ('We could remove this constraint
+    [padding to a multiple of 128] by supporting partial blocks at the fringe
+    of the problem', DESIGN reading R23): the dense
+    expert-grouped rows are NOT padded — row u holds assignment sorted_idx[u],
+    expert e's rows are [bins[e] - counts[e], bins[e]) — while the block
+    structure (BCSR over the padded block-rows) is unchanged. Block-row r, the
+    i-th of expert e, covers the dense rows [brow_start[r], brow_start[r] +
+    brow_rows[r]) with brow_start = bins[e] - counts[e] + bs*i and brow_rows =
+    min(bs, counts[e] - bs*i); rows of its blocks at or beyond brow_rows are
+    the fringe (zero in the sparse values). Returns (brow_start, brow_rows),
+    int64 [Tp / bs]."""
+    nbr = plan.Tp // bs
+    brow_start = np.zeros(nbr, np.int64)
+    brow_rows = np.zeros(nbr, np.int64)
+    for e in range(plan.counts.size):
+        r0 = (plan.padded_bins[e] - plan.padded_counts[e]) // bs
+        u0 = plan.bins[e] - plan.counts[e]
+        for i in range(plan.padded_counts[e] // bs):
+            brow_start[r0 + i] = u0 + bs * i
+            brow_rows[r0 + i] = min(bs, plan.counts[e] - bs * i)
+    return brow_start, brow_rows
+
+
 # ----------------------------------------------------------------------------
 # Block-sparse products, Triton notation (§4 'Preliminaries', P:177): output,
 # left input, right input; superscript T transposes an input. §5.1 (P:205-206):

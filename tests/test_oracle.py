@@ -651,3 +651,34 @@ def test_forward_given_expert_idx_vs_autograd(T, h, f, E, k, renorm):
     np.testing.assert_allclose(g["dwr"], twr.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw1"], tw1.grad.numpy(), atol=1e-10)
     np.testing.assert_allclose(g["dw2"], tw2.grad.numpy(), atol=1e-10)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fringe_rows_link_padded_and_unpadded_layouts(seed):
+    """fringe_rows (P:297 partial blocks at the fringe; R23): every assignment
+    at padded row p = pos[i] sits in block-row r = p // bs at offset p % bs;
+    in the unpadded layout it is dense row sorted_pos[i] = brow_start[r] +
+    p % bs, inside the block's valid rows; each expert's block-rows hold
+    exactly its counts (only the last one partial) and tile [bins-counts, bins)."""
+    rng = np.random.default_rng(seed)
+    E, bs = int(rng.integers(1, 9)), int(rng.choice([2, 4, 8]))
+    T, k = int(rng.integers(1, 60)), int(rng.integers(1, min(E, 3) + 1))
+    idx = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    plan = O.make_plan(idx, E, bs)
+    bst, brows = O.fringe_rows(plan, bs)
+    assert bst.size == plan.Tp // bs
+    sorted_pos = np.empty(T * k, np.int64)
+    sorted_pos[plan.sorted_idx] = np.arange(T * k)
+    for i in range(T * k):
+        p = plan.pos[i]
+        r, off = p // bs, p % bs
+        assert off < brows[r]
+        assert sorted_pos[i] == bst[r] + off
+    for e in range(E):
+        r0 = (plan.padded_bins[e] - plan.padded_counts[e]) // bs
+        nr = plan.padded_counts[e] // bs
+        assert brows[r0:r0 + nr].sum() == plan.counts[e]
+        if nr:
+            assert (brows[r0:r0 + nr - 1] == bs).all()
+            assert bst[r0] == plan.bins[e] - plan.counts[e]
+            assert bst[r0 + nr - 1] + brows[r0 + nr - 1] == plan.bins[e]
