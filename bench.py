@@ -191,7 +191,12 @@ class Step:
             ("topology", L.moe_topology_from_router, (c, d(sv.expert_idx), topo, ws, s)),
         ]
         gfused = bool(L.moe_gather_is_fused(c))   # layer.cu: the padded gather inside the SDD / DD^TS loads
-        if gfused:
+        unp = bool(cfg.unpadded)                  # layer.cu: no pad rows, partial blocks at the fringe
+        if unp:
+            self.calls += [("gather", L.moe_sort_rows, (c, d(t["x"]), topo, d(sv.x_g), s)),
+                           ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
+                                                     None if idn else d(sv.act_deriv), s))]
+        elif gfused:
             self.calls += [("sdd+gather", L.moe_sdd_gather, (c, d(t["x"]), d(t["w1"]), topo, cfg.act, d(sv.a),
                                                             None if idn else d(sv.act_deriv), d(sv.x_g), s))]
         else:
@@ -203,7 +208,14 @@ class Step:
                                                  d(t["y"]), s)),
         ]
         fused =cfg.num_experts % 64 == 0 and cfg.num_experts <= 256 and cfg.top_k <= 8
-        if fused:   # moe_backward's tensor-core router path (layer.cu)
+        if fused and unp:
+            bwd = [("scatter_bwd", L.moe_unsort_rows_bwd_router, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates),
+                                                                  d(sv.logits), d(sv.expert_idx), wsl["dy_g"],
+                                                                  wsl["dgates"], wsl["dlogits"], s))]
+        elif unp:
+            bwd = [("scatter_bwd", L.moe_unsort_rows_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"],
+                                                           wsl["dgates"], s))]
+        elif fused:   # moe_backward's tensor-core router path (layer.cu)
             bwd = [("scatter_bwd", L.moe_scatter_bwd_router, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), d(sv.logits),
                                                               d(sv.expert_idx), wsl["dy_g"], wsl["dgates"],
                                                               wsl["dlogits"], s))]
@@ -225,7 +237,8 @@ class Step:
         else:
             bwd += [("dsdT", L.moe_dsd, (c, wsl["dh"], 0, d(t["w1"]), 1, topo, wsl["dx_g"], s)),
                     ddts,
-                    ("gather_bwd", L.moe_gather_bwd, (c, wsl["dx_g"], topo, d(t["dx"]), s)),
+                    ("gather_bwd", L.moe_sort_rows_bwd if unp else L.moe_gather_bwd, (c, wsl["dx_g"], topo,
+                                                                                        d(t["dx"]), s)),
                     ("router_bwd", L.moe_router_bwd, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
                                                       wsl["dgates"], d(t["dwr"]), d(t["dx"]), ws, s))]
         self.calls += bwd
@@ -264,7 +277,8 @@ def run_ours_single(args, peaks):
     T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
     inp = S.make_inputs(shp, seed=0)
     cap = A.moe_expert_capacity(T, E, args.capacity_factor) if args.capacity_factor > 0 else 0
-    cfg = A.make_config(T, h, E, k, f, act=shp.act, capacity=cap)   # capacity 0: dropless (the headline)
+    cfg = A.make_config(T, h, E, k, f, act=shp.act, capacity=cap,   # capacity 0: dropless (the headline)
+                        unpadded=(args.layout == "unpadded" and not cap))
     stream = torch.cuda.current_stream()
     x = inp["x"].to(dev)
     dy = inp["dy"].to(dev)
@@ -427,6 +441,7 @@ def run_ours_single(args, peaks):
         "config": {"workload": shp.name, "tokens": T, "hidden": h, "ffn_hidden": f, "num_experts": E, "top_k": k,
                    "block_size": 128, "act": "gelu_tanh", "routing": shp.routing, "parallelism": "ep1",
                    "padded_rows": Tp, "nnz_blocks": nnz,
+                   "layout": "unpadded (partial blocks at the fringe, P:297)" if cfg.unpadded else "padded (P:297)",
                    "expert_load_max_over_mean": round(float(counts.max() / counts.mean()), 3),
                    **({"formulation": "token-dropping", "capacity_factor": args.capacity_factor, "capacity": cap,
                        "dropped_fraction": round(1.0 - float(counts.sum()) / (T * k), 4)} if cap else
@@ -647,6 +662,9 @@ def main():
                     help="> 0: time the token-dropping formulation (P:112-116) with this capacity factor "
                          "instead of the dropless layer (context only; the headline is dropless)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--layout", default=os.environ.get("MOE_BENCH_LAYOUT", "padded"), choices=["padded", "unpadded"],
+                    help="dense expert-grouped rows padded to 128 per expert (P:297, the paper's layout) or not "
+                         "(partial blocks at the fringe, NEXT-3); same outputs")
     ap.add_argument("--transport", default=os.environ.get("MOE_EP_TRANSPORT", "auto"), choices=["auto", "nccl", "p2p"],
                     help="expert-parallel token exchange: device-initiated peer stores (p2p; auto = p2p with an "
                          "NCCL fallback if peer memory is unusable) or NCCL all-to-all")

@@ -79,6 +79,13 @@ typedef struct {
                            expert is e, held constant; P_e = mean router probability). moe_forward
                            writes it to the workspace (moe_workspace_offset 5) and moe_backward
                            adds its gradient (d total / d aux = 1) to the router's. */
+  int32_t unpadded;     /* 0: the dense expert-grouped rows (X_g, Y_g, dY_g, dX_g) are padded to a multiple of
+                           bs per expert, as the paper implements it. 1: they are NOT padded (row u =
+                           assignment sorted_idx[u]) and every expert's last block-row is a partial block at
+                           the fringe ("We could remove this constraint by supporting partial blocks at
+                           the fringe"; reading R23): the block topology is unchanged, the
+                           sparse values' rows beyond brow_rows are exact zeros, the products read / write
+                           dense rows at brow_start. Dropless only (capacity 0). Same outputs. */
 } moe_config;
 
 /* ---- configuration and size queries (host only, no CUDA calls) ---------- */
@@ -139,6 +146,11 @@ typedef struct {
   int32_t* row_src;         /* [max_rows] flat id i = t*k + j held by padded row p (the
                                     inverse of pos), -1 for pad rows                          */
   int32_t* sizes;           /* [3] = {Tp, nnz, row pairs}, written on the device             */
+  int32_t* brow_start;      /* [max_rows/bs] unpadded layout (moe_config.unpadded, P:297 partial blocks at
+                                    the fringe): first dense row of block-row r = bins[e]-counts[e]+bs*i
+                                    for the i-th block-row of expert e                         */
+  int32_t* brow_rows;       /* [max_rows/bs] rows of block-row r that hold assignments: min(bs,
+                                    counts[e]-bs*i); the rest of its blocks is the fringe       */
 } moe_topology_t;
 
 /* Router, §2.1: logits = x . wr (fp32 accumulate of bf16 inputs),

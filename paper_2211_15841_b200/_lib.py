@@ -19,12 +19,12 @@ class MoeConfig(ctypes.Structure):
     _fields_ = [("tokens", ctypes.c_int64), ("hidden", ctypes.c_int64), ("num_experts", ctypes.c_int64),
                 ("top_k", ctypes.c_int64), ("ffn_hidden", ctypes.c_int64), ("block_size", ctypes.c_int64),
                 ("act", ctypes.c_int32), ("capacity", ctypes.c_int32),
-                ("renormalize", ctypes.c_int32), ("aux_loss_coeff", ctypes.c_float)]
+                ("renormalize", ctypes.c_int32), ("aux_loss_coeff", ctypes.c_float), ("unpadded", ctypes.c_int32)]
 
 
 TOPO_FIELDS = ["counts", "bins", "padded_bins", "sorted_idx", "pos", "sorted_pos", "row_offsets",
                "col_indices", "row_indices", "t_col_offsets", "t_block_offsets", "t_row_indices", "pair_bins", "row_src",
-               "sizes"]
+               "sizes", "brow_start", "brow_rows"]
 
 
 class MoeTopology(ctypes.Structure):

@@ -15,13 +15,13 @@ ACT_IDENTITY, ACT_GELU, ACT_RELU = 0, 1, 2
 
 
 def make_config(tokens, hidden, num_experts, top_k, ffn_hidden, block_size=128, act=ACT_GELU,
-                capacity=0, renormalize=False, aux_loss_coeff=0.0) -> MoeConfig:
+                capacity=0, renormalize=False, aux_loss_coeff=0.0, unpadded=False) -> MoeConfig:
     """capacity = 0: dropless (the method). > 0: the token-dropping formulation
     with that many assignments kept per expert (moe_expert_capacity).
     renormalize: divide each token's k gates by their sum. aux_loss_coeff > 0:
     auxiliary load-balancing loss (moe_load_balance_loss)."""
     return MoeConfig(int(tokens), int(hidden), int(num_experts), int(top_k), int(ffn_hidden), int(block_size),
-                     int(act), int(capacity), int(bool(renormalize)), float(aux_loss_coeff))
+                     int(act), int(capacity), int(bool(renormalize)), float(aux_loss_coeff), int(bool(unpadded)))
 
 
 def aux_region(cfg, ws) -> torch.Tensor:
@@ -95,7 +95,7 @@ class Topology:
         shapes = {"counts": E, "bins": E, "padded_bins": E, "sorted_idx": R, "pos": R, "sorted_pos": R,
                   "row_offsets": rows // bs + 1, "col_indices": nnz, "row_indices": nnz,
                   "t_col_offsets": E * F + 1, "t_block_offsets": nnz, "t_row_indices": nnz, "pair_bins": E,
-                  "row_src": rows, "sizes": 3}
+                  "row_src": rows, "sizes": 3, "brow_start": rows // bs, "brow_rows": rows // bs}
         # one allocation, 16-byte aligned views (TMA / int4 loads read row_src)
         sizes = [((max(int(shapes[n]), 1) + 3) // 4) * 4 for n in TOPO_FIELDS]
         self.buf = torch.empty(sum(sizes), dtype=torch.int32, device=device)

@@ -114,20 +114,28 @@ struct TileInfo {
   int u, v;        // SDD: (block row, block col); DSD_ROW/DDS_ROW: (r, dense tile);
                    // DS_COL/DDS_COL: (block col, dense tile); DENSE: (m tile, n tile)
   int s;           // SDD: first block storage index; DENSE: split
+  int drow;        // SDD / DSD_ROW: first dense row of block-row u (u*BM; brow_start[u] unpadded)
+  int vr;          // SDD / DSD_ROW: rows of block-row u holding assignments (BM padded; brow_rows[u])
 };
 
 __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pair, int tile) {
   TileInfo t;
   t.s = 0;
   t.walk_begin = 0;
+  t.drow = 0;
+  t.vr = BM;
   if (mode == SDD) {
     t.s = tile * pair;
     t.u = __ldg(p.row_indices + t.s);
     t.v = __ldg(p.col_indices + t.s);
     t.kiters = p.k_dense / BK;
+    t.drow = p.unpadded ? __ldg(p.brow_start + t.u) : t.u * BM;
+    if (p.unpadded) t.vr = __ldg(p.brow_rows + t.u);
   } else if (mode == DSD_ROW || mode == DDS_ROW) {
     t.u = tile / p.dense_tiles;
     t.v = tile % p.dense_tiles;
+    t.drow = p.unpadded ? __ldg(p.brow_start + t.u) : t.u * BM;
+    if (p.unpadded) t.vr = __ldg(p.brow_rows + t.u);
     const int b = __ldg(p.row_offsets + t.u), e = __ldg(p.row_offsets + t.u + 1);
     t.walk_begin = b;
     t.kiters = KPB * (e - b);
@@ -163,7 +171,7 @@ __device__ __forceinline__ void out_coords(const GemmParams& p, int mode, const 
       y = blk * BM + row0;
       break;
     }
-    case DSD_ROW: x = t.v * BN + col; y = t.u * BM + row0; break;
+    case DSD_ROW: x = t.v * BN + col; y = t.drow + row0; break;
     case DS_COL: x = t.v * BN + col; y = t.u * BM + row0; break;
     case DDS_COL: x = t.u * 128 + col; y = t.v * BM + row0; break;
     case DDS_ROW: x = t.u * 128 + col; y = t.v * BM + row0; break;
@@ -189,13 +197,14 @@ __device__ __forceinline__ void ld3(void* dst, const CUtensorMap* m, uint64_t* f
 template <int MODE, bool A_MN, bool B_MN, int BN>
 __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtensorMap* tb, const GemmParams& p,
                                             const TileInfo& t, int kit, int sblk, int oblk, uint8_t* sa, uint8_t* sb,
-                                            uint64_t* fb, int part = 3) {
+                                            uint64_t* fb, int part = 3, int odrow = 0) {
+  // odrow: first dense row of the walked block-row oblk (column walks: oblk*BM, brow_start[oblk] unpadded)
   const int kk = kit % KPB;
   if (!(part & 1)) ta = nullptr;  // A boxes skipped below
   if (!(part & 2)) tb = nullptr;
   if (MODE == SDD) {
     const int k0 = kit * BK;
-    tma_load_2d(sa, ta, fb, k0, t.u * BM);
+    tma_load_2d(sa, ta, fb, k0, t.drow);
     if (B_MN)
       tma_load_3d(sb, tb, fb, 0, k0, t.v * 2);
     else
@@ -209,14 +218,14 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtenso
   } else if (MODE == DS_COL) {
     tma_load_3d(sa, ta, fb, 0, sblk * BM + kk * BK, 0);
     if (B_MN)
-      tma_load_3d(sb, tb, fb, 0, oblk * BM + kk * BK, t.v * (BN / 64));
+      tma_load_3d(sb, tb, fb, 0, odrow + kk * BK, t.v * (BN / 64));
     else
-      tma_load_2d(sb, tb, fb, oblk * BM + kk * BK, t.v * BN);
+      tma_load_2d(sb, tb, fb, odrow + kk * BK, t.v * BN);
   } else if (MODE == DDS_COL) {
     if (A_MN)
-      tma_load_3d(sa, ta, fb, 0, oblk * BM + kk * BK, t.v * 2);
+      tma_load_3d(sa, ta, fb, 0, odrow + kk * BK, t.v * 2);
     else
-      tma_load_2d(sa, ta, fb, oblk * BM + kk * BK, t.v * BM);
+      tma_load_2d(sa, ta, fb, odrow + kk * BK, t.v * BM);
 #pragma unroll
     for (int j = 0; j < BN / 128; ++j)  // blocks (r, c + j): storage sblk + j
       tma_load_3d(sb + j * (2 * BK * 128), tb, fb, 0, (sblk + j) * BM + kk * BK, 0);
@@ -313,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tile_i) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
       if (lane == 0) trace_ev(p, tile_i, 0);
-      int idx_a = 0, idx_b = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
+      int idx_a = 0, idx_b = 0, idx_c = 0;  // per-lane cached walk entries (32 sparse blocks at a time)
       int4 atok = make_int4(0, 0, 0, 0);
       if (MODE == SDD && p.gather_a) {
         const int4 r = tok_next;
@@ -324,10 +333,18 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       }
       int4 gtok = make_int4(0, 0, 0, 0);
       if (MODE == DSD_ROW && p.extra_k) {  // tokens of the tile's rows 4*lane .. 4*lane+3
-        const int4 src = __ldg(reinterpret_cast<const int4*>(p.row_src + t.u * BM) + lane);
         const int oob = p.scatter_T;
-        gtok = make_int4(src.x >= 0 ? src.x : oob, src.y >= 0 ? src.y : oob, src.z >= 0 ? src.z : oob,
-                         src.w >= 0 ? src.w : oob);
+        if (p.unpadded) {  // dense row drow + r holds flat id sorted_idx[drow + r] (= the token, top-1)
+          const int r = 4 * lane;
+          gtok = make_int4(r < t.vr ? __ldg(p.sorted_idx + t.drow + r) : oob,
+                           r + 1 < t.vr ? __ldg(p.sorted_idx + t.drow + r + 1) : oob,
+                           r + 2 < t.vr ? __ldg(p.sorted_idx + t.drow + r + 2) : oob,
+                           r + 3 < t.vr ? __ldg(p.sorted_idx + t.drow + r + 3) : oob);
+        } else {
+          const int4 src = __ldg(reinterpret_cast<const int4*>(p.row_src + t.u * BM) + lane);
+          gtok = make_int4(src.x >= 0 ? src.x : oob, src.y >= 0 ? src.y : oob, src.z >= 0 ? src.z : oob,
+                           src.w >= 0 ? src.w : oob);
+        }
       }
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit / KPB, kk = kit % KPB;
@@ -340,11 +357,13 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             } else {
               idx_a = __ldg(p.t_block_offsets + q);
               idx_b = __ldg(p.t_row_indices + q);
+              idx_c = p.unpadded ? __ldg(p.brow_start + idx_b) : idx_b * BM;
             }
           }
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
+        const int odrow = __shfl_sync(0xffffffffu, idx_c, blk & 31);
         const bool mine = stage % C::NP == warp;
         if (mine) mbar_wait(&empty[stage], phase ^ 1);
         if (mine && MODE == DSD_ROW && kit >= t.s) {
@@ -373,7 +392,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
           } else {
             mbar_arrive_expect_tx(fb, C::STAGE);
             issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
-                                              smem_b + stage * C::B_BYTES, fb);
+                                              smem_b + stage * C::B_BYTES, fb, 3, odrow);
           }
         }
         __syncwarp();
@@ -451,6 +470,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     // instruction): the epilogue does not queue behind the TMA unit, which
     // stays with the operand loads. `tok` maps staging row -> output row
     // (scatter to token rows; < 0 or >= rows: dropped).
+    TileInfo cur_tile{};  // the tile being stored (row clipping of the unpadded layout)
     auto store_direct = [&](__nv_bfloat16* base, long long ld, long long nrows, const float* v, int x, int y,
                             int tok_of_lane) {
       uint8_t* buf = stg + sbuf * EPI_BUF;
@@ -471,6 +491,15 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;  // the other buffer next: one __syncwarp per chunk
     };
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
+      if (MODE == DSD_ROW && p.unpadded && map == &tmap_c) {
+        // the tile's block-row ends at the fringe (the rows below belong to the
+        // next expert): warps with rows past it store row-clipped
+        const TileInfo& tc = cur_tile;
+        if (row0 + 32 > tc.vr) {
+          store_direct(p.out_c, p.ldc, (long long)tc.drow + tc.vr, v, x, y, INT_MIN);
+          return;
+        }
+      }
       if (p.direct) {
         if (map == &tmap_c)
           store_direct(p.out_c, p.ldc, p.rows_c, v, x, y, INT_MIN);
@@ -533,8 +562,12 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
     int tile_i = -1;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const TileInfo t = decode(p, MODE, PAIR, p.reverse ? ntiles - 1 - tile : tile);
+      cur_tile = t;
       ++tile_i;
       const bool has_acc = (p.dbg & 64) ? false : t.kiters > 0;
+      // unpadded layout: this lane's row of an SDD tile is past the block-row's
+      // assignments (the fringe): its values are written as exact zeros
+      const bool fringe = MODE == SDD && p.unpadded && row0 + lane >= t.vr;
       // DENSE + EPI_ADD_ROWS: this lane's addend rows for all of its chunks are
       // in registers before the accumulator is waited for; the next tile's rows
       // are loaded now, so the gather latency overlaps this tile's epilogue.
@@ -543,7 +576,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
       int my_tok = 0x7fffffff;  // scatter target row (out of range: dropped)
       float my_gate = 0.f;
       if (MODE == DSD_ROW && p.scatter_y) {
-        const int src = __ldg(p.row_src + t.u * BM + row0 + lane);
+        const int src = p.unpadded ? (row0 + lane < t.vr ? __ldg(p.sorted_idx + t.drow + row0 + lane) : -1)
+                                   : __ldg(p.row_src + t.u * BM + row0 + lane);
         if (src >= 0) {
           my_tok = src;
           my_gate = p.scatter_gates ? __ldg(p.scatter_gates + src) : 1.f;
@@ -599,12 +633,20 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 32; ++e) v[e] = 0.f;
           }
+          if (fringe) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = 0.f;
+          }
           int x, y;
           out_coords(p, MODE, t, c, row0, BN, x, y);
           if (p.epi == EPI_ACT_FWD) {
             if (p.has_pre && p.aux_deriv) {  // save act'(H) beside act(H)
               float g[32];
               act_fwd_deriv32(p.act, v, g);
+              if (fringe) {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) g[e] = 0.f;
+              }
               store_chunk(&tmap_d, g, x, y);
             } else {
               if (p.has_pre) store_chunk(&tmap_d, v, x, y);
@@ -1001,6 +1043,10 @@ GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo) {
   p.padded_bins = topo->padded_bins;
   p.F = (int)(cfg->ffn_hidden / cfg->block_size);
   p.E = (int)cfg->num_experts;
+  p.unpadded = cfg->unpadded;
+  p.brow_start = topo->brow_start;
+  p.brow_rows = topo->brow_rows;
+  p.sorted_idx = topo->sorted_idx;
   p.n_block_cols = (int)(cfg->num_experts * cfg->ffn_hidden / cfg->block_size);
   p.k_dense = (int)cfg->hidden;
   p.epi = EPI_STORE;
@@ -1149,7 +1195,9 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
 }
 
 // The fused-gather products need the CTA-pair column kernels (even F, h % 256 == 0) and 64-wide K-steps.
-static bool gather_fusable(const moe_config* cfg) { return use_pair(cfg) && BK == 64 && cfg->block_size == 128; }
+static bool gather_fusable(const moe_config* cfg) {
+  return use_pair(cfg) && BK == 64 && cfg->block_size == 128 && !cfg->unpadded;
+}
 
 // Whether the layer (moe_forward / moe_backward) gathers inside the products.
 // Off by default: the 32 tile::gather4 requests per stage (one 128 B row each
@@ -1193,7 +1241,12 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
   MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  const bool pair = use_pair(cfg) && (trans_s || use_pair_rows());
+  // (the row-pair DSD exists only for the padded layout)
+  const bool pair = use_pair(cfg) && (trans_s || (use_pair_rows() && !cfg->unpadded));
+  // dense rows the products read along K: with the unpadded layout the rows
+  // past the last expert's fringe are out of range (TMA zero fill), so their
+  // stale contents never meet the fringe's zero sparse rows
+  const int64_t drows = cfg->unpadded ? cfg->tokens * cfg->top_k : rows;
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.bn = pick_bn(cfg, false);
@@ -1235,9 +1288,9 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
     L.max_tiles = (pair ? L.p.n_block_cols / 2 : L.p.n_block_cols) * L.p.dense_tiles;
     MOE_TRY(make_tmap_bf16_mn(&L.ta, s, 128, nnz * 128, 128, 2, "moe_dsd s^T"));
     if (!trans_b)
-      MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, rows, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
+      MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, drows, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
-      MOE_TRY(make_tmap_bf16(&L.tb, b, rows, h, rows, BK, bbox, "moe_dsd b^T", KSW));
+      MOE_TRY(make_tmap_bf16(&L.tb, b, drows, h, rows, BK, bbox, "moe_dsd b^T", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, h, N, h, "moe_dsd out"));
     set_epi_out(L.p, 0, out, N, h);
   }
@@ -1264,6 +1317,9 @@ moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, con
   // general k: dX_g = dH . W1^T, then dx = sum_j dX_g[pos] (+ dlogits . Wr^T)
   MOE_CHECK_ARG(dx_g, "moe_dsd_dx: top_k > 1 needs the dx_g scratch buffer");
   MOE_TRY(moe_dsd(cfg, dh, 0, w1, 1, topo, dx_g, stream));
+  if (cfg->unpadded)  // unpadded rows: the expert-order re-sort (+ the router term, tcgen05)
+    return router_term ? moe_sort_rows_bwd_router(cfg, dx_g, topo, dlogits_bf16, wr, dx, stream)
+                       : moe_sort_rows_bwd(cfg, dx_g, topo, dx, stream);
   if (!router_term) return moe_gather_bwd(cfg, dx_g, topo, dx, stream);
   static int gathered = -1;  // MOE_ROUTER_DX_GATHERED=1: the router-dx GEMM gathers the k rows itself
   if (gathered < 0) {
@@ -1286,6 +1342,7 @@ moe_status moe_dsd_scatter(const moe_config* cfg, const void* s, const void* b, 
   if (cfg && cfg->top_k == 1 && cfg->capacity == 0 && cfg->block_size == 128 && !use_pair_rows())
     return dsd_launch(cfg, s, 0, b, 0, topo, y_g, gates, y, stream);
   MOE_TRY(moe_dsd(cfg, s, 0, b, 0, topo, y_g, stream));  // k > 1: slots are summed by the combine kernel
+  if (cfg && cfg->unpadded) return moe_unsort_rows(cfg, y_g, topo, gates, y, stream);  // unpadded rows
   return moe_scatter(cfg, y_g, topo, gates, y, stream);
 }
 
@@ -1313,6 +1370,7 @@ static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, 
   MOE_CHECK_ARG(a && s && out, "moe_dds: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
+  const int64_t drows = cfg->unpadded ? cfg->tokens * cfg->top_k : rows;  // see dsd_launch
   GemmLaunch L{};
   L.p = gemm_params_topo(cfg, topo);
   L.a_mn = trans_a != 0;
@@ -1333,15 +1391,17 @@ static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, 
       L.p.gather_T = (int)cfg->tokens;
       L.p.row_src = topo->row_src;
     } else if (trans_a)
-      MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, rows, h, 2, "moe_dds a^T"));
+      MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, drows, h, 2, "moe_dds a^T"));
     else
-      MOE_TRY(make_tmap_bf16(&L.ta, a, rows, h, rows, BK, 128, "moe_dds a", KSW));
+      MOE_TRY(make_tmap_bf16(&L.ta, a, drows, h, rows, BK, 128, "moe_dds a", KSW));
     MOE_TRY(make_tmap_epi(&L.tc, out, N, h, N, "moe_dds out"));
     set_epi_out(L.p, 0, out, h, N);
     L.td = L.tc;
     return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
   }
   // out [h, rows] = A_eff [h, E*f] . S^T ; walk rows
+  if (cfg->unpadded)
+    return set_error(MOE_EUNSUPPORTED, "moe_dds(trans_s=1): the padded layout only (its output columns are dense rows)");
   L.p.dense_tiles = (int)(h / BM);
   L.name = trans_a ? "moe_dds(T,S^T)" : "moe_dds(S^T)";
   L.mode = DDS_ROW;

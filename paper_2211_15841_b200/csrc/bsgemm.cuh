@@ -40,6 +40,12 @@ struct GemmParams {
   int extra_k;
   int gather_a, gather_k, gather_T;  // SDD / DDS_COL: A rows gathered from x [T, h] by row_src / k (OOB: zeros)  // DSD_ROW: dense K-steps appended per tile (A: tmap_e gathered by row_src, B: tmap_f)
   const int32_t* row_src;
+  // unpadded dense layout (moe_config.unpadded, P:297 partial blocks at the fringe): dense rows of
+  // block-row r start at brow_start[r], rows >= brow_rows[r] of its blocks are the fringe
+  int unpadded;
+  const int32_t* brow_start;
+  const int32_t* brow_rows;
+  const int32_t* sorted_idx;  // dense row u -> flat id (the token for top-1)
   const float* scatter_gates;  // EPI_ACT_FWD: the aux output is act'(H), not H; EPI_ACT_BWD: the source holds act'(H)
   int rows_valid;  // rows of the output that exist (DENSE: M)
   // EPI_ROUTER

@@ -247,7 +247,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     for (int tile = cid; tile < ntiles && !idle; tile += ncl, ++tile_i) {
       const Tile2 t = decode2(p, MODE, tile, rank);
       if (lane == 0) trace_ev(p, tile_i, 0);
-      int idx_a = 0, idx_b = 0;
+      int idx_a = 0, idx_b = 0, idx_c = 0;
+      // SDD: first dense row of this CTA's block-row (unpadded layout: brow_start; a
+      // missing second row of a half-empty pair loads the first row's, stores nothing)
+      const int sdd_row = MODE == SDD ? (p.unpadded ? __ldg(p.brow_start + t.r0 + ((rank && t.second) ? 1 : 0))
+                                                    : (t.r0 + rank) * BM)
+                                      : 0;
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
@@ -259,11 +264,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             } else {
               idx_a = __ldg(p.t_block_offsets + qq) + rank;  // this CTA's column of the pair
               idx_b = __ldg(p.t_row_indices + qq);
+              idx_c = p.unpadded ? __ldg(p.brow_start + idx_b) : idx_b * BM;  // its dense rows
             }
           }
         }
         const int sblk = __shfl_sync(0xffffffffu, idx_a, blk & 31);
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
+        const int odrow = __shfl_sync(0xffffffffu, idx_c, blk & 31);
         int4 atok = make_int4(0, 0, 0, 0);
         if (gat) {
           la_issue();  // K-step g_step + TD
@@ -295,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           if (leader) mbar_arrive_expect_tx(fb, 2 * P_STAGE);
           if (MODE == SDD) {
             const int k0 = kit * BK;
-            tma_load_2d_pair(sa, &tmap_a, fb, k0, (t.r0 + rank) * BM);
+            tma_load_2d_pair(sa, &tmap_a, fb, k0, sdd_row);
             if (B_MN) {  // W1 [h, E*f]: this CTA's block column c0 + rank (3-D MN box, 2 chunks)
               tma_load_3d_pair(sb, &tmap_b, fb, 0, k0, (t.c0 + rank) * 2);
             } else {     // W2 [E*f, h]
@@ -313,16 +320,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             tma_load_3d_pair(sa, &tmap_a, fb, 0, sblk * BM + kk * BK, 0);
             const int n0 = t.v * P_BN + rank * P_BH;
             if (B_MN) {
-              tma_load_3d_pair(sb, &tmap_b, fb, 0, oblk * BM + kk * BK, n0 / 64);
+              tma_load_3d_pair(sb, &tmap_b, fb, 0, odrow + kk * BK, n0 / 64);
             } else {
-              tma_load_2d_pair(sb, &tmap_b, fb, oblk * BM + kk * BK, n0);
+              tma_load_2d_pair(sb, &tmap_b, fb, odrow + kk * BK, n0);
             }
           } else {  // DDS_COL: A = dense rows (2v + rank) tile, B = block sblk (this CTA's column)
             const int m0 = (2 * t.v + rank) * BM;
             if (A_MN) {
-              tma_load_3d_pair(sa, &tmap_a, fb, 0, oblk * BM + kk * BK, m0 / 64);
+              tma_load_3d_pair(sa, &tmap_a, fb, 0, odrow + kk * BK, m0 / 64);
             } else {
-              tma_load_2d_pair(sa, &tmap_a, fb, oblk * BM + kk * BK, m0);
+              tma_load_2d_pair(sa, &tmap_a, fb, odrow + kk * BK, m0);
             }
             tma_load_3d_pair(sb, &tmap_b, fb, 0, sblk * BM + kk * BK, 0);
           }
@@ -420,6 +427,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       ++tile_i;
       const bool has_acc = t.kiters > 0;
       const bool mine = rank == 0 || t.second;  // does this CTA own real output rows?
+      // unpadded layout: this lane's row of the CTA's SDD block-row is the fringe: zeros
+      const bool fringe = MODE == SDD && p.unpadded && mine && row0 + lane >= __ldg(p.brow_rows + t.r0 + rank);
       if (EPI_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
@@ -448,12 +457,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.f;
           }
+          if (fringe) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
           int x, y;
           out_coords2(p, MODE, t, rank, c, row0, p.F, x, y);
           if (p.epi == EPI_ACT_FWD) {
             if (p.has_pre && p.aux_deriv) {
               float g[32];
               act_fwd_deriv32(p.act, v, g);
+              if (fringe) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) g[i] = 0.f;
+              }
               store_chunk(&tmap_d, g, x, y);
             } else {
               if (p.has_pre) store_chunk(&tmap_d, v, x, y);

@@ -87,7 +87,7 @@ moe_status ep_alloc(moe_ep* ep, void** p, size_t bytes) {
 moe_status ep_topology(moe_ep* ep, const moe_config* cfg, moe_topology_t* t) {
   const int64_t E = cfg->num_experts, bs = cfg->block_size, R = cfg->tokens * cfg->top_k;
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg), F = cfg->ffn_hidden / bs;
-  const int64_t n[] = {E, E, E, R, R, R, rows / bs + 1, nnz, nnz, E * F + 1, nnz, nnz, E, rows, 3};
+  const int64_t n[] = {E, E, E, R, R, R, rows / bs + 1, nnz, nnz, E * F + 1, nnz, nnz, E, rows, 3, rows / bs, rows / bs};
   int64_t total = 0;
   for (int64_t v : n) total += (v + 3) / 4 * 4;  // 16-byte aligned fields (int4 loads of row_src)
   void* buf;
@@ -95,9 +95,9 @@ moe_status ep_topology(moe_ep* ep, const moe_config* cfg, moe_topology_t* t) {
   int32_t* p = reinterpret_cast<int32_t*>(buf);
   int32_t** f[] = {&t->counts, &t->bins, &t->padded_bins, &t->sorted_idx, &t->pos, &t->sorted_pos,
                    &t->row_offsets, &t->col_indices, &t->row_indices, &t->t_col_offsets, &t->t_block_offsets,
-                   &t->t_row_indices, &t->pair_bins, &t->row_src, &t->sizes};
-  static_assert(sizeof(f) / sizeof(f[0]) == 15, "moe_topology_t has 15 arrays");
-  for (int i = 0; i < 15; ++i) {
+                   &t->t_row_indices, &t->pair_bins, &t->row_src, &t->sizes, &t->brow_start, &t->brow_rows};
+  static_assert(sizeof(f) / sizeof(f[0]) == 17, "moe_topology_t has 17 arrays");
+  for (int i = 0; i < 17; ++i) {
     *f[i] = p;
     p += (n[i] + 3) / 4 * 4;
   }

@@ -66,7 +66,11 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   MOE_TRY(moe_topology_from_router(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
-  if (moe_gather_is_fused(cfg)) {  // the gather happens inside the SDD's loads (tile::gather4)
+  if (cfg->unpadded) {  // P:297 partial blocks at the fringe: X_g rows in expert order, no pad rows
+    MOE_TRY(moe_sort_rows(cfg, x, &sv->topo, sv->x_g, stream));
+    MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
+                          stream));
+  } else if (moe_gather_is_fused(cfg)) {  // the gather happens inside the SDD's loads (tile::gather4)
     MOE_TRY(moe_sdd_gather(cfg, x, w->w1, &sv->topo, cfg->act, sv->a, id ? nullptr : sv->act_deriv, sv->x_g, stream));
   } else {
     MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
@@ -95,7 +99,13 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   __nv_bfloat16* dl16 = reinterpret_cast<__nv_bfloat16*>(wsb + L.dlogits);
   // b1: dY_g = gates * dy (un-permuted rows), dgates = <Y_g, dy>
   //     [+ b7's dlogits = p * (dp - <p,dp>) in the same pass]
-  if (fused_router) {
+  if (cfg->unpadded && fused_router) {  // unpadded rows: the expert-order backward (+ softmax backward)
+    MOE_TRY(moe_unsort_rows_bwd_router(cfg, dy, sv->y_g, topo, sv->gates, sv->logits, sv->expert_idx, dy_g, dgates,
+                                       dl16, stream));
+    MOE_TRY(moe_add_aux_dlogits(cfg, sv->logits, dl16, ws, stream));
+  } else if (cfg->unpadded) {
+    MOE_TRY(moe_unsort_rows_bwd(cfg, dy, sv->y_g, topo, sv->gates, dy_g, dgates, stream));
+  } else if (fused_router) {
     const float* aux_c = cfg->aux_loss_coeff > 0.f ? reinterpret_cast<const float*>(wsb + L.aux) + 1 : nullptr;
     MOE_TRY(scatter_bwd_router_aux(cfg, dy, sv->y_g, topo, sv->gates, sv->logits, sv->expert_idx, dy_g, dgates,
                                    dl16, aux_c, as_stream(stream)));
@@ -150,7 +160,10 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   else
     MOE_TRY(moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, stream));
   // b6: dx = sum_j dX_g[pos]
-  MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
+  if (cfg->unpadded)
+    MOE_TRY(moe_sort_rows_bwd(cfg, dx_g, topo, dx, stream));
+  else
+    MOE_TRY(moe_gather_bwd(cfg, dx_g, topo, dx, stream));
   // b7: router backward (dWr, dx += dlogits . Wr^T)
   MOE_TRY(moe_router_bwd(cfg, x, w->wr, sv->logits, sv->expert_idx, dgates, g->dwr, dx, ws, stream));
   return MOE_OK;

@@ -49,7 +49,7 @@ moe_status check_topo(const moe_topology_t* t) {
   if (!t) return set_error(MOE_EINVAL, "topology pointer is NULL");
   if (!t->counts || !t->bins || !t->padded_bins || !t->sorted_idx || !t->pos || !t->sorted_pos ||
       !t->row_offsets || !t->col_indices || !t->row_indices || !t->t_col_offsets || !t->t_block_offsets ||
-      !t->t_row_indices || !t->pair_bins || !t->row_src || !t->sizes)
+      !t->t_row_indices || !t->pair_bins || !t->row_src || !t->sizes || !t->brow_start || !t->brow_rows)
     return set_error(MOE_EINVAL, "topology has a NULL array");
   return MOE_OK;
 }
@@ -139,6 +139,10 @@ moe_status moe_check_config(const moe_config* cfg) {
     return set_error(MOE_EINVAL, "renormalize=%d must be 0 or 1", cfg->renormalize);
   if (!(cfg->aux_loss_coeff >= 0.f) || isinf(cfg->aux_loss_coeff))
     return set_error(MOE_EINVAL, "aux_loss_coeff=%g must be finite and >= 0", (double)cfg->aux_loss_coeff);
+  if (cfg->unpadded != 0 && cfg->unpadded != 1)
+    return set_error(MOE_EINVAL, "unpadded=%d must be 0 or 1", cfg->unpadded);
+  if (cfg->unpadded && cfg->capacity > 0)
+    return set_error(MOE_EUNSUPPORTED, "unpadded=1 is dropless only (capacity=%d)", cfg->capacity);
   if (cfg->block_size != 128)
     return set_error(MOE_EUNSUPPORTED, "block_size=%lld: the sm_100a path implements 128x128 blocks (P:222)",
                      (long long)cfg->block_size);

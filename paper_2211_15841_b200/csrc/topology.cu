@@ -210,7 +210,13 @@ __global__ void __launch_bounds__(1024) topo_scan_emit_kernel(const int32_t* __r
     topo.row_indices[s] = r;
     topo.col_indices[s] = e * F + j;
     const int32_t pc = ((s_cnt[e] + bs - 1) / bs) * bs;
-    if (j == 0) topo.row_offsets[r] = s;
+    if (j == 0) {
+      topo.row_offsets[r] = s;
+      // the unpadded layout (P:297 partial blocks at the fringe, R23): dense rows of block-row r
+      const int i = r - r0;
+      topo.brow_start[r] = s_start[e] + bs * i;
+      topo.brow_rows[r] = min(bs, s_cnt[e] - bs * i);
+    }
     // pad rows of this block-row (the tail of expert e's group) hold no
     // assignment: the row's F threads write them strided
     const int pad0 = s_pstart[e] + s_cnt[e];

@@ -71,6 +71,10 @@ def check_topology_exact(A, topo_gpu, plan, topo, R):
     src = np.full(Tp, -1, np.int64)
     src[plan.pos] = np.arange(R)
     np.testing.assert_array_equal(g["row_src"][:Tp], src)
+    # the unpadded layout's block-row starts / valid rows (P:297 fringe, R23)
+    bst, brows = O.fringe_rows(plan, 128)
+    np.testing.assert_array_equal(g["brow_start"][:Tp // 128], bst)
+    np.testing.assert_array_equal(g["brow_rows"][:Tp // 128], brows)
 
 
 # ------------------------------------------------------------------ routing
@@ -566,12 +570,16 @@ def assert_layer_close(y, dx, dwr, dw1, dw2, yo, go):
     assert_close("dwr", dwr.cpu().double().numpy(), go["dwr"], per="none")
 
 
+@pytest.mark.parametrize("unpadded", [False, True])
 @pytest.mark.parametrize("name,T,k,shp", LAYER_CASES)
-def test_layer_forward_backward(name, T, k, shp):
+def test_layer_forward_backward(name, T, k, shp, unpadded):
+    """moe_forward / moe_backward vs the oracle; unpadded=True: the dense rows
+    are not padded and each expert's last block-row is a partial block at the
+    fringe (NEXT-3) — same outputs, same topology."""
     d = dev()
     A = api()
     inp = S.make_inputs(shp, seed=3, tokens=T)
-    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, unpadded=unpadded)
     xd = inp["x"].to(d)
     wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
     y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
@@ -600,8 +608,9 @@ def test_layer_deterministic():
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C4"])
-def test_full_size_every_output(name):
+@pytest.mark.parametrize("name,unpadded", [("C1", False), ("C2", False), ("C4", False), ("C1", True),
+                                           ("C4", True)])
+def test_full_size_every_output(name, unpadded):
     """BASELINE configs[1] (MoE-XS, the bench workload, in bench.py's launch
     configuration), configs[2] (MoE-Small with the skewed router: empty and
     overloaded experts) and configs[4] (MoE-Medium top-2) at FULL size through
@@ -614,7 +623,7 @@ def test_full_size_every_output(name):
     shp = S.CONFIGS[name]
     T, h, f, E, k = shp.tokens, shp.hidden, shp.ffn, shp.experts, shp.top_k
     inp = S.make_inputs(shp, seed=0)
-    cfg = A.make_config(T, h, E, k, f, act=shp.act)
+    cfg = A.make_config(T, h, E, k, f, act=shp.act, unpadded=unpadded)
     xd = inp["x"].to(d)
     wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
     y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
@@ -837,7 +846,7 @@ def test_bench_ep_multi_rank_flow():
 
 RENORM_CASES = [("C0-k2", 1000, S.CONFIGS["C0"].replace(top_k=2), 0.0), ("C4-k2", 2048, S.CONFIGS["C4"], 0.0),
                 ("E64-k4", 1024, S.MoEShape("E64-k4", 1024, 256, 256, 64, 4), 0.0),
-                ("C4-k2-cf1", 2048, S.CONFIGS["C4"], 1.0)]
+                ("C4-k2-cf1", 2048, S.CONFIGS["C4"], 1.0), ("C4-k2-unpadded", 2048, S.CONFIGS["C4"], -1.0)]
 
 
 @pytest.mark.parametrize("name,T,shp,cf", RENORM_CASES)
@@ -851,7 +860,8 @@ def test_layer_renormalized_gates(name, T, shp, cf):
     A = api()
     inp = S.make_inputs(shp, seed=8, tokens=T)
     C = A.moe_expert_capacity(T, shp.experts, cf) if cf > 0 else 0
-    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, capacity=C, renormalize=True)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, capacity=C, renormalize=True,
+                        unpadded=cf < 0)      # cf = -1: dropless with the unpadded layout
     xd = inp["x"].to(d)
     wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
     y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
@@ -868,9 +878,13 @@ def test_layer_renormalized_gates(name, T, shp, cf):
 
 # ------------------------------------------------------------------ auxiliary load-balancing loss (NEXT-4)
 
-@pytest.mark.parametrize("name,T,shp", [("C0", 1024, S.CONFIGS["C0"]), ("C1-reduced", 4096, S.CONFIGS["C1"]),
-                                        ("C4-k2", 2048, S.CONFIGS["C4"]), ("C2-skew", 4096, S.CONFIGS["C2"])])
-def test_layer_aux_load_balance_loss(name, T, shp):
+@pytest.mark.parametrize("name,T,shp,unpadded", [("C0", 1024, S.CONFIGS["C0"], False),
+                                                 ("C1-reduced", 4096, S.CONFIGS["C1"], False),
+                                                 ("C4-k2", 2048, S.CONFIGS["C4"], False),
+                                                 ("C2-skew", 4096, S.CONFIGS["C2"], False),
+                                                 ("C1-reduced-unpadded", 4096, S.CONFIGS["C1"], True),
+                                                 ("C0-unpadded", 1024, S.CONFIGS["C0"], True)])
+def test_layer_aux_load_balance_loss(name, T, shp, unpadded):
     """cfg.aux_loss_coeff > 0: moe_forward writes the auxiliary loss to
     the workspace and moe_backward adds its router gradient; loss value and
     dx / dWr against the oracle routed from the GPU's logits."""
@@ -878,7 +892,8 @@ def test_layer_aux_load_balance_loss(name, T, shp):
     A = api()
     coeff = 0.01
     inp = S.make_inputs(shp, seed=12, tokens=T)
-    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, aux_loss_coeff=coeff)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, aux_loss_coeff=coeff,
+                        unpadded=unpadded)
     ws = A.workspace(cfg, d)
     xd = inp["x"].to(d)
     wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
@@ -894,16 +909,17 @@ def test_layer_aux_load_balance_loss(name, T, shp):
     assert_layer_close(y, dx, dwr, dw1, dw2, yo, go)
 
 
+@pytest.mark.parametrize("unpadded", [False, True])
 @pytest.mark.parametrize("T,shp", [(1, S.CONFIGS["C0"]), (3, S.CONFIGS["C1"]), (129, S.CONFIGS["C4"]),
                                    (2, S.CONFIGS["C0"].replace(top_k=2))])
-def test_layer_degenerate_token_counts(T, shp):
+def test_layer_degenerate_token_counts(T, shp, unpadded):
     """Degenerate batches through moe_forward / moe_backward: one token, fewer
     tokens than experts (most experts empty, a single partial block), one block
     plus one row; against the oracle routed from the GPU's logits."""
     d = dev()
     A = api()
     inp = S.make_inputs(shp, seed=31, tokens=T)
-    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act, unpadded=unpadded)
     xd = inp["x"].to(d)
     wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
     y, saved = A.moe_forward(cfg, wr, w1, w2, xd)
