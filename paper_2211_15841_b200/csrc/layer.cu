@@ -35,6 +35,18 @@ moe_status side_stream(SideStream** out) {
   return MOE_OK;
 }
 
+// MOE_BWD_CONCURRENT=1: the backward's independent products run two at a time
+// on split SM budgets (SDD^T beside dWr + DS^TD, then DD^TS beside DSD^T):
+// experiment knob (the persistent kernels' ramps and tails overlap).
+int bwd_concurrent() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_BWD_CONCURRENT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 // SMs given to the router dWr GEMM while the SDD^T runs beside it (MOE_DWR_SMS, 0 = serial).
 int dwr_side_sms() {
   static int v = -1;
@@ -129,12 +141,45 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
       return set_error(MOE_ECUDA, "moe_backward: join record failed");
     set_gemm_sm_budget(moe_device_sm_count() - side_sms);
   }
+  const int conc = side ? bwd_concurrent() : 0;
+  const int all = moe_device_sm_count();
+  if (conc) {
+    // b3 on the side stream after dWr, beside the SDD^T (dY_g is all it needs)
+    const int b3 = (int)(all * 0.42) & ~1;
+    set_gemm_sm_budget(b3);
+    const moe_status st = moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, side->s);
+    set_gemm_sm_budget(0);
+    MOE_TRY(st);
+    if (cudaEventRecord(side->join, side->s) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: join record failed");
+    set_gemm_sm_budget(all - b3 - side_sms);
+  }
   // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
   {
     const moe_status st =
         moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream);
     set_gemm_sm_budget(0);
     MOE_TRY(st);
+  }
+  if (conc) {
+    // b5 on the side stream (after b3) beside b4 + b6 + b7 on the main stream; both need dH
+    if (cudaEventRecord(side->fork, as_stream(stream)) != cudaSuccess ||
+        cudaStreamWaitEvent(side->s, side->fork, 0) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: fork failed");
+    const int b5 = (all / 2) & ~1;
+    set_gemm_sm_budget(b5);
+    const moe_status st = moe_dds(cfg, sv->x_g, 1, dh, 0, topo, g->dw1, side->s);
+    set_gemm_sm_budget(0);
+    MOE_TRY(st);
+    if (cudaEventRecord(side->join, side->s) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: join record failed");
+    set_gemm_sm_budget(all - b5);
+    const moe_status st2 = moe_dsd_dx(cfg, dh, w->w1, topo, dl16, w->wr, dx, dx_g, stream);
+    set_gemm_sm_budget(0);
+    MOE_TRY(st2);
+    if (cudaStreamWaitEvent(as_stream(stream), side->join, 0) != cudaSuccess)
+      return set_error(MOE_ECUDA, "moe_backward: join failed");
+    return MOE_OK;
   }
   // b3: DS^TD: dW2 = A^T . dY_g                              "second layer weight gradient"
   MOE_TRY(moe_dsd(cfg, sv->a, 1, dy_g, 0, topo, g->dw2, stream));
