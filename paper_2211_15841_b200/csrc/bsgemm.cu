@@ -72,9 +72,12 @@ __host__ __device__ constexpr int epi_bufs(int mode, int bn, bool epi_h) {
   return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_NBUF : 2;
 }
 
-template <int MODE, int BN, bool EPI_H>
+// OCC = CTAs per SM: 2 for the router's forward GEMM (its 128-row tiles are
+// ~1.7 waves on one CTA per SM; two resident CTAs per SM take them in one
+// wave), 1 elsewhere. OCC 2 halves the shared memory and uses 4 epilogue warps.
+template <int MODE, int BN, bool EPI_H, int OCC = 1>
 struct Cfg {
-  static constexpr int EPW = epi_warps(MODE, BN, EPI_H);
+  static constexpr int EPW = OCC == 2 ? 4 : epi_warps(MODE, BN, EPI_H);
   static constexpr int NP = MOE_GEMM_NP;           // TMA producer warps (stage s is issued by warp s % NP)
   static_assert(NP >= 1, "at least one producer warp");
   static constexpr int MMA_WARP = NP;
@@ -88,7 +91,8 @@ struct Cfg {
   // router epilogue exchange (+ the tile's expert histogram, E <= 256)
   static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 + 256 * 4 : 0;
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
+  static constexpr int SMEM_CTA = OCC == 2 ? 113 * 1024 : SMEM_LIMIT;
+  static constexpr int STAGES_RAW = (SMEM_CTA - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
   static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES + XCH;
@@ -250,13 +254,13 @@ __device__ __forceinline__ void issue_stage(const CUtensorMap* ta, const CUtenso
 #undef tma_load_2d
 #undef tma_load_3d
 
-template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
-__global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
+template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H, int OCC>
+__global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
     bsgemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
                   const __grid_constant__ CUtensorMap tmap_e, const __grid_constant__ CUtensorMap tmap_f,
                   const GemmParams p) {
-  using C = Cfg<MODE, BN, EPI_H>;
+  using C = Cfg<MODE, BN, EPI_H, OCC>;
   constexpr int STAGES = C::STAGES;
   constexpr int EPW = C::EPW;
   constexpr int NG = EPW / 4;  // epilogue warps per TMEM lane quarter
@@ -823,9 +827,9 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             xr[2 + kMaxRouterTopK + j] = __int_as_float(be[j]);
           }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+        if (NG > 1) asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
         if (grp == 0) {
-          const float m1 = xr[0], s1 = xr[1];
+          const float m1 = NG > 1 ? xr[0] : -FLT_MAX, s1 = NG > 1 ? xr[1] : 0.f;
           const float M = fmaxf(mx, m1);
           const float S = ssum * __expf(mx - M) + s1 * __expf(m1 - M);
           // merge the two descending lists; on equal values list 0 (lower experts) first
@@ -841,7 +845,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
               for (int u = 0; u < kMaxRouterTopK; ++u) {
                 if (u == i0) { v0 = bv[u]; e0 = be[u]; }
               }
-              if (i1 < kMaxRouterTopK) {
+              if (NG > 1 && i1 < kMaxRouterTopK) {
                 v1 = xr[2 + i1];
                 e1 = __float_as_int(xr[2 + kMaxRouterTopK + i1]);
               }
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H>::THREADS, 1)
             for (int e = ht; e < p.E; e += 128) p.hist_out[(long long)t.u * p.E + e] = s_hist[e];
           }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // xr reused by the next tile
+        if (NG > 1) asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");  // xr reused by the next tile
       } else if (MODE == DENSE) {  // EPI_F32: fp32 partial tile (split-K)
         const int r = t.u * BM + row0 + lane;
         float* dst = p.out_f32 + (long long)t.s * p.split_stride + (long long)r * p.ld_f32 + t.v * BN;
@@ -947,17 +951,17 @@ unsigned long long* gemm_trace_slot() {
   return g_trace + per * g_trace_next++;
 }
 
-template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H>
+template <int MODE, bool A_MN, bool B_MN, int BN, bool EPI_H, int OCC = 1>
 static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
-  using C = Cfg<MODE, BN, EPI_H>;
-  auto kern = bsgemm_kernel<MODE, A_MN, B_MN, BN, EPI_H>;
+  using C = Cfg<MODE, BN, EPI_H, OCC>;
+  auto kern = bsgemm_kernel<MODE, A_MN, B_MN, BN, EPI_H, OCC>;
   {
     static unsigned long long smem_mask = 0;  // per device (the attribute is per device)
     static int smem_set = 0;
     cudaError_t e = set_smem_attr_once(kern, (int)C::SMEM, smem_mask, smem_set);
     if (e != cudaSuccess) return set_error(MOE_ECUDA, "%s: smem attribute: %s", L.name, cudaGetErrorString(e));
   }
-  int grid = gemm_sm_budget();
+  int grid = OCC * gemm_sm_budget();
   if (L.max_tiles < grid) grid = L.max_tiles;
   if (grid < 1) grid = 1;
   GemmParams p = L.p;
@@ -990,6 +994,15 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
   return MOE_OK;
 }
 
+static int router_occ() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_ROUTER_OCC");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
 #define MOE_GEMM_CASE(MODE, AMN, BMN, BN, H)                                                     \
   if (L.mode == MODE && L.a_mn == AMN && L.b_mn == BMN && L.bn == BN && L.epi_h == H)          \
     return launch_t<MODE, AMN, BMN, BN, H>(L, stream);
@@ -1018,7 +1031,12 @@ moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream) {
   MOE_GEMM_CASE(DDS_ROW, false, false, 128, false)
   MOE_GEMM_CASE(DDS_ROW, true, false, 128, false)
   // router
-  MOE_GEMM_CASE(DENSE, false, true, 64, false)     // logits = x . Wr (+top-k epilogue)
+  // logits = x . Wr (+top-k epilogue): two CTAs per SM (MOE_ROUTER_OCC=1: one)
+  if (L.mode == DENSE && !L.a_mn && L.b_mn && !L.epi_h && L.p.epi == EPI_ROUTER && router_occ() == 2) {
+    if (L.bn == 64) return launch_t<DENSE, false, true, 64, false, 2>(L, stream);
+    if (L.bn == 128) return launch_t<DENSE, false, true, 128, false, 2>(L, stream);
+  }
+  MOE_GEMM_CASE(DENSE, false, true, 64, false)
   MOE_GEMM_CASE(DENSE, false, true, 128, false)
   MOE_GEMM_CASE(DENSE, false, true, 256, false)
   MOE_GEMM_CASE(DENSE, true, true, 64, false)      // dWr partials = x^T . dlogits

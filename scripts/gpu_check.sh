@@ -21,8 +21,14 @@ for s in $STEPS; do
         python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_list_$TAG.log 2>&1
       echo "ncu_list_exit=$?" ;;
     full)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:bsgemm -s 27 -c 9 \
+      # the 8 tcgen05 GEMM launches of the third eager warm-up step
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:bsgemm -s 16 -c 8 \
         -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$TAG.log 2>&1
       echo "ncu_full_exit=$?" ;;
+    perm)
+      # topology, padded gather and scatter backward of the third warm-up step
+      timeout 900 ncu --set full --clock-control none -k "regex:topo|scatter" -s 6 -c 3 \
+        -o gpurun_out/prof_perm_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_perm_$TAG.log 2>&1
+      echo "ncu_perm_exit=$?" ;;
   esac
 done

@@ -17,7 +17,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = {  # bsgemm template -> step name (launch order within one layer step)
-    "bsgemm_kernel<5, 0, 1, 64": "router", "bsgemm_kernel<0, 0, 1, 256, 0": "sdd",
+    "bsgemm_kernel<5, 0, 1, 64": "router", "bsgemm_kernel<0, 0, 1, 256, 0": "sdd", "bsgemm2_kernel<0, 0, 1": "sdd",
     "bsgemm_kernel<1, 0, 1, 256": "dsd+scatter", "bsgemm_kernel<0, 0, 0, 256, 1": "sddT",
     "bsgemm2_kernel<2, 1, 1": "dsTd", "bsgemm2_kernel<3, 1, 1": "ddTs",
     "bsgemm_kernel<5, 1, 1, 64": "router_dwr", "bsgemm_kernel<5, 0, 0, 128": "router_dx",
@@ -47,7 +47,13 @@ def launches(tag, label):
     # the last complete step: the library kernels after the last router launch
     starts = [i for i, r in enumerate(rows) if "bsgemm_kernel<(int)5, (bool)0, (bool)1, (int)64" in r["Kernel Name"]
               or "bsgemm_kernel<5, 0, 1, 64" in r["Kernel Name"]]
-    step = rows[starts[-1]:] if starts else rows
+    if len(starts) > 1:  # a complete step: from the second-to-last router launch to the last
+        step = rows[starts[-2]:starts[-1]]
+        starts = []
+    else:
+        step = None
+    if step is None:
+        step = rows[starts[-1]:] if starts else rows
     shutil.copy(src, os.path.join(ROOT, "profiles", f"{label}_launches.csv"))
     tot = sum(float(r["Metric Value"]) for r in step)
     out = [f"# {label} — ncu launch list of one C1 step (gpu__time_duration.sum, --clock-control none)", "",
@@ -80,8 +86,9 @@ def gemm_full(tag, label):
            "-k regex:bsgemm). Per-launch times are cold-cache, serialised, under ncu: compare shares, not absolutes.",
            "", "| step | kernel | ncu us | DRAM read MB | DRAM write MB | DRAM % peak | tensor pipe % | L2 % | issue % | regs |",
            "|---|---|---|---|---|---|---|---|---|---|"]
+    import datetime
     traffic = {"source": f"profiles/{label}_gemm_ncu_full.md (ncu --set full, dram__bytes_read.sum + "
-                         "dram__bytes_write.sum per launch, bytes)"}
+                         f"dram__bytes_write.sum per launch, bytes; captured {datetime.date.today().isoformat()})"}
     for d in data:
         k = d[ix["Kernel Name"]]
         nm = step_name(k)

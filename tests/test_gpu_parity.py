@@ -179,7 +179,8 @@ def test_topology_deterministic_repeat():
     Tp, nnz = t1.sizes()
     assert (Tp, nnz) == t2.sizes()
     valid = {"row_offsets": Tp // 128 + 1, "col_indices": nnz, "row_indices": nnz, "t_block_offsets": nnz,
-             "t_row_indices": nnz, "row_src": Tp}   # contents beyond the device-side sizes are unspecified (moe.h)
+             "t_row_indices": nnz, "row_src": Tp, "brow_start": Tp // 128, "brow_rows": Tp // 128}
+    # (contents beyond the device-side sizes are unspecified, moe.h)
     for name in t1.t:
         n = valid.get(name, t1[name].numel())
         assert torch.equal(t1[name][:n], t2[name][:n]), name
