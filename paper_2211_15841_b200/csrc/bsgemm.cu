@@ -72,9 +72,10 @@ __host__ __device__ constexpr int epi_bufs(int mode, int bn, bool epi_h) {
   return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_NBUF : 2;
 }
 
-// OCC = CTAs per SM: 2 for the router's forward GEMM (its 128-row tiles are
-// ~1.7 waves on one CTA per SM; two resident CTAs per SM take them in one
-// wave), 1 elsewhere. OCC 2 halves the shared memory and uses 4 epilogue warps.
+// OCC = CTAs per SM: 1, or 2 for the router's forward GEMM under
+// MOE_ROUTER_OCC=2 (its 128-row tiles are ~1.7 waves on one CTA per SM; two
+// resident CTAs per SM take them in one wave, but with half the shared memory
+// and 4 epilogue warps it measured slower). OCC 2 uses 4 epilogue warps.
 template <int MODE, int BN, bool EPI_H, int OCC = 1>
 struct Cfg {
   static constexpr int EPW = OCC == 2 ? 4 : epi_warps(MODE, BN, EPI_H);
@@ -997,8 +998,8 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
 static int router_occ() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("MOE_ROUTER_OCC");
-    v = (e && e[0] == '1') ? 1 : 2;
+    const char* e = getenv("MOE_ROUTER_OCC");  // 2: two CTAs per SM (measured slower: 21.3 vs 18.7 us at
+    v = (e && e[0] == '2') ? 2 : 1;             // MoE-XS, 4 epilogue warps with register spills); default 1
   }
   return v;
 }
@@ -1031,7 +1032,7 @@ moe_status gemm_launch(const GemmLaunch& L, cudaStream_t stream) {
   MOE_GEMM_CASE(DDS_ROW, false, false, 128, false)
   MOE_GEMM_CASE(DDS_ROW, true, false, 128, false)
   // router
-  // logits = x . Wr (+top-k epilogue): two CTAs per SM (MOE_ROUTER_OCC=1: one)
+  // logits = x . Wr (+top-k epilogue); MOE_ROUTER_OCC=2: two CTAs per SM (experiment)
   if (L.mode == DENSE && !L.a_mn && L.b_mn && !L.epi_h && L.p.epi == EPI_ROUTER && router_occ() == 2) {
     if (L.bn == 64) return launch_t<DENSE, false, true, 64, false, 2>(L, stream);
     if (L.bn == 128) return launch_t<DENSE, false, true, 128, false, 2>(L, stream);
