@@ -187,8 +187,9 @@ class Step:
         L = lib
         wsl = t["ws_layout"]
         self.calls = [
-            ("router", L.moe_router, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx), d(sv.gates), ws, s)),
-            ("topology", L.moe_topology_from_router, (c, d(sv.expert_idx), topo, ws, s)),
+            # router + top-k + topology: one launch where possible (layer.cu: moe_router_topology)
+            ("router+topology", L.moe_router_topology, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
+                                                        d(sv.gates), topo, ws, s)),
         ]
         gfused = bool(L.moe_gather_is_fused(c))   # layer.cu: the padded gather inside the SDD / DD^TS loads
         unp = bool(cfg.unpadded)                  # layer.cu: no pad rows, partial blocks at the fringe
@@ -472,6 +473,7 @@ def kernel_roofline(name, wm, dur_s, peaks, prod_names, byte_names):
     latency-bound: a tiny frac is expected)."""
     T, h, E, R = wm["T"], wm["h"], wm["E"], wm["R"]
     extra = {"router": 2 * T * h + 4 * T * E + 8 * R + 2 * h * E,
+             "router+topology": 2 * T * h + 4 * T * E + 8 * R + 2 * h * E + 12 * R + 12 * wm["nnz"],
              "router_dwr": 2 * T * h + 2 * T * E + 4 * h * E,
              "topology": 12 * R + 12 * wm["nnz"]}
     out = {}

@@ -179,6 +179,14 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
  * epilogue already wrote per-128-token expert histograms into ws, so the
  * whole topology is one launch ("custom CUDA kernel"); otherwise it is
  * moe_topology. Same outputs, bit for bit. */
+/* moe_router followed by the topology (Fig. 5 lines 1-2) in ONE
+ * launch where possible: on the tensor-core router path with top_k <= 2 the
+ * router kernel is launched cooperatively and, after a grid barrier, builds
+ * the whole topology from its per-tile histograms. Otherwise
+ * moe_router + moe_topology_from_router. Outputs identical to moe_router then
+ * moe_topology, bit for bit. ws: moe_workspace_bytes, required. */
+moe_status moe_router_topology(const moe_config* cfg, const void* x, const void* wr, float* logits,
+                               int32_t* expert_idx, float* gates, const moe_topology_t* topo, void* ws, void* stream);
 moe_status moe_topology_from_router(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
                                     void* ws, void* stream);
 moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,

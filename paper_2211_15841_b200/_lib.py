@@ -78,6 +78,7 @@ SIGNATURES = {
     "moe_topk": (STATUS, [CFG, P, P, P, P]),
     "moe_topology": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_topology_from_router": (STATUS, [CFG, P, TOPO, P, P]),
+    "moe_router_topology": (STATUS, [CFG, P, P, P, P, P, TOPO, P, P]),
     "moe_gather": (STATUS, [CFG, P, TOPO, P, P]),
     "moe_scatter": (STATUS, [CFG, P, TOPO, P, P, P]),
     "moe_scatter_bwd": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),

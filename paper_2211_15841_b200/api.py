@@ -142,6 +142,21 @@ def moe_topology(cfg, expert_idx, topo: Topology | None = None, ws=None) -> Topo
     return topo
 
 
+def moe_router_topology(cfg, x, wr, ws=None, topo: Topology | None = None):
+    """moe_router_topology (include/moe.h): router, top-k and topology, one
+    launch where possible. Returns (logits, expert_idx, gates, topology)."""
+    T, E, k = cfg.tokens, cfg.num_experts, cfg.top_k
+    dev = x.device
+    logits = torch.empty(T, E, dtype=torch.float32, device=dev)
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    gates = torch.empty(T, k, dtype=torch.float32, device=dev)
+    ws = ws if ws is not None else workspace(cfg, dev)
+    topo = topo if topo is not None else Topology(cfg, dev)
+    check("moe_router_topology", lib.moe_router_topology(ctypes.byref(cfg), _p(x), _p(wr), _p(logits), _p(idx),
+                                                         _p(gates), ctypes.byref(topo.struct), _p(ws), _stream()))
+    return logits, idx, gates, topo
+
+
 def moe_topology_from_router(cfg, expert_idx, ws, topo: Topology | None = None) -> Topology:
     """moe_topology_from_router (include/moe.h): the topology from the per-tile
     histograms moe_router(cfg, ..., ws) left in ws (tensor-core router), else moe_topology."""

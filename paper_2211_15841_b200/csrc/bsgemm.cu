@@ -37,8 +37,11 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "bsgemm.cuh"
 #include "gemm_util.cuh"
+#include "topo_body.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tma.cuh"
@@ -907,6 +910,25 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
     if (lane == 0) bulk_wait<0>();
   }
 
+  if (MODE == DENSE && p.topo_fused) {
+    // router + top-k + topology in one launch ("custom CUDA kernel"): every
+    // CTA's expert ids and tile histograms are in global memory after the grid
+    // barrier; the operand ring (idle now) is the topology's scratch
+    __syncthreads();
+    cooperative_groups::this_grid().sync();
+    const int k = p.topk, row_chunk = 128 * k;
+    const int rows_per_cta = (int)blockDim.x / row_chunk;
+    const int n_rows = p.m_tiles;
+    TopoTask tk;
+    tk.rank_first = blockIdx.x;
+    tk.rank_stride = gridDim.x;
+    tk.emit_first = blockIdx.x;
+    tk.emit_stride = gridDim.x;
+    tk.publish = blockIdx.x == 0;
+    topo_scan_emit_body(p.idx, p.rows_valid * k, p.E, p.topo_bs, p.topo_F, (n_rows + rows_per_cta - 1) / rows_per_cta,
+                        p.hist_out, p.topo, p.topo_capacity, n_rows, row_chunk, rows_per_cta, tk,
+                        reinterpret_cast<int32_t*>(smem));
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == C::MMA_WARP) {
@@ -989,7 +1011,22 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
     }
     if ((rev >> MODE) & 1) p.reverse = 1;
   }
-  cudaError_t le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
+  cudaError_t le;
+  if (MODE == DENSE && p.topo_fused) {  // grid barrier inside: cooperative launch (all CTAs co-resident)
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(C::THREADS);
+    lc.dynamicSmemBytes = C::SMEM;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    le = cudaLaunchKernelEx(&lc, kern, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
+  } else {
+    le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
+  }
   if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
   MOE_CHECK_LAUNCH(L.name);
   return MOE_OK;

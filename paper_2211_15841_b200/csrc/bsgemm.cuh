@@ -55,6 +55,10 @@ struct GemmParams {
   int E, topk;
   int renorm;  // gates divided by the sum of the token's k gates
   int32_t* hist_out;  // optional: per-tile expert histogram [m_tiles][E] of the selected experts (topology input)
+  // EPI_ROUTER with topo_fused: after a grid barrier (cooperative launch) every CTA
+  // builds the topology from hist_out (topo_body.cuh): router + top-k + topology in one launch
+  int topo_fused, topo_bs, topo_F, topo_capacity;
+  moe_topology_t topo;
   // EPI_F32
   float* out_f32;
   long long ld_f32, split_stride;

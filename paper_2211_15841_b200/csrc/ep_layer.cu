@@ -270,9 +270,8 @@ moe_status moe_ep_forward(moe_ep* ep, int64_t tokens, const moe_weights* w, cons
   const moe_config* ce = &ep->cfg_e;
   const bool id = ep->d.act == MOE_ACT_IDENTITY;
   // token owner: (1) router + top-k [+ aux loss], (2) topology over the global experts
-  MOE_TRY(moe_router(&cl, x, w->wr, ep->logits, ep->idx, ep->gates, ep->ws_l, stream));
+  MOE_TRY(moe_router_topology(&cl, x, w->wr, ep->logits, ep->idx, ep->gates, &ep->topo_l, ep->ws_l, stream));
   if (cl.aux_loss_coeff > 0.f) MOE_TRY(moe_load_balance_loss(&cl, ep->logits, ep->idx, ep->ws_l, stream));
-  MOE_TRY(moe_topology_from_router(&cl, ep->idx, &ep->topo_l, ep->ws_l, stream));
   // count exchange + dispatch into the owners' padded expert-grouped layouts
   MOE_TRY(moe_ep_exchange_counts(&ep->ex, ep->topo_l.counts, stream));
   MOE_TRY(moe_ep_dispatch_padded(&ep->ex, MOE_EP_RECV_X, x, ep->topo_l.sorted_pos, (int)cl.top_k, stream));

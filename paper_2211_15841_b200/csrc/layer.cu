@@ -70,12 +70,11 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   const bool id = cfg->act == MOE_ACT_IDENTITY;
   MOE_CHECK_ARG(id || sv->act_deriv, "moe_forward: saved->act_deriv required for a non-identity activation");
   // (1) indices, weights = router(x)
-  MOE_TRY(moe_router(cfg, x, w->wr, sv->logits, sv->expert_idx, sv->gates, ws, stream));
+  // (2) topology = make_topology(indices)                  P:265, P:299
+  //     (one launch with the router where possible: moe_router_topology)
+  MOE_TRY(moe_router_topology(cfg, x, w->wr, sv->logits, sv->expert_idx, sv->gates, &sv->topo, ws, stream));
   //     + the auxiliary load-balancing loss into the workspace
   if (cfg->aux_loss_coeff > 0.f) MOE_TRY(moe_load_balance_loss(cfg, sv->logits, sv->expert_idx, ws, stream));
-  // (2) topology = make_topology(indices)                  P:265, P:299
-  //     (tensor-core router: from the per-tile histograms its epilogue wrote)
-  MOE_TRY(moe_topology_from_router(cfg, sv->expert_idx, &sv->topo, ws, stream));
   // (3) x = padded_gather(x, indices)
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
   if (cfg->unpadded) {  // P:297 partial blocks at the fringe: X_g rows in expert order, no pad rows

@@ -335,44 +335,78 @@ moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_
   return MOE_OK;
 }
 
+// logits = x . Wr on tcgen05 (M = tokens, N = E, K = h) with the greedy top-k
+// + softmax gate epilogue fused (one thread per token row); with topo, the
+// topology is built in the same (cooperative) launch.
+static moe_status router_tc_launch(const moe_config* cfg, const void* x, const void* wr, float* logits,
+                                   int32_t* expert_idx, float* gates, void* ws, const moe_topology_t* topo,
+                                   void* stream) {
+  const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
+  GemmLaunch L{};
+  L.name = topo ? "moe_router_topology" : "moe_router";
+  L.mode = DENSE;
+  L.bn = E;
+  L.a_mn = false;
+  L.b_mn = true;
+  L.p.m_tiles = (int)ceil_div(T, 128);
+  L.p.n_tiles = 1;
+  L.p.splits = 1;
+  L.p.k_iters_total = L.p.kiters_split = (int)ceil_div(h, BK);
+  L.p.epi = EPI_ROUTER;
+  L.p.rows_valid = T;
+  L.p.logits = logits;
+  L.p.idx = expert_idx;
+  L.p.gates = gates;
+  L.p.E = E;
+  L.p.topk = (int)cfg->top_k;
+  L.p.renorm = cfg->renormalize;
+  // per-tile expert histograms for the topology (moe_topology_from_router, or fused below)
+  L.p.hist_out = ws ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + ws_layout(cfg).router_hist) : nullptr;
+  if (topo) {
+    L.p.topo_fused = 1;
+    L.p.topo = *topo;
+    L.p.topo_bs = (int)cfg->block_size;
+    L.p.topo_F = (int)(cfg->ffn_hidden / cfg->block_size);
+    L.p.topo_capacity = (int)cfg->capacity;
+  }
+  L.max_tiles = L.p.m_tiles;
+  MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, BK, 128, "moe_router x", KSW));
+  MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
+  MOE_TRY(make_tmap_f32(&L.tc, logits, E, T, E, "moe_router logits"));
+  L.td = L.tc;
+  return gemm_launch(L, as_stream(stream));
+}
+
 moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, float* logits, int32_t* expert_idx,
                       float* gates, void* ws, void* stream) {
   MOE_TRY(moe_check_config(cfg));
   MOE_CHECK_ARG(x && wr && logits && expert_idx && gates, "moe_router: NULL pointer");
   const int T = (int)cfg->tokens, h = (int)cfg->hidden, E = (int)cfg->num_experts;
-  if (router_on_tensor_cores(cfg)) {
-    // logits = x . Wr on tcgen05 (M = tokens, N = E, K = h) with the greedy
-    // top-k + softmax gate epilogue fused (one thread per token row)
-    GemmLaunch L{};
-    L.name = "moe_router";
-    L.mode = DENSE;
-    L.bn = E;
-    L.a_mn = false;
-    L.b_mn = true;
-    L.p.m_tiles = (int)ceil_div(T, 128);
-    L.p.n_tiles = 1;
-    L.p.splits = 1;
-    L.p.k_iters_total = L.p.kiters_split = (int)ceil_div(h, BK);
-    L.p.epi = EPI_ROUTER;
-    L.p.rows_valid = T;
-    L.p.logits = logits;
-    L.p.idx = expert_idx;
-    L.p.gates = gates;
-    L.p.E = E;
-    L.p.topk = (int)cfg->top_k;
-    L.p.renorm = cfg->renormalize;
-    // per-tile expert histograms for the topology (moe_forward: topology_from_hist)
-    L.p.hist_out = ws ? reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + ws_layout(cfg).router_hist) : nullptr;
-    L.max_tiles = L.p.m_tiles;
-    MOE_TRY(make_tmap_bf16(&L.ta, x, h, T, h, BK, 128, "moe_router x", KSW));
-    MOE_TRY(make_tmap_bf16_mn(&L.tb, wr, E, h, E, L.bn / 64, "moe_router wr"));
-    MOE_TRY(make_tmap_f32(&L.tc, logits, E, T, E, "moe_router logits"));
-    L.td = L.tc;
-    return gemm_launch(L, as_stream(stream));
-  }
+  if (router_on_tensor_cores(cfg)) return router_tc_launch(cfg, x, wr, logits, expert_idx, gates, ws, nullptr, stream);
   dim3 grid((unsigned)ceil_div(T, RT_TOK), (unsigned)ceil_div(E, RT_EXP));
   MOE_LAUNCH("router_logits", router_logits_kernel, dim3(grid), dim3(256), 0, as_stream(stream), reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(wr), logits, T, h, E);
   return moe_topk(cfg, logits, expert_idx, gates, stream);
+}
+
+// Whether moe_router_topology builds the topology inside the router launch
+// (MOE_ROUTER_TOPO_FUSED=1, read per call; default off): the tensor-core
+// router, 128*k assignments per router tile within one CTA's threads (k <= 2).
+// Measured at MoE-XS: 36.0 us fused against 28.7 us for the router plus the
+// one-launch topology (the grid barrier and every CTA rescanning the
+// histograms cost more than the launch they save).
+static bool router_topo_fusable(const moe_config* cfg) {
+  const char* e = getenv("MOE_ROUTER_TOPO_FUSED");
+  return e && e[0] == '1' && router_on_tensor_cores(cfg) && cfg->top_k <= 2;
+}
+
+moe_status moe_router_topology(const moe_config* cfg, const void* x, const void* wr, float* logits,
+                               int32_t* expert_idx, float* gates, const moe_topology_t* topo, void* ws, void* stream) {
+  MOE_TRY(moe_check_config(cfg));
+  MOE_TRY(check_topo(topo));
+  MOE_CHECK_ARG(x && wr && logits && expert_idx && gates && ws, "moe_router_topology: NULL pointer");
+  if (router_topo_fusable(cfg)) return router_tc_launch(cfg, x, wr, logits, expert_idx, gates, ws, topo, stream);
+  MOE_TRY(moe_router(cfg, x, wr, logits, expert_idx, gates, ws, stream));
+  return moe_topology_from_router(cfg, expert_idx, topo, ws, stream);
 }
 
 moe_status moe_router_bwd(const moe_config* cfg, const void* x, const void* wr, const float* logits,

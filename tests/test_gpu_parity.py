@@ -1153,3 +1153,40 @@ def test_topology_from_router_histograms(T, E, k, h):
     ridx, _ = resolved_routing(L, logit_error_bound(x64, wr64), idx.cpu().numpy(), want_idx)
     plan, tt = oracle_plan_topo(ridx, E, 256)
     check_topology_exact(A, topo, plan, tt, T * k)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("T,E,k,h,cap", [(32768, 64, 1, 512, 0), (1000, 64, 2, 256, 0), (129, 256, 1, 256, 0),
+                                         (5000, 128, 2, 768, 0), (4096, 64, 1, 256, 80), (40000, 64, 1, 512, 0)])
+def test_router_topology_one_launch(T, E, k, h, cap, fused, monkeypatch):
+    """moe_router_topology: the tcgen05 router launched cooperatively builds the
+    whole topology after a grid barrier; every array bit-exact against
+    the oracle's plan of the oracle's routing (near-ties resolved the GPU's way,
+    R6), also with a capacity (keep-earliest) and more router tiles than SMs."""
+    d = dev()
+    A = api()
+    g = torch.Generator().manual_seed(T + E + k + cap)
+    x = torch.randn(T, h, generator=g).to(torch.bfloat16)
+    wr = (torch.randn(h, E, generator=g) / h ** 0.5).to(torch.bfloat16)
+    cfg = A.make_config(T, h, E, k, 256, capacity=cap)
+    monkeypatch.setenv("MOE_ROUTER_TOPO_FUSED", fused)   # 1: the cooperative one-launch form
+    logits, idx, gates, topo = A.moe_router_topology(cfg, x.to(d), wr.to(d))
+    torch.cuda.synchronize()
+    x64, wr64 = S.to_f64(x), S.to_f64(wr)
+    L = O.router_logits(x64, wr64)
+    want_idx, _ = O.topk(L, k)
+    ridx, _ = resolved_routing(L, logit_error_bound(x64, wr64), idx.cpu().numpy(), want_idx)
+    if cap:
+        plan = O.make_plan(ridx, E, 128, capacity=cap)
+        tt = O.make_topology_closed_form(plan, 128, 256)
+        Tp, nnz = topo.sizes()
+        assert Tp == plan.Tp and nnz == tt.nnz
+        gg = {n: v.cpu().numpy() for n, v in topo.t.items()}
+        np.testing.assert_array_equal(gg["counts"], plan.counts)
+        np.testing.assert_array_equal(gg["pos"][:T * k], plan.pos)
+        np.testing.assert_array_equal(gg["sorted_idx"][:plan.sorted_idx.size], plan.sorted_idx)
+        np.testing.assert_array_equal(gg["col_indices"][:nnz], tt.col_indices)
+        np.testing.assert_array_equal(gg["t_block_offsets"][:nnz], tt.t_block_offsets)
+    else:
+        plan, tt = oracle_plan_topo(ridx, E, 256)
+        check_topology_exact(A, topo, plan, tt, T * k)
