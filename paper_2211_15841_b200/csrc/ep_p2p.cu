@@ -119,9 +119,13 @@ __device__ inline uint8_t* peer_win(const EpArgs& a, int q) { return reinterpret
 // CTA completing the count bumps arrive[region][rank] at every destination.
 __device__ void signal_peers(const EpArgs& a, int region) {
   __shared__ bool s_last;
-  __threadfence_system();  // every thread: its peer stores before the CTA's completion
+  // the CTA's peer stores happen before thread 0's system-scope release fence
+  // (bar.sync orders them at CTA scope; the release is cumulative over them):
+  // one fence per CTA, not per thread (a per-thread fence.sc.sys made the copy
+  // kernels membar-stall bound: 25-28 us for 37 MB at one rank)
   __syncthreads();
   if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     const WinLayout L = win_layout(a.P, a.E, a.h, a.cap, a.owner);
     uint32_t* done = reinterpret_cast<uint32_t*>(peer_win(a, a.rank) + L.done) + region;
     const uint32_t prev = atomicAdd(done, 1u);
@@ -274,7 +278,10 @@ EpArgs ep_args(const moe_ep_t* ep) {
   return a;
 }
 
-constexpr int kRowsPerWarp = 4;  // rows in flight per warp (all loads, then all stores)
+#ifndef MOE_EP_ROWS_PER_WARP
+#define MOE_EP_ROWS_PER_WARP 4
+#endif
+constexpr int kRowsPerWarp = MOE_EP_ROWS_PER_WARP;  // rows in flight per warp (all loads, then all stores)
 
 // Padded exchange. Dispatch: sorted position u of this rank's expert order
 // belongs to global expert e (my_start) and lands in the owner's padded layout

@@ -66,10 +66,18 @@ class EpLayer:
             err = f"init: {exc}"
         handles = [None] * self.P
         dist.all_gather_object(handles, handle, group=group)
+        uuids = [None] * self.P              # explicit peer-access check (NVLink / PCIe P2P) before mapping
+        dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(self.device).uuid), group=group)
         if err is None:
             try:
                 if any(hq is None for hq in handles):
                     raise RuntimeError("a rank has no window")
+                mine = self.device.index if self.device.index is not None else torch.cuda.current_device()
+                local = {str(torch.cuda.get_device_properties(j).uuid): j for j in range(torch.cuda.device_count())}
+                for q, u in enumerate(uuids):
+                    j = local.get(u)
+                    if j is not None and j != mine and not torch.cuda.can_device_access_peer(mine, j):
+                        raise RuntimeError(f"GPU {mine} cannot access rank {q}'s GPU {j} (cudaDeviceCanAccessPeer)")
                 buf = (ctypes.c_char * (64 * self.P)).from_buffer_copy(b"".join(handles))
                 check("moe_ep_connect", lib.moe_ep_connect(self.h_ep, buf))
             except Exception as exc:  # noqa: BLE001
