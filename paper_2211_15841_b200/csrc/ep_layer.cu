@@ -164,8 +164,14 @@ moe_status moe_ep_init(moe_ep** out, const moe_ep_desc* d, int device) {
   const int64_t cap = d->recv_rows_cap > 0 ? d->recv_rows_cap : full;
   MOE_CHECK_ARG(cap <= full, "moe_ep_init: recv_rows_cap=%lld above nranks*max_tokens*top_k=%lld",
                 (long long)cap, (long long)full);
+  int prev_device = 0;
+  cudaGetDevice(&prev_device);
   cudaError_t ce = cudaSetDevice(device);
   if (ce != cudaSuccess) return set_error(MOE_ECUDA, "moe_ep_init: cudaSetDevice(%d): %s", device, cudaGetErrorString(ce));
+  struct RestoreDevice {  // the caller's current device is left as it was
+    int d;
+    ~RestoreDevice() { cudaSetDevice(d); }
+  } restore{prev_device};
 
   moe_ep* ep = new moe_ep();
   ep->d = *d;
@@ -387,10 +393,13 @@ moe_status moe_ep_exchange_desc(const moe_ep* ep, moe_ep_t* out) {
 
 moe_status moe_ep_destroy(moe_ep* ep) {
   if (!ep) return MOE_OK;
+  int prev_device = 0;
+  cudaGetDevice(&prev_device);
   cudaSetDevice(ep->device);
   cudaDeviceSynchronize();
   ep_free_all(ep);
   delete ep;
+  cudaSetDevice(prev_device);
   return MOE_OK;
 }
 
