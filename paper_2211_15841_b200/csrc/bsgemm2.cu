@@ -50,14 +50,20 @@ constexpr int P_A_BYTES = A_BYTES;             // 128 x 64
 constexpr int P_B_BYTES = P_BH * BK * 2;       // 128 x 64
 constexpr int P_STAGE = P_A_BYTES + P_B_BYTES;
 
+#ifndef MOE_PAIR_NBUF
+#define MOE_PAIR_NBUF 2
+#endif
+constexpr int P_NBUF = MOE_PAIR_NBUF;                          // staging buffers per epilogue warp
+constexpr int P_EPI_BYTES = NUM_EPI_WARPS * P_NBUF * EPI_BUF;
+
 template <bool EPI_H>
 struct Cfg2 {
   static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
   static constexpr int TOK = 4 * 16 * 16;  // DDS_COL gather: token ring, 4 K-steps x 16 lanes x int4
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - EPI_BYTES - H_BYTES - TOK) / P_STAGE;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK) / P_STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * P_BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + EPI_BYTES + H_BYTES + TOK;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + P_EPI_BYTES + H_BYTES + TOK;
 };
 
 struct Tile2 {
@@ -154,7 +160,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem_a + STAGES * P_A_BYTES;
   uint8_t* smem_epi = smem_b + STAGES * P_B_BYTES;
-  uint8_t* smem_h = smem_epi + EPI_BYTES;
+  uint8_t* smem_h = smem_epi + P_EPI_BYTES;
   int4* tokring = reinterpret_cast<int4*>(smem_h + C::H_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES + C::TOK);
   uint64_t* empty = full + STAGES;
@@ -390,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const int half = wq >> 2;                  // this warp's first chunk; it takes every EPG-th
     constexpr int EPG = NUM_EPI_WARPS / 4;     // epilogue warps per TMEM lane quarter
     const int row0 = q * 32;
-    uint8_t* stg = smem_epi + wq * 2 * EPI_BUF;
+    uint8_t* stg = smem_epi + wq * P_NBUF * EPI_BUF;
     uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
     uint64_t* hb = hbar + wq * 2;
     uint32_t hphase[2] = {0, 0};
@@ -400,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     uint32_t acc_phase = 0;
 
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
-      if (lane == 0) bulk_wait_read<1>();
+      if (lane == 0) bulk_wait_read<P_NBUF - 1>();
       __syncwarp();
       stage_row(stg + sbuf * EPI_BUF, lane, v);
       fence_proxy_async_smem();
@@ -409,7 +415,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
         bulk_commit();
       }
-      sbuf ^= 1;
+      sbuf = sbuf + 1 == P_NBUF ? 0 : sbuf + 1;
     };
     auto load_h = [&](const Tile2& t, int c, int b) {
       if (lane == 0) {
