@@ -1133,6 +1133,17 @@ static bool use_pair_rows() {
 
 // 2-SM (cta_group::2) 256 x 256 tiles: needs even F and h % 256 == 0.
 // MOE_GEMM_PAIR=0 in the environment selects the 1-SM kernels (A/B testing).
+// The CTA-pair forward SDD's epilogue stores 4 KB boxes (64 x 32, 128 B
+// swizzle; 111 -> 104 us at MoE-XS); MOE_PAIR_WIDE=0: 2 KB boxes.
+static bool pair_wide() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_PAIR_WIDE");
+    v = e && e[0] == '0' ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool use_pair(const moe_config* cfg) {
   static int env = -1;
   if (env < 0) {
@@ -1211,17 +1222,17 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   }
   L.epi_h = L.p.epi == EPI_ACT_BWD;
   // Row-pair 2-SM (cta_group::2) tiles: each SM streams half of the expert's
-  // W1 columns, so the forward SDD's operand traffic per output drops to 2/3
-  // (measured 109 -> 101 us at MoE-XS despite the half-empty pairs of odd-row
-  // experts). The SDD^T keeps the 1-SM kernel (its act'(H) prefetch measured
-  // slower on pairs: 99 -> 116 us). MOE_SDD_PAIR=0: 1-SM for both, =1: pairs for both.
-  static int pair_env = -2;
-  if (pair_env == -2) {
-    const char* e = getenv("MOE_SDD_PAIR");
-    pair_env = e ? (e[0] == '1' ? 1 : 0) : -1;
-  }
+  // weight columns, so the operand traffic per output drops to 2/3 (MoE-XS:
+  // SDD 109 -> 101 us, SDD^T 99.3 -> 97.6 with the in-place 4 KB act'(H)
+  // ring) — when the experts average >= 3 block-rows: with fewer, the
+  // half-empty pairs of odd-row experts cost more than the pairs save
+  // (MoE-Medium T=8192: SDD 139.5 us 1-SM vs 143.4 pairs; top-2: SDD 189 vs
+  // 199, SDD^T 191 vs 201). MOE_SDD_PAIR=0: 1-SM for both, =1: pairs for both.
+  const char* pe = getenv("MOE_SDD_PAIR");  // read per call: the tests cover both forms in one process
+  const int pair_env = pe && pe[0] ? (pe[0] == '1' ? 1 : 0) : -1;
   // (the A-row gather inside the loads, moe_sdd_gather, exists only in the 1-SM kernel)
-  const bool pair = use_pair(cfg) && !x_gather && (pair_env == 1 || (pair_env == -1 && !act_src));
+  const bool deep = cfg->tokens * cfg->top_k >= 3LL * cfg->num_experts * BM;
+  const bool pair = use_pair(cfg) && !x_gather && (pair_env == 1 || (pair_env == -1 && deep));
   L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
   if (x_gather) {  // A rows = x[row_src / k] by tile::gather4 (X_g never materialised)
     MOE_TRY(make_tmap_bf16(&L.ta, x_gather, h, cfg->tokens, h, BK, 1, "moe_sdd_gather x", KSW));
@@ -1236,11 +1247,14 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
     MOE_TRY(make_tmap_bf16_mn(&L.tb, b, N, h, N, pair ? 2 : L.bn / 64, "moe_sdd b"));
   else
     MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, pair ? 128 : L.bn, "moe_sdd b^T", KSW));
-  MOE_TRY(make_tmap_epi(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
+  const bool wide = pair && (act_src ? gemm2_wide_h() : pair_wide());
+  L.p.wide = wide ? 1 : 0;
+  auto epi_map = wide ? make_tmap_epi_wide : make_tmap_epi;
+  MOE_TRY(epi_map(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   set_epi_out(L.p, 0, out_s, nnz * 128, 128);
-  if (out_aux) MOE_TRY(make_tmap_epi(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
+  if (out_aux) MOE_TRY(epi_map(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));
   if (out_aux) set_epi_out(L.p, 1, out_aux, nnz * 128, 128);
-  if (act_src) MOE_TRY(make_tmap_epi(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
+  if (act_src) MOE_TRY(epi_map(&L.td, act_src, 128, nnz * 128, 128, "moe_sdd act src"));
   if (!out_aux && !act_src) L.td = L.tc;
   return pair ? gemm2_launch(L, as_stream(stream)) : gemm_launch(L, as_stream(stream));
 }

@@ -76,6 +76,7 @@ struct GemmParams {
   __nv_bfloat16* out_d;
   long long ldc, ldd, rows_c, rows_d;
   int direct;
+  int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)
   unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
   int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
   int dbg;  // experiment knobs (MOE_GEMM_DBG): 1 = no epilogue work, 2 = no MMA, 4 = no activation
@@ -141,6 +142,7 @@ __device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev
 // CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
 // 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);
+bool gemm2_wide_h();  // the CTA-pair SDD^T takes 64 x 32 (4 KB) act'(H) / dH maps
 GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo);
 
 }  // namespace moe

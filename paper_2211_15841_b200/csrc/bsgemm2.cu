@@ -54,11 +54,27 @@ constexpr int P_STAGE = P_A_BYTES + P_B_BYTES;
 #define MOE_PAIR_NBUF 2
 #endif
 constexpr int P_NBUF = MOE_PAIR_NBUF;                          // staging buffers per epilogue warp
-constexpr int P_EPI_BYTES = NUM_EPI_WARPS * P_NBUF * EPI_BUF;
+#ifndef MOE_PAIR_WIDE
+#define MOE_PAIR_WIDE 1
+#endif
+#ifndef MOE_PAIR_NHW
+#define MOE_PAIR_NHW 3
+#endif
 
-template <bool EPI_H>
+template <bool EPI_H, int MODE = -1>
 struct Cfg2 {
-  static constexpr int H_BYTES = EPI_H ? EPI_BYTES : 0;
+  // the forward SDD stores 64-column chunks (4 KB TMA boxes, two staging
+  // buffers of 4 KB per warp: one per output); the others 32-column chunks
+  // (DS^TD / DD^TS measured no faster with 4 KB boxes: 73.8 / 76.6 us vs
+  // 71.4 / 75.5, the larger staging costing two pipeline stages)
+  static constexpr bool WIDE = MOE_PAIR_WIDE && MODE == SDD && !EPI_H;
+  // SDD^T: a per-warp ring of NHW 4 KB act'(H) boxes (64 x 32), each turned
+  // into the dH box in place and stored from the same buffer
+  static constexpr bool WIDE_H = MOE_PAIR_WIDE && EPI_H;
+  static constexpr int NHW = MOE_PAIR_NHW;
+  static constexpr int NHB = WIDE_H ? NHW : 2;  // act'(H) barriers per epilogue warp
+  static constexpr int P_EPI_BYTES = WIDE_H ? 0 : NUM_EPI_WARPS * (WIDE ? 2 * 4096 : P_NBUF * EPI_BUF);
+  static constexpr int H_BYTES = EPI_H ? (WIDE_H ? NUM_EPI_WARPS * NHW * 4096 : EPI_BYTES) : 0;
   static constexpr int TOK = 4 * 16 * 16;  // DDS_COL gather: token ring, 4 K-steps x 16 lanes x int4
   static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK) / P_STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
@@ -152,8 +168,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     bsgemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                    const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_d,
                    const GemmParams p) {
-  using C = Cfg2<EPI_H>;
+  using C = Cfg2<EPI_H, MODE>;
   constexpr int STAGES = C::STAGES;
+  constexpr int P_EPI_BYTES = C::P_EPI_BYTES;
   constexpr int NCHUNK = P_BN / EPI_COLS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -167,7 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* hbar = tempty + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + 2 * NUM_EPI_WARPS);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hbar + C::NHB * NUM_EPI_WARPS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -184,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2 * NUM_EPI_WARPS);
     }
-    for (int i = 0; i < 2 * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
+    for (int i = 0; i < C::NHB * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
@@ -396,9 +413,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const int half = wq >> 2;                  // this warp's first chunk; it takes every EPG-th
     constexpr int EPG = NUM_EPI_WARPS / 4;     // epilogue warps per TMEM lane quarter
     const int row0 = q * 32;
-    uint8_t* stg = smem_epi + wq * P_NBUF * EPI_BUF;
-    uint8_t* hst = smem_h + wq * 2 * EPI_BUF;
-    uint64_t* hb = hbar + wq * 2;
+    uint8_t* stg = smem_epi + wq * (C::WIDE ? 2 * 4096 : P_NBUF * EPI_BUF);
+    uint8_t* hst = smem_h + wq * (C::WIDE_H ? C::NHW * 4096 : 2 * EPI_BUF);
+    uint64_t* hb = hbar + wq * C::NHB;
     uint32_t hphase[2] = {0, 0};
     int hslot = 0;
     int sbuf = 0;
@@ -427,6 +444,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       }
     };
 
+    // SDD^T, wide: this warp's 64-column super-chunks form one sequence j over
+    // its tiles (tile cid + (j / SPW) * ncl, super-chunk half + (j % SPW) * EPG);
+    // the act'(H) box of j + NHW - 1 is loaded while j is processed
+    constexpr int SPW = (P_BN / 64) / EPG;
+    const int hw_end = (ntiles > cid ? (ntiles - 1 - cid) / ncl + 1 : 0) * SPW;
+    int hw_seq = 0;
+    uint32_t hw_phase = 0;  // bit b: parity of slot b's next completion
+    auto load_hw = [&](int j) {  // lane 0
+      if (j >= hw_end) return;
+      const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank);
+      if (!(rank == 0 || tj.second)) return;  // nothing stored for this CTA's half: nothing loaded
+      int x, y;
+      out_coords2(p, MODE, tj, rank, 2 * (half + (j % SPW) * EPG), row0, p.F, x, y);
+      const int b = j % C::NHW;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&hb[b], 4096);
+      tma_load_2d(hst + b * 4096, &tmap_d, &hb[b], x, y);
+    };
+    if (C::WIDE_H && lane == 0)
+      for (int j = 0; j < C::NHW - 1; ++j) load_hw(j);
+
     int tile_i = -1;
     for (int tile = cid; tile < ntiles; tile += ncl) {
       const Tile2 t = decode2(p, MODE, tile, rank);
@@ -435,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       const bool mine = rank == 0 || t.second;  // does this CTA own real output rows?
       // unpadded layout: this lane's row of the CTA's SDD block-row is the fringe: zeros
       const bool fringe = MODE == SDD && p.unpadded && mine && row0 + lane >= __ldg(p.brow_rows + t.r0 + rank);
-      if (EPI_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
+      if (EPI_H && !C::WIDE_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -448,6 +486,105 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tmem_ld32(taddr, r);
           tmem_ld_wait();
           if (r[0] == 0x7fffffffu && r[1] == 0x12345u) p.gates[0] = 1.f;
+        }
+      } else if (C::WIDE_H) {
+        // dH = dA (x) act'(H) per 64-column super-chunk: two 32-column TMEM
+        // loads, the act'(H) box read and overwritten in place, one 4 KB store
+#pragma unroll 1
+        for (int s = 0; s < SPW; ++s, ++hw_seq) {
+          const int b = hw_seq % C::NHW;
+          if (mine) {
+            const int sc = half + s * EPG;
+            mbar_wait(&hb[b], (hw_phase >> b) & 1u);
+            hw_phase ^= 1u << b;
+            uint8_t* slot = hst + b * 4096;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              float v[32];
+              if (has_acc) {
+                uint32_t r[32];
+                tmem_ld32(taddr + (2 * sc + hh) * EPI_COLS, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fringe ? 0.f : __uint_as_float(r[i]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              }
+              float hf[32];
+              load_row_half128(slot, lane, hf, hh);
+              if (p.aux_deriv) {
+                mul32(v, hf);
+              } else {
+                act_grad_mul32(p.act, v, hf);
+              }
+              stage_row_half128(slot, lane, v, hh);  // this lane's row only: in place is safe
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              int x, y;
+              out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
+              tma_store_2d(&tmap_c, slot, x, y);
+              bulk_commit();
+            }
+          }
+          if (lane == 0) {
+            bulk_wait_read<1>();  // the store of step hw_seq - 1 has read its slot: refill it
+            load_hw(hw_seq + C::NHW - 1);
+          }
+          __syncwarp();
+        }
+      } else if (C::WIDE && p.wide && mine) {
+        // 64-column super-chunks C = half, half + EPG (2 per warp per tile),
+        // each two 32-column TMEM loads staged into 128B-swizzled rows, then
+        // one 4 KB TMA store per output (act(H) to tmap_c; the forward SDD's
+        // H or act'(H) to tmap_d)
+        uint8_t* bufc = stg;
+        uint8_t* bufd = stg + 4096;
+        const bool two = p.epi == EPI_ACT_FWD && p.has_pre;
+#pragma unroll 1
+        for (int sc = half; sc < P_BN / 64; sc += EPG) {
+          if (lane == 0) bulk_wait_read<0>();  // the previous super-chunk's stores have read both buffers
+          __syncwarp();
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            float v[32];
+            if (has_acc) {
+              uint32_t r[32];
+              tmem_ld32(taddr + (2 * sc + hh) * EPI_COLS, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fringe ? 0.f : __uint_as_float(r[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (p.epi == EPI_ACT_FWD) {
+              if (p.has_pre && p.aux_deriv) {
+                float g[32];
+                act_fwd_deriv32(p.act, v, g);
+                if (fringe) {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) g[i] = 0.f;
+                }
+                stage_row_half128(bufd, lane, g, hh);
+              } else {
+                if (p.has_pre) stage_row_half128(bufd, lane, v, hh);
+                act_fwd32(p.act, v);
+              }
+            }
+            stage_row_half128(bufc, lane, v, hh);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            int x, y;
+            out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
+            tma_store_2d(&tmap_c, bufc, x, y);
+            if (two) tma_store_2d(&tmap_d, bufd, x, y);
+            bulk_commit();
+          }
         }
       } else if (mine) {
         // chunks c = half, half + EPG, ...; MOE_PAIR_PINGPONG=1 at build time:
@@ -539,7 +676,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 
 template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
 static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
-  using C = Cfg2<EPI_H>;
+  using C = Cfg2<EPI_H, MODE>;
+  if (C::WIDE_H && !L.p.wide)
+    return set_error(MOE_EUNSUPPORTED, "%s: the CTA-pair SDD^T needs 64 x 32 act'(H) / dH maps", L.name);
   auto kern = bsgemm2_kernel<MODE, A_MN, B_MN, EPI_H>;
   {
     static unsigned long long smem_mask = 0;  // per device (the attribute is per device)
@@ -561,6 +700,8 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
 
 #define MOE_GEMM2_CASE(MODE, AMN, BMN, H) \
   if (L.mode == MODE && L.a_mn == AMN && L.b_mn == BMN && L.epi_h == H) return launch2_t<MODE, AMN, BMN, H>(L, stream);
+
+bool gemm2_wide_h() { return Cfg2<true, SDD>::WIDE_H; }
 
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream) {
   MOE_GEMM2_CASE(SDD, false, true, false)      // SDD      X_g . W1 (+act, +pre)

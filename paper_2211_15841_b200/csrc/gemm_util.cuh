@@ -89,6 +89,36 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v
                  : "memory");
   }
 }
+// Write 32 fp32 values as bf16 into half `hh` (columns 32hh..32hh+31) of this
+// thread's 128-byte row in a 128B-swizzled [32 rows][128 B] staging buffer
+// (TMA SWIZZLE_128B: 16-byte chunk j of row r at chunk j ^ (r & 7));
+// conflict-free 16-byte stores.
+__device__ __forceinline__ void stage_row_half128(uint8_t* buf, int lane, const float* v, int hh) {
+  const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = 4 * hh + j;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((cj ^ (lane & 7)) << 4)),
+                 "r"(pack_bf16x2(v[8 * j + 0], v[8 * j + 1])), "r"(pack_bf16x2(v[8 * j + 2], v[8 * j + 3])),
+                 "r"(pack_bf16x2(v[8 * j + 4], v[8 * j + 5])), "r"(pack_bf16x2(v[8 * j + 6], v[8 * j + 7]))
+                 : "memory");
+  }
+}
+// Read half `hh` (columns 32hh..32hh+31) of this thread's 128B-swizzled row
+// (the layout stage_row_half128 writes and a SWIZZLE_128B TMA load leaves).
+__device__ __forceinline__ void load_row_half128(const uint8_t* buf, int lane, float* f, int hh) {
+  const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = 4 * hh + j;
+    uint4 w;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                 : "r"(row + ((cj ^ (lane & 7)) << 4))
+                 : "memory");
+    unpack8(w, f + 8 * j);
+  }
+}
 // Read this thread's 32 bf16 values back from a 64B-swizzled staging row.
 __device__ __forceinline__ void load_row(const uint8_t* buf, int lane, float* f) {
   const uint32_t row = smem_u32(buf) + lane * 64;

@@ -23,4 +23,11 @@ inline moe_status make_tmap_epi(CUtensorMap* map, const void* base, uint64_t inn
                                 uint64_t row_elems, const char* what) {
   return make_tmap_bf16(map, base, inner, outer, row_elems, 32, 32, what, 64);
 }
+// Wide epilogue store maps: 64 x 32 boxes (4 KB: 32 rows of 128 B), 128 B
+// swizzle — twice the bytes per TMA store of make_tmap_epi (TMA store
+// throughput grows with the box: scripts/micro/tma_store_bw.cu).
+inline moe_status make_tmap_epi_wide(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                     uint64_t row_elems, const char* what) {
+  return make_tmap_bf16(map, base, inner, outer, row_elems, 64, 32, what, 128);
+}
 }  // namespace moe

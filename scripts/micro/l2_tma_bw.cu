@@ -102,6 +102,42 @@ __global__ void __launch_bounds__(128, 1) bw_kernel(const __grid_constant__ Maps
       }
       for (int s = warp * ns; s < (warp + 1) * ns; ++s) mbar_wait(&full[s], ((iters / P) / ns - 1) & 1);
     }
+  } else if (G >= 600 && G < 700) {
+    // P = G - 600 producer warps (stage s issued by warp s % P), one consumer
+    // warp (warp 3) freeing every stage on all CTAs of the cluster; with C > 1
+    // each CTA loads 1/C of the box and multicasts it
+    const int P = G - 600;
+    if (warp < P && lane == 0) {
+      for (int i = 0; i < iters; ++i) {
+        const int s = i % NS;
+        if (s % P != warp) continue;
+        const uint32_t ph = (i / NS) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        const int box = mode == 0 ? (int)(((long long)b * iters + i) % nboxes)
+                                  : (int)(((long long)(b / C) * 7919 + i) % nboxes);
+        mbar_expect(&full[s], BOX);
+        if (C == 1) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+              ::"r"(su32(buf + s * BOX)), "l"(&maps.m[0]), "r"(0), "r"(box * rows_per_box), "r"(su32(&full[s])) : "memory");
+        } else {
+          const int rows = rows_per_box / C;
+          const uint16_t mask = (uint16_t)((1u << C) - 1);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, "
+              "{%2, %3}], [%4], %5;"
+              ::"r"(su32(buf + s * BOX + rank * rows * 128)), "l"(&maps.m[0]), "r"(0),
+              "r"(box * rows_per_box + (int)rank * rows), "r"(su32(&full[s])), "h"(mask) : "memory");
+        }
+      }
+    } else if (warp == 3 && lane == 0) {
+      for (int i = 0; i < iters; ++i) {
+        const int s = i % NS;
+        mbar_wait(&full[s], (i / NS) & 1);
+        if (C == 1) mbar_arrive(&empty[s]);
+        else for (int c = 0; c < C; ++c) mbar_arrive_cluster(&empty[s], c);
+      }
+    }
   } else if (warp == 0 && lane == 0) {
     for (int i = 0; i < iters; ++i) {
       const int s = i % NS;
@@ -247,6 +283,12 @@ int main() {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const int ring = 128 * 1024, NS = ring / BOX, smem = ring + 1024;
+  // 3 producer warps + a consumer: distinct vs cluster multicast
+  for (int P : {1, 2, 3}) {
+    run<1>(maps, sms, 0, 600 + P, BOX, NS, rows, nboxes, smem);
+    run<2>(m2, sms, 2, 600 + P, BOX, NS, rows, nboxes, smem);
+    run<4>(m4, sms, 2, 600 + P, BOX, NS, rows, nboxes, smem);
+  }
   run<1>(maps, sms, 0, 1, BOX, NS, rows, nboxes, smem);
   run<1>(maps, sms, 1, 2, BOX, NS, rows, nboxes, smem);
   run<1>(maps, sms, 1, 4, BOX, NS, rows, nboxes, smem);

@@ -423,8 +423,16 @@ def test_dsd_scatter(case):
     assert rel_fro(f64(y1), want1) < FRO_TOL
 
 
+@pytest.mark.parametrize("sdd_form", ["auto", "1", "0"])
 @pytest.mark.parametrize("case", PRODUCT_CASES)
-def test_six_products(case):
+def test_six_products(case, sdd_form, monkeypatch):
+    """The six products (§5.1) against the oracle. sdd_form: the
+    SDD / SDD^T kernel choice (auto: CTA pairs when the experts average >= 3
+    block-rows; "1": CTA pairs; "0": 1-SM tiles)."""
+    if sdd_form == "auto":
+        monkeypatch.delenv("MOE_SDD_PAIR", raising=False)
+    else:
+        monkeypatch.setenv("MOE_SDD_PAIR", sdd_form)
     d = dev()
     A = api()
     T, h, f, E, k, zipf, seed = case
