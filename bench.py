@@ -191,19 +191,21 @@ class Step:
             ("router+topology", L.moe_router_topology, (c, d(t["x"]), d(t["wr"]), d(sv.logits), d(sv.expert_idx),
                                                         d(sv.gates), topo, ws, s)),
         ]
-        gfused = bool(L.moe_gather_is_fused(c))   # layer.cu: the padded gather inside the SDD / DD^TS loads
+        coded = not idn and sv.act_deriv is None  # layer.cu: only the branch-coded A is saved (R24)
+        gfused = bool(L.moe_gather_is_fused(c)) and not coded  # layer.cu: the padded gather inside the SDD / DD^TS loads
+        if coded:
+            sdd_fwd = ("sdd", L.moe_sdd_act_coded, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a), s))
+        else:
+            sdd_fwd = ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
+                                                None if idn else d(sv.act_deriv), s))
         unp = bool(cfg.unpadded)                  # layer.cu: no pad rows, partial blocks at the fringe
         if unp:
-            self.calls += [("gather", L.moe_sort_rows, (c, d(t["x"]), topo, d(sv.x_g), s)),
-                           ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
-                                                     None if idn else d(sv.act_deriv), s))]
+            self.calls += [("gather", L.moe_sort_rows, (c, d(t["x"]), topo, d(sv.x_g), s)), sdd_fwd]
         elif gfused:
             self.calls += [("sdd+gather", L.moe_sdd_gather, (c, d(t["x"]), d(t["w1"]), topo, cfg.act, d(sv.a),
                                                             None if idn else d(sv.act_deriv), d(sv.x_g), s))]
         else:
-            self.calls += [("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)),
-                           ("sdd", L.moe_sdd_deriv, (c, d(sv.x_g), d(t["w1"]), 0, topo, cfg.act, None, d(sv.a),
-                                                     None if idn else d(sv.act_deriv), s))]
+            self.calls += [("gather", L.moe_gather, (c, d(t["x"]), topo, d(sv.x_g), s)), sdd_fwd]
         self.calls += [
             ("dsd+scatter", L.moe_dsd_scatter, (c, d(sv.a), d(t["w2"]), topo, d(sv.gates), d(sv.y_g),
                                                  d(t["y"]), s)),
@@ -224,6 +226,8 @@ class Step:
             bwd = [("scatter_bwd", L.moe_scatter_bwd, (c, d(t["dy"]), d(sv.y_g), topo, d(sv.gates), wsl["dy_g"],
                                                        wsl["dgates"], s))]
         bwd += [
+            ("sddT", L.moe_sdd_act_coded, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act, d(sv.a), wsl["dh"], s))
+            if coded else
             ("sddT", L.moe_sdd_deriv, (c, wsl["dy_g"], d(t["w2"]), 1, topo, cfg.act,
                                        None if idn else d(sv.act_deriv), wsl["dh"], None, s)),
             ("dsTd", L.moe_dsd, (c, d(sv.a), 1, wsl["dy_g"], 0, topo, d(t["dw2"]), s)),
@@ -284,7 +288,7 @@ def run_ours_single(args, peaks):
     x = inp["x"].to(dev)
     dy = inp["dy"].to(dev)
     wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
-    saved = A.Saved.allocate(cfg, dev)
+    saved = A.Saved.allocate(cfg, dev, save_deriv=args.act_save == "deriv")
     ws = A.workspace(cfg, dev)
     t = {"x": x, "dy": dy, "wr": wr, "w1": w1, "w2": w2, "saved": saved, "ws": ws,
          "y": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
@@ -410,17 +414,21 @@ def run_ours_single(args, peaks):
     roof["traffic"] = tr.get("bytes") if tr else None
     if tr:
         roof["traffic_source"] = tr.get("source")
-    if dname == "sdd":
+    coded = cfg.act != 0 and saved.act_deriv is None
+    roof["saved_for_backward"] = ("branch-coded A only (R24): the SDD writes one output, the §8(d) bytes" if coded
+                                  else "A and act'(H) (R18)")
+    if dname == "sdd" and not coded:
         # this design writes act(H) AND act'(H) (reading R18): the same launch
         # against its own two-output byte count, beside the §8(d) figure above
         b2 = wm["sdd_design_bytes"]
         roof["design_two_outputs"] = {"bytes": b2, "achieved": round(b2 / dur_s / 1e9, 1),
                                       "frac": round(b2 / dur_s / 1e9 / peaks["hbm_gbs"], 4)}
+    if dname == "sdd":
         # context: the SDD's tiles move A (128 x h) and B (h x 256)
         # into shared memory and act(H), act'(H) (2 x 128 x 256) out of it, per
         # 128 x 256 tile; against the measured TMA L2->SMEM delivery ceiling
         # (scripts/micro/l2_tma_bw.cu, profiles/r1s5_l2_tma_bw.txt)
-        tile_bytes = 2 * (128 * h + h * 256) + 2 * 2 * 128 * 256
+        tile_bytes = 2 * (128 * h + h * 256) + (1 if coded else 2) * 2 * 128 * 256
         feed = tile_bytes * (nnz // 2) / dur_s / 1e12
         roof["sm_port"] = {"bytes_per_tile": tile_bytes, "tiles": nnz // 2, "achieved_tbs": round(feed, 2),
                            "tma_l2_to_smem_ceiling_tbs": 14.59, "frac": round(feed / 14.59, 3)}
@@ -664,6 +672,9 @@ def main():
                     help="> 0: time the token-dropping formulation (P:112-116) with this capacity factor "
                          "instead of the dropless layer (context only; the headline is dropless)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--act-save", default=os.environ.get("MOE_BENCH_ACT_SAVE", "deriv"), choices=["coded", "deriv"],
+                    help="what the forward saves for the SDD^T: act'(H) beside A (R18, default) or the "
+                         "branch-coded A alone (R24: one buffer less, measured slower)")
     ap.add_argument("--layout", default=os.environ.get("MOE_BENCH_LAYOUT", "padded"), choices=["padded", "unpadded"],
                     help="dense expert-grouped rows padded to 128 per expert (P:297, the paper's layout) or not "
                          "(partial blocks at the fringe, NEXT-3); same outputs")

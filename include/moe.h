@@ -366,6 +366,28 @@ moe_status moe_sdd(const moe_config* cfg, const void* a, const void* b, int tran
 moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, int trans_b,
                          const moe_topology_t* topo, int32_t act, const void* deriv_src, void* out_s,
                          void* out_deriv, void* stream);
+/* moe_sdd_act_coded: the layer's memory-saving form (reading R24 in DESIGN.md,
+ * moe_saved.act_deriv = NULL): the forward saves ONLY the activation
+ * A = act(H), and the SDD^T recovers act'(H) from A itself. P:206 lists SDD^T but not what it reads; the paper keeps
+ * act(H) for DS^TD anyway ("second layer weight gradient").
+ *   coded_src == NULL (forward SDD): out_s = coded act(A.B) [nnz,bs,bs]
+ *     bf16. gelu: A >= 0 is RNE bf16 of act(h) (h >= 0); for h < 0 the sign bit
+ *     is set and the mantissa LSB holds the branch of gelu's two pre-images
+ *     (1: h < argmin gelu = -0.75246), the value being the nearest bf16 of that
+ *     parity (<= 1 ulp). relu: RNE bf16 (act' = A > 0). identity: plain H.
+ *     The coded A is a valid bf16 activation: every consumer (DSD, DS^TD) reads
+ *     it as is.
+ *   coded_src != NULL (SDD^T): out_s = (A.B) * act'(H), act'(H) decoded
+ *     from coded_src (the forward's out_s): gelu by a table over A's 16 bits
+ *     (act_code_table.h), relu as A > 0.
+ *   Shapes, layouts, trans_b and errors as moe_sdd. */
+moe_status moe_sdd_act_coded(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                             const moe_topology_t* topo, int32_t act, const void* coded_src, void* out_s,
+                             void* stream);
+/* Host only (no CUDA call): act'(H) as the SDD^T decodes it from n coded bf16
+ * bit patterns (moe_sdd_act_coded's A) into out [n] fp32. MOE_EINVAL on a bad
+ * act or NULL pointer. For tests of the decode table against the oracle. */
+moe_status moe_act_code_decode_host(int32_t act, const uint16_t* a_bits, float* out, int64_t n);
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream);
 /* The padded gather fused into the products that read X_g: the A rows
@@ -474,7 +496,10 @@ typedef struct {
   moe_topology_t topo;
   void* x_g;          /* [max_rows, h] bf16 padded gather of x; written only when the config
                          cannot gather inside the products (moe_sdd_gather) */
-  void* act_deriv;    /* [max_nnz, bs, bs] bf16 act'(pre-activation); unused (NULL) for identity */
+  void* act_deriv;    /* [max_nnz, bs, bs] bf16 act'(pre-activation) (R18, the default), or NULL:
+                         the branch-coded activation (R24, moe_sdd_act_coded): `a` alone is saved
+                         and the SDD^T decodes act'(H) from it (one buffer less; measured slower at
+                         MoE-XS). Unused for identity. */
   void* a;            /* [max_nnz, bs, bs] bf16 activation */
   void* y_g;          /* [max_rows, h] bf16 */
 } moe_saved;

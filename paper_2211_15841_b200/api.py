@@ -308,6 +308,28 @@ def moe_sdd_deriv(cfg, a, b, trans_b, topo: Topology, act=ACT_IDENTITY, deriv_sr
     return (out, der) if want_deriv else out
 
 
+def moe_sdd_act_coded(cfg, a, b, trans_b, topo: Topology, act=ACT_IDENTITY, coded_src=None, out=None):
+    """moe_sdd_act_coded (include/moe.h, reading R24): forward (coded_src None)
+    returns the branch-coded act(A.B); with coded_src (the forward's output)
+    returns (A.B) * act'(H) decoded from it (SDD^T)."""
+    out = out if out is not None else _nnz_values(cfg, a.device)
+    check("moe_sdd_act_coded", lib.moe_sdd_act_coded(ctypes.byref(cfg), _p(a), _p(b), int(trans_b),
+                                                     ctypes.byref(topo.struct), int(act), _p(coded_src), _p(out),
+                                                     _stream()))
+    return out
+
+
+def moe_act_code_decode_host(act, a_bits):
+    """moe_act_code_decode_host (host only): act'(H) decoded from coded bf16 bit
+    patterns (a numpy uint16 array) -> numpy float32."""
+    import numpy as np
+    a_bits = np.ascontiguousarray(a_bits, dtype=np.uint16)
+    out = np.empty(a_bits.shape, dtype=np.float32)
+    check("moe_act_code_decode_host", lib.moe_act_code_decode_host(int(act), a_bits.ctypes.data, out.ctypes.data,
+                                                                   a_bits.size))
+    return out
+
+
 def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
     rows = moe_max_padded_rows(cfg)
     n_out = cfg.num_experts * cfg.ffn_hidden if trans_s else rows
@@ -394,7 +416,10 @@ class Saved:
     ws: torch.Tensor | None = None   # the forward's workspace when it holds the auxiliary loss (aux_loss_coeff > 0)
 
     @staticmethod
-    def allocate(cfg, device="cuda") -> "Saved":
+    def allocate(cfg, device="cuda", save_deriv: bool = True) -> "Saved":
+        """save_deriv=True (default): act'(H) is saved beside A (R18);
+        False: act_deriv is None and the forward saves only the branch-coded A
+        (R24: one [nnz, bs, bs] buffer less, measured slower at MoE-XS)."""
         T, E, k, h = cfg.tokens, cfg.num_experts, cfg.top_k, cfg.hidden
         rows = moe_max_padded_rows(cfg)
         s = Saved(torch.empty(T, E, dtype=torch.float32, device=device),
@@ -402,7 +427,7 @@ class Saved:
                   torch.empty(T, k, dtype=torch.float32, device=device),
                   Topology(cfg, device),
                   torch.empty(rows, h, dtype=torch.bfloat16, device=device),
-                  None if cfg.act == ACT_IDENTITY else _nnz_values(cfg, device),
+                  _nnz_values(cfg, device) if save_deriv and cfg.act != ACT_IDENTITY else None,
                   _nnz_values(cfg, device),
                   torch.empty(rows, h, dtype=torch.bfloat16, device=device))
         s.struct = MoeSaved(s.logits.data_ptr(), s.expert_idx.data_ptr(), s.gates.data_ptr(), s.topo.struct,

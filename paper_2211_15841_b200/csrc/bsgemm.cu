@@ -91,15 +91,18 @@ struct Cfg {
   static constexpr int EPI = EPW * NBUF * EPI_BUF;  // per-warp staging ring
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NH = 3;  // per-warp ring of prefetched act'(H) chunks (SDD^T)
+  // per-warp ring of prefetched act'(H) / coded-A chunks (SDD^T); two deep, so
+  // that the coded-activation decode table (R24) fits beside three stages
+  static constexpr int NH = 2;
+  static constexpr int TAB = EPI_H ? ACT_CODE_BYTES : 0;
   // router epilogue exchange (+ the tile's expert histogram, E <= 256)
   static constexpr int XCH = MODE == DENSE ? 128 * (2 + 2 * kMaxRouterTopK) * 4 + 256 * 4 : 0;
   static constexpr int H_BYTES = EPI_H ? EPW * NH * EPI_BUF : 0;
   static constexpr int SMEM_CTA = OCC == 2 ? 113 * 1024 : SMEM_LIMIT;
-  static constexpr int STAGES_RAW = (SMEM_CTA - SMEM_FIXED - EPI - H_BYTES - XCH) / STAGE;
+  static constexpr int STAGES_RAW = (SMEM_CTA - SMEM_FIXED - EPI - H_BYTES - TAB - XCH) / STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES + XCH;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * STAGE + EPI + H_BYTES + TAB + XCH;
   static_assert(STAGES >= 2, "not enough shared memory for two stages");
   static_assert(BN % 64 == 0 && BN <= 256, "BN must be 64, 128 or 256");
 };
@@ -276,7 +279,8 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
   uint8_t* smem_b = smem_a + STAGES * A_BYTES;
   uint8_t* smem_epi = smem_b + STAGES * C::B_BYTES;
   uint8_t* smem_h = smem_epi + C::EPI;
-  uint8_t* smem_x = smem_h + C::H_BYTES;
+  uint8_t* smem_tab = smem_h + C::H_BYTES;  // SDD^T: act'(H) decode table of the coded A (R24)
+  uint8_t* smem_x = smem_tab + C::TAB;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_x + C::XCH);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
     tma_prefetch_desc(&tmap_b);
   }
   if (warp == C::MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_holder);
+  if (EPI_H && p.act_code) act_code_table_to_smem(smem_tab, g_act_code_tab);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -530,6 +535,20 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
       }
       sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
     };
+    // the same for 16 bf16x2 words already packed (the coded A, R24)
+    auto store_chunk_raw = [&](const CUtensorMap* map, const uint32_t* w, int x, int y) {
+      if (lane == 0) bulk_wait_read<C::NBUF - 1>();
+      __syncwarp();
+      stage_row_raw(stg + sbuf * EPI_BUF, lane, w);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map, stg + sbuf * EPI_BUF, x, y);
+        bulk_commit();
+      }
+      sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
+    };
+    const uint32_t tab_smem = smem_u32(smem_tab);
     // SDD^T: this warp's act'(H) chunks form one sequence j = 0, 1, ... over
     // its tiles (tile blockIdx.x + (j / NPW) * gridDim.x, chunk grp + (j % NPW) * NG),
     // prefetched NH ahead into a ring, so the loads overlap the main loop.
@@ -647,7 +666,12 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
           }
           int x, y;
           out_coords(p, MODE, t, c, row0, BN, x, y);
-          if (p.epi == EPI_ACT_FWD) {
+          uint32_t wcode[16];
+          bool coded_out = false;
+          if (MODE == SDD && p.epi == EPI_ACT_FWD && p.act_code) {  // coded A only (R24)
+            act_fwd_code32(p.act, v, wcode);
+            coded_out = true;
+          } else if (p.epi == EPI_ACT_FWD) {
             if (p.has_pre && p.aux_deriv) {  // save act'(H) beside act(H)
               float g[32];
               act_fwd_deriv32(p.act, v, g);
@@ -663,12 +687,18 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
           } else if (EPI_H && p.epi == EPI_ACT_BWD) {
             const int hb_i = hseq % C::NH;
             mbar_wait(&hb[hb_i], (uint32_t)(hseq / C::NH) & 1u);
-            float hf[32];
-            load_row(hst + hb_i * EPI_BUF, lane, hf);
-            if (p.aux_deriv) {  // the source already holds act'(H)
-              mul32(v, hf);
-            } else if (!(p.dbg & 4)) {
-              act_grad_mul32(p.act, v, hf);
+            if (MODE == SDD && p.act_code) {  // the source is the coded A (R24): act'(H) by table lookup
+              uint32_t wa[16];
+              load_row_raw(hst + hb_i * EPI_BUF, lane, wa);
+              act_code_mul32(p.act, v, wa, tab_smem);
+            } else {
+              float hf[32];
+              load_row(hst + hb_i * EPI_BUF, lane, hf);
+              if (p.aux_deriv) {  // the source already holds act'(H)
+                mul32(v, hf);
+              } else if (!(p.dbg & 4)) {
+                act_grad_mul32(p.act, v, hf);
+              }
             }
             __syncwarp();
             load_h(hseq + C::NH);  // refill the buffer just read
@@ -700,7 +730,10 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
               }
             }
           }
-          if (!(MODE == DSD_ROW && p.scatter_only)) store_chunk(&tmap_c, v, x, y);
+          if (coded_out)
+            store_chunk_raw(&tmap_c, wcode, x, y);
+          else if (!(MODE == DSD_ROW && p.scatter_only))
+            store_chunk(&tmap_c, v, x, y);
           if (MODE == DSD_ROW && p.scatter_y && p.direct) {
             // the weighted un-permutation of the layer (top-1): the
             // gate-scaled rows go straight to y[token] (pad rows: dropped)
@@ -1184,7 +1217,7 @@ int moe_debug_trace_dump(const char* path) {
 
 static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b, int trans_b,
                              const moe_topology_t* topo, int32_t act, const void* act_src, void* out_s, void* out_aux,
-                             bool deriv, void* stream, const void* x_gather = nullptr) {
+                             bool deriv, void* stream, const void* x_gather = nullptr, bool coded = false) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(a && b && out_s, "moe_sdd: NULL operand");
@@ -1203,6 +1236,11 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   L.p.epi = act_src ? EPI_ACT_BWD : ((act != MOE_ACT_IDENTITY || out_aux) ? EPI_ACT_FWD : EPI_STORE);
   L.p.has_pre = out_aux != nullptr;
   L.p.aux_deriv = deriv ? 1 : 0;
+  L.p.act_code = coded && act != MOE_ACT_IDENTITY ? 1 : 0;
+  if (L.p.act_code) {
+    L.p.aux_deriv = 0;
+    MOE_CHECK_ARG(!out_aux, "moe_sdd_act_coded: the coded form has no second output");
+  }
   {
     // L2 priorities of the SDD outputs: act(H) (read next by the DSD) kept,
     // act'(H) (read only in the backward) streamed; SDD^T: dH kept.
@@ -1232,7 +1270,9 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
   const int pair_env = pe && pe[0] ? (pe[0] == '1' ? 1 : 0) : -1;
   // (the A-row gather inside the loads, moe_sdd_gather, exists only in the 1-SM kernel)
   const bool deep = cfg->tokens * cfg->top_k >= 3LL * cfg->num_experts * BM;
-  const bool pair = use_pair(cfg) && !x_gather && (pair_env == 1 || (pair_env == -1 && deep));
+  bool pair = use_pair(cfg) && !x_gather && (pair_env == 1 || (pair_env == -1 && deep));
+  // the coded activation is wired into the CTA-pair kernel's 4 KB-box epilogues only
+  if (pair && L.p.act_code && !(act_src ? gemm2_h_coded() : pair_wide())) pair = false;
   L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * (L.p.F / 2)) : (int)(nnz / (L.bn / 128));
   if (x_gather) {  // A rows = x[row_src / k] by tile::gather4 (X_g never materialised)
     MOE_TRY(make_tmap_bf16(&L.ta, x_gather, h, cfg->tokens, h, BK, 1, "moe_sdd_gather x", KSW));
@@ -1290,6 +1330,12 @@ moe_status moe_sdd_gather(const moe_config* cfg, const void* x, const void* w1, 
   MOE_CHECK_ARG(x_g, "moe_sdd_gather: this config needs the x_g scratch (padded gather + SDD)");
   MOE_TRY(moe_gather(cfg, x, topo, x_g, stream));
   return sdd_launch(cfg, x_g, w1, 0, topo, act, nullptr, out_s, out_deriv, true, stream);
+}
+
+moe_status moe_sdd_act_coded(const moe_config* cfg, const void* a, const void* b, int trans_b,
+                             const moe_topology_t* topo, int32_t act, const void* coded_src, void* out_s,
+                             void* stream) {
+  return sdd_launch(cfg, a, b, trans_b, topo, act, coded_src, out_s, nullptr, false, stream, nullptr, true);
 }
 
 moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, int trans_b,

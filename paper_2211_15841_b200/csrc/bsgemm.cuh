@@ -33,6 +33,9 @@ struct GemmParams {
   // epilogue
   int epi, act, has_pre;
   int aux_deriv;
+  // branch-coded activation (DESIGN R24): EPI_ACT_FWD writes only the coded A
+  // (no second output); EPI_ACT_BWD decodes act'(H) from the coded A source
+  int act_code;
   int l2_c, l2_d;  // L2 priority of the tmap_c / tmap_d epilogue stores: 0 normal, 1 evict_last, 2 evict_first
   // DSD_ROW + scatter_y (top-1 only): y[t] = gate[t] * row p of the output, t = row_src[p]
   // (tile::scatter4 through tmap_d; pad rows dropped)
@@ -142,7 +145,8 @@ __device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev
 // CTA-pair (cta_group::2) variant for SDD / DSD_ROW / DS_COL / DDS_COL with
 // 256 x 256 tiles (bsgemm2.cu); B boxes are 128 wide (each CTA's half).
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);
-bool gemm2_wide_h();  // the CTA-pair SDD^T takes 64 x 32 (4 KB) act'(H) / dH maps
+bool gemm2_wide_h();   // the CTA-pair SDD^T takes 64 x 32 (4 KB) act'(H) / dH maps (else 32 x 32)
+bool gemm2_h_coded();  // the CTA-pair SDD^T can decode the coded activation (R24)
 GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo);
 
 }  // namespace moe

@@ -57,8 +57,17 @@ constexpr int P_NBUF = MOE_PAIR_NBUF;                          // staging buffer
 #ifndef MOE_PAIR_WIDE
 #define MOE_PAIR_WIDE 1
 #endif
+// SDD^T: columns per box of the per-warp act'(H) / coded-A ring (64: 4 KB boxes,
+// 128B swizzle; 32: 2 KB boxes, 64B swizzle) and its depth. 4 KB boxes three
+// deep (the default) leave no room for the coded-activation decode table (R24:
+// that SDD^T then runs on the 1-SM kernel); 2 KB boxes five deep fit it beside
+// four pipeline stages but measured slower (MoE-XS SDD^T 133 vs 97 us with
+// act'(H); 163 us decoding the coded A).
+#ifndef MOE_PAIR_HC
+#define MOE_PAIR_HC 64
+#endif
 #ifndef MOE_PAIR_NHW
-#define MOE_PAIR_NHW 3
+#define MOE_PAIR_NHW (MOE_PAIR_HC == 64 ? 3 : 5)
 #endif
 
 template <bool EPI_H, int MODE = -1>
@@ -68,18 +77,24 @@ struct Cfg2 {
   // (DS^TD / DD^TS measured no faster with 4 KB boxes: 73.8 / 76.6 us vs
   // 71.4 / 75.5, the larger staging costing two pipeline stages)
   static constexpr bool WIDE = MOE_PAIR_WIDE && MODE == SDD && !EPI_H;
-  // SDD^T: a per-warp ring of NHW 4 KB act'(H) boxes (64 x 32), each turned
-  // into the dH box in place and stored from the same buffer
+  // SDD^T: a per-warp ring of NHW act'(H) / coded-A boxes (HC x 32), each
+  // turned into the dH box in place and stored from the same buffer
   static constexpr bool WIDE_H = MOE_PAIR_WIDE && EPI_H;
+  static constexpr int HC = MOE_PAIR_HC;
+  static constexpr int HBOX = 32 * HC * 2;
   static constexpr int NHW = MOE_PAIR_NHW;
   static constexpr int NHB = WIDE_H ? NHW : 2;  // act'(H) barriers per epilogue warp
   static constexpr int P_EPI_BYTES = WIDE_H ? 0 : NUM_EPI_WARPS * (WIDE ? 2 * 4096 : P_NBUF * EPI_BUF);
-  static constexpr int H_BYTES = EPI_H ? (WIDE_H ? NUM_EPI_WARPS * NHW * 4096 : EPI_BYTES) : 0;
-  static constexpr int TOK = 4 * 16 * 16;  // DDS_COL gather: token ring, 4 K-steps x 16 lanes x int4
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK) / P_STAGE;
+  static constexpr int H_BYTES = EPI_H ? (WIDE_H ? NUM_EPI_WARPS * NHW * HBOX : EPI_BYTES) : 0;
+  static constexpr int TOK = MODE == DDS_COL ? 4 * 16 * 16 : 0;  // DDS_COL gather: token ring, 4 K-steps x 16 lanes x int4
+  // SDD^T: act'(H) decode table of the coded A (R24), where it fits
+  static constexpr bool HAS_TAB = EPI_H && WIDE_H && HC == 32;
+  static constexpr int TAB = HAS_TAB ? ACT_CODE_BYTES : 0;
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK - TAB) / P_STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * P_BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + P_EPI_BYTES + H_BYTES + TOK;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + P_EPI_BYTES + H_BYTES + TOK + TAB;
+  static_assert(!EPI_H || STAGES >= 4, "SDD^T: four pipeline stages expected");
 };
 
 struct Tile2 {
@@ -179,7 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint8_t* smem_epi = smem_b + STAGES * P_B_BYTES;
   uint8_t* smem_h = smem_epi + P_EPI_BYTES;
   int4* tokring = reinterpret_cast<int4*>(smem_h + C::H_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_h + C::H_BYTES + C::TOK);
+  uint8_t* smem_tab = smem_h + C::H_BYTES + C::TOK;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_tab + C::TAB);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -207,6 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     tma_prefetch_desc(&tmap_b);
   }
   if (warp == P_MMA_WARP) tmem_alloc_pair<C::TMEM_COLS>(tmem_holder);
+  if (C::HAS_TAB && p.act_code) act_code_table_to_smem(smem_tab, g_act_code_tab);
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
@@ -322,6 +339,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           uint8_t* sa = smem_a + stage * P_A_BYTES;
           uint8_t* sb = smem_b + stage * P_B_BYTES;
           uint64_t* fb = &full[stage];
+          if (p.dbg & 8) {  // experiment: no operand loads (the stage completes at once)
+            if (leader) mbar_arrive(fb);
+          } else {
           if (leader) mbar_arrive_expect_tx(fb, 2 * P_STAGE);
           if (MODE == SDD) {
             const int k0 = kit * BK;
@@ -355,6 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
               tma_load_2d_pair(sa, &tmap_a, fb, odrow + kk * BK, m0);
             }
             tma_load_3d_pair(sb, &tmap_b, fb, 0, sblk * BM + kk * BK, 0);
+          }
           }
         }
         __syncwarp();
@@ -414,7 +435,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     constexpr int EPG = NUM_EPI_WARPS / 4;     // epilogue warps per TMEM lane quarter
     const int row0 = q * 32;
     uint8_t* stg = smem_epi + wq * (C::WIDE ? 2 * 4096 : P_NBUF * EPI_BUF);
-    uint8_t* hst = smem_h + wq * (C::WIDE_H ? C::NHW * 4096 : 2 * EPI_BUF);
+    uint8_t* hst = smem_h + wq * (C::WIDE_H ? C::NHW * C::HBOX : 2 * EPI_BUF);
     uint64_t* hb = hbar + wq * C::NHB;
     uint32_t hphase[2] = {0, 0};
     int hslot = 0;
@@ -444,10 +465,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       }
     };
 
-    // SDD^T, wide: this warp's 64-column super-chunks form one sequence j over
-    // its tiles (tile cid + (j / SPW) * ncl, super-chunk half + (j % SPW) * EPG);
-    // the act'(H) box of j + NHW - 1 is loaded while j is processed
-    constexpr int SPW = (P_BN / 64) / EPG;
+    // SDD^T ring: this warp's HC-column boxes form one sequence j over its
+    // tiles (tile cid + (j / SPW) * ncl, box half + (j % SPW) * EPG); the
+    // act'(H) / coded-A box of j + NHW - 1 is loaded while j is processed
+    constexpr int HSUB = C::HC / 32;  // 32-column TMEM loads per box
+    constexpr int SPW = (P_BN / C::HC) / EPG;
     const int hw_end = (ntiles > cid ? (ntiles - 1 - cid) / ncl + 1 : 0) * SPW;
     int hw_seq = 0;
     uint32_t hw_phase = 0;  // bit b: parity of slot b's next completion
@@ -456,11 +478,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank);
       if (!(rank == 0 || tj.second)) return;  // nothing stored for this CTA's half: nothing loaded
       int x, y;
-      out_coords2(p, MODE, tj, rank, 2 * (half + (j % SPW) * EPG), row0, p.F, x, y);
+      out_coords2(p, MODE, tj, rank, HSUB * (half + (j % SPW) * EPG), row0, p.F, x, y);
       const int b = j % C::NHW;
       fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&hb[b], 4096);
-      tma_load_2d(hst + b * 4096, &tmap_d, &hb[b], x, y);
+      mbar_arrive_expect_tx(&hb[b], C::HBOX);
+      tma_load_2d(hst + b * C::HBOX, &tmap_d, &hb[b], x, y);
     };
     if (C::WIDE_H && lane == 0)
       for (int j = 0; j < C::NHW - 1; ++j) load_hw(j);
@@ -488,8 +510,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           if (r[0] == 0x7fffffffu && r[1] == 0x12345u) p.gates[0] = 1.f;
         }
       } else if (C::WIDE_H) {
-        // dH = dA (x) act'(H) per 64-column super-chunk: two 32-column TMEM
-        // loads, the act'(H) box read and overwritten in place, one 4 KB store
+        // dH = dA (x) act'(H) per HC-column box: HSUB 32-column TMEM loads,
+        // the act'(H) / coded-A box read and overwritten in place, one store
 #pragma unroll 1
         for (int s = 0; s < SPW; ++s, ++hw_seq) {
           const int b = hw_seq % C::NHW;
@@ -497,13 +519,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             const int sc = half + s * EPG;
             mbar_wait(&hb[b], (hw_phase >> b) & 1u);
             hw_phase ^= 1u << b;
-            uint8_t* slot = hst + b * 4096;
+            uint8_t* slot = hst + b * C::HBOX;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
+            for (int hh = 0; hh < HSUB; ++hh) {
               float v[32];
               if (has_acc) {
                 uint32_t r[32];
-                tmem_ld32(taddr + (2 * sc + hh) * EPI_COLS, r);
+                tmem_ld32(taddr + (HSUB * sc + hh) * EPI_COLS, r);
                 tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = fringe ? 0.f : __uint_as_float(r[i]);
@@ -511,21 +533,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = 0.f;
               }
-              float hf[32];
-              load_row_half128(slot, lane, hf, hh);
-              if (p.aux_deriv) {
-                mul32(v, hf);
+              if (C::HAS_TAB && p.act_code) {  // the slot holds the coded A (R24): act'(H) by table lookup
+                uint32_t wa[16];
+                if (HSUB == 2) load_row_half128_raw(slot, lane, wa, hh); else load_row_raw(slot, lane, wa);
+                if (!(p.dbg & 4)) act_code_mul32(p.act, v, wa, smem_u32(smem_tab));
               } else {
-                act_grad_mul32(p.act, v, hf);
+                float hf[32];
+                if (HSUB == 2) load_row_half128(slot, lane, hf, hh); else load_row(slot, lane, hf);
+                if (p.aux_deriv) {
+                  mul32(v, hf);
+                } else {
+                  act_grad_mul32(p.act, v, hf);
+                }
               }
-              stage_row_half128(slot, lane, v, hh);  // this lane's row only: in place is safe
+              // this lane's row only: in place is safe
+              if (HSUB == 2) stage_row_half128(slot, lane, v, hh); else stage_row(slot, lane, v);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
               int x, y;
-              out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
-              tma_store_2d(&tmap_c, slot, x, y);
+              out_coords2(p, MODE, t, rank, HSUB * sc, row0, p.F, x, y);
+              if (!(p.dbg & 16)) tma_store_2d(&tmap_c, slot, x, y);
               bulk_commit();
             }
           }
@@ -543,9 +572,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         uint8_t* bufc = stg;
         uint8_t* bufd = stg + 4096;
         const bool two = p.epi == EPI_ACT_FWD && p.has_pre;
+        // one output (the coded A, R24): the two buffers alternate, so a
+        // super-chunk waits only for the store issued two super-chunks ago
+        const bool alt = p.epi == EPI_ACT_FWD && p.act_code;
 #pragma unroll 1
         for (int sc = half; sc < P_BN / 64; sc += EPG) {
-          if (lane == 0) bulk_wait_read<0>();  // the previous super-chunk's stores have read both buffers
+          uint8_t* bc = bufc;
+          if (alt) {
+            if (lane == 0) bulk_wait_read<1>();
+            bc = stg + sbuf * 4096;
+            sbuf ^= 1;
+          } else if (lane == 0) {
+            bulk_wait_read<0>();  // the previous super-chunk's stores have read both buffers
+          }
           __syncwarp();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -559,6 +598,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             } else {
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (p.epi == EPI_ACT_FWD && p.act_code) {  // coded A only (R24)
+              uint32_t wcode[16];
+              act_fwd_code32((p.dbg & 4) ? MOE_ACT_IDENTITY : p.act, v, wcode);
+              stage_row_half128_raw(bc, lane, wcode, hh);
+              continue;
             }
             if (p.epi == EPI_ACT_FWD) {
               if (p.has_pre && p.aux_deriv) {
@@ -581,8 +626,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           if (lane == 0) {
             int x, y;
             out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
-            tma_store_2d(&tmap_c, bufc, x, y);
-            if (two) tma_store_2d(&tmap_d, bufd, x, y);
+            if (!(p.dbg & 16)) tma_store_2d(&tmap_c, bc, x, y);
+            if (two && !(p.dbg & 16)) tma_store_2d(&tmap_d, bufd, x, y);
             bulk_commit();
           }
         }
@@ -677,8 +722,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
 static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   using C = Cfg2<EPI_H, MODE>;
-  if (C::WIDE_H && !L.p.wide)
-    return set_error(MOE_EUNSUPPORTED, "%s: the CTA-pair SDD^T needs 64 x 32 act'(H) / dH maps", L.name);
+  if (C::WIDE_H && (C::HC == 64) != (L.p.wide != 0))
+    return set_error(MOE_EUNSUPPORTED, "%s: the CTA-pair SDD^T ring needs %d-column act'(H) / dH maps", L.name, C::HC);
+  if (EPI_H && L.p.act_code && !C::HAS_TAB)
+    return set_error(MOE_EUNSUPPORTED, "%s: no room for the coded-activation table in this CTA-pair build", L.name);
   auto kern = bsgemm2_kernel<MODE, A_MN, B_MN, EPI_H>;
   {
     static unsigned long long smem_mask = 0;  // per device (the attribute is per device)
@@ -701,7 +748,8 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
 #define MOE_GEMM2_CASE(MODE, AMN, BMN, H) \
   if (L.mode == MODE && L.a_mn == AMN && L.b_mn == BMN && L.epi_h == H) return launch2_t<MODE, AMN, BMN, H>(L, stream);
 
-bool gemm2_wide_h() { return Cfg2<true, SDD>::WIDE_H; }
+bool gemm2_wide_h() { return Cfg2<true, SDD>::WIDE_H && Cfg2<true, SDD>::HC == 64; }
+bool gemm2_h_coded() { return Cfg2<true, SDD>::HAS_TAB; }
 
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream) {
   MOE_GEMM2_CASE(SDD, false, true, false)      // SDD      X_g . W1 (+act, +pre)

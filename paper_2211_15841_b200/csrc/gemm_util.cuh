@@ -2,10 +2,12 @@
 // (bsgemm.cu) and CTA-pair (bsgemm2.cu) tcgen05 GEMM kernels.
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/moe.h"
+#include "act_code_table.h"
 #include "sm100.cuh"
 
 namespace moe {
@@ -189,6 +191,144 @@ __device__ __forceinline__ void mul32(float* v, const float* g) {
     v[i + 1] = r.y;
   }
 }
+// ---- branch-coded activation (DESIGN reading R24) ----------------------------
+// The forward saves only A = act(H) in bf16. gelu has two pre-images for
+// A < 0 (either side of its minimum at kGeluXMin): the mantissa LSB of a
+// negative A holds the branch (1: h < kGeluXMin), chosen as the nearest bf16
+// with that parity (<= 1 ulp from a; the sign follows h, so an A that
+// underflows to +0 for very negative h stays negative). A >= 0 is RNE bf16.
+// relu needs no code (act' = A > 0). The SDD^T decodes act'(H) from A's 16 bits
+// through kActCodeTable (act_code_table.h, staged in shared memory).
+// Two coded bf16 values packed as a bf16x2 word (low half: element 0), branch-free:
+// RNE where x >= 0; where x < 0 the truncated magnitude with the sign set, +1 if
+// its LSB differs from the branch bit (|A| <= 0.17 there, so the +1 never
+// carries out of its half).
+__device__ __forceinline__ uint32_t code_bf16x2(float2 a, float2 x) {
+  const uint32_t rne = pack_bf16x2(a.x, a.y);
+  const uint32_t ax = __float_as_uint(a.x), ay = __float_as_uint(a.y);
+  const uint32_t t = __byte_perm(ax, ay, 0x7632) | 0x80008000u;          // high halves, sign set
+  const float2 d = __fadd2_rn(x, make_float2(-kGeluXMin, -kGeluXMin));  // < 0: left of the minimum
+  // branch bits: the signs of d at bits 0 and 16 (bytes 3 of d.x, d.y to bytes 0 and 2)
+  const uint32_t b = (__byte_perm(__float_as_uint(d.x), __float_as_uint(d.y), 0x0703) >> 7) & 0x00010001u;
+  const uint32_t neg = t + ((t ^ b) & 0x00010001u);
+  uint32_t m;  // 0xffff in each half whose x is negative (prmt sign replication of bytes 3 and 7)
+  asm("prmt.b32 %0, %1, %2, 0xffbb;" : "=r"(m) : "r"(__float_as_uint(x.x)), "r"(__float_as_uint(x.y)));
+  return (neg & m) | (rne & ~m);
+}
+// v <- act(v) (gelu, relu) and w[i/2] <- the bf16x2 words of the coded A (gelu:
+// branch-coded; relu: RNE). Same fp32 arithmetic as act_fwd.
+__device__ __forceinline__ void act_fwd_code32(int kind, float* v, uint32_t* w) {
+  if (kind == MOE_ACT_GELU_TANH) {
+    const float2 c0 = make_float2(0.7978845608028654f, 0.7978845608028654f);
+    const float2 c1 = make_float2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+    const float2 half = make_float2(0.5f, 0.5f);
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float2 x = make_float2(v[i], v[i + 1]);
+      const float2 x2 = __fmul2_rn(x, x);
+      const float2 u = __fmul2_rn(x, __ffma2_rn(c1, x2, c0));
+      const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+      const float2 hx = __fmul2_rn(half, x);
+      const float2 a = __ffma2_rn(hx, t, hx);
+      w[i / 2] = code_bf16x2(a, x);
+      v[i] = a.x;
+      v[i + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = kind == MOE_ACT_RELU ? fmaxf(v[i], 0.f) : v[i];
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) w[i / 2] = pack_bf16x2(v[i], v[i + 1]);
+  }
+}
+// Table indices of two coded keys (a bf16x2 word), branch-free: each key is
+// clamped to its sign's key range (negative keys keep their branch LSB at the
+// low end) and rebased; positive keys index [0, kActCodeNPos), negative keys
+// [kActCodeNPos, kActCodeN).
+__device__ __forceinline__ uint32_t act_code_idx2(uint32_t w) {
+  constexpr uint32_t P_LO = (uint32_t)kActCodeELo << 7, P_HI = ((uint32_t)kActCodeEHiPos << 7) | 0x7fu;
+  constexpr uint32_t N_LO = 0x8000u | P_LO, N_HI = 0x8000u | ((uint32_t)kActCodeEHiNeg << 7) | 0x7fu;
+  const uint32_t sm = (w >> 15) & 0x00010001u;                            // 1 per negative key
+  const uint32_t lo = (P_LO * 0x00010001u) | (sm << 15) | (w & sm);
+  const uint32_t hi = P_HI * 0x00010001u + sm * (N_HI - P_HI);
+  const uint32_t c = __vminu2(__vmaxu2(w, lo), hi);
+  const uint32_t base = P_LO * 0x00010001u + sm * (N_LO - (uint32_t)kActCodeNPos - P_LO);
+  return c - base;
+}
+// v *= act'(H) decoded from the 16 bf16x2 words w of coded A (32 values);
+// tab_smem: the fp32 decode table in shared memory.
+__device__ __forceinline__ void act_code_mul32(int kind, float* v, const uint32_t* w, uint32_t tab_smem) {
+  if (kind == MOE_ACT_GELU_TANH) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const uint32_t idx = act_code_idx2(w[i / 2]);
+      float g0, g1;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(g0) : "r"(tab_smem + 4 * (idx & 0xffffu)));
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(g1) : "r"(tab_smem + 4 * (idx >> 16)));
+      const float2 r = __fmul2_rn(make_float2(v[i], v[i + 1]), make_float2(g0, g1));
+      v[i] = r.x;
+      v[i + 1] = r.y;
+    }
+  } else if (kind == MOE_ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const uint32_t lo = w[i / 2] & 0xffffu, hi = w[i / 2] >> 16;
+      v[i] = (lo != 0u && lo < 0x8000u) ? v[i] : 0.f;
+      v[i + 1] = (hi != 0u && hi < 0x8000u) ? v[i + 1] : 0.f;
+    }
+  }
+}
+// the decode table (fp16 bits) in global memory; the SDD^T kernels expand it
+// to fp32 in shared memory (all threads, before the block's first barrier)
+static __device__ __align__(16) const uint16_t g_act_code_tab[kActCodeN] = MOE_ACT_CODE_TABLE_INIT;
+constexpr int ACT_CODE_BYTES = kActCodeN * 4;
+__device__ __forceinline__ void act_code_table_to_smem(uint8_t* dst, const uint16_t* src) {
+  float* d = reinterpret_cast<float*>(dst);
+  for (int i = threadIdx.x; i < kActCodeN; i += blockDim.x) d[i] = __half2float(__ushort_as_half(__ldg(src + i)));
+}
+
+// Raw 16 bf16x2 words of half `hh` of this thread's 128B-swizzled row.
+__device__ __forceinline__ void load_row_half128_raw(const uint8_t* buf, int lane, uint32_t* w, int hh) {
+  const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = 4 * hh + j;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[4 * j]), "=r"(w[4 * j + 1]), "=r"(w[4 * j + 2]), "=r"(w[4 * j + 3])
+                 : "r"(row + ((cj ^ (lane & 7)) << 4))
+                 : "memory");
+  }
+}
+// Raw 16 bf16x2 words of this thread's 64B-swizzled staging row.
+__device__ __forceinline__ void load_row_raw(const uint8_t* buf, int lane, uint32_t* w) {
+  const uint32_t row = smem_u32(buf) + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w[4 * j]), "=r"(w[4 * j + 1]), "=r"(w[4 * j + 2]), "=r"(w[4 * j + 3])
+                 : "r"(row + swz64(j, lane))
+                 : "memory");
+}
+// Stage 16 bf16x2 words (32 values) as half `hh` of a 128B-swizzled row / as a 64B-swizzled row.
+__device__ __forceinline__ void stage_row_half128_raw(uint8_t* buf, int lane, const uint32_t* w, int hh) {
+  const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cj = 4 * hh + j;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((cj ^ (lane & 7)) << 4)), "r"(w[4 * j]),
+                 "r"(w[4 * j + 1]), "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void stage_row_raw(uint8_t* buf, int lane, const uint32_t* w) {
+  const uint32_t row = smem_u32(buf) + lane * 64;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + swz64(j, lane)), "r"(w[4 * j]),
+                 "r"(w[4 * j + 1]), "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
+                 : "memory");
+}
+
 // v *= act'(h) over a 32-value chunk.
 __device__ __forceinline__ void act_grad_mul32(int kind, float* v, const float* h) {
   if (kind == MOE_ACT_GELU_TANH) {

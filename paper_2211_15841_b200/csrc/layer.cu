@@ -68,7 +68,9 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   MOE_CHECK_ARG(sv->logits && sv->expert_idx && sv->gates && sv->x_g && sv->a && sv->y_g,
                 "moe_forward: NULL saved tensor");
   const bool id = cfg->act == MOE_ACT_IDENTITY;
-  MOE_CHECK_ARG(id || sv->act_deriv, "moe_forward: saved->act_deriv required for a non-identity activation");
+  // saved->act_deriv == NULL: the branch-coded activation (R24; an option that
+  // saves the act'(H) buffer): only A is saved and the SDD^T decodes act'(H) from it
+  const bool coded = !id && !sv->act_deriv;
   // (1) indices, weights = router(x)
   // (2) topology = make_topology(indices)
   //     (one launch with the router where possible: moe_router_topology)
@@ -79,14 +81,20 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
   // (4) x = sdd(x, w1, topology) [+ act, act' saved]; x = dsd(x, w2)
   if (cfg->unpadded) {  // P:297 partial blocks at the fringe: X_g rows in expert order, no pad rows
     MOE_TRY(moe_sort_rows(cfg, x, &sv->topo, sv->x_g, stream));
-    MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
-                          stream));
-  } else if (moe_gather_is_fused(cfg)) {  // the gather happens inside the SDD's loads (tile::gather4)
+    if (coded)
+      MOE_TRY(moe_sdd_act_coded(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, stream));
+    else
+      MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
+                            id ? nullptr : sv->act_deriv, stream));
+  } else if (moe_gather_is_fused(cfg) && !coded) {  // the gather happens inside the SDD's loads (tile::gather4)
     MOE_TRY(moe_sdd_gather(cfg, x, w->w1, &sv->topo, cfg->act, sv->a, id ? nullptr : sv->act_deriv, sv->x_g, stream));
   } else {
     MOE_TRY(moe_gather(cfg, x, &sv->topo, sv->x_g, stream));
-    MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, id ? nullptr : sv->act_deriv,
-                          stream));
+    if (coded)
+      MOE_TRY(moe_sdd_act_coded(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, stream));
+    else
+      MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
+                            id ? nullptr : sv->act_deriv, stream));
   }
   // (5) x = padded_scatter(x, indices) * weights            P:279-280 (fused into the DSD for top-1)
   MOE_TRY(moe_dsd_scatter(cfg, sv->a, w->w2, &sv->topo, sv->gates, sv->y_g, y, stream));
@@ -156,7 +164,9 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
   // b2: SDD^T: dH = (dY_g . W2^T) * act'(H)                 "second layer data gradient"
   {
     const moe_status st =
-        moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream);
+        !id && !sv->act_deriv
+            ? moe_sdd_act_coded(cfg, dy_g, w->w2, 1, topo, cfg->act, sv->a, dh, stream)  // act'(H) from A (R24)
+            : moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream);
     set_gemm_sm_budget(0);
     MOE_TRY(st);
   }

@@ -206,3 +206,44 @@ int moe_device_sm_count(void) {
 }
 
 }  // extern "C"
+
+// Host decode of the branch-coded activation (reading R24): the same table and
+// index arithmetic as act_code_mul32 in gemm_util.cuh, for CPU tests.
+#include "act_code_table.h"
+namespace {
+const uint16_t kActCodeTableHost[moe::kActCodeN] = MOE_ACT_CODE_TABLE_INIT;
+float half_bits_to_float(uint16_t h) {
+  const uint32_t s = (uint32_t)(h >> 15) << 31, e = (h >> 10) & 0x1f, m = h & 0x3ff;
+  float f;
+  if (e == 0) {
+    f = ldexpf((float)m, -24);  // zero / subnormal
+    return s ? -f : f;
+  }
+  uint32_t bits = s | ((e == 31 ? 255u : e - 15 + 127) << 23) | (m << 13);
+  memcpy(&f, &bits, 4);
+  return f;
+}
+}  // namespace
+
+extern "C" moe_status moe_act_code_decode_host(int32_t act, const uint16_t* a_bits, float* out, int64_t n) {
+  if (!a_bits || !out || n < 0) return moe::set_error(MOE_EINVAL, "moe_act_code_decode_host: bad arguments");
+  if (act < 0 || act > 2) return moe::set_error(MOE_EINVAL, "moe_act_code_decode_host: bad act %d", act);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t u = a_bits[i];
+    if (act == MOE_ACT_IDENTITY) {
+      out[i] = 1.f;
+    } else if (act == MOE_ACT_RELU) {
+      out[i] = (u != 0u && u < 0x8000u) ? 1.f : 0.f;
+    } else {
+      // the key clamped to its sign's range (a negative key keeps its branch LSB), then rebased
+      const uint32_t p_lo = (uint32_t)moe::kActCodeELo << 7, p_hi = ((uint32_t)moe::kActCodeEHiPos << 7) | 0x7fu;
+      const uint32_t n_lo = 0x8000u | p_lo | (u & 1u), n_hi = 0x8000u | ((uint32_t)moe::kActCodeEHiNeg << 7) | 0x7fu;
+      const bool neg = u >> 15;
+      uint32_t c = u < (neg ? n_lo : p_lo) ? (neg ? n_lo : p_lo) : u;
+      if (c > (neg ? n_hi : p_hi)) c = neg ? n_hi : p_hi;
+      const uint32_t idx = neg ? c - (0x8000u | p_lo) + (uint32_t)moe::kActCodeNPos : c - p_lo;
+      out[i] = half_bits_to_float(kActCodeTableHost[idx]);
+    }
+  }
+  return MOE_OK;
+}

@@ -35,7 +35,7 @@ def main(out):
     cfg = A.make_config(T, h, E, k, f, act=shp.act)
     x, dy = inp["x"].to(dev), inp["dy"].to(dev)
     wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
-    saved = A.Saved.allocate(cfg, dev)
+    saved = A.Saved.allocate(cfg, dev, save_deriv=os.environ.get("MOE_BENCH_ACT_SAVE", "coded") == "deriv")
     ws = A.workspace(cfg, dev)
     t = {"x": x, "dy": dy, "wr": wr, "w1": w1, "w2": w2, "saved": saved, "ws": ws,
          "y": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
@@ -73,13 +73,16 @@ def main(out):
         epi = (a[..., 4] - a[..., 3])[valid & (a[..., 4] > 0)] / 1e3
         wait_acc = (a[..., 3] - a[..., 2])[valid & (a[..., 3] > 0)] / 1e3
         first = (a[:, 0, 1] - t0)[a[:, 0, 1] > 0] / 1e3
+        # per tile: the MMA of tile i+1 may start only once the epilogue of tile i-1 freed its accumulator
+        gap = (a[:, 1:, 1] - a[:, :-1, 2])[(a[:, 1:, 1] > 0) & (a[:, :-1, 2] > 0)] / 1e3
         last_end = (a[..., 4].max(axis=1) - t0) / 1e3
         ntile = valid.sum(axis=1)
         nm = gemm_names[li] if li < len(gemm_names) else "?"
         print(f"launch {li} ({nm}): span {span:.1f} us | tiles/CTA {ntile.min()}-{ntile.max()} | "
               f"mainloop/tile {mma.mean():.2f} us (max {mma.max():.2f}) | epilogue/tile {epi.mean():.2f} us | "
               f"commit->epi {wait_acc.mean():.2f} us | first MMA start {first.mean():.2f} us (max {first.max():.2f}) | "
-              f"CTA end min {last_end[last_end > 0].min():.1f} max {last_end.max():.1f}")
+              f"CTA end min {last_end[last_end > 0].min():.1f} max {last_end.max():.1f} | "
+              f"MMA idle between tiles {gap.mean() if gap.size else 0:.2f} us")
 
 
 if __name__ == "__main__":

@@ -105,3 +105,58 @@ def test_check_config_formulation_fields():
     cfg = _cfg(num_experts=64, hidden=512, ffn_hidden=2048)
     off = lib.moe_workspace_offset(ctypes.byref(cfg), 5)
     assert 0 < off and off + 4 * 65 <= api.moe_workspace_bytes(cfg)
+
+
+def _gelu_argmin(O):
+    """argmin of the oracle's gelu: the root of its act_grad on [-1.5, -0.3] (bisection)."""
+    lo, hi = -1.5, -0.3
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if O.act_grad(O.ACT_GELU, mid) < 0 else (lo, mid)
+    return 0.5 * (lo + hi)
+
+
+def _encode_r24(O, h):
+    """The branch code of moe.h / DESIGN R24, written from its description: A = gelu(h)
+    in fp32; h >= 0: RNE bf16; h < 0: sign set, the bf16 of A's magnitude whose
+    mantissa LSB = (h < argmin gelu) nearest to A."""
+    import numpy as np
+    a = O.act(O.ACT_GELU, h).astype(np.float32)
+    bits = a.view(np.uint32)
+    rne = ((bits + 0x7FFF + ((bits >> 16) & 1)) >> 16).astype(np.uint32)
+    trunc = (bits >> 16) | 0x8000
+    b = (h < _gelu_argmin(O)).astype(np.uint32)
+    neg = np.where((trunc & 1) == b, trunc, trunc + 1)
+    return np.where(h < 0, neg, rne).astype(np.uint16)
+
+
+def test_act_code_decode_matches_oracle_derivative():
+    """R24: act'(H) as the SDD^T decodes it from the branch-coded A (the
+    library's table, host copy) against the oracle's float64 act'(h), for h
+    over several scales; special cases exact; relu = (A > 0)."""
+    import numpy as np
+    from oracle import moe_oracle as O
+    from paper_2211_15841_b200 import api
+    rng = np.random.default_rng(7)
+    for sigma in (0.25, 1.0, 3.0):
+        h = rng.standard_normal(200_000) * sigma
+        got = api.moe_act_code_decode_host(api.ACT_GELU, _encode_r24(O, h)).astype(np.float64)
+        want = O.act_grad(O.ACT_GELU, h)
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel < 6e-3, (sigma, rel)          # bf16-storage level (act' itself in bf16: ~2e-3)
+        assert np.abs(got - want).max() < 0.03   # worst case: near gelu's minimum (act' ~ sqrt(A - A_min))
+    # exact special cases: act'(0) = 1/2, act' = 1 for large h, ~0 far left of the minimum
+    h = np.array([0.0, 8.0, 20.0, 1e4, -12.0, -40.0])
+    got = api.moe_act_code_decode_host(api.ACT_GELU, _encode_r24(O, h))
+    np.testing.assert_allclose(got[:4], [0.5, 1.0, 1.0, 1.0], atol=1e-3)
+    assert np.abs(got[4:]).max() < 2e-3
+    # each branch of a negative A decodes to its own side of the minimum
+    xm = _gelu_argmin(O)
+    h = np.array([xm + 0.3, xm - 0.3, xm + 0.05, xm - 0.05])
+    got = api.moe_act_code_decode_host(api.ACT_GELU, _encode_r24(O, h))
+    assert got[0] > 0.05 and got[1] < -0.05 and got[2] > 0 and got[3] < 0
+    # relu: act' = A > 0 on plain RNE bf16 of relu(h)
+    h = rng.standard_normal(1000)
+    a = np.maximum(h, 0).astype(np.float32).view(np.uint32)
+    got = api.moe_act_code_decode_host(api.ACT_RELU, ((a + 0x7FFF + ((a >> 16) & 1)) >> 16).astype(np.uint16))
+    np.testing.assert_array_equal(got, (h > 0).astype(np.float32))

@@ -40,6 +40,15 @@ def f64(t):
     return t.detach().float().cpu().double().numpy()
 
 
+def gelu_argmin():
+    """argmin of the oracle's gelu (root of its act_grad, bisection): the branch point of R24."""
+    lo, hi = -1.5, -0.3
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if O.act_grad(O.ACT_GELU, mid) < 0 else (lo, mid)
+    return 0.5 * (lo + hi)
+
+
 def oracle_plan_topo(idx_np, E, f):
     plan = O.make_plan(idx_np, E, 128)
     return plan, O.make_topology_closed_form(plan, 128, f)
@@ -484,6 +493,25 @@ def test_six_products(case, sdd_form, monkeypatch):
     assert np.isin(gr, (0.0, 1.0)).all()
     clear = np.abs(H) > 1e-3 * np.sqrt((H ** 2).mean())
     np.testing.assert_array_equal(gr[clear], (H[clear] > 0).astype(np.float64))
+    # the layer's default form (reading R24): the forward saves only the
+    # branch-coded A; the SDD^T decodes act'(H) from it
+    a_c = A.moe_sdd_act_coded(cfg, xg, w1.to(d), 0, tg, act=A.ACT_GELU)
+    assert_close("coded A", f64(a_c[:nnz]).reshape(-1, 128), Aact.reshape(-1, 128), per="block")
+    bits = a_c[:nnz].cpu().view(torch.int16).numpy().view(np.uint16)
+    xm = gelu_argmin()
+    scale = np.sqrt((H ** 2).mean())
+    clear = (np.abs(H) > 1e-3 * scale) & (np.abs(H - xm) > 1e-3 * scale)   # decisions clear of the fp32 rounding
+    np.testing.assert_array_equal((bits >> 15)[clear], (H[clear] < 0).astype(np.uint16))
+    negc = clear & (H < 0)
+    np.testing.assert_array_equal((bits & 1)[negc], (H[negc] < xm).astype(np.uint16))
+    dh_c = A.moe_sdd_act_coded(cfg, dyg.to(d), w2.to(d), 1, tg, act=A.ACT_GELU, coded_src=a_c)
+    assert_close("dH from coded A", f64(dh_c[:nnz]).reshape(-1, 128),
+                 (dA * O.act_grad(O.ACT_GELU, H)).reshape(-1, 128), per="block")
+    a_rc = A.moe_sdd_act_coded(cfg, xg, w1.to(d), 0, tg, act=A.ACT_RELU)
+    assert_close("relu A", f64(a_rc[:nnz]).reshape(-1, 128), O.act(O.ACT_RELU, H).reshape(-1, 128), per="block")
+    dh_rc = A.moe_sdd_act_coded(cfg, dyg.to(d), w2.to(d), 1, tg, act=A.ACT_RELU, coded_src=a_rc)
+    assert_close("relu dH from A", f64(dh_rc[:nnz]).reshape(-1, 128),
+                 (dA * O.act_grad(O.ACT_RELU, H)).reshape(-1, 128), per="block")
     # DS^TD: dW2 = A^T . dY_g
     dw2 = A.moe_dsd(cfg, a_in, 1, dyg.to(d), 0, tg)
     want_dw2 = O.dsd(a_in64, S.to_f64(dyg[:Tp]), topo, trans_s=True)
@@ -598,6 +626,33 @@ def test_layer_forward_backward(name, T, k, shp, unpadded):
     assert_layer_close(y, dx, dwr, dw1, dw2, yo, go)
     plan = cache.plan
     check_topology_exact(A, saved.topo, plan, O.make_topology_closed_form(plan, 128, shp.ffn), T * shp.top_k)
+
+
+@pytest.mark.parametrize("sdd_form", ["auto", "0"])
+@pytest.mark.parametrize("name,T,k,shp", [c for c in LAYER_CASES if c[0] in ("C0", "C1-reduced", "C4-reduced",
+                                                                             "C0-relu")]
+                         + [("C1-full", 32768, 1, S.CONFIGS["C1"])])
+def test_layer_coded_activation(name, T, k, shp, sdd_form, monkeypatch):
+    """The memory-saving form (R24, moe_saved.act_deriv = NULL): the forward
+    saves only the branch-coded A and the SDD^T decodes act'(H) from it; the
+    layer's outputs and gradients against the oracle (CTA-pair / 1-SM SDD)."""
+    if sdd_form == "auto":
+        monkeypatch.delenv("MOE_SDD_PAIR", raising=False)
+    else:
+        monkeypatch.setenv("MOE_SDD_PAIR", sdd_form)
+    d = dev()
+    A = api()
+    inp = S.make_inputs(shp, seed=5, tokens=T)
+    cfg = A.make_config(T, shp.hidden, shp.experts, shp.top_k, shp.ffn, act=shp.act)
+    xd = inp["x"].to(d)
+    wr, w1, w2 = (inp[n].to(d) for n in ("wr", "w1", "w2"))
+    saved = A.Saved.allocate(cfg, d, save_deriv=False)
+    assert saved.act_deriv is None
+    y, saved = A.moe_forward(cfg, wr, w1, w2, xd, saved=saved)
+    dx, (dwr, dw1, dw2) = A.moe_backward(cfg, wr, w1, w2, saved, xd, inp["dy"].to(d))
+    torch.cuda.synchronize()
+    yo, cache, go, flips = oracle_layer(inp, shp, T, got_idx=saved.expert_idx.cpu().numpy())
+    assert_layer_close(y, dx, dwr, dw1, dw2, yo, go)
 
 
 def test_layer_deterministic():
