@@ -1289,6 +1289,16 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
     MOE_TRY(make_tmap_bf16(&L.tb, b, h, N, h, BK, pair ? 128 : L.bn, "moe_sdd b^T", KSW));
   const bool wide = pair && (act_src ? gemm2_wide_h() : pair_wide());
   L.p.wide = wide ? 1 : 0;
+  {
+    // an expert's lone last block-row as an M = 128 CTA-pair tile instead of a
+    // half-empty 256-row pair (the 4 KB-box epilogues; MOE_SDD_HALF=0: off)
+    static int half_env = -1;
+    if (half_env < 0) {
+      const char* e = getenv("MOE_SDD_HALF");
+      half_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    L.p.sdd_half = pair && half_env && (act_src ? gemm2_h_ring() : wide) ? 1 : 0;
+  }
   auto epi_map = wide ? make_tmap_epi_wide : make_tmap_epi;
   MOE_TRY(epi_map(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   set_epi_out(L.p, 0, out_s, nnz * 128, 128);

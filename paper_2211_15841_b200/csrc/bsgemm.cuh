@@ -79,6 +79,7 @@ struct GemmParams {
   __nv_bfloat16* out_d;
   long long ldc, ldd, rows_c, rows_d;
   int direct;
+  int sdd_half;  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)
   unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
   int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
@@ -147,6 +148,7 @@ __device__ __forceinline__ void trace_ev(const GemmParams& p, int tile_i, int ev
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream);
 bool gemm2_wide_h();   // the CTA-pair SDD^T takes 64 x 32 (4 KB) act'(H) / dH maps (else 32 x 32)
 bool gemm2_h_coded();  // the CTA-pair SDD^T can decode the coded activation (R24)
+bool gemm2_h_ring();   // the CTA-pair SDD^T runs the act'(H) ring epilogue (half pairs supported)
 GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo);
 
 }  // namespace moe

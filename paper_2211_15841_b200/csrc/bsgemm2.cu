@@ -178,6 +178,18 @@ __device__ __forceinline__ void out_coords2(const GemmParams& p, int mode, const
   }
 }
 
+// SDD half pair (p.sdd_half, an expert's lone last block-row r0): one M = 128
+// cta_group::2 MMA, each CTA holding 64 of its rows; TMEM lanes 0-63 hold the
+// CTA's rows x tile columns 0-127, lanes 64-127 the same rows x columns
+// 128-255. TMA store coordinates of 32-column TMEM chunk c (0..3) of lane
+// quarter q.
+__device__ __forceinline__ void out_coords2_half(const GemmParams& p, const Tile2& t, int rank, int c, int q, int F,
+                                                 int& x, int& y) {
+  const int blk = t.r0 * F + (t.c0 % F) + (q >> 1);
+  x = c * EPI_COLS;
+  y = blk * BM + rank * 64 + (q & 1) * 32;
+}
+
 template <int MODE, bool A_MN, bool B_MN, bool EPI_H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     bsgemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -290,9 +302,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       int idx_a = 0, idx_b = 0, idx_c = 0;
       // SDD: first dense row of this CTA's block-row (unpadded layout: brow_start; a
       // missing second row of a half-empty pair loads the first row's, stores nothing)
-      const int sdd_row = MODE == SDD ? (p.unpadded ? __ldg(p.brow_start + t.r0 + ((rank && t.second) ? 1 : 0))
-                                                    : (t.r0 + rank) * BM)
-                                      : 0;
+      // half pair (p.sdd_half): both CTAs load the lone block-row, CTA 1 from its 64th row
+      const bool hm = MODE == SDD && p.sdd_half && !t.second;
+      const int sdd_row = MODE != SDD ? 0
+                          : hm        ? (p.unpadded ? __ldg(p.brow_start + t.r0) : t.r0 * BM) + rank * 64
+                          : (p.unpadded ? __ldg(p.brow_start + t.r0 + ((rank && t.second) ? 1 : 0)) : (t.r0 + rank) * BM);
       for (int kit = 0; kit < t.kiters; ++kit) {
         const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
@@ -388,7 +402,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   } else if (warp == P_MMA_WARP) {
     // ===================== MMA issuer (leader CTA, one thread) =====================
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, P_BN, A_MN, B_MN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(2 * BM, P_BN, A_MN, B_MN);
+      constexpr uint32_t idesc_half = make_idesc_bf16(BM, P_BN, A_MN, B_MN);  // SDD half pair: M = 128
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -398,6 +413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         const Tile2 t = decode2(p, MODE, tile, 0);
         ++tile_i;
         if (t.kiters == 0) continue;
+        const uint32_t idesc = (MODE == SDD && p.sdd_half && !t.second) ? idesc_half : idesc_full;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         trace_ev(p, tile_i, 1);
@@ -476,9 +492,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     auto load_hw = [&](int j) {  // lane 0
       if (j >= hw_end) return;
       const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank);
-      if (!(rank == 0 || tj.second)) return;  // nothing stored for this CTA's half: nothing loaded
+      const bool hmj = MODE == SDD && p.sdd_half && !tj.second;
+      const int scj = half + (j % SPW) * EPG;
+      if (hmj ? HSUB * scj >= 4 : !(rank == 0 || tj.second)) return;  // nothing stored here: nothing loaded
       int x, y;
-      out_coords2(p, MODE, tj, rank, HSUB * (half + (j % SPW) * EPG), row0, p.F, x, y);
+      if (hmj)
+        out_coords2_half(p, tj, rank, HSUB * scj, q, p.F, x, y);
+      else
+        out_coords2(p, MODE, tj, rank, HSUB * scj, row0, p.F, x, y);
       const int b = j % C::NHW;
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&hb[b], C::HBOX);
@@ -492,9 +513,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       const Tile2 t = decode2(p, MODE, tile, rank);
       ++tile_i;
       const bool has_acc = t.kiters > 0;
-      const bool mine = rank == 0 || t.second;  // does this CTA own real output rows?
+      // SDD half pair (an expert's lone last block-row, p.sdd_half): both CTAs own 64 of its rows
+      const bool hm = MODE == SDD && p.sdd_half && !t.second;
+      const bool mine = rank == 0 || t.second || hm;  // does this CTA own real output rows?
       // unpadded layout: this lane's row of the CTA's SDD block-row is the fringe: zeros
-      const bool fringe = MODE == SDD && p.unpadded && mine && row0 + lane >= __ldg(p.brow_rows + t.r0 + rank);
+      const bool fringe =
+          MODE == SDD && p.unpadded && mine &&
+          (hm ? rank * 64 + (q & 1) * 32 + lane >= __ldg(p.brow_rows + t.r0)
+              : row0 + lane >= __ldg(p.brow_rows + t.r0 + rank));
       if (EPI_H && !C::WIDE_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
       if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
@@ -515,8 +541,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 #pragma unroll 1
         for (int s = 0; s < SPW; ++s, ++hw_seq) {
           const int b = hw_seq % C::NHW;
-          if (mine) {
-            const int sc = half + s * EPG;
+          const int sc = half + s * EPG;
+          if (mine && !(hm && HSUB * sc >= 4)) {  // a half pair holds TMEM columns 0-127 only
             mbar_wait(&hb[b], (hw_phase >> b) & 1u);
             hw_phase ^= 1u << b;
             uint8_t* slot = hst + b * C::HBOX;
@@ -553,7 +579,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             __syncwarp();
             if (lane == 0) {
               int x, y;
-              out_coords2(p, MODE, t, rank, HSUB * sc, row0, p.F, x, y);
+              if (hm)
+                out_coords2_half(p, t, rank, HSUB * sc, q, p.F, x, y);
+              else
+                out_coords2(p, MODE, t, rank, HSUB * sc, row0, p.F, x, y);
               if (!(p.dbg & 16)) tma_store_2d(&tmap_c, slot, x, y);
               bulk_commit();
             }
@@ -576,7 +605,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // super-chunk waits only for the store issued two super-chunks ago
         const bool alt = p.epi == EPI_ACT_FWD && p.act_code;
 #pragma unroll 1
-        for (int sc = half; sc < P_BN / 64; sc += EPG) {
+        for (int sc = half; sc < (hm ? 2 : P_BN / 64); sc += EPG) {  // a half pair: TMEM columns 0-127
+          // both 32-column TMEM loads of the super-chunk in flight while this
+          // warp waits for its staging buffers
+          uint32_t r[2][32];
+          if (has_acc) {
+            tmem_ld32(taddr + (2 * sc) * EPI_COLS, r[0]);
+            tmem_ld32(taddr + (2 * sc + 1) * EPI_COLS, r[1]);
+          }
           uint8_t* bc = bufc;
           if (alt) {
             if (lane == 0) bulk_wait_read<1>();
@@ -586,16 +622,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             bulk_wait_read<0>();  // the previous super-chunk's stores have read both buffers
           }
           __syncwarp();
+          if (has_acc) tmem_ld_wait();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            float v[32];
-            if (has_acc) {
-              uint32_t r[32];
-              tmem_ld32(taddr + (2 * sc + hh) * EPI_COLS, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = fringe ? 0.f : __uint_as_float(r[i]);
-            } else {
+            float* v = reinterpret_cast<float*>(r[hh]);
+            if (!has_acc || (p.unpadded && fringe)) {  // no accumulator / the fringe rows: zeros
 #pragma unroll
               for (int i = 0; i < 32; ++i) v[i] = 0.f;
             }
@@ -608,8 +639,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             if (p.epi == EPI_ACT_FWD) {
               if (p.has_pre && p.aux_deriv) {
                 float g[32];
-                act_fwd_deriv32(p.act, v, g);
-                if (fringe) {
+                act_fwd_deriv32((p.dbg & 4) ? MOE_ACT_IDENTITY : p.act, v, g);
+                if (p.unpadded && fringe) {
 #pragma unroll
                   for (int i = 0; i < 32; ++i) g[i] = 0.f;
                 }
@@ -619,13 +650,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                 act_fwd32(p.act, v);
               }
             }
-            stage_row_half128(bufc, lane, v, hh);
+            stage_row_half128(bc, lane, v, hh);
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             int x, y;
-            out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
+            if (hm)
+              out_coords2_half(p, t, rank, 2 * sc, q, p.F, x, y);
+            else
+              out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
             if (!(p.dbg & 16)) tma_store_2d(&tmap_c, bc, x, y);
             if (two && !(p.dbg & 16)) tma_store_2d(&tmap_d, bufd, x, y);
             bulk_commit();
@@ -750,6 +784,7 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
 
 bool gemm2_wide_h() { return Cfg2<true, SDD>::WIDE_H && Cfg2<true, SDD>::HC == 64; }
 bool gemm2_h_coded() { return Cfg2<true, SDD>::HAS_TAB; }
+bool gemm2_h_ring() { return Cfg2<true, SDD>::WIDE_H; }
 
 moe_status gemm2_launch(const GemmLaunch& L, cudaStream_t stream) {
   MOE_GEMM2_CASE(SDD, false, true, false)      // SDD      X_g . W1 (+act, +pre)
