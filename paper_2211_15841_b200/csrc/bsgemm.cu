@@ -1298,6 +1298,12 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
       half_env = (e && e[0] == '0') ? 0 : 1;
     }
     L.p.sdd_half = pair && half_env && (act_src ? gemm2_h_ring() : wide) ? 1 : 0;
+    static int alt_env = -1;
+    if (alt_env < 0) {
+      const char* e = getenv("MOE_PAIR_EPI_ALT");
+      alt_env = (e && e[0] == '1') ? 1 : 0;
+    }
+    L.p.epi_alt = pair && wide && !act_src && alt_env ? 1 : 0;
   }
   auto epi_map = wide ? make_tmap_epi_wide : make_tmap_epi;
   MOE_TRY(epi_map(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));

@@ -79,7 +79,8 @@ struct GemmParams {
   __nv_bfloat16* out_d;
   long long ldc, ldd, rows_c, rows_d;
   int direct;
-  int sdd_half;  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
+  int sdd_half;
+  int epi_alt;   // CTA-pair forward SDD (4 KB boxes): two epilogue warp groups drain alternate tiles  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)
   unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
   int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
@@ -130,7 +131,7 @@ int gemm_dbg();
 // Timeline tracing of the GEMM engine (debug only, env MOE_GEMM_TRACE=1):
 // slot [launch][cta][tile][event], events: 0 producer first load, 1 MMA start,
 // 2 MMA last commit, 3 epilogue got accumulator, 4 epilogue done.
-constexpr int kTraceLaunches = 16, kTraceCtas = 160, kTraceTiles = 32, kTraceEvents = 5;
+constexpr int kTraceLaunches = 16, kTraceCtas = 160, kTraceTiles = 32, kTraceEvents = 14;
 unsigned long long* gemm_trace_slot();
 
 #ifdef __CUDACC__

@@ -219,6 +219,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   const int rank = (int)cluster_ctarank();
   const bool leader = rank == 0;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) trace_ev(p, 0, 13);  // kernel entry (trace slot tile 0, event 13)
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -227,7 +228,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2 * NUM_EPI_WARPS);
+      // epi_alt: each accumulator is drained by one group of NUM_EPI_WARPS / 2 warps per CTA
+      mbar_init(&tempty[i], (C::WIDE && p.epi_alt) ? NUM_EPI_WARPS : 2 * NUM_EPI_WARPS);
     }
     for (int i = 0; i < C::NHB * NUM_EPI_WARPS; ++i) mbar_init(&hbar[i], 1);
     fence_barrier_init();
@@ -296,6 +298,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       la_decode();
       for (int i = 0; i < TD; ++i) la_issue();
     }
+#ifndef MOE_PAIR_SDD_LANE0
+#define MOE_PAIR_SDD_LANE0 1
+#endif
+    // SDD (no index walk): one thread per producer warp runs the whole loop, so the
+    // other 31 lanes leave the sub-partition's issue slots to the epilogue warps
+    // sharing it
+    if (MODE == SDD && MOE_PAIR_SDD_LANE0 && !gat) {
+      if (lane == 0) {
+        for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
+          const Tile2 t = decode2(p, MODE, tile, rank);
+          trace_ev(p, tile_i, 0);
+          const bool hm = p.sdd_half && !t.second;
+          const int sdd_row = hm ? (p.unpadded ? __ldg(p.brow_start + t.r0) : t.r0 * BM) + rank * 64
+                                 : (p.unpadded ? __ldg(p.brow_start + t.r0 + ((rank && t.second) ? 1 : 0))
+                                               : (t.r0 + rank) * BM);
+          for (int kit = 0; kit < t.kiters; ++kit) {
+            if (stage % P_NP == warp) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sa = smem_a + stage * P_A_BYTES;
+              uint8_t* sb = smem_b + stage * P_B_BYTES;
+              uint64_t* fb = &full[stage];
+              if (p.dbg & 8) {
+                if (leader) mbar_arrive(fb);
+              } else {
+                if (leader) mbar_arrive_expect_tx(fb, 2 * P_STAGE);
+                const int k0 = kit * BK;
+                tma_load_2d_pair(sa, &tmap_a, fb, k0, sdd_row);
+                if (B_MN)
+                  tma_load_3d_pair(sb, &tmap_b, fb, 0, k0, (t.c0 + rank) * 2);
+                else
+                  tma_load_2d_pair(sb, &tmap_b, fb, k0, (t.c0 + rank) * 128);
+              }
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    } else
     for (int tile = cid; tile < ntiles && !idle; tile += ncl, ++tile_i) {
       const Tile2 t = decode2(p, MODE, tile, rank);
       if (lane == 0) trace_ev(p, tile_i, 0);
@@ -509,9 +552,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       for (int j = 0; j < C::NHW - 1; ++j) load_hw(j);
 
     int tile_i = -1;
+    // epi_alt (forward SDD, 4 KB boxes): warp group `half` drains accumulator
+    // `half`, i.e. every other tile, all of its columns; the two groups work on
+    // consecutive tiles at different phases instead of splitting each tile
+    const bool ealt = C::WIDE && p.epi_alt && p.wide;
+    uint32_t aphase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
       const Tile2 t = decode2(p, MODE, tile, rank);
       ++tile_i;
+      if (ealt && (tile_i & 1) != half) continue;  // the other group's tile
+      const int acc_t = ealt ? half : acc;
+      const uint32_t ph_t = ealt ? aphase : acc_phase;
       const bool has_acc = t.kiters > 0;
       // SDD half pair (an expert's lone last block-row, p.sdd_half): both CTAs own 64 of its rows
       const bool hm = MODE == SDD && p.sdd_half && !t.second;
@@ -523,11 +574,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
               : row0 + lane >= __ldg(p.brow_rows + t.r0 + rank));
       if (EPI_H && !C::WIDE_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
       if (has_acc) {
-        mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait(&tfull[acc_t], ph_t);
         tc_fence_after();
       }
       if (wq == 0 && lane == 0) trace_ev(p, tile_i, 3);
-      const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc * P_BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)row0 << 16) + acc_t * P_BN;
       if (p.dbg & 1) {
         if (has_acc) {
           uint32_t r[32];
@@ -605,7 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // super-chunk waits only for the store issued two super-chunks ago
         const bool alt = p.epi == EPI_ACT_FWD && p.act_code;
 #pragma unroll 1
-        for (int sc = half; sc < (hm ? 2 : P_BN / 64); sc += EPG) {  // a half pair: TMEM columns 0-127
+        for (int sc = ealt ? 0 : half; sc < (hm ? 2 : P_BN / 64); sc += ealt ? 1 : EPG) {  // a half pair: TMEM columns 0-127
           // both 32-column TMEM loads of the super-chunk in flight while this
           // warp waits for its staging buffers
           uint32_t r[2][32];
@@ -736,11 +787,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       if (has_acc) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_leader(&tempty[acc]);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (lane == 0) mbar_arrive_leader(&tempty[acc_t]);
+        if (ealt) {
+          aphase ^= 1;
+        } else {
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
       }
       if (wq == 0 && lane == 0) trace_ev(p, tile_i, 4);
+      if (lane == 0 && wq < 8) trace_ev(p, tile_i, 5 + wq);  // each epilogue warp's finish
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -751,6 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     tc_fence_after();
     tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
   }
+  if (threadIdx.x == 0) trace_ev(p, 1, 13);  // kernel exit (trace slot tile 1, event 13)
 }
 
 template <int MODE, bool A_MN, bool B_MN, bool EPI_H>

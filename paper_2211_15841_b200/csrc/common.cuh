@@ -23,9 +23,15 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif
 bool pdl_enabled();
+// MOE_CARVEOUT=1 (experiment): every kernel of the library prefers the maximum
+// shared-memory carveout, so consecutive kernels never re-partition L1 / shared
+// memory between launches. Measured: the GEMMs unchanged, the permutation
+// kernels slower (less L1), so off by default. Set once per kernel and device.
+void prefer_max_smem(const void* kern);
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  prefer_max_smem(reinterpret_cast<const void*>(kern));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

@@ -22,6 +22,30 @@ bool pdl_enabled() {
 }
 
 
+void prefer_max_smem(const void* kern) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MOE_CARVEOUT");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!on) return;
+  // per thread: (kernel, device) pairs already set (a few dozen kernels)
+  thread_local const void* done_k[256];
+  thread_local int done_d[256];
+  thread_local int n_done = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  for (int i = 0; i < n_done; ++i)
+    if (done_k[i] == kern && done_d[i] == dev) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  cudaGetLastError();
+  if (n_done < 256) {
+    done_k[n_done] = kern;
+    done_d[n_done] = dev;
+    ++n_done;
+  }
+}
+
 static thread_local char g_err[512] = "";
 static thread_local int g_launches = 0;
 static std::atomic<long long> g_total_launches{0};

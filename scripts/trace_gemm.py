@@ -19,7 +19,7 @@ os.environ.setdefault("MOE_GEMM_TRACE", "1")
 
 import bench  # noqa: E402
 
-L, C, TT, EV = 16, 160, 32, 5
+L, C, TT, EV = 16, 160, 32, 14
 
 
 def main(out):
@@ -35,7 +35,7 @@ def main(out):
     cfg = A.make_config(T, h, E, k, f, act=shp.act)
     x, dy = inp["x"].to(dev), inp["dy"].to(dev)
     wr, w1, w2 = (inp[n].to(dev) for n in ("wr", "w1", "w2"))
-    saved = A.Saved.allocate(cfg, dev, save_deriv=os.environ.get("MOE_BENCH_ACT_SAVE", "coded") == "deriv")
+    saved = A.Saved.allocate(cfg, dev, save_deriv=os.environ.get("MOE_BENCH_ACT_SAVE", "deriv") == "deriv")
     ws = A.workspace(cfg, dev)
     t = {"x": x, "dy": dy, "wr": wr, "w1": w1, "w2": w2, "saved": saved, "ws": ws,
          "y": torch.empty(T, h, dtype=torch.bfloat16, device=dev),
@@ -78,6 +78,26 @@ def main(out):
         last_end = (a[..., 4].max(axis=1) - t0) / 1e3
         ntile = valid.sum(axis=1)
         nm = gemm_names[li] if li < len(gemm_names) else "?"
+        ent, ext = a[:, 0, 13], a[:, 1, 13]
+        if (ent > 0).any():
+            e0 = ent[ent > 0].min()
+            first_ev = a[:, :, 0:13]
+            fe = np.where(first_ev > 0, first_ev, np.inf).min(axis=(1, 2))
+            print(f"   kernel entry spread {(ent[ent > 0].max() - e0) / 1e3:.2f} us | entry -> first tile event "
+                  f"{np.mean((fe - ent)[(ent > 0) & np.isfinite(fe)]) / 1e3:.2f} us | last exit "
+                  f"{(ext.max() - e0) / 1e3:.2f} us after the first entry | last tile event -> exit "
+                  f"{np.mean((ext - a[:, :, 0:13].max(axis=(1, 2)))[ext > 0]) / 1e3:.2f} us")
+        wend = a[..., 5:13]
+        if (wend > 0).any():
+            # CTA pairs (leader 2c, peer 2c+1): each epilogue warp's finish after the leader's accumulator-ready
+            lead, peer = a[0::2], a[1::2]
+            nt_ = min(lead.shape[0], peer.shape[0])
+            r0 = lead[:nt_, :, 3:4]
+            for nm_, src in (("leader", lead[:nt_, :, 5:13]), ("peer", peer[:nt_, :, 5:13])):
+                ok = (src > 0) & (r0 > 0)
+                rel = src - r0
+                print(f"   epilogue warp done (us after acc ready), {nm_}:",
+                      " ".join(f"{rel[..., w][ok[..., w]].mean() / 1e3:.2f}" for w in range(8)))
         print(f"launch {li} ({nm}): span {span:.1f} us | tiles/CTA {ntile.min()}-{ntile.max()} | "
               f"mainloop/tile {mma.mean():.2f} us (max {mma.max():.2f}) | epilogue/tile {epi.mean():.2f} us | "
               f"commit->epi {wait_acc.mean():.2f} us | first MMA start {first.mean():.2f} us (max {first.max():.2f}) | "
