@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
         const int oblk = __shfl_sync(0xffffffffu, idx_b, blk & 31);
         const int odrow = __shfl_sync(0xffffffffu, idx_c, blk & 31);
         const bool mine = stage % C::NP == warp;
-        if (mine) mbar_wait(&empty[stage], phase ^ 1);
+        if (mine) mbar_wait_sleep(&empty[stage], phase ^ 1);
         if (mine && MODE == DSD_ROW && kit >= t.s) {
           // appended dense K-steps (dsdT + router dx): A = dlogits rows of the
           // tile's tokens, gathered 4 rows per lane (tile::gather4; pad rows are
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
         addend_prefetch(tile + (int)gridDim.x, pre_next);
       }
       if (has_acc) {
-        mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait_sleep(&tfull[acc], acc_phase);
         tc_fence_after();
       }
       if (wq == 0 && lane == 0) trace_ev(p, tile_i, 3);

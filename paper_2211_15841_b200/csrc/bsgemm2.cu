@@ -315,7 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
                                                : (t.r0 + rank) * BM);
           for (int kit = 0; kit < t.kiters; ++kit) {
             if (stage % P_NP == warp) {
-              mbar_wait(&empty[stage], phase ^ 1);
+              mbar_wait_sleep(&empty[stage], phase ^ 1);
               uint8_t* sa = smem_a + stage * P_A_BYTES;
               uint8_t* sb = smem_b + stage * P_B_BYTES;
               uint64_t* fb = &full[stage];
@@ -380,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           ++g_step;
         }
         const bool mine = gat || stage % P_NP == warp;
-        if (mine) mbar_wait(&empty[stage], phase ^ 1);
+        if (mine) mbar_wait_sleep(&empty[stage], phase ^ 1);
         if (gat) {
           // A = X_g^T: 64 gathered K-rows x this CTA's 128 h-columns (two 64-wide
           // MN chunks); lane l: chunk l / 16, rows 4 (l % 16) .. +3
@@ -574,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
               : row0 + lane >= __ldg(p.brow_rows + t.r0 + rank));
       if (EPI_H && !C::WIDE_H && p.epi == EPI_ACT_BWD && mine) load_h(t, half, hslot);
       if (has_acc) {
-        mbar_wait(&tfull[acc_t], ph_t);
+        mbar_wait_sleep(&tfull[acc_t], ph_t);
         tc_fence_after();
       }
       if (wq == 0 && lane == 0) trace_ev(p, tile_i, 3);

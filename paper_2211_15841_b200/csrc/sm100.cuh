@@ -65,6 +65,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// Wait with optional back-off for threads that are far ahead of the barrier
+// (TMA producers waiting for a free stage, epilogue warps waiting for an
+// accumulator): -DMOE_WAIT_SLEEP_NS=n sleeps n ns after each failed probe.
+// ncu counts the producers' try_wait spins at ~1/4 of the instructions the
+// CTA-pair SDD issues, but back-off of 64 / 256 ns measured neutral (the spin
+// loop's YIELD already gives the issue slot away), so 0 by default.
+#ifndef MOE_WAIT_SLEEP_NS
+#define MOE_WAIT_SLEEP_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+#if MOE_WAIT_SLEEP_NS > 0
+    __nanosleep(MOE_WAIT_SLEEP_NS);
+#endif
+  }
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
