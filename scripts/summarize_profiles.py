@@ -18,7 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = {  # bsgemm template -> step name (launch order within one layer step)
     "bsgemm_kernel<5, 0, 1, 64": "router", "bsgemm_kernel<0, 0, 1, 256, 0": "sdd", "bsgemm2_kernel<0, 0, 1": "sdd",
-    "bsgemm_kernel<1, 0, 1, 256": "dsd+scatter", "bsgemm_kernel<0, 0, 0, 256, 1": "sddT",
+    "bsgemm_kernel<1, 0, 1, 256": "dsd+scatter", "bsgemm_kernel<0, 0, 0, 256, 1": "sddT", "bsgemm2_kernel<0, 0, 0, 1": "sddT",
     "bsgemm2_kernel<2, 1, 1": "dsTd", "bsgemm2_kernel<3, 1, 1": "ddTs",
     "bsgemm_kernel<5, 1, 1, 64": "router_dwr", "bsgemm_kernel<5, 0, 0, 128": "router_dx",
     "bsgemm_kernel<1, 0, 0, 256": "dsdT+dx",
