@@ -306,6 +306,18 @@ moe_status moe_ep_exchange_counts(const moe_ep_t* ep, const int32_t* counts_loca
 moe_status moe_ep_dispatch_padded(const moe_ep_t* ep, int region, const void* x, const int32_t* sorted_pos,
                                   int top_k, void* stream);
 moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* rows_padded, void* stream);
+/* The combine fused into the expert side's DSD (P:399 overlap):
+ * moe_ep_combine_dest writes, for each of this rank's padded rows p <
+ * max_rows, the DEVICE address moe_ep_combine_padded would copy row p to (its
+ * source's return region `region` at the row's sorted position, through the
+ * peer mapping), 0 for pad rows and rows past the plan's padded count;
+ * dest [max_rows] uint64 device. moe_dsd_rows then stores each output row
+ * straight to dest[p] (over NVLink for remote sources), and moe_ep_signal
+ * publishes the region's completion to every peer (one CTA: a system-scope
+ * release after the stream-ordered stores), as the copy kernel's last CTA
+ * does; moe_ep_wait on the receivers is unchanged. */
+moe_status moe_ep_combine_dest(const moe_ep_t* ep, int region, uint64_t* dest, int64_t max_rows, void* stream);
+moe_status moe_ep_signal(const moe_ep_t* ep, int region, void* stream);
 int moe_ep_plan_offset(int nranks, int num_experts, int which);
 
 /* Topology (P:235-242 hybrid blocked-CSR-COO, P:290 transpose indices, P:297
@@ -390,6 +402,13 @@ moe_status moe_sdd_act_coded(const moe_config* cfg, const void* a, const void* b
 moe_status moe_act_code_decode_host(int32_t act, const uint16_t* a_bits, float* out, int64_t n);
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream);
+/* moe_dsd_rows: the DSD / DSD^T (trans_s = 0) with output row p (of the padded
+ * [max_rows, h] result) stored to the device address row_dst[p] instead of a
+ * dense buffer (row_dst == 0: not stored); row_dst [max_rows] uint64 device,
+ * each address 16-byte aligned (moe_ep_combine_dest writes them). Rows go
+ * out with 16-byte st.global (peer addresses allowed). */
+moe_status moe_dsd_rows(const moe_config* cfg, const void* s, const void* b, int trans_b,
+                        const moe_topology_t* topo, const uint64_t* row_dst, void* stream);
 /* The padded gather fused into the products that read X_g: the A rows
  * are fetched from x [T, h] by token (topo->row_src / k) with TMA
  * tile::gather4, pad rows read as zeros, so X_g is never materialised.

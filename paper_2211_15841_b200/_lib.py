@@ -112,6 +112,9 @@ SIGNATURES = {
     "moe_sdd_act_coded": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, ctypes.c_int32, P, P, P]),
     "moe_act_code_decode_host": (STATUS, [ctypes.c_int32, P, P, ctypes.c_int64]),
     "moe_dsd": (STATUS, [CFG, P, ctypes.c_int, P, ctypes.c_int, TOPO, P, P]),
+    "moe_dsd_rows": (STATUS, [CFG, P, P, ctypes.c_int, TOPO, P, P]),
+    "moe_ep_combine_dest": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P, ctypes.c_int64, P]),
+    "moe_ep_signal": (STATUS, [ctypes.POINTER(MoeEp), ctypes.c_int, P]),
     "moe_dsd_scatter": (STATUS, [CFG, P, P, TOPO, P, P, P, P]),
     "moe_sdd_gather": (STATUS, [CFG, P, P, TOPO, ctypes.c_int32, P, P, P, P]),
     "moe_dds_gather": (STATUS, [CFG, P, P, TOPO, P, P, P]),

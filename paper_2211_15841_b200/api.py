@@ -339,6 +339,13 @@ def moe_dsd(cfg, s, trans_s, b, trans_b, topo: Topology, out=None):
     return out
 
 
+def moe_dsd_rows(cfg, s, b, trans_b, topo: Topology, row_dst):
+    """moe_dsd_rows (include/moe.h): DSD / DSD^T with output row p stored to the
+    device address row_dst[p] (int64 tensor on the device; 0: not stored)."""
+    check("moe_dsd_rows", lib.moe_dsd_rows(ctypes.byref(cfg), _p(s), _p(b), int(trans_b), ctypes.byref(topo.struct),
+                                           _p(row_dst), _stream()))
+
+
 def moe_gather_is_fused(cfg) -> bool:
     return bool(lib.moe_gather_is_fused(ctypes.byref(cfg)))
 

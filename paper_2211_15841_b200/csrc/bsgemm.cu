@@ -503,7 +503,31 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
       }
       sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;  // the other buffer next: one __syncwarp per chunk
     };
+    // moe_dsd_rows: this lane's output row goes to the address row_dst[y + lane]
+    // (the EP combine fused into the DSD: a peer's return window; 0: pad row)
+    auto store_rows_ptr = [&](const float* v, int x, int y) {
+      uint8_t* buf = stg + sbuf * EPI_BUF;
+      stage_row(buf, lane, v);
+      const unsigned long long mine_p = __ldg(p.row_dst + y + lane);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = i * 8 + (lane >> 2), j = lane & 3;
+        uint4 w;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(smem_u32(buf) + r * 64 + swz64(j, r))
+                     : "memory");
+        const unsigned long long rp = __shfl_sync(0xffffffffu, mine_p, r);
+        if (rp) *reinterpret_cast<uint4*>(rp + 2ull * (unsigned long long)(x + j * 8)) = w;
+      }
+      sbuf = sbuf + 1 == C::NBUF ? 0 : sbuf + 1;
+    };
     auto store_chunk = [&](const CUtensorMap* map, const float* v, int x, int y) {
+      if (MODE == DSD_ROW && p.row_dst && map == &tmap_c) {
+        store_rows_ptr(v, x, y);
+        return;
+      }
       if (MODE == DSD_ROW && p.unpadded && map == &tmap_c) {
         // the tile's block-row ends at the fringe (the rows below belong to the
         // next expert): warps with rows past it store row-clipped
@@ -1367,14 +1391,15 @@ moe_status moe_sdd_deriv(const moe_config* cfg, const void* a, const void* b, in
 // of dx, P:98 chain rule) and writes only y.
 static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                              const moe_topology_t* topo, void* out, const float* gates, void* y, void* stream,
-                             const void* dl16 = nullptr, const void* wr = nullptr) {
+                             const void* dl16 = nullptr, const void* wr = nullptr,
+                             const unsigned long long* row_dst = nullptr) {
   MOE_TRY(moe_check_config(cfg));
   MOE_TRY(check_topo(topo));
-  MOE_CHECK_ARG(s && b && out, "moe_dsd: NULL operand");
+  MOE_CHECK_ARG(s && b && (out || row_dst), "moe_dsd: NULL operand");
   const int64_t rows = moe_max_padded_rows(cfg), nnz = moe_max_nnz_blocks(cfg);
   const int64_t h = cfg->hidden, N = cfg->num_experts * cfg->ffn_hidden;
-  // (the row-pair DSD exists only for the padded layout)
-  const bool pair = use_pair(cfg) && (trans_s || (use_pair_rows() && !cfg->unpadded));
+  // (the row-pair DSD exists only for the padded layout; the row-address stores only in the 1-SM kernel)
+  const bool pair = use_pair(cfg) && (trans_s || (use_pair_rows() && !cfg->unpadded && !row_dst));
   // dense rows the products read along K: with the unpadded layout the rows
   // past the last expert's fringe are out of range (TMA zero fill), so their
   // stale contents never meet the fringe's zero sparse rows
@@ -1396,8 +1421,13 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
       MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, N, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else
       MOE_TRY(make_tmap_bf16(&L.tb, b, N, h, N, BK, bbox, "moe_dsd b^T", KSW));
-    MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
-    set_epi_out(L.p, 0, out, rows, h);
+    if (row_dst) {  // rows stored by address (the map is never used for a store)
+      L.p.row_dst = row_dst;
+      MOE_TRY(make_tmap_epi(&L.tc, s, 128, nnz * 128, 128, "moe_dsd_rows (unused map)"));
+    } else {
+      MOE_TRY(make_tmap_epi(&L.tc, out, h, rows, h, "moe_dsd out"));
+      set_epi_out(L.p, 0, out, rows, h);
+    }
     if (y) {  // fused weighted un-permutation (top-1): rows scattered to y[token] by tile::scatter4
       MOE_TRY(make_tmap_bf16(&L.td, y, h, cfg->tokens, h, 32, 1, "moe_dsd_scatter y", 64));
       set_epi_out(L.p, 1, y, cfg->tokens, h);
@@ -1433,6 +1463,14 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
 moe_status moe_dsd(const moe_config* cfg, const void* s, int trans_s, const void* b, int trans_b,
                    const moe_topology_t* topo, void* out, void* stream) {
   return dsd_launch(cfg, s, trans_s, b, trans_b, topo, out, nullptr, nullptr, stream);
+}
+
+moe_status moe_dsd_rows(const moe_config* cfg, const void* s, const void* b, int trans_b,
+                        const moe_topology_t* topo, const uint64_t* row_dst, void* stream) {
+  MOE_CHECK_ARG(row_dst, "moe_dsd_rows: NULL row_dst");
+  MOE_CHECK_ARG(cfg && !cfg->unpadded, "moe_dsd_rows: the padded layout only");
+  return dsd_launch(cfg, s, 0, b, trans_b, topo, nullptr, nullptr, nullptr, stream, nullptr, nullptr,
+                    reinterpret_cast<const unsigned long long*>(row_dst));
 }
 
 moe_status moe_dsd_dx(const moe_config* cfg, const void* dh, const void* w1, const moe_topology_t* topo,

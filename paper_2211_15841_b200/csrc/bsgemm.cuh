@@ -79,6 +79,7 @@ struct GemmParams {
   __nv_bfloat16* out_d;
   long long ldc, ldd, rows_c, rows_d;
   int direct;
+  const unsigned long long* row_dst;  // DSD_ROW: output row p goes to address row_dst[p] (0: dropped)
   int sdd_half;
   int epi_alt;   // CTA-pair forward SDD (4 KB boxes): two epilogue warp groups drain alternate tiles  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)

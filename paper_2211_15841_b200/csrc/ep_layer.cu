@@ -66,6 +66,13 @@ struct moe_ep {
   void* dh = nullptr;         // bf16 [max_nnz_e, bs, bs]
   void* y_g = nullptr;        // bf16 [max_rows_e, h]
   void* dx_g = nullptr;       // bf16 [max_rows_e, h]
+  // the combine fused into the DSD / DSD^T (NEXT-1): each padded row's address
+  // in its source's return region (moe_ep_combine_dest), the rows stored there
+  // by moe_dsd_rows; y_g / dx_g then stay unused
+  uint64_t* dest_y = nullptr;   // [max_rows_e]
+  uint64_t* dest_dx = nullptr;  // [max_rows_e]
+  int64_t rows_e = 0;
+  bool fused_combine = true;
   // side stream for dWr
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -227,6 +234,13 @@ moe_status moe_ep_init(moe_ep** out, const moe_ep_desc* d, int device) {
   if ((st = ep_alloc(ep, &ep->dh, 2 * nnz_e * blk)) != MOE_OK) return fail(st);
   if ((st = ep_alloc(ep, &ep->y_g, 2 * rows_e * h)) != MOE_OK) return fail(st);
   if ((st = ep_alloc(ep, &ep->dx_g, 2 * rows_e * h)) != MOE_OK) return fail(st);
+  if ((st = ep_alloc(ep, (void**)&ep->dest_y, sizeof(uint64_t) * rows_e)) != MOE_OK) return fail(st);
+  if ((st = ep_alloc(ep, (void**)&ep->dest_dx, sizeof(uint64_t) * rows_e)) != MOE_OK) return fail(st);
+  ep->rows_e = rows_e;
+  {
+    const char* fc = getenv("MOE_EP_FUSED_COMBINE");  // 0: the separate combine copy (A/B)
+    ep->fused_combine = !(fc && fc[0] == '0');
+  }
   if (cudaStreamCreateWithFlags(&ep->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&ep->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ep->join, cudaEventDisableTiming) != cudaSuccess)
@@ -289,9 +303,16 @@ moe_status moe_ep_forward(moe_ep* ep, int64_t tokens, const moe_weights* w, cons
   MOE_TRY(moe_zero_pad_rows(ce, &ep->topo_e, x_g, stream));
   MOE_TRY(moe_sdd_deriv(ce, x_g, w->w1, 0, &ep->topo_e, ep->d.act, nullptr, ep->a, id ? nullptr : ep->act_deriv,
                         stream));
-  MOE_TRY(moe_dsd(ce, ep->a, 0, w->w2, 0, &ep->topo_e, ep->y_g, stream));
-  // combine back to the token owners, then the gate-weighted un-permutation
-  MOE_TRY(moe_ep_combine_padded(&ep->ex, MOE_EP_RET_Y, ep->y_g, stream));
+  // combine back to the token owners, then the gate-weighted un-permutation;
+  // fused (NEXT-1): the DSD stores every row straight into its source's return region
+  if (ep->fused_combine) {
+    MOE_TRY(moe_ep_combine_dest(&ep->ex, MOE_EP_RET_Y, ep->dest_y, ep->rows_e, stream));
+    MOE_TRY(moe_dsd_rows(ce, ep->a, w->w2, 0, &ep->topo_e, ep->dest_y, stream));
+    MOE_TRY(moe_ep_signal(&ep->ex, MOE_EP_RET_Y, stream));
+  } else {
+    MOE_TRY(moe_dsd(ce, ep->a, 0, w->w2, 0, &ep->topo_e, ep->y_g, stream));
+    MOE_TRY(moe_ep_combine_padded(&ep->ex, MOE_EP_RET_Y, ep->y_g, stream));
+  }
   MOE_TRY(moe_ep_wait(&ep->ex, MOE_EP_RET_Y, stream));
   MOE_TRY(moe_unsort_rows(&cl, win_region(ep, MOE_EP_RET_Y), &ep->topo_l, ep->gates, y, stream));
   ep->tokens = tokens;
@@ -343,9 +364,15 @@ moe_status moe_ep_backward(moe_ep* ep, const moe_weights* w, const void* x, cons
                         stream));
   MOE_TRY(moe_dsd(ce, ep->a, 1, dy_g, 0, &ep->topo_e, g->dw2, stream));
   MOE_TRY(moe_dds(ce, x_g, 1, ep->dh, 0, &ep->topo_e, g->dw1, stream));
-  MOE_TRY(moe_dsd(ce, ep->dh, 0, w->w1, 1, &ep->topo_e, ep->dx_g, stream));
-  // dX rows back to the token owners; b6 (+ b7's dx += dlogits . Wr^T)
-  MOE_TRY(moe_ep_combine_padded(&ep->ex, MOE_EP_RET_DX, ep->dx_g, stream));
+  // dX rows back to the token owners (fused: the DSD^T stores them there); b6 (+ b7's dx += dlogits . Wr^T)
+  if (ep->fused_combine) {
+    MOE_TRY(moe_ep_combine_dest(&ep->ex, MOE_EP_RET_DX, ep->dest_dx, ep->rows_e, stream));
+    MOE_TRY(moe_dsd_rows(ce, ep->dh, w->w1, 1, &ep->topo_e, ep->dest_dx, stream));
+    MOE_TRY(moe_ep_signal(&ep->ex, MOE_EP_RET_DX, stream));
+  } else {
+    MOE_TRY(moe_dsd(ce, ep->dh, 0, w->w1, 1, &ep->topo_e, ep->dx_g, stream));
+    MOE_TRY(moe_ep_combine_padded(&ep->ex, MOE_EP_RET_DX, ep->dx_g, stream));
+  }
   MOE_TRY(moe_ep_wait(&ep->ex, MOE_EP_RET_DX, stream));
   const void* dx_sorted = win_region(ep, MOE_EP_RET_DX);
   if (fused) {

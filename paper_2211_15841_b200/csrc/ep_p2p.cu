@@ -356,6 +356,55 @@ __global__ void __launch_bounds__(256) ep_copy_padded_kernel(EpArgs a, const uin
   signal_peers(a, region);
 }
 
+// The combine fused into the expert side's DSD: the device
+// address every padded row of this rank goes to (its source's return region at
+// the row's sorted position, as ep_copy_padded_kernel<true> would copy it), 0
+// for pad rows and rows past the plan's padded count.
+__global__ void __launch_bounds__(256) ep_combine_dest_kernel(EpArgs a, size_t region_off,
+                                                              unsigned long long* __restrict__ dest,
+                                                              long long max_rows) {
+  pdl_trigger();
+  pdl_wait();
+  PlanView v = plan_view(a.plan, a.P, a.E);
+  const int rows = *v.n_padded;
+  const int nseg = a.El * a.P;
+  extern __shared__ int32_t s_tab[];
+  int32_t* starts = s_tab;
+  int32_t* lens = s_tab + nseg;
+  int32_t* dsts = s_tab + 2 * nseg;
+  for (int i = threadIdx.x; i < nseg; i += blockDim.x) {
+    starts[i] = v.seg_pstart[i];
+    lens[i] = v.seg_len[i];
+    dsts[i] = v.seg_dst[i];
+  }
+  __syncthreads();
+  const long long row_bytes = a.h * 2;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < max_rows;
+       u += (long long)gridDim.x * blockDim.x) {
+    unsigned long long d = 0ull;
+    if (u < rows) {
+      int lo = 0, hi = nseg - 1;  // last segment starting at or before u
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (starts[mid] <= u) lo = mid; else hi = mid - 1;
+      }
+      if (u < starts[lo] + lens[lo])  // else a pad row
+        d = reinterpret_cast<unsigned long long>(peer_win(a, lo % a.P) + region_off) +
+            (unsigned long long)(dsts[lo] + (u - starts[lo])) * row_bytes;
+    }
+    dest[u] = d;
+  }
+}
+
+// Completion of stores a previous kernel made into the peers' `region` (e.g.
+// the fused-combine DSD): stream order puts them before this one-CTA kernel's
+// system-scope release, which bumps the region's arrival counters.
+__global__ void __launch_bounds__(64) ep_signal_kernel(EpArgs a, int region) {
+  pdl_trigger();
+  pdl_wait();
+  signal_peers(a, region);
+}
+
 template <bool COMBINE>
 moe_status ep_copy_launch(const moe_ep_t* ep, const void* rows, int region, size_t off, void* stream,
                           const int32_t* src_map = nullptr, int src_k = 1) {
@@ -481,6 +530,28 @@ moe_status moe_ep_combine_padded(const moe_ep_t* ep, int region, const void* row
   const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
   const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
   return ep_copy_launch<true>(ep, rows_padded, region, off, stream);
+}
+
+moe_status moe_ep_combine_dest(const moe_ep_t* ep, int region, uint64_t* dest, int64_t max_rows, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_combine_dest"));
+  MOE_CHECK_ARG(dest && max_rows >= 0 && (region == MOE_EP_RET_Y || region == MOE_EP_RET_DX),
+                "moe_ep_combine_dest: NULL dest, max_rows < 0 or region %d not a return region", region);
+  if (max_rows == 0) return MOE_OK;
+  const WinLayout L = win_layout(ep->nranks, ep->num_experts, ep->hidden, ep->cap_rows, ep->owner_rows);
+  const size_t off = region == MOE_EP_RET_Y ? L.ret_y : L.ret_dx;
+  const size_t tab = 3 * sizeof(int32_t) * (size_t)ep->num_experts;
+  const int ctas = (int)std::min<int64_t>(ceil_div(max_rows, 256), 2 * 148);
+  MOE_LAUNCH("ep_combine_dest", ep_combine_dest_kernel, dim3(ctas), dim3(256), tab, as_stream(stream), ep_args(ep),
+             off, reinterpret_cast<unsigned long long*>(dest), (long long)max_rows);
+  return MOE_OK;
+}
+
+moe_status moe_ep_signal(const moe_ep_t* ep, int region, void* stream) {
+  MOE_TRY(check_ep(ep, "moe_ep_signal"));
+  MOE_CHECK_ARG(region >= MOE_EP_COUNTS && region <= MOE_EP_RET_DX, "moe_ep_signal: bad region %d", region);
+  MOE_LAUNCH("ep_signal", ep_signal_kernel, dim3(1), dim3(64), 0, as_stream(stream), ep_args(ep),
+             region - MOE_EP_COUNTS);
+  return MOE_OK;
 }
 
 int moe_ep_plan_offset(int nranks, int num_experts, int which) {

@@ -339,6 +339,44 @@ def product_case(T, h, f, E, k, zipf, seed):
 PRODUCT_CASES = [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2), (2500, 768, 384, 8, 1, 0.5, 3)]
 
 
+@pytest.mark.parametrize("trans_b", [0, 1])
+@pytest.mark.parametrize("case", PRODUCT_CASES)
+def test_dsd_rows_by_address(case, trans_b):
+    """moe_dsd_rows (the EP combine fused into the DSD / DSD^T, NEXT-1): output
+    row p goes to the device address row_dst[p] (0: not stored). Rows are sent
+    to a shuffled target buffer, every third row dropped; each stored row equals
+    the oracle's DSD row, untouched rows keep their sentinel."""
+    d = dev()
+    A = api()
+    T, h, f, E, k, zipf, seed = case
+    idx, plan, topo, x, w1, w2, dyg = product_case(*case)
+    Tp, nnz = plan.Tp, topo.nnz
+    cfg = A.make_config(T, h, E, k, f, act=A.ACT_GELU)
+    tg = A.moe_topology(cfg, idx.to(d))
+    nmax, rows = A.moe_max_nnz_blocks(cfg), A.moe_max_padded_rows(cfg)
+    g = torch.Generator().manual_seed(seed + 11)
+    svals = torch.zeros(nmax, 128, 128, dtype=torch.bfloat16)
+    svals[:nnz] = (torch.randn(nnz, 128, 128, generator=g) / 8).to(torch.bfloat16)
+    b = w2 if not trans_b else w1            # DSD: S . W2; DSD^T: S . W1^T
+    want = O.dsd(S.to_f64(svals[:nnz]), S.to_f64(b), topo, trans_b=bool(trans_b))
+    target = torch.full((rows + 7, h), 7.0, dtype=torch.bfloat16, device=d)
+    perm = torch.randperm(rows, generator=g)
+    keep = (torch.arange(rows) % 3) != 2
+    base = target.data_ptr()
+    dst = torch.where(keep, base + perm.to(torch.int64) * h * 2, torch.zeros(rows, dtype=torch.int64))
+    dst_d = dst.to(d)
+    A.moe_dsd_rows(cfg, svals.to(d), b.to(d), trans_b, tg, dst_d)
+    torch.cuda.synchronize()
+    got = target.cpu()
+    kp = keep[:Tp].numpy()
+    rows_got = f64(got[perm[:Tp]])
+    assert_close("dsd rows", rows_got[kp], want[kp])
+    # dropped rows and rows past Tp leave their target rows untouched
+    untouched = torch.ones(rows + 7, dtype=torch.bool)
+    untouched[perm[:Tp][torch.from_numpy(kp)]] = False
+    assert (got[untouched].float() == 7.0).all()
+
+
 @pytest.mark.parametrize("case", [(1000, 256, 512, 4, 1, 0.0, 1), (3000, 512, 1024, 16, 2, 1.2, 2),
                                   (2500, 768, 384, 8, 1, 0.5, 3), (4100, 512, 2048, 64, 1, 0.0, 4)])
 def test_gather_fused_products(case):
