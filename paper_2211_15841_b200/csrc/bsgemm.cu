@@ -158,6 +158,13 @@ __device__ __forceinline__ TileInfo decode(const GemmParams& p, int mode, int pa
     const int b = __ldg(p.t_col_offsets + t.u), e = __ldg(p.t_col_offsets + t.u + 1);
     t.walk_begin = b;
     t.kiters = KPB * (e - b);
+    // the column's last block-row (its expert's fringe) holds <= 64 assignments:
+    // its second K-step multiplies zero rows only (pad rows / zero sparse rows)
+    // (the expert's count decides it: (count - 1) % 128 < 64; one load, off the index chain)
+    if (KPB == 2 && p.kskip && e > b) {
+      const int cnt = __ldg(p.counts + t.u / p.F);
+      if (cnt > 0 && (cnt - 1) % BM < BM / 2) --t.kiters;
+    }
   } else {  // DENSE: tile = (split * m_tiles + m) * n_tiles + n
     t.v = tile % p.n_tiles;
     const int rest = tile / p.n_tiles;
@@ -363,7 +370,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
         const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && MODE != DENSE && (blk & 31) == 0 && kk == 0 && (MODE != DSD_ROW || kit < t.s)) {
           const int q = t.walk_begin + blk + lane;
-          if (q < t.walk_begin + (t.kiters / KPB)) {
+          if (q < t.walk_begin + (t.kiters + KPB - 1) / KPB) {  // (a skipped last half K-step still needs its block)
             if (MODE == DSD_ROW || MODE == DDS_ROW) {
               idx_a = q;
               idx_b = __ldg(p.col_indices + q);
@@ -1154,11 +1161,22 @@ GemmParams gemm_params_topo(const moe_config* cfg, const moe_topology_t* topo) {
   p.t_row_indices = topo->t_row_indices;
   p.pair_bins = topo->pair_bins;
   p.padded_bins = topo->padded_bins;
+  p.counts = topo->counts;
   p.F = (int)(cfg->ffn_hidden / cfg->block_size);
   p.E = (int)cfg->num_experts;
   p.unpadded = cfg->unpadded;
   p.brow_start = topo->brow_start;
   p.brow_rows = topo->brow_rows;
+  {
+    // column walks skip the all-zero second K-step of a half-filled last
+    // block-row (MOE_KSKIP=0: off)
+    static int ks = -1;
+    if (ks < 0) {
+      const char* e = getenv("MOE_KSKIP");
+      ks = (e && e[0] == '0') ? 0 : 1;
+    }
+    p.kskip = ks;
+  }
   p.sorted_idx = topo->sorted_idx;
   p.n_block_cols = (int)(cfg->num_experts * cfg->ffn_hidden / cfg->block_size);
   p.k_dense = (int)cfg->hidden;
@@ -1560,6 +1578,7 @@ static moe_status dds_launch(const moe_config* cfg, const void* a, int trans_a, 
       L.p.gather_k = (int)cfg->top_k;
       L.p.gather_T = (int)cfg->tokens;
       L.p.row_src = topo->row_src;
+      L.p.kskip = 0;  // the gathered token ring walks whole blocks
     } else if (trans_a)
       MOE_TRY(make_tmap_bf16_mn(&L.ta, a, h, drows, h, 2, "moe_dds a^T"));
     else

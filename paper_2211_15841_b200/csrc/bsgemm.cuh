@@ -24,6 +24,7 @@ struct GemmParams {
   const int32_t* t_row_indices;
   const int32_t* pair_bins;    // [E] inclusive cumsum of same-expert block-row pairs
   const int32_t* padded_bins;  // [E]
+  const int32_t* counts;       // [E] assignments (kept) per expert
   int n_block_cols;  // E*F
   int F;             // block-columns per expert
   int dense_tiles;   // output tiles along the dense dimension
@@ -80,6 +81,7 @@ struct GemmParams {
   long long ldc, ldd, rows_c, rows_d;
   int direct;
   const unsigned long long* row_dst;  // DSD_ROW: output row p goes to address row_dst[p] (0: dropped)
+  int kskip;     // DS_COL / DDS_COL: skip the second K-step of a column's last block-row when it holds <= 64 rows
   int sdd_half;
   int epi_alt;   // CTA-pair forward SDD (4 KB boxes): two epilogue warp groups drain alternate tiles  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)

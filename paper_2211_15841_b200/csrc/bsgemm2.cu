@@ -70,6 +70,8 @@ constexpr int P_NBUF = MOE_PAIR_NBUF;                          // staging buffer
 #define MOE_PAIR_NHW (MOE_PAIR_HC == 64 ? 3 : 5)
 #endif
 
+constexpr int P_PB_MAX = 384;  // experts whose pair offsets fit the shared-memory copy (row_pair)
+
 template <bool EPI_H, int MODE = -1>
 struct Cfg2 {
   // the forward SDD stores 64-column chunks (4 KB TMA boxes, two staging
@@ -90,10 +92,11 @@ struct Cfg2 {
   // SDD^T: act'(H) decode table of the coded A (R24), where it fits
   static constexpr bool HAS_TAB = EPI_H && WIDE_H && HC == 32;
   static constexpr int TAB = HAS_TAB ? ACT_CODE_BYTES : 0;
-  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK - TAB) / P_STAGE;
+  static constexpr int PB = (MODE == SDD || MODE == DSD_ROW) ? P_PB_MAX * 4 : 0;  // pair offsets (row_pair)
+  static constexpr int STAGES_RAW = (SMEM_LIMIT - SMEM_FIXED - P_EPI_BYTES - H_BYTES - TOK - TAB - PB) / P_STAGE;
   static constexpr int STAGES = STAGES_RAW > MOE_MAX_STAGES ? MOE_MAX_STAGES : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * P_BN;
-  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + P_EPI_BYTES + H_BYTES + TOK + TAB;
+  static constexpr size_t SMEM = SMEM_FIXED + (size_t)STAGES * P_STAGE + P_EPI_BYTES + H_BYTES + TOK + TAB + PB;
   static_assert(!EPI_H || STAGES >= 4, "SDD^T: four pipeline stages expected");
 };
 
@@ -116,35 +119,38 @@ __device__ __forceinline__ int num_tiles2(const GemmParams& p, int mode) {
   }
 }
 
-// Row pair p -> (first block-row, whether the second row exists), via the
-// per-expert pair offsets (binary search over E).
-__device__ __forceinline__ void row_pair(const GemmParams& p, int pr, int& r0, bool& second) {
+// Row pair p -> (first block-row, whether the second row exists; returns the
+// expert), via the per-expert pair offsets `pbins` (binary search over E; a
+// shared-memory copy when E is small: the search is on every tile's decode
+// path, and six dependent L2 round trips there stalled the TMA producer at
+// each tile boundary).
+__device__ __forceinline__ int row_pair(const GemmParams& p, const int32_t* pbins, int pr, int& r0, bool& second) {
   int lo = 0, hi = p.E - 1;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (__ldg(p.pair_bins + mid) > pr) hi = mid; else lo = mid + 1;
+    if (pbins[mid] > pr) hi = mid; else lo = mid + 1;
   }
   const int e = lo;
   const int pb = __ldg(p.padded_bins + e);
   const int pc = pb - (e > 0 ? __ldg(p.padded_bins + e - 1) : 0);
   const int nrows = pc / BM;
-  const int i = pr - (__ldg(p.pair_bins + e) - (nrows + 1) / 2);
+  const int i = pr - (pbins[e] - (nrows + 1) / 2);
   r0 = (pb - pc) / BM + 2 * i;
   second = 2 * i + 1 < nrows;
+  return e;
 }
 
-__device__ __forceinline__ Tile2 decode2(const GemmParams& p, int mode, int tile, int rank) {
+__device__ __forceinline__ Tile2 decode2(const GemmParams& p, int mode, int tile, int rank, const int32_t* pbins) {
   Tile2 t{};
   if (mode == SDD) {
     const int pr = tile / (p.F / 2), cp = tile % (p.F / 2);
-    row_pair(p, pr, t.r0, t.second);
-    const int e = __ldg(p.col_indices + (long long)__ldg(p.row_offsets + t.r0)) / p.F;
+    const int e = row_pair(p, pbins, pr, t.r0, t.second);
     t.c0 = e * p.F + 2 * cp;
     t.kiters = p.k_dense / BK;
   } else if (mode == DSD_ROW) {
     const int pr = tile / p.dense_tiles;
     t.v = tile % p.dense_tiles;
-    row_pair(p, pr, t.r0, t.second);
+    row_pair(p, pbins, pr, t.r0, t.second);
     const int b = __ldg(p.row_offsets + t.r0), e = __ldg(p.row_offsets + t.r0 + 1);
     t.walk_begin = b;
     t.kiters = KPB * (e - b);
@@ -155,6 +161,13 @@ __device__ __forceinline__ Tile2 decode2(const GemmParams& p, int mode, int tile
     const int b = __ldg(p.t_col_offsets + t.c0), e = __ldg(p.t_col_offsets + t.c0 + 1);
     t.walk_begin = b;
     t.kiters = KPB * (e - b);
+    // the columns' last block-row (the expert's fringe) holds <= 64 assignments:
+    // its second K-step multiplies zero rows only (pad rows / zero sparse rows)
+    // (the expert's count decides it: (count - 1) % 128 < 64; one load, off the index chain)
+    if (KPB == 2 && p.kskip && e > b) {
+      const int cnt = __ldg(p.counts + t.c0 / p.F);
+      if (cnt > 0 && (cnt - 1) % BM < BM / 2) --t.kiters;
+    }
     t.second = true;
   }
   return t;
@@ -207,7 +220,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   uint8_t* smem_h = smem_epi + P_EPI_BYTES;
   int4* tokring = reinterpret_cast<int4*>(smem_h + C::H_BYTES);
   uint8_t* smem_tab = smem_h + C::H_BYTES + C::TOK;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_tab + C::TAB);
+  int32_t* smem_pb = reinterpret_cast<int32_t*>(smem_tab + C::TAB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_tab + C::TAB + C::PB);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -245,6 +259,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   pdl_trigger();
   pdl_wait();
   const int ntiles = num_tiles2(p, MODE);
+  // the pair offsets in shared memory for the row-pair decode (E <= P_PB_MAX)
+  const int32_t* s_pb = p.pair_bins;
+  if (C::PB && p.E <= P_PB_MAX) {
+    for (int i = threadIdx.x; i < p.E; i += blockDim.x) smem_pb[i] = __ldg(p.pair_bins + i);
+    __syncthreads();
+    s_pb = smem_pb;
+  }
 
   if (warp < P_NP) {
     // ===================== TMA producers (both CTAs; warp s % P_NP issues stage s) =====================
@@ -307,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     if (MODE == SDD && MOE_PAIR_SDD_LANE0 && !gat) {
       if (lane == 0) {
         for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
-          const Tile2 t = decode2(p, MODE, tile, rank);
+          const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
           trace_ev(p, tile_i, 0);
           const bool hm = p.sdd_half && !t.second;
           const int sdd_row = hm ? (p.unpadded ? __ldg(p.brow_start + t.r0) : t.r0 * BM) + rank * 64
@@ -340,7 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       }
     } else
     for (int tile = cid; tile < ntiles && !idle; tile += ncl, ++tile_i) {
-      const Tile2 t = decode2(p, MODE, tile, rank);
+      const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0, idx_c = 0;
       // SDD: first dense row of this CTA's block-row (unpadded layout: brow_start; a
@@ -354,7 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         const int blk = kit / KPB, kk = kit % KPB;
         if (MODE != SDD && (blk & 31) == 0 && kk == 0) {
           const int qq = t.walk_begin + blk + lane;
-          if (qq < t.walk_begin + (t.kiters / KPB)) {
+          if (qq < t.walk_begin + (t.kiters + KPB - 1) / KPB) {  // (a skipped last half K-step still needs its block)
             if (MODE == DSD_ROW) {
               idx_a = qq + t.q_off;               // this CTA's row: same column, next row
               idx_b = __ldg(p.col_indices + qq);  // block column
@@ -453,7 +474,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       uint32_t acc_phase = 0;
       int tile_i = -1;
       for (int tile = cid; tile < ntiles; tile += ncl) {
-        const Tile2 t = decode2(p, MODE, tile, 0);
+        const Tile2 t = decode2(p, MODE, tile, 0, s_pb);
         ++tile_i;
         if (t.kiters == 0) continue;
         const uint32_t idesc = (MODE == SDD && p.sdd_half && !t.second) ? idesc_half : idesc_full;
@@ -534,7 +555,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     uint32_t hw_phase = 0;  // bit b: parity of slot b's next completion
     auto load_hw = [&](int j) {  // lane 0
       if (j >= hw_end) return;
-      const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank);
+      const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank, s_pb);
       const bool hmj = MODE == SDD && p.sdd_half && !tj.second;
       const int scj = half + (j % SPW) * EPG;
       if (hmj ? HSUB * scj >= 4 : !(rank == 0 || tj.second)) return;  // nothing stored here: nothing loaded
@@ -558,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const bool ealt = C::WIDE && p.epi_alt && p.wide;
     uint32_t aphase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
-      const Tile2 t = decode2(p, MODE, tile, rank);
+      const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
       ++tile_i;
       if (ealt && (tile_i & 1) != half) continue;  // the other group's tile
       const int acc_t = ealt ? half : acc;
