@@ -48,6 +48,17 @@ int bwd_concurrent() {
 }
 
 // SMs given to the router dWr GEMM while the SDD^T runs beside it (MOE_DWR_SMS, 0 = serial).
+// MOE_SAVE_PRE=1 (experiment): the forward saves H in the act_deriv buffer and
+// the SDD^T evaluates act'(H) itself (the round-1 form before R18).
+bool save_pre() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_SAVE_PRE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int dwr_side_sms() {
   static int v = -1;
   if (v < 0) {
@@ -84,8 +95,10 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
     if (coded)
       MOE_TRY(moe_sdd_act_coded(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, stream));
     else
-      MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
-                            id ? nullptr : sv->act_deriv, stream));
+      MOE_TRY(save_pre() && !id
+                  ? moe_sdd(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, sv->act_deriv, stream)
+                  : moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
+                                  id ? nullptr : sv->act_deriv, stream));
   } else if (moe_gather_is_fused(cfg) && !coded) {  // the gather happens inside the SDD's loads (tile::gather4)
     MOE_TRY(moe_sdd_gather(cfg, x, w->w1, &sv->topo, cfg->act, sv->a, id ? nullptr : sv->act_deriv, sv->x_g, stream));
   } else {
@@ -93,8 +106,10 @@ moe_status moe_forward(const moe_config* cfg, const moe_weights* w, const void* 
     if (coded)
       MOE_TRY(moe_sdd_act_coded(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, stream));
     else
-      MOE_TRY(moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
-                            id ? nullptr : sv->act_deriv, stream));
+      MOE_TRY(save_pre() && !id
+                  ? moe_sdd(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a, sv->act_deriv, stream)
+                  : moe_sdd_deriv(cfg, sv->x_g, w->w1, 0, &sv->topo, cfg->act, nullptr, sv->a,
+                                  id ? nullptr : sv->act_deriv, stream));
   }
   // (5) x = padded_scatter(x, indices) * weights            P:279-280 (fused into the DSD for top-1)
   MOE_TRY(moe_dsd_scatter(cfg, sv->a, w->w2, &sv->topo, sv->gates, sv->y_g, y, stream));
@@ -166,7 +181,10 @@ moe_status moe_backward(const moe_config* cfg, const moe_weights* w, const moe_s
     const moe_status st =
         !id && !sv->act_deriv
             ? moe_sdd_act_coded(cfg, dy_g, w->w2, 1, topo, cfg->act, sv->a, dh, stream)  // act'(H) from A (R24)
-            : moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr, stream);
+            : save_pre() && !id
+                  ? moe_sdd(cfg, dy_g, w->w2, 1, topo, cfg->act, sv->act_deriv, dh, nullptr, stream)  // act'(H) here
+                  : moe_sdd_deriv(cfg, dy_g, w->w2, 1, topo, cfg->act, id ? nullptr : sv->act_deriv, dh, nullptr,
+                                  stream);
     set_gemm_sm_budget(0);
     MOE_TRY(st);
   }
