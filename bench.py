@@ -424,13 +424,29 @@ def run_ours_single(args, peaks):
         roof["design_two_outputs"] = {"bytes": b2, "achieved": round(b2 / dur_s / 1e9, 1),
                                       "frac": round(b2 / dur_s / 1e9 / peaks["hbm_gbs"], 4)}
     if dname == "sdd":
-        # context: the SDD's tiles move A (128 x h) and B (h x 256)
-        # into shared memory and act(H), act'(H) (2 x 128 x 256) out of it, per
-        # 128 x 256 tile; against the measured TMA L2->SMEM delivery ceiling
-        # (scripts/micro/l2_tma_bw.cu, profiles/r1s5_l2_tma_bw.txt)
-        tile_bytes = 2 * (128 * h + h * 256) + (1 if coded else 2) * 2 * 128 * 256
-        feed = tile_bytes * (nnz // 2) / dur_s / 1e12
-        roof["sm_port"] = {"bytes_per_tile": tile_bytes, "tiles": nnz // 2, "achieved_tbs": round(feed, 2),
+        # context: bytes the SDD moves through the SMs' TMA ports.
+        # The default CTA-pair kernel: per 256 x 256 pair tile each CTA loads
+        # its 128 rows of X_g and 128 columns of W1 (2 x 128 x h bf16 each) and
+        # stores its 128 x 256 share of act(H) and act'(H); an expert's lone
+        # last block-row runs as an M = 128 pair tile (64 rows per CTA, same
+        # loads, half the stores). Against the measured TMA L2->SMEM ceiling
+        # (scripts/micro/l2_tma_bw.cu, profiles/r1s5_l2_tma_bw.txt).
+        brows = (counts + 127) // 128
+        full_pairs, half_pairs = int((brows // 2).sum()), int((brows % 2).sum())
+        F = f // 128
+        outs = 1 if coded else 2
+        per_cta_load = 2 * (128 * h + 128 * h)
+        per_cta_store = outs * 2 * 128 * 256
+        pair_kernel = T * k >= 3 * E * 128 and F % 2 == 0 and h % 256 == 0 and os.environ.get("MOE_SDD_PAIR", "") != "0"
+        if pair_kernel:
+            port_bytes = (full_pairs + half_pairs) * (F // 2) * 2 * per_cta_load \
+                + (full_pairs + 0.5 * half_pairs) * (F // 2) * 2 * per_cta_store
+            tiles = {"pair_tiles": (full_pairs + half_pairs) * (F // 2), "half_pair_tiles": half_pairs * (F // 2)}
+        else:  # 1-SM 128 x 256 tiles: A (128 x h) and B (h x 256) in, the outputs out
+            port_bytes = (nnz // 2) * (2 * (128 * h + h * 256) + outs * 2 * 128 * 256)
+            tiles = {"tiles_1sm": nnz // 2}
+        feed = port_bytes / dur_s / 1e12
+        roof["sm_port"] = {"bytes": int(port_bytes), **tiles, "achieved_tbs": round(feed, 2),
                            "tma_l2_to_smem_ceiling_tbs": 14.59, "frac": round(feed / 14.59, 3)}
     breakdown = {nm: {"ms": round(float(m), 4), "share": round(float(s_), 4),
                       **kernel_roofline(nm, wm, m / 1e3, peaks, prod_names, byte_names)}

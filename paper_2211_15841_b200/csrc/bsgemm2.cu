@@ -553,24 +553,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const int hw_end = (ntiles > cid ? (ntiles - 1 - cid) / ncl + 1 : 0) * SPW;
     int hw_seq = 0;
     uint32_t hw_phase = 0;  // bit b: parity of slot b's next completion
-    auto load_hw = [&](int j) {  // lane 0
-      if (j >= hw_end) return;
+    // coordinates of ring item j (false: nothing is stored for it on this CTA)
+    auto coords_hw = [&](int j, int& x, int& y) {
       const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank, s_pb);
       const bool hmj = MODE == SDD && p.sdd_half && !tj.second;
       const int scj = half + (j % SPW) * EPG;
-      if (hmj ? HSUB * scj >= 4 : !(rank == 0 || tj.second)) return;  // nothing stored here: nothing loaded
-      int x, y;
+      if (hmj ? HSUB * scj >= 4 : !(rank == 0 || tj.second)) return false;
       if (hmj)
         out_coords2_half(p, tj, rank, HSUB * scj, q, p.F, x, y);
       else
         out_coords2(p, MODE, tj, rank, HSUB * scj, row0, p.F, x, y);
+      return true;
+    };
+#ifndef MOE_PAIR_HPF
+#define MOE_PAIR_HPF 0  // ring items ahead that the act'(H) boxes are prefetched into L2 (measured: 4 -> SDD^T 114 vs 94.5 us; 0: none)
+#endif
+    auto load_hw = [&](int j) {  // lane 0
+      if (MOE_PAIR_HPF > 0 && j + MOE_PAIR_HPF < hw_end) {  // the box MOE_PAIR_HPF items on: into L2 now
+        int px, py;
+        if (coords_hw(j + MOE_PAIR_HPF, px, py)) tma_prefetch_2d(&tmap_d, px, py);
+      }
+      if (j >= hw_end) return;
+      int x, y;
+      if (!coords_hw(j, x, y)) return;  // nothing stored here: nothing loaded
       const int b = j % C::NHW;
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&hb[b], C::HBOX);
       tma_load_2d(hst + b * C::HBOX, &tmap_d, &hb[b], x, y);
     };
-    if (C::WIDE_H && lane == 0)
+    if (C::WIDE_H && lane == 0) {
+      for (int j = 0; j < MOE_PAIR_HPF; ++j) {  // the first items' boxes into L2
+        int px, py;
+        if (j + C::NHW - 1 < hw_end && coords_hw(j + C::NHW - 1, px, py)) tma_prefetch_2d(&tmap_d, px, py);
+      }
       for (int j = 0; j < C::NHW - 1; ++j) load_hw(j);
+    }
 
     int tile_i = -1;
     // epi_alt (forward SDD, 4 KB boxes): warp group `half` drains accumulator
