@@ -149,6 +149,21 @@ __device__ __forceinline__ void act_fwd32(int kind, float* v) {
 // v <- act(v) and g <- act'(v) over a 32-value chunk (one tanh per element
 // serves both; the forward saves g for the SDD^T epilogue). gelu runs on the
 // packed fp32x2 pipe (FFMA2/FMUL2: half the issue slots, same fp32 rounding).
+// MOE_TANH_F16X2=1 (experiment): the two tanh of a pair on one MUFU.TANH.F16x2
+// (fp16 argument and result, rel. error ~2^-11 < the bf16 outputs' ulp)
+#ifndef MOE_TANH_F16X2
+#define MOE_TANH_F16X2 0
+#endif
+__device__ __forceinline__ float2 tanh2_fast(float2 u) {
+#if MOE_TANH_F16X2
+  const __half2 h = __floats2half2_rn(u.x, u.y);
+  uint32_t r;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<const uint32_t*>(&h)));
+  return __half22float2(*reinterpret_cast<const __half2*>(&r));
+#else
+  return make_float2(tanh_fast(u.x), tanh_fast(u.y));
+#endif
+}
 __device__ __forceinline__ void act_fwd_deriv32(int kind, float* v, float* g) {
   if (kind == MOE_ACT_GELU_TANH) {
     const float2 c0 = make_float2(0.7978845608028654f, 0.7978845608028654f);
@@ -160,7 +175,7 @@ __device__ __forceinline__ void act_fwd_deriv32(int kind, float* v, float* g) {
       const float2 x = make_float2(v[i], v[i + 1]);
       const float2 x2 = __fmul2_rn(x, x);
       const float2 u = __fmul2_rn(x, __ffma2_rn(c1, x2, c0));
-      const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+      const float2 t = tanh2_fast(u);
       const float2 du = __ffma2_rn(c3, x2, c0);
       const float2 hx = __fmul2_rn(half, x);
       const float2 a = __ffma2_rn(hx, t, hx);
