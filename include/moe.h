@@ -166,7 +166,10 @@ moe_status moe_router(const moe_config* cfg, const void* x, const void* wr, floa
 moe_status moe_topk(const moe_config* cfg, const float* logits, int32_t* expert_idx, float* gates,
                     void* stream);
 
-/* Topology + permutation plan from expert_idx [T*k].
+/* Topology + permutation plan from expert_idx [T*k]. Unlike the
+ * products, this call also accepts block_size 32 or 64 (the
+ * bs = 64 topology for smaller tiles); every array then follows that
+ * block size (max sizes from the same config).
  * Writes every array of *topo (caller-allocated, sized by the max queries)
  * and topo->sizes = {Tp, nnz}. Integer outputs are bit-exact (closed form of
  * the block-diagonal pattern). ws: moe_workspace_bytes.

@@ -95,7 +95,16 @@ using namespace moe;
 
 extern "C" moe_status moe_topology(const moe_config* cfg, const int32_t* expert_idx, const moe_topology_t* topo,
                                    void* ws, void* stream) {
-  MOE_TRY(moe_check_config(cfg));
+  // the topology alone is generic in the block size (NEXT-3, "smaller tile
+  // dimensions"): bs = 32 or 64 as well as 128; the products need bs = 128
+  if (cfg && (cfg->block_size == 32 || cfg->block_size == 64)) {
+    moe_config c128 = *cfg;
+    c128.block_size = 128;
+    MOE_CHECK_ARG(cfg->ffn_hidden % cfg->block_size == 0, "moe_topology: ffn_hidden %% block_size != 0");
+    if (cfg->ffn_hidden % 128 == 0) MOE_TRY(moe_check_config(&c128));
+  } else {
+    MOE_TRY(moe_check_config(cfg));
+  }
   MOE_TRY(check_topo(topo));
   MOE_CHECK_ARG(expert_idx && ws, "moe_topology: NULL expert_idx or workspace");
   const int R = (int)(cfg->tokens * cfg->top_k);

@@ -43,6 +43,8 @@ CONFIGS = {
     "C2": MoEShape("C2-MoE-Small-skew", 32768, 768, 3072, 64, 1, routing="skew", skew=0.5),
     "C3": MoEShape("C3-MoE-Medium", 8192, 1024, 4096, 64, 1),
     "C4": MoEShape("C4-MoE-Medium-top2", 8192, 1024, 4096, 64, 2),
+    # "also report C3 at T_local = 32768 (it fits in B200 memory)"
+    "C3L": MoEShape("C3-MoE-Medium-T32k", 32768, 1024, 4096, 64, 1),
 }
 
 # tensor ids used to derive per-tensor seeds: seed = base * 1000 + id

@@ -49,12 +49,12 @@ def gelu_argmin():
     return 0.5 * (lo + hi)
 
 
-def oracle_plan_topo(idx_np, E, f):
-    plan = O.make_plan(idx_np, E, 128)
-    return plan, O.make_topology_closed_form(plan, 128, f)
+def oracle_plan_topo(idx_np, E, f, bs=128):
+    plan = O.make_plan(idx_np, E, bs)
+    return plan, O.make_topology_closed_form(plan, bs, f)
 
 
-def check_topology_exact(A, topo_gpu, plan, topo, R):
+def check_topology_exact(A, topo_gpu, plan, topo, R, bs=128):
     Tp, nnz = topo_gpu.sizes()
     assert Tp == plan.Tp and nnz == topo.nnz
     g = {k: v.cpu().numpy() for k, v in topo_gpu.t.items()}
@@ -66,14 +66,14 @@ def check_topology_exact(A, topo_gpu, plan, topo, R):
     inv = np.empty(R, np.int64)
     inv[plan.sorted_idx] = np.arange(R)
     np.testing.assert_array_equal(g["sorted_pos"][:R], inv)
-    np.testing.assert_array_equal(g["row_offsets"][:Tp // 128 + 1], topo.row_offsets)
+    np.testing.assert_array_equal(g["row_offsets"][:Tp // bs + 1], topo.row_offsets)
     np.testing.assert_array_equal(g["col_indices"][:nnz], topo.col_indices)
     np.testing.assert_array_equal(g["row_indices"][:nnz], topo.row_indices)
     np.testing.assert_array_equal(g["t_col_offsets"], topo.t_col_offsets)
     np.testing.assert_array_equal(g["t_block_offsets"][:nnz], topo.t_block_offsets)
     np.testing.assert_array_equal(g["t_row_indices"][:nnz], topo.t_row_indices)
     # 2-SM tiling helper: per-expert pairs of block-rows, ceil(rows_e / 2), cumulated
-    pairs = np.cumsum((plan.padded_counts // 128 + 1) // 2)
+    pairs = np.cumsum((plan.padded_counts // bs + 1) // 2)
     np.testing.assert_array_equal(g["pair_bins"], pairs)
     assert int(g["sizes"][2]) == int(pairs[-1])
     # row_src: the inverse of pos over the padded rows, -1 on pad rows
@@ -81,9 +81,9 @@ def check_topology_exact(A, topo_gpu, plan, topo, R):
     src[plan.pos] = np.arange(R)
     np.testing.assert_array_equal(g["row_src"][:Tp], src)
     # the unpadded layout's block-row starts / valid rows (P:297 fringe, R23)
-    bst, brows = O.fringe_rows(plan, 128)
-    np.testing.assert_array_equal(g["brow_start"][:Tp // 128], bst)
-    np.testing.assert_array_equal(g["brow_rows"][:Tp // 128], brows)
+    bst, brows = O.fringe_rows(plan, bs)
+    np.testing.assert_array_equal(g["brow_start"][:Tp // bs], bst)
+    np.testing.assert_array_equal(g["brow_rows"][:Tp // bs], brows)
 
 
 # ------------------------------------------------------------------ routing
@@ -176,6 +176,25 @@ def test_topology_bit_exact(T, E, k, f, zipf):
     topo = A.moe_topology(cfg, idx.to(d))
     plan, otopo = oracle_plan_topo(idx.numpy(), E, f)
     check_topology_exact(A, topo, plan, otopo, T * k)
+
+
+@pytest.mark.parametrize("bs", [64, 32])
+@pytest.mark.parametrize("T,E,k,f,zipf", [(1000, 4, 1, 512, 0.0), (8192, 64, 1, 4096, 0.0), (8192, 64, 2, 4096, 0.0),
+                                          (5000, 64, 1, 3072, 1.5), (3, 64, 1, 256, 0.0), (20000, 1024, 2, 128, 0.3)])
+def test_topology_small_blocks_bit_exact(T, E, k, f, zipf, bs):
+    """NEXT-3 (P:383 smaller tiles): the topology at block size 64 / 32 against
+    the oracle's plan and closed-form topology at that block size, every array
+    bit-exact; MoE-Medium (C3, T = 8192) pads far fewer rows than at 128."""
+    d = dev()
+    A = api()
+    idx = S.random_expert_idx(T, E, k, seed=T + bs, zipf=zipf)
+    cfg = A.make_config(T, 256, E, k, f, block_size=bs)
+    topo = A.moe_topology(cfg, idx.to(d))
+    plan, otopo = oracle_plan_topo(idx.numpy(), E, f, bs)
+    check_topology_exact(A, topo, plan, otopo, T * k, bs)
+    if (T, E, k) == (8192, 64, 1):  # the C3 padding the paper's 128 blocks add, and what bs = 64 leaves
+        p128, _ = oracle_plan_topo(idx.numpy(), E, f, 128)
+        assert plan.Tp < p128.Tp
 
 
 def test_topology_deterministic_repeat():
