@@ -53,23 +53,36 @@ __device__ inline void topo_scan_emit_body(const int32_t* __restrict__ idx, int 
   const int span = rows_per_cta * row_chunk;
   const int warp_id = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
   // (1) per-expert totals: the threads split into S = nt / E row slices x E
-  //     experts (coalesced over e), each summing its slice with independent loads
+  //     experts (coalesced over e), each summing its slice with independent loads.
+  //     A CTA ranking exactly one group also sums the rows before its group in
+  //     the same pass (its per-expert base, s_base), instead of a second pass.
+  const bool one_group = tk.rank_first < n_rank && tk.rank_first + tk.rank_stride >= n_rank;
+  const int first0 = one_group ? tk.rank_first * rows_per_cta : 0;
   {
     const int S = nt / E;
     const int t = threadIdx.x;
     if (t < S * E) {
       const int sl = t / E, e = t - sl * E;
       const int r0 = (int)((long long)n_rows * sl / S), r1 = (int)((long long)n_rows * (sl + 1) / S);
-      int32_t tot = 0;
+      int32_t tot = 0, pre = 0;
 #pragma unroll 8
-      for (int c = r0; c < r1; ++c) tot += __ldg(chunk_counts + (size_t)c * E + e);
+      for (int c = r0; c < r1; ++c) {
+        const int32_t v = __ldg(chunk_counts + (size_t)c * E + e);
+        tot += v;
+        pre += c < first0 ? v : 0;
+      }
       s_start[t] = tot;
+      s_pstart[t] = pre;  // scratch until the scans
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += nt) {
-      int32_t tot = 0;
-      for (int sl = 0; sl < S; ++sl) tot += s_start[sl * E + e];
+      int32_t tot = 0, pre = 0;
+      for (int sl = 0; sl < S; ++sl) {
+        tot += s_start[sl * E + e];
+        pre += s_pstart[sl * E + e];
+      }
       s_cnt[e] = capacity > 0 ? min(tot, capacity) : tot;  // kept assignments (token dropping)
+      s_base[e] = pre;
     }
   }
   __syncthreads();
@@ -141,9 +154,10 @@ __device__ inline void topo_scan_emit_body(const int32_t* __restrict__ idx, int 
   //     per-warp prefix) -> sorted_idx, pos, sorted_pos, row_src
   __syncthreads();  // the publish above has read s_pair, reused as scratch below
   for (int g = tk.rank_first; g < n_rank; g += tk.rank_stride) {
-    // this group's exclusive base per expert: rows [0, g*rows_per_cta)
+    // this group's exclusive base per expert: rows [0, g*rows_per_cta) (already
+    // summed in pass (1) when the CTA ranks one group)
     const int first = g * rows_per_cta;
-    {
+    if (!one_group) {
       const int S = nt / E;
       const int t = threadIdx.x;
       if (t < S * E) {
@@ -154,7 +168,6 @@ __device__ inline void topo_scan_emit_body(const int32_t* __restrict__ idx, int 
         for (int c = r0; c < r1; ++c) pre += __ldg(chunk_counts + (size_t)c * E + e);
         s_pair[m - 1 - t] = pre;  // s_pair's tail as scratch (the pair scan is no longer needed)
       }
-      for (int i = threadIdx.x; i < nw * E; i += nt) s_dyn[i] = 0;
       __syncthreads();
       for (int e = threadIdx.x; e < E; e += nt) {
         int32_t pre = 0;
@@ -162,6 +175,7 @@ __device__ inline void topo_scan_emit_body(const int32_t* __restrict__ idx, int 
         s_base[e] = pre;
       }
     }
+    for (int i = threadIdx.x; i < nw * E; i += nt) s_dyn[i] = 0;
     __syncthreads();
     const int i = g * span + threadIdx.x;
     const bool valid = (int)threadIdx.x < span && i < R;
