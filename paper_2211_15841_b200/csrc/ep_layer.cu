@@ -362,9 +362,8 @@ moe_status moe_ep_backward(moe_ep* ep, const moe_weights* w, const void* x, cons
   // b2 SDD^T (+act'), b3 DS^TD, b5 DD^TS, b4 DSD^T; experts without rows get exact zero columns
   MOE_TRY(moe_sdd_deriv(ce, dy_g, w->w2, 1, &ep->topo_e, ep->d.act, id ? nullptr : ep->act_deriv, ep->dh, nullptr,
                         stream));
-  MOE_TRY(moe_dsd(ce, ep->a, 1, dy_g, 0, &ep->topo_e, g->dw2, stream));
-  MOE_TRY(moe_dds(ce, x_g, 1, ep->dh, 0, &ep->topo_e, g->dw1, stream));
-  // dX rows back to the token owners (fused: the DSD^T stores them there); b6 (+ b7's dx += dlogits . Wr^T)
+  // dX rows back to the token owners first (fused: the DSD^T stores them there),
+  // so their transfer overlaps the weight-gradient products below (NEXT-1)
   if (ep->fused_combine) {
     MOE_TRY(moe_ep_combine_dest(&ep->ex, MOE_EP_RET_DX, ep->dest_dx, ep->rows_e, stream));
     MOE_TRY(moe_dsd_rows(ce, ep->dh, w->w1, 1, &ep->topo_e, ep->dest_dx, stream));
@@ -373,6 +372,9 @@ moe_status moe_ep_backward(moe_ep* ep, const moe_weights* w, const void* x, cons
     MOE_TRY(moe_dsd(ce, ep->dh, 0, w->w1, 1, &ep->topo_e, ep->dx_g, stream));
     MOE_TRY(moe_ep_combine_padded(&ep->ex, MOE_EP_RET_DX, ep->dx_g, stream));
   }
+  MOE_TRY(moe_dsd(ce, ep->a, 1, dy_g, 0, &ep->topo_e, g->dw2, stream));
+  MOE_TRY(moe_dds(ce, x_g, 1, ep->dh, 0, &ep->topo_e, g->dw1, stream));
+  // b6 (+ b7's dx += dlogits . Wr^T) once every source's dX rows arrived
   MOE_TRY(moe_ep_wait(&ep->ex, MOE_EP_RET_DX, stream));
   const void* dx_sorted = win_region(ep, MOE_EP_RET_DX);
   if (fused) {
