@@ -1346,6 +1346,13 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
       alt_env = (e && e[0] == '1') ? 1 : 0;
     }
     L.p.epi_alt = pair && wide && !act_src && alt_env ? 1 : 0;
+    static int hd_env = -1;
+    if (hd_env < 0) {
+      const char* e = getenv("MOE_SDDT_HDIRECT");
+      hd_env = (e && e[0] == '1') ? 1 : 0;
+    }
+    L.p.h_direct = pair && act_src && !L.p.act_code && hd_env ? 1 : 0;
+    L.p.h_src = reinterpret_cast<const __nv_bfloat16*>(act_src);
   }
   auto epi_map = wide ? make_tmap_epi_wide : make_tmap_epi;
   MOE_TRY(epi_map(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));

@@ -581,7 +581,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       mbar_arrive_expect_tx(&hb[b], C::HBOX);
       tma_load_2d(hst + b * C::HBOX, &tmap_d, &hb[b], x, y);
     };
-    if (C::WIDE_H && lane == 0) {
+    // h_direct: each lane reads its row's 64 act'(H) values of ring item j
+    // straight from global memory into registers (8 x 16 B, L1-allocating),
+    // one item ahead, so the act'(H) stream bypasses the SM's TMA unit (which
+    // the operand loads and the dH stores keep busy)
+    const bool hdir = C::WIDE_H && C::HC == 64 && p.h_direct;
+    uint4 hnx[8];
+    auto ldg_hw = [&](int j) {
+      int x, y;
+      if (j < hw_end && coords_hw(j, x, y)) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.h_src + ((long long)(y + lane) * 128 + x));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) hnx[u] = __ldg(src + u);
+      }
+    };
+    if (hdir) ldg_hw(0);
+    if (C::WIDE_H && !hdir && lane == 0) {
       for (int j = 0; j < MOE_PAIR_HPF; ++j) {  // the first items' boxes into L2
         int px, py;
         if (j + C::NHW - 1 < hw_end && coords_hw(j + C::NHW - 1, px, py)) tma_prefetch_2d(&tmap_d, px, py);
@@ -623,6 +638,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tmem_ld32(taddr, r);
           tmem_ld_wait();
           if (r[0] == 0x7fffffffu && r[1] == 0x12345u) p.gates[0] = 1.f;
+        }
+      } else if (C::WIDE_H && hdir) {
+        // dH = dA (x) act'(H) per 64-column box, act'(H) from registers (h_direct);
+        // the dH box is staged in the item's slot of the (now store-only) ring
+#pragma unroll 1
+        for (int s = 0; s < SPW; ++s, ++hw_seq) {
+          const int sc = half + s * EPG;
+          uint4 hcur[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) hcur[u] = hnx[u];
+          ldg_hw(hw_seq + 1);  // the next item's rows, in flight while this one is processed
+          if (mine && !(hm && 2 * sc >= 4)) {
+            uint8_t* slot = hst + (hw_seq % C::NHW) * C::HBOX;
+            if (lane == 0) bulk_wait_read<C::NHW - 1>();  // the store NHW items ago has read this slot
+            __syncwarp();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              float v[32];
+              if (has_acc) {
+                uint32_t r[32];
+                tmem_ld32(taddr + (2 * sc + hh) * EPI_COLS, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fringe ? 0.f : __uint_as_float(r[i]);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              }
+              float hf[32];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) unpack8(hcur[4 * hh + u], hf + 8 * u);
+              if (p.aux_deriv) {
+                mul32(v, hf);
+              } else {
+                act_grad_mul32(p.act, v, hf);
+              }
+              stage_row_half128(slot, lane, v, hh);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              int x, y;
+              if (hm)
+                out_coords2_half(p, t, rank, 2 * sc, q, p.F, x, y);
+              else
+                out_coords2(p, MODE, t, rank, 2 * sc, row0, p.F, x, y);
+              if (!(p.dbg & 16)) tma_store_2d(&tmap_c, slot, x, y);
+              bulk_commit();
+            }
+          }
         }
       } else if (C::WIDE_H) {
         // dH = dA (x) act'(H) per HC-column box: HSUB 32-column TMEM loads,
