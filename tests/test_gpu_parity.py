@@ -631,6 +631,8 @@ LAYER_CASES = [
     ("C0-ragged-k2", 1000, 2, S.CONFIGS["C0"].replace(top_k=2)),
     ("C1-reduced", 4096, 1, S.CONFIGS["C1"]),
     ("C2-reduced-skew", 4096, 1, S.CONFIGS["C2"]),
+    # SURVEY §8(d) stress setting: skew s = 1.0 (max/mean ~ 31, empty experts)
+    ("C2-stress-skew1", 8192, 1, S.CONFIGS["C2"].replace(skew=1.0)),
     ("C4-reduced", 2048, 2, S.CONFIGS["C4"]),
     ("C0-relu", 1024, 1, S.CONFIGS["C0"].replace(act=2)),
     ("C0-identity", 1024, 1, S.CONFIGS["C0"].replace(act=0)),
