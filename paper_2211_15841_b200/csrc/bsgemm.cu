@@ -1346,6 +1346,12 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
       alt_env = (e && e[0] == '1') ? 1 : 0;
     }
     L.p.epi_alt = pair && wide && !act_src && alt_env ? 1 : 0;
+    static int tall_env = -1;
+    if (tall_env < 0) {
+      const char* e = getenv("MOE_PAIR_TALL");
+      tall_env = (e && e[0] == '1') ? 1 : 0;
+    }
+    L.p.tall = pair && wide && !act_src && !L.p.act_code && !L.p.epi_alt && tall_env ? 1 : 0;
     static int hd_env = -1;
     if (hd_env < 0) {
       const char* e = getenv("MOE_SDDT_HDIRECT");
@@ -1354,7 +1360,7 @@ static moe_status sdd_launch(const moe_config* cfg, const void* a, const void* b
     L.p.h_direct = pair && act_src && !L.p.act_code && hd_env ? 1 : 0;
     L.p.h_src = reinterpret_cast<const __nv_bfloat16*>(act_src);
   }
-  auto epi_map = wide ? make_tmap_epi_wide : make_tmap_epi;
+  auto epi_map = L.p.tall ? make_tmap_epi_tall : wide ? make_tmap_epi_wide : make_tmap_epi;
   MOE_TRY(epi_map(&L.tc, out_s, 128, nnz * 128, 128, "moe_sdd out"));
   set_epi_out(L.p, 0, out_s, nnz * 128, 128);
   if (out_aux) MOE_TRY(epi_map(&L.td, out_aux, 128, nnz * 128, 128, "moe_sdd aux"));

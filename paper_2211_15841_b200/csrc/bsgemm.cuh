@@ -84,6 +84,7 @@ struct GemmParams {
   int kskip;     // DS_COL / DDS_COL: skip the second K-step of a column's last block-row when it holds <= 64 rows
   int h_direct;                    // CTA-pair SDD^T: act'(H) read by the epilogue lanes, not by TMA
   const __nv_bfloat16* h_src;      // ... from here ([nnz*128, 128] bf16)
+  int tall;      // CTA-pair forward SDD: 64 x 64 (8 KB) store boxes staged by pairs of epilogue warps
   int sdd_half;
   int epi_alt;   // CTA-pair forward SDD (4 KB boxes): two epilogue warp groups drain alternate tiles  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)

@@ -754,6 +754,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         // H or act'(H) to tmap_d)
         uint8_t* bufc = stg;
         uint8_t* bufd = stg + 4096;
+        // p.tall: the warps of lane quarters 2j and 2j+1 (same column group)
+        // stage one 64 x 64 (8 KB) box per output together — the even
+        // quarter's staging holds act(H), the odd one's act'(H), each warp's 32
+        // rows at (q & 1) * 4 KB — and the even-quarter warp issues the stores
+        const bool tall = p.tall != 0;
+        const bool issuer = !tall || !(q & 1);
+        const int pbar = 7 + half * 2 + (q >> 1);
+        if (tall) {
+          const int pair_wq = 4 * half + (((q ^ 1) + 1) & 3);  // warp wq + 3 holds lane quarter (wq + 3) & 3
+          bufc = smem_epi + ((q & 1) ? pair_wq : wq) * (2 * 4096) + (q & 1) * 4096;
+          bufd = smem_epi + ((q & 1) ? wq : pair_wq) * (2 * 4096) + (q & 1) * 4096;
+        }
         const bool two = p.epi == EPI_ACT_FWD && p.has_pre;
         // one output (the coded A, R24): the two buffers alternate, so a
         // super-chunk waits only for the store issued two super-chunks ago
@@ -772,10 +784,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             if (lane == 0) bulk_wait_read<1>();
             bc = stg + sbuf * 4096;
             sbuf ^= 1;
-          } else if (lane == 0) {
+          } else if (lane == 0 && issuer) {
             bulk_wait_read<0>();  // the previous super-chunk's stores have read both buffers
           }
-          __syncwarp();
+          if (tall)
+            named_bar_sync(pbar, 64);
+          else
+            __syncwarp();
           if (has_acc) tmem_ld_wait();
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
@@ -807,8 +822,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
             stage_row_half128(bc, lane, v, hh);
           }
           fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
+          if (tall)
+            named_bar_sync(pbar, 64);
+          else
+            __syncwarp();
+          if (lane == 0 && issuer) {
             int x, y;
             if (hm)
               out_coords2_half(p, t, rank, 2 * sc, q, p.F, x, y);

@@ -30,4 +30,10 @@ inline moe_status make_tmap_epi_wide(CUtensorMap* map, const void* base, uint64_
                                      uint64_t row_elems, const char* what) {
   return make_tmap_bf16(map, base, inner, outer, row_elems, 64, 32, what, 128);
 }
+// Tall epilogue store maps: 64 x 64 boxes (8 KB: 64 rows of 128 B), 128 B
+// swizzle — two warps of adjacent TMEM lane quarters stage one box together.
+inline moe_status make_tmap_epi_tall(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                                     uint64_t row_elems, const char* what) {
+  return make_tmap_bf16(map, base, inner, outer, row_elems, 64, 64, what, 128);
+}
 }  // namespace moe
