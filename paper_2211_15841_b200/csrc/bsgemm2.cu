@@ -259,6 +259,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   pdl_trigger();
   pdl_wait();
   const int ntiles = num_tiles2(p, MODE);
+  // SDD with p.reverse: tiles walked last-to-first (the X_g / dY_g rows the
+  // previous kernel wrote last are the ones still in L2)
+  auto rtile = [&](int tile) { return (MODE == SDD && p.reverse) ? ntiles - 1 - tile : tile; };
   // the pair offsets in shared memory for the row-pair decode (E <= P_PB_MAX)
   const int32_t* s_pb = p.pair_bins;
   if (C::PB && p.E <= P_PB_MAX) {
@@ -328,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     if (MODE == SDD && MOE_PAIR_SDD_LANE0 && !gat) {
       if (lane == 0) {
         for (int tile = cid; tile < ntiles; tile += ncl, ++tile_i) {
-          const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
+          const Tile2 t = decode2(p, MODE, rtile(tile), rank, s_pb);
           trace_ev(p, tile_i, 0);
           const bool hm = p.sdd_half && !t.second;
           const int sdd_row = hm ? (p.unpadded ? __ldg(p.brow_start + t.r0) : t.r0 * BM) + rank * 64
@@ -361,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       }
     } else
     for (int tile = cid; tile < ntiles && !idle; tile += ncl, ++tile_i) {
-      const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
+      const Tile2 t = decode2(p, MODE, rtile(tile), rank, s_pb);
       if (lane == 0) trace_ev(p, tile_i, 0);
       int idx_a = 0, idx_b = 0, idx_c = 0;
       // SDD: first dense row of this CTA's block-row (unpadded layout: brow_start; a
@@ -474,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       uint32_t acc_phase = 0;
       int tile_i = -1;
       for (int tile = cid; tile < ntiles; tile += ncl) {
-        const Tile2 t = decode2(p, MODE, tile, 0, s_pb);
+        const Tile2 t = decode2(p, MODE, rtile(tile), 0, s_pb);
         ++tile_i;
         if (t.kiters == 0) continue;
         const uint32_t idesc = (MODE == SDD && p.sdd_half && !t.second) ? idesc_half : idesc_full;
@@ -555,7 +558,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     uint32_t hw_phase = 0;  // bit b: parity of slot b's next completion
     // coordinates of ring item j (false: nothing is stored for it on this CTA)
     auto coords_hw = [&](int j, int& x, int& y) {
-      const Tile2 tj = decode2(p, MODE, cid + (j / SPW) * ncl, rank, s_pb);
+      const Tile2 tj = decode2(p, MODE, rtile(cid + (j / SPW) * ncl), rank, s_pb);
       const bool hmj = MODE == SDD && p.sdd_half && !tj.second;
       const int scj = half + (j % SPW) * EPG;
       if (hmj ? HSUB * scj >= 4 : !(rank == 0 || tj.second)) return false;
@@ -611,7 +614,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
     const bool ealt = C::WIDE && p.epi_alt && p.wide;
     uint32_t aphase = 0;
     for (int tile = cid; tile < ntiles; tile += ncl) {
-      const Tile2 t = decode2(p, MODE, tile, rank, s_pb);
+      const Tile2 t = decode2(p, MODE, rtile(tile), rank, s_pb);
       ++tile_i;
       if (ealt && (tile_i & 1) != half) continue;  // the other group's tile
       const int acc_t = ealt ? half : acc;
@@ -950,6 +953,14 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   if (grid < 2) grid = 2;
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
+  {
+    static int rev = -1;  // MOE_GEMM_REVERSE bit m: walk mode m's tiles last-to-first (here: SDD only)
+    if (rev < 0) {
+      const char* e = getenv("MOE_GEMM_REVERSE");
+      rev = e ? atoi(e) : (1 << DSD_ROW);
+    }
+    p.reverse = (MODE == SDD && ((rev >> SDD) & 1)) ? 1 : 0;
+  }
   p.trace = gemm_trace_slot();
   cudaError_t le = launch_k(kern, dim3(grid), dim3(P_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
   if (le != cudaSuccess) return set_error(MOE_ECUDA, "%s: %s", L.name, cudaGetErrorString(le));
