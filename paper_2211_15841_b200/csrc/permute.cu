@@ -342,6 +342,29 @@ __global__ void __launch_bounds__(256) zero_pad_kernel(uint4* __restrict__ dst, 
 }
 
 static int row_grid() { return moe_device_sm_count() * 8; }
+// One wave of the kernel's resident CTAs (the row kernels are grid-stride
+// loops: a second, partial wave of CTAs only adds a launch tail; e.g. the
+// padded gather holds 5 CTAs per SM at 48 registers, not 8). MOE_ROW_GRID=8:
+// the fixed 8 CTAs per SM.
+template <typename K>
+static int row_grid_for(K* kern) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("MOE_ROW_GRID");
+    env = e ? atoi(e) : 0;
+  }
+  if (env > 0) return moe_device_sm_count() * env;
+  static int per_sm = 0;  // per kernel instantiation (the occupancy depends on the kernel only)
+  if (per_sm == 0) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32 * kWarpsPerCta, 0) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = 8;
+    }
+    per_sm = n < 8 ? n : 8;
+  }
+  return moe_device_sm_count() * per_sm;
+}
 
 static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, const char* name) {
   MOE_TRY(moe_check_config(cfg));
@@ -353,7 +376,7 @@ static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, 
 }
 
 #define MOE_VEC_CASE(V, NAME, KERNEL, ...) \
-  case V: MOE_LAUNCH(NAME, KERNEL<V>, dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break;
+  case V: MOE_LAUNCH(NAME, KERNEL<V>, dim3(row_grid_for(KERNEL<V>)), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break;
 #define MOE_VEC_DISPATCH(VEC_EXPR, NAME, KERNEL, ...)  \
   switch (VEC_EXPR) {                                  \
     MOE_VEC_CASE(1, NAME, KERNEL, __VA_ARGS__)         \
@@ -363,7 +386,7 @@ static moe_status check_rows(const moe_config* cfg, const moe_topology_t* topo, 
     MOE_VEC_CASE(5, NAME, KERNEL, __VA_ARGS__)         \
     MOE_VEC_CASE(6, NAME, KERNEL, __VA_ARGS__)         \
     MOE_VEC_CASE(7, NAME, KERNEL, __VA_ARGS__)         \
-    default: MOE_LAUNCH(NAME, KERNEL<8>, dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break; \
+    default: MOE_LAUNCH(NAME, KERNEL<8>, dim3(row_grid_for(KERNEL<8>)), dim3(32 * kWarpsPerCta), 0, s, __VA_ARGS__); break; \
   }
 
 struct SbwdArgs {
@@ -389,11 +412,13 @@ struct SbwdArgs {
 template <int V, int TPW>
 static moe_status sbwd_launch(const SbwdArgs& a, cudaStream_t s) {
   if (a.E <= 64)
-    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 2>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
+    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 2>), dim3(row_grid_for(scatter_bwd_kernel<V, TPW, 2>)),
+               dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
                a.counts, a.pbins, a.bs, a.renorm, a.aux_c);
   else
-    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 8>), dim3(row_grid()), dim3(32 * kWarpsPerCta), 0, s, a.dy,
+    MOE_LAUNCH("scatter_bwd", (scatter_bwd_kernel<V, TPW, 8>), dim3(row_grid_for(scatter_bwd_kernel<V, TPW, 8>)),
+               dim3(32 * kWarpsPerCta), 0, s, a.dy,
                a.y_rows, a.map, a.gates, a.dy_rows, a.dgates, a.T, a.k, a.logits, a.expert_idx, a.E, a.dl16, a.dl32,
                a.counts, a.pbins, a.bs, a.renorm, a.aux_c);
   return MOE_OK;
