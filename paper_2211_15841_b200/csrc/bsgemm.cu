@@ -56,6 +56,13 @@
 #define MOE_SDD_NBUF 2
 #endif
 
+#ifndef MOE_DSD_EPW  // experiment: epilogue warps of the row-walk DSD (its scattered last-tile epilogue is exposed)
+#define MOE_DSD_EPW 8
+#endif
+#ifndef MOE_DSD_NBUF
+#define MOE_DSD_NBUF 2
+#endif
+
 #ifndef MOE_MAX_STAGES
 #define MOE_MAX_STAGES 16
 #endif
@@ -68,11 +75,11 @@ using namespace sm100;
 // tiles, whose epilogues are store-latency bound; 8 elsewhere (router GEMMs,
 // SDD^T whose H staging would not leave room for the operand ring).
 __host__ __device__ constexpr int epi_warps(int mode, int bn, bool epi_h) {
-  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_EPW : 8;
+  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_EPW : (mode == DSD_ROW && bn == 256) ? MOE_DSD_EPW : 8;
 }
 // Staging buffers per epilogue warp (stores in flight per warp).
 __host__ __device__ constexpr int epi_bufs(int mode, int bn, bool epi_h) {
-  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_NBUF : 2;
+  return (mode == SDD && bn == 256 && !epi_h) ? MOE_SDD_NBUF : (mode == DSD_ROW && bn == 256) ? MOE_DSD_NBUF : 2;
 }
 
 // OCC = CTAs per SM: 1, or 2 for the router's forward GEMM under
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], p.mcast ? 2 : 1);  // multicast A: both CTAs' MMAs free a stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -318,6 +325,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (MODE == DSD_ROW && p.mcast) cluster_sync();  // the peer's barriers are initialised before its multicasts
   pdl_trigger();
   pdl_wait();  // operands and device-side sizes come from the previous kernels
   const int ntiles = num_tiles(p, MODE, PAIR);
@@ -411,8 +419,18 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
             mbar_arrive(fb);
           } else {
             mbar_arrive_expect_tx(fb, C::STAGE);
-            issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
-                                              smem_b + stage * C::B_BYTES, fb, 3, odrow);
+            if (MODE == DSD_ROW && p.mcast) {
+              // the cluster's CTAs hold the two column tiles of one block-row: each
+              // loads 64 of the A block's 128 rows into both (128 B swizzle atoms are 8 rows)
+              const uint32_t r = cluster_ctarank();
+              tma_load_2d_mcast(smem_a + stage * A_BYTES + r * (BM / 2) * KSW, &tmap_a, fb, (kit % KPB) * BK,
+                                sblk * BM + (int)r * (BM / 2), 0x3);
+              issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+                                                smem_b + stage * C::B_BYTES, fb, 2, odrow);
+            } else {
+              issue_stage<MODE, A_MN, B_MN, BN>(&tmap_a, &tmap_b, p, t, kit, sblk, oblk, smem_a + stage * A_BYTES,
+                                                smem_b + stage * C::B_BYTES, fb, 3, odrow);
+            }
           }
         }
         __syncwarp();
@@ -452,7 +470,10 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
                 B_MN ? make_sdesc(b_base + k * 2048, BK * 128, 1024) : make_sdesc(b_base + k * 32, 16, KSW * 8, KSW);
             if (!(p.dbg & 2)) mma_bf16(d_tmem, adesc, bdesc, idesc, (kit | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          if (MODE == DSD_ROW && p.mcast)
+            mma_commit_mcast(&empty[stage], 0x3);  // the stage may be refilled by either CTA's multicast
+          else
+            mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -995,6 +1016,7 @@ __global__ void __launch_bounds__(Cfg<MODE, BN, EPI_H, OCC>::THREADS, OCC)
   }
   tc_fence_before();
   __syncthreads();
+  if (MODE == DSD_ROW && p.mcast) cluster_sync();  // the peer's last commits / multicasts into this CTA are done
   if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -1087,6 +1109,23 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    le = cudaLaunchKernelEx(&lc, kern, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
+  } else if (MODE == DSD_ROW && p.mcast) {  // 2-CTA clusters (an even grid: the clusters walk tile pairs)
+    grid &= ~1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(C::THREADS);
+    lc.dynamicSmemBytes = C::SMEM;
+    lc.stream = stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl_enabled() ? 2 : 1;
     le = cudaLaunchKernelEx(&lc, kern, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
   } else {
     le = launch_k(kern, dim3(grid), dim3(C::THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, L.te, L.tf, p);
@@ -1201,6 +1240,17 @@ static bool use_pair_rows() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("MOE_GEMM_PAIR_ROWS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// MOE_DSD_MCAST=1: the row-walk DSD runs in 2-CTA clusters whose CTAs hold the
+// two column tiles of one block-row and share its A loads by TMA multicast.
+static bool dsd_mcast() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOE_DSD_MCAST");
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
@@ -1447,7 +1497,9 @@ static moe_status dsd_launch(const moe_config* cfg, const void* s, int trans_s, 
     L.a_mn = false;
     L.max_tiles = pair ? (int)((rows / BM / 2 + cfg->num_experts) * L.p.dense_tiles)
                        : (int)(rows / BM * L.p.dense_tiles);
-    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, BK, 128, "moe_dsd s", KSW));
+    // 2-CTA clusters sharing A across the block-row's column tiles (pairs of them)
+    L.p.mcast = (!pair && dsd_mcast() && L.p.dense_tiles % 2 == 0) ? 1 : 0;
+    MOE_TRY(make_tmap_bf16(&L.ta, s, 128, nnz * 128, 128, BK, L.p.mcast ? 64 : 128, "moe_dsd s", KSW));
     if (!trans_b)
       MOE_TRY(make_tmap_bf16_mn(&L.tb, b, h, N, h, pair ? 2 : L.bn / 64, "moe_dsd b"));
     else

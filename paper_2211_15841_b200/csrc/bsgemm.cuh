@@ -89,6 +89,8 @@ struct GemmParams {
   int epi_alt;   // CTA-pair forward SDD (4 KB boxes): two epilogue warp groups drain alternate tiles  // CTA-pair SDD / SDD^T: an expert's lone last block-row runs as an M = 128 pair tile
   int wide;  // CTA-pair forward SDD: tmap_c / tmap_d have 64 x 32 boxes, 128 B swizzle (make_tmap_epi_wide)
   unsigned long long* trace;  // MOE_GEMM_TRACE: per-CTA per-tile timestamps (see gemm_trace_*)
+  int mcast;    // DSD_ROW in 2-CTA clusters: the two column tiles of a block-row share A (each CTA
+                // loads 64 of its 128 rows, multicast to both; MOE_DSD_MCAST)
   int reverse;  // walk the tiles last-to-first (reuse what the previous kernel left in L2)
   int dbg;  // experiment knobs (MOE_GEMM_DBG): 1 = no epilogue work, 2 = no MMA, 4 = no activation
            // math, 8 = no TMA loads, 64 = epilogue decoupled from the accumulator (timing only)
