@@ -259,9 +259,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   pdl_trigger();
   pdl_wait();
   const int ntiles = num_tiles2(p, MODE);
-  // SDD with p.reverse: tiles walked last-to-first (the X_g / dY_g rows the
-  // previous kernel wrote last are the ones still in L2)
-  auto rtile = [&](int tile) { return (MODE == SDD && p.reverse) ? ntiles - 1 - tile : tile; };
+  // p.reverse: tiles walked last-to-first (the operand rows the previous
+  // kernel wrote last are the ones still in L2)
+  auto rtile = [&](int tile) { return p.reverse ? ntiles - 1 - tile : tile; };
   // the pair offsets in shared memory for the row-pair decode (E <= P_PB_MAX)
   const int32_t* s_pb = p.pair_bins;
   if (C::PB && p.E <= P_PB_MAX) {
@@ -954,12 +954,12 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
   GemmParams p = L.p;
   p.dbg = gemm_dbg();
   {
-    static int rev = -1;  // MOE_GEMM_REVERSE bit m: walk mode m's tiles last-to-first (here: SDD only)
+    static int rev = -1;  // MOE_GEMM_REVERSE bit m: walk mode m's tiles last-to-first (default as bsgemm.cu)
     if (rev < 0) {
       const char* e = getenv("MOE_GEMM_REVERSE");
-      rev = e ? atoi(e) : (1 << DSD_ROW);
+      rev = e ? atoi(e) : (1 << DSD_ROW) | (1 << DS_COL) | (1 << DDS_COL);
     }
-    p.reverse = (MODE == SDD && ((rev >> SDD) & 1)) ? 1 : 0;
+    p.reverse = ((rev >> MODE) & 1) ? 1 : 0;
   }
   p.trace = gemm_trace_slot();
   cudaError_t le = launch_k(kern, dim3(grid), dim3(P_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
