@@ -1096,7 +1096,7 @@ static moe_status launch_t(const GemmLaunch& L, cudaStream_t stream) {
       const char* e = getenv("MOE_GEMM_REVERSE");
       rev = e ? atoi(e) : (1 << DSD_ROW) | (1 << DS_COL) | (1 << DDS_COL);
     }
-    if ((rev >> MODE) & 1) p.reverse = 1;
+    if (((rev >> MODE) & 1) && !(MODE != SDD && p.gather_a)) p.reverse = 1;  // gathered DD^TS: forward order
   }
   cudaError_t le;
   if (MODE == DENSE && p.topo_fused) {  // grid barrier inside: cooperative launch (all CTAs co-resident)

@@ -959,7 +959,8 @@ static moe_status launch2_t(const GemmLaunch& L, cudaStream_t stream) {
       const char* e = getenv("MOE_GEMM_REVERSE");
       rev = e ? atoi(e) : (1 << DSD_ROW) | (1 << DS_COL) | (1 << DDS_COL);
     }
-    p.reverse = ((rev >> MODE) & 1) ? 1 : 0;
+    // (the gathered DD^TS token ring is prefetched in forward tile order: no reversal there)
+    p.reverse = ((rev >> MODE) & 1) && !(MODE != SDD && p.gather_a) ? 1 : 0;
   }
   p.trace = gemm_trace_slot();
   cudaError_t le = launch_k(kern, dim3(grid), dim3(P_THREADS), C::SMEM, stream, L.ta, L.tb, L.tc, L.td, p);
